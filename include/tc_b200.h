@@ -1,0 +1,165 @@
+/*
+ * tc_b200.h — C ABI of the B200-native TensorCommitments prover (libtcb200.so).
+ *
+ * The reference (/root/reference/pkg) has no FFI: its prover entry points are Python
+ * functions, and the commit / open / tree ones exist only as contracts in SPEC.md.  Each
+ * entry point below is the native body of one of those Python functions; the Python
+ * package paper_2602_12630_b200 binds them with ctypes and keeps the
+ * reference's names, argument meaning and exception types.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  "d_" pointers are CUDA device pointers (e.g. a torch
+ *     tensor's data_ptr()), everything else is host memory.
+ *   - Field elements cross the ABI in CANONICAL little-endian form (never Montgomery):
+ *     as 6 x uint32 limbs on the device (24 B), or as the reference's 21-byte
+ *     encode_scalar layout on the host (backend.py:335-336).
+ *   - Group elements cross as the reference's 43-byte encode_elem layout
+ *     (0x04 || x LE21 || y LE21, infinity = 43 zero bytes; backend.py:309-317).
+ *   - A context is bound to one device and one CUDA stream; calls on a context are
+ *     stream-ordered, not re-entrant.  SRS handles are read-only after creation and may be
+ *     shared by contexts on the same device.
+ *   - Every call returns a status; TC_OK = 0.  The message of the last failure on a
+ *     context is tc_ctx_last_error().  No exceptions cross the ABI.
+ *   - No CPU fallback: every compute entry point launches CUDA kernels and fails with
+ *     TC_ERR_CUDA when no device is usable.
+ */
+#ifndef TC_B200_H
+#define TC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TC_ABI_VERSION 1
+#define TC_MAX_AXES 16
+
+/* status codes -> Python exception types of the reference */
+enum {
+  TC_OK = 0,
+  TC_ERR_VALUE = 1,          /* ValueError        (mvpoly.py:30-37, backend.py:319-333) */
+  TC_ERR_INDEX = 2,          /* IndexError        (mvpoly.py:57) */
+  TC_ERR_ZERO_DIVISION = 3,  /* ZeroDivisionError (field.py:41-42) */
+  TC_ERR_BACKEND = 4,        /* BackendError      (backend.py:26-27) */
+  TC_ERR_OVERFLOW = 5,       /* OverflowError     (mvpoly.py:546-547) */
+  TC_ERR_CUDA = 10,          /* RuntimeError: CUDA failure / no device */
+  TC_ERR_MEMORY = 11,        /* MemoryError */
+  TC_ERR_ARGUMENT = 12       /* ValueError: malformed call (null pointer, bad dtype) */
+};
+
+/* input element types */
+enum {
+  TC_DTYPE_F16 = 1,
+  TC_DTYPE_BF16 = 2,
+  TC_DTYPE_F32 = 3,
+  TC_DTYPE_F64 = 4,
+  TC_DTYPE_FP_LIMBS = 16 /* already field elements: canonical 6 x u32 LE, < p */
+};
+
+/* SRS contents */
+enum { TC_SRS_MONOMIAL = 1, TC_SRS_LAGRANGE = 2 };
+
+/* commit / open routes (all produce identical bytes: the commitment g^{f_T(tau)} is unique) */
+enum {
+  TC_ROUTE_AUTO = 0,      /* Lagrange route when the SRS has Lagrange elements */
+  TC_ROUTE_MONOMIAL = 1,  /* interpolate -> MSM over monomial SRS (SPEC.md:279 verbatim) */
+  TC_ROUTE_LAGRANGE = 2   /* MSM of grid values over g^{L_i(tau)} */
+};
+
+typedef struct tc_ctx tc_ctx;
+typedef struct tc_srs tc_srs;
+
+int tc_abi_version(void);
+
+/* ---- context ---------------------------------------------------------------------- */
+int tc_ctx_create(int device, void* cuda_stream, tc_ctx** out);
+int tc_ctx_destroy(tc_ctx* ctx);
+int tc_ctx_set_stream(tc_ctx* ctx, void* cuda_stream);
+int tc_ctx_synchronize(tc_ctx* ctx);
+const char* tc_ctx_last_error(const tc_ctx* ctx);
+uint64_t tc_ctx_launch_count(const tc_ctx* ctx);
+
+/* ---- setup_srs (Srs SPEC.md:44-50) ----------------------------------
+ * Monomial elements g^{prod_j tau_j^{i_j}} in lex order (mvpoly.py:3-5) and, with
+ * TC_SRS_LAGRANGE, the grid-Lagrange elements g^{prod_j L_{j,i_j}(tau_j)} on the default
+ * grid 1..d_j (mvpoly.py:130-133).  taus_le21: m x 21 bytes (canonical, < p). */
+int tc_srs_generate(tc_ctx* ctx, const uint32_t* shape, int m, const uint8_t* taus_le21,
+                    int flags, tc_srs** out);
+/* SRS from public points (TCSR payload): monomial43 N x 43 B, axis43 m x 43 B */
+int tc_srs_load(tc_ctx* ctx, const uint32_t* shape, int m, const uint8_t* monomial43,
+                const uint8_t* axis43, tc_srs** out);
+/* export N x 43 B (which = TC_SRS_MONOMIAL | TC_SRS_LAGRANGE) or the m axis elements */
+int tc_srs_export(tc_ctx* ctx, const tc_srs* srs, int which, uint8_t* out43);
+int tc_srs_export_axis(const tc_srs* srs, uint8_t* out43);
+int tc_srs_has(const tc_srs* srs, int which);
+uint64_t tc_srs_size(const tc_srs* srs);
+int tc_srs_destroy(tc_srs* srs);
+
+/* ---- quantize: RNE(v * 2^scale_bits), negatives -> p - |q| ------------
+ * TC_ERR_VALUE when a value is not finite or |v| * 2^scale_bits >= p/2. */
+int tc_quantize(tc_ctx* ctx, const void* d_in, int dtype, uint64_t n, int scale_bits,
+                uint32_t* d_out_limbs);
+
+/* ---- mvpoly.interpolate_lagrange (mvpoly.py:233-247), default grid, in place ---------- */
+int tc_interpolate(tc_ctx* ctx, uint32_t* d_limbs, const uint32_t* shape, int m);
+
+/* ---- mvpoly.evaluate (mvpoly.py:140-161) of a coefficient array at a point ------------- */
+int tc_evaluate(tc_ctx* ctx, const uint32_t* d_coeffs, const uint32_t* shape, int m,
+                const uint8_t* point_le21, uint8_t* out_y21);
+
+/* ---- mvpoly.open_quotients (mvpoly.py:521-534) ----------------------------------------
+ * d_quotients: m x N canonical limbs (each quotient keeps f's shape, mvpoly.py:455-456). */
+int tc_open_quotients(tc_ctx* ctx, const uint32_t* d_coeffs, const uint32_t* shape, int m,
+                      const uint8_t* omega_le21, uint32_t* d_quotients, uint8_t* out_y21);
+
+/* ---- multi-exponentiation prod_k G_k^{a_k} ---------------------
+ * over the SRS's monomial or Lagrange elements (which), scalars canonical device limbs. */
+int tc_msm(tc_ctx* ctx, const tc_srs* srs, int which, const uint32_t* d_scalars, uint64_t n,
+           uint8_t* out43);
+
+/* ---- tc_commit ----------------------------------------------------------
+ * d_in holds N = prod(shape) values of dtype (float dtypes are quantised at scale_bits). */
+int tc_commit(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int scale_bits,
+              int route, uint8_t* out43);
+/* count tensors of the SRS's shape (protocol.prover_commit's per-layer loop) */
+int tc_commit_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count,
+                    int dtype, int scale_bits, int route, uint8_t* out43);
+
+/* ---- tc_open: y = f_T(omega), pi_i = g^{q_i(tau)} ----------------------- */
+int tc_open(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int scale_bits,
+            const uint8_t* omega_le21, int route, uint8_t* out_y21, uint8_t* out_pi43);
+
+/* ---- Terkle build ------------------------------------
+ * leaves: n x 21 B field elements.  Pads with zeros to B^L (B = node SRS size,
+ * L = max(1, ceil(log_B n))) and commits every node bottom-up; a child node enters its
+ * parent as hash_to_scalar(encode_elem(C), b"terkle/node") (backend.py:346-348).
+ * out_nodes43 receives all node commitments level by level (bottom first);
+ * capacity in nodes is *inout_count, the number written is returned in it. */
+int tc_terkle_build(tc_ctx* ctx, const tc_srs* node_srs, const uint8_t* leaves_le21,
+                    uint64_t n, uint8_t* out_nodes43, uint64_t* inout_count);
+
+/* ---- host-side verifier primitive (backend.py:219-291), CPU only ------------------------ */
+int tc_pairing(const uint8_t* a43, const uint8_t* b43, uint8_t* out_f2_42);
+
+/* tc_verify in the product-of-pairings form, CPU only:
+ * e(C * g^-y, g) == prod_i e(pi_i, axis_i * g^-omega_i).  *ok = 1 accept / 0 reject. */
+int tc_verify_host(int m, const uint8_t* axis43, const uint8_t* c43, const uint8_t* omega_le21,
+                   const uint8_t* y21, const uint8_t* proofs43, int* ok);
+/* hash_to_scalar (backend.py:346-348) */
+int tc_host_hash_to_scalar(const uint8_t* data, uint32_t n, const uint8_t* tag, uint32_t tn,
+                           uint8_t* out21);
+
+/* ---- self-test hooks (host arithmetic of the shared __host__ __device__ core) ----------- */
+int tc_host_fq_mul(const uint32_t* a, const uint32_t* b, uint32_t* out);   /* canonical */
+int tc_host_fp_mul(const uint32_t* a, const uint32_t* b, uint32_t* out);   /* canonical */
+int tc_host_g_mul(const uint8_t* k_le21, uint8_t* out43);                  /* k * g */
+/* device field-op check: op 0 = Fq mul, 1 = Fp mul, 2 = Fq add, 3 = Fq sub, 4 = Fq inv */
+int tc_debug_field(tc_ctx* ctx, int op, const uint32_t* d_a, const uint32_t* d_b,
+                   uint32_t* d_out, uint64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TC_B200_H */

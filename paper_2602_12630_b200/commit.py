@@ -1,0 +1,291 @@
+"""TensorCommitments: setup / commit / open / verify on the B200.
+
+Drop-in for the spec-only `commit` module of the reference and
+`setup_srs` of `algebra`, with the reference's types: points are affine
+(x, y) int tuples or None (backend.py:15-17), scalars are ints in [0, p).
+
+Every compute step (SRS generation, quantisation, interpolation, MSM, quotients) runs in
+libtcb200.so on the GPU; `tc_verify` is the CPU verifier (product of
+pairings SPEC.md:313) implemented natively in the same library.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import struct
+from dataclasses import dataclass
+
+from . import _conv, _lib
+from .curve import ELEM_BYTES, P, decode_elem, decode_elems, encode_elem, encode_scalar, hash_to_scalar
+from .mvpoly import Grid, check_shape, default_grid
+
+SCALE_BITS = 16   # protocol.quantize fixed-point scale
+
+_ROUTES = {"auto": _lib.ROUTE_AUTO, "monomial": _lib.ROUTE_MONOMIAL, "lagrange": _lib.ROUTE_LAGRANGE}
+
+
+def shape_header(magic: bytes, shape) -> bytes:
+    """magic ‖ <HH version=1, m> ‖ <I d_j>×m — the wire header of mvpoly.py:567-572."""
+    return magic + struct.pack("<HH", 1, len(shape)) + b"".join(struct.pack("<I", d) for d in shape)
+
+
+def derive_taus(shape, entropy: bytes):
+    """Frozen trapdoor PRF (SPEC.md:81 leaves it open):
+    tau_j = hash_to_scalar(entropy ‖ u32le(j) ‖ TCSR header(shape), tag=b"srs/tau")."""
+    hdr = shape_header(b"TCSR", shape)
+    return tuple(hash_to_scalar(bytes(entropy) + struct.pack("<I", j) + hdr, b"srs/tau") for j in range(len(shape)))
+
+
+@dataclass(frozen=True)
+class Trapdoors:
+    """only the trusted setup and tests may hold these."""
+    taus: tuple
+
+
+@dataclass(frozen=True)
+class Commitment:
+    """a single group element."""
+    elem: object
+
+    def to_bytes(self) -> bytes:
+        return encode_elem(self.elem)
+
+
+@dataclass(frozen=True)
+class TensorOpening:
+    """claimed value y and m quotient commitments."""
+    y: int
+    proofs: tuple
+
+    def to_bytes(self, point) -> bytes:
+        """TCOP wire format: magic, m (u16), omega, y, m proof elements."""
+        out = [b"TCOP", struct.pack("<H", len(self.proofs))]
+        out += [encode_scalar(w) for w in point]
+        out.append(encode_scalar(self.y))
+        out += [encode_elem(e) for e in self.proofs]
+        return b"".join(out)
+
+
+class Srs:
+    """Structured reference string resident in device memory.
+
+    monomial_elems / lagrange_elems are materialised on the host lazily (they are
+    large); the kernels use the device copy directly.
+    """
+
+    def __init__(self, shape, handle, device, axis_elems, grid=None):
+        self.shape = tuple(int(d) for d in shape)
+        self._h = handle
+        self.device = device
+        self.axis_elems = tuple(axis_elems)
+        self.grid = grid if grid is not None else default_grid(None, self.shape)
+        self._cache = {}
+
+    @property
+    def size(self) -> int:
+        return int(_lib.lib().tc_srs_size(self._h))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def has(self, which: int) -> bool:
+        return bool(_lib.lib().tc_srs_has(self._h, which))
+
+    def _export(self, which):
+        if which not in self._cache:
+            ctx = _lib.Context.get(self.device)
+            n = self.size
+            buf = C.create_string_buffer(n * ELEM_BYTES)
+            with ctx.lock:
+                ctx.bind_stream()
+                ctx.check(_lib.lib().tc_srs_export(ctx.handle, self._h, which, buf), "tc_srs_export")
+            self._cache[which] = decode_elems(buf.raw, n)
+        return self._cache[which]
+
+    @property
+    def monomial_elems(self):
+        return self._export(_lib.SRS_MONOMIAL)
+
+    @property
+    def lagrange_elems(self):
+        return self._export(_lib.SRS_LAGRANGE)
+
+    def to_bytes(self) -> bytes:
+        """TCSR file: header, monomial elements, axis elements, grid."""
+        out = [shape_header(b"TCSR", self.shape)]
+        out += [encode_elem(e) for e in self.monomial_elems]
+        out += [encode_elem(e) for e in self.axis_elems]
+        for nodes in self.grid.axes:
+            out += [encode_scalar(z) for z in nodes]
+        return b"".join(out)
+
+    @classmethod
+    def from_bytes(cls, raw: bytes, device=None) -> "Srs":
+        if raw[:4] != b"TCSR":
+            raise ValueError("bad magic, expected b'TCSR'")
+        version, m = struct.unpack_from("<HH", raw, 4)
+        if version != 1:
+            raise ValueError(f"unsupported version {version}")
+        shape = struct.unpack_from("<" + "I" * m, raw, 8)
+        n = check_shape(shape)
+        off = 8 + 4 * m
+        mono = raw[off:off + n * ELEM_BYTES]
+        off += n * ELEM_BYTES
+        axis = raw[off:off + m * ELEM_BYTES]
+        if len(mono) != n * ELEM_BYTES or len(axis) != m * ELEM_BYTES:
+            raise ValueError("srs payload length mismatch")
+        return load_srs(shape, mono, axis, device=device)
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h and _lib is not None and _lib._lib is not None:
+            try:
+                _lib.lib().tc_srs_destroy(h)
+            except Exception:  # pragma: no cover - interpreter shutdown
+                pass
+
+    def __repr__(self):
+        return f"Srs(shape={self.shape})"
+
+
+def _shape_arr(shape):
+    return (C.c_uint32 * len(shape))(*shape)
+
+
+def setup_srs(shape, entropy: bytes, *, lagrange: bool = True, monomial: bool = True, device=None):
+    """setup_srs(shape, entropy) -> (Srs, Trapdoors).
+
+    Monomial elements g^{prod tau_j^{i_j}} (lex order) and — used by the fast commit
+    route — the grid-Lagrange elements g^{prod L_{j,i_j}(tau_j)}, both generated on the
+    GPU by fixed-base scalar multiplication."""
+    shape = tuple(int(d) for d in shape)
+    check_shape(shape)
+    taus = derive_taus(shape, entropy)
+    ctx = _lib.Context.get(device)
+    flags = (_lib.SRS_MONOMIAL if monomial else 0) | (_lib.SRS_LAGRANGE if lagrange else 0)
+    h = C.c_void_p()
+    taus_b = b"".join(encode_scalar(t) for t in taus)
+    with ctx.lock:
+        ctx.bind_stream()
+        ctx.check(_lib.lib().tc_srs_generate(ctx.handle, _shape_arr(shape), len(shape), taus_b, flags, C.byref(h)),
+                  "setup_srs")
+    axis_buf = C.create_string_buffer(len(shape) * ELEM_BYTES)
+    _lib.lib().tc_srs_export_axis(h, axis_buf)
+    srs = Srs(shape, h, ctx.device, decode_elems(axis_buf.raw, len(shape)))
+    return srs, Trapdoors(taus)
+
+
+def load_srs(shape, monomial43: bytes, axis43: bytes, device=None) -> Srs:
+    """Srs from public points only (e.g. a TCSR file); monomial commit route only."""
+    shape = tuple(int(d) for d in shape)
+    check_shape(shape)
+    ctx = _lib.Context.get(device)
+    h = C.c_void_p()
+    with ctx.lock:
+        ctx.bind_stream()
+        ctx.check(_lib.lib().tc_srs_load(ctx.handle, _shape_arr(shape), len(shape), bytes(monomial43), bytes(axis43),
+                                         C.byref(h)), "load_srs")
+    return Srs(shape, h, ctx.device, decode_elems(axis43, len(shape), validate=True))
+
+
+def _route(route) -> int:
+    try:
+        return _ROUTES[route]
+    except KeyError:
+        raise ValueError(f"unknown route {route!r}") from None
+
+
+def tc_commit(srs: Srs, T, *, scale_bits: int = SCALE_BITS, route: str = "auto") -> Commitment:
+    """C_T = g^{f_T(tau)}.
+
+    T: field tensor (sequence of ints / integer array) or a float tensor (torch / numpy),
+    which is quantised on the device at 2^scale_bits first."""
+    ctx = _lib.Context.get(srs.device)
+    ptr, dt, keep = _conv.device_input(T, srs.size, f"cuda:{ctx.device}")
+    out = C.create_string_buffer(ELEM_BYTES)
+    with ctx.lock:
+        ctx.bind_stream()
+        ctx.check(_lib.lib().tc_commit(ctx.handle, srs.handle, ptr, dt, scale_bits, _route(route), out), "tc_commit")
+    del keep
+    return Commitment(decode_elem(out.raw, validate=False))
+
+
+def tc_commit_many(srs: Srs, tensors, *, scale_bits: int = SCALE_BITS, route: str = "auto"):
+    """Commit several tensors of the SRS's shape (one C call)."""
+    ctx = _lib.Context.get(srs.device)
+    keeps, ptrs, dts = [], [], set()
+    for T in tensors:
+        ptr, dt, keep = _conv.device_input(T, srs.size, f"cuda:{ctx.device}")
+        ptrs.append(ptr)
+        dts.add(dt)
+        keeps.append(keep)
+    if len(dts) > 1:
+        raise ValueError("tc_commit_many: all tensors must share one dtype")
+    if not ptrs:
+        return []
+    arr = (C.c_void_p * len(ptrs))(*ptrs)
+    out = C.create_string_buffer(ELEM_BYTES * len(ptrs))
+    with ctx.lock:
+        ctx.bind_stream()
+        ctx.check(_lib.lib().tc_commit_batch(ctx.handle, srs.handle, arr, len(ptrs), dts.pop(), scale_bits,
+                                             _route(route), out), "tc_commit_many")
+    del keeps
+    return [Commitment(decode_elem(out.raw[i * ELEM_BYTES:(i + 1) * ELEM_BYTES], validate=False))
+            for i in range(len(ptrs))]
+
+
+def tc_open(srs: Srs, T, point, *, scale_bits: int = SCALE_BITS, route: str = "auto") -> TensorOpening:
+    """y = f_T(omega), pi_i = g^{q_i(tau)} from open_quotients."""
+    if len(point) != len(srs.shape):
+        raise ValueError("point arity does not match polynomial")
+    ctx = _lib.Context.get(srs.device)
+    ptr, dt, keep = _conv.device_input(T, srs.size, f"cuda:{ctx.device}")
+    m = len(srs.shape)
+    om = b"".join(encode_scalar(int(w)) for w in point)
+    y = C.create_string_buffer(21)
+    pis = C.create_string_buffer(ELEM_BYTES * m)
+    with ctx.lock:
+        ctx.bind_stream()
+        ctx.check(_lib.lib().tc_open(ctx.handle, srs.handle, ptr, dt, scale_bits, om, _route(route), y, pis), "tc_open")
+    del keep
+    return TensorOpening(int.from_bytes(y.raw, "little"), decode_elems(pis.raw, m))
+
+
+def tc_verify(srs: Srs, C_T, point, opening: TensorOpening) -> bool:
+    """e(C g^-y, g) == prod_i e(pi_i, axis_i g^-omega_i). CPU."""
+    m = len(srs.shape)
+    if len(opening.proofs) != m:
+        raise ValueError("proof count does not match tensor order")
+    if len(point) != m:
+        raise ValueError("point arity does not match polynomial")
+    elem = C_T.elem if isinstance(C_T, Commitment) else C_T
+    ok = C.c_int(0)
+    st = _lib.lib().tc_verify_host(
+        m,
+        b"".join(encode_elem(a) for a in srs.axis_elems),
+        encode_elem(elem),
+        b"".join(encode_scalar(int(w)) for w in point),
+        encode_scalar(int(opening.y)),
+        b"".join(encode_elem(e) for e in opening.proofs),
+        C.byref(ok),
+    )
+    _lib.check(st, None, "tc_verify")
+    return bool(ok.value)
+
+
+def pair(a, b):
+    """The reference's modified Tate pairing e(a, b) (backend.py:219-291), on the CPU."""
+    out = C.create_string_buffer(42)
+    _lib.check(_lib.lib().tc_pairing(encode_elem(a), encode_elem(b), out), None, "pair")
+    return (int.from_bytes(out.raw[:21], "little"), int.from_bytes(out.raw[21:], "little"))
+
+
+def g_mul(k: int):
+    """k * g on the host (test helper)."""
+    out = C.create_string_buffer(ELEM_BYTES)
+    _lib.lib().tc_host_g_mul(encode_scalar(int(k) % P), out)
+    return decode_elem(out.raw, validate=False)
+
+
+__all__ = ["Commitment", "Grid", "Srs", "TensorOpening", "Trapdoors", "derive_taus", "g_mul", "load_srs", "pair",
+           "setup_srs", "tc_commit", "tc_commit_many", "tc_open", "tc_verify"]

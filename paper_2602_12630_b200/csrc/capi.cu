@@ -1,0 +1,746 @@
+// C ABI of libtcb200.so (include/tc_b200.h): context / SRS management and the prover entry
+// points (quantize, interpolate, evaluate, open_quotients, msm, commit, open, Terkle build),
+// plus the CPU-side verifier primitive (pairing) that the reference keeps on the host.
+#include <cstdarg>
+#include <cstring>
+
+#include "sha256.cuh"
+#include "tc_internal.cuh"
+
+using namespace tc;
+
+// ======================================================================================
+// runtime helpers
+// ======================================================================================
+namespace tcrt {
+
+int fail(tc_ctx* ctx, int code, const char* fmt, ...) {
+  if (ctx) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    ctx->err = buf;
+  }
+  return code;
+}
+
+int scratch(tc_ctx* ctx, const char* name, size_t bytes, void** out) {
+  auto& b = ctx->scratch[name];
+  if (b.n < bytes) {
+    if (b.p) {
+      cudaError_t e = cudaFreeAsync(b.p, ctx->stream);
+      if (e != cudaSuccess) return fail(ctx, TC_ERR_CUDA, "cudaFreeAsync(%s): %s", name, cudaGetErrorString(e));
+      b.p = nullptr;
+      b.n = 0;
+    }
+    size_t want = bytes + bytes / 4 + 256;
+    cudaError_t e = cudaMallocAsync(&b.p, want, ctx->stream);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ctx, TC_ERR_MEMORY, "scratch %s: cannot allocate %zu bytes: %s", name, want, cudaGetErrorString(e));
+    }
+    b.n = want;
+  }
+  *out = b.p;
+  return TC_OK;
+}
+
+}  // namespace tcrt
+
+using tcrt::fail;
+
+namespace {
+
+// ---- host encodings (backend.py:309-348) ----
+bool le21_to_fe(const uint8_t* b, Fe& out) {
+  for (int i = 0; i < 6; i++) out.v[i] = 0;
+  for (int i = 0; i < 21; i++) out.v[i / 4] |= (uint32_t)b[i] << (8 * (i % 4));
+  // < p ?
+  Fe t;
+  return Fp::sub_km(t, out, FpParams::M0, FpParams::M5) != 0;
+}
+void fe_to_le21(const Fe& a, uint8_t* b) {
+  for (int i = 0; i < 21; i++) b[i] = (uint8_t)(a.v[i / 4] >> (8 * (i % 4)));
+}
+// decode_elem (backend.py:319-333); false on malformed / off-curve
+bool decode43(const uint8_t* raw, Aff& out) {
+  if (raw[0] == 0) {
+    for (int i = 1; i < 43; i++)
+      if (raw[i]) return false;
+    out = aff_inf();
+    return true;
+  }
+  if (raw[0] != 4) return false;
+  Fe x, y;
+  for (int i = 0; i < 6; i++) x.v[i] = y.v[i] = 0;
+  for (int i = 0; i < 21; i++) {
+    x.v[i / 4] |= (uint32_t)raw[1 + i] << (8 * (i % 4));
+    y.v[i / 4] |= (uint32_t)raw[22 + i] << (8 * (i % 4));
+  }
+  Fe t;
+  if (!Fq::sub_km(t, x, FqParams::M0, FqParams::M5) || !Fq::sub_km(t, y, FqParams::M0, FqParams::M5)) return false;
+  Fe xm = Fq::to_mont(x), ym = Fq::to_mont(y);
+  Fe lhs = Fq::sqr(ym);
+  Fe rhs = Fq::add(Fq::mul(Fq::sqr(xm), xm), xm);
+  if (!Fq::eq(lhs, rhs)) return false;
+  out = Aff{Fq::canon(xm), Fq::canon(ym)};
+  return true;
+}
+
+Aff g_host() {
+  Fe x{{0xbe9bb8c2u, 0x9f4698deu, 0x2e04a40bu, 0x96df9421u, 0xd6e0e406u, 0x000000abu}};
+  Fe y{{0xca83210eu, 0x0d3911f8u, 0x28e6ecd6u, 0xfcd508bdu, 0xc7320595u, 0x00000018u}};
+  return Aff{Fq::to_mont(x), Fq::to_mont(y)};
+}
+
+// k * P on the host (canonical scalar k < 2^192), MSB-first double-and-add
+Xyzz host_mul(const Aff& P, const Fe& k) {
+  Xyzz acc = xyzz_inf();
+  bool started = false;
+  for (int b = 191; b >= 0; b--) {
+    if (started) acc = xyzz_dbl(acc);
+    if ((k.v[b >> 5] >> (b & 31)) & 1u) {
+      xyzz_add_aff(acc, P);
+      started = true;
+    }
+  }
+  return acc;
+}
+Aff host_aff(const Xyzz& p) {
+  Aff r = xyzz_to_aff(p);
+  if (!aff_is_inf(r)) r = Aff{Fq::canon(r.x), Fq::canon(r.y)};
+  return r;
+}
+Fe fp_neg_canon(const Fe& a) {   // (-a) mod p, canonical input
+  Fe z{{0, 0, 0, 0, 0, 0}};
+  return Fp::canon(Fp::sub(z, a));
+}
+
+// ---- device encode/decode of SRS point arrays ----
+__global__ void k_encode43(const Aff* pts, uint64_t n, uint8_t* out) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  aff_encode43(pts[i], out + i * 43);
+}
+__global__ void k_decode43(const uint8_t* raw, uint64_t n, Aff* out, uint32_t* bad) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint8_t* r = raw + i * 43;
+  if (r[0] == 0) {
+    bool ok = true;
+    for (int k = 1; k < 43; k++) ok &= (r[k] == 0);
+    if (!ok) atomicOr(bad, 1u);
+    out[i] = aff_inf();
+    return;
+  }
+  Fe x, y;
+  for (int k = 0; k < 6; k++) x.v[k] = y.v[k] = 0;
+  for (int k = 0; k < 21; k++) {
+    x.v[k / 4] |= (uint32_t)r[1 + k] << (8 * (k % 4));
+    y.v[k / 4] |= (uint32_t)r[22 + k] << (8 * (k % 4));
+  }
+  Fe t;
+  bool inrange = Fq::sub_km(t, x, FqParams::M0, FqParams::M5) && Fq::sub_km(t, y, FqParams::M0, FqParams::M5);
+  Fe xm = Fq::to_mont(x), ym = Fq::to_mont(y);
+  bool on = Fq::eq(Fq::sqr(ym), Fq::add(Fq::mul(Fq::sqr(xm), xm), xm));
+  if (r[0] != 4 || !inrange || !on) atomicOr(bad, 1u);
+  out[i] = Aff{Fq::canon(xm), Fq::canon(ym)};
+}
+
+__global__ void k_field_op(int op, const Fe* a, const Fe* b, Fe* out, uint64_t n) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Fe r;
+  switch (op) {
+    case 0: r = Fq::from_mont(Fq::mul(Fq::to_mont(a[i]), Fq::to_mont(b[i]))); break;
+    case 1: r = Fp::from_mont(Fp::mul(Fp::to_mont(a[i]), Fp::to_mont(b[i]))); break;
+    case 2: r = Fq::canon(Fq::add(a[i], b[i])); break;
+    case 3: r = Fq::canon(Fq::sub(a[i], b[i])); break;
+    default: r = Fq::from_mont(Fq::inv(Fq::to_mont(a[i]))); break;
+  }
+  out[i] = r;
+}
+
+// read one device Aff result and encode it on the host
+int fetch_encode(tc_ctx* ctx, const Aff* d_pt, uint8_t* out43) {
+  Aff h;
+  TC_CUDA(ctx, cudaMemcpyAsync(&h, d_pt, sizeof(Aff), cudaMemcpyDeviceToHost, ctx->stream));
+  TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  aff_encode43(h, out43);
+  return TC_OK;
+}
+
+uint64_t shape_size(const uint32_t* shape, int m) {
+  uint64_t n = 1;
+  for (int j = 0; j < m; j++) n *= shape[j];
+  return n;
+}
+
+int check_shape(tc_ctx* ctx, const uint32_t* shape, int m) {
+  if (m < 1 || m > TC_MAX_AXES) return fail(ctx, TC_ERR_VALUE, "shape needs 1..%d axes, got %d", TC_MAX_AXES, m);
+  uint64_t n = 1;
+  for (int j = 0; j < m; j++) {
+    if (shape[j] < 1) return fail(ctx, TC_ERR_VALUE, "axis degree bound must be >= 1, got %u", shape[j]);
+    n *= shape[j];
+    if (n > (1ull << 26)) return fail(ctx, TC_ERR_VALUE, "coefficient array exceeds limit 2^26");
+  }
+  return TC_OK;
+}
+
+// canonical F_p tensor of the SRS shape from a device input of any dtype
+int load_field_tensor(tc_ctx* ctx, const void* d_in, int dtype, uint64_t n, int scale_bits, Fe** out,
+                      const char* name) {
+  Fe* buf;
+  TC_TRY(tcrt::scratch_t(ctx, name, n, &buf));
+  if (dtype == TC_DTYPE_FP_LIMBS) {
+    TC_CUDA(ctx, cudaMemcpyAsync(buf, d_in, n * sizeof(Fe), cudaMemcpyDeviceToDevice, ctx->stream));
+  } else {
+    TC_TRY(tcrt::quantize_device(ctx, d_in, dtype, n, scale_bits, buf));
+  }
+  *out = buf;
+  return TC_OK;
+}
+
+// ---- per-axis SRS exponent tables (host, F_p Montgomery arithmetic) ----
+// monomial: tau^e, e < d ; Lagrange on nodes 1..d: L_a(tau) = prod_{b != a} (tau - b)/(a - b)
+void axis_tables(const Fe& tau_c, uint32_t d, bool lagrange, std::vector<Fe>& out) {
+  Fe tau = Fp::to_mont(tau_c);
+  if (!lagrange) {
+    Fe acc = Fp::one();
+    for (uint32_t e = 0; e < d; e++) {
+      out.push_back(Fp::from_mont(acc));
+      acc = Fp::mul(acc, tau);
+    }
+    return;
+  }
+  // exact node?
+  for (uint32_t a = 0; a < d; a++) {
+    if (Fp::eq(tau, Fp::to_mont_small(a + 1))) {
+      for (uint32_t b = 0; b < d; b++) out.push_back(b == a ? Fp::from_mont(Fp::one()) : Fp::zero());
+      return;
+    }
+  }
+  // master = prod (tau - b); L_a = master / (tau - a) / w_a,  w_a = a! (d-1-a)! (-1)^(d-1-a)
+  std::vector<Fe> diff(d), fact(d + 1);
+  Fe master = Fp::one();
+  for (uint32_t b = 0; b < d; b++) {
+    diff[b] = Fp::sub(tau, Fp::to_mont_small(b + 1));
+    master = Fp::mul(master, diff[b]);
+  }
+  fact[0] = Fp::one();
+  for (uint32_t i = 1; i <= d; i++) fact[i] = Fp::mul(fact[i - 1], Fp::to_mont_small(i));
+  // batch-invert diff[a] * w_a
+  std::vector<Fe> den(d), pref(d);
+  Fe run = Fp::one();
+  for (uint32_t a = 0; a < d; a++) {
+    Fe w = Fp::mul(fact[a], fact[d - 1 - a]);
+    if ((d - 1 - a) & 1u) w = Fp::neg(w);
+    den[a] = Fp::mul(diff[a], w);
+    pref[a] = run;
+    run = Fp::mul(run, den[a]);
+  }
+  Fe inv = Fp::inv(run);
+  std::vector<Fe> res(d);
+  for (int a = (int)d - 1; a >= 0; a--) {
+    Fe ia = Fp::mul(inv, pref[a]);
+    inv = Fp::mul(inv, den[a]);
+    res[a] = Fp::from_mont(Fp::mul(master, ia));
+  }
+  out.insert(out.end(), res.begin(), res.end());
+}
+
+int srs_build_points(tc_ctx* ctx, tc_srs* srs, const std::vector<Fe>& taus, bool lagrange, Aff** dst) {
+  std::vector<Fe> tabs;
+  for (int j = 0; j < srs->m; j++) axis_tables(taus[j], srs->shape[j], lagrange, tabs);
+  Fe* d_exps;
+  TC_TRY(tcrt::scratch_t(ctx, "srs.exps", srs->n, &d_exps));
+  TC_TRY(tcrt::srs_exponents(ctx, tabs, srs->shape, srs->m, srs->n, d_exps));
+  TC_CUDA(ctx, cudaMalloc(dst, srs->n * sizeof(Aff)));
+  TC_TRY(tcrt::fixed_base_g(ctx, d_exps, srs->n, *dst));
+  return TC_OK;
+}
+
+// ---- host pairing (backend.py:219-291), restated over the shared F_q core ----
+struct F2 {
+  Fe a, b;
+};
+F2 f2mul(const F2& u, const F2& v) {
+  return F2{Fq::sub(Fq::mul(u.a, v.a), Fq::mul(u.b, v.b)), Fq::add(Fq::mul(u.a, v.b), Fq::mul(u.b, v.a))};
+}
+F2 f2sqr(const F2& u) {
+  return F2{Fq::mul(Fq::sub(u.a, u.b), Fq::add(u.a, u.b)), Fq::dbl(Fq::mul(u.a, u.b))};
+}
+
+// returns false on "pairing argument of unexpected order" (BackendError)
+bool host_pairing(const Aff& S, const Aff& T, F2& out) {
+  if (aff_is_inf(S) || aff_is_inf(T)) {
+    out = F2{Fq::one(), Fq::zero()};
+    return true;
+  }
+  Fe xq = Fq::neg(T.x), yq = T.y, xp = S.x, yp = S.y;
+  F2 f{Fq::one(), Fq::zero()};
+  Fe X = xp, Y = yp, Z = Fq::one();
+  // bits of p below the MSB: p = 2^161 + 2^24 + 1 -> bits 160..0
+  for (int bit = 160; bit >= 0; bit--) {
+    Fe XX = Fq::sqr(X), YY = Fq::sqr(Y), YYYY = Fq::sqr(YY), ZZ = Fq::sqr(Z);
+    Fe t = Fq::add(X, YY);
+    Fe Sd = Fq::dbl(Fq::sub(Fq::sub(Fq::sqr(t), XX), YYYY));
+    Fe M = Fq::add(Fq::add(Fq::dbl(XX), XX), Fq::sqr(ZZ));
+    // tangent line at R evaluated at (xq, i*yq)
+    Fe lr = Fq::sub(Fq::neg(Fq::dbl(YY)), Fq::mul(M, Fq::sub(Fq::mul(xq, ZZ), X)));
+    Fe li = Fq::mul(Fq::mul(Fq::mul(Fq::dbl(Y), Z), ZZ), yq);
+    f = f2mul(f2sqr(f), F2{lr, li});
+    Fe X3 = Fq::sub(Fq::sqr(M), Fq::dbl(Sd));
+    Fe Y3 = Fq::sub(Fq::mul(M, Fq::sub(Sd, X3)), Fq::dbl(Fq::dbl(Fq::dbl(YYYY))));
+    Fe Z3 = Fq::sub(Fq::sub(Fq::sqr(Fq::add(Y, Z)), YY), ZZ);
+    X = X3, Y = Y3, Z = Z3;
+    bool set = (bit == 0) || (bit == 24);
+    if (set) {
+      ZZ = Fq::sqr(Z);
+      Fe U2 = Fq::mul(xp, ZZ);
+      Fe S2 = Fq::mul(Fq::mul(yp, Z), ZZ);
+      Fe H = Fq::sub(U2, X);
+      Fe num = Fq::sub(S2, Y);
+      bool hz = Fq::is_zero(H), nz = Fq::is_zero(num);
+      if (hz && nz) return false;
+      if (!hz) {
+        Fe den = Fq::mul(H, Z);
+        Fe lr2 = Fq::sub(Fq::neg(Fq::mul(den, yp)), Fq::mul(num, Fq::sub(xq, xp)));
+        Fe li2 = Fq::mul(den, yq);
+        f = f2mul(f, F2{lr2, li2});
+        Fe HH = Fq::sqr(H);
+        Fe I = Fq::dbl(Fq::dbl(HH));
+        Fe J = Fq::mul(H, I);
+        Fe V = Fq::mul(X, I);
+        Fe r2 = Fq::dbl(num);
+        Fe X4 = Fq::sub(Fq::sub(Fq::sqr(r2), J), Fq::dbl(V));
+        Fe Y4 = Fq::sub(Fq::mul(r2, Fq::sub(V, X4)), Fq::dbl(Fq::mul(Y, J)));
+        Fe Z4 = Fq::sub(Fq::sub(Fq::sqr(Fq::add(Z, H)), ZZ), HH);
+        X = X4, Y = Y4, Z = Z4;
+      } else {
+        X = Fq::zero(), Y = Fq::one(), Z = Fq::zero();
+      }
+    }
+  }
+  // final exponentiation: (conj(f) / f)^120
+  Fe norm = Fq::add(Fq::sqr(f.a), Fq::sqr(f.b));
+  Fe ni = Fq::inv(norm);
+  Fe inva = Fq::mul(f.a, ni), invb = Fq::neg(Fq::mul(f.b, ni));
+  F2 g{Fq::add(Fq::mul(f.a, inva), Fq::mul(f.b, invb)), Fq::sub(Fq::mul(f.a, invb), Fq::mul(f.b, inva))};
+  F2 o{Fq::one(), Fq::zero()};
+  for (uint32_t e = 120; e; e >>= 1) {
+    if (e & 1u) o = f2mul(o, g);
+    g = f2sqr(g);
+  }
+  out = F2{Fq::canon(o.a), Fq::canon(o.b)};
+  return true;
+}
+
+bool f2_eq(const F2& u, const F2& v) { return Fq::eq(u.a, v.a) && Fq::eq(u.b, v.b); }
+
+}  // namespace
+
+// ======================================================================================
+// exported ABI
+// ======================================================================================
+extern "C" {
+
+int tc_abi_version(void) { return TC_ABI_VERSION; }
+
+int tc_ctx_create(int device, void* cuda_stream, tc_ctx** out) {
+  if (!out) return TC_ERR_ARGUMENT;
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return TC_ERR_CUDA;
+  }
+  if (device < 0 || device >= count) return TC_ERR_ARGUMENT;
+  if (cudaSetDevice(device) != cudaSuccess) return TC_ERR_CUDA;
+  tc_ctx* ctx = new tc_ctx();
+  ctx->device = device;
+  ctx->stream = (cudaStream_t)cuda_stream;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) ctx->num_sms = prop.multiProcessorCount;
+  if (cudaMalloc(&ctx->d_flags, 64) != cudaSuccess || cudaMallocHost(&ctx->h_flags, 64) != cudaSuccess) {
+    delete ctx;
+    return TC_ERR_CUDA;
+  }
+  *out = ctx;
+  return TC_OK;
+}
+
+int tc_ctx_destroy(tc_ctx* ctx) {
+  if (!ctx) return TC_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& kv : ctx->scratch)
+    if (kv.second.p) cudaFreeAsync(kv.second.p, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+  cudaFree(ctx->d_flags);
+  cudaFreeHost(ctx->h_flags);
+  delete ctx;
+  return TC_OK;
+}
+
+int tc_ctx_set_stream(tc_ctx* ctx, void* s) {
+  if (!ctx) return TC_ERR_ARGUMENT;
+  ctx->stream = (cudaStream_t)s;
+  return TC_OK;
+}
+
+int tc_ctx_synchronize(tc_ctx* ctx) {
+  TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return TC_OK;
+}
+
+const char* tc_ctx_last_error(const tc_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+uint64_t tc_ctx_launch_count(const tc_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// ---- SRS ----
+int tc_srs_generate(tc_ctx* ctx, const uint32_t* shape, int m, const uint8_t* taus_le21, int flags, tc_srs** out) {
+  if (!ctx || !shape || !taus_le21 || !out) return TC_ERR_ARGUMENT;
+  TC_TRY(check_shape(ctx, shape, m));
+  if (!(flags & (TC_SRS_MONOMIAL | TC_SRS_LAGRANGE))) return fail(ctx, TC_ERR_ARGUMENT, "srs flags");
+  std::vector<Fe> taus(m);
+  for (int j = 0; j < m; j++)
+    if (!le21_to_fe(taus_le21 + 21 * j, taus[j])) return fail(ctx, TC_ERR_VALUE, "trapdoor %d out of range", j);
+  tc_srs* srs = new tc_srs();
+  srs->device = ctx->device;
+  srs->m = m;
+  for (int j = 0; j < m; j++) srs->shape[j] = shape[j];
+  srs->n = shape_size(shape, m);
+  int s = TC_OK;
+  if (flags & TC_SRS_MONOMIAL) s = srs_build_points(ctx, srs, taus, false, &srs->monomial);
+  if (!s && (flags & TC_SRS_LAGRANGE)) s = srs_build_points(ctx, srs, taus, true, &srs->lagrange);
+  if (!s) {   // axis elements g^{tau_j}
+    Fe* d_t;
+    Aff* d_a;
+    s = tcrt::scratch_t(ctx, "srs.axis_t", m, &d_t);
+    if (!s) s = tcrt::scratch_t(ctx, "srs.axis_a", m, &d_a);
+    if (!s && cudaMemcpyAsync(d_t, taus.data(), m * sizeof(Fe), cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess)
+      s = fail(ctx, TC_ERR_CUDA, "copy taus");
+    if (!s) s = tcrt::fixed_base_g(ctx, d_t, m, d_a);
+    if (!s && cudaMemcpyAsync(srs->axis, d_a, m * sizeof(Aff), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess)
+      s = fail(ctx, TC_ERR_CUDA, "copy axis");
+    if (!s && cudaStreamSynchronize(ctx->stream) != cudaSuccess) s = fail(ctx, TC_ERR_CUDA, "sync");
+  }
+  if (s) {
+    tc_srs_destroy(srs);
+    return s;
+  }
+  *out = srs;
+  return TC_OK;
+}
+
+int tc_srs_load(tc_ctx* ctx, const uint32_t* shape, int m, const uint8_t* monomial43, const uint8_t* axis43, tc_srs** out) {
+  if (!ctx || !shape || !monomial43 || !axis43 || !out) return TC_ERR_ARGUMENT;
+  TC_TRY(check_shape(ctx, shape, m));
+  tc_srs* srs = new tc_srs();
+  srs->device = ctx->device;
+  srs->m = m;
+  for (int j = 0; j < m; j++) srs->shape[j] = shape[j];
+  srs->n = shape_size(shape, m);
+  for (int j = 0; j < m; j++) {
+    if (!decode43(axis43 + 43 * j, srs->axis[j])) {
+      delete srs;
+      return fail(ctx, TC_ERR_VALUE, "axis element %d: bad encoding or point not on curve", j);
+    }
+  }
+  uint8_t* d_raw;
+  int s = tcrt::scratch_t(ctx, "srs.raw", srs->n * 43, &d_raw);
+  if (!s && cudaMalloc(&srs->monomial, srs->n * sizeof(Aff)) != cudaSuccess) s = fail(ctx, TC_ERR_MEMORY, "srs alloc");
+  if (!s && cudaMemcpyAsync(d_raw, monomial43, srs->n * 43, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess)
+    s = fail(ctx, TC_ERR_CUDA, "copy srs");
+  if (!s && cudaMemsetAsync(ctx->d_flags, 0, 4, ctx->stream) != cudaSuccess) s = fail(ctx, TC_ERR_CUDA, "memset");
+  if (!s) {
+    k_decode43<<<tcrt::blocks_for(srs->n, 128), 128, 0, ctx->stream>>>(d_raw, srs->n, srs->monomial, ctx->d_flags);
+    ctx->launches++;
+    if (cudaMemcpyAsync(ctx->h_flags, ctx->d_flags, 4, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+      s = fail(ctx, TC_ERR_CUDA, "decode srs: %s", cudaGetErrorString(cudaGetLastError()));
+    else if (ctx->h_flags[0])
+      s = fail(ctx, TC_ERR_VALUE, "srs element: bad encoding or point not on curve");
+  }
+  if (s) {
+    tc_srs_destroy(srs);
+    return s;
+  }
+  *out = srs;
+  return TC_OK;
+}
+
+int tc_srs_export(tc_ctx* ctx, const tc_srs* srs, int which, uint8_t* out43) {
+  if (!ctx || !srs || !out43) return TC_ERR_ARGUMENT;
+  const Aff* pts = (which == TC_SRS_LAGRANGE) ? srs->lagrange : srs->monomial;
+  if (!pts) return fail(ctx, TC_ERR_VALUE, "srs has no elements of kind %d", which);
+  uint8_t* d_raw;
+  TC_TRY(tcrt::scratch_t(ctx, "srs.raw", srs->n * 43, &d_raw));
+  k_encode43<<<tcrt::blocks_for(srs->n, 128), 128, 0, ctx->stream>>>(pts, srs->n, d_raw);
+  TC_LAUNCHED(ctx);
+  TC_CUDA(ctx, cudaMemcpyAsync(out43, d_raw, srs->n * 43, cudaMemcpyDeviceToHost, ctx->stream));
+  TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return TC_OK;
+}
+
+int tc_srs_export_axis(const tc_srs* srs, uint8_t* out43) {
+  if (!srs || !out43) return TC_ERR_ARGUMENT;
+  for (int j = 0; j < srs->m; j++) aff_encode43(srs->axis[j], out43 + 43 * j);
+  return TC_OK;
+}
+
+int tc_srs_has(const tc_srs* srs, int which) {
+  if (!srs) return 0;
+  return which == TC_SRS_LAGRANGE ? srs->lagrange != nullptr : srs->monomial != nullptr;
+}
+
+uint64_t tc_srs_size(const tc_srs* srs) { return srs ? srs->n : 0; }
+
+int tc_srs_destroy(tc_srs* srs) {
+  if (!srs) return TC_OK;
+  cudaSetDevice(srs->device);
+  if (srs->monomial) cudaFree(srs->monomial);
+  if (srs->lagrange) cudaFree(srs->lagrange);
+  delete srs;
+  return TC_OK;
+}
+
+// ---- polynomial entry points ----
+int tc_quantize(tc_ctx* ctx, const void* d_in, int dtype, uint64_t n, int scale_bits, uint32_t* d_out) {
+  if (!ctx || (n && (!d_in || !d_out))) return TC_ERR_ARGUMENT;
+  if (dtype == TC_DTYPE_FP_LIMBS) return fail(ctx, TC_ERR_ARGUMENT, "quantize: input already field elements");
+  return tcrt::quantize_device(ctx, d_in, dtype, n, scale_bits, (Fe*)d_out);
+}
+
+int tc_interpolate(tc_ctx* ctx, uint32_t* d_limbs, const uint32_t* shape, int m) {
+  if (!ctx || !d_limbs || !shape) return TC_ERR_ARGUMENT;
+  TC_TRY(check_shape(ctx, shape, m));
+  return tcrt::interpolate_device(ctx, (Fe*)d_limbs, shape, m);
+}
+
+int tc_evaluate(tc_ctx* ctx, const uint32_t* d_coeffs, const uint32_t* shape, int m, const uint8_t* point_le21,
+                uint8_t* out_y21) {
+  if (!ctx || !d_coeffs || !shape || !point_le21 || !out_y21) return TC_ERR_ARGUMENT;
+  TC_TRY(check_shape(ctx, shape, m));
+  std::vector<Fe> pt(m);
+  for (int j = 0; j < m; j++)
+    if (!le21_to_fe(point_le21 + 21 * j, pt[j])) return fail(ctx, TC_ERR_VALUE, "point coordinate %d out of range", j);
+  Fe y;
+  TC_TRY(tcrt::evaluate_device(ctx, (const Fe*)d_coeffs, shape, m, pt.data(), &y));
+  fe_to_le21(y, out_y21);
+  return TC_OK;
+}
+
+int tc_open_quotients(tc_ctx* ctx, const uint32_t* d_coeffs, const uint32_t* shape, int m, const uint8_t* omega_le21,
+                      uint32_t* d_quotients, uint8_t* out_y21) {
+  if (!ctx || !d_coeffs || !shape || !omega_le21 || !d_quotients || !out_y21) return TC_ERR_ARGUMENT;
+  TC_TRY(check_shape(ctx, shape, m));
+  std::vector<Fe> om(m);
+  for (int j = 0; j < m; j++)
+    if (!le21_to_fe(omega_le21 + 21 * j, om[j])) return fail(ctx, TC_ERR_VALUE, "point coordinate %d out of range", j);
+  Fe y;
+  TC_TRY(tcrt::open_quotients_device(ctx, (const Fe*)d_coeffs, shape, m, om.data(), (Fe*)d_quotients, &y));
+  fe_to_le21(y, out_y21);
+  return TC_OK;
+}
+
+int tc_msm(tc_ctx* ctx, const tc_srs* srs, int which, const uint32_t* d_scalars, uint64_t n, uint8_t* out43) {
+  if (!ctx || !srs || !out43 || (n && !d_scalars)) return TC_ERR_ARGUMENT;
+  const Aff* bases = (which == TC_SRS_LAGRANGE) ? srs->lagrange : srs->monomial;
+  if (!bases) return fail(ctx, TC_ERR_VALUE, "srs has no elements of kind %d", which);
+  if (n > srs->n) return fail(ctx, TC_ERR_VALUE, "msm: %llu scalars for an srs of %llu elements",
+                              (unsigned long long)n, (unsigned long long)srs->n);
+  Aff* d_out;
+  TC_TRY(tcrt::scratch_t(ctx, "msm.out", 1, &d_out));
+  TC_TRY(tcrt::msm_device(ctx, tcrt::SCALAR_FP_CANON, d_scalars, bases, n, d_out));
+  return fetch_encode(ctx, d_out, out43);
+}
+
+static int commit_one(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int scale_bits, int route,
+                      uint8_t* out43) {
+  const uint64_t n = srs->n;
+  bool lag = (route == TC_ROUTE_LAGRANGE) || (route == TC_ROUTE_AUTO && srs->lagrange);
+  if (lag && !srs->lagrange) return fail(ctx, TC_ERR_VALUE, "srs has no Lagrange elements");
+  if (!lag && !srs->monomial) return fail(ctx, TC_ERR_VALUE, "srs has no monomial elements");
+  Fe* vals;
+  TC_TRY(load_field_tensor(ctx, d_in, dtype, n, scale_bits, &vals, "commit.vals"));
+  Aff* d_out;
+  TC_TRY(tcrt::scratch_t(ctx, "commit.out", 1, &d_out));
+  if (lag) {
+    // C_T = sum_grid T[w] * g^{L_w(tau)}: no interpolation, scalars are the raw grid values
+    TC_TRY(tcrt::msm_device(ctx, tcrt::SCALAR_FP_CANON, vals, srs->lagrange, n, d_out));
+  } else {
+    TC_TRY(tcrt::interpolate_device(ctx, vals, srs->shape, srs->m));
+    TC_TRY(tcrt::msm_device(ctx, tcrt::SCALAR_FP_CANON, vals, srs->monomial, n, d_out));
+  }
+  return fetch_encode(ctx, d_out, out43);
+}
+
+int tc_commit(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int scale_bits, int route, uint8_t* out43) {
+  if (!ctx || !srs || !d_in || !out43) return TC_ERR_ARGUMENT;
+  return commit_one(ctx, srs, d_in, dtype, scale_bits, route, out43);
+}
+
+int tc_commit_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype, int scale_bits,
+                    int route, uint8_t* out43) {
+  if (!ctx || !srs || !d_ins || !out43 || count < 0) return TC_ERR_ARGUMENT;
+  for (int i = 0; i < count; i++) TC_TRY(commit_one(ctx, srs, d_ins[i], dtype, scale_bits, route, out43 + 43 * i));
+  return TC_OK;
+}
+
+int tc_open(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int scale_bits, const uint8_t* omega_le21,
+            int route, uint8_t* out_y21, uint8_t* out_pi43) {
+  if (!ctx || !srs || !d_in || !omega_le21 || !out_y21 || !out_pi43) return TC_ERR_ARGUMENT;
+  if (!srs->monomial) return fail(ctx, TC_ERR_VALUE, "tc_open needs the monomial srs");
+  (void)route;
+  const uint64_t n = srs->n;
+  const int m = srs->m;
+  std::vector<Fe> om(m);
+  for (int j = 0; j < m; j++)
+    if (!le21_to_fe(omega_le21 + 21 * j, om[j])) return fail(ctx, TC_ERR_VALUE, "point coordinate %d out of range", j);
+  Fe* vals;
+  TC_TRY(load_field_tensor(ctx, d_in, dtype, n, scale_bits, &vals, "open.vals"));
+  TC_TRY(tcrt::interpolate_device(ctx, vals, srs->shape, m));
+  Fe* qs;
+  TC_TRY(tcrt::scratch_t(ctx, "open.q", (uint64_t)m * n, &qs));
+  Fe y;
+  TC_TRY(tcrt::open_quotients_device(ctx, vals, srs->shape, m, om.data(), qs, &y));
+  fe_to_le21(y, out_y21);
+  Aff* d_out;
+  TC_TRY(tcrt::scratch_t(ctx, "open.out", 1, &d_out));
+  uint64_t span = n;   // quotient a is supported on the lex prefix of length prod_{t>=a} d_t
+  for (int a = 0; a < m; a++) {
+    TC_TRY(tcrt::msm_device(ctx, tcrt::SCALAR_FP_CANON, qs + (uint64_t)a * n, srs->monomial, span, d_out));
+    TC_TRY(fetch_encode(ctx, d_out, out_pi43 + 43 * a));
+    span /= srs->shape[a];
+  }
+  return TC_OK;
+}
+
+// ---- Terkle ----
+int tc_terkle_build(tc_ctx* ctx, const tc_srs* node_srs, const uint8_t* leaves_le21, uint64_t n, uint8_t* out_nodes43,
+                    uint64_t* inout_count) {
+  if (!ctx || !node_srs || !leaves_le21 || !out_nodes43 || !inout_count) return TC_ERR_ARGUMENT;
+  if (n == 0) return fail(ctx, TC_ERR_VALUE, "empty leaf list");
+  const uint64_t B = node_srs->n;
+  if (B < 2) return fail(ctx, TC_ERR_VALUE, "tree arity must be >= 2");
+  uint64_t L = 1, cap = B;
+  while (cap < n) cap *= B, L++;
+  uint64_t total_nodes = 0, w = cap;
+  for (uint64_t l = 0; l < L; l++) w /= B, total_nodes += w;
+  if (*inout_count < total_nodes) return fail(ctx, TC_ERR_VALUE, "need room for %llu nodes", (unsigned long long)total_nodes);
+  std::vector<Fe> vals(cap);
+  for (uint64_t i = 0; i < cap; i++) {
+    if (i < n) {
+      if (!le21_to_fe(leaves_le21 + 21 * i, vals[i])) return fail(ctx, TC_ERR_VALUE, "leaf %llu out of range", (unsigned long long)i);
+    } else {
+      vals[i] = Fe{{0, 0, 0, 0, 0, 0}};
+    }
+  }
+  Fe* d_vals;
+  Aff* d_out;
+  TC_TRY(tcrt::scratch_t(ctx, "terkle.vals", cap, &d_vals));
+  TC_TRY(tcrt::scratch_t(ctx, "terkle.out", 1, &d_out));
+  const Aff* bases = node_srs->lagrange ? node_srs->lagrange : node_srs->monomial;
+  bool lag = node_srs->lagrange != nullptr;
+  uint64_t written = 0;
+  const uint8_t tag[] = {'t', 'e', 'r', 'k', 'l', 'e', '/', 'n', 'o', 'd', 'e'};
+  for (uint64_t l = 0; l < L; l++) {
+    uint64_t nodes = vals.size() / B;
+    TC_CUDA(ctx, cudaMemcpyAsync(d_vals, vals.data(), vals.size() * sizeof(Fe), cudaMemcpyHostToDevice, ctx->stream));
+    std::vector<Fe> next(nodes);
+    for (uint64_t u = 0; u < nodes; u++) {
+      Fe* z = d_vals + u * B;
+      if (!lag) TC_TRY(tcrt::interpolate_device(ctx, z, node_srs->shape, node_srs->m));
+      TC_TRY(tcrt::msm_device(ctx, tcrt::SCALAR_FP_CANON, z, bases, B, d_out));
+      uint8_t* enc = out_nodes43 + 43 * written;
+      TC_TRY(fetch_encode(ctx, d_out, enc));
+      next[u] = hash_to_scalar(enc, 43, tag, sizeof tag);
+      written++;
+    }
+    vals.swap(next);
+  }
+  *inout_count = written;
+  return TC_OK;
+}
+
+// ---- host verifier primitive ----
+int tc_pairing(const uint8_t* a43, const uint8_t* b43, uint8_t* out42) {
+  if (!a43 || !b43 || !out42) return TC_ERR_ARGUMENT;
+  Aff a, b;
+  if (!decode43(a43, a) || !decode43(b43, b)) return TC_ERR_VALUE;
+  F2 r;
+  if (!host_pairing(a, b, r)) return TC_ERR_BACKEND;
+  Fe ra = Fq::from_mont(r.a), rb = Fq::from_mont(r.b);
+  fe_to_le21(ra, out42);
+  fe_to_le21(rb, out42 + 21);
+  return TC_OK;
+}
+
+// tc_verify (product-of-pairings form SPEC.md:313), CPU only
+int tc_verify_host(int m, const uint8_t* axis43, const uint8_t* c43, const uint8_t* omega_le21, const uint8_t* y21,
+                   const uint8_t* proofs43, int* ok) {
+  if (!axis43 || !c43 || !omega_le21 || !y21 || !proofs43 || !ok || m < 1) return TC_ERR_ARGUMENT;
+  Aff C, g = g_host();
+  if (!decode43(c43, C)) return TC_ERR_VALUE;
+  Fe y;
+  if (!le21_to_fe(y21, y)) return TC_ERR_VALUE;
+  Xyzz lhs_pt = host_mul(g, fp_neg_canon(y));
+  if (!aff_is_inf(C)) xyzz_add_aff(lhs_pt, C);
+  F2 lhs, rhs{Fq::one(), Fq::zero()};
+  if (!host_pairing(host_aff(lhs_pt), g, lhs)) return TC_ERR_BACKEND;
+  for (int i = 0; i < m; i++) {
+    Aff pi, ax;
+    Fe w;
+    if (!decode43(proofs43 + 43 * i, pi) || !decode43(axis43 + 43 * i, ax) || !le21_to_fe(omega_le21 + 21 * i, w))
+      return TC_ERR_VALUE;
+    Xyzz t = host_mul(g, fp_neg_canon(w));
+    if (!aff_is_inf(ax)) xyzz_add_aff(t, ax);
+    F2 e;
+    if (!host_pairing(pi, host_aff(t), e)) return TC_ERR_BACKEND;
+    rhs = f2mul(rhs, e);
+  }
+  *ok = f2_eq(lhs, rhs) ? 1 : 0;
+  return TC_OK;
+}
+
+// ---- self-test hooks ----
+int tc_host_fq_mul(const uint32_t* a, const uint32_t* b, uint32_t* out) {
+  Fe x, y;
+  memcpy(x.v, a, 24);
+  memcpy(y.v, b, 24);
+  Fe r = Fq::from_mont(Fq::mul(Fq::to_mont(x), Fq::to_mont(y)));
+  memcpy(out, r.v, 24);
+  return TC_OK;
+}
+int tc_host_fp_mul(const uint32_t* a, const uint32_t* b, uint32_t* out) {
+  Fe x, y;
+  memcpy(x.v, a, 24);
+  memcpy(y.v, b, 24);
+  Fe r = Fp::from_mont(Fp::mul(Fp::to_mont(x), Fp::to_mont(y)));
+  memcpy(out, r.v, 24);
+  return TC_OK;
+}
+int tc_host_g_mul(const uint8_t* k_le21, uint8_t* out43) {
+  Fe k;
+  for (int i = 0; i < 6; i++) k.v[i] = 0;
+  for (int i = 0; i < 21; i++) k.v[i / 4] |= (uint32_t)k_le21[i] << (8 * (i % 4));
+  aff_encode43(host_aff(host_mul(g_host(), k)), out43);
+  return TC_OK;
+}
+int tc_host_hash_to_scalar(const uint8_t* data, uint32_t n, const uint8_t* tag, uint32_t tn, uint8_t* out21) {
+  fe_to_le21(hash_to_scalar(data, n, tag, tn), out21);
+  return TC_OK;
+}
+
+int tc_debug_field(tc_ctx* ctx, int op, const uint32_t* d_a, const uint32_t* d_b, uint32_t* d_out, uint64_t n) {
+  if (!ctx) return TC_ERR_ARGUMENT;
+  k_field_op<<<tcrt::blocks_for(n, 128), 128, 0, ctx->stream>>>(op, (const Fe*)d_a, (const Fe*)d_b, (Fe*)d_out, n);
+  TC_LAUNCHED(ctx);
+  TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return TC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,230 @@
+// K2 / K4: the polynomial side of the prover on the device.
+//
+// interpolate_device  — mvpoly.interpolate_lagrange (mvpoly.py:233-247): for each axis j the
+//   d_j x d_j matrix B_j (column l = monomial coefficients of the l-th Lagrange basis
+//   polynomial on nodes 1..d_j, mvpoly.py:193-218) is applied to every fibre along axis j
+//   (mvpoly.py:168-186).  A block stages FB whole fibres in shared memory; each output
+//   coefficient is a length-d_j dot product accumulated as full 384-bit products and
+//   Montgomery-reduced ONCE (sum < 4 d p^2 < p R for d < 2^28), so a MAC costs the 6x6
+//   product only.  B_j is kept in Montgomery form and the samples canonical, so the
+//   reduction lands directly on canonical coefficients.
+// open_quotients_device — mvpoly.open_quotients (mvpoly.py:521-534) built from
+//   divide_by_linear (mvpoly.py:452-484): after dividing along axis a the remainder is
+//   independent of X_0..X_a, i.e. supported on the lex prefix of length prod_{t>a} d_t, so
+//   axis a only touches fibres of that prefix (one thread per fibre, synthetic division).
+// evaluate_device — mvpoly.evaluate (mvpoly.py:140-161): per-axis Horner contraction.
+#include "tc_internal.cuh"
+
+using namespace tc;
+
+namespace {
+
+// acc[0..11] += a * b  (12-limb accumulator; callers keep the sum below 2^384)
+__device__ __forceinline__ void mac_wide(uint32_t acc[12], const Fe& a, const Fe& b) {
+  uint32_t T[12];
+  Fp::mul_wide(T, a, b);
+  asm("add.cc.u32  %0, %0, %12;\n\t"
+      "addc.cc.u32 %1, %1, %13;\n\t"
+      "addc.cc.u32 %2, %2, %14;\n\t"
+      "addc.cc.u32 %3, %3, %15;\n\t"
+      "addc.cc.u32 %4, %4, %16;\n\t"
+      "addc.cc.u32 %5, %5, %17;\n\t"
+      "addc.cc.u32 %6, %6, %18;\n\t"
+      "addc.cc.u32 %7, %7, %19;\n\t"
+      "addc.cc.u32 %8, %8, %20;\n\t"
+      "addc.cc.u32 %9, %9, %21;\n\t"
+      "addc.cc.u32 %10, %10, %22;\n\t"
+      "addc.u32    %11, %11, %23;\n\t"
+      : "+r"(acc[0]), "+r"(acc[1]), "+r"(acc[2]), "+r"(acc[3]), "+r"(acc[4]), "+r"(acc[5]),
+        "+r"(acc[6]), "+r"(acc[7]), "+r"(acc[8]), "+r"(acc[9]), "+r"(acc[10]), "+r"(acc[11])
+      : "r"(T[0]), "r"(T[1]), "r"(T[2]), "r"(T[3]), "r"(T[4]), "r"(T[5]), "r"(T[6]), "r"(T[7]),
+        "r"(T[8]), "r"(T[9]), "r"(T[10]), "r"(T[11]));
+}
+
+__device__ __forceinline__ uint64_t fibre_addr(uint64_t f, uint32_t l, uint32_t d, uint64_t stride) {
+  uint64_t o = f / stride, i = f - o * stride;
+  return o * d * stride + (uint64_t)l * stride + i;
+}
+
+// one block = FB fibres along an axis with extent d and stride `stride`
+__global__ void __launch_bounds__(256) k_interp_axis(Fe* data, const Fe* Bm, uint32_t d, uint64_t stride,
+                                                     uint64_t nfib, uint32_t FB) {
+  extern __shared__ Fe sh[];   // FB * d samples, fibre-major
+  uint64_t f0 = (uint64_t)blockIdx.x * FB;
+  uint32_t nloc = (nfib - f0 < FB) ? (uint32_t)(nfib - f0) : FB;
+  uint32_t tot = nloc * d;
+  const bool contiguous = (stride == 1);
+  for (uint32_t idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+    uint32_t fl, l;
+    if (contiguous) {
+      fl = idx / d;
+      l = idx - fl * d;
+    } else {
+      l = idx / nloc;
+      fl = idx - l * nloc;
+    }
+    sh[fl * d + l] = data[fibre_addr(f0 + fl, l, d, stride)];
+  }
+  __syncthreads();
+  for (uint32_t idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+    uint32_t fl, k;
+    if (contiguous) {
+      fl = idx / d;
+      k = idx - fl * d;
+    } else {
+      k = idx / nloc;
+      fl = idx - k * nloc;
+    }
+    uint32_t acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    const Fe* v = sh + fl * d;
+    for (uint32_t l = 0; l < d; l++) mac_wide(acc, v[l], Bm[(uint64_t)l * d + k]);
+    Fe r = Fp::canon(Fp::redc(acc));
+    // every sample of this block was staged before any write, fibres are disjoint
+    data[fibre_addr(f0 + fl, k, d, stride)] = r;
+  }
+}
+
+// divide the prefix-supported remainder r by (X_a - v) along axis a (extent d, stride s):
+// fibres i in [0, s); q written at the same offsets; r keeps only its X_a^0 slice
+__global__ void k_divide_axis(Fe* r, Fe* q, uint32_t d, uint64_t s, Fe v_mont) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= s) return;
+  Fe carry = r[(uint64_t)(d - 1) * s + i];
+  if (d > 1) r[(uint64_t)(d - 1) * s + i] = Fp::zero();
+  for (int c = (int)d - 2; c >= 0; c--) {
+    uint64_t pos = (uint64_t)c * s + i;
+    q[pos] = Fp::canon(carry);
+    carry = Fp::add(r[pos], Fp::mul(v_mont, carry));
+    r[pos] = Fp::zero();
+  }
+  r[i] = Fp::canon(carry);
+}
+
+// out[rest] = sum_k c[k, rest] x^k  (Horner along the leading axis of extent d)
+__global__ void k_horner_lead(const Fe* c, Fe* out, uint32_t d, uint64_t rest, Fe x_mont) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= rest) return;
+  Fe acc = c[(uint64_t)(d - 1) * rest + i];
+  for (int k = (int)d - 2; k >= 0; k--) acc = Fp::add(Fp::mul(acc, x_mont), c[(uint64_t)k * rest + i]);
+  out[i] = Fp::canon(acc);
+}
+
+// ---- host-side B_j (Montgomery form), cached per extent d ----
+std::vector<Fe> lagrange_matrix_host(uint32_t d) {
+  using F = Fp;
+  std::vector<Fe> master(d + 1, F::zero());
+  master[0] = F::one();
+  uint32_t deg = 0;
+  for (uint32_t z = 1; z <= d; z++) {   // multiply by (X - z)
+    Fe zm = F::to_mont_small(z);
+    for (int k = (int)deg + 1; k >= 0; k--) {
+      Fe lower = (k > 0) ? master[k - 1] : F::zero();
+      master[k] = F::sub(lower, F::mul(master[k], zm));
+    }
+    deg++;
+  }
+  // w_l = prod_{r != l} (l - r) over nodes 1..d: l! * (d-1-l)! * (-1)^(d-1-l)
+  std::vector<Fe> fact(d + 1);
+  fact[0] = F::one();
+  for (uint32_t i = 1; i <= d; i++) fact[i] = F::mul(fact[i - 1], F::to_mont_small(i));
+  std::vector<Fe> B((size_t)d * d);
+  std::vector<Fe> q(d);
+  for (uint32_t l = 0; l < d; l++) {
+    Fe zm = F::to_mont_small(l + 1);
+    Fe carry = master[d];
+    for (int k = (int)d - 1; k >= 0; k--) {
+      q[k] = carry;
+      carry = F::add(master[k], F::mul(carry, zm));
+    }
+    Fe w = F::mul(fact[l], fact[d - 1 - l]);
+    if ((d - 1 - l) & 1u) w = F::neg(w);
+    Fe wi = F::inv(w);
+    for (uint32_t k = 0; k < d; k++) B[(size_t)l * d + k] = F::canon(F::mul(q[k], wi));
+  }
+  return B;
+}
+
+}  // namespace
+
+namespace tcrt {
+
+int interpolate_device(tc_ctx* ctx, Fe* d_vals, const uint32_t* shape, int m) {
+  cudaStream_t st = ctx->stream;
+  uint64_t n = 1;
+  for (int j = 0; j < m; j++) n *= shape[j];
+  uint64_t stride = n;
+  for (int j = 0; j < m; j++) {
+    uint32_t d = shape[j];
+    stride /= d;
+    if (d == 1) continue;   // degree-0 axis: identity transform
+    std::string key = "interp.B." + std::to_string(d);
+    Fe* dB;
+    bool have = ctx->scratch.count(key + ".ready") != 0;
+    TC_TRY(scratch_t(ctx, key.c_str(), (uint64_t)d * d, &dB));
+    if (!have) {
+      std::vector<Fe> B = lagrange_matrix_host(d);
+      TC_CUDA(ctx, cudaMemcpyAsync(dB, B.data(), B.size() * sizeof(Fe), cudaMemcpyHostToDevice, st));
+      TC_CUDA(ctx, cudaStreamSynchronize(st));
+      ctx->scratch[key + ".ready"] = tc_ctx::Buf{};
+    }
+    uint32_t FB = std::max<uint32_t>(1u, 2048u / d);
+    uint64_t nfib = n / d;
+    size_t smem = (size_t)FB * d * sizeof(Fe);
+    if (smem > 48 * 1024)
+      TC_CUDA(ctx, cudaFuncSetAttribute(k_interp_axis, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    unsigned grid = (unsigned)((nfib + FB - 1) / FB);
+    k_interp_axis<<<grid, 256, smem, st>>>(d_vals, dB, d, stride, nfib, FB);
+    TC_LAUNCHED(ctx);
+  }
+  return TC_OK;
+}
+
+// r (scratch copy of the coefficients) is consumed; quotients are m x n, zero outside
+// their support.  omega canonical; returns y canonical on the host.
+int open_quotients_device(tc_ctx* ctx, const Fe* d_coeffs, const uint32_t* shape, int m,
+                          const Fe* omega_canon, Fe* d_quotients, Fe* h_y) {
+  cudaStream_t st = ctx->stream;
+  uint64_t n = 1;
+  for (int j = 0; j < m; j++) n *= shape[j];
+  Fe* r;
+  TC_TRY(scratch_t(ctx, "open.rem", n, &r));
+  TC_CUDA(ctx, cudaMemcpyAsync(r, d_coeffs, n * sizeof(Fe), cudaMemcpyDeviceToDevice, st));
+  TC_CUDA(ctx, cudaMemsetAsync(d_quotients, 0, (uint64_t)m * n * sizeof(Fe), st));
+  uint64_t span = n;   // remainder support: lex prefix of length span
+  for (int a = 0; a < m; a++) {
+    uint32_t d = shape[a];
+    uint64_t s = span / d;
+    Fe vm = Fp::to_mont(omega_canon[a]);
+    k_divide_axis<<<blocks_for(s, 128), 128, 0, st>>>(r, d_quotients + (uint64_t)a * n, d, s, vm);
+    TC_LAUNCHED(ctx);
+    span = s;
+  }
+  TC_CUDA(ctx, cudaMemcpyAsync(h_y, r, sizeof(Fe), cudaMemcpyDeviceToHost, st));
+  TC_CUDA(ctx, cudaStreamSynchronize(st));
+  return TC_OK;
+}
+
+int evaluate_device(tc_ctx* ctx, const Fe* d_coeffs, const uint32_t* shape, int m,
+                    const Fe* point_canon, Fe* h_y) {
+  cudaStream_t st = ctx->stream;
+  uint64_t n = 1;
+  for (int j = 0; j < m; j++) n *= shape[j];
+  Fe *bufA, *bufB;
+  TC_TRY(scratch_t(ctx, "eval.a", n, &bufA));
+  TC_TRY(scratch_t(ctx, "eval.b", n, &bufB));
+  const Fe* src = d_coeffs;
+  uint64_t rest = n;
+  for (int a = 0; a < m; a++) {
+    uint32_t d = shape[a];
+    rest /= d;
+    Fe* dst = (a & 1) ? bufB : bufA;
+    k_horner_lead<<<blocks_for(rest, 128), 128, 0, st>>>(src, dst, d, rest, Fp::to_mont(point_canon[a]));
+    TC_LAUNCHED(ctx);
+    src = dst;
+  }
+  TC_CUDA(ctx, cudaMemcpyAsync(h_y, src, sizeof(Fe), cudaMemcpyDeviceToHost, st));
+  TC_CUDA(ctx, cudaStreamSynchronize(st));
+  return TC_OK;
+}
+
+}  // namespace tcrt

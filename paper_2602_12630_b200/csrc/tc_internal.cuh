@@ -1,0 +1,116 @@
+// Host-side runtime shared by all kernels: per-device context bound to one CUDA stream,
+// grow-only stream-ordered scratch buffers, status codes and last-error text.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/tc_b200.h"
+#include "ec.cuh"
+
+struct tc_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  std::string err;
+  struct Buf {
+    void* p = nullptr;
+    size_t n = 0;
+  };
+  std::map<std::string, Buf> scratch;
+  uint32_t* d_flags = nullptr;   // device status word (quantize overflow / NaN ...)
+  uint32_t* h_flags = nullptr;   // pinned mirror
+  uint64_t launches = 0;         // kernels launched by this ctx (bench accounting)
+};
+
+struct tc_srs {
+  int device = 0;
+  int m = 0;
+  uint32_t shape[TC_MAX_AXES] = {0};
+  uint64_t n = 0;
+  tc::Aff* monomial = nullptr;   // N affine points, Montgomery form, lex order
+  tc::Aff* lagrange = nullptr;   // N affine points g^{L_i(tau)} (optional)
+  tc::Aff axis[TC_MAX_AXES];     // g^{tau_j} (host copy)
+};
+
+namespace tcrt {
+
+int fail(tc_ctx* ctx, int code, const char* fmt, ...);
+
+#define TC_CUDA(ctx, call)                                                                 \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return tcrt::fail((ctx), TC_ERR_CUDA, "%s failed: %s (%s:%d)", #call,                \
+                        cudaGetErrorString(e_), __FILE__, __LINE__);                       \
+  } while (0)
+
+#define TC_LAUNCHED(ctx)                                                                   \
+  do {                                                                                     \
+    (ctx)->launches++;                                                                     \
+    cudaError_t e_ = cudaGetLastError();                                                   \
+    if (e_ != cudaSuccess)                                                                 \
+      return tcrt::fail((ctx), TC_ERR_CUDA, "kernel launch failed: %s (%s:%d)",            \
+                        cudaGetErrorString(e_), __FILE__, __LINE__);                       \
+  } while (0)
+
+#define TC_TRY(call)          \
+  do {                        \
+    int s_ = (call);          \
+    if (s_ != TC_OK) return s_; \
+  } while (0)
+
+// grow-only scratch buffer named `name` of at least `bytes` (stream ordered)
+int scratch(tc_ctx* ctx, const char* name, size_t bytes, void** out);
+
+template <class T>
+int scratch_t(tc_ctx* ctx, const char* name, size_t count, T** out) {
+  void* p = nullptr;
+  int s = scratch(ctx, name, count * sizeof(T) + 16, &p);
+  *out = (T*)p;
+  return s;
+}
+
+inline unsigned blocks_for(uint64_t n, unsigned threads) {
+  uint64_t b = (n + threads - 1) / threads;
+  return (unsigned)(b ? b : 1);
+}
+
+// ---- MSM entry used by commit/open/terkle ----------------------------------------------
+enum ScalarKind { SCALAR_FP_CANON = 0, SCALAR_I64 = 1 };
+
+// result = sum_k scalars[k] * bases[k]; bases are device affine points.  out_aff on device
+// (one Aff) receives the canonical-Montgomery affine result.
+int msm_device(tc_ctx* ctx, ScalarKind kind, const void* d_scalars, const tc::Aff* d_bases,
+               uint64_t n, tc::Aff* d_out);
+
+// fixed-base batch: out[i] = e_i * g for canonical F_p exponents e (device arrays)
+int fixed_base_g(tc_ctx* ctx, const tc::Fe* d_exps, uint64_t n, tc::Aff* d_out);
+
+// quantize n values of dtype into canonical F_p limbs (device -> device)
+int quantize_device(tc_ctx* ctx, const void* d_in, int dtype, uint64_t n, int scale_bits,
+                    tc::Fe* d_out);
+// quantize into signed int64 (exact for fp16/bf16/fp32 at scale_bits <= 16)
+int quantize_i64_device(tc_ctx* ctx, const void* d_in, int dtype, uint64_t n, int scale_bits,
+                        int64_t* d_out);
+
+// e_i = prod_j tabs_j[i_j] for the lex index i (per-axis tables concatenated, canonical)
+int srs_exponents(tc_ctx* ctx, const std::vector<tc::Fe>& tabs_host, const uint32_t* shape,
+                  int m, uint64_t n, tc::Fe* d_exps);
+
+// per-axis Lagrange->monomial interpolation in place (canonical limbs in / out)
+int interpolate_device(tc_ctx* ctx, tc::Fe* d_vals, const uint32_t* shape, int m);
+
+// mvpoly.evaluate on device (per-axis Horner), y returned on the host
+int evaluate_device(tc_ctx* ctx, const tc::Fe* d_coeffs, const uint32_t* shape, int m,
+                    const tc::Fe* point_canon, tc::Fe* h_y);
+
+// open_quotients on device: coefficient array (canonical) -> m quotient arrays + y
+int open_quotients_device(tc_ctx* ctx, const tc::Fe* d_coeffs, const uint32_t* shape, int m,
+                          const tc::Fe* omega_canon, tc::Fe* d_quotients, tc::Fe* h_y);
+
+}  // namespace tcrt

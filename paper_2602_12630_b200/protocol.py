@@ -1,0 +1,77 @@
+"""Prover side of the protocol harness, hot-path subset:
+
+quantize       SPEC.md:536-544 — RNE(v * 2^16) into F_p on the device (K1)
+prover_commit  SPEC.md:546-554 — per-layer commitments + Terkle root over their leaves
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+from . import _conv, _lib
+from .authtree import TreeConfig, build, leaf_of
+from .commit import SCALE_BITS, tc_commit_many
+
+
+@dataclass
+class FieldTensor:
+    """Quantised tensor resident on the device: canonical limbs, shape (n, 6) int32."""
+    limbs: object
+    shape: tuple
+
+    def tolist(self):
+        return _conv.limbs_to_ints(self.limbs)
+
+    def __len__(self):
+        return int(self.limbs.shape[0])
+
+
+def quantize(tensor, scale_bits: int = SCALE_BITS) -> FieldTensor:
+    """Round-to-nearest-even fixed point: q = RNE(v * 2^scale_bits), negatives -> p - |q|.
+    ValueError on non-finite values or |v| * 2^scale_bits >= p/2."""
+    import numpy as np
+    import torch
+
+    if isinstance(tensor, np.ndarray):
+        tensor = torch.from_numpy(np.ascontiguousarray(tensor))
+    if not isinstance(tensor, torch.Tensor) or not tensor.is_floating_point():
+        tensor = torch.as_tensor(tensor, dtype=torch.float64)
+    ctx = _lib.Context.get(tensor.device if tensor.is_cuda else None)
+    dev = f"cuda:{ctx.device}"
+    t = tensor.detach().to(dev).contiguous()
+    n = t.numel()
+    out = _conv.empty_limbs(n, dev)
+    code = _conv._float_codes()[t.dtype]
+    with ctx.lock:
+        ctx.bind_stream()
+        ctx.check(_lib.lib().tc_quantize(ctx.handle, t.data_ptr(), code, n, scale_bits, out.data_ptr()), "quantize")
+    return FieldTensor(out, tuple(tensor.shape))
+
+
+def prover_commit(tensors, srs_pool, *, tree_config: TreeConfig = None, scale_bits: int = SCALE_BITS,
+                  route: str = "auto"):
+    """Per-layer commitments C_l = tc_commit(srs[shape_l], quantize(T_l)) and a Terkle tree
+    over leaves hash_to_scalar(encode_elem(C_l), b"terkle/leaf").
+
+    srs_pool: an Srs (all layers share it) or a mapping shape -> Srs.
+    Returns (commitments, root, tree)."""
+    tensors = list(tensors)
+    if not tensors:
+        raise ValueError("no tensors to commit")
+    groups = {}
+    for idx, T in enumerate(tensors):
+        srs = srs_pool if not isinstance(srs_pool, dict) else None
+        if srs is None:
+            key = tuple(T.shape) if hasattr(T, "shape") else None
+            srs = srs_pool.get(key)
+            if srs is None:
+                raise ValueError(f"no srs for tensor shape {key}")
+        groups.setdefault(id(srs), (srs, []))[1].append(idx)
+    commitments = [None] * len(tensors)
+    for srs, idxs in groups.values():
+        cs = tc_commit_many(srs, [tensors[i] for i in idxs], scale_bits=scale_bits, route=route)
+        for i, c in zip(idxs, cs):
+            commitments[i] = c
+    cfg = tree_config or TreeConfig()
+    tree, root = build(cfg, [leaf_of(c) for c in commitments])
+    return commitments, root, tree

@@ -1,0 +1,242 @@
+"""GPU parity: every device result equals the oracle / reference golden vectors bit for bit.
+All calls go through the C ABI (libtcb200.so) via the package."""
+import random
+
+import numpy as np
+import pytest
+
+from oracle import tc_oracle as O
+from tests.golden_io import elem, ints, load
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def T():
+    import paper_2602_12630_b200 as tcb
+    return tcb
+
+
+# ---------------------------------------------------------------- field core on device
+def test_device_field_ops():
+    from paper_2602_12630_b200 import _conv, _lib
+    rng = random.Random(11)
+    n = 4096
+    a = [rng.randrange(O.Q) for _ in range(n - 4)] + [0, 1, O.Q - 1, O.Q - 2]
+    b = [rng.randrange(O.Q) for _ in range(n - 4)] + [O.Q - 1, O.Q - 1, O.Q - 1, 1]
+    # raw (non-reduced mod p) limbs: build directly, _conv reduces mod p
+    def lim(vals):
+        buf = b"".join(v.to_bytes(24, "little") for v in vals)
+        return torch.from_numpy(np.frombuffer(buf, dtype=np.int32).copy()).cuda()
+    da, db = lim(a), lim(b)
+    out = torch.empty_like(da)
+    ctx = _lib.Context.get()
+    L = _lib.lib()
+    for op, fn in [(0, lambda x, y: x * y % O.Q), (2, lambda x, y: (x + y) % O.Q), (3, lambda x, y: (x - y) % O.Q)]:
+        ctx.check(L.tc_debug_field(ctx.handle, op, da.data_ptr(), db.data_ptr(), out.data_ptr(), n))
+        got = _conv.limbs_to_ints(out.view(-1, 6))
+        assert got == [fn(x, y) for x, y in zip(a, b)], op
+    ctx.check(L.tc_debug_field(ctx.handle, 4, da.data_ptr(), db.data_ptr(), out.data_ptr(), 64))
+    got = _conv.limbs_to_ints(out.view(-1, 6)[:64])
+    assert got == [pow(x, O.Q - 2, O.Q) for x in a[:64]]
+    ap = [x % O.P for x in a]
+    bp = [x % O.P for x in b]
+    dap, dbp = lim(ap), lim(bp)   # keep both alive: temporaries would share freed memory
+    ctx.check(L.tc_debug_field(ctx.handle, 1, dap.data_ptr(), dbp.data_ptr(), out.data_ptr(), n))
+    assert _conv.limbs_to_ints(out.view(-1, 6)) == [x * y % O.P for x, y in zip(ap, bp)]
+
+
+# ---------------------------------------------------------------- K1 quantize
+@pytest.mark.parametrize("dtype", ["float16", "bfloat16", "float32", "float64"])
+def test_quantize_matches_oracle(dtype):
+    tcb = T()
+    g = np.random.default_rng(1)
+    x = np.concatenate([g.standard_t(3, 20000) * 3.0, [0.0, -0.0, 1.5, -1.0, 2.0 ** -17, 3 * 2.0 ** -17,
+                                                     -(2.0 ** -17), 2.0 ** -24, 65504.0, -65504.0, 1e-8]])
+    t = torch.tensor(x, dtype=getattr(torch, dtype))
+    exact = t.to(torch.float64).numpy()
+    got = tcb.quantize(t.cuda()).tolist()
+    assert got == O.quantize(exact, 16)
+
+
+def test_quantize_spec_examples_and_errors():
+    tcb = T()
+    assert tcb.quantize(torch.tensor([0.0, 1.5, -1.0])).tolist() == [0, 98304, O.P - 65536]
+    with pytest.raises(ValueError):
+        tcb.quantize(torch.tensor([1.0, float("nan")]))
+    with pytest.raises(ValueError):
+        tcb.quantize(torch.tensor([float("inf")]))
+    with pytest.raises(ValueError):
+        tcb.quantize(torch.tensor([2.0 ** 150], dtype=torch.float64))
+    big = 2.0 ** 120   # fp32 max is ~2^128; |q| = 2^136 needs 5 limbs
+    assert tcb.quantize(torch.tensor([big, -big], dtype=torch.float32)).tolist() == O.quantize(np.array([big, -big]), 16)
+
+
+# ---------------------------------------------------------------- K2 / K4 polynomial engine
+@pytest.mark.parametrize("case", load("mvpoly.json"), ids=lambda c: "x".join(map(str, c["shape"])))
+def test_mvpoly_device_golden(case):
+    tcb = T()
+    shape = tuple(case["shape"])
+    dom = tcb.PrimeField()
+    f = tcb.interpolate_lagrange(dom, ints(case["values"]), tcb.default_grid(dom, shape))
+    assert list(f.coeffs) == ints(case["coeffs"])
+    pt = ints(case["point"])
+    assert tcb.evaluate(dom, f, pt) == int(case["eval"], 16)
+    qs, y = tcb.open_quotients(dom, f, pt)
+    assert y == int(case["y"], 16)
+    assert [list(q.coeffs) for q in qs] == [ints(q) for q in case["quotients"]]
+    qg, yg = tcb.open_quotients(dom, f, case["grid_point"])
+    assert yg == int(case["grid_y"], 16)
+    assert [list(q.coeffs) for q in qg] == [ints(q) for q in case["grid_quotients"]]
+
+
+@pytest.mark.parametrize("shape", [(4096,), (64, 64), (16, 16, 16), (8, 8, 8, 8), (4, 4, 4, 4, 4, 4), (128, 32)])
+def test_interpolation_config2_shapes(shape):
+    """Config-2 grid sweep: coefficients equal the golden digest (reference) / oracle."""
+    import hashlib
+    tcb = T()
+    x = np.random.default_rng(0).standard_normal(4096, dtype=np.float32)
+    if np.prod(shape) != 4096:
+        x = np.random.default_rng(9).standard_normal(int(np.prod(shape)), dtype=np.float32)
+    vals = O.quantize(x, 16)
+    dom = tcb.PrimeField()
+    f = tcb.interpolate_lagrange(dom, vals, tcb.default_grid(dom, shape))
+    gold = {tuple(c["shape"]): c for c in load("config2.json")}
+    if shape in gold:
+        dig = hashlib.sha256(b"".join(O.encode_scalar(c) for c in f.coeffs)).hexdigest()
+        assert dig == gold[shape]["coeff_digest"]
+    else:
+        assert list(f.coeffs) == O.interpolate_lagrange(vals, shape)
+    # round trip: the interpolant reproduces the samples at sampled grid points
+    rng = random.Random(4)
+    for _ in range(4):
+        idx = [rng.randrange(d) for d in shape]
+        assert tcb.evaluate(dom, f, [i + 1 for i in idx]) == vals[O.lex_index(idx, shape)]
+
+
+# ---------------------------------------------------------------- SRS / commit / open / verify
+@pytest.mark.parametrize("case", load("commit_small.json"), ids=lambda c: "x".join(map(str, c["shape"])) + "-" + c["kind"])
+def test_commit_open_small_golden(case):
+    tcb = T()
+    shape = tuple(case["shape"])
+    srs, td = tcb.setup_srs(shape, bytes.fromhex(case["entropy"]))
+    assert list(td.taus) == ints(case["taus"])
+    assert [O.encode_elem(e).hex() for e in srs.monomial_elems] == case["srs"]
+    assert [O.encode_elem(e).hex() for e in srs.axis_elems] == case["axis"]
+    vals = ints(case["values"])
+    for route in ("monomial", "lagrange"):
+        c = tcb.tc_commit(srs, vals, route=route)
+        assert O.encode_elem(c.elem).hex() == case["commitment"], route
+    pt = ints(case["point"])
+    op = tcb.tc_open(srs, vals, pt)
+    assert op.y == int(case["y"], 16)
+    assert [O.encode_elem(e).hex() for e in op.proofs] == case["proofs"]
+    assert tcb.tc_verify(srs, tcb.Commitment(elem(case["commitment"])), pt, op) is True
+    bad = tcb.TensorOpening((op.y + 1) % O.P, op.proofs)
+    assert tcb.tc_verify(srs, tcb.Commitment(elem(case["commitment"])), pt, bad) is False
+
+
+def test_lagrange_srs_matches_trapdoor():
+    tcb = T()
+    shape = (3, 4, 5)
+    srs, td = tcb.setup_srs(shape, b"lag")
+    exps = O.lagrange_exponents(shape, list(td.taus))
+    got = srs.lagrange_elems
+    for i in [0, 1, 7, 31, 59]:
+        assert got[i] == O.ec_mul(O.G, exps[i])
+
+
+def test_config1_commit_and_openings_golden():
+    """BASELINE config 1 end to end against the reference-composed golden file."""
+    tcb = T()
+    gold = load("config1.json")
+    x = np.random.default_rng(0).standard_normal(4096, dtype=np.float32)
+    shape = tuple(gold["shape"])
+    srs, td = tcb.setup_srs(shape, bytes.fromhex(gold["entropy"]))
+    assert [O.encode_elem(e).hex() for e in srs.monomial_elems[:8]] == gold["srs_head"]
+    t = torch.from_numpy(x).cuda()
+    for route in ("monomial", "lagrange"):
+        c = tcb.tc_commit(srs, t, route=route)
+        assert O.encode_elem(c.elem).hex() == gold["commitment"], route
+    for o in gold["openings"]:
+        pt = ints(o["point"])
+        op = tcb.tc_open(srs, t, pt)
+        assert op.y == int(o["y"], 16)
+        assert [O.encode_elem(e).hex() for e in op.proofs] == o["proofs"]
+        assert tcb.tc_verify(srs, c, pt, op)
+
+
+def test_config2_commitments_golden():
+    tcb = T()
+    x = np.random.default_rng(0).standard_normal(4096, dtype=np.float32)
+    t = torch.from_numpy(x).cuda()
+    for g in load("config2.json"):
+        shape = tuple(g["shape"])
+        srs, _ = tcb.setup_srs(shape, bytes.fromhex(g["entropy"]))
+        for route in ("monomial", "lagrange"):
+            c = tcb.tc_commit(srs, t, route=route)
+            assert O.encode_elem(c.elem).hex() == g["commitment"], (shape, route)
+
+
+@pytest.mark.parametrize("shape", [(32, 32, 32, 64)])
+def test_full_size_layer_trapdoor_oracle(shape):
+    """A full config-3 layer (2^21 elements, fp16 Student-t): commitment and one opening
+    equal the trapdoor oracle g^{f(tau)} (barycentric evaluation, mvpoly.py:340-371)."""
+    tcb = T()
+    g = np.random.default_rng(3)
+    x = (g.standard_t(3, size=int(np.prod(shape))) * 2.5).astype(np.float16)
+    srs, td = tcb.setup_srs(shape, b"full-layer")
+    t = torch.from_numpy(x).cuda()
+    vals = O.quantize(x.astype(np.float64), 16)
+    want = O.commit_trapdoor(vals, shape, list(td.taus))
+    for route in ("lagrange", "monomial"):
+        c = tcb.tc_commit(srs, t, route=route)
+        assert c.elem == want, route
+
+
+# ---------------------------------------------------------------- Terkle
+def test_terkle_build_prove_verify_vs_oracle():
+    tcb = T()
+    cfg = tcb.TreeConfig(shape=(2, 2, 2))
+    rng = random.Random(8)
+    leaves = [rng.randrange(O.P) for _ in range(32)]
+    srs = tcb.authtree.node_srs(cfg)
+    tree, root = tcb.build(cfg, leaves, srs=srs)
+    node_elems = list(srs.monomial_elems)
+    levels, _ = O.terkle_build(leaves, (2, 2, 2), lambda z: O.tc_commit(node_elems, z, (2, 2, 2)))
+    assert [[O.encode_elem(c) for c in lv] for lv in tree.levels] == [[O.encode_elem(c) for c in lv] for lv in levels]
+    for i in (0, 13, 31):
+        pf = tcb.prove(tree, i)
+        assert len(pf.openings) == 2 and all(len(o.proofs) == 3 for o in pf.openings)
+        assert tcb.verify(root, i, leaves[i], pf, cfg, srs=srs)
+        assert not tcb.verify(root, i, (leaves[i] + 1) % O.P, pf, cfg, srs=srs)
+        assert not tcb.verify(root, (i + 1) % 32, leaves[i], pf, cfg, srs=srs)
+
+
+def test_prover_commit_small_layers():
+    tcb = T()
+    shape = (8, 8, 8)
+    srs, td = tcb.setup_srs(shape, b"layers")
+    g = np.random.default_rng(5)
+    tensors = [torch.from_numpy((g.standard_t(3, 512) * s).astype(np.float16)).cuda() for s in (0.5, 1.0, 4.0)]
+    comms, root, tree = tcb.prover_commit(tensors, srs)
+    for t, c in zip(tensors, comms):
+        vals = O.quantize(t.cpu().numpy().astype(np.float64), 16)
+        assert c.elem == O.commit_trapdoor(vals, shape, list(td.taus))
+    leaves = [O.leaf_of_commitment(c.elem) for c in comms]
+    tree2, root2 = tcb.build(tcb.TreeConfig(), leaves)
+    assert root2 == root
+    # determinism and sensitivity
+    comms_b, root_b, _ = tcb.prover_commit(tensors, srs)
+    assert root_b == root
+    t2 = tensors[1].clone()
+    t2[17] += 1.0
+    _, root_c, _ = tcb.prover_commit([tensors[0], t2, tensors[2]], srs)
+    assert root_c != root
