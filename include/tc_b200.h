@@ -80,6 +80,11 @@ int tc_ctx_set_stream(tc_ctx* ctx, void* cuda_stream);
 int tc_ctx_synchronize(tc_ctx* ctx);
 const char* tc_ctx_last_error(const tc_ctx* ctx);
 uint64_t tc_ctx_launch_count(const tc_ctx* ctx);
+/* per-kernel CUDA-event timing on the ctx stream (bench roofline); clears the stats.
+ * "msm.accumulate": Pippenger bucket accumulation, units = bucket entries (mixed adds). */
+int tc_ctx_set_profiling(tc_ctx* ctx, int on);
+int tc_ctx_kernel_stats(const tc_ctx* ctx, const char* name, double* ms, uint64_t* launches,
+                        double* units);
 
 /* ---- setup_srs (Srs SPEC.md:44-50) ----------------------------------
  * Monomial elements g^{prod_j tau_j^{i_j}} in lex order (mvpoly.py:3-5) and, with
@@ -90,8 +95,10 @@ int tc_srs_generate(tc_ctx* ctx, const uint32_t* shape, int m, const uint8_t* ta
 /* SRS from public points (TCSR payload): monomial43 N x 43 B, axis43 m x 43 B */
 int tc_srs_load(tc_ctx* ctx, const uint32_t* shape, int m, const uint8_t* monomial43,
                 const uint8_t* axis43, tc_srs** out);
-/* export N x 43 B (which = TC_SRS_MONOMIAL | TC_SRS_LAGRANGE) or the m axis elements */
-int tc_srs_export(tc_ctx* ctx, const tc_srs* srs, int which, uint8_t* out43);
+/* export elements [offset, offset+count) as count x 43 B (which = TC_SRS_MONOMIAL |
+ * TC_SRS_LAGRANGE), or the m axis elements */
+int tc_srs_export(tc_ctx* ctx, const tc_srs* srs, int which, uint64_t offset, uint64_t count,
+                  uint8_t* out43);
 int tc_srs_export_axis(const tc_srs* srs, uint8_t* out43);
 int tc_srs_has(const tc_srs* srs, int which);
 uint64_t tc_srs_size(const tc_srs* srs);
@@ -155,6 +162,8 @@ int tc_host_hash_to_scalar(const uint8_t* data, uint32_t n, const uint8_t* tag, 
 int tc_host_fq_mul(const uint32_t* a, const uint32_t* b, uint32_t* out);   /* canonical */
 int tc_host_fp_mul(const uint32_t* a, const uint32_t* b, uint32_t* out);   /* canonical */
 int tc_host_g_mul(const uint8_t* k_le21, uint8_t* out43);                  /* k * g */
+/* measured mad.lo.u32 throughput of the device at current clocks, in 10^12 ops/s */
+int tc_measure_imad_peak(tc_ctx* ctx, double* tops);
 /* device field-op check: op 0 = Fq mul, 1 = Fp mul, 2 = Fq add, 3 = Fq sub, 4 = Fq inv */
 int tc_debug_field(tc_ctx* ctx, int op, const uint32_t* d_a, const uint32_t* d_b,
                    uint32_t* d_out, uint64_t n);

@@ -50,9 +50,12 @@ _SIGS = [
     ("tc_ctx_synchronize", C.c_int, [_P]),
     ("tc_ctx_last_error", C.c_char_p, [_P]),
     ("tc_ctx_launch_count", C.c_uint64, [_P]),
+    ("tc_ctx_set_profiling", C.c_int, [_P, C.c_int]),
+    ("tc_ctx_kernel_stats", C.c_int, [_P, C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64),
+                                      C.POINTER(C.c_double)]),
     ("tc_srs_generate", C.c_int, [_P, _U32P, C.c_int, C.c_char_p, C.c_int, C.POINTER(_P)]),
     ("tc_srs_load", C.c_int, [_P, _U32P, C.c_int, C.c_char_p, C.c_char_p, C.POINTER(_P)]),
-    ("tc_srs_export", C.c_int, [_P, _P, C.c_int, _P]),
+    ("tc_srs_export", C.c_int, [_P, _P, C.c_int, C.c_uint64, C.c_uint64, _P]),
     ("tc_srs_export_axis", C.c_int, [_P, _P]),
     ("tc_srs_has", C.c_int, [_P, C.c_int]),
     ("tc_srs_size", C.c_uint64, [_P]),
@@ -73,6 +76,7 @@ _SIGS = [
     ("tc_host_fp_mul", C.c_int, [_U32P, _U32P, _U32P]),
     ("tc_host_g_mul", C.c_int, [C.c_char_p, _P]),
     ("tc_debug_field", C.c_int, [_P, C.c_int, _P, _P, _P, C.c_uint64]),
+    ("tc_measure_imad_peak", C.c_int, [_P, C.POINTER(C.c_double)]),
 ]
 
 EXPORTED = [s[0] for s in _SIGS]
@@ -156,3 +160,11 @@ class Context:
     @property
     def launches(self) -> int:
         return int(lib().tc_ctx_launch_count(self.handle))
+
+    def set_profiling(self, on: bool):
+        self.check(lib().tc_ctx_set_profiling(self.handle, 1 if on else 0), "set_profiling")
+
+    def kernel_stats(self, name: str):
+        ms, n, units = C.c_double(), C.c_uint64(), C.c_double()
+        self.check(lib().tc_ctx_kernel_stats(self.handle, name.encode(), C.byref(ms), C.byref(n), C.byref(units)))
+        return {"ms": ms.value, "launches": int(n.value), "units": units.value}

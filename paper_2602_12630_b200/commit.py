@@ -91,15 +91,18 @@ class Srs:
     def has(self, which: int) -> bool:
         return bool(_lib.lib().tc_srs_has(self._h, which))
 
+    def export_range(self, which: int, start: int, count: int):
+        """Elements [start, start+count) of the monomial / Lagrange SRS as points."""
+        ctx = _lib.Context.get(self.device)
+        buf = C.create_string_buffer(max(1, count) * ELEM_BYTES)
+        with ctx.lock:
+            ctx.bind_stream()
+            ctx.check(_lib.lib().tc_srs_export(ctx.handle, self._h, which, start, count, buf), "tc_srs_export")
+        return decode_elems(buf.raw, count)
+
     def _export(self, which):
         if which not in self._cache:
-            ctx = _lib.Context.get(self.device)
-            n = self.size
-            buf = C.create_string_buffer(n * ELEM_BYTES)
-            with ctx.lock:
-                ctx.bind_stream()
-                ctx.check(_lib.lib().tc_srs_export(ctx.handle, self._h, which, buf), "tc_srs_export")
-            self._cache[which] = decode_elems(buf.raw, n)
+            self._cache[which] = self.export_range(which, 0, self.size)
         return self._cache[which]
 
     @property

@@ -163,6 +163,22 @@ __global__ void k_field_op(int op, const Fe* a, const Fe* b, Fe* out, uint64_t n
   out[i] = r;
 }
 
+// 16 independent dependent-chains of mad.lo.u32 per thread: saturates the IMAD pipe
+__global__ void k_imad_peak(uint32_t* sink, uint32_t seed, int iters) {
+  uint32_t a[16];
+  const uint32_t b = seed ^ (threadIdx.x * 2654435761u);
+#pragma unroll
+  for (int i = 0; i < 16; i++) a[i] = seed * (i + 3) + threadIdx.x;
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int i = 0; i < 16; i++) asm volatile("mad.lo.u32 %0, %0, %1, %0;" : "+r"(a[i]) : "r"(b));
+  }
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; i++) s ^= a[i];
+  if (s == 0x7f4a7c15u) sink[0] = s;
+}
+
 // read one device Aff result and encode it on the host
 int fetch_encode(tc_ctx* ctx, const Aff* d_pt, uint8_t* out43) {
   Aff h;
@@ -399,6 +415,30 @@ int tc_ctx_synchronize(tc_ctx* ctx) {
 const char* tc_ctx_last_error(const tc_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 uint64_t tc_ctx_launch_count(const tc_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int tc_ctx_set_profiling(tc_ctx* ctx, int on) {
+  if (!ctx) return TC_ERR_ARGUMENT;
+  if (on && !ctx->ev[0]) {
+    TC_CUDA(ctx, cudaEventCreate(&ctx->ev[0]));
+    TC_CUDA(ctx, cudaEventCreate(&ctx->ev[1]));
+  }
+  ctx->prof = on != 0;
+  ctx->stats.clear();
+  return TC_OK;
+}
+
+int tc_ctx_kernel_stats(const tc_ctx* ctx, const char* name, double* ms, uint64_t* launches, double* units) {
+  if (!ctx || !name || !ms || !launches || !units) return TC_ERR_ARGUMENT;
+  auto it = ctx->stats.find(name);
+  if (it == ctx->stats.end()) {
+    *ms = 0, *launches = 0, *units = 0;
+    return TC_OK;
+  }
+  *ms = it->second.ms;
+  *launches = it->second.launches;
+  *units = it->second.units;
+  return TC_OK;
+}
+
 // ---- SRS ----
 int tc_srs_generate(tc_ctx* ctx, const uint32_t* shape, int m, const uint8_t* taus_le21, int flags, tc_srs** out) {
   if (!ctx || !shape || !taus_le21 || !out) return TC_ERR_ARGUMENT;
@@ -472,15 +512,17 @@ int tc_srs_load(tc_ctx* ctx, const uint32_t* shape, int m, const uint8_t* monomi
   return TC_OK;
 }
 
-int tc_srs_export(tc_ctx* ctx, const tc_srs* srs, int which, uint8_t* out43) {
+int tc_srs_export(tc_ctx* ctx, const tc_srs* srs, int which, uint64_t offset, uint64_t count, uint8_t* out43) {
   if (!ctx || !srs || !out43) return TC_ERR_ARGUMENT;
   const Aff* pts = (which == TC_SRS_LAGRANGE) ? srs->lagrange : srs->monomial;
   if (!pts) return fail(ctx, TC_ERR_VALUE, "srs has no elements of kind %d", which);
+  if (offset > srs->n || count > srs->n - offset) return fail(ctx, TC_ERR_INDEX, "srs export range out of bounds");
+  if (count == 0) return TC_OK;
   uint8_t* d_raw;
-  TC_TRY(tcrt::scratch_t(ctx, "srs.raw", srs->n * 43, &d_raw));
-  k_encode43<<<tcrt::blocks_for(srs->n, 128), 128, 0, ctx->stream>>>(pts, srs->n, d_raw);
+  TC_TRY(tcrt::scratch_t(ctx, "srs.raw", count * 43, &d_raw));
+  k_encode43<<<tcrt::blocks_for(count, 128), 128, 0, ctx->stream>>>(pts + offset, count, d_raw);
   TC_LAUNCHED(ctx);
-  TC_CUDA(ctx, cudaMemcpyAsync(out43, d_raw, srs->n * 43, cudaMemcpyDeviceToHost, ctx->stream));
+  TC_CUDA(ctx, cudaMemcpyAsync(out43, d_raw, count * 43, cudaMemcpyDeviceToHost, ctx->stream));
   TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return TC_OK;
 }
@@ -732,6 +774,33 @@ int tc_host_g_mul(const uint8_t* k_le21, uint8_t* out43) {
 }
 int tc_host_hash_to_scalar(const uint8_t* data, uint32_t n, const uint8_t* tag, uint32_t tn, uint8_t* out21) {
   fe_to_le21(hash_to_scalar(data, n, tag, tn), out21);
+  return TC_OK;
+}
+
+// integer-multiply pipe peak (IMAD, mad.lo.u32) at the current clocks: the roofline
+// denominator for the integer-bound kernels (MEASURED_PEAKS.json carries none)
+int tc_measure_imad_peak(tc_ctx* ctx, double* tops) {
+  if (!ctx || !tops) return TC_ERR_ARGUMENT;
+  uint32_t* d_sink;
+  TC_TRY(tcrt::scratch_t(ctx, "imad.sink", 4, &d_sink));
+  cudaEvent_t e0, e1;
+  TC_CUDA(ctx, cudaEventCreate(&e0));
+  TC_CUDA(ctx, cudaEventCreate(&e1));
+  const int iters = 8192, threads = 512, blocks = ctx->num_sms * 4;
+  double best = 0;
+  for (int rep = 0; rep < 4; rep++) {
+    TC_CUDA(ctx, cudaEventRecord(e0, ctx->stream));
+    k_imad_peak<<<blocks, threads, 0, ctx->stream>>>(d_sink, 0x9e3779b9u + rep, iters);
+    TC_CUDA(ctx, cudaEventRecord(e1, ctx->stream));
+    TC_CUDA(ctx, cudaEventSynchronize(e1));
+    float ms = 0;
+    TC_CUDA(ctx, cudaEventElapsedTime(&ms, e0, e1));
+    double ops = (double)blocks * threads * iters * 16;
+    best = std::max(best, ops / (ms * 1e-3) / 1e12);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *tops = best;
   return TC_OK;
 }
 

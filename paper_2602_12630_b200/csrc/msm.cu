@@ -399,8 +399,21 @@ int msm_device(tc_ctx* ctx, ScalarKind kind, const void* d_scalars, const Aff* d
   TC_LAUNCHED(ctx);
   TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(d_scan, scan_bytes, np, offA, (int)(nb + 1), st));
   ctx->launches += 2;
+  if (ctx->prof) TC_CUDA(ctx, cudaEventRecord(ctx->ev[0], st));
   k_accum_aff<<<blocks_for(max_items, 128), 128, 0, st>>>(svals, d_bases, bstart, bend, offA, nb, T, itemsA);
   TC_LAUNCHED(ctx);
+  if (ctx->prof) {
+    // one extra sync per MSM while profiling: read the kernel time and its entry count
+    TC_CUDA(ctx, cudaEventRecord(ctx->ev[1], st));
+    TC_CUDA(ctx, cudaMemcpyAsync(ctx->h_flags + 4, d_nnz, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    TC_CUDA(ctx, cudaEventSynchronize(ctx->ev[1]));
+    float ms = 0;
+    TC_CUDA(ctx, cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]));
+    auto& s = ctx->stats["msm.accumulate"];
+    s.ms += ms;
+    s.launches += 1;
+    s.units += (double)ctx->h_flags[4];
+  }
   uint64_t items_bound = max_items;
   for (int l = 1; l < levels; l++) {
     k_piece_count_off<<<blocks_for(nb + 1, 256), 256, 0, st>>>(offA, nb, T, np);

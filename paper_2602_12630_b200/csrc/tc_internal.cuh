@@ -25,6 +25,15 @@ struct tc_ctx {
   uint32_t* d_flags = nullptr;   // device status word (quantize overflow / NaN ...)
   uint32_t* h_flags = nullptr;   // pinned mirror
   uint64_t launches = 0;         // kernels launched by this ctx (bench accounting)
+  // optional per-kernel timing (CUDA events on the ctx stream) for the roofline report
+  bool prof = false;
+  struct Stat {
+    double ms = 0;
+    uint64_t launches = 0;
+    double units = 0;   // kernel-specific work units (e.g. bucket entries accumulated)
+  };
+  std::map<std::string, Stat> stats;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
 };
 
 struct tc_srs {
