@@ -380,7 +380,9 @@ int tc_ctx_create(int device, void* cuda_stream, tc_ctx** out) {
   ctx->stream = (cudaStream_t)cuda_stream;
   cudaDeviceProp prop;
   if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) ctx->num_sms = prop.multiProcessorCount;
-  if (cudaMalloc(&ctx->d_flags, 64) != cudaSuccess || cudaMallocHost(&ctx->h_flags, 64) != cudaSuccess) {
+  ctx->h_stage_bytes = 1 << 20;
+  if (cudaMalloc(&ctx->d_flags, 64) != cudaSuccess || cudaMallocHost(&ctx->h_flags, 64) != cudaSuccess ||
+      cudaMallocHost(&ctx->h_stage, ctx->h_stage_bytes) != cudaSuccess) {
     delete ctx;
     return TC_ERR_CUDA;
   }
@@ -397,6 +399,8 @@ int tc_ctx_destroy(tc_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   cudaFree(ctx->d_flags);
   cudaFreeHost(ctx->h_flags);
+  cudaFreeHost(ctx->h_stage);
+  if (ctx->ev[0]) cudaEventDestroy(ctx->ev[0]), cudaEventDestroy(ctx->ev[1]);
   delete ctx;
   return TC_OK;
 }
@@ -600,36 +604,63 @@ int tc_msm(tc_ctx* ctx, const tc_srs* srs, int which, const uint32_t* d_scalars,
   return fetch_encode(ctx, d_out, out43);
 }
 
-static int commit_one(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int scale_bits, int route,
-                      uint8_t* out43) {
+// copy L device results to the host (pinned staging) and encode them
+static int fetch_encode_many(tc_ctx* ctx, const Aff* d_pts, int L, uint8_t* out43) {
+  for (int base = 0; base < L;) {
+    int k = std::min<int>(L - base, (int)(ctx->h_stage_bytes / sizeof(Aff)));
+    TC_CUDA(ctx, cudaMemcpyAsync(ctx->h_stage, d_pts + base, k * sizeof(Aff), cudaMemcpyDeviceToHost, ctx->stream));
+    TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    const Aff* h = (const Aff*)ctx->h_stage;
+    for (int i = 0; i < k; i++) aff_encode43(h[i], out43 + 43 * (base + i));
+    base += k;
+  }
+  return TC_OK;
+}
+
+// count tensors of the SRS shape in one batched MSM pipeline
+static int commit_many(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype, int scale_bits,
+                       int route, uint8_t* out43) {
   const uint64_t n = srs->n;
   bool lag = (route == TC_ROUTE_LAGRANGE) || (route == TC_ROUTE_AUTO && srs->lagrange);
   if (lag && !srs->lagrange) return fail(ctx, TC_ERR_VALUE, "srs has no Lagrange elements");
   if (!lag && !srs->monomial) return fail(ctx, TC_ERR_VALUE, "srs has no monomial elements");
-  Fe* vals;
-  TC_TRY(load_field_tensor(ctx, d_in, dtype, n, scale_bits, &vals, "commit.vals"));
+  if (count == 0) return TC_OK;
   Aff* d_out;
-  TC_TRY(tcrt::scratch_t(ctx, "commit.out", 1, &d_out));
+  TC_TRY(tcrt::scratch_t(ctx, "commit.out", (uint64_t)count, &d_out));
   if (lag) {
-    // C_T = sum_grid T[w] * g^{L_w(tau)}: no interpolation, scalars are the raw grid values
-    TC_TRY(tcrt::msm_device(ctx, tcrt::SCALAR_FP_CANON, vals, srs->lagrange, n, d_out));
+    // C_T = sum_grid T[w] * g^{L_w(tau)}: no interpolation; the raw grid values (quantised
+    // inside the digit kernel for float inputs) are the scalars
+    TC_TRY(tcrt::msm_batch_device(ctx, dtype, scale_bits, d_ins, count, srs->lagrange, n, d_out));
   } else {
-    TC_TRY(tcrt::interpolate_device(ctx, vals, srs->shape, srs->m));
-    TC_TRY(tcrt::msm_device(ctx, tcrt::SCALAR_FP_CANON, vals, srs->monomial, n, d_out));
+    // SPEC.md:279 verbatim: interpolate every tensor, then MSM over the monomial SRS
+    Fe* coeffs;
+    TC_TRY(tcrt::scratch_t(ctx, "commit.coeffs", (uint64_t)count * n, &coeffs));
+    std::vector<const void*> ptrs(count);
+    for (int i = 0; i < count; i++) {
+      Fe* dst = coeffs + (uint64_t)i * n;
+      if (dtype == TC_DTYPE_FP_LIMBS) {
+        TC_CUDA(ctx, cudaMemcpyAsync(dst, d_ins[i], n * sizeof(Fe), cudaMemcpyDeviceToDevice, ctx->stream));
+      } else {
+        TC_TRY(tcrt::quantize_device(ctx, d_ins[i], dtype, n, scale_bits, dst));
+      }
+      TC_TRY(tcrt::interpolate_device(ctx, dst, srs->shape, srs->m));
+      ptrs[i] = dst;
+    }
+    TC_TRY(tcrt::msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, ptrs.data(), count, srs->monomial, n, d_out));
   }
-  return fetch_encode(ctx, d_out, out43);
+  return fetch_encode_many(ctx, d_out, count, out43);
 }
 
 int tc_commit(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int scale_bits, int route, uint8_t* out43) {
   if (!ctx || !srs || !d_in || !out43) return TC_ERR_ARGUMENT;
-  return commit_one(ctx, srs, d_in, dtype, scale_bits, route, out43);
+  const void* ptrs[1] = {d_in};
+  return commit_many(ctx, srs, ptrs, 1, dtype, scale_bits, route, out43);
 }
 
 int tc_commit_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype, int scale_bits,
                     int route, uint8_t* out43) {
   if (!ctx || !srs || !d_ins || !out43 || count < 0) return TC_ERR_ARGUMENT;
-  for (int i = 0; i < count; i++) TC_TRY(commit_one(ctx, srs, d_ins[i], dtype, scale_bits, route, out43 + 43 * i));
-  return TC_OK;
+  return commit_many(ctx, srs, d_ins, count, dtype, scale_bits, route, out43);
 }
 
 int tc_open(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int scale_bits, const uint8_t* omega_le21,
@@ -650,15 +681,14 @@ int tc_open(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int sca
   Fe y;
   TC_TRY(tcrt::open_quotients_device(ctx, vals, srs->shape, m, om.data(), qs, &y));
   fe_to_le21(y, out_y21);
+  // the m quotient MSMs in one batch (quotient a is zero outside its lex-prefix support,
+  // and zero scalars emit no bucket entries)
   Aff* d_out;
-  TC_TRY(tcrt::scratch_t(ctx, "open.out", 1, &d_out));
-  uint64_t span = n;   // quotient a is supported on the lex prefix of length prod_{t>=a} d_t
-  for (int a = 0; a < m; a++) {
-    TC_TRY(tcrt::msm_device(ctx, tcrt::SCALAR_FP_CANON, qs + (uint64_t)a * n, srs->monomial, span, d_out));
-    TC_TRY(fetch_encode(ctx, d_out, out_pi43 + 43 * a));
-    span /= srs->shape[a];
-  }
-  return TC_OK;
+  TC_TRY(tcrt::scratch_t(ctx, "open.out", (uint64_t)m, &d_out));
+  std::vector<const void*> ptrs(m);
+  for (int a = 0; a < m; a++) ptrs[a] = qs + (uint64_t)a * n;
+  TC_TRY(tcrt::msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, ptrs.data(), m, srs->monomial, n, d_out));
+  return fetch_encode_many(ctx, d_out, m, out_pi43);
 }
 
 // ---- Terkle ----
@@ -684,24 +714,28 @@ int tc_terkle_build(tc_ctx* ctx, const tc_srs* node_srs, const uint8_t* leaves_l
   Fe* d_vals;
   Aff* d_out;
   TC_TRY(tcrt::scratch_t(ctx, "terkle.vals", cap, &d_vals));
-  TC_TRY(tcrt::scratch_t(ctx, "terkle.out", 1, &d_out));
+  TC_TRY(tcrt::scratch_t(ctx, "terkle.out", cap / B, &d_out));
   const Aff* bases = node_srs->lagrange ? node_srs->lagrange : node_srs->monomial;
   bool lag = node_srs->lagrange != nullptr;
   uint64_t written = 0;
   const uint8_t tag[] = {'t', 'e', 'r', 'k', 'l', 'e', '/', 'n', 'o', 'd', 'e'};
   for (uint64_t l = 0; l < L; l++) {
-    uint64_t nodes = vals.size() / B;
-    TC_CUDA(ctx, cudaMemcpyAsync(d_vals, vals.data(), vals.size() * sizeof(Fe), cudaMemcpyHostToDevice, ctx->stream));
-    std::vector<Fe> next(nodes);
+    const uint64_t nodes = vals.size() / B;
+    // pageable source: the synchronous copy completes before `vals` is reused
+    TC_CUDA(ctx, cudaMemcpy(d_vals, vals.data(), vals.size() * sizeof(Fe), cudaMemcpyHostToDevice));
+    std::vector<const void*> ptrs(nodes);
     for (uint64_t u = 0; u < nodes; u++) {
       Fe* z = d_vals + u * B;
       if (!lag) TC_TRY(tcrt::interpolate_device(ctx, z, node_srs->shape, node_srs->m));
-      TC_TRY(tcrt::msm_device(ctx, tcrt::SCALAR_FP_CANON, z, bases, B, d_out));
-      uint8_t* enc = out_nodes43 + 43 * written;
-      TC_TRY(fetch_encode(ctx, d_out, enc));
-      next[u] = hash_to_scalar(enc, 43, tag, sizeof tag);
-      written++;
+      ptrs[u] = z;
     }
+    // every node of the level in one batched MSM
+    TC_TRY(tcrt::msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, ptrs.data(), (int)nodes, bases, B, d_out));
+    uint8_t* enc = out_nodes43 + 43 * written;
+    TC_TRY(fetch_encode_many(ctx, d_out, (int)nodes, enc));
+    std::vector<Fe> next(nodes);
+    for (uint64_t u = 0; u < nodes; u++) next[u] = hash_to_scalar(enc + 43 * u, 43, tag, sizeof tag);
+    written += nodes;
     vals.swap(next);
   }
   *inout_count = written;

@@ -24,6 +24,8 @@ struct tc_ctx {
   std::map<std::string, Buf> scratch;
   uint32_t* d_flags = nullptr;   // device status word (quantize overflow / NaN ...)
   uint32_t* h_flags = nullptr;   // pinned mirror
+  void* h_stage = nullptr;       // pinned staging for small host<->device transfers
+  size_t h_stage_bytes = 0;
   uint64_t launches = 0;         // kernels launched by this ctx (bench accounting)
   // optional per-kernel timing (CUDA events on the ctx stream) for the roofline report
   bool prof = false;
@@ -97,15 +99,18 @@ enum ScalarKind { SCALAR_FP_CANON = 0, SCALAR_I64 = 1 };
 int msm_device(tc_ctx* ctx, ScalarKind kind, const void* d_scalars, const tc::Aff* d_bases,
                uint64_t n, tc::Aff* d_out);
 
+// L MSMs over the same n bases in one pipeline: d_out[l] = sum_k s_l[k] * bases[k].
+// h_ptrs: L device pointers (host array) to n scalars of `dtype` (TC_DTYPE_FP_LIMBS =
+// canonical limbs; float dtypes are quantised at scale_bits inside the digit kernel).
+int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* h_ptrs, int L,
+                     const tc::Aff* d_bases, uint64_t n, tc::Aff* d_out);
+
 // fixed-base batch: out[i] = e_i * g for canonical F_p exponents e (device arrays)
 int fixed_base_g(tc_ctx* ctx, const tc::Fe* d_exps, uint64_t n, tc::Aff* d_out);
 
 // quantize n values of dtype into canonical F_p limbs (device -> device)
 int quantize_device(tc_ctx* ctx, const void* d_in, int dtype, uint64_t n, int scale_bits,
                     tc::Fe* d_out);
-// quantize into signed int64 (exact for fp16/bf16/fp32 at scale_bits <= 16)
-int quantize_i64_device(tc_ctx* ctx, const void* d_in, int dtype, uint64_t n, int scale_bits,
-                        int64_t* d_out);
 
 // e_i = prod_j tabs_j[i_j] for the lex index i (per-axis tables concatenated, canonical)
 int srs_exponents(tc_ctx* ctx, const std::vector<tc::Fe>& tabs_host, const uint32_t* shape,
