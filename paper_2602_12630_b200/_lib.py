@@ -11,7 +11,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtcb200.so")
+LIB_PATH = os.environ.get("TC_LIB", os.path.join(HERE, "libtcb200.so"))   # TC_LIB: A/B builds
 
 TC_OK = 0
 TC_ERR_VALUE, TC_ERR_INDEX, TC_ERR_ZERO_DIVISION, TC_ERR_BACKEND, TC_ERR_OVERFLOW = 1, 2, 3, 4, 5

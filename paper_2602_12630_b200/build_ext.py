@@ -7,7 +7,6 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libtcb200.so")
-BUILD = os.path.join(HERE, "_build")
 SOURCES = ["capi.cu", "msm.cu", "srs.cu", "quantize.cu", "interp.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -15,17 +14,17 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-I" + os.path.join(os.path.dirname(HERE), "include")]
 
 
-def _compile(src):
-    obj = os.path.join(BUILD, src.replace(".cu", ".o"))
-    cmd = [NVCC] + FLAGS + ["-c", os.path.join(CSRC, src), "-o", obj]
+def _compile(src, build_dir, extra):
+    obj = os.path.join(build_dir, src.replace(".cu", ".o"))
+    cmd = [NVCC] + FLAGS + list(extra) + ["-c", os.path.join(CSRC, src), "-o", obj]
     subprocess.run(cmd, check=True)
     return obj
 
 
-def _stale():
-    if not os.path.exists(OUT):
+def _stale(out):
+    if not os.path.exists(out):
         return True
-    t = os.path.getmtime(OUT)
+    t = os.path.getmtime(out)
     for root in (CSRC, os.path.join(os.path.dirname(HERE), "include")):
         for f in os.listdir(root):
             if os.path.getmtime(os.path.join(root, f)) > t:
@@ -33,19 +32,30 @@ def _stale():
     return os.path.getmtime(__file__) > t
 
 
-def build(force=False, verbose=True):
-    if not force and not _stale():
-        return OUT
-    os.makedirs(BUILD, exist_ok=True)
+def build(force=False, verbose=True, out=OUT, extra=()):
+    """Compile every CUDA source for sm_100a and link the shared library `out`.
+    `extra`: additional nvcc flags (e.g. -DTC_MULV=0 for A/B variants)."""
+    if not force and not _stale(out):
+        return out
+    build_dir = os.path.join(HERE, "_build", os.path.basename(out).replace(".so", ""))
+    os.makedirs(build_dir, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(_compile, SOURCES))
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", OUT + ".tmp"] + objs
+        objs = list(ex.map(lambda s: _compile(s, build_dir, extra), SOURCES))
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out + ".tmp"] + objs
     subprocess.run(cmd, check=True)
-    os.replace(OUT + ".tmp", OUT)
+    os.replace(out + ".tmp", out)
     if verbose:
-        print("built", OUT, file=sys.stderr)
-    return OUT
+        print("built", out, file=sys.stderr)
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv)
+    args = [a for a in sys.argv[1:] if a != "--force"]
+    out = OUT
+    extra = []
+    for a in args:
+        if a.startswith("--out="):
+            out = os.path.abspath(a[6:])
+        else:
+            extra.append(a)
+    build(force="--force" in sys.argv or bool(extra), out=out, extra=extra)

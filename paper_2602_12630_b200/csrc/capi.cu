@@ -158,6 +158,8 @@ __global__ void k_field_op(int op, const Fe* a, const Fe* b, Fe* out, uint64_t n
     case 1: r = Fp::from_mont(Fp::mul(Fp::to_mont(a[i]), Fp::to_mont(b[i]))); break;
     case 2: r = Fq::canon(Fq::add(a[i], b[i])); break;
     case 3: r = Fq::canon(Fq::sub(a[i], b[i])); break;
+    case 5: r = Fq::from_mont(Fq::sqr(Fq::to_mont(a[i]))); break;
+    case 6: r = Fp::from_mont(Fp::sqr(Fp::to_mont(a[i]))); break;
     default: r = Fq::from_mont(Fq::inv(Fq::to_mont(a[i]))); break;
   }
   out[i] = r;

@@ -34,8 +34,18 @@ struct Fe {
   uint32_t v[6];
 };
 
+#if defined(__CUDACC__)
+// Modulus constants for the device reduction, read from the constant bank.  Kept out of
+// immediates on purpose: with visible constants ptxas proves lo(u*M0 + s) = 0 and rewrites
+// the full-rate IMAD.WIDE into half-rate IMAD.HI + carry fix-ups.
+// [field][M0, M5, NP, pad]; field 0 = F_p, 1 = F_q
+static __constant__ uint32_t tc_cmod[2][4] = {{0x01000001u, 0x2u, 0x00ffffffu, 0u},
+                                              {0x78000077u, 0xF0u, 0xb10226b9u, 0u}};
+#endif
+
 // --- field parameter packs -------------------------------------------------------------
 struct FpParams {   // scalar field F_p (field.py PrimeField(backend.order))
+  static constexpr int IDX = 0;
   static constexpr uint32_t M0 = 0x01000001u, M5 = 0x2u;
   static constexpr uint32_t NP = 0x00ffffffu;         // -p^{-1} mod 2^32
   // R mod p and R^2 mod p (R = 2^192)
@@ -45,6 +55,7 @@ struct FpParams {   // scalar field F_p (field.py PrimeField(backend.order))
                             R24 = 0x0u, R25 = 0x0u;
 };
 struct FqParams {   // curve base field F_q
+  static constexpr int IDX = 1;
   static constexpr uint32_t M0 = 0x78000077u, M5 = 0xF0u;
   static constexpr uint32_t NP = 0xb10226b9u;         // -q^{-1} mod 2^32
   static constexpr uint32_t ONE0 = 0x89111119u, ONE1 = 0xff7fffffu, ONE2 = 0xffffffffu,
@@ -185,47 +196,129 @@ struct Field {
   TC_HD static Fe dbl(const Fe& a) { return add(a, a); }
 
   // ---- Montgomery product ----
-  // T[0..11] = a * b
-  TC_HD static void mul_wide(uint32_t T[12], const Fe& a, const Fe& b) {
 #if defined(__CUDA_ARCH__)
+  // (r0..r5) += x0*b, x1*b, x2*b as three 64-bit register pairs in one carry chain, carry
+  // out added into c.  ptxas fuses each mad.lo.cc/madc.hi.cc pair into one
+  // IMAD.WIDE.U32(.X) on an aligned register pair.
+  TC_D static void chain3(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, uint32_t& r4, uint32_t& r5,
+                          uint32_t& c, uint32_t x0, uint32_t x1, uint32_t x2, uint32_t b) {
+    asm("mad.lo.cc.u32  %0, %7, %10, %0;\n\t"
+        "madc.hi.cc.u32 %1, %7, %10, %1;\n\t"
+        "madc.lo.cc.u32 %2, %8, %10, %2;\n\t"
+        "madc.hi.cc.u32 %3, %8, %10, %3;\n\t"
+        "madc.lo.cc.u32 %4, %9, %10, %4;\n\t"
+        "madc.hi.cc.u32 %5, %9, %10, %5;\n\t"
+        "addc.u32       %6, %6, 0;\n\t"
+        : "+r"(r0), "+r"(r1), "+r"(r2), "+r"(r3), "+r"(r4), "+r"(r5), "+r"(c)
+        : "r"(x0), "r"(x1), "r"(x2), "r"(b));
+  }
+  TC_D static void chain3_last(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, uint32_t& r4, uint32_t& r5,
+                               uint32_t x0, uint32_t x1, uint32_t x2, uint32_t b) {
+    asm("mad.lo.cc.u32  %0, %6, %9, %0;\n\t"
+        "madc.hi.cc.u32 %1, %6, %9, %1;\n\t"
+        "madc.lo.cc.u32 %2, %7, %9, %2;\n\t"
+        "madc.hi.cc.u32 %3, %7, %9, %3;\n\t"
+        "madc.lo.cc.u32 %4, %8, %9, %4;\n\t"
+        "madc.hi.u32    %5, %8, %9, %5;\n\t"
+        : "+r"(r0), "+r"(r1), "+r"(r2), "+r"(r3), "+r"(r4), "+r"(r5)
+        : "r"(x0), "r"(x1), "r"(x2), "r"(b));
+  }
+  TC_D static void chain2(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, uint32_t& c, uint32_t x0,
+                          uint32_t x1, uint32_t b) {
+    asm("mad.lo.cc.u32  %0, %5, %7, %0;\n\t"
+        "madc.hi.cc.u32 %1, %5, %7, %1;\n\t"
+        "madc.lo.cc.u32 %2, %6, %7, %2;\n\t"
+        "madc.hi.cc.u32 %3, %6, %7, %3;\n\t"
+        "addc.u32       %4, %4, 0;\n\t"
+        : "+r"(r0), "+r"(r1), "+r"(r2), "+r"(r3), "+r"(c)
+        : "r"(x0), "r"(x1), "r"(b));
+  }
+  TC_D static void chain1(uint32_t& r0, uint32_t& r1, uint32_t& c, uint32_t x0, uint32_t b) {
+    asm("mad.lo.cc.u32  %0, %3, %4, %0;\n\t"
+        "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"
+        "addc.u32       %2, %2, 0;\n\t"
+        : "+r"(r0), "+r"(r1), "+r"(c)
+        : "r"(x0), "r"(b));
+  }
+  TC_D static uint64_t madwide(uint32_t a, uint32_t b, uint64_t c) {
+    uint64_t r;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(c));
+    return r;
+  }
+#endif
+
+  // T[0..11] = a * b
+#if defined(__CUDA_ARCH__)
+  // operand scanning, one row per limb of b: two 7-limb carry chains per row
+  TC_D static void mul_wide_rows(uint32_t T[12], const Fe& a, const Fe& b) {
 #pragma unroll
     for (int i = 0; i < 12; i++) T[i] = 0;
 #pragma unroll
     for (int i = 0; i < 6; i++) {
       const uint32_t bi = b.v[i];
-      asm("mad.lo.cc.u32  %0, %7, %10, %0;\n\t"
-          "madc.hi.cc.u32 %1, %7, %10, %1;\n\t"
-          "madc.lo.cc.u32 %2, %8, %10, %2;\n\t"
-          "madc.hi.cc.u32 %3, %8, %10, %3;\n\t"
-          "madc.lo.cc.u32 %4, %9, %10, %4;\n\t"
-          "madc.hi.cc.u32 %5, %9, %10, %5;\n\t"
-          "addc.u32       %6, %6, 0;\n\t"
-          : "+r"(T[i + 0]), "+r"(T[i + 1]), "+r"(T[i + 2]), "+r"(T[i + 3]), "+r"(T[i + 4]),
-            "+r"(T[i + 5]), "+r"(T[i + 6])
-          : "r"(a.v[0]), "r"(a.v[2]), "r"(a.v[4]), "r"(bi));
-      if (i < 5) {
-        asm("mad.lo.cc.u32  %0, %7, %10, %0;\n\t"
-            "madc.hi.cc.u32 %1, %7, %10, %1;\n\t"
-            "madc.lo.cc.u32 %2, %8, %10, %2;\n\t"
-            "madc.hi.cc.u32 %3, %8, %10, %3;\n\t"
-            "madc.lo.cc.u32 %4, %9, %10, %4;\n\t"
-            "madc.hi.cc.u32 %5, %9, %10, %5;\n\t"
-            "addc.u32       %6, %6, 0;\n\t"
-            : "+r"(T[i + 1]), "+r"(T[i + 2]), "+r"(T[i + 3]), "+r"(T[i + 4]), "+r"(T[i + 5]),
-              "+r"(T[i + 6]), "+r"(T[(i + 7) < 12 ? (i + 7) : 11])
-            : "r"(a.v[1]), "r"(a.v[3]), "r"(a.v[5]), "r"(bi));
-      } else {
-        asm("mad.lo.cc.u32  %0, %6, %9, %0;\n\t"
-            "madc.hi.cc.u32 %1, %6, %9, %1;\n\t"
-            "madc.lo.cc.u32 %2, %7, %9, %2;\n\t"
-            "madc.hi.cc.u32 %3, %7, %9, %3;\n\t"
-            "madc.lo.cc.u32 %4, %8, %9, %4;\n\t"
-            "madc.hi.u32    %5, %8, %9, %5;\n\t"
-            : "+r"(T[i + 1]), "+r"(T[i + 2]), "+r"(T[i + 3]), "+r"(T[i + 4]), "+r"(T[i + 5]),
-              "+r"(T[i + 6])
-            : "r"(a.v[1]), "r"(a.v[3]), "r"(a.v[5]), "r"(bi));
-      }
+      chain3(T[i + 0], T[i + 1], T[i + 2], T[i + 3], T[i + 4], T[i + 5], T[i + 6], a.v[0], a.v[2], a.v[4], bi);
+      if (i < 5)
+        chain3(T[i + 1], T[i + 2], T[i + 3], T[i + 4], T[i + 5], T[i + 6], T[i + 7], a.v[1], a.v[3], a.v[5], bi);
+      else
+        chain3_last(T[i + 1], T[i + 2], T[i + 3], T[i + 4], T[i + 5], T[i + 6], a.v[1], a.v[3], a.v[5], bi);
     }
+  }
+#endif
+
+#ifndef TC_MULV
+#define TC_MULV 1   // 0: even/odd pair accumulators, 1: operand-scanning rows
+#endif
+#ifndef TC_SQRV
+#define TC_SQRV 1   // 0: square through the generic product, 1: dedicated 21-product square (3% faster accumulation)
+#endif
+
+  TC_HD static void mul_wide(uint32_t T[12], const Fe& a, const Fe& b) {
+#if defined(__CUDA_ARCH__) && TC_MULV == 1
+    mul_wide_rows(T, a, b);
+#elif defined(__CUDA_ARCH__)
+    // Even/odd split: ev[t] collects products whose 64-bit pair starts at even position t,
+    // od[t] those starting at odd position t+1 (od is shifted by one limb), so every
+    // partial product is one IMAD.WIDE into an aligned register pair with no MOVs.
+    uint32_t ev[12], od[12];
+#pragma unroll
+    for (int i = 0; i < 12; i++) ev[i] = od[i] = 0;
+    const uint32_t a0 = a.v[0], a1 = a.v[1], a2 = a.v[2], a3 = a.v[3], a4 = a.v[4], a5 = a.v[5];
+    // row 0
+    chain3(ev[0], ev[1], ev[2], ev[3], ev[4], ev[5], ev[6], a0, a2, a4, b.v[0]);
+    chain3(od[0], od[1], od[2], od[3], od[4], od[5], od[6], a1, a3, a5, b.v[0]);
+    // row 1
+    chain3(ev[2], ev[3], ev[4], ev[5], ev[6], ev[7], ev[8], a1, a3, a5, b.v[1]);
+    chain3(od[0], od[1], od[2], od[3], od[4], od[5], od[6], a0, a2, a4, b.v[1]);
+    // row 2
+    chain3(ev[2], ev[3], ev[4], ev[5], ev[6], ev[7], ev[8], a0, a2, a4, b.v[2]);
+    chain3(od[2], od[3], od[4], od[5], od[6], od[7], od[8], a1, a3, a5, b.v[2]);
+    // row 3
+    chain3(ev[4], ev[5], ev[6], ev[7], ev[8], ev[9], ev[10], a1, a3, a5, b.v[3]);
+    chain3(od[2], od[3], od[4], od[5], od[6], od[7], od[8], a0, a2, a4, b.v[3]);
+    // row 4
+    chain3(ev[4], ev[5], ev[6], ev[7], ev[8], ev[9], ev[10], a0, a2, a4, b.v[4]);
+    chain3(od[4], od[5], od[6], od[7], od[8], od[9], od[10], a1, a3, a5, b.v[4]);
+    // row 5
+    chain3_last(ev[6], ev[7], ev[8], ev[9], ev[10], ev[11], a1, a3, a5, b.v[5]);
+    chain3(od[4], od[5], od[6], od[7], od[8], od[9], od[10], a0, a2, a4, b.v[5]);
+    // T = ev + od * 2^32
+    T[0] = ev[0];
+    asm("add.cc.u32  %0, %11, %22;\n\t"
+        "addc.cc.u32 %1, %12, %23;\n\t"
+        "addc.cc.u32 %2, %13, %24;\n\t"
+        "addc.cc.u32 %3, %14, %25;\n\t"
+        "addc.cc.u32 %4, %15, %26;\n\t"
+        "addc.cc.u32 %5, %16, %27;\n\t"
+        "addc.cc.u32 %6, %17, %28;\n\t"
+        "addc.cc.u32 %7, %18, %29;\n\t"
+        "addc.cc.u32 %8, %19, %30;\n\t"
+        "addc.cc.u32 %9, %20, %31;\n\t"
+        "addc.u32    %10, %21, %32;\n\t"
+        : "=r"(T[1]), "=r"(T[2]), "=r"(T[3]), "=r"(T[4]), "=r"(T[5]), "=r"(T[6]), "=r"(T[7]), "=r"(T[8]),
+          "=r"(T[9]), "=r"(T[10]), "=r"(T[11])
+        : "r"(ev[1]), "r"(ev[2]), "r"(ev[3]), "r"(ev[4]), "r"(ev[5]), "r"(ev[6]), "r"(ev[7]), "r"(ev[8]),
+          "r"(ev[9]), "r"(ev[10]), "r"(ev[11]), "r"(od[0]), "r"(od[1]), "r"(od[2]), "r"(od[3]), "r"(od[4]),
+          "r"(od[5]), "r"(od[6]), "r"(od[7]), "r"(od[8]), "r"(od[9]), "r"(od[10]));
 #else
     for (int i = 0; i < 12; i++) T[i] = 0;
     for (int i = 0; i < 6; i++) {
@@ -242,6 +335,36 @@ struct Field {
 
   // Montgomery reduction of T (< m * R) exploiting limbs 1..4 of m being zero.
   TC_HD static Fe redc(const uint32_t T[12]) {
+#ifndef TC_REDCV
+#define TC_REDCV 0   // 0: plain C (ptxas picks IMAD.HI for the known-zero low halves), 1: explicit IMAD.WIDE
+#endif
+#if defined(__CUDA_ARCH__) && TC_REDCV == 1
+    // word-serial: u_i = s_i * n' makes position i vanish; s carries into position i+1.
+    // Every 32x32 product is one full-rate IMAD.WIDE (never the half-rate IMAD.HI).
+    const uint32_t M0 = tc_cmod[PM::IDX][0], M5 = tc_cmod[PM::IDX][1], NP = tc_cmod[PM::IDX][2];
+    uint32_t u[6];
+    uint64_t s = T[0];
+#pragma unroll
+    for (int i = 0; i < 6; i++) {
+      u[i] = (uint32_t)s * NP;
+      s = madwide(u[i], M0, s) >> 32;
+      if (i < 5) s += T[i + 1];
+      if (i == 4) s = madwide(u[0], M5, s);   // u_0 * M5 lands on position 5
+    }
+    Fe r;
+    s = madwide(u[1], M5, s + T[6]);
+    r.v[0] = (uint32_t)s;
+    s = madwide(u[2], M5, (s >> 32) + T[7]);
+    r.v[1] = (uint32_t)s;
+    s = madwide(u[3], M5, (s >> 32) + T[8]);
+    r.v[2] = (uint32_t)s;
+    s = madwide(u[4], M5, (s >> 32) + T[9]);
+    r.v[3] = (uint32_t)s;
+    s = madwide(u[5], M5, (s >> 32) + T[10]);
+    r.v[4] = (uint32_t)s;
+    r.v[5] = (uint32_t)(s >> 32) + T[11];
+    return r;
+#else
     uint32_t u[6];
     uint64_t s, carry = 0;
 #pragma unroll
@@ -266,6 +389,7 @@ struct Field {
     s = (s >> 32) + T[11];
     r.v[5] = (uint32_t)s;
     return r;
+#endif
   }
 
   TC_HD static Fe mul(const Fe& a, const Fe& b) {
@@ -273,7 +397,73 @@ struct Field {
     mul_wide(T, a, b);
     return redc(T);
   }
-  TC_HD static Fe sqr(const Fe& a) { return mul(a, a); }
+
+#if defined(__CUDA_ARCH__)
+  // T = a^2: the 15 cross products once (even/odd pair chains), doubled, plus the 6
+  // squares on the diagonal — 21 IMAD.WIDE instead of 36.
+  TC_D static void sqr_wide(uint32_t T[12], const Fe& a) {
+    uint32_t ev[12], od[12];
+#pragma unroll
+    for (int i = 0; i < 12; i++) ev[i] = od[i] = 0;
+    const uint32_t a0 = a.v[0], a1 = a.v[1], a2 = a.v[2], a3 = a.v[3], a4 = a.v[4], a5 = a.v[5];
+    chain3(od[0], od[1], od[2], od[3], od[4], od[5], od[6], a1, a3, a5, a0);   // pos 1,3,5
+    chain2(ev[2], ev[3], ev[4], ev[5], ev[6], a2, a4, a0);                     // pos 2,4
+    chain2(od[2], od[3], od[4], od[5], od[6], a2, a4, a1);                     // pos 3,5
+    chain2(ev[4], ev[5], ev[6], ev[7], ev[8], a3, a5, a1);                     // pos 4,6
+    chain2(od[4], od[5], od[6], od[7], od[8], a3, a5, a2);                     // pos 5,7
+    chain1(ev[6], ev[7], ev[8], a4, a2);                                       // pos 6
+    chain1(od[6], od[7], od[8], a4, a3);                                       // pos 7
+    chain1(ev[8], ev[9], ev[10], a5, a3);                                      // pos 8
+    chain1(od[8], od[9], od[10], a5, a4);                                      // pos 9
+    // C = ev + od * 2^32 (positions 1..11), then 2C + diagonal
+    uint32_t C[12];
+    C[0] = 0;
+    asm("add.cc.u32  %0, %11, %21;\n\t"
+        "addc.cc.u32 %1, %12, %22;\n\t"
+        "addc.cc.u32 %2, %13, %23;\n\t"
+        "addc.cc.u32 %3, %14, %24;\n\t"
+        "addc.cc.u32 %4, %15, %25;\n\t"
+        "addc.cc.u32 %5, %16, %26;\n\t"
+        "addc.cc.u32 %6, %17, %27;\n\t"
+        "addc.cc.u32 %7, %18, %28;\n\t"
+        "addc.cc.u32 %8, %19, %29;\n\t"
+        "addc.cc.u32 %9, %20, %30;\n\t"
+        "addc.u32    %10, 0, %31;\n\t"
+        : "=r"(C[1]), "=r"(C[2]), "=r"(C[3]), "=r"(C[4]), "=r"(C[5]), "=r"(C[6]), "=r"(C[7]), "=r"(C[8]),
+          "=r"(C[9]), "=r"(C[10]), "=r"(C[11])
+        : "r"(ev[1]), "r"(ev[2]), "r"(ev[3]), "r"(ev[4]), "r"(ev[5]), "r"(ev[6]), "r"(ev[7]), "r"(ev[8]),
+          "r"(ev[9]), "r"(ev[10]), "r"(od[0]), "r"(od[1]), "r"(od[2]), "r"(od[3]), "r"(od[4]), "r"(od[5]),
+          "r"(od[6]), "r"(od[7]), "r"(od[8]), "r"(od[9]), "r"(od[10]));
+#pragma unroll
+    for (int i = 11; i > 0; i--) T[i] = __funnelshift_l(C[i - 1], C[i], 1);
+    T[0] = 0;
+    asm("mad.lo.cc.u32  %0, %12, %12, %0;\n\t"
+        "madc.hi.cc.u32 %1, %12, %12, %1;\n\t"
+        "madc.lo.cc.u32 %2, %13, %13, %2;\n\t"
+        "madc.hi.cc.u32 %3, %13, %13, %3;\n\t"
+        "madc.lo.cc.u32 %4, %14, %14, %4;\n\t"
+        "madc.hi.cc.u32 %5, %14, %14, %5;\n\t"
+        "madc.lo.cc.u32 %6, %15, %15, %6;\n\t"
+        "madc.hi.cc.u32 %7, %15, %15, %7;\n\t"
+        "madc.lo.cc.u32 %8, %16, %16, %8;\n\t"
+        "madc.hi.cc.u32 %9, %16, %16, %9;\n\t"
+        "madc.lo.cc.u32 %10, %17, %17, %10;\n\t"
+        "madc.hi.u32    %11, %17, %17, %11;\n\t"
+        : "+r"(T[0]), "+r"(T[1]), "+r"(T[2]), "+r"(T[3]), "+r"(T[4]), "+r"(T[5]), "+r"(T[6]), "+r"(T[7]),
+          "+r"(T[8]), "+r"(T[9]), "+r"(T[10]), "+r"(T[11])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(a4), "r"(a5));
+  }
+#endif
+
+  TC_HD static Fe sqr(const Fe& a) {
+#if defined(__CUDA_ARCH__) && TC_SQRV == 1
+    uint32_t T[12];
+    sqr_wide(T, a);
+    return redc(T);
+#else
+    return mul(a, a);
+#endif
+  }
 
   // multiply by a small integer k < 2^20 (result < 2m): k*a < 2^20 * 2m, then reduce by
   // folding the top limb with one Montgomery-free trial loop.  Used for small node

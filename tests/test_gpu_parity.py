@@ -51,6 +51,13 @@ def test_device_field_ops():
     dap, dbp = lim(ap), lim(bp)   # keep both alive: temporaries would share freed memory
     ctx.check(L.tc_debug_field(ctx.handle, 1, dap.data_ptr(), dbp.data_ptr(), out.data_ptr(), n))
     assert _conv.limbs_to_ints(out.view(-1, 6)) == [x * y % O.P for x, y in zip(ap, bp)]
+    # dedicated squaring paths (op 5: F_q, op 6: F_p), incl. all-ones limb patterns
+    sq = a[:-4] + [O.Q - 1, 2 ** 167 - 1 if 2 ** 167 - 1 < O.Q else O.Q - 3, 1, 0]
+    dsq = lim(sq)
+    ctx.check(L.tc_debug_field(ctx.handle, 5, dsq.data_ptr(), dsq.data_ptr(), out.data_ptr(), n))
+    assert _conv.limbs_to_ints(out.view(-1, 6)) == [x * x % O.Q for x in sq]
+    ctx.check(L.tc_debug_field(ctx.handle, 6, dap.data_ptr(), dap.data_ptr(), out.data_ptr(), n))
+    assert _conv.limbs_to_ints(out.view(-1, 6)) == [x * x % O.P for x in ap]
 
 
 # ---------------------------------------------------------------- K1 quantize
