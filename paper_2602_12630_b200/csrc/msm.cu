@@ -6,23 +6,25 @@
 // designates it the single performance hot-spot.  The prover runs many MSMs against one
 // SRS (32 layers per forward, m quotients per opening, 8 nodes per Terkle level), so the
 // whole batch goes through ONE pipeline:
-//   1. k_scan_bits    — max bit length of the centred scalar magnitudes + quantisation
-//                       errors (scalars are either canonical F_p limbs or raw floats that
-//                       are quantised on the fly, fusing K1 into the MSM)
-//   2. k_digits       — signed c-bit window digits; only NON-ZERO digits are emitted,
-//                       compacted per block: key = (l*nwin + w)*B + |d|-1, value =
-//                       point index | sign<<31
-//   3. radix sort     — (key, value) by bucket, CUB onesweep over the used key bits
-//   4. k_bounds       — [start, end) of every bucket
-//   5. levels         — load-balanced segmented reduction: each bucket is cut into pieces
-//                       of <= T entries, one thread per piece (XYZZ accumulator, mixed
-//                       affine adds at level 0); piece sums feed the next level until every
-//                       bucket is one point (heavy-tailed activations make a few buckets
-//                       huge — they get split, not serialised)
-//   6. k_bucket_reduce— per (msm, window, segment of buckets): sum_b b * B_b by running sums
-//   7. k_window_sum, k_final — segments -> window sums -> Horner over windows -> affine
-// Affine outputs are canonical and the group is abelian, so any window size, bucket order
-// or coordinate system reproduces the reference's bytes exactly.
+//   1. k_scan_bits    — histogram of the bit lengths of the centred scalar magnitudes +
+//                       quantisation errors (scalars are canonical F_p limbs, or raw floats
+//                       quantised on the fly: K1 is fused into the MSM)
+//   2. window plan    — (host) variable-width signed windows chosen from that histogram:
+//                       a DP minimising  #non-zero digits + kappa * #buckets.  Heavy-tailed
+//                       activations get a wide low window and a narrow high window, so most
+//                       elements contribute ONE bucket entry, not two.
+//   3. k_digits       — signed digits; only NON-ZERO digits are emitted, compacted per
+//                       block: key = l*nbm + base_w + |d|-1, value = point index | sign<<31
+//   4. radix sort     — (key, value) by bucket, CUB onesweep over the used key bits
+//   5. k_bounds       — [start, end) of every bucket
+//   6. levels         — load-balanced segmented reduction: buckets are cut into pieces of
+//                       <= T entries (one thread per piece, XYZZ accumulator, mixed affine
+//                       adds); single-piece buckets are final at once, multi-piece buckets
+//                       (the heavy tail) feed further levels of T1-way reduction
+//   7. k_bucket_reduce— per segment of buckets: sum_b b * B_b by running sums
+//   8. k_window_sum, k_final — segments -> window sums -> Horner over the windows -> affine
+// Affine outputs are canonical and the group is abelian, so any window layout, bucket
+// order or coordinate system reproduces the reference's bytes exactly.
 #include <cub/cub.cuh>
 
 #include "quant.cuh"
@@ -34,6 +36,16 @@ namespace {
 
 constexpr uint32_t SIGN_BIT = 0x80000000u;
 constexpr int DT_LIMBS = 0;   // template code for canonical F_p scalars
+constexpr int MAXW = 48;      // windows per scalar (>= ceil(163 / 4))
+constexpr int NHIST = 168;    // bit-length histogram bins
+
+struct WinPlan {
+  int nwin;
+  uint32_t nbm;              // buckets per MSM = sum_w 2^(c_w - 1)
+  uint8_t off[MAXW];         // first bit of window w
+  uint8_t width[MAXW];       // c_w
+  uint32_t base[MAXW + 1];   // first bucket of window w inside one MSM
+};
 
 __device__ __forceinline__ uint32_t bitlen6(const Fe& a) {
 #pragma unroll
@@ -63,34 +75,36 @@ __device__ __forceinline__ uint32_t window_bits(const Fe& m, int lo, int c) {
   return (uint32_t)(w >> sh) & ((1u << c) - 1u);
 }
 
+// out[0] = quantisation flags, out[1..NHIST] = bit-length histogram
 template <int DT>
 __global__ void k_scan_bits(const void* const* ptrs, uint64_t n, int scale_bits, uint32_t* out) {
+  __shared__ uint32_t hist[NHIST];
+  for (int i = threadIdx.x; i < NHIST; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
   const void* p = ptrs[blockIdx.y];
-  uint32_t mx = 0, f = 0;
+  uint32_t f = 0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     Fe mag;
     bool neg;
     load_scalar<DT>(p, i, scale_bits, mag, neg, f);
-    mx = max(mx, bitlen6(mag));
+    atomicAdd(&hist[bitlen6(mag)], 1u);
   }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    f |= __shfl_xor_sync(0xffffffffu, f, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    if (mx) atomicMax(out, mx);
-    if (f) atomicOr(out + 1, f);
-  }
+  for (int o = 16; o; o >>= 1) f |= __shfl_xor_sync(0xffffffffu, f, o);
+  if ((threadIdx.x & 31) == 0 && f) atomicOr(out, f);
+  __syncthreads();
+  for (int i = threadIdx.x; i < NHIST; i += blockDim.x)
+    if (hist[i]) atomicAdd(out + 1 + i, hist[i]);
 }
 
-// signed digits of `mag`: calls emit(w, |d|, digit_negative) for every non-zero digit
+// signed digits of `mag` under plan P: emit(w, |d|, digit_negative) for non-zero digits
 template <class F>
-__device__ __forceinline__ void for_digits(const Fe& mag, int c, int nwin, F&& emit) {
-  const uint32_t half = 1u << (c - 1), full = 1u << c;
+__device__ __forceinline__ void for_digits(const Fe& mag, const WinPlan& P, F&& emit) {
   uint32_t carry = 0;
-  for (int w = 0; w < nwin; w++) {
-    uint32_t d = window_bits(mag, w * c, c) + carry;
+  for (int w = 0; w < P.nwin; w++) {
+    const int c = P.width[w];
+    const uint32_t half = 1u << (c - 1), full = 1u << c;
+    uint32_t d = window_bits(mag, P.off[w], c) + carry;
     bool dn = false;
     if (d > half) {   // d - 2^c, carry into the next window
       d = full - d;
@@ -104,21 +118,20 @@ __device__ __forceinline__ void for_digits(const Fe& mag, int c, int nwin, F&& e
 }
 
 template <int DT>
-__global__ void __launch_bounds__(256) k_digits(const void* const* ptrs, uint64_t n, int scale_bits, int c, int nwin,
+__global__ void __launch_bounds__(256) k_digits(const void* const* ptrs, uint64_t n, int scale_bits, WinPlan P,
                                                 uint32_t* keys, uint32_t* vals, uint32_t* count) {
   __shared__ uint32_t warp_tot[8];
   __shared__ uint32_t base;
   const uint32_t l = blockIdx.y;
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  const uint32_t B = 1u << (c - 1);
   Fe mag;
   bool neg = false;
   uint32_t f = 0, cnt = 0;
   if (i < n) {
     load_scalar<DT>(ptrs[l], i, scale_bits, mag, neg, f);
-    for_digits(mag, c, nwin, [&](int, uint32_t, bool) { cnt++; });
+    for_digits(mag, P, [&](int, uint32_t, bool) { cnt++; });
   }
-  // block-wide exclusive scan of cnt
+  // block-wide exclusive scan of cnt -> one atomic per block
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint32_t incl = cnt;
 #pragma unroll
@@ -140,9 +153,9 @@ __global__ void __launch_bounds__(256) k_digits(const void* const* ptrs, uint64_
   __syncthreads();
   uint32_t pos = base + warp_tot[wid] + incl - cnt;
   if (cnt) {
-    const uint32_t key0 = l * (uint32_t)nwin * B;
-    for_digits(mag, c, nwin, [&](int w, uint32_t d, bool dn) {
-      keys[pos] = key0 + (uint32_t)w * B + d - 1u;
+    const uint32_t key0 = l * P.nbm;
+    for_digits(mag, P, [&](int w, uint32_t d, bool dn) {
+      keys[pos] = key0 + P.base[w] + d - 1u;
       vals[pos] = (uint32_t)i | ((neg != dn) ? SIGN_BIT : 0u);
       pos++;
     });
@@ -158,18 +171,23 @@ __global__ void k_bounds(const uint32_t* keys, const uint32_t* count, uint32_t* 
   if (j + 1 == E || keys[j + 1] != k) bend[k] = (uint32_t)j + 1u;
 }
 
-// pieces per bucket; np has nb+1 entries (last = 0).  Sizes from [bstart, bend) or from
-// the previous level's offsets (prev_off != nullptr).
-__global__ void k_piece_count(const uint32_t* bstart, const uint32_t* bend, const uint32_t* prev_off, uint32_t nb,
-                              uint32_t T, uint32_t* np) {
+// level 0 piece counts: np[k] = ceil(size/T) (threads), npm[k] = np[k] if > 1 (items)
+__global__ void k_count0(const uint32_t* bstart, const uint32_t* bend, uint32_t nb, uint32_t T, uint32_t* np,
+                         uint32_t* npm) {
   uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k > nb) return;
-  if (k == nb) {
-    np[k] = 0;
-    return;
-  }
-  uint32_t sz = prev_off ? prev_off[k + 1] - prev_off[k] : bend[k] - bstart[k];
-  np[k] = (sz + T - 1) / T;
+  uint32_t c = (k == nb) ? 0u : (bend[k] - bstart[k] + T - 1) / T;
+  np[k] = c;
+  npm[k] = c > 1 ? c : 0u;
+}
+
+// level >= 1: items of bucket k are [off_in[k], off_in[k+1]) (0 or >= 2 of them)
+__global__ void k_count(const uint32_t* off_in, uint32_t nb, uint32_t T, uint32_t* np, uint32_t* npm) {
+  uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k > nb) return;
+  uint32_t c = (k == nb) ? 0u : (off_in[k + 1] - off_in[k] + T - 1) / T;
+  np[k] = c;
+  npm[k] = c > 1 ? c : 0u;
 }
 
 __device__ __forceinline__ uint32_t find_bucket(const uint32_t* off, uint32_t nb, uint32_t p) {
@@ -184,15 +202,17 @@ __device__ __forceinline__ uint32_t find_bucket(const uint32_t* off, uint32_t nb
   return lo;
 }
 
-// level 0: entries are (sign | point index) into the shared affine bases
+// level 0: entries are (sign | point index) into the shared affine bases.  A bucket that
+// fits in one piece is final (written to buckets[k]); otherwise its piece sums go to items.
 __global__ void __launch_bounds__(128) k_accum_aff(const uint32_t* vals, const Aff* bases, const uint32_t* bstart,
-                                                   const uint32_t* bend, const uint32_t* off, uint32_t nb, uint32_t T,
-                                                   Xyzz* out) {
+                                                   const uint32_t* bend, const uint32_t* toff, const uint32_t* ooff,
+                                                   uint32_t nb, uint32_t T, Xyzz* items, Xyzz* buckets) {
   uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t total = off[nb];
+  uint32_t total = toff[nb];
   if (p >= total) return;
-  uint32_t k = find_bucket(off, nb, p);
-  uint32_t a = bstart[k] + (p - off[k]) * T;
+  uint32_t k = find_bucket(toff, nb, p);
+  uint32_t piece = p - toff[k];
+  uint32_t a = bstart[k] + piece * T;
   uint32_t b = min(a + T, bend[k]);
   Xyzz acc = xyzz_inf();
   for (uint32_t j = a; j < b; j++) {
@@ -201,55 +221,62 @@ __global__ void __launch_bounds__(128) k_accum_aff(const uint32_t* vals, const A
     if (v & SIGN_BIT) q.y = Fq::neg(q.y);
     xyzz_add_aff(acc, q);
   }
-  out[p] = acc;
+  if (toff[k + 1] - toff[k] == 1)
+    buckets[k] = acc;
+  else
+    items[ooff[k] + piece] = acc;
 }
 
-// level >= 1: bucket k's entries are in[prev_off[k] .. prev_off[k+1])
-__global__ void __launch_bounds__(128) k_accum_xyzz(const Xyzz* in, const uint32_t* prev_off, const uint32_t* off,
-                                                    uint32_t nb, uint32_t T, Xyzz* out) {
+// level >= 1: bucket k's items are in[iofs[k] .. iofs[k+1])
+__global__ void __launch_bounds__(128) k_accum_xyzz(const Xyzz* in, const uint32_t* iofs, const uint32_t* toff,
+                                                    const uint32_t* ooff, uint32_t nb, uint32_t T, Xyzz* out,
+                                                    Xyzz* buckets) {
   uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t total = off[nb];
+  uint32_t total = toff[nb];
   if (p >= total) return;
-  uint32_t k = find_bucket(off, nb, p);
-  uint32_t a = prev_off[k] + (p - off[k]) * T;
-  uint32_t b = min(a + T, prev_off[k + 1]);
+  uint32_t k = find_bucket(toff, nb, p);
+  uint32_t piece = p - toff[k];
+  uint32_t a = iofs[k] + piece * T;
+  uint32_t b = min(a + T, iofs[k + 1]);
   Xyzz acc = in[a];
   for (uint32_t j = a + 1; j < b; j++) xyzz_add(acc, in[j]);
-  out[p] = acc;
+  if (toff[k + 1] - toff[k] == 1)
+    buckets[k] = acc;
+  else
+    out[ooff[k] + piece] = acc;
 }
 
-__global__ void k_gather_buckets(const Xyzz* in, const uint32_t* off, uint32_t nb, Xyzz* buckets) {
-  uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= nb) return;
-  buckets[k] = (off[k + 1] > off[k]) ? in[off[k]] : xyzz_inf();
-}
-
-// per (window, segment): sum_{b in seg} (b+1) * B_b via running sums from the top
-__global__ void __launch_bounds__(128) k_bucket_reduce(const Xyzz* buckets, uint32_t B, uint32_t nwin_total,
+// segment s covers buckets [s*LS, (s+1)*LS) of the global bucket array (LS divides every
+// window's bucket count): sum_b (digit_b) * B_b with digit_b = b - base_w + 1
+__global__ void __launch_bounds__(128, 4) k_bucket_reduce(const Xyzz* buckets, WinPlan P, uint32_t nseg_total,
                                                        uint32_t LS, Xyzz* segs) {
-  uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t nseg = B / LS;
-  if (t >= nwin_total * nseg) return;
-  uint32_t w = t / nseg, s = t % nseg;
-  uint32_t lo = s * LS;
-  const Xyzz* bw = buckets + (uint64_t)w * B;
+  uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nseg_total) return;
+  uint32_t g = s * LS;
+  uint32_t r = g % P.nbm;
+  int w = 0;
+  while (w + 1 < P.nwin && P.base[w + 1] <= r) w++;
+  uint32_t lo = r - P.base[w];   // digit of the segment's first bucket minus 1
+  const Xyzz* bw = buckets + g;
   Xyzz run = xyzz_inf(), sum = xyzz_inf();
-  for (int b = (int)(lo + LS) - 1; b >= (int)lo; b--) {
+  for (int b = (int)LS - 1; b >= 0; b--) {
     xyzz_add(run, bw[b]);
     xyzz_add(sum, run);
   }
-  if (lo) {   // sum_b (b - lo + 1) B_b + lo * sum_b B_b
+  if (lo) {   // sum_b (b + 1) B_b + lo * sum_b B_b
     Xyzz extra = xyzz_mul_small(run, lo);
     xyzz_add(sum, extra);
   }
-  segs[t] = sum;
+  segs[s] = sum;
 }
 
-__global__ void __launch_bounds__(128) k_window_sum(const Xyzz* segs, uint32_t nseg, Xyzz* wsum) {
+// one block per (msm, window): tree-sum the window's segments
+__global__ void __launch_bounds__(128) k_window_sum(const Xyzz* segs, WinPlan P, uint32_t LS, Xyzz* wsum) {
   __shared__ Xyzz sh[128];
-  uint32_t w = blockIdx.x;
+  const uint32_t l = blockIdx.x / P.nwin, w = blockIdx.x % P.nwin;
+  const uint32_t s0 = (l * P.nbm + P.base[w]) / LS, s1 = (l * P.nbm + P.base[w + 1]) / LS;
   Xyzz acc = xyzz_inf();
-  for (uint32_t s = threadIdx.x; s < nseg; s += blockDim.x) xyzz_add(acc, segs[(uint64_t)w * nseg + s]);
+  for (uint32_t s = s0 + threadIdx.x; s < s1; s += blockDim.x) xyzz_add(acc, segs[s]);
   sh[threadIdx.x] = acc;
   __syncthreads();
   for (uint32_t st = blockDim.x / 2; st; st >>= 1) {
@@ -260,17 +287,17 @@ __global__ void __launch_bounds__(128) k_window_sum(const Xyzz* segs, uint32_t n
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) wsum[w] = sh[0];
+  if (threadIdx.x == 0) wsum[blockIdx.x] = sh[0];
 }
 
-// Horner over the windows of MSM l: sum_w 2^{c w} S_{l,w}, then canonical affine
-__global__ void k_final(const Xyzz* wsum, uint32_t L, uint32_t nwin, uint32_t c, Aff* out) {
+// Horner over the windows of MSM l: acc = 2^{c_w} acc + S_w from the top, then affine
+__global__ void k_final(const Xyzz* wsum, uint32_t L, WinPlan P, Aff* out) {
   uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= L) return;
-  const Xyzz* ws = wsum + (uint64_t)l * nwin;
-  Xyzz acc = ws[nwin - 1];
-  for (int w = (int)nwin - 2; w >= 0; w--) {
-    for (uint32_t i = 0; i < c; i++) acc = xyzz_dbl(acc);
+  const Xyzz* ws = wsum + (uint64_t)l * P.nwin;
+  Xyzz acc = ws[P.nwin - 1];
+  for (int w = P.nwin - 2; w >= 0; w--) {
+    for (int i = 0; i < P.width[w]; i++) acc = xyzz_dbl(acc);
     xyzz_add(acc, ws[w]);
   }
   Aff r = xyzz_to_aff(acc);
@@ -288,19 +315,69 @@ __global__ void k_fill_inf(Aff* out, uint32_t L) {
 
 uint32_t bitlen_u32(uint32_t v) { return v ? 32u - __builtin_clz(v) : 0u; }
 
-// window size minimising ~ nwin * (entries + 2.5 * buckets) per MSM
-int choose_c(uint64_t n, uint32_t nbits) {
-  int best_c = 4;
-  double best = 1e300;
-  for (int c = 4; c <= 20; c++) {
-    uint32_t nwin = (nbits + 1 + c - 1) / c;
-    double cost = (double)nwin * ((double)n + 2.5 * (double)(1u << (c - 1)));
-    if (cost < best) {
-      best = cost;
-      best_c = c;
+// Window plan from the bit-length histogram.  Window w (bits [o, o+c)) holds a non-zero
+// digit roughly iff the magnitude has bit length > o (carries included), so it costs
+// E_w = #{elements with bitlen > o} bucket entries plus L * 2^(c-1) buckets, each costing
+// ~KAPPA entries in the running-sum reduction.  DP over window boundaries.
+WinPlan plan_windows(const uint32_t* hist, uint32_t nbits, uint64_t L) {
+  // KAPPA: cost of one bucket in bucket-entry units.  Besides the two full XYZZ adds of
+  // the (latency-bound) running sum, every bucket widens the sort key; the sweep in
+  // tools/ab_kappa.sh on config 3 plateaus for KAPPA >= 64 with windows >= 8 bits
+  // (16.1 ms/step vs 17.7 ms for uniform 16-bit windows).
+  static const double KAPPA = getenv("TC_MSM_KAPPA") ? atof(getenv("TC_MSM_KAPPA")) : 64.0;
+  const int top = (int)nbits + 1;   // bits to cover incl. the final carry
+  double above[NHIST + 2];          // above[o] = #elements with bitlen > o
+  double acc = 0;
+  for (int b = NHIST; b >= 0; b--) {
+    above[b] = acc;
+    if (b < NHIST) acc += hist[b];
+  }
+  above[NHIST + 1] = 0;
+  const int CMAX = 20;
+  static const int CMIN_ENV = getenv("TC_MSM_CMIN") ? atoi(getenv("TC_MSM_CMIN")) : 8;
+  const int CMIN = std::max(CMIN_ENV, (top + MAXW - 1) / MAXW);   // at most MAXW windows
+  std::vector<double> best(top + CMAX + 1, 1e300);
+  std::vector<int> from(top + CMAX + 1, -1);
+  best[0] = 0;
+  for (int o = 0; o < top; o++) {
+    if (best[o] >= 1e299) continue;
+    for (int c = CMIN; c <= CMAX; c++) {
+      // a window may overshoot the top: the bits above nbits are zero
+      const int dst = std::min(o + c, top);
+      const double cost = best[o] + (o <= NHIST ? above[o] : 0) + KAPPA * (double)L * (double)(1u << (c - 1));
+      if (cost < best[dst]) {
+        best[dst] = cost;
+        from[dst] = o * 64 + c;   // window start and width
+      }
     }
   }
-  return best_c;
+  // backtrack
+  int pos = top;
+  std::vector<std::pair<int, int>> wins;
+  while (pos > 0) {
+    int f = from[pos];
+    int o = f / 64, c = f % 64;
+    wins.push_back({o, c});
+    pos = o;
+  }
+  WinPlan P;
+  P.nwin = (int)wins.size();
+  uint32_t b = 0;
+  for (int w = 0; w < P.nwin; w++) {
+    auto oc = wins[P.nwin - 1 - w];
+    P.off[w] = (uint8_t)oc.first;
+    P.width[w] = (uint8_t)oc.second;
+    P.base[w] = b;
+    b += 1u << (oc.second - 1);
+  }
+  P.base[P.nwin] = b;
+  P.nbm = b;
+  if (getenv("TC_MSM_DEBUG")) {
+    fprintf(stderr, "[tc msm] L=%llu nbits=%u windows:", (unsigned long long)L, nbits);
+    for (int w = 0; w < P.nwin; w++) fprintf(stderr, " [%d,+%d)", P.off[w], P.width[w]);
+    fprintf(stderr, " buckets/msm=%u\n", P.nbm);
+  }
+  return P;
 }
 
 template <class F>
@@ -339,10 +416,11 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   memcpy(ctx->h_stage, h_ptrs, sizeof(void*) * L);
   TC_CUDA(ctx, cudaMemcpyAsync(d_ptrs, ctx->h_stage, sizeof(void*) * L, cudaMemcpyHostToDevice, st));
 
-  // 1. magnitude bits + quantisation status
+  // 1. bit-length histogram + quantisation status
   uint32_t* d_small;
-  TC_TRY(scratch_t(ctx, "msm.small", 8, &d_small));
-  TC_CUDA(ctx, cudaMemsetAsync(d_small, 0, 8 * sizeof(uint32_t), st));
+  const int NSMALL = NHIST + 8;
+  TC_TRY(scratch_t(ctx, "msm.small", NSMALL, &d_small));
+  TC_CUDA(ctx, cudaMemsetAsync(d_small, 0, NSMALL * sizeof(uint32_t), st));
   {
     unsigned gx = std::min<unsigned>(blocks_for(n, 256), std::max(1u, (unsigned)ctx->num_sms * 8 / (unsigned)L + 1));
     int s = dispatch_dt(ctx, dtype, [&](auto dt) {
@@ -351,50 +429,57 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     if (s) return s;
     TC_LAUNCHED(ctx);
   }
-  TC_CUDA(ctx, cudaMemcpyAsync(ctx->h_flags, d_small, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  uint32_t* h_small = (uint32_t*)((char*)ctx->h_stage + 65536);
+  TC_CUDA(ctx, cudaMemcpyAsync(h_small, d_small, (NHIST + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   TC_CUDA(ctx, cudaStreamSynchronize(st));
-  const uint32_t nbits = ctx->h_flags[0];
-  TC_TRY(quantize_flags_to_status(ctx, ctx->h_flags[1]));
+  TC_TRY(quantize_flags_to_status(ctx, h_small[0]));
+  const uint32_t* hist = h_small + 1;
+  uint32_t nbits = 0;
+  for (int b = NHIST - 1; b > 0; b--)
+    if (hist[b]) {
+      nbits = (uint32_t)b;
+      break;
+    }
   if (nbits == 0) {
     k_fill_inf<<<blocks_for(L, 64), 64, 0, st>>>(d_out, (uint32_t)L);
     TC_LAUNCHED(ctx);
     return TC_OK;
   }
 
-  const int c = choose_c(n, nbits);
-  const uint32_t nwin = (nbits + 1 + c - 1) / c;
-  const uint32_t B = 1u << (c - 1);
-  const uint64_t nb64 = (uint64_t)L * nwin * B;
+  // 2. window plan
+  const WinPlan P = plan_windows(hist, nbits, (uint64_t)L);
+  if (P.nwin > MAXW) return fail(ctx, TC_ERR_VALUE, "msm: window plan too long");
+  const uint64_t nb64 = (uint64_t)L * P.nbm;
   if (nb64 >= (1ull << 31)) return fail(ctx, TC_ERR_VALUE, "msm batch too large (%llu buckets)", (unsigned long long)nb64);
   const uint32_t nb = (uint32_t)nb64;
-  const uint64_t cap = (uint64_t)L * n * nwin;
+  const uint64_t cap = (uint64_t)L * n * P.nwin;
   const int end_bit = (int)bitlen_u32(nb - 1);
 
-  // 2. non-zero digits, compacted
+  // 3. non-zero digits, compacted
   uint32_t *keys, *vals, *keys2, *vals2;
   TC_TRY(scratch_t(ctx, "msm.keys", cap, &keys));
   TC_TRY(scratch_t(ctx, "msm.vals", cap, &vals));
   TC_TRY(scratch_t(ctx, "msm.keys2", cap, &keys2));
   TC_TRY(scratch_t(ctx, "msm.vals2", cap, &vals2));
-  uint32_t* d_count = d_small + 2;
+  uint32_t* d_count = d_small + NHIST + 2;
   {
     int s = dispatch_dt(ctx, dtype, [&](auto dt) {
-      k_digits<decltype(dt)::value><<<dim3(blocks_for(n, 256), L), 256, 0, st>>>(d_ptrs, n, scale_bits, c, (int)nwin,
-                                                                                  keys, vals, d_count);
+      k_digits<decltype(dt)::value><<<dim3(blocks_for(n, 256), L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, keys, vals,
+                                                                                  d_count);
     });
     if (s) return s;
     TC_LAUNCHED(ctx);
   }
-  TC_CUDA(ctx, cudaMemcpyAsync(ctx->h_flags + 2, d_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  TC_CUDA(ctx, cudaMemcpyAsync(h_small, d_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   TC_CUDA(ctx, cudaStreamSynchronize(st));
-  const uint64_t E = ctx->h_flags[2];
+  const uint64_t E = h_small[0];
   if (E == 0) {
     k_fill_inf<<<blocks_for(L, 64), 64, 0, st>>>(d_out, (uint32_t)L);
     TC_LAUNCHED(ctx);
     return TC_OK;
   }
 
-  // 3. sort by bucket
+  // 4. sort by bucket
   size_t tmp_bytes = 0;
   cub::DoubleBuffer<uint32_t> dk(keys, keys2), dv(vals, vals2);
   cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, dk, dv, (int)E, 0, end_bit, st);
@@ -405,7 +490,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   const uint32_t* skeys = dk.Current();
   const uint32_t* svals = dv.Current();
 
-  // 4. bucket bounds
+  // 5. bucket bounds
   uint32_t *bstart, *bend;
   TC_TRY(scratch_t(ctx, "msm.bstart", (uint64_t)nb + 1, &bstart));
   TC_TRY(scratch_t(ctx, "msm.bend", (uint64_t)nb + 1, &bend));
@@ -414,33 +499,37 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   k_bounds<<<blocks_for(E, 256), 256, 0, st>>>(skeys, d_count, bstart, bend);
   TC_LAUNCHED(ctx);
 
-  // 5. levels of load-balanced segmented reduction (a bucket holds <= n entries)
-  // level 0 sums runs of T affine entries; later levels sum T1 partial points per thread
-  // (short sequential chains keep the latency of the few huge buckets low)
+  // 6. levels (a bucket holds <= n entries)
   const uint32_t T = (E >= (1u << 20)) ? 32u : (E >= (1u << 14) ? 16u : 8u);
   const uint32_t T1 = 8u;
   int levels = 1;
   for (uint64_t capT = T; capT < n; capT *= T1) levels++;
-  const uint64_t max_items = (E + T - 1) / T + nb;
-  uint32_t *offA, *offB, *np;
+  // items = pieces of multi-piece buckets: ceil(sz/T) <= 2 sz / T for sz > T
+  const uint64_t max_items = 2 * ((E + T - 1) / T) + 2;
+  uint32_t *np, *npm, *toff, *offA, *offB;
   Xyzz *itemsA, *itemsB, *buckets;
+  TC_TRY(scratch_t(ctx, "msm.np", (uint64_t)nb + 1, &np));
+  TC_TRY(scratch_t(ctx, "msm.npm", (uint64_t)nb + 1, &npm));
+  TC_TRY(scratch_t(ctx, "msm.toff", (uint64_t)nb + 1, &toff));
   TC_TRY(scratch_t(ctx, "msm.offA", (uint64_t)nb + 1, &offA));
   TC_TRY(scratch_t(ctx, "msm.offB", (uint64_t)nb + 1, &offB));
-  TC_TRY(scratch_t(ctx, "msm.np", (uint64_t)nb + 1, &np));
   TC_TRY(scratch_t(ctx, "msm.itemsA", max_items, &itemsA));
   TC_TRY(scratch_t(ctx, "msm.itemsB", max_items, &itemsB));
   TC_TRY(scratch_t(ctx, "msm.buckets", nb, &buckets));
+  TC_CUDA(ctx, cudaMemsetAsync(buckets, 0, (uint64_t)nb * sizeof(Xyzz), st));   // ZZ = 0: infinity
   size_t scan_bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, np, offA, (int)(nb + 1), st);
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, np, toff, (int)(nb + 1), st);
   void* d_scan;
   TC_TRY(scratch(ctx, "msm.scantmp", scan_bytes, &d_scan));
 
-  k_piece_count<<<blocks_for((uint64_t)nb + 1, 256), 256, 0, st>>>(bstart, bend, nullptr, nb, T, np);
+  k_count0<<<blocks_for((uint64_t)nb + 1, 256), 256, 0, st>>>(bstart, bend, nb, T, np, npm);
   TC_LAUNCHED(ctx);
-  TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(d_scan, scan_bytes, np, offA, (int)(nb + 1), st));
-  ctx->launches += 2;
+  TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(d_scan, scan_bytes, np, toff, (int)(nb + 1), st));
+  TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(d_scan, scan_bytes, npm, offA, (int)(nb + 1), st));
+  ctx->launches += 4;
   if (ctx->prof) TC_CUDA(ctx, cudaEventRecord(ctx->ev[0], st));
-  k_accum_aff<<<blocks_for(max_items, 128), 128, 0, st>>>(svals, d_bases, bstart, bend, offA, nb, T, itemsA);
+  k_accum_aff<<<blocks_for((E + T - 1) / T + nb, 128), 128, 0, st>>>(svals, d_bases, bstart, bend, toff, offA, nb, T,
+                                                                       itemsA, buckets);
   TC_LAUNCHED(ctx);
   if (ctx->prof) {
     TC_CUDA(ctx, cudaEventRecord(ctx->ev[1], st));
@@ -454,35 +543,35 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   }
   uint64_t items_bound = max_items;
   for (int lv = 1; lv < levels; lv++) {
-    k_piece_count<<<blocks_for((uint64_t)nb + 1, 256), 256, 0, st>>>(nullptr, nullptr, offA, nb, T1, np);
+    k_count<<<blocks_for((uint64_t)nb + 1, 256), 256, 0, st>>>(offA, nb, T1, np, npm);
     TC_LAUNCHED(ctx);
-    TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(d_scan, scan_bytes, np, offB, (int)(nb + 1), st));
-    ctx->launches += 2;
-    uint64_t bound = (items_bound + T1 - 1) / T1 + nb;
-    k_accum_xyzz<<<blocks_for(bound, 128), 128, 0, st>>>(itemsA, offA, offB, nb, T1, itemsB);
+    TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(d_scan, scan_bytes, np, toff, (int)(nb + 1), st));
+    TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(d_scan, scan_bytes, npm, offB, (int)(nb + 1), st));
+    ctx->launches += 4;
+    // every piece holds >= 1 item, and a multi-piece bucket of c >= 2 items yields
+    // ceil(c/T1) <= c items: both threads and the next level's items are <= items_bound
+    k_accum_xyzz<<<blocks_for(items_bound, 128), 128, 0, st>>>(itemsA, offA, toff, offB, nb, T1, itemsB, buckets);
     TC_LAUNCHED(ctx);
-    items_bound = bound;
     std::swap(offA, offB);
     std::swap(itemsA, itemsB);
   }
-  k_gather_buckets<<<blocks_for(nb, 256), 256, 0, st>>>(itemsA, offA, nb, buckets);
-  TC_LAUNCHED(ctx);
 
-  // 6-7. bucket reduction, window sums, Horner, affine
-  const uint32_t nw_total = (uint32_t)L * nwin;
-  // segment length: enough threads to cover the GPU, short running-sum chains
+  // 7-8. bucket reduction, window sums, Horner, affine
+  uint32_t minB = 1u << 30;
+  for (int w = 0; w < P.nwin; w++) minB = std::min<uint32_t>(minB, 1u << (P.width[w] - 1));
   uint32_t LS = 32u;
-  while (LS > 2u && (uint64_t)nw_total * B / LS < (uint64_t)ctx->num_sms * 256u) LS >>= 1;
-  LS = std::min<uint32_t>(B, LS);
-  const uint32_t nseg = B / LS;
+  while (LS > 2u && (uint64_t)nb / LS < (uint64_t)ctx->num_sms * 256u) LS >>= 1;
+  LS = std::min<uint32_t>(LS, minB);
+  const uint32_t nseg_total = nb / LS;
+  const uint32_t nw_total = (uint32_t)L * P.nwin;
   Xyzz *segs, *wsum;
-  TC_TRY(scratch_t(ctx, "msm.segs", (uint64_t)nw_total * nseg, &segs));
+  TC_TRY(scratch_t(ctx, "msm.segs", nseg_total, &segs));
   TC_TRY(scratch_t(ctx, "msm.wsum", nw_total, &wsum));
-  k_bucket_reduce<<<blocks_for((uint64_t)nw_total * nseg, 128), 128, 0, st>>>(buckets, B, nw_total, LS, segs);
+  k_bucket_reduce<<<blocks_for(nseg_total, 128), 128, 0, st>>>(buckets, P, nseg_total, LS, segs);
   TC_LAUNCHED(ctx);
-  k_window_sum<<<nw_total, 128, 0, st>>>(segs, nseg, wsum);
+  k_window_sum<<<nw_total, 128, 0, st>>>(segs, P, LS, wsum);
   TC_LAUNCHED(ctx);
-  k_final<<<blocks_for(L, 32), 32, 0, st>>>(wsum, (uint32_t)L, nwin, (uint32_t)c, d_out);
+  k_final<<<blocks_for(L, 32), 32, 0, st>>>(wsum, (uint32_t)L, P, d_out);
   TC_LAUNCHED(ctx);
   return TC_OK;
 }
