@@ -162,6 +162,125 @@ __global__ void __launch_bounds__(256) k_digits(const void* const* ptrs, uint64_
   }
 }
 
+// ---- bucket-major layout without a radix sort (few buckets per MSM) -------------------
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Pass A: one digit pass.  Per window, a warp reserves slots for its non-zero digits in
+// MSM l's private region (one atomic per warp) and lanes with equal bucket keys combine
+// their shared-memory histogram increments (__match_any_sync); the block's histogram is
+// flushed into the global per-bucket counts at the end.
+template <int DT>
+__global__ void __launch_bounds__(256) k_digits_hist(const void* const* ptrs, uint64_t n, int scale_bits, WinPlan P,
+                                                     uint32_t CH, uint64_t cap_l, uint32_t* keys, uint32_t* vals,
+                                                     uint32_t* lcount, uint32_t* gcount) {
+  extern __shared__ uint32_t hist[];   // P.nbm counters
+  const uint32_t l = blockIdx.y;
+  const uint64_t c0 = (uint64_t)blockIdx.x * CH;
+  const uint64_t c1 = (c0 + CH < n) ? c0 + CH : n;
+  const void* p = ptrs[l];
+  uint32_t* keys_l = keys + l * cap_l;
+  uint32_t* vals_l = vals + l * cap_l;
+  const uint32_t lane = threadIdx.x & 31, ltmask = lanemask_lt();
+  for (uint32_t b = threadIdx.x; b < P.nbm; b += blockDim.x) hist[b] = 0;
+  __syncthreads();
+  uint32_t f = 0;
+  for (uint64_t i0 = c0 + (threadIdx.x & ~31u); i0 < c1; i0 += blockDim.x) {   // warp-uniform trip count
+    const uint64_t i = i0 + lane;
+    const bool valid = i < c1;
+    Fe mag = Fp::zero();
+    bool neg = false;
+    if (valid) load_scalar<DT>(p, i, scale_bits, mag, neg, f);
+    uint32_t carry = 0;
+    for (int w = 0; w < P.nwin; w++) {
+      const int c = P.width[w];
+      const uint32_t half = 1u << (c - 1), full = 1u << c;
+      uint32_t d = window_bits(mag, P.off[w], c) + carry;
+      bool dn = false;
+      if (d > half) {
+        d = full - d;
+        dn = true;
+        carry = 1;
+      } else {
+        carry = 0;
+      }
+      const bool nz = valid && d != 0;
+      const uint32_t act = __ballot_sync(0xffffffffu, nz);
+      if (!act) continue;
+      uint32_t wbase = 0;
+      if (lane == (uint32_t)(__ffs(act) - 1)) wbase = atomicAdd(&lcount[l], (uint32_t)__popc(act));
+      wbase = __shfl_sync(0xffffffffu, wbase, __ffs(act) - 1);
+      if (nz) {
+        const uint32_t key = P.base[w] + d - 1u;
+        const uint32_t at = wbase + __popc(act & ltmask);
+        keys_l[at] = key;
+        vals_l[at] = (uint32_t)i | ((neg != dn) ? SIGN_BIT : 0u);
+        const uint32_t same = __match_any_sync(act, key);
+        if (lane == (uint32_t)(__ffs(same) - 1)) atomicAdd(&hist[key], (uint32_t)__popc(same));
+      }
+    }
+  }
+  if (f) atomicOr(lcount + gridDim.y, f);   // quantisation flags after the L counters
+  __syncthreads();
+  const uint32_t key0 = l * P.nbm;
+  for (uint32_t b = threadIdx.x; b < P.nbm; b += blockDim.x)
+    if (hist[b]) atomicAdd(&gcount[key0 + b], hist[b]);
+}
+
+// Pass B: a block takes a chunk of MSM l's entries, reserves a contiguous slice of every
+// bucket it touches (one global atomic per bucket) and scatters the values there (ranks
+// from warp-aggregated shared-memory atomics).  Order inside a bucket is arbitrary — EC
+// addition is commutative and the result canonical.
+__global__ void __launch_bounds__(256) k_scatter(const uint32_t* keys, const uint32_t* vals, uint64_t cap_l,
+                                                 const uint32_t* lcount, uint32_t CHB, uint32_t nbm,
+                                                 const uint32_t* bstart, uint32_t* gcursor, uint32_t* out) {
+  extern __shared__ uint32_t sh[];   // cnt[nbm], gpos[nbm]
+  uint32_t* cnt = sh;
+  uint32_t* gpos = sh + nbm;
+  const uint32_t l = blockIdx.y;
+  const uint32_t e0 = blockIdx.x * CHB, ecount = lcount[l];
+  if (e0 >= ecount) return;
+  const uint32_t e1 = min(e0 + CHB, ecount);
+  const uint32_t* keys_l = keys + l * cap_l;
+  const uint32_t* vals_l = vals + l * cap_l;
+  const uint32_t key0 = l * nbm, lane = threadIdx.x & 31, ltmask = lanemask_lt();
+  for (uint32_t b = threadIdx.x; b < nbm; b += blockDim.x) cnt[b] = 0;
+  __syncthreads();
+  for (uint32_t j0 = e0 + (threadIdx.x & ~31u); j0 < e1; j0 += blockDim.x) {
+    const uint32_t j = j0 + lane;
+    const bool valid = j < e1;
+    const uint32_t act = __ballot_sync(0xffffffffu, valid);
+    if (valid) {
+      const uint32_t key = keys_l[j];
+      const uint32_t same = __match_any_sync(act, key);
+      if (lane == (uint32_t)(__ffs(same) - 1)) atomicAdd(&cnt[key], (uint32_t)__popc(same));
+    }
+  }
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < nbm; b += blockDim.x) {
+    const uint32_t c = cnt[b];
+    gpos[b] = c ? bstart[key0 + b] + atomicAdd(&gcursor[key0 + b], c) : 0u;
+  }
+  __syncthreads();
+  for (uint32_t j0 = e0 + (threadIdx.x & ~31u); j0 < e1; j0 += blockDim.x) {
+    const uint32_t j = j0 + lane;
+    const bool valid = j < e1;
+    const uint32_t act = __ballot_sync(0xffffffffu, valid);
+    if (valid) {
+      const uint32_t key = keys_l[j];
+      const uint32_t same = __match_any_sync(act, key);
+      const uint32_t leader = __ffs(same) - 1;
+      uint32_t b0 = 0;
+      if (lane == leader) b0 = atomicAdd(&gpos[key], (uint32_t)__popc(same));
+      b0 = __shfl_sync(same, b0, leader);
+      out[b0 + __popc(same & ltmask)] = vals_l[j];
+    }
+  }
+}
+
 __global__ void k_bounds(const uint32_t* keys, const uint32_t* count, uint32_t* bstart, uint32_t* bend) {
   uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   uint32_t E = *count;
@@ -462,42 +581,84 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   TC_TRY(scratch_t(ctx, "msm.keys2", cap, &keys2));
   TC_TRY(scratch_t(ctx, "msm.vals2", cap, &vals2));
   uint32_t* d_count = d_small + NHIST + 2;
-  {
+  const uint32_t* svals;
+  uint32_t *bstart, *bend;
+  uint64_t E;
+  // Optional bucket-major layout by histogram + scatter instead of the radix sort
+  // (TC_MSM_BUCKETED=1).  Measured slower on config 3 (pass A 3.8 ms + scatter 2.8 ms vs
+  // digits 0.8 + onesweep 2.3 + bounds 0.4 ms): the per-layer slot counters and the
+  // __match_any_sync aggregation serialise; kept for small-bucket experiments.
+  static const bool want_bucketed = getenv("TC_MSM_BUCKETED") != nullptr;
+  const bool bucketed = want_bucketed && (size_t)P.nbm * 8 <= 160 * 1024;
+  if (bucketed) {
+    const uint32_t CH = 8192, CHB = 8192;
+    const uint64_t cap_l = n * P.nwin;
+    const uint32_t gx = (uint32_t)((n + CH - 1) / CH), gxb = (uint32_t)((cap_l + CHB - 1) / CHB);
+    uint32_t *lcount, *gcount, *gcursor, *sorted;
+    TC_TRY(scratch_t(ctx, "msm.lcount", (uint64_t)L + 1, &lcount));
+    TC_TRY(scratch_t(ctx, "msm.gcount", (uint64_t)nb + 1, &gcount));
+    TC_TRY(scratch_t(ctx, "msm.gcursor", (uint64_t)nb + 1, &gcursor));
+    TC_TRY(scratch_t(ctx, "msm.bstart", (uint64_t)nb + 1, &bstart));
+    TC_TRY(scratch_t(ctx, "msm.sorted", cap, &sorted));
+    TC_CUDA(ctx, cudaMemsetAsync(lcount, 0, ((uint64_t)L + 1) * sizeof(uint32_t), st));
+    TC_CUDA(ctx, cudaMemsetAsync(gcount, 0, ((uint64_t)nb + 1) * sizeof(uint32_t), st));
+    TC_CUDA(ctx, cudaMemsetAsync(gcursor, 0, ((uint64_t)nb + 1) * sizeof(uint32_t), st));
+    const size_t smemA = (size_t)P.nbm * 4, smemB = (size_t)P.nbm * 8;
     int s = dispatch_dt(ctx, dtype, [&](auto dt) {
-      k_digits<decltype(dt)::value><<<dim3(blocks_for(n, 256), L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, keys, vals,
-                                                                                  d_count);
+      auto kern = k_digits_hist<decltype(dt)::value>;
+      if (smemA > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemA);
+      kern<<<dim3(gx, L), 256, smemA, st>>>(d_ptrs, n, scale_bits, P, CH, cap_l, keys, vals, lcount, gcount);
     });
     if (s) return s;
     TC_LAUNCHED(ctx);
-  }
-  TC_CUDA(ctx, cudaMemcpyAsync(h_small, d_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-  TC_CUDA(ctx, cudaStreamSynchronize(st));
-  const uint64_t E = h_small[0];
-  if (E == 0) {
-    k_fill_inf<<<blocks_for(L, 64), 64, 0, st>>>(d_out, (uint32_t)L);
+    size_t sb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, sb, gcount, bstart, (int)(nb + 1), st);
+    void* d_sb;
+    TC_TRY(scratch(ctx, "msm.scantmp0", sb, &d_sb));
+    TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(d_sb, sb, gcount, bstart, (int)(nb + 1), st));
+    ctx->launches += 2;
+    if (smemB > 48 * 1024)
+      TC_CUDA(ctx, cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemB));
+    k_scatter<<<dim3(gxb, L), 256, smemB, st>>>(keys, vals, cap_l, lcount, CHB, P.nbm, bstart, gcursor, sorted);
     TC_LAUNCHED(ctx);
-    return TC_OK;
+    svals = sorted;
+    bend = bstart + 1;   // bucket k = [bstart[k], bstart[k+1])
+    E = cap;             // upper bound (no host readback of the entry count)
+  } else {
+    {
+      int s = dispatch_dt(ctx, dtype, [&](auto dt) {
+        k_digits<decltype(dt)::value><<<dim3(blocks_for(n, 256), L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, keys,
+                                                                                    vals, d_count);
+      });
+      if (s) return s;
+      TC_LAUNCHED(ctx);
+    }
+    TC_CUDA(ctx, cudaMemcpyAsync(h_small, d_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    TC_CUDA(ctx, cudaStreamSynchronize(st));
+    E = h_small[0];
+    if (E == 0) {
+      k_fill_inf<<<blocks_for(L, 64), 64, 0, st>>>(d_out, (uint32_t)L);
+      TC_LAUNCHED(ctx);
+      return TC_OK;
+    }
+    // 4. sort by bucket
+    size_t tmp_bytes = 0;
+    cub::DoubleBuffer<uint32_t> dk(keys, keys2), dv(vals, vals2);
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, dk, dv, (int)E, 0, end_bit, st);
+    void* d_tmp;
+    TC_TRY(scratch(ctx, "msm.cubtmp", tmp_bytes, &d_tmp));
+    TC_CUDA(ctx, cub::DeviceRadixSort::SortPairs(d_tmp, tmp_bytes, dk, dv, (int)E, 0, end_bit, st));
+    ctx->launches += 1 + (end_bit + 7) / 8;
+    const uint32_t* skeys = dk.Current();
+    svals = dv.Current();
+    // 5. bucket bounds
+    TC_TRY(scratch_t(ctx, "msm.bstart", (uint64_t)nb + 1, &bstart));
+    TC_TRY(scratch_t(ctx, "msm.bend", (uint64_t)nb + 1, &bend));
+    TC_CUDA(ctx, cudaMemsetAsync(bstart, 0, ((uint64_t)nb + 1) * sizeof(uint32_t), st));
+    TC_CUDA(ctx, cudaMemsetAsync(bend, 0, ((uint64_t)nb + 1) * sizeof(uint32_t), st));
+    k_bounds<<<blocks_for(E, 256), 256, 0, st>>>(skeys, d_count, bstart, bend);
+    TC_LAUNCHED(ctx);
   }
-
-  // 4. sort by bucket
-  size_t tmp_bytes = 0;
-  cub::DoubleBuffer<uint32_t> dk(keys, keys2), dv(vals, vals2);
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, dk, dv, (int)E, 0, end_bit, st);
-  void* d_tmp;
-  TC_TRY(scratch(ctx, "msm.cubtmp", tmp_bytes, &d_tmp));
-  TC_CUDA(ctx, cub::DeviceRadixSort::SortPairs(d_tmp, tmp_bytes, dk, dv, (int)E, 0, end_bit, st));
-  ctx->launches += 1 + (end_bit + 7) / 8;
-  const uint32_t* skeys = dk.Current();
-  const uint32_t* svals = dv.Current();
-
-  // 5. bucket bounds
-  uint32_t *bstart, *bend;
-  TC_TRY(scratch_t(ctx, "msm.bstart", (uint64_t)nb + 1, &bstart));
-  TC_TRY(scratch_t(ctx, "msm.bend", (uint64_t)nb + 1, &bend));
-  TC_CUDA(ctx, cudaMemsetAsync(bstart, 0, ((uint64_t)nb + 1) * sizeof(uint32_t), st));
-  TC_CUDA(ctx, cudaMemsetAsync(bend, 0, ((uint64_t)nb + 1) * sizeof(uint32_t), st));
-  k_bounds<<<blocks_for(E, 256), 256, 0, st>>>(skeys, d_count, bstart, bend);
-  TC_LAUNCHED(ctx);
 
   // 6. levels (a bucket holds <= n entries)
   const uint32_t T = (E >= (1u << 20)) ? 32u : (E >= (1u << 14) ? 16u : 8u);
@@ -539,7 +700,10 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     auto& s = ctx->stats["msm.accumulate"];
     s.ms += ms;
     s.launches += 1;
-    s.units += (double)E;
+    // entries actually accumulated = last bucket end (bucket starts are an exclusive scan)
+    uint32_t e_true = 0;
+    TC_CUDA(ctx, cudaMemcpy(&e_true, bend + nb - 1, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    s.units += (double)e_true;
   }
   uint64_t items_bound = max_items;
   for (int lv = 1; lv < levels; lv++) {
