@@ -57,7 +57,7 @@ def empty_limbs(n: int, device):
 def limbs_to_device(arr_np: np.ndarray, device):
     import torch
 
-    return torch.from_numpy(np.ascontiguousarray(arr_np).view(np.int32)).to(device)
+    return torch.from_numpy(np.array(arr_np, copy=True).view(np.int32)).to(device)
 
 
 def device_input(T, n: int, device):

@@ -551,6 +551,8 @@ int tc_srs_destroy(tc_srs* srs) {
   cudaSetDevice(srs->device);
   if (srs->monomial) cudaFree(srs->monomial);
   if (srs->lagrange) cudaFree(srs->lagrange);
+  for (auto* t : srs->small_tab)
+    if (t) cudaFree(t);
   delete srs;
   return TC_OK;
 }
@@ -619,6 +621,26 @@ static int fetch_encode_many(tc_ctx* ctx, const Aff* d_pts, int L, uint8_t* out4
   return TC_OK;
 }
 
+// L MSMs over the SRS's `which` elements: the fixed-base table kernel for small SRSs
+// (Terkle nodes), the batched Pippenger pipeline otherwise
+static int msm_srs(tc_ctx* ctx, const tc_srs* srs, int which, int dtype, int scale_bits, const void* const* ptrs,
+                   int L, Aff* d_out) {
+  const Aff* bases = (which == TC_SRS_LAGRANGE) ? srs->lagrange : srs->monomial;
+  if (!bases) return fail(ctx, TC_ERR_VALUE, "srs has no elements of kind %d", which);
+  if (srs->n > SMALL_MSM_MAX)
+    return tcrt::msm_batch_device(ctx, dtype, scale_bits, ptrs, L, bases, srs->n, d_out);
+  std::vector<const void*> fp(ptrs, ptrs + L);
+  if (dtype != TC_DTYPE_FP_LIMBS) {   // quantise first: the table kernel takes field elements
+    Fe* q;
+    TC_TRY(tcrt::scratch_t(ctx, "small.q_in", (uint64_t)L * srs->n, &q));
+    for (int i = 0; i < L; i++) {
+      TC_TRY(tcrt::quantize_device(ctx, ptrs[i], dtype, srs->n, scale_bits, q + (uint64_t)i * srs->n));
+      fp[i] = q + (uint64_t)i * srs->n;
+    }
+  }
+  return tcrt::small_msm_device(ctx, const_cast<tc_srs*>(srs), which, fp.data(), L, d_out);
+}
+
 // count tensors of the SRS shape in one batched MSM pipeline
 static int commit_many(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype, int scale_bits,
                        int route, uint8_t* out43) {
@@ -632,7 +654,7 @@ static int commit_many(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins,
   if (lag) {
     // C_T = sum_grid T[w] * g^{L_w(tau)}: no interpolation; the raw grid values (quantised
     // inside the digit kernel for float inputs) are the scalars
-    TC_TRY(tcrt::msm_batch_device(ctx, dtype, scale_bits, d_ins, count, srs->lagrange, n, d_out));
+    TC_TRY(msm_srs(ctx, srs, TC_SRS_LAGRANGE, dtype, scale_bits, d_ins, count, d_out));
   } else {
     // SPEC.md:279 verbatim: interpolate every tensor, then MSM over the monomial SRS
     Fe* coeffs;
@@ -648,7 +670,7 @@ static int commit_many(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins,
       TC_TRY(tcrt::interpolate_device(ctx, dst, srs->shape, srs->m));
       ptrs[i] = dst;
     }
-    TC_TRY(tcrt::msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, ptrs.data(), count, srs->monomial, n, d_out));
+    TC_TRY(msm_srs(ctx, srs, TC_SRS_MONOMIAL, TC_DTYPE_FP_LIMBS, 0, ptrs.data(), count, d_out));
   }
   return fetch_encode_many(ctx, d_out, count, out43);
 }
@@ -689,7 +711,7 @@ int tc_open(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int sca
   TC_TRY(tcrt::scratch_t(ctx, "open.out", (uint64_t)m, &d_out));
   std::vector<const void*> ptrs(m);
   for (int a = 0; a < m; a++) ptrs[a] = qs + (uint64_t)a * n;
-  TC_TRY(tcrt::msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, ptrs.data(), m, srs->monomial, n, d_out));
+  TC_TRY(msm_srs(ctx, srs, TC_SRS_MONOMIAL, TC_DTYPE_FP_LIMBS, 0, ptrs.data(), m, d_out));
   return fetch_encode_many(ctx, d_out, m, out_pi43);
 }
 
@@ -732,7 +754,8 @@ int tc_terkle_build(tc_ctx* ctx, const tc_srs* node_srs, const uint8_t* leaves_l
       ptrs[u] = z;
     }
     // every node of the level in one batched MSM
-    TC_TRY(tcrt::msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, ptrs.data(), (int)nodes, bases, B, d_out));
+    TC_TRY(msm_srs(ctx, node_srs, lag ? TC_SRS_LAGRANGE : TC_SRS_MONOMIAL, TC_DTYPE_FP_LIMBS, 0, ptrs.data(),
+                   (int)nodes, d_out));
     uint8_t* enc = out_nodes43 + 43 * written;
     TC_TRY(fetch_encode_many(ctx, d_out, (int)nodes, enc));
     std::vector<Fe> next(nodes);

@@ -1,0 +1,124 @@
+// Small fixed-base MSMs (Terkle node commitments, and the quotient MSMs of
+// node openings): L independent MSMs over an SRS of only B <= 64 points with full 162-bit
+// scalars.  Pippenger is the wrong tool here (its window-combination Horner is ~160
+// sequential doublings); instead every SRS point gets a byte-window table
+//     tab[k][w][j] = (j+1) * 2^{8w} * G_k        (21 windows x 255 entries, affine)
+// built once per SRS, and one warp per MSM sums the <= 21*B table entries selected by the
+// scalar bytes (mixed adds), reduces across lanes with shuffles and converts to affine.
+#include "tc_internal.cuh"
+
+using namespace tc;
+
+namespace {
+
+constexpr int SW = 21;    // byte windows (168 >= 162 bits)
+constexpr int SE = 255;   // non-zero byte values
+
+// Q[k][w] = 2^{8w} G_k  (one thread per point, sequential doublings)
+__global__ void k_tab_bases(const Aff* pts, uint32_t B, Xyzz* q) {
+  uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= B) return;
+  Xyzz acc = xyzz_from_aff(pts[k]);
+  for (int w = 0; w < SW; w++) {
+    q[k * SW + w] = acc;
+    for (int i = 0; i < 8; i++) acc = xyzz_dbl(acc);
+  }
+}
+
+// tab[k][w][j] = (j+1) Q[k][w]
+__global__ void k_tab_fill(const Xyzz* q, uint32_t B, Aff* tab) {
+  uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= B * SW * SE) return;
+  uint32_t j = t % SE + 1, kw = t / SE;
+  const Xyzz base = q[kw];
+  Xyzz acc = xyzz_inf();
+  for (int b = 7; b >= 0; b--) {
+    acc = xyzz_dbl(acc);
+    if ((j >> b) & 1u) xyzz_add(acc, base);
+  }
+  Aff r = xyzz_to_aff(acc);
+  if (!aff_is_inf(r)) r = Aff{Fq::canon(r.x), Fq::canon(r.y)};
+  tab[t] = r;
+}
+
+__device__ __forceinline__ Xyzz shfl_xyzz(const Xyzz& p, int src) {
+  Xyzz r;
+#pragma unroll
+  for (int i = 0; i < 6; i++) {
+    r.X.v[i] = __shfl_down_sync(0xffffffffu, p.X.v[i], src);
+    r.Y.v[i] = __shfl_down_sync(0xffffffffu, p.Y.v[i], src);
+    r.ZZ.v[i] = __shfl_down_sync(0xffffffffu, p.ZZ.v[i], src);
+    r.ZZZ.v[i] = __shfl_down_sync(0xffffffffu, p.ZZZ.v[i], src);
+  }
+  return r;
+}
+
+// one warp per MSM; scalars are canonical F_p limbs: ptrs[l][k], k < B
+__global__ void __launch_bounds__(128) k_small_msm(const Fe* const* ptrs, uint32_t L, uint32_t B, const Aff* tab,
+                                                   Aff* out) {
+  const uint32_t l = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (l >= L) return;   // whole warps exit together
+  const Fe* s = ptrs[l];
+  Xyzz acc = xyzz_inf();
+  for (uint32_t kw = lane; kw < B * SW; kw += 32) {
+    const uint32_t k = kw / SW, w = kw % SW;
+    const uint32_t byte = (s[k].v[w >> 2] >> (8 * (w & 3))) & 0xffu;
+    if (byte) xyzz_add_aff(acc, tab[(uint64_t)kw * SE + byte - 1]);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    Xyzz other = shfl_xyzz(acc, o);
+    if (lane < (uint32_t)o) xyzz_add(acc, other);
+  }
+  if (lane == 0) {
+    Aff r = xyzz_to_aff(acc);
+    if (!aff_is_inf(r)) r = Aff{Fq::canon(r.x), Fq::canon(r.y)};
+    out[l] = r;
+  }
+}
+
+}  // namespace
+
+namespace tcrt {
+
+// build (once) the byte-window tables of the SRS's `which` elements
+static int small_tables(tc_ctx* ctx, tc_srs* srs, int which, const Aff** out) {
+  const int idx = (which == TC_SRS_LAGRANGE) ? 1 : 0;
+  if (!srs->small_tab[idx]) {
+    const Aff* pts = idx ? srs->lagrange : srs->monomial;
+    if (!pts) return fail(ctx, TC_ERR_VALUE, "srs has no elements of kind %d", which);
+    const uint32_t B = (uint32_t)srs->n;
+    Xyzz* q;
+    TC_TRY(scratch_t(ctx, "small.q", (uint64_t)B * SW, &q));
+    Aff* tab = nullptr;
+    TC_CUDA(ctx, cudaMalloc(&tab, (size_t)B * SW * SE * sizeof(Aff)));
+    k_tab_bases<<<blocks_for(B, 32), 32, 0, ctx->stream>>>(pts, B, q);
+    TC_LAUNCHED(ctx);
+    k_tab_fill<<<blocks_for((uint64_t)B * SW * SE, 128), 128, 0, ctx->stream>>>(q, B, tab);
+    TC_LAUNCHED(ctx);
+    TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    srs->small_tab[idx] = tab;
+  }
+  *out = srs->small_tab[idx];
+  return TC_OK;
+}
+
+int small_msm_device(tc_ctx* ctx, tc_srs* srs, int which, const void* const* h_ptrs, int L, Aff* d_out) {
+  if (L <= 0) return TC_OK;
+  if (srs->n > ::SMALL_MSM_MAX) return fail(ctx, TC_ERR_VALUE, "small msm: srs too large");
+  const Aff* tab;
+  TC_TRY(small_tables(ctx, srs, which, &tab));
+  const Fe** d_ptrs;
+  TC_TRY(scratch_t(ctx, "small.ptrs", (uint64_t)L, (Fe***)&d_ptrs));
+  memcpy(ctx->h_stage, h_ptrs, sizeof(void*) * L);
+  TC_CUDA(ctx, cudaMemcpyAsync(d_ptrs, ctx->h_stage, sizeof(void*) * L, cudaMemcpyHostToDevice, ctx->stream));
+  k_small_msm<<<blocks_for((uint64_t)L * 32, 128), 128, 0, ctx->stream>>>(d_ptrs, (uint32_t)L, (uint32_t)srs->n, tab,
+                                                                          d_out);
+  TC_LAUNCHED(ctx);
+  // the pointer upload reads h_stage asynchronously: finish before h_stage is reused
+  TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return TC_OK;
+}
+
+}  // namespace tcrt

@@ -46,7 +46,11 @@ struct tc_srs {
   tc::Aff* monomial = nullptr;   // N affine points, Montgomery form, lex order
   tc::Aff* lagrange = nullptr;   // N affine points g^{L_i(tau)} (optional)
   tc::Aff axis[TC_MAX_AXES];     // g^{tau_j} (host copy)
+  tc::Aff* small_tab[2] = {nullptr, nullptr};   // byte-window tables (monomial, Lagrange), n <= 64
 };
+
+// SRS sizes up to this many points use the fixed-base small-MSM kernel (small_msm.cu)
+constexpr uint64_t SMALL_MSM_MAX = 64;
 
 namespace tcrt {
 
@@ -104,6 +108,10 @@ int msm_device(tc_ctx* ctx, ScalarKind kind, const void* d_scalars, const tc::Af
 // canonical limbs; float dtypes are quantised at scale_bits inside the digit kernel).
 int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* h_ptrs, int L,
                      const tc::Aff* d_bases, uint64_t n, tc::Aff* d_out);
+
+// L MSMs over a small SRS (n <= SMALL_MSM_MAX) with canonical F_p scalars, via per-point
+// byte-window tables built once per SRS (`which` = TC_SRS_MONOMIAL | TC_SRS_LAGRANGE)
+int small_msm_device(tc_ctx* ctx, tc_srs* srs, int which, const void* const* h_ptrs, int L, tc::Aff* d_out);
 
 // fixed-base batch: out[i] = e_i * g for canonical F_p exponents e (device arrays)
 int fixed_base_g(tc_ctx* ctx, const tc::Fe* d_exps, uint64_t n, tc::Aff* d_out);
