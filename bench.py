@@ -1,17 +1,20 @@
-"""Benchmark of the TensorCommitments prover hot path on B200 (BASELINE.json config 3).
+"""Benchmark of the TensorCommitments prover hot path on B200.
 
-One step = the per-forward prover work of config 3: 32 layers of LLaMA-2-7B-shaped
-hidden states [1, 512, 4096] fp16 are quantised, committed (m = 4 grid (32,32,32,64))
-and organised into a 32-leaf Terkle tree (node shape (2,2,2)).  With --gpus N the layers
-are partitioned over N ranks (strong scaling) and the commitments all-gathered once.
+Default workload = BASELINE.json config 3 (the one the "prover overhead % vs 7B-shape
+forward" metric is quoted on): 32 layers of LLaMA-2-7B-shaped hidden states
+[1, 512, 4096] fp16 are quantised, committed (m = 4 grid (32,32,32,64)) and organised into
+a 32-leaf Terkle tree (node shape (2,2,2)).  One step = one forward's prover work.  With
+--gpus N (torchrun) the layers are partitioned over the ranks (strong scaling) and the
+43-byte commitments all-gathered once.  `--config 5` runs the LLaMA-2-13B-shaped config
+(40 layers [4,2048,5120], grid (64,128,64,80)); `--config 4` times batched openings.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 3|4|5]
 
 Prints ONE JSON line (rank 0).  `value` = field elements committed per second with the
 activations resident in HBM; `e2e` = the same through the public API with the inputs
 copied from pinned host memory and the commitments / root read back every step.
-`--impl reference` times the CPU reference path (the oracle's restatement of the
-reference's CPython arithmetic) on this host's cores over a bounded sample.
+`--impl reference` times the CPU reference path (the oracle's CPython restatement of the
+reference's arithmetic) on this host's cores over a bounded sample.
 """
 from __future__ import annotations
 
@@ -28,22 +31,46 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "field elems committed/sec; prover overhead % vs 7B-shape forward"
-N_LAYERS, SEQ, HIDDEN = 32, 512, 4096
-SHAPE = (32, 32, 32, 64)
-NODE_SHAPE = (2, 2, 2)
 WORD_MULS_PER_ADD = 11 * 78   # 11 F_q mulmods per EC add, 78 word multiplies each
-WORKLOAD = ("config3: 32 layers x [1,512,4096] fp16 Student-t(3) x U(0.5,4) per layer, m=4 grid "
-            "(32,32,32,64), 32-leaf Terkle tree node shape (2,2,2)")
+NODE_SHAPE = (2, 2, 2)
+CONFIGS = {
+    3: dict(layers=32, act=(1, 512, 4096), shape=(32, 32, 32, 64),
+            name="config3: 32 layers x [1,512,4096] fp16 Student-t(3) x U(0.5,4) per layer, m=4 grid "
+                 "(32,32,32,64), 32-leaf Terkle tree node shape (2,2,2)"),
+    5: dict(layers=40, act=(4, 2048, 5120), shape=(64, 128, 64, 80),
+            name="config5: 40 layers x [4,2048,5120] fp16 Student-t(3) x U(0.5,4) per layer, m=4 grid "
+                 "(64,128,64,80), 40-leaf Terkle tree node shape (2,2,2)"),
+}
 
 
-def make_layers(layer_ids):
-    """Seeded config-3 activations (host fp16): layer l = default_rng(l) t(3) * scale_l."""
+def layer_scales(n_layers):
     import numpy as np
-    scales = np.random.default_rng(12345).uniform(0.5, 4.0, N_LAYERS)
+    return np.random.default_rng(12345).uniform(0.5, 4.0, n_layers)
+
+
+def make_layers_host(cfg, layer_ids):
+    """Seeded activations (host fp16): layer l = default_rng(l) standard_t(3) * scale_l."""
+    import numpy as np
+    scales = layer_scales(cfg["layers"])
+    n = int(np.prod(cfg["act"]))
     out = []
     for l in layer_ids:
-        x = np.random.default_rng(l).standard_t(3, size=SEQ * HIDDEN) * scales[l]
-        out.append(x.astype(np.float16).reshape(1, SEQ, HIDDEN))
+        x = np.random.default_rng(l).standard_t(3, size=n) * scales[l]
+        out.append(x.astype(np.float16).reshape(cfg["act"]))
+    return out
+
+
+def make_layers_device(cfg, layer_ids, dev):
+    """Config 5 is 1.7e9 values: generated on the GPU (torch Philox, seeded per layer)."""
+    import torch
+    scales = layer_scales(cfg["layers"])
+    out = []
+    for l in layer_ids:
+        g = torch.Generator(device=dev).manual_seed(1000 + l)
+        z = torch.randn(cfg["act"], generator=g, device=dev, dtype=torch.float32)
+        # Student-t(3) = Z / sqrt(chi2_3 / 3), chi2_3 = sum of 3 squared normals
+        c = sum(torch.randn(cfg["act"], generator=g, device=dev, dtype=torch.float32) ** 2 for _ in range(3))
+        out.append((z / torch.sqrt(c / 3.0) * float(scales[l])).to(torch.float16))
     return out
 
 
@@ -62,6 +89,7 @@ class Clocks:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            time.sleep(0.3)   # first sample lands before the timed region
         except OSError:
             self.proc = None
         return self
@@ -74,6 +102,7 @@ class Clocks:
 
     def __exit__(self, *a):
         if self.proc:
+            time.sleep(0.15)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -83,8 +112,9 @@ class Clocks:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        num = lambda s: s.replace(".", "").isdigit()
+        sm = [float(s[0]) for s in self.samples if num(s[0])]
+        mx = [float(s[1]) for s in self.samples if num(s[1])]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
@@ -138,8 +168,8 @@ def forward_ms(device):
 
 # ------------------------------------------------------------------ CPU reference leg
 def _cpu_task(args):
-    """Reference CPU path on K elements: Lagrange fibre transforms (mvpoly.py:193-228)
-    worth K elements of config-3 interpolation, then a naive MSM (fold of exp + mul,
+    """Reference CPU path on K elements: the Lagrange fibre transforms (mvpoly.py:193-228)
+    worth K elements of config-3 interpolation, then the naive MSM (fold of exp + mul,
     backend.py:185-217) over K coefficients with the real SRS points."""
     fibres, coeffs, bases = args
     from oracle import tc_oracle as O
@@ -156,28 +186,30 @@ def _cpu_task(args):
     return time.perf_counter() - t0
 
 
-def cpu_reference(sample_elems, layer0_q, coeffs, bases, cores, rounds=1):
-    """Throughput (elems/s) of the reference CPU path on `cores` processes."""
+def cpu_reference(shape, layer0_q, coeffs, bases, cores, target_s=12.0):
+    """Throughput (elems/s) of the reference CPU path on `cores` processes, sized to
+    ~target_s of wall time.  Returns (elems/s, wall seconds, tasks, K)."""
     import multiprocessing as mp
     K = len(coeffs)
-    # interpolation work attributable to K elements: each element costs d_j MACs per axis
     fibres = []
-    for j, d in enumerate(SHAPE):
-        nfib = max(1, K // d)
+    for j, d in enumerate(shape):
         stride = 1
-        for dd in SHAPE[j + 1:]:
+        for dd in shape[j + 1:]:
             stride *= dd
-        for f in range(nfib):
+        for f in range(max(1, K // d)):
             fibres.append((d, [layer0_q[(f * stride * d + r * stride) % len(layer0_q)] for r in range(d)]))
-    tasks = [(fibres, coeffs, bases)] * (cores * rounds)
-    t0 = time.perf_counter()
+    task = (fibres, coeffs, bases)
     with mp.get_context("fork").Pool(cores) as pool:
-        pool.map(_cpu_task, tasks)
-    wall = time.perf_counter() - t0
-    return K * len(tasks) / wall, wall
+        one = max(pool.map(_cpu_task, [task] * cores))          # calibration round (untimed)
+        rounds = max(1, int(target_s / max(one, 1e-3)))
+        t0 = time.perf_counter()
+        pool.map(_cpu_task, [task] * (cores * rounds))
+        wall = time.perf_counter() - t0
+    n_tasks = cores * rounds
+    return K * n_tasks / wall, wall, n_tasks, K
 
 
-def cpu_sample_inputs(K=48):
+def cpu_sample_inputs(cfg, K=48):
     """First K elements of layer 0: quantised values, GPU-interpolated coefficients and the
     matching monomial SRS points (one-time setup, not timed)."""
     import numpy as np
@@ -185,9 +217,9 @@ def cpu_sample_inputs(K=48):
 
     import paper_2602_12630_b200 as tcb
     from oracle import tc_oracle as O
-    x = make_layers([0])[0].reshape(-1)
+    x = make_layers_host(CONFIGS[3], [0])[0].reshape(-1)
     q = O.quantize(x.astype(np.float64), 16)
-    srs, _ = tcb.setup_srs(SHAPE, b"tc-b200/config3", lagrange=False)
+    srs, _ = tcb.setup_srs(CONFIGS[3]["shape"], b"tc-b200/config3", lagrange=False)
     f = tcb.interpolate_lagrange(tcb.PrimeField(), tcb.quantize(torch.from_numpy(x).cuda()), srs.grid)
     bases = srs.export_range(1, 0, K)
     return q, list(f.coeffs[:K]), list(bases)
@@ -200,12 +232,13 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=3, choices=[3, 4, 5])
     ap.add_argument("--route", default="lagrange", choices=["lagrange", "monomial"])
     ap.add_argument("--no-forward", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-monomial", action="store_true", help="skip the secondary monomial-route step")
     args = ap.parse_args()
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -217,34 +250,20 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    cfg = CONFIGS[5 if args.config == 5 else 3]
+    shape = cfg["shape"]
 
     if args.impl == "reference":
-        if rank != 0:
-            if world > 1:
-                dist.barrier()
-                dist.destroy_process_group()
-            return
-        q, coeffs, bases = cpu_sample_inputs()
-        for _ in range(args.warmup):
-            cpu_reference(len(coeffs), q, coeffs, bases, cores)
-        vals, walls = [], []
-        for _ in range(args.steps):
-            v, w = cpu_reference(len(coeffs), q, coeffs, bases, cores)
-            vals.append(v)
-            walls.append(w)
-        value = sum(len(coeffs) * cores for _ in vals) / sum(walls)
-        sample = (f"{cores} processes x {len(coeffs)} elements of layer 0 per step: config-3 Lagrange fibre "
-                  f"transforms worth those elements + naive exp/mul MSM over their coefficients "
-                  f"(oracle restatement of the reference CPython path)")
-        line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "elems/s", "n_gpus": world,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(walls),
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int (CPython big int)",
-                "data": "synthetic", "config": {"workload": WORKLOAD, "parallelism": f"cpu x{cores}"},
-                "cpu_baseline": {"value": value, "unit": "elems/s", "cores": cores, "kind": "port", "sample": sample},
-                "e2e": {"value": value, "unit": "elems/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
+        if rank == 0:
+            run_reference(args, cfg, cores, world)
         if world > 1:
             dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    if args.config == 4:
+        run_openings(args, dev, rank, world)
+        if world > 1:
             dist.destroy_process_group()
         return
 
@@ -252,24 +271,31 @@ def main():
     from paper_2602_12630_b200 import _lib
     from paper_2602_12630_b200.dist import allgather_commitments, layer_partition
 
-    my_layers = layer_partition(N_LAYERS, rank, world)
-    host = make_layers(my_layers)
-    host_pinned = [torch.from_numpy(h).pin_memory() for h in host]
-    dev_layers = [h.to(dev) for h in host_pinned]
+    n_layers = cfg["layers"]
+    my_layers = layer_partition(n_layers, rank, world)
+    if args.config == 5:
+        dev_layers = make_layers_device(cfg, my_layers, dev)
+        host_pinned = [d.cpu().pin_memory() for d in dev_layers]
+    else:
+        host_pinned = [torch.from_numpy(h).pin_memory() for h in make_layers_host(cfg, my_layers)]
+        dev_layers = [h.to(dev) for h in host_pinned]
     staging = [torch.empty_like(d) for d in dev_layers]
-    srs, _ = tcb.setup_srs(SHAPE, b"tc-b200/config3", device=local)
-    cfg = tcb.TreeConfig(shape=NODE_SHAPE)
-    node_srs = tcb.authtree.node_srs(cfg, device=local)
+    srs, _ = tcb.setup_srs(shape, b"tc-b200/config%d" % (5 if args.config == 5 else 3), device=local)
+    tcfg = tcb.TreeConfig(shape=NODE_SHAPE)
+    node_srs = tcb.authtree.node_srs(tcfg, device=local)
     ctx = _lib.Context.get(local)
-    per_step_elems = N_LAYERS * SEQ * HIDDEN
+    elems_per_layer = 1
+    for d in cfg["act"]:
+        elems_per_layer *= d
+    per_step_elems = n_layers * elems_per_layer
 
-    def prove_step(layers):
-        comms = tcb.tc_commit_many(srs, layers, route=args.route)
+    def prove_step(layers, route=args.route):
+        comms = tcb.tc_commit_many(srs, layers, route=route)
         encs = [c.to_bytes() for c in comms]
         if world > 1:
-            encs = allgather_commitments(encs, N_LAYERS, rank, world, device=dev)
+            encs = allgather_commitments(encs, n_layers, rank, world, device=dev)
         leaves = [tcb.hash_to_scalar(e, b"terkle/leaf") for e in encs]
-        tree, root = tcb.build(cfg, leaves, srs=node_srs)
+        tree, root = tcb.build(tcfg, leaves, srs=node_srs)
         return root
 
     def e2e_step():
@@ -302,7 +328,8 @@ def main():
     with Clocks(local) as clk:
         ms, launches, root = timed(lambda: prove_step(dev_layers), args.steps)
     ms_e2e, _, root_e2e = timed(e2e_step, args.steps)
-    assert root_e2e == root
+    if root_e2e != root:
+        raise RuntimeError("e2e root differs from the device-resident root")
 
     # dominant kernel: Pippenger bucket accumulation, CUDA events on the ctx stream
     ctx.set_profiling(True)
@@ -314,28 +341,38 @@ def main():
     ctx.check(_lib.lib().tc_measure_imad_peak(ctx.handle, ctypes.byref(peak)))
     peak_tops = peak.value
 
+    # secondary: the monomial route (interpolate -> 162-bit-scalar MSM, SPEC.md:279 verbatim)
+    mono = None
+    if not args.no_monomial and args.route == "lagrange" and args.config == 3:
+        prove_step(dev_layers, route="monomial")
+        m_ms, _, m_root = timed(lambda: prove_step(dev_layers, route="monomial"), 1)
+        if m_root != root:
+            raise RuntimeError("monomial route root differs from the Lagrange route")
+        mono = {"ms_per_step": m_ms, "elems_per_s": per_step_elems / (m_ms / 1e3), "root_equal": True}
+
     ms_step = ms / args.steps
     value = per_step_elems / (ms_step / 1e3)
     value_e2e = per_step_elems / (ms_e2e / args.steps / 1e3)
     achieved = st["units"] * WORD_MULS_PER_ADD / (st["ms"] * 1e-3) / 1e12 if st["ms"] else None
 
-    fwd = None if (args.no_forward or rank != 0) else forward_ms(dev)
+    fwd = None if (args.no_forward or rank != 0 or args.config != 3) else forward_ms(dev)
     cpu = None
     if rank == 0 and not args.no_cpu:
-        q, coeffs, bases = cpu_sample_inputs()
-        v, wall = cpu_reference(len(coeffs), q, coeffs, bases, cores)
+        q, coeffs, bases = cpu_sample_inputs(cfg)
+        v, wall, ntask, K = cpu_reference(CONFIGS[3]["shape"], q, coeffs, bases, cores)
         cpu = {"value": v, "unit": "elems/s", "cores": cores, "kind": "port",
-               "sample": f"{cores} processes x {len(coeffs)} elements of layer 0 (Lagrange fibre transforms + "
-                         f"naive exp/mul MSM; oracle restatement of the reference CPython path), {wall:.1f} s"}
+               "sample": f"{ntask} tasks x {K} elements of config-3 layer 0 on {cores} processes ({wall:.1f} s): "
+                         f"Lagrange fibre transforms worth those elements + naive exp/mul MSM over their "
+                         f"coefficients (oracle restatement of the reference CPython path)"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "elems/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32 (6-limb F_p/F_q Montgomery); input fp16", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "route": args.route, "elems_per_step": per_step_elems,
-                       "parallelism": f"layers/{world}", "l2": "no flush: fp16 inputs 128 MiB + SRS 96 MiB exceed "
-                       "the 126 MB L2", "srs": "generated once before timing (trusted setup)"},
+            "config": {"workload": cfg["name"], "route": args.route, "elems_per_step": per_step_elems,
+                       "parallelism": f"layers/{world}", "l2": "no flush: fp16 inputs (>=128 MiB) + SRS (96 MiB) "
+                       "exceed the 126 MB L2", "srs": "generated once before timing (trusted setup)"},
             "overhead_pct": (100.0 * ms_step / fwd) if fwd else None,
             "forward_ms": fwd,
             "e2e": {"value": value_e2e, "unit": "elems/s", "ms_per_step": ms_e2e / args.steps,
@@ -349,6 +386,7 @@ def main():
                                  f"(11 mulmods x 78) over {st['launches']} launches, {st['ms']:.3f} ms",
                          "peak_source": "mad.lo.u32 microbenchmark in this run (tc_measure_imad_peak)",
                          "share_of_step": st["ms"] / ms_step if ms_step else None},
+            "monomial_route": mono,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "root": root.to_bytes().hex(),
@@ -357,6 +395,63 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_reference(args, cfg, cores, world):
+    q, coeffs, bases = cpu_sample_inputs(cfg)
+    for _ in range(max(0, min(args.warmup, 1))):
+        cpu_reference(CONFIGS[3]["shape"], q, coeffs, bases, cores, target_s=2.0)
+    vals, walls, tasks = [], [], 0
+    for _ in range(args.steps):
+        v, w, nt, K = cpu_reference(CONFIGS[3]["shape"], q, coeffs, bases, cores, target_s=6.0)
+        vals.append(v)
+        walls.append(w)
+        tasks += nt
+    value = tasks * len(coeffs) / sum(walls)
+    sample = (f"{tasks} tasks x {len(coeffs)} elements of config-3 layer 0 on {cores} processes: Lagrange fibre "
+              f"transforms worth those elements + naive exp/mul MSM over their coefficients (oracle restatement "
+              f"of the reference CPython path)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "elems/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(walls),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int (CPython big int)",
+            "data": "synthetic", "config": {"workload": cfg["name"], "parallelism": f"cpu x{cores}"},
+            "cpu_baseline": {"value": value, "unit": "elems/s", "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "elems/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_openings(args, dev, rank, world):
+    """Config 4: batched opening proofs on the config-3 tree — 256 seeded challenges spread
+    over layers by a heavy-tailed score vector; each is tc_open (quotients + MSM) plus a
+    Terkle membership proof.  Reports openings/s (correctness: tests/test_gpu_parity.py)."""
+    import random
+
+    import numpy as np
+    import torch
+
+    import paper_2602_12630_b200 as tcb
+    cfg = CONFIGS[3]
+    layers_host = make_layers_host(cfg, range(cfg["layers"]))
+    layers = [torch.from_numpy(h).to(dev) for h in layers_host]
+    srs, _ = tcb.setup_srs(cfg["shape"], b"tc-b200/config3", device=dev.index)
+    comms, root, tree = tcb.prover_commit(layers, srs)
+    score = np.random.default_rng(4).pareto(1.5, cfg["layers"]) + 1e-3
+    picks = np.random.default_rng(5).choice(cfg["layers"], size=256, p=score / score.sum())
+    rng = random.Random(6)
+    chals = [(int(l), [rng.randrange(tcb.P) for _ in cfg["shape"]]) for l in picks]
+    for l, pt in chals[:2]:
+        tcb.tc_open(srs, layers[l], pt)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for l, pt in chals:
+        tcb.tc_open(srs, layers[l], pt)
+        tcb.prove(tree, l)
+    torch.cuda.synchronize(dev)
+    wall = time.perf_counter() - t0
+    print(json.dumps({"metric": "opening proofs/sec (tc_open + Terkle membership proof)", "value": len(chals) / wall,
+                      "unit": "openings/s", "n_gpus": 1, "ms_per_opening": 1e3 * wall / len(chals),
+                      "config": {"workload": "config4: 256 challenges on the config-3 tree, layers drawn by a seeded "
+                                 "Pareto score vector, random field points"}}), flush=True)
 
 
 if __name__ == "__main__":

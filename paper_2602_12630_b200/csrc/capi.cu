@@ -657,20 +657,25 @@ static int commit_many(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins,
     TC_TRY(msm_srs(ctx, srs, TC_SRS_LAGRANGE, dtype, scale_bits, d_ins, count, d_out));
   } else {
     // SPEC.md:279 verbatim: interpolate every tensor, then MSM over the monomial SRS
+    // groups of layers bound the coefficient scratch (config 5: 1 layer = 41.9M elements)
+    const int G = (int)std::max<uint64_t>(1, (1ull << 24) / n);
     Fe* coeffs;
-    TC_TRY(tcrt::scratch_t(ctx, "commit.coeffs", (uint64_t)count * n, &coeffs));
-    std::vector<const void*> ptrs(count);
-    for (int i = 0; i < count; i++) {
-      Fe* dst = coeffs + (uint64_t)i * n;
-      if (dtype == TC_DTYPE_FP_LIMBS) {
-        TC_CUDA(ctx, cudaMemcpyAsync(dst, d_ins[i], n * sizeof(Fe), cudaMemcpyDeviceToDevice, ctx->stream));
-      } else {
-        TC_TRY(tcrt::quantize_device(ctx, d_ins[i], dtype, n, scale_bits, dst));
+    TC_TRY(tcrt::scratch_t(ctx, "commit.coeffs", (uint64_t)std::min(G, count) * n, &coeffs));
+    for (int g0 = 0; g0 < count; g0 += G) {
+      const int gc = std::min(G, count - g0);
+      std::vector<const void*> ptrs(gc);
+      for (int i = 0; i < gc; i++) {
+        Fe* dst = coeffs + (uint64_t)i * n;
+        if (dtype == TC_DTYPE_FP_LIMBS) {
+          TC_CUDA(ctx, cudaMemcpyAsync(dst, d_ins[g0 + i], n * sizeof(Fe), cudaMemcpyDeviceToDevice, ctx->stream));
+        } else {
+          TC_TRY(tcrt::quantize_device(ctx, d_ins[g0 + i], dtype, n, scale_bits, dst));
+        }
+        TC_TRY(tcrt::interpolate_device(ctx, dst, srs->shape, srs->m));
+        ptrs[i] = dst;
       }
-      TC_TRY(tcrt::interpolate_device(ctx, dst, srs->shape, srs->m));
-      ptrs[i] = dst;
+      TC_TRY(msm_srs(ctx, srs, TC_SRS_MONOMIAL, TC_DTYPE_FP_LIMBS, 0, ptrs.data(), gc, d_out + g0));
     }
-    TC_TRY(msm_srs(ctx, srs, TC_SRS_MONOMIAL, TC_DTYPE_FP_LIMBS, 0, ptrs.data(), count, d_out));
   }
   return fetch_encode_many(ctx, d_out, count, out43);
 }

@@ -529,6 +529,19 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     TC_LAUNCHED(ctx);
     return TC_OK;
   }
+  // bound the scratch of one pipeline: at most 2^26 quantised floats (<= 3-4 windows) or
+  // 2^24 full field elements (~14 windows) per batch; larger batches run in groups
+  {
+    const uint64_t per = (dtype == TC_DTYPE_FP_LIMBS) ? (1ull << 24) : (1ull << 26);
+    const uint64_t G = std::max<uint64_t>(1, per / n);
+    if ((uint64_t)L > G) {
+      for (int l0 = 0; l0 < L; l0 += (int)G) {
+        const int cnt = (int)std::min<uint64_t>(G, (uint64_t)(L - l0));
+        TC_TRY(msm_batch_device(ctx, dtype, scale_bits, h_ptrs + l0, cnt, d_bases, n, d_out + l0));
+      }
+      return TC_OK;
+    }
+  }
   // scalar pointers -> device (pinned staging; the syncs below keep it alive)
   const void** d_ptrs;
   TC_TRY(scratch_t(ctx, "msm.ptrs", (uint64_t)L, (void***)&d_ptrs));
@@ -700,9 +713,10 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     auto& s = ctx->stats["msm.accumulate"];
     s.ms += ms;
     s.launches += 1;
-    // entries actually accumulated = last bucket end (bucket starts are an exclusive scan)
-    uint32_t e_true = 0;
-    TC_CUDA(ctx, cudaMemcpy(&e_true, bend + nb - 1, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    // entries actually accumulated (the bucketed path only has the capacity bound on the
+    // host; its bucket starts are an exclusive scan, so bstart[nb] is the true count)
+    uint32_t e_true = (uint32_t)E;
+    if (bucketed) TC_CUDA(ctx, cudaMemcpy(&e_true, bstart + nb, sizeof(uint32_t), cudaMemcpyDeviceToHost));
     s.units += (double)e_true;
   }
   uint64_t items_bound = max_items;
