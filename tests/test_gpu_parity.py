@@ -247,3 +247,59 @@ def test_prover_commit_small_layers():
     t2[17] += 1.0
     _, root_c, _ = tcb.prover_commit([tensors[0], t2, tensors[2]], srs)
     assert root_c != root
+
+
+# ---------------------------------------------------------------- full-size configs
+def _config3_layer(l):
+    scales = np.random.default_rng(12345).uniform(0.5, 4.0, 32)
+    return (np.random.default_rng(l).standard_t(3, size=512 * 4096) * scales[l]).astype(np.float16)
+
+
+def test_config4_openings_full_size_trapdoor():
+    """Config 4 at full size: openings of a config-3 layer at random field points equal the
+    trapdoor oracle (y and every pi_i), and verify on the CPU verifier."""
+    tcb = T()
+    shape = (32, 32, 32, 64)
+    srs, td = tcb.setup_srs(shape, b"tc-b200/config3")
+    x = _config3_layer(5)
+    t = torch.from_numpy(x).cuda()
+    vals = O.quantize(x.astype(np.float64), 16)
+    C = tcb.tc_commit(srs, t)
+    assert C.elem == O.commit_trapdoor(vals, shape, list(td.taus))
+    rng = random.Random(11)
+    pt = [rng.randrange(O.P) for _ in shape]
+    op = tcb.tc_open(srs, t, pt)
+    y, proofs = O.open_trapdoor(vals, shape, list(td.taus), pt)
+    assert op.y == y and list(op.proofs) == proofs
+    assert tcb.tc_verify(srs, C, pt, op)
+    assert not tcb.tc_verify(srs, C, pt, tcb.TensorOpening(op.y, (op.proofs[1], op.proofs[0]) + op.proofs[2:]))
+
+
+def test_config3_prover_commit_subset_and_tree():
+    """Config-3 prover_commit on 4 full layers: every commitment equals the trapdoor oracle and
+    the Terkle root equals the oracle tree over the oracle's leaves."""
+    tcb = T()
+    shape = (32, 32, 32, 64)
+    srs, td = tcb.setup_srs(shape, b"tc-b200/config3")
+    xs = [_config3_layer(l) for l in range(4)]
+    comms, root, tree = tcb.prover_commit([torch.from_numpy(x).cuda() for x in xs], srs)
+    want = [O.commit_trapdoor(O.quantize(x.astype(np.float64), 16), shape, list(td.taus)) for x in xs]
+    assert [c.elem for c in comms] == want
+    node = tcb.authtree.node_srs(tcb.TreeConfig())
+    node_elems = list(node.monomial_elems)
+    levels, _ = O.terkle_build([O.leaf_of_commitment(c) for c in want], (2, 2, 2),
+                               lambda z: O.tc_commit(node_elems, z, (2, 2, 2)))
+    assert root.elem == levels[-1][0]
+
+
+@pytest.mark.slow
+def test_config5_layer_trapdoor():
+    """One full config-5 layer (41,943,040 fp16 elements, grid (64,128,64,80)) on both routes."""
+    tcb = T()
+    shape = (64, 128, 64, 80)
+    srs, td = tcb.setup_srs(shape, b"tc-b200/config5")
+    x = (np.random.default_rng(7).standard_t(3, size=4 * 2048 * 5120) * 2.0).astype(np.float16)
+    t = torch.from_numpy(x).cuda()
+    want = O.commit_trapdoor(O.quantize(x.astype(np.float64), 16), shape, list(td.taus))
+    assert tcb.tc_commit(srs, t, route="lagrange").elem == want
+    assert tcb.tc_commit(srs, t, route="monomial").elem == want
