@@ -409,6 +409,65 @@ __global__ void __launch_bounds__(128) k_window_sum(const Xyzz* segs, WinPlan P,
   if (threadIdx.x == 0) wsum[blockIdx.x] = sh[0];
 }
 
+// ---- weighted bucket sums A_g = sum_j (j+1) x_j by recursive segmentation ----------------
+// Split each group into segments of SEG items: per segment k, T_k = sum x_j and
+// U_k = sum (j - SEG k + 1) x_j (running sums).  Then
+//     A(x) = sum_k U_k + SEG * sum_k k T_k = sum_k U_k + SEG * A(T) - SEG * S,
+// S = sum x.  Recursing on T (SEG x fewer items per level) and carrying
+//     D = sum_{levels r} SEG^{r-1} sum_k U_{r,k}
+// in a second stream gives, after R levels (every group reduced to one item, T = S),
+//     A(x) = D - S * (SEG^R - SEG) / (SEG - 1).
+// No per-segment scalar multiplications and SEG x more parallelism than one thread per
+// window; every level is one launch over all groups of the batch.
+constexpr uint32_t SEG = 8;
+
+struct GroupTab {   // per group: input offset, input count, output offset (device)
+  const uint32_t* in_off;
+  const uint32_t* in_cnt;
+  const uint32_t* out_off;
+  uint32_t ngroups;
+};
+
+__global__ void __launch_bounds__(128) k_wsum_level(const Xyzz* Tin, const Xyzz* Din, GroupTab G, uint32_t total_out,
+                                                    uint32_t dbl_shift, Xyzz* Tout, Xyzz* Dout) {
+  const uint32_t o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= total_out) return;
+  uint32_t lo = 0, hi = G.ngroups;   // group g with out_off[g] <= o < out_off[g+1]
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (G.out_off[mid] <= o)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  const uint32_t g = lo, k = o - G.out_off[g];
+  const uint32_t a = G.in_off[g] + k * SEG;
+  const uint32_t len = min(SEG, G.in_cnt[g] - k * SEG);
+  Xyzz run = xyzz_inf(), u = xyzz_inf();
+  for (int j = (int)len - 1; j >= 0; j--) {
+    xyzz_add(run, Tin[a + j]);
+    xyzz_add(u, run);
+  }
+  Tout[o] = run;
+  // D_out = sum of D_in over the segment + SEG^{r-1} * U
+  for (uint32_t i = 0; i < dbl_shift; i++) u = xyzz_dbl(u);
+  if (Din)
+    for (uint32_t j = 0; j < len; j++) xyzz_add(u, Din[a + j]);
+  Dout[o] = u;
+}
+
+// W_g = D_g - c * S_g
+__global__ void k_wsum_final(const Xyzz* T, const Xyzz* D, uint32_t ngroups, uint32_t c, Xyzz* W) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= ngroups) return;
+  Xyzz w = D[g];
+  if (c) {
+    Xyzz s = xyzz_mul_small(T[g], c);
+    xyzz_add(w, xyzz_neg(s));
+  }
+  W[g] = w;
+}
+
 // Horner over the windows of MSM l: acc = 2^{c_w} acc + S_w from the top, then affine
 __global__ void k_final(const Xyzz* wsum, uint32_t L, WinPlan P, Aff* out) {
   uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
@@ -439,11 +498,11 @@ uint32_t bitlen_u32(uint32_t v) { return v ? 32u - __builtin_clz(v) : 0u; }
 // E_w = #{elements with bitlen > o} bucket entries plus L * 2^(c-1) buckets, each costing
 // ~KAPPA entries in the running-sum reduction.  DP over window boundaries.
 WinPlan plan_windows(const uint32_t* hist, uint32_t nbits, uint64_t L) {
-  // KAPPA: cost of one bucket in bucket-entry units.  Besides the two full XYZZ adds of
-  // the (latency-bound) running sum, every bucket widens the sort key; the sweep in
-  // tools/ab_kappa.sh on config 3 plateaus for KAPPA >= 64 with windows >= 8 bits
-  // (16.1 ms/step vs 17.7 ms for uniform 16-bit windows).
-  static const double KAPPA = getenv("TC_MSM_KAPPA") ? atof(getenv("TC_MSM_KAPPA")) : 64.0;
+  // KAPPA: cost of one bucket in bucket-entry units (~2.4 full XYZZ adds in the recursive
+  // bucket weighting + sort-key width).  tools/ab_kappa.sh on config 3: KAPPA 2..6 picks
+  // an 18-bit low window, 13.95 ms/step (vs 15.4 ms at KAPPA 64 / 10-bit windows and
+  // 17.7 ms for uniform 16-bit windows).
+  static const double KAPPA = getenv("TC_MSM_KAPPA") ? atof(getenv("TC_MSM_KAPPA")) : 4.0;
   const int top = (int)nbits + 1;   // bits to cover incl. the final carry
   double above[NHIST + 2];          // above[o] = #elements with bitlen > o
   double acc = 0;
@@ -453,7 +512,7 @@ WinPlan plan_windows(const uint32_t* hist, uint32_t nbits, uint64_t L) {
   }
   above[NHIST + 1] = 0;
   const int CMAX = 20;
-  static const int CMIN_ENV = getenv("TC_MSM_CMIN") ? atoi(getenv("TC_MSM_CMIN")) : 8;
+  static const int CMIN_ENV = getenv("TC_MSM_CMIN") ? atoi(getenv("TC_MSM_CMIN")) : 4;
   const int CMIN = std::max(CMIN_ENV, (top + MAXW - 1) / MAXW);   // at most MAXW windows
   std::vector<double> best(top + CMAX + 1, 1e300);
   std::vector<int> from(top + CMAX + 1, -1);
@@ -735,13 +794,83 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   }
 
   // 7-8. bucket reduction, window sums, Horner, affine
+  const uint32_t nw_total = (uint32_t)L * P.nwin;
+  static const bool old_reduce = getenv("TC_MSM_RUNSUM") != nullptr;
+  if (!old_reduce) {
+    // recursive segmentation (k_wsum_level): host builds all level tables, one upload
+    std::vector<uint32_t> cnt(nw_total), off(nw_total);
+    for (uint32_t g = 0; g < nw_total; g++) {
+      const uint32_t l = g / P.nwin, w = g % P.nwin;
+      cnt[g] = P.base[w + 1] - P.base[w];
+      off[g] = l * P.nbm + P.base[w];
+    }
+    std::vector<uint32_t> tabs;   // per level: in_off[ng], in_cnt[ng], out_off[ng+1]
+    std::vector<uint32_t> totals;
+    bool more = true;
+    while (more) {
+      std::vector<uint32_t> oo(nw_total + 1);
+      uint32_t acc = 0;
+      more = false;
+      for (uint32_t g = 0; g < nw_total; g++) {
+        oo[g] = acc;
+        const uint32_t k = (cnt[g] + SEG - 1) / SEG;
+        acc += k;
+        if (k > 1) more = true;
+      }
+      oo[nw_total] = acc;
+      tabs.insert(tabs.end(), off.begin(), off.end());
+      tabs.insert(tabs.end(), cnt.begin(), cnt.end());
+      tabs.insert(tabs.end(), oo.begin(), oo.end());
+      totals.push_back(acc);
+      for (uint32_t g = 0; g < nw_total; g++) {
+        off[g] = oo[g];
+        cnt[g] = oo[g + 1] - oo[g];
+      }
+    }
+    const uint32_t R = (uint32_t)totals.size();
+    const size_t tab_bytes = tabs.size() * sizeof(uint32_t);
+    const size_t stage_off = 256 * 1024;
+    if (tab_bytes + stage_off <= ctx->h_stage_bytes && R <= 9) {
+      uint32_t* d_tabs;
+      TC_TRY(scratch_t(ctx, "msm.wtabs", tabs.size(), &d_tabs));
+      memcpy((char*)ctx->h_stage + stage_off, tabs.data(), tab_bytes);
+      TC_CUDA(ctx, cudaMemcpyAsync(d_tabs, (char*)ctx->h_stage + stage_off, tab_bytes, cudaMemcpyHostToDevice, st));
+      Xyzz *TA, *TB, *DA, *DB, *wsum;
+      TC_TRY(scratch_t(ctx, "msm.wTA", totals[0] + 1, &TA));
+      TC_TRY(scratch_t(ctx, "msm.wTB", totals[0] + 1, &TB));
+      TC_TRY(scratch_t(ctx, "msm.wDA", totals[0] + 1, &DA));
+      TC_TRY(scratch_t(ctx, "msm.wDB", totals[0] + 1, &DB));
+      TC_TRY(scratch_t(ctx, "msm.wsum", nw_total, &wsum));
+      const uint32_t stride = 3 * nw_total + 1;
+      const Xyzz* Tin = buckets;
+      const Xyzz* Din = nullptr;
+      for (uint32_t r = 0; r < R; r++) {
+        GroupTab G{d_tabs + r * stride, d_tabs + r * stride + nw_total, d_tabs + r * stride + 2 * nw_total, nw_total};
+        Xyzz* To = (r & 1) ? TB : TA;
+        Xyzz* Do = (r & 1) ? DB : DA;
+        k_wsum_level<<<blocks_for(totals[r], 128), 128, 0, st>>>(Tin, Din, G, totals[r], 3 * r, To, Do);
+        TC_LAUNCHED(ctx);
+        Tin = To;
+        Din = Do;
+      }
+      uint64_t p8 = 1;
+      for (uint32_t r = 0; r < R; r++) p8 *= SEG;
+      const uint32_t c = (uint32_t)((p8 - SEG) / (SEG - 1));
+      k_wsum_final<<<blocks_for(nw_total, 64), 64, 0, st>>>(Tin, Din, nw_total, c, wsum);
+      TC_LAUNCHED(ctx);
+      k_final<<<blocks_for(L, 32), 32, 0, st>>>(wsum, (uint32_t)L, P, d_out);
+      TC_LAUNCHED(ctx);
+      // the table upload reads h_stage asynchronously: finish before it can be reused
+      TC_CUDA(ctx, cudaStreamSynchronize(st));
+      return TC_OK;
+    }
+  }
   uint32_t minB = 1u << 30;
   for (int w = 0; w < P.nwin; w++) minB = std::min<uint32_t>(minB, 1u << (P.width[w] - 1));
   uint32_t LS = 32u;
   while (LS > 2u && (uint64_t)nb / LS < (uint64_t)ctx->num_sms * 256u) LS >>= 1;
   LS = std::min<uint32_t>(LS, minB);
   const uint32_t nseg_total = nb / LS;
-  const uint32_t nw_total = (uint32_t)L * P.nwin;
   Xyzz *segs, *wsum;
   TC_TRY(scratch_t(ctx, "msm.segs", nseg_total, &segs));
   TC_TRY(scratch_t(ctx, "msm.wsum", nw_total, &wsum));
