@@ -354,6 +354,15 @@ def main():
     value = per_step_elems / (ms_step / 1e3)
     value_e2e = per_step_elems / (ms_e2e / args.steps / 1e3)
     achieved = st["units"] * WORD_MULS_PER_ADD / (st["ms"] * 1e-3) / 1e12 if st["ms"] else None
+    traffic = None   # dram bytes per launch of k_accum_aff from the committed ncu --set full capture
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_accum_summary.txt")) as fh:
+            kv = dict(l.split(" = ", 1) for l in fh if " = " in l)
+        to_b = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        traffic = sum(float(kv[k].split()[0]) * to_b[kv[k].split()[1]]
+                      for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+    except (OSError, KeyError, ValueError, IndexError):
+        pass
 
     fwd = None if (args.no_forward or rank != 0 or args.config != 3) else forward_ms(dev)
     cpu = None
@@ -381,7 +390,9 @@ def main():
             "gpu_launches": launches,
             "roofline": {"bound": "int", "kernel": "k_accum_aff (Pippenger bucket accumulation)",
                          "achieved": achieved, "peak": peak_tops, "unit": "T word-mul/s",
-                         "frac": (achieved / peak_tops) if achieved and peak_tops else None, "traffic": None,
+                         "frac": (achieved / peak_tops) if achieved and peak_tops else None, "traffic": traffic,
+                         "traffic_note": "dram read+write bytes per launch, profiles/r01_ncu_accum_summary.txt "
+                                         "(point gathers: ~48 B per bucket entry)",
                          "work": f"{st['units']:.0f} bucket entries x {WORD_MULS_PER_ADD} word-muls "
                                  f"(11 mulmods x 78) over {st['launches']} launches, {st['ms']:.3f} ms",
                          "peak_source": "mad.lo.u32 microbenchmark in this run (tc_measure_imad_peak)",
