@@ -245,9 +245,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TC_DIST_BACKEND=gloo lets several ranks share one GPU in tests (the gather is the only
+    # collective; the kernels never wait on another rank)
+    backend = os.environ.get("TC_DIST_BACKEND", "nccl")
+    dev_index = local if backend == "nccl" else local % max(1, torch.cuda.device_count())
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(dev_index)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
+    local = dev_index
     dev = torch.device("cuda", local)
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     cfg = CONFIGS[5 if args.config == 5 else 3]
@@ -293,7 +301,7 @@ def main():
         comms = tcb.tc_commit_many(srs, layers, route=route)
         encs = [c.to_bytes() for c in comms]
         if world > 1:
-            encs = allgather_commitments(encs, n_layers, rank, world, device=dev)
+            encs = allgather_commitments(encs, n_layers, rank, world, device=dev if backend == "nccl" else None)
         leaves = [tcb.hash_to_scalar(e, b"terkle/leaf") for e in encs]
         tree, root = tcb.build(tcfg, leaves, srs=node_srs)
         return root
@@ -318,7 +326,7 @@ def main():
             dist.barrier()
         ms = e0.elapsed_time(e1)
         if world > 1:
-            t = torch.tensor([ms], device=dev)
+            t = torch.tensor([ms], device=dev if backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms, ctx.launches - l0, root

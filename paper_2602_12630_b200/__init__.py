@@ -7,6 +7,7 @@ opening proofs, with hand-written sm_100a CUDA kernels behind a C ABI
 or a CUDA device the compute entry points raise.
 """
 from .authtree import MembershipProof, TerkleTree, TreeConfig, build, leaf_of, prove, verify
+from .capture import ActivationCapture, infer_and_capture
 from .commit import (Commitment, Srs, TensorOpening, Trapdoors, derive_taus, load_srs, pair, setup_srs, tc_commit,
                      tc_commit_many, tc_open, tc_verify)
 from .curve import G, P, Q, decode_elem, decode_scalar, encode_elem, encode_scalar, hash_to_scalar
@@ -15,7 +16,7 @@ from .mvpoly import Grid, MultiPoly, default_grid, evaluate, interpolate_lagrang
 from .protocol import FieldTensor, prover_commit, quantize
 
 __all__ = [
-    "Commitment", "FieldTensor", "G", "Grid", "MembershipProof", "MultiPoly", "P", "PrimeField", "Q", "Srs",
+    "ActivationCapture", "infer_and_capture", "Commitment", "FieldTensor", "G", "Grid", "MembershipProof", "MultiPoly", "P", "PrimeField", "Q", "Srs",
     "TensorOpening", "TerkleTree", "Trapdoors", "TreeConfig", "build", "decode_elem", "decode_scalar", "default_grid",
     "derive_taus", "encode_elem", "encode_scalar", "evaluate", "hash_to_scalar", "interpolate_lagrange", "leaf_of",
     "lex_index", "load_srs", "open_quotients", "pair", "prove", "prover_commit", "quantize", "setup_srs", "tc_commit",
