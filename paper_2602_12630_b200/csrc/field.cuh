@@ -370,26 +370,46 @@ struct Field {
 #pragma unroll
     for (int i = 0; i < 6; i++) {
       s = (uint64_t)T[i] + carry;
-      if (i == 5) s += (uint64_t)u[0] * PM::M5;
+      if (i == 5) s += mul_m5(u[0]);
       u[i] = (uint32_t)s * PM::NP;
       s += (uint64_t)u[i] * PM::M0;
       carry = s >> 32;
     }
     Fe r;
-    s = (uint64_t)T[6] + carry + (uint64_t)u[1] * PM::M5;
+    s = (uint64_t)T[6] + carry + mul_m5(u[1]);
     r.v[0] = (uint32_t)s;
-    s = (s >> 32) + T[7] + (uint64_t)u[2] * PM::M5;
+    s = (s >> 32) + T[7] + mul_m5(u[2]);
     r.v[1] = (uint32_t)s;
-    s = (s >> 32) + T[8] + (uint64_t)u[3] * PM::M5;
+    s = (s >> 32) + T[8] + mul_m5(u[3]);
     r.v[2] = (uint32_t)s;
-    s = (s >> 32) + T[9] + (uint64_t)u[4] * PM::M5;
+    s = (s >> 32) + T[9] + mul_m5(u[4]);
     r.v[3] = (uint32_t)s;
-    s = (s >> 32) + T[10] + (uint64_t)u[5] * PM::M5;
+    s = (s >> 32) + T[10] + mul_m5(u[5]);
     r.v[4] = (uint32_t)s;
     s = (s >> 32) + T[11];
     r.v[5] = (uint32_t)s;
     return r;
 #endif
+  }
+
+  // u * M5 for the small top limb of the modulus (q: 0xF0 = 2^8 - 2^4, p: 2).  With
+  // -DTC_REDC_SHIFT the device uses shifts (ALU pipe) instead of the half-rate IMAD.WIDE;
+  // measured 5% SLOWER in k_accum_aff (ptxas then emits twice the IMAD.MOVs), so off.
+  TC_HD static uint64_t mul_m5(uint32_t u) {
+#if defined(__CUDA_ARCH__) && defined(TC_REDC_SHIFT)
+    uint64_t r;
+    if (PM::M5 == 0xF0u) {
+      asm("{.reg .u64 a, b;\n\t"
+          "cvt.u64.u32 a, %1;\n\t"
+          "shl.b64 b, a, 8;\n\t"
+          "shl.b64 a, a, 4;\n\t"
+          "sub.u64 %0, b, a;}"
+          : "=l"(r) : "r"(u));
+      return r;
+    }
+    if (PM::M5 == 2u) return (uint64_t)u << 1;
+#endif
+    return (uint64_t)u * PM::M5;
   }
 
   TC_HD static Fe mul(const Fe& a, const Fe& b) {
