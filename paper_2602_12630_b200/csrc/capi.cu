@@ -269,14 +269,36 @@ void axis_tables(const Fe& tau_c, uint32_t d, bool lagrange, std::vector<Fe>& ou
   out.insert(out.end(), res.begin(), res.end());
 }
 
-int srs_build_points(tc_ctx* ctx, tc_srs* srs, const std::vector<Fe>& taus, bool lagrange, Aff** dst) {
+// g^{prod_j tab_j[i_j]} for every lex index of `shape` into the preallocated dst
+int srs_fill_points(tc_ctx* ctx, const uint32_t* shape, int m, const Fe* taus, bool lagrange, Aff* dst) {
   std::vector<Fe> tabs;
-  for (int j = 0; j < srs->m; j++) axis_tables(taus[j], srs->shape[j], lagrange, tabs);
+  uint64_t n = 1;
+  for (int j = 0; j < m; j++) axis_tables(taus[j], shape[j], lagrange, tabs), n *= shape[j];
   Fe* d_exps;
-  TC_TRY(tcrt::scratch_t(ctx, "srs.exps", srs->n, &d_exps));
-  TC_TRY(tcrt::srs_exponents(ctx, tabs, srs->shape, srs->m, srs->n, d_exps));
+  TC_TRY(tcrt::scratch_t(ctx, "srs.exps", n, &d_exps));
+  TC_TRY(tcrt::srs_exponents(ctx, tabs, shape, m, n, d_exps));
+  TC_TRY(tcrt::fixed_base_g(ctx, d_exps, n, dst));
+  return TC_OK;
+}
+
+int srs_build_points(tc_ctx* ctx, tc_srs* srs, const std::vector<Fe>& taus, bool lagrange, Aff** dst) {
   TC_CUDA(ctx, cudaMalloc(dst, srs->n * sizeof(Aff)));
-  TC_TRY(tcrt::fixed_base_g(ctx, d_exps, srs->n, *dst));
+  return srs_fill_points(ctx, srs->shape, srs->m, taus.data(), lagrange, *dst);
+}
+
+// sub-grid Lagrange sets for the suffixes i = 1..m-1 (Lagrange-route opening quotients)
+int srs_build_sublag(tc_ctx* ctx, tc_srs* srs, const std::vector<Fe>& taus) {
+  if (srs->m < 2) return TC_OK;
+  uint64_t total = 0;
+  for (int i = 1; i < srs->m; i++) {
+    uint64_t ni = 1;
+    for (int j = i; j < srs->m; j++) ni *= srs->shape[j];
+    srs->sublag_off[i] = total;
+    total += ni;
+  }
+  TC_CUDA(ctx, cudaMalloc(&srs->sublag, total * sizeof(Aff)));
+  for (int i = 1; i < srs->m; i++)
+    TC_TRY(srs_fill_points(ctx, srs->shape + i, srs->m - i, taus.data() + i, true, srs->sublag + srs->sublag_off[i]));
   return TC_OK;
 }
 
@@ -461,6 +483,7 @@ int tc_srs_generate(tc_ctx* ctx, const uint32_t* shape, int m, const uint8_t* ta
   int s = TC_OK;
   if (flags & TC_SRS_MONOMIAL) s = srs_build_points(ctx, srs, taus, false, &srs->monomial);
   if (!s && (flags & TC_SRS_LAGRANGE)) s = srs_build_points(ctx, srs, taus, true, &srs->lagrange);
+  if (!s && (flags & TC_SRS_LAGRANGE)) s = srs_build_sublag(ctx, srs, taus);
   if (!s) {   // axis elements g^{tau_j}
     Fe* d_t;
     Aff* d_a;
@@ -553,6 +576,7 @@ int tc_srs_destroy(tc_srs* srs) {
   if (srs->lagrange) cudaFree(srs->lagrange);
   for (auto* t : srs->small_tab)
     if (t) cudaFree(t);
+  if (srs->sublag) cudaFree(srs->sublag);
   delete srs;
   return TC_OK;
 }
@@ -695,8 +719,6 @@ int tc_commit_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, in
 int tc_open(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int scale_bits, const uint8_t* omega_le21,
             int route, uint8_t* out_y21, uint8_t* out_pi43) {
   if (!ctx || !srs || !d_in || !omega_le21 || !out_y21 || !out_pi43) return TC_ERR_ARGUMENT;
-  if (!srs->monomial) return fail(ctx, TC_ERR_VALUE, "tc_open needs the monomial srs");
-  (void)route;
   const uint64_t n = srs->n;
   const int m = srs->m;
   std::vector<Fe> om(m);
@@ -704,6 +726,58 @@ int tc_open(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int sca
     if (!le21_to_fe(omega_le21 + 21 * j, om[j])) return fail(ctx, TC_ERR_VALUE, "point coordinate %d out of range", j);
   Fe* vals;
   TC_TRY(load_field_tensor(ctx, d_in, dtype, n, scale_bits, &vals, "open.vals"));
+  // Lagrange route: quotients evaluated on the grid straight from the samples (no
+  // interpolation), committed over the (sub-grid) Lagrange elements.  Needs omega off the
+  // grid on every axis (on a node the quotient value is a derivative) — else monomial.
+  bool on_grid = false;
+  for (int a = 0; a < m; a++)
+    for (uint32_t k = 1; k <= srs->shape[a] && !on_grid; k++) {
+      Fe z{{k, 0, 0, 0, 0, 0}};
+      on_grid = (memcmp(z.v, om[a].v, sizeof z.v) == 0);
+    }
+  const bool lag_ok = srs->lagrange && (m == 1 || srs->sublag) && !on_grid;
+  if (route == TC_ROUTE_LAGRANGE && !lag_ok && !on_grid)
+    return fail(ctx, TC_ERR_VALUE, "srs has no Lagrange elements");
+  if (lag_ok && route != TC_ROUTE_MONOMIAL) {
+    std::vector<Fe> lam, inv;
+    for (int a = 0; a < m; a++) {
+      const uint32_t d = srs->shape[a];
+      std::vector<Fe> la;
+      axis_tables(om[a], d, true, la);   // L_k(omega_a), canonical
+      const Fe w = Fp::to_mont(om[a]);
+      std::vector<Fe> diff(d), pref(d);
+      Fe run = Fp::one();
+      for (uint32_t k = 0; k < d; k++) {
+        diff[k] = Fp::sub(Fp::to_mont_small(k + 1), w);
+        pref[k] = run;
+        run = Fp::mul(run, diff[k]);
+      }
+      Fe iv = Fp::inv(run);
+      std::vector<Fe> ik(d);
+      for (int k = (int)d - 1; k >= 0; k--) {
+        ik[k] = Fp::canon(Fp::mul(iv, pref[k]));
+        iv = Fp::mul(iv, diff[k]);
+      }
+      for (uint32_t k = 0; k < d; k++) lam.push_back(Fp::canon(Fp::to_mont(la[k])));
+      inv.insert(inv.end(), ik.begin(), ik.end());
+    }
+    Fe* qs;
+    TC_TRY(tcrt::scratch_t(ctx, "open.q", (uint64_t)m * n, &qs));
+    Fe y;
+    TC_TRY(tcrt::open_quotients_lagrange_device(ctx, vals, srs->shape, m, lam, inv, qs, &y));
+    fe_to_le21(y, out_y21);
+    Aff* d_out;
+    TC_TRY(tcrt::scratch_t(ctx, "open.out", (uint64_t)m, &d_out));
+    uint64_t span = n;
+    for (int a = 0; a < m; a++) {
+      const Aff* bases = a == 0 ? srs->lagrange : srs->sublag + srs->sublag_off[a];
+      const void* ptr = qs + (uint64_t)a * n;
+      TC_TRY(tcrt::msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, &ptr, 1, bases, span, d_out + a));
+      span /= srs->shape[a];
+    }
+    return fetch_encode_many(ctx, d_out, m, out_pi43);
+  }
+  if (!srs->monomial) return fail(ctx, TC_ERR_VALUE, "tc_open needs the monomial srs");
   TC_TRY(tcrt::interpolate_device(ctx, vals, srs->shape, m));
   Fe* qs;
   TC_TRY(tcrt::scratch_t(ctx, "open.q", (uint64_t)m * n, &qs));

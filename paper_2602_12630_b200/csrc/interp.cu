@@ -100,6 +100,22 @@ __global__ void k_divide_axis(Fe* r, Fe* q, uint32_t d, uint64_t s, Fe v_mont) {
   r[i] = Fp::canon(carry);
 }
 
+// Lagrange-route opening along the leading axis (extent d, `rest` trailing elements):
+// rn[r] = sum_k r[k, r] lam[k];  q[k, r] = (r[k, r] - rn[r]) * inv[k]
+__global__ void k_open_axis_lag(const Fe* r, uint32_t d, uint64_t rest, const Fe* lam, const Fe* inv, Fe* rn,
+                                Fe* q) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= rest) return;
+  uint32_t acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (uint32_t k = 0; k < d; k++) mac_wide(acc, r[(uint64_t)k * rest + i], lam[k]);
+  const Fe next = Fp::canon(Fp::redc(acc));
+  rn[i] = next;
+  for (uint32_t k = 0; k < d; k++) {
+    const uint64_t pos = (uint64_t)k * rest + i;
+    q[pos] = Fp::canon(Fp::mul(Fp::sub(r[pos], next), inv[k]));
+  }
+}
+
 // out[rest] = sum_k c[k, rest] x^k  (Horner along the leading axis of extent d)
 __global__ void k_horner_lead(const Fe* c, Fe* out, uint32_t d, uint64_t rest, Fe x_mont) {
   uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -198,6 +214,44 @@ int open_quotients_device(tc_ctx* ctx, const Fe* d_coeffs, const uint32_t* shape
     k_divide_axis<<<blocks_for(s, 128), 128, 0, st>>>(r, d_quotients + (uint64_t)a * n, d, s, vm);
     TC_LAUNCHED(ctx);
     span = s;
+  }
+  TC_CUDA(ctx, cudaMemcpyAsync(h_y, r, sizeof(Fe), cudaMemcpyDeviceToHost, st));
+  TC_CUDA(ctx, cudaStreamSynchronize(st));
+  return TC_OK;
+}
+
+int open_quotients_lagrange_device(tc_ctx* ctx, Fe* d_vals, const uint32_t* shape, int m,
+                                   const std::vector<Fe>& lam, const std::vector<Fe>& inv, Fe* d_quotients,
+                                   Fe* h_y) {
+  cudaStream_t st = ctx->stream;
+  uint64_t n = 1;
+  uint32_t dsum = 0;
+  for (int j = 0; j < m; j++) n *= shape[j], dsum += shape[j];
+  Fe *tabs, *bufA, *bufB;
+  TC_TRY(scratch_t(ctx, "openlag.tabs", 2 * (uint64_t)dsum, &tabs));
+  TC_TRY(scratch_t(ctx, "openlag.rA", n / shape[0] + 1, &bufA));
+  TC_TRY(scratch_t(ctx, "openlag.rB", (m > 1 ? n / shape[0] / shape[1] : 1) + 1, &bufB));
+  // weights + inverses -> device through the pinned staging area, one copy
+  Fe* stage = (Fe*)((char*)ctx->h_stage + 512 * 1024);
+  if ((size_t)2 * dsum * sizeof(Fe) > 256 * 1024) return fail(ctx, TC_ERR_VALUE, "open: axes too long");
+  memcpy(stage, lam.data(), dsum * sizeof(Fe));
+  memcpy(stage + dsum, inv.data(), dsum * sizeof(Fe));
+  TC_CUDA(ctx, cudaMemcpyAsync(tabs, stage, 2 * dsum * sizeof(Fe), cudaMemcpyHostToDevice, st));
+  Fe* r = d_vals;
+  uint64_t span = n;
+  uint32_t off = 0;
+  for (int a = 0; a < m; a++) {
+    const uint32_t d = shape[a];
+    const uint64_t rest = span / d;
+    // r_{a+1} alternates between two buffers (A holds r_1, B is large enough for r_2..);
+    // kernels are stream-ordered, so r_a is never overwritten while it is read
+    Fe* rn = (a & 1) ? bufB : bufA;
+    k_open_axis_lag<<<blocks_for(rest, 128), 128, 0, st>>>(r, d, rest, tabs + off, tabs + dsum + off, rn,
+                                                           d_quotients + (uint64_t)a * n);
+    TC_LAUNCHED(ctx);
+    r = rn;
+    span = rest;
+    off += d;
   }
   TC_CUDA(ctx, cudaMemcpyAsync(h_y, r, sizeof(Fe), cudaMemcpyDeviceToHost, st));
   TC_CUDA(ctx, cudaStreamSynchronize(st));

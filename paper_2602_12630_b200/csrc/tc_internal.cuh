@@ -47,6 +47,10 @@ struct tc_srs {
   tc::Aff* lagrange = nullptr;   // N affine points g^{L_i(tau)} (optional)
   tc::Aff axis[TC_MAX_AXES];     // g^{tau_j} (host copy)
   tc::Aff* small_tab[2] = {nullptr, nullptr};   // byte-window tables (monomial, Lagrange), n <= 64
+  // sub-grid Lagrange elements g^{prod_{j>=i} L_{j,a_j}(tau_j)} for suffixes i = 1..m-1
+  // (commitments of the Lagrange-route opening quotients q_i, which live on axes i..m-1)
+  tc::Aff* sublag = nullptr;
+  uint64_t sublag_off[TC_MAX_AXES] = {0};
 };
 
 // SRS sizes up to this many points use the fixed-base small-MSM kernel (small_msm.cu)
@@ -130,6 +134,14 @@ int interpolate_device(tc_ctx* ctx, tc::Fe* d_vals, const uint32_t* shape, int m
 // mvpoly.evaluate on device (per-axis Horner), y returned on the host
 int evaluate_device(tc_ctx* ctx, const tc::Fe* d_coeffs, const uint32_t* shape, int m,
                     const tc::Fe* point_canon, tc::Fe* h_y);
+
+// Lagrange-route quotients on the grid (no interpolation): r_0 = grid values (consumed);
+// per axis a: r_{a+1} = contraction of r_a with lam[a] (Montgomery L_k(omega_a)), and
+// q_a[k, rest] = (r_a[k, rest] - r_{a+1}[rest]) * inv[a][k] (Montgomery 1/(z_k - omega_a)).
+// q_a is written at d_quotients + a*N (only its first prod_{j>=a} d_j entries); y on host.
+int open_quotients_lagrange_device(tc_ctx* ctx, tc::Fe* d_vals, const uint32_t* shape, int m,
+                                   const std::vector<tc::Fe>& lam, const std::vector<tc::Fe>& inv,
+                                   tc::Fe* d_quotients, tc::Fe* h_y);
 
 // open_quotients on device: coefficient array (canonical) -> m quotient arrays + y
 int open_quotients_device(tc_ctx* ctx, const tc::Fe* d_coeffs, const uint32_t* shape, int m,

@@ -174,10 +174,19 @@ def test_config1_commit_and_openings_golden():
         assert O.encode_elem(c.elem).hex() == gold["commitment"], route
     for o in gold["openings"]:
         pt = ints(o["point"])
-        op = tcb.tc_open(srs, t, pt)
-        assert op.y == int(o["y"], 16)
-        assert [O.encode_elem(e).hex() for e in op.proofs] == o["proofs"]
-        assert tcb.tc_verify(srs, c, pt, op)
+        for route in ("lagrange", "monomial"):
+            op = tcb.tc_open(srs, t, pt, route=route)
+            assert op.y == int(o["y"], 16), route
+            assert [O.encode_elem(e).hex() for e in op.proofs] == o["proofs"], route
+            assert tcb.tc_verify(srs, c, pt, op)
+    # a challenge on the grid falls back to the monomial route (quotient = derivative there)
+    gp = [3, 60]
+    coeffs = O.interpolate_lagrange(O.quantize(x, 16), shape)
+    qs, y = O.open_quotients(coeffs, shape, gp)
+    op = tcb.tc_open(srs, t, gp)
+    assert op.y == y
+    srs_pts = srs.monomial_elems
+    assert list(op.proofs) == [O.msm_naive(q, srs_pts) for q in qs]
 
 
 def test_config2_commitments_golden():
