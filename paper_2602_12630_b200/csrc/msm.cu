@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(128) k_window_sum(const Xyzz* segs, WinPlan P,
 //     A(x) = D - S * (SEG^R - SEG) / (SEG - 1).
 // No per-segment scalar multiplications and SEG x more parallelism than one thread per
 // window; every level is one launch over all groups of the batch.
-constexpr uint32_t SEG = 8;
+// segment length SEG = 2^lg (runtime: TC_MSM_SEG_LG, default 3)
 
 struct GroupTab {   // per group: input offset, input count, output offset (device)
   const uint32_t* in_off;
@@ -461,7 +461,7 @@ struct GroupTab {   // per group: input offset, input count, output offset (devi
 };
 
 __global__ void __launch_bounds__(128) k_wsum_level(const Xyzz* Tin, const Xyzz* Din, GroupTab G, uint32_t total_out,
-                                                    uint32_t dbl_shift, Xyzz* Tout, Xyzz* Dout) {
+                                                    uint32_t dbl_shift, uint32_t SEG, Xyzz* Tout, Xyzz* Dout) {
   const uint32_t o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= total_out) return;
   uint32_t lo = 0, hi = G.ngroups;   // group g with out_off[g] <= o < out_off[g+1]
@@ -765,8 +765,10 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   }
 
   // 6. levels (a bucket holds <= n entries)
-  const uint32_t T = (E >= (1u << 20)) ? 32u : (E >= (1u << 14) ? 16u : 8u);
-  const uint32_t T1 = 8u;
+  static const uint32_t T_ENV = getenv("TC_MSM_T") ? (uint32_t)atoi(getenv("TC_MSM_T")) : 32u;
+  static const uint32_t T1_ENV = getenv("TC_MSM_T1") ? (uint32_t)atoi(getenv("TC_MSM_T1")) : 8u;
+  const uint32_t T = (E >= (1u << 20)) ? T_ENV : (E >= (1u << 14) ? 16u : 8u);
+  const uint32_t T1 = T1_ENV;
   int levels = 1;
   for (uint64_t capT = T; capT < n; capT *= T1) levels++;
   // items = pieces of multi-piece buckets: ceil(sz/T) <= 2 sz / T for sz > T
@@ -828,6 +830,8 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   // 7-8. bucket reduction, window sums, Horner, affine
   const uint32_t nw_total = (uint32_t)L * P.nwin;
   static const bool old_reduce = getenv("TC_MSM_RUNSUM") != nullptr;
+  static const uint32_t SEG_LG = getenv("TC_MSM_SEG_LG") ? (uint32_t)atoi(getenv("TC_MSM_SEG_LG")) : 3u;
+  const uint32_t SEG = 1u << SEG_LG;
   if (!old_reduce) {
     // recursive segmentation (k_wsum_level): host builds all level tables, one upload
     std::vector<uint32_t> cnt(nw_total), off(nw_total);
@@ -880,7 +884,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
         GroupTab G{d_tabs + r * stride, d_tabs + r * stride + nw_total, d_tabs + r * stride + 2 * nw_total, nw_total};
         Xyzz* To = (r & 1) ? TB : TA;
         Xyzz* Do = (r & 1) ? DB : DA;
-        k_wsum_level<<<blocks_for(totals[r], 128), 128, 0, st>>>(Tin, Din, G, totals[r], 3 * r, To, Do);
+        k_wsum_level<<<blocks_for(totals[r], 128), 128, 0, st>>>(Tin, Din, G, totals[r], SEG_LG * r, SEG, To, Do);
         TC_LAUNCHED(ctx);
         Tin = To;
         Din = Do;
