@@ -10,6 +10,7 @@ Membership proofs open each node on the path at its child's grid point kappa + 1
 from __future__ import annotations
 
 import ctypes as C
+import struct
 from dataclasses import dataclass, field
 
 from . import _lib
@@ -59,6 +60,38 @@ class MembershipProof:
     index: int
     nodes: tuple
     openings: tuple
+
+    def to_bytes(self, config: "TreeConfig") -> bytes:
+        """TCTP wire format: magic, kind byte (2 = terkle), depth u16, leaf
+        index u64, then per level a length-prefixed payload: node point ‖ TCOP opening."""
+        out = [b"TCTP", bytes([2]), struct.pack("<HQ", len(self.nodes), self.index)]
+        for lvl, (node, op) in enumerate(zip(self.nodes, self.openings)):
+            slot = (self.index // config.arity ** lvl) % config.arity
+            payload = encode_elem(node) + op.to_bytes(child_point(slot, config.shape))
+            out.append(struct.pack("<I", len(payload)) + payload)
+        return b"".join(out)
+
+    @staticmethod
+    def from_bytes(raw: bytes) -> "MembershipProof":
+        raw = bytes(raw)
+        if raw[:4] != b"TCTP" or len(raw) < 15 or raw[4] != 2:
+            raise ValueError("bad terkle proof header")
+        depth, index = struct.unpack_from("<HQ", raw, 5)
+        off, nodes, ops = 15, [], []
+        for _ in range(depth):
+            if off + 4 > len(raw):
+                raise ValueError("truncated terkle proof")
+            (ln,) = struct.unpack_from("<I", raw, off)
+            off += 4
+            payload = raw[off: off + ln]
+            if len(payload) != ln or ln < ELEM_BYTES:
+                raise ValueError("truncated terkle proof")
+            nodes.append(decode_elem(payload[:ELEM_BYTES]))
+            ops.append(TensorOpening.from_bytes(payload[ELEM_BYTES:])[1])
+            off += ln
+        if off != len(raw):
+            raise ValueError("trailing bytes in terkle proof")
+        return MembershipProof(index, tuple(nodes), tuple(ops))
 
 
 _NODE_SRS = {}

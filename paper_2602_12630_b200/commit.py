@@ -15,7 +15,8 @@ import struct
 from dataclasses import dataclass
 
 from . import _conv, _lib
-from .curve import ELEM_BYTES, P, decode_elem, decode_elems, encode_elem, encode_scalar, hash_to_scalar
+from .curve import (ELEM_BYTES, P, decode_elem, decode_elems, decode_scalar, encode_elem, encode_scalar,
+                    hash_to_scalar)
 from .mvpoly import Grid, check_shape, default_grid
 
 SCALE_BITS = 16   # protocol.quantize fixed-point scale
@@ -63,6 +64,24 @@ class TensorOpening:
         out.append(encode_scalar(self.y))
         out += [encode_elem(e) for e in self.proofs]
         return b"".join(out)
+
+    @staticmethod
+    def from_bytes(raw: bytes):
+        """Inverse of to_bytes: returns (point, TensorOpening); ValueError on malformed input."""
+        raw = bytes(raw)
+        if raw[:4] != b"TCOP":
+            raise ValueError("bad magic, expected b'TCOP'")
+        (m,) = struct.unpack_from("<H", raw, 4)
+        need = 6 + 21 * (m + 1) + ELEM_BYTES * m
+        if len(raw) != need:
+            raise ValueError("opening payload length mismatch")
+        off = 6
+        point = tuple(decode_scalar(raw[off + 21 * i: off + 21 * (i + 1)]) for i in range(m))
+        off += 21 * m
+        y = decode_scalar(raw[off: off + 21])
+        off += 21
+        proofs = tuple(decode_elem(raw[off + ELEM_BYTES * i: off + ELEM_BYTES * (i + 1)]) for i in range(m))
+        return point, TensorOpening(y, proofs)
 
 
 class Srs:

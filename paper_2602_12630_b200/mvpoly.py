@@ -159,3 +159,57 @@ def open_quotients(dom, f: MultiPoly, point):
     flat = _conv.limbs_to_ints(q)
     qs = [MultiPoly(tuple(f.shape), tuple(flat[a * n:(a + 1) * n])) for a in range(m)]
     return qs, int.from_bytes(y.raw, "little")
+
+
+# ---------------------------------------------------------------- wire format (mvpoly.py:567-631)
+WIRE_VERSION = 1
+
+
+def _header(magic: bytes, shape) -> bytes:
+    import struct
+    return magic + struct.pack("<HH", WIRE_VERSION, len(shape)) + b"".join(struct.pack("<I", d) for d in shape)
+
+
+def _read_header(raw: bytes, magic: bytes):
+    import struct
+    if raw[:4] != magic:
+        raise ValueError(f"bad magic, expected {magic!r}")
+    version, m = struct.unpack_from("<HH", raw, 4)
+    if version != WIRE_VERSION:
+        raise ValueError(f"unsupported version {version}")
+    shape = struct.unpack_from("<" + "I" * m, raw, 8)
+    return tuple(shape), 8 + 4 * m
+
+
+def poly_to_bytes(backend, f: MultiPoly) -> bytes:
+    """TCPL: header then 21-byte canonical coefficients (backend accepted for drop-in use)."""
+    return _header(b"TCPL", f.shape) + b"".join(encode_scalar(int(c)) for c in f.coeffs)
+
+
+def poly_from_bytes(backend, raw: bytes) -> MultiPoly:
+    from .curve import decode_scalar
+    raw = bytes(raw)
+    shape, off = _read_header(raw, b"TCPL")
+    n = check_shape(shape)
+    if len(raw) != off + 21 * n:
+        raise ValueError("polynomial payload length mismatch")
+    return MultiPoly(shape, tuple(decode_scalar(raw[off + 21 * k: off + 21 * (k + 1)]) for k in range(n)))
+
+
+def tensor_to_bytes(backend, shape, values) -> bytes:
+    """TCTN: header then 21-byte canonical field elements."""
+    n = check_shape(shape)
+    values = list(values)
+    if len(values) != n:
+        raise ValueError("tensor size does not match shape")
+    return _header(b"TCTN", shape) + b"".join(encode_scalar(int(v)) for v in values)
+
+
+def tensor_from_bytes(backend, raw: bytes):
+    from .curve import decode_scalar
+    raw = bytes(raw)
+    shape, off = _read_header(raw, b"TCTN")
+    n = check_shape(shape)
+    if len(raw) != off + 21 * n:
+        raise ValueError("tensor payload length mismatch")
+    return shape, [decode_scalar(raw[off + 21 * k: off + 21 * (k + 1)]) for k in range(n)]
