@@ -133,6 +133,19 @@ int tc_commit(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int s
 /* count tensors of the SRS's shape (protocol.prover_commit's per-layer loop) */
 int tc_commit_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count,
                     int dtype, int scale_bits, int route, uint8_t* out43);
+/* Same with HOST inputs (pinned for an asynchronous upload; pageable works, synchronously):
+ * uploaded on a copy stream in groups of `group` (0 = one group) and committed as each
+ * group becomes resident.  The entry point a reference-side caller holding numpy / CPU
+ * activations binds (protocol.prover_commit). */
+int tc_commit_batch_host(tc_ctx* ctx, const tc_srs* srs, const void* const* h_ins, int count,
+                         int dtype, int scale_bits, int route, int group, uint8_t* out43);
+/* Streaming host-input commits, one call per forward: commits h_cur and overlaps the upload
+ * of h_next (the next forward's activations, or NULL) with this commit.  h_cur is taken
+ * from the device slot a previous call prefetched it into when the pointers match, else
+ * uploaded first.  Buffers passed as h_next must stay unchanged until they are committed. */
+int tc_commit_stream(tc_ctx* ctx, const tc_srs* srs, const void* const* h_cur,
+                     const void* const* h_next, int count, int dtype, int scale_bits, int route,
+                     uint8_t* out43);
 
 /* ---- tc_open: y = f_T(omega), pi_i = g^{q_i(tau)} ----------------------- */
 int tc_open(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int scale_bits,

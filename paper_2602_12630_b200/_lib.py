@@ -67,6 +67,8 @@ _SIGS = [
     ("tc_msm", C.c_int, [_P, _P, C.c_int, _P, C.c_uint64, _P]),
     ("tc_commit", C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_int, _P]),
     ("tc_commit_batch", C.c_int, [_P, _P, C.POINTER(_P), C.c_int, C.c_int, C.c_int, C.c_int, _P]),
+    ("tc_commit_batch_host", C.c_int, [_P, _P, C.POINTER(_P), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P]),
+    ("tc_commit_stream", C.c_int, [_P, _P, C.POINTER(_P), C.POINTER(_P), C.c_int, C.c_int, C.c_int, C.c_int, _P]),
     ("tc_open", C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_char_p, C.c_int, _P, _P]),
     ("tc_terkle_build", C.c_int, [_P, _P, C.c_char_p, C.c_uint64, _P, C.POINTER(C.c_uint64)]),
     ("tc_pairing", C.c_int, [C.c_char_p, C.c_char_p, _P]),

@@ -232,9 +232,43 @@ def tc_commit(srs: Srs, T, *, scale_bits: int = SCALE_BITS, route: str = "auto")
     return Commitment(decode_elem(out.raw, validate=False))
 
 
-def tc_commit_many(srs: Srs, tensors, *, scale_bits: int = SCALE_BITS, route: str = "auto"):
-    """Commit several tensors of the SRS's shape (one C call)."""
+def _host_floats(tensors):
+    """CPU float tensors / arrays of one dtype -> (contiguous torch tensors, dtype code), else None."""
+    import numpy as np
+    import torch
+
+    out = []
+    for T in tensors:
+        if isinstance(T, np.ndarray) and T.dtype.kind == "f":
+            T = torch.from_numpy(np.ascontiguousarray(T))
+        if not (isinstance(T, torch.Tensor) and T.device.type == "cpu" and T.dtype in _conv._float_codes()):
+            return None
+        out.append(T.detach().contiguous())
+    if not out or len({t.dtype for t in out}) != 1:
+        return None
+    return out, _conv._float_codes()[out[0].dtype]
+
+
+def tc_commit_many(srs: Srs, tensors, *, scale_bits: int = SCALE_BITS, route: str = "auto", group: int = 0):
+    """Commit several tensors of the SRS's shape (one C call).  Host (CPU) float tensors go
+    through tc_commit_batch_host: uploaded in groups on a copy stream, overlapped with the
+    commitments of the groups already on the device (pin them for full overlap)."""
     ctx = _lib.Context.get(srs.device)
+    tensors = list(tensors)
+    host = _host_floats(tensors)
+    if host is not None:
+        ts, code = host
+        for t in ts:
+            if t.numel() != srs.size:
+                raise ValueError("tensor size does not match grid shape")
+        arr = (C.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
+        out = C.create_string_buffer(ELEM_BYTES * len(ts))
+        with ctx.lock:
+            ctx.bind_stream()
+            ctx.check(_lib.lib().tc_commit_batch_host(ctx.handle, srs.handle, arr, len(ts), code, scale_bits,
+                                                      _route(route), int(group), out), "tc_commit_many")
+        return [Commitment(decode_elem(out.raw[i * ELEM_BYTES:(i + 1) * ELEM_BYTES], validate=False))
+                for i in range(len(ts))]
     keeps, ptrs, dts = [], [], set()
     for T in tensors:
         ptr, dt, keep = _conv.device_input(T, srs.size, f"cuda:{ctx.device}")
@@ -254,6 +288,37 @@ def tc_commit_many(srs: Srs, tensors, *, scale_bits: int = SCALE_BITS, route: st
     del keeps
     return [Commitment(decode_elem(out.raw[i * ELEM_BYTES:(i + 1) * ELEM_BYTES], validate=False))
             for i in range(len(ptrs))]
+
+
+def tc_commit_stream(srs: Srs, cur, nxt=None, *, scale_bits: int = SCALE_BITS, route: str = "auto"):
+    """Streaming commits of host (CPU) float tensors, one call per forward: commits `cur`
+    while the upload of `nxt` (the next forward's tensors, or None) runs on the copy stream.
+    `cur` is consumed from the prefetched device slot when it is the previous call's `nxt`.
+    Tensors passed as `nxt` must not change until the call that commits them returns."""
+    ctx = _lib.Context.get(srs.device)
+    hc = _host_floats(list(cur))
+    if hc is None:
+        raise ValueError("tc_commit_stream: cur must be CPU float tensors of one dtype")
+    ts, code = hc
+    for t in ts:
+        if t.numel() != srs.size:
+            raise ValueError("tensor size does not match grid shape")
+    arr = (C.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
+    narr = None
+    if nxt is not None:
+        hn = _host_floats(list(nxt))
+        if hn is None or hn[1] != code or len(hn[0]) != len(ts):
+            raise ValueError("tc_commit_stream: nxt must match cur (count, dtype, CPU)")
+        if any(t.numel() != srs.size for t in hn[0]):
+            raise ValueError("tensor size does not match grid shape")
+        narr = (C.c_void_p * len(ts))(*[t.data_ptr() for t in hn[0]])
+    out = C.create_string_buffer(ELEM_BYTES * len(ts))
+    with ctx.lock:
+        ctx.bind_stream()
+        ctx.check(_lib.lib().tc_commit_stream(ctx.handle, srs.handle, arr, narr, len(ts), code, scale_bits,
+                                              _route(route), out), "tc_commit_stream")
+    return [Commitment(decode_elem(out.raw[i * ELEM_BYTES:(i + 1) * ELEM_BYTES], validate=False))
+            for i in range(len(ts))]
 
 
 def tc_open(srs: Srs, T, point, *, scale_bits: int = SCALE_BITS, route: str = "auto") -> TensorOpening:

@@ -1,6 +1,7 @@
 // C ABI of libtcb200.so (include/tc_b200.h): context / SRS management and the prover entry
 // points (quantize, interpolate, evaluate, open_quotients, msm, commit, open, Terkle build),
 // plus the CPU-side verifier primitive (pairing) that the reference keeps on the host.
+#include <algorithm>
 #include <cstdarg>
 #include <cstring>
 
@@ -425,6 +426,10 @@ int tc_ctx_destroy(tc_ctx* ctx) {
   cudaFreeHost(ctx->h_flags);
   cudaFreeHost(ctx->h_stage);
   if (ctx->ev[0]) cudaEventDestroy(ctx->ev[0]), cudaEventDestroy(ctx->ev[1]);
+  for (cudaEvent_t e : ctx->copy_ev) cudaEventDestroy(e);
+  for (auto& sl : ctx->slot)
+    if (sl.ready) cudaEventDestroy(sl.ready);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   delete ctx;
   return TC_OK;
 }
@@ -714,6 +719,131 @@ int tc_commit_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, in
                     int route, uint8_t* out43) {
   if (!ctx || !srs || !d_ins || !out43 || count < 0) return TC_ERR_ARGUMENT;
   return commit_many(ctx, srs, d_ins, count, dtype, scale_bits, route, out43);
+}
+
+static int dtype_size(int dtype, size_t* esz) {
+  switch (dtype) {
+    case TC_DTYPE_F16: case TC_DTYPE_BF16: *esz = 2; return TC_OK;
+    case TC_DTYPE_F32: *esz = 4; return TC_OK;
+    case TC_DTYPE_F64: *esz = 8; return TC_OK;
+    case TC_DTYPE_FP_LIMBS: *esz = sizeof(Fe); return TC_OK;
+    default: return TC_ERR_ARGUMENT;
+  }
+}
+
+static int ensure_copy_stream(tc_ctx* ctx) {
+  if (!ctx->copy_stream) TC_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  return TC_OK;
+}
+
+// Host-resident inputs: the layers are uploaded on a copy stream in groups of `group`
+// (0 = one group) and the ctx stream commits each group once it is resident.  Splitting a
+// forward into several MSM batches was measured SLOWER on config 3 (groups of 8: +3.4 ms of
+// per-batch reduction tails for 1.9 ms of hidden upload), so the default is one group; the
+// overlap that pays is across forwards (tc_commit_stream).
+int tc_commit_batch_host(tc_ctx* ctx, const tc_srs* srs, const void* const* h_ins, int count, int dtype,
+                         int scale_bits, int route, int group, uint8_t* out43) {
+  if (!ctx || !srs || !h_ins || !out43 || count < 0 || group < 0) return TC_ERR_ARGUMENT;
+  if (count == 0) return TC_OK;
+  size_t esz;
+  if (dtype_size(dtype, &esz)) return fail(ctx, TC_ERR_ARGUMENT, "commit_batch_host: unsupported dtype %d", dtype);
+  for (int i = 0; i < count; i++)
+    if (!h_ins[i]) return TC_ERR_ARGUMENT;
+  static const int G_ENV = getenv("TC_PIPE_GROUP") ? atoi(getenv("TC_PIPE_GROUP")) : 0;
+  int G = group ? group : (G_ENV > 0 ? G_ENV : count);
+  G = std::min(G, count);
+  const int ngroups = (count + G - 1) / G;
+  const size_t bytes = (size_t)srs->n * esz;
+  uint8_t* stage;
+  TC_TRY(tcrt::scratch(ctx, "host.stage", bytes * count, (void**)&stage));
+  TC_TRY(ensure_copy_stream(ctx));
+  while ((int)ctx->copy_ev.size() < ngroups) {
+    cudaEvent_t e;
+    TC_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->copy_ev.push_back(e);
+  }
+  // the staging buffer may still be read by earlier work on the ctx stream
+  TC_CUDA(ctx, cudaEventRecord(ctx->copy_ev[0], ctx->stream));
+  TC_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_ev[0], 0));
+  for (int g = 0; g < ngroups; g++) {
+    for (int i = g * G; i < std::min(count, (g + 1) * G); i++)
+      TC_CUDA(ctx, cudaMemcpyAsync(stage + bytes * i, h_ins[i], bytes, cudaMemcpyHostToDevice, ctx->copy_stream));
+    TC_CUDA(ctx, cudaEventRecord(ctx->copy_ev[g], ctx->copy_stream));
+  }
+  std::vector<const void*> ptrs(count);
+  for (int i = 0; i < count; i++) ptrs[i] = stage + bytes * i;
+  for (int g = 0; g < ngroups; g++) {
+    const int g0 = g * G, gc = std::min(G, count - g0);
+    TC_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->copy_ev[g], 0));
+    TC_TRY(commit_many(ctx, srs, ptrs.data() + g0, gc, dtype, scale_bits, route, out43 + 43 * (size_t)g0));
+  }
+  return TC_OK;
+}
+
+// upload `count` host tensors into stream slot s (copy stream), record its ready event
+static int slot_upload(tc_ctx* ctx, int s, const void* const* h, int count, int dtype, uint64_t n, size_t esz) {
+  auto& sl = ctx->slot[s];
+  uint8_t* dst;
+  TC_TRY(tcrt::scratch(ctx, s ? "stream.slot1" : "stream.slot0", (size_t)n * esz * count, (void**)&dst));
+  if (!sl.ready) TC_CUDA(ctx, cudaEventCreateWithFlags(&sl.ready, cudaEventDisableTiming));
+  for (int i = 0; i < count; i++)
+    TC_CUDA(ctx, cudaMemcpyAsync(dst + (size_t)n * esz * i, h[i], (size_t)n * esz, cudaMemcpyHostToDevice,
+                                 ctx->copy_stream));
+  TC_CUDA(ctx, cudaEventRecord(sl.ready, ctx->copy_stream));
+  sl.host.assign(h, h + count);
+  sl.dtype = dtype;
+  sl.n = n;
+  sl.valid = true;
+  return TC_OK;
+}
+
+// Streaming commits, one call per forward: commits h_cur and, before the commit starts,
+// enqueues the upload of h_next (the next forward's activations; may be NULL) on the copy
+// stream, so the PCIe transfer of forward k+1 runs under the MSMs of forward k.  h_cur is
+// consumed from the slot a previous call prefetched it into (same pointers, count, dtype),
+// else uploaded now.  Host buffers passed as h_next must not change until the call that
+// commits them returns.
+int tc_commit_stream(tc_ctx* ctx, const tc_srs* srs, const void* const* h_cur, const void* const* h_next, int count,
+                     int dtype, int scale_bits, int route, uint8_t* out43) {
+  if (!ctx || !srs || !h_cur || !out43 || count < 0) return TC_ERR_ARGUMENT;
+  if (count == 0) return TC_OK;
+  size_t esz;
+  if (dtype_size(dtype, &esz)) return fail(ctx, TC_ERR_ARGUMENT, "commit_stream: unsupported dtype %d", dtype);
+  for (int i = 0; i < count; i++)
+    if (!h_cur[i] || (h_next && !h_next[i])) return TC_ERR_ARGUMENT;
+  TC_TRY(ensure_copy_stream(ctx));
+  const uint64_t n = srs->n;
+  int s = -1;
+  for (int k = 0; k < 2 && s < 0; k++) {
+    const auto& sl = ctx->slot[k];
+    if (sl.valid && sl.dtype == dtype && sl.n == n && (int)sl.host.size() == count &&
+        std::equal(sl.host.begin(), sl.host.end(), h_cur))
+      s = k;
+  }
+  if (s < 0) {
+    s = 0;
+    // slot 0 may still be read by earlier work on the ctx stream
+    if (!ctx->slot[0].ready) TC_CUDA(ctx, cudaEventCreateWithFlags(&ctx->slot[0].ready, cudaEventDisableTiming));
+    TC_CUDA(ctx, cudaEventRecord(ctx->slot[0].ready, ctx->stream));
+    TC_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->slot[0].ready, 0));
+    TC_TRY(slot_upload(ctx, 0, h_cur, count, dtype, n, esz));
+  }
+  uint8_t* cur;
+  TC_TRY(tcrt::scratch(ctx, s ? "stream.slot1" : "stream.slot0", (size_t)n * esz * count, (void**)&cur));
+  TC_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->slot[s].ready, 0));
+  ctx->slot[s].valid = false;   // consumed by this call
+  if (h_next) {
+    // the other slot was last read by a previous call, which finished (commits end with a
+    // host synchronisation); order the copy after everything on the ctx stream anyway
+    auto& o = ctx->slot[1 - s];
+    if (!o.ready) TC_CUDA(ctx, cudaEventCreateWithFlags(&o.ready, cudaEventDisableTiming));
+    TC_CUDA(ctx, cudaEventRecord(o.ready, ctx->stream));
+    TC_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, o.ready, 0));
+    TC_TRY(slot_upload(ctx, 1 - s, h_next, count, dtype, n, esz));
+  }
+  std::vector<const void*> ptrs(count);
+  for (int i = 0; i < count; i++) ptrs[i] = cur + (size_t)n * esz * i;
+  return commit_many(ctx, srs, ptrs.data(), count, dtype, scale_bits, route, out43);
 }
 
 int tc_open(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int scale_bits, const uint8_t* omega_le21,

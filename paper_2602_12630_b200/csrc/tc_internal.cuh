@@ -36,6 +36,19 @@ struct tc_ctx {
   };
   std::map<std::string, Stat> stats;
   cudaEvent_t ev[2] = {nullptr, nullptr};
+  // host-input pipeline (tc_commit_batch_host): a copy stream and one event per group
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> copy_ev;
+  // streaming commits (tc_commit_stream): two device slots; a slot remembers which host
+  // buffers it was filled from so the next call can consume a prefetched upload
+  struct Slot {
+    std::vector<const void*> host;
+    int dtype = 0;
+    uint64_t n = 0;
+    bool valid = false;
+    cudaEvent_t ready = nullptr;
+  };
+  Slot slot[2];
 };
 
 struct tc_srs {

@@ -10,7 +10,7 @@ from dataclasses import dataclass
 
 from . import _conv, _lib
 from .authtree import TreeConfig, build, leaf_of
-from .commit import SCALE_BITS, tc_commit_many
+from .commit import SCALE_BITS, tc_commit_many, tc_commit_stream
 
 
 @dataclass
@@ -75,3 +75,25 @@ def prover_commit(tensors, srs_pool, *, tree_config: TreeConfig = None, scale_bi
     cfg = tree_config or TreeConfig()
     tree, root = build(cfg, [leaf_of(c) for c in commitments])
     return commitments, root, tree
+
+
+def prover_commit_stream(batches, srs, *, tree_config: TreeConfig = None, node_srs=None,
+                         scale_bits: int = SCALE_BITS, route: str = "auto"):
+    """prover_commit over a stream of forwards (an iterable of per-forward lists of HOST
+    tensors sharing one SRS): yields (commitments, root, tree) per forward.  The upload of
+    forward k+1's activations overlaps the commitments of forward k (tc_commit_stream)."""
+    cfg = tree_config or TreeConfig()
+    it = iter(batches)
+    try:
+        cur = list(next(it))
+    except StopIteration:
+        return
+    while cur is not None:
+        try:
+            nxt = list(next(it))
+        except StopIteration:
+            nxt = None
+        commitments = tc_commit_stream(srs, cur, nxt, scale_bits=scale_bits, route=route)
+        tree, root = build(cfg, [leaf_of(c) for c in commitments], srs=node_srs)
+        yield commitments, root, tree
+        cur = nxt

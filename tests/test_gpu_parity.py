@@ -258,6 +258,53 @@ def test_prover_commit_small_layers():
     assert root_c != root
 
 
+@pytest.mark.parametrize("group", [0, 1, 2, 5])
+@pytest.mark.parametrize("pinned", [True, False])
+def test_commit_many_host_inputs_pipelined(group, pinned):
+    """Host (CPU) inputs go through tc_commit_batch_host (grouped upload on a copy stream
+    overlapped with the commits): identical commitments to the device-input path and the
+    trapdoor oracle, for every grouping and for pinned and pageable memory."""
+    tcb = T()
+    shape = (8, 8, 16)
+    srs, td = tcb.setup_srs(shape, b"host-pipe")
+    g = np.random.default_rng(23)
+    xs = [(g.standard_t(3, 1024) * s).astype(np.float16) for s in (0.5, 1.0, 2.0, 3.0, 4.0)]
+    host = [torch.from_numpy(x) for x in xs]
+    if pinned:
+        host = [h.pin_memory() for h in host]
+    got = tcb.tc_commit_many(srs, host, group=group)
+    dev = tcb.tc_commit_many(srs, [h.cuda() for h in host])
+    assert [c.elem for c in got] == [c.elem for c in dev]
+    want = [O.commit_trapdoor(O.quantize(x.astype(np.float64), 16), shape, list(td.taus)) for x in xs]
+    assert [c.elem for c in got] == want
+    # numpy float inputs take the same path
+    assert [c.elem for c in tcb.tc_commit_many(srs, xs)] == want
+
+
+def test_commit_stream_prefetch_and_prover_stream():
+    """tc_commit_stream / prover_commit_stream: each forward's commitments equal the
+    one-shot path whether its inputs were prefetched by the previous call or not, and
+    mismatched prefetches (different buffers) are re-uploaded, not reused."""
+    tcb = T()
+    shape = (8, 8, 16)
+    srs, td = tcb.setup_srs(shape, b"host-stream")
+    g = np.random.default_rng(29)
+    fwd = [[torch.from_numpy((g.standard_t(3, 1024) * s).astype(np.float16)).pin_memory() for s in (0.5, 2.0, 4.0)]
+           for _ in range(4)]
+    want = [[c.elem for c in tcb.tc_commit_many(srs, [t.cuda() for t in f])] for f in fwd]
+    got = [[c.elem for c in tcb.tc_commit_stream(srs, fwd[k], fwd[k + 1] if k + 1 < 4 else None)] for k in range(4)]
+    assert got == want
+    # prefetch of fwd[1] but then commit fwd[2]: must upload fwd[2], not reuse the slot
+    tcb.tc_commit_stream(srs, fwd[0], fwd[1])
+    assert [c.elem for c in tcb.tc_commit_stream(srs, fwd[2])] == want[2]
+    # prefetched buffer consumed once: committing it again re-uploads the same bytes
+    assert [c.elem for c in tcb.tc_commit_stream(srs, fwd[2])] == want[2]
+    roots = [r for _, r, _ in tcb.prover_commit_stream(fwd, srs)]
+    for f, r in zip(fwd, roots):
+        _, root, _ = tcb.prover_commit([t.cuda() for t in f], srs)
+        assert r == root
+
+
 # ---------------------------------------------------------------- full-size configs
 def _config3_layer(l):
     scales = np.random.default_rng(12345).uniform(0.5, 4.0, 32)

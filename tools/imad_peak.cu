@@ -60,6 +60,45 @@ __global__ void k_madd(uint32_t* out, const Aff* pts, int npts, int iters) {
   if (acc.X.v[0] == 0x12345678) out[0] = acc.X.v[1];
 }
 
+// FP64 pipe: independent DFMA chains; MODE 1 mixes 8 DFMA + 8 IMAD chains to see whether
+// the two pipes issue concurrently (a hybrid integer/float multiprecision design needs it).
+template <int MODE>
+__global__ void k_dfma(uint32_t* out, double seed, int iters) {
+  double d[16];
+  uint32_t a[8];
+  const double b = seed * 1.0000001 + threadIdx.x * 1e-9;
+  const uint32_t bi = __double2uint_rz(seed) ^ (threadIdx.x * 2654435761u);
+#pragma unroll
+  for (int i = 0; i < 16; i++) d[i] = seed * (i + 1) + threadIdx.x;
+#pragma unroll
+  for (int i = 0; i < 8; i++) a[i] = bi * (i + 3);
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int i = 0; i < 16; i++) {
+      if (MODE == 0 || (MODE < 4 && i < 8)) asm volatile("fma.rn.f64 %0, %0, %1, %1;" : "+d"(d[i]) : "d"(b));
+      if (MODE == 4) {
+        uint64_t w;
+        asm volatile("mad.wide.u32 %0, %1, %2, %3;" : "=l"(w) : "r"(a[i & 7]), "r"(bi), "l"((uint64_t)a[i & 7]));
+        a[i & 7] = (uint32_t)(w >> 32) ^ (uint32_t)w;
+      }
+      if (MODE == 1 && i >= 8) asm volatile("mad.lo.u32 %0, %0, %1, %0;" : "+r"(a[i - 8]) : "r"(bi));
+      if (MODE == 2 && i >= 8) asm volatile("mad.hi.u32 %0, %0, %1, %0;" : "+r"(a[i - 8]) : "r"(bi));
+      if (MODE == 3 && i >= 8) {   // dependent 32x32->64 multiply-add (IMAD.WIDE), not hoistable
+        uint64_t w;
+        asm volatile("mad.wide.u32 %0, %1, %2, %3;" : "=l"(w) : "r"(a[i - 8]), "r"(bi), "l"((uint64_t)a[i - 8]));
+        a[i - 8] = (uint32_t)(w >> 32) ^ (uint32_t)w;
+      }
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; i++) s += d[i];
+  uint32_t t = 0;
+#pragma unroll
+  for (int i = 0; i < 8; i++) t ^= a[i];
+  if (s == 1.2345 || t == 0x12345678) out[0] = t;
+}
+
 int main() {
   cudaDeviceProp prop;
   cudaGetDeviceProperties(&prop, 0);
@@ -90,6 +129,16 @@ int main() {
   printf("{\"op\": \"mad.lo.u32\", \"Tops\": %.3f}\n", n16 / t0 / 1e9);
   printf("{\"op\": \"mad.hi.u32\", \"Tops\": %.3f}\n", n16 / t1 / 1e9);
   printf("{\"op\": \"mad.wide.u32 (64-bit acc)\", \"Tops\": %.3f}\n", n8 / t2 / 1e9);
+  float td0 = timeit([&] { k_dfma<0><<<blocks, threads>>>(out, 0.5, iters); });
+  float td1 = timeit([&] { k_dfma<1><<<blocks, threads>>>(out, 0.5, iters); });
+  printf("{\"op\": \"fma.rn.f64\", \"Tops\": %.3f}\n", n16 / td0 / 1e9);
+  float td2 = timeit([&] { k_dfma<2><<<blocks, threads>>>(out, 0.5, iters); });
+  float td3 = timeit([&] { k_dfma<3><<<blocks, threads>>>(out, 0.5, iters); });
+  float td4 = timeit([&] { k_dfma<4><<<blocks, threads>>>(out, 0.5, iters); });
+  printf("{\"op\": \"8 fma.f64 + 8 mad.hi\", \"ms\": %.3f}\n", td2);
+  printf("{\"op\": \"8 fma.f64 + 8 mad.wide(+xor)\", \"ms\": %.3f}\n", td3);
+  printf("{\"op\": \"16 mad.wide(+xor)\", \"ms\": %.3f}\n", td4);
+  printf("{\"op\": \"8 fma.f64 + 8 mad.lo chains\", \"ms\": %.3f, \"ms_imad16\": %.3f, \"ms_dfma16\": %.3f}\n", td1, t0, td0);
   for (int tpb : {128, 256, 384}) {
     int it = 512;
     float t = timeit([&] { k_fqmul<<<sms * 8, tpb>>>(out, 11, it); });
