@@ -287,6 +287,17 @@ int srs_build_points(tc_ctx* ctx, tc_srs* srs, const std::vector<Fe>& taus, bool
   return srs_fill_points(ctx, srs->shape, srs->m, taus.data(), lagrange, *dst);
 }
 
+// Edwards copies of every basis the Pippenger pipeline may read (built at setup, so the
+// shared read-only SRS is never mutated by a commit)
+int srs_build_edwards(tc_ctx* ctx, tc_srs* srs) {
+  const EdAff* e;
+  if (srs->n <= SMALL_MSM_MAX && !srs->sublag) return TC_OK;   // node SRSs use the table kernel
+  if (srs->monomial) TC_TRY(tcrt::srs_edwards(ctx, srs, TC_SRS_MONOMIAL, &e));
+  if (srs->lagrange) TC_TRY(tcrt::srs_edwards(ctx, srs, TC_SRS_LAGRANGE, &e));
+  if (srs->sublag) TC_TRY(tcrt::srs_edwards(ctx, srs, 0, &e));
+  return TC_OK;
+}
+
 // sub-grid Lagrange sets for the suffixes i = 1..m-1 (Lagrange-route opening quotients)
 int srs_build_sublag(tc_ctx* ctx, tc_srs* srs, const std::vector<Fe>& taus) {
   if (srs->m < 2) return TC_OK;
@@ -489,6 +500,7 @@ int tc_srs_generate(tc_ctx* ctx, const uint32_t* shape, int m, const uint8_t* ta
   if (flags & TC_SRS_MONOMIAL) s = srs_build_points(ctx, srs, taus, false, &srs->monomial);
   if (!s && (flags & TC_SRS_LAGRANGE)) s = srs_build_points(ctx, srs, taus, true, &srs->lagrange);
   if (!s && (flags & TC_SRS_LAGRANGE)) s = srs_build_sublag(ctx, srs, taus);
+  s = s ? s : srs_build_edwards(ctx, srs);
   if (!s) {   // axis elements g^{tau_j}
     Fe* d_t;
     Aff* d_a;
@@ -538,6 +550,7 @@ int tc_srs_load(tc_ctx* ctx, const uint32_t* shape, int m, const uint8_t* monomi
     else if (ctx->h_flags[0])
       s = fail(ctx, TC_ERR_VALUE, "srs element: bad encoding or point not on curve");
   }
+  if (!s) s = srs_build_edwards(ctx, srs);
   if (s) {
     tc_srs_destroy(srs);
     return s;
@@ -582,6 +595,8 @@ int tc_srs_destroy(tc_srs* srs) {
   for (auto* t : srs->small_tab)
     if (t) cudaFree(t);
   if (srs->sublag) cudaFree(srs->sublag);
+  for (auto* e : {srs->ed_monomial, srs->ed_lagrange, srs->ed_sublag})
+    if (e) cudaFree(e);
   delete srs;
   return TC_OK;
 }
@@ -627,8 +642,8 @@ int tc_open_quotients(tc_ctx* ctx, const uint32_t* d_coeffs, const uint32_t* sha
 
 int tc_msm(tc_ctx* ctx, const tc_srs* srs, int which, const uint32_t* d_scalars, uint64_t n, uint8_t* out43) {
   if (!ctx || !srs || !out43 || (n && !d_scalars)) return TC_ERR_ARGUMENT;
-  const Aff* bases = (which == TC_SRS_LAGRANGE) ? srs->lagrange : srs->monomial;
-  if (!bases) return fail(ctx, TC_ERR_VALUE, "srs has no elements of kind %d", which);
+  const EdAff* bases;
+  TC_TRY(tcrt::srs_edwards(ctx, const_cast<tc_srs*>(srs), which, &bases));
   if (n > srs->n) return fail(ctx, TC_ERR_VALUE, "msm: %llu scalars for an srs of %llu elements",
                               (unsigned long long)n, (unsigned long long)srs->n);
   Aff* d_out;
@@ -654,10 +669,13 @@ static int fetch_encode_many(tc_ctx* ctx, const Aff* d_pts, int L, uint8_t* out4
 // (Terkle nodes), the batched Pippenger pipeline otherwise
 static int msm_srs(tc_ctx* ctx, const tc_srs* srs, int which, int dtype, int scale_bits, const void* const* ptrs,
                    int L, Aff* d_out) {
-  const Aff* bases = (which == TC_SRS_LAGRANGE) ? srs->lagrange : srs->monomial;
-  if (!bases) return fail(ctx, TC_ERR_VALUE, "srs has no elements of kind %d", which);
-  if (srs->n > SMALL_MSM_MAX)
+  if (!((which == TC_SRS_LAGRANGE) ? srs->lagrange : srs->monomial))
+    return fail(ctx, TC_ERR_VALUE, "srs has no elements of kind %d", which);
+  if (srs->n > SMALL_MSM_MAX) {
+    const EdAff* bases;
+    TC_TRY(tcrt::srs_edwards(ctx, const_cast<tc_srs*>(srs), which, &bases));
     return tcrt::msm_batch_device(ctx, dtype, scale_bits, ptrs, L, bases, srs->n, d_out);
+  }
   std::vector<const void*> fp(ptrs, ptrs + L);
   if (dtype != TC_DTYPE_FP_LIMBS) {   // quantise first: the table kernel takes field elements
     Fe* q;
@@ -899,8 +917,11 @@ int tc_open(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int sca
     Aff* d_out;
     TC_TRY(tcrt::scratch_t(ctx, "open.out", (uint64_t)m, &d_out));
     uint64_t span = n;
+    const EdAff *ed_lag, *ed_sub = nullptr;
+    TC_TRY(tcrt::srs_edwards(ctx, const_cast<tc_srs*>(srs), TC_SRS_LAGRANGE, &ed_lag));
+    if (m > 1) TC_TRY(tcrt::srs_edwards(ctx, const_cast<tc_srs*>(srs), 0, &ed_sub));
     for (int a = 0; a < m; a++) {
-      const Aff* bases = a == 0 ? srs->lagrange : srs->sublag + srs->sublag_off[a];
+      const EdAff* bases = a == 0 ? ed_lag : ed_sub + srs->sublag_off[a];
       const void* ptr = qs + (uint64_t)a * n;
       TC_TRY(tcrt::msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, &ptr, 1, bases, span, d_out + a));
       span /= srs->shape[a];

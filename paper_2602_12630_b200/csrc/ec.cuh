@@ -206,4 +206,119 @@ TC_HD void aff_encode43(const Aff& p, uint8_t out[43]) {
   }
 }
 
+// ---- twisted Edwards model for the MSM ---------------------------------------------------
+// The reference curve y^2 = x^3 + x is the Montgomery curve B v^2 = u^3 + A u^2 + u with
+// A = 0, B = 1, hence birational to the twisted Edwards curve a x^2 + y^2 = 1 + d x^2 y^2
+// with a = (A+2)/B = 2, d = (A-2)/B = -2 via x = u/v, y = (u-1)/(u+1).  Over F_q
+// (q = 7 mod 8) a = 2 is a square and d = -2 is not, so the unified extended-coordinate
+// addition (Hisil-Wong-Carter-Dawson 2008) is COMPLETE: no branch for P + P, P - P or the
+// neutral element.  A mixed add costs 8M (XYZZ: 8M + 2S), a full add 9M (XYZZ: 12M + 2S),
+// and d = -2, a = 2 are additions.  The map is defined on the whole odd-order subgroup
+// the SRS lives in; only the Montgomery 2-torsion point (0, 0) <-> (0, -1) is special.
+// Affine points carry t = x*y (precomputed when the SRS is converted).
+struct EdAff {
+  Fe x, y, t;
+};
+struct Ext {
+  Fe X, Y, Z, T;
+};
+
+TC_HD Ext ext_zero() { return Ext{Fq::zero(), Fq::one(), Fq::one(), Fq::zero()}; }
+TC_HD Ext ext_from_aff(const EdAff& p) { return Ext{p.x, p.y, Fq::one(), p.t}; }
+TC_HD EdAff edaff_neg(const EdAff& p) { return EdAff{Fq::neg(p.x), p.y, Fq::neg(p.t)}; }
+TC_HD Ext ext_neg(const Ext& p) { return Ext{Fq::neg(p.X), p.Y, p.Z, Fq::neg(p.T)}; }
+
+// acc += q (q affine with t = x y): madd-2008-hwcd, a = 2, d = -2
+TC_HD void ext_madd(Ext& acc, const EdAff& q) {
+  const Fe A = Fq::mul(acc.X, q.x);
+  const Fe B = Fq::mul(acc.Y, q.y);
+  const Fe C2 = Fq::dbl(Fq::mul(acc.T, q.t));   // -d T1 T2
+  const Fe E = Fq::sub(Fq::sub(Fq::mul(Fq::add(acc.X, acc.Y), Fq::add(q.x, q.y)), A), B);
+  const Fe F = Fq::add(acc.Z, C2);               // Z1 - d T1 T2
+  const Fe G = Fq::sub(acc.Z, C2);               // Z1 + d T1 T2
+  const Fe H = Fq::sub(B, Fq::dbl(A));           // B - a A
+  acc.X = Fq::mul(E, F);
+  acc.Y = Fq::mul(G, H);
+  acc.T = Fq::mul(E, H);
+  acc.Z = Fq::mul(F, G);
+}
+
+// acc += q, both extended: add-2008-hwcd (unified, complete here)
+TC_HD void ext_add(Ext& acc, const Ext& q) {
+  const Fe A = Fq::mul(acc.X, q.X);
+  const Fe B = Fq::mul(acc.Y, q.Y);
+  const Fe C2 = Fq::dbl(Fq::mul(acc.T, q.T));
+  const Fe D = Fq::mul(acc.Z, q.Z);
+  const Fe E = Fq::sub(Fq::sub(Fq::mul(Fq::add(acc.X, acc.Y), Fq::add(q.X, q.Y)), A), B);
+  const Fe F = Fq::add(D, C2);
+  const Fe G = Fq::sub(D, C2);
+  const Fe H = Fq::sub(B, Fq::dbl(A));
+  acc.X = Fq::mul(E, F);
+  acc.Y = Fq::mul(G, H);
+  acc.T = Fq::mul(E, H);
+  acc.Z = Fq::mul(F, G);
+}
+
+// 2P: dbl-2008-hwcd, a = 2 (4M + 4S)
+TC_HD Ext ext_dbl(const Ext& p) {
+  const Fe A = Fq::sqr(p.X);
+  const Fe B = Fq::sqr(p.Y);
+  const Fe C = Fq::dbl(Fq::sqr(p.Z));
+  const Fe D = Fq::dbl(A);
+  const Fe E = Fq::sub(Fq::sub(Fq::sqr(Fq::add(p.X, p.Y)), A), B);
+  const Fe G = Fq::add(D, B);
+  const Fe F = Fq::sub(G, C);
+  const Fe H = Fq::sub(D, B);
+  return Ext{Fq::mul(E, F), Fq::mul(G, H), Fq::mul(F, G), Fq::mul(E, H)};
+}
+
+// k * P for a small non-negative k, double-and-add from the MSB
+TC_HD Ext ext_mul_small(const Ext& p, uint32_t k) {
+  Ext r = ext_zero();
+  bool started = false;
+  for (int b = 31; b >= 0; b--) {
+    if (started) r = ext_dbl(r);
+    if ((k >> b) & 1u) {
+      if (started) {
+        ext_add(r, p);
+      } else {
+        r = p;
+        started = true;
+      }
+    }
+  }
+  return r;
+}
+
+// Edwards (X:Y:Z:T) -> Montgomery affine (u, v) = ((Z+Y)/(Z-Y), (Z+Y) Z / ((Z-Y) X)),
+// one inversion.  Neutral -> infinity; (0 : -1) -> the 2-torsion point (0, 0).
+TC_HD Aff ext_to_aff(const Ext& p) {
+  if (Fq::is_zero(p.X)) {
+    if (Fq::eq(p.Y, p.Z)) return aff_inf();
+    return Aff{Fq::zero(), Fq::zero()};
+  }
+  const Fe zpy = Fq::add(p.Z, p.Y);
+  const Fe inv = Fq::inv(Fq::mul(Fq::sub(p.Z, p.Y), p.X));
+  return Aff{Fq::mul(Fq::mul(zpy, p.X), inv), Fq::mul(Fq::mul(zpy, p.Z), inv)};
+}
+
+// Montgomery affine -> Edwards affine given inv = 1 / (v (u + 1)):
+// x = u / v = u (u + 1) inv, y = (u - 1) / (u + 1) = (u - 1) v inv, t = x y.
+// `den` returns v (u + 1) (1 for the special points so a batch inversion stays valid).
+TC_HD Fe aff_ed_den(const Aff& p) {
+  if (aff_is_inf(p) || Fq::is_zero(p.y)) return Fq::one();
+  return Fq::mul(p.y, Fq::add(p.x, Fq::one()));
+}
+TC_HD EdAff aff_to_ed_with_inv(const Aff& p, const Fe& inv) {
+  if (aff_is_inf(p)) return EdAff{Fq::zero(), Fq::one(), Fq::zero()};
+  if (Fq::is_zero(p.y)) return EdAff{Fq::zero(), Fq::neg(Fq::one()), Fq::zero()};   // (0,0) -> (0,-1)
+  const Fe x = Fq::mul(Fq::mul(p.x, Fq::add(p.x, Fq::one())), inv);
+  const Fe y = Fq::mul(Fq::mul(Fq::sub(p.x, Fq::one()), p.y), inv);
+  return EdAff{x, y, Fq::mul(x, y)};
+}
+TC_HD EdAff aff_to_ed(const Aff& p) {
+  const Fe d = aff_ed_den(p);
+  return aff_to_ed_with_inv(p, Fq::inv(d));
+}
+
 }  // namespace tc

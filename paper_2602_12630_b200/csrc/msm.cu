@@ -18,13 +18,16 @@
 //   4. radix sort     — (key, value) by bucket, CUB onesweep over the used key bits
 //   5. k_bounds       — [start, end) of every bucket
 //   6. levels         — load-balanced segmented reduction: buckets are cut into pieces of
-//                       <= T entries (one thread per piece, XYZZ accumulator, mixed affine
-//                       adds); single-piece buckets are final at once, multi-piece buckets
-//                       (the heavy tail) feed further levels of T1-way reduction
+//                       <= T entries (one thread per piece, extended twisted Edwards
+//                       accumulator, complete 8M mixed adds, ec.cuh); single-piece buckets
+//                       are final at once, multi-piece buckets (the heavy tail) feed
+//                       further levels of T1-way reduction
 //   7. k_bucket_reduce— per segment of buckets: sum_b b * B_b by running sums
 //   8. k_window_sum, k_final — segments -> window sums -> Horner over the windows -> affine
 // Affine outputs are canonical and the group is abelian, so any window layout, bucket
-// order or coordinate system reproduces the reference's bytes exactly.
+// order or coordinate system reproduces the reference's bytes exactly.  The bases are the
+// SRS points mapped to the twisted Edwards model of the curve (tc_srs::ed_*, built once per
+// SRS); results are mapped back to Montgomery affine by k_final.
 #include <cub/cub.cuh>
 
 #include "quant.cuh"
@@ -353,11 +356,13 @@ __device__ __forceinline__ uint32_t find_bucket(const uint32_t* off, uint32_t nb
   return lo;
 }
 
-// level 0: entries are (sign | point index) into the shared affine bases.  A bucket that
-// fits in one piece is final (written to buckets[k]); otherwise its piece sums go to items.
-__global__ void __launch_bounds__(128) k_accum_aff(const uint32_t* vals, const Aff* bases, const uint32_t* bstart,
+// level 0: entries are (sign | point index) into the shared Edwards affine bases.  A bucket
+// that fits in one piece is final (written to buckets[k]); otherwise its piece sums go to
+// items.  The accumulator starts as the piece's first point, then one complete 8M mixed
+// add per entry (no exceptional cases, ec.cuh).
+__global__ void __launch_bounds__(128) k_accum_aff(const uint32_t* vals, const EdAff* bases, const uint32_t* bstart,
                                                    const uint32_t* bend, const uint32_t* toff, const uint32_t* ooff,
-                                                   uint32_t nb, uint32_t T, Xyzz* items, Xyzz* buckets) {
+                                                   uint32_t nb, uint32_t T, Ext* items, Ext* buckets) {
   uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t total = toff[nb];
   if (p >= total) return;
@@ -365,12 +370,15 @@ __global__ void __launch_bounds__(128) k_accum_aff(const uint32_t* vals, const A
   uint32_t piece = p - toff[k];
   uint32_t a = bstart[k] + piece * T;
   uint32_t b = min(a + T, bend[k]);
-  Xyzz acc = xyzz_inf();
-  for (uint32_t j = a; j < b; j++) {
-    uint32_t v = vals[j];
-    Aff q = bases[v & ~SIGN_BIT];
-    if (v & SIGN_BIT) q.y = Fq::neg(q.y);
-    xyzz_add_aff(acc, q);
+  uint32_t v = vals[a];
+  EdAff q = bases[v & ~SIGN_BIT];
+  if (v & SIGN_BIT) q = edaff_neg(q);
+  Ext acc = ext_from_aff(q);
+  for (uint32_t j = a + 1; j < b; j++) {
+    v = vals[j];
+    q = bases[v & ~SIGN_BIT];
+    if (v & SIGN_BIT) q = edaff_neg(q);
+    ext_madd(acc, q);
   }
   if (toff[k + 1] - toff[k] == 1)
     buckets[k] = acc;
@@ -378,10 +386,16 @@ __global__ void __launch_bounds__(128) k_accum_aff(const uint32_t* vals, const A
     items[ooff[k] + piece] = acc;
 }
 
+// empty buckets hold the neutral element (0 : 1 : 1 : 0)
+__global__ void k_fill_zero(Ext* b, uint32_t n) {
+  uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) b[k] = ext_zero();
+}
+
 // level >= 1: bucket k's items are in[iofs[k] .. iofs[k+1])
-__global__ void __launch_bounds__(128) k_accum_xyzz(const Xyzz* in, const uint32_t* iofs, const uint32_t* toff,
-                                                    const uint32_t* ooff, uint32_t nb, uint32_t T, Xyzz* out,
-                                                    Xyzz* buckets) {
+__global__ void __launch_bounds__(128) k_accum_ext(const Ext* in, const uint32_t* iofs, const uint32_t* toff,
+                                                    const uint32_t* ooff, uint32_t nb, uint32_t T, Ext* out,
+                                                    Ext* buckets) {
   uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t total = toff[nb];
   if (p >= total) return;
@@ -389,8 +403,8 @@ __global__ void __launch_bounds__(128) k_accum_xyzz(const Xyzz* in, const uint32
   uint32_t piece = p - toff[k];
   uint32_t a = iofs[k] + piece * T;
   uint32_t b = min(a + T, iofs[k + 1]);
-  Xyzz acc = in[a];
-  for (uint32_t j = a + 1; j < b; j++) xyzz_add(acc, in[j]);
+  Ext acc = in[a];
+  for (uint32_t j = a + 1; j < b; j++) ext_add(acc, in[j]);
   if (toff[k + 1] - toff[k] == 1)
     buckets[k] = acc;
   else
@@ -399,8 +413,8 @@ __global__ void __launch_bounds__(128) k_accum_xyzz(const Xyzz* in, const uint32
 
 // segment s covers buckets [s*LS, (s+1)*LS) of the global bucket array (LS divides every
 // window's bucket count): sum_b (digit_b) * B_b with digit_b = b - base_w + 1
-__global__ void __launch_bounds__(128, 4) k_bucket_reduce(const Xyzz* buckets, WinPlan P, uint32_t nseg_total,
-                                                       uint32_t LS, Xyzz* segs) {
+__global__ void __launch_bounds__(128, 4) k_bucket_reduce(const Ext* buckets, WinPlan P, uint32_t nseg_total,
+                                                       uint32_t LS, Ext* segs) {
   uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= nseg_total) return;
   uint32_t g = s * LS;
@@ -408,32 +422,32 @@ __global__ void __launch_bounds__(128, 4) k_bucket_reduce(const Xyzz* buckets, W
   int w = 0;
   while (w + 1 < P.nwin && P.base[w + 1] <= r) w++;
   uint32_t lo = r - P.base[w];   // digit of the segment's first bucket minus 1
-  const Xyzz* bw = buckets + g;
-  Xyzz run = xyzz_inf(), sum = xyzz_inf();
+  const Ext* bw = buckets + g;
+  Ext run = ext_zero(), sum = ext_zero();
   for (int b = (int)LS - 1; b >= 0; b--) {
-    xyzz_add(run, bw[b]);
-    xyzz_add(sum, run);
+    ext_add(run, bw[b]);
+    ext_add(sum, run);
   }
   if (lo) {   // sum_b (b + 1) B_b + lo * sum_b B_b
-    Xyzz extra = xyzz_mul_small(run, lo);
-    xyzz_add(sum, extra);
+    Ext extra = ext_mul_small(run, lo);
+    ext_add(sum, extra);
   }
   segs[s] = sum;
 }
 
 // one block per (msm, window): tree-sum the window's segments
-__global__ void __launch_bounds__(128) k_window_sum(const Xyzz* segs, WinPlan P, uint32_t LS, Xyzz* wsum) {
-  __shared__ Xyzz sh[128];
+__global__ void __launch_bounds__(128) k_window_sum(const Ext* segs, WinPlan P, uint32_t LS, Ext* wsum) {
+  __shared__ Ext sh[128];
   const uint32_t l = blockIdx.x / P.nwin, w = blockIdx.x % P.nwin;
   const uint32_t s0 = (l * P.nbm + P.base[w]) / LS, s1 = (l * P.nbm + P.base[w + 1]) / LS;
-  Xyzz acc = xyzz_inf();
-  for (uint32_t s = s0 + threadIdx.x; s < s1; s += blockDim.x) xyzz_add(acc, segs[s]);
+  Ext acc = ext_zero();
+  for (uint32_t s = s0 + threadIdx.x; s < s1; s += blockDim.x) ext_add(acc, segs[s]);
   sh[threadIdx.x] = acc;
   __syncthreads();
   for (uint32_t st = blockDim.x / 2; st; st >>= 1) {
     if (threadIdx.x < st) {
-      Xyzz a = sh[threadIdx.x];
-      xyzz_add(a, sh[threadIdx.x + st]);
+      Ext a = sh[threadIdx.x];
+      ext_add(a, sh[threadIdx.x + st]);
       sh[threadIdx.x] = a;
     }
     __syncthreads();
@@ -460,8 +474,8 @@ struct GroupTab {   // per group: input offset, input count, output offset (devi
   uint32_t ngroups;
 };
 
-__global__ void __launch_bounds__(128) k_wsum_level(const Xyzz* Tin, const Xyzz* Din, GroupTab G, uint32_t total_out,
-                                                    uint32_t dbl_shift, uint32_t SEG, Xyzz* Tout, Xyzz* Dout) {
+__global__ void __launch_bounds__(128) k_wsum_level(const Ext* Tin, const Ext* Din, GroupTab G, uint32_t total_out,
+                                                    uint32_t dbl_shift, uint32_t SEG, Ext* Tout, Ext* Dout) {
   const uint32_t o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= total_out) return;
   uint32_t lo = 0, hi = G.ngroups;   // group g with out_off[g] <= o < out_off[g+1]
@@ -475,42 +489,42 @@ __global__ void __launch_bounds__(128) k_wsum_level(const Xyzz* Tin, const Xyzz*
   const uint32_t g = lo, k = o - G.out_off[g];
   const uint32_t a = G.in_off[g] + k * SEG;
   const uint32_t len = min(SEG, G.in_cnt[g] - k * SEG);
-  Xyzz run = xyzz_inf(), u = xyzz_inf();
+  Ext run = ext_zero(), u = ext_zero();
   for (int j = (int)len - 1; j >= 0; j--) {
-    xyzz_add(run, Tin[a + j]);
-    xyzz_add(u, run);
+    ext_add(run, Tin[a + j]);
+    ext_add(u, run);
   }
   Tout[o] = run;
   // D_out = sum of D_in over the segment + SEG^{r-1} * U
-  for (uint32_t i = 0; i < dbl_shift; i++) u = xyzz_dbl(u);
+  for (uint32_t i = 0; i < dbl_shift; i++) u = ext_dbl(u);
   if (Din)
-    for (uint32_t j = 0; j < len; j++) xyzz_add(u, Din[a + j]);
+    for (uint32_t j = 0; j < len; j++) ext_add(u, Din[a + j]);
   Dout[o] = u;
 }
 
 // W_g = D_g - c * S_g
-__global__ void k_wsum_final(const Xyzz* T, const Xyzz* D, uint32_t ngroups, uint32_t c, Xyzz* W) {
+__global__ void k_wsum_final(const Ext* T, const Ext* D, uint32_t ngroups, uint32_t c, Ext* W) {
   const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= ngroups) return;
-  Xyzz w = D[g];
+  Ext w = D[g];
   if (c) {
-    Xyzz s = xyzz_mul_small(T[g], c);
-    xyzz_add(w, xyzz_neg(s));
+    Ext s = ext_mul_small(T[g], c);
+    ext_add(w, ext_neg(s));
   }
   W[g] = w;
 }
 
 // Horner over the windows of MSM l: acc = 2^{c_w} acc + S_w from the top, then affine
-__global__ void k_final(const Xyzz* wsum, uint32_t L, WinPlan P, Aff* out) {
+__global__ void k_final(const Ext* wsum, uint32_t L, WinPlan P, Aff* out) {
   uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= L) return;
-  const Xyzz* ws = wsum + (uint64_t)l * P.nwin;
-  Xyzz acc = ws[P.nwin - 1];
+  const Ext* ws = wsum + (uint64_t)l * P.nwin;
+  Ext acc = ws[P.nwin - 1];
   for (int w = P.nwin - 2; w >= 0; w--) {
-    for (int i = 0; i < P.width[w]; i++) acc = xyzz_dbl(acc);
-    xyzz_add(acc, ws[w]);
+    for (int i = 0; i < P.width[w]; i++) acc = ext_dbl(acc);
+    ext_add(acc, ws[w]);
   }
-  Aff r = xyzz_to_aff(acc);
+  Aff r = ext_to_aff(acc);
   if (!aff_is_inf(r)) {
     r.x = Fq::canon(r.x);
     r.y = Fq::canon(r.y);
@@ -608,7 +622,7 @@ namespace tcrt {
 
 int quantize_flags_to_status(tc_ctx* ctx, uint32_t f);
 
-int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* h_ptrs, int L, const Aff* d_bases,
+int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* h_ptrs, int L, const EdAff* d_bases,
                      uint64_t n, Aff* d_out) {
   cudaStream_t st = ctx->stream;
   if (L <= 0) return TC_OK;
@@ -774,7 +788,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   // items = pieces of multi-piece buckets: ceil(sz/T) <= 2 sz / T for sz > T
   const uint64_t max_items = 2 * ((E + T - 1) / T) + 2;
   uint32_t *np, *npm, *toff, *offA, *offB;
-  Xyzz *itemsA, *itemsB, *buckets;
+  Ext *itemsA, *itemsB, *buckets;
   TC_TRY(scratch_t(ctx, "msm.np", (uint64_t)nb + 1, &np));
   TC_TRY(scratch_t(ctx, "msm.npm", (uint64_t)nb + 1, &npm));
   TC_TRY(scratch_t(ctx, "msm.toff", (uint64_t)nb + 1, &toff));
@@ -783,7 +797,8 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   TC_TRY(scratch_t(ctx, "msm.itemsA", max_items, &itemsA));
   TC_TRY(scratch_t(ctx, "msm.itemsB", max_items, &itemsB));
   TC_TRY(scratch_t(ctx, "msm.buckets", nb, &buckets));
-  TC_CUDA(ctx, cudaMemsetAsync(buckets, 0, (uint64_t)nb * sizeof(Xyzz), st));   // ZZ = 0: infinity
+  k_fill_zero<<<blocks_for(nb, 256), 256, 0, st>>>(buckets, nb);   // empty buckets: neutral
+  TC_LAUNCHED(ctx);
   size_t scan_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, np, toff, (int)(nb + 1), st);
   void* d_scan;
@@ -821,7 +836,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     ctx->launches += 4;
     // every piece holds >= 1 item, and a multi-piece bucket of c >= 2 items yields
     // ceil(c/T1) <= c items: both threads and the next level's items are <= items_bound
-    k_accum_xyzz<<<blocks_for(items_bound, 128), 128, 0, st>>>(itemsA, offA, toff, offB, nb, T1, itemsB, buckets);
+    k_accum_ext<<<blocks_for(items_bound, 128), 128, 0, st>>>(itemsA, offA, toff, offB, nb, T1, itemsB, buckets);
     TC_LAUNCHED(ctx);
     std::swap(offA, offB);
     std::swap(itemsA, itemsB);
@@ -871,19 +886,19 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
       TC_TRY(scratch_t(ctx, "msm.wtabs", tabs.size(), &d_tabs));
       memcpy((char*)ctx->h_stage + stage_off, tabs.data(), tab_bytes);
       TC_CUDA(ctx, cudaMemcpyAsync(d_tabs, (char*)ctx->h_stage + stage_off, tab_bytes, cudaMemcpyHostToDevice, st));
-      Xyzz *TA, *TB, *DA, *DB, *wsum;
+      Ext *TA, *TB, *DA, *DB, *wsum;
       TC_TRY(scratch_t(ctx, "msm.wTA", totals[0] + 1, &TA));
       TC_TRY(scratch_t(ctx, "msm.wTB", totals[0] + 1, &TB));
       TC_TRY(scratch_t(ctx, "msm.wDA", totals[0] + 1, &DA));
       TC_TRY(scratch_t(ctx, "msm.wDB", totals[0] + 1, &DB));
       TC_TRY(scratch_t(ctx, "msm.wsum", nw_total, &wsum));
       const uint32_t stride = 3 * nw_total + 1;
-      const Xyzz* Tin = buckets;
-      const Xyzz* Din = nullptr;
+      const Ext* Tin = buckets;
+      const Ext* Din = nullptr;
       for (uint32_t r = 0; r < R; r++) {
         GroupTab G{d_tabs + r * stride, d_tabs + r * stride + nw_total, d_tabs + r * stride + 2 * nw_total, nw_total};
-        Xyzz* To = (r & 1) ? TB : TA;
-        Xyzz* Do = (r & 1) ? DB : DA;
+        Ext* To = (r & 1) ? TB : TA;
+        Ext* Do = (r & 1) ? DB : DA;
         k_wsum_level<<<blocks_for(totals[r], 128), 128, 0, st>>>(Tin, Din, G, totals[r], SEG_LG * r, SEG, To, Do);
         TC_LAUNCHED(ctx);
         Tin = To;
@@ -907,7 +922,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   while (LS > 2u && (uint64_t)nb / LS < (uint64_t)ctx->num_sms * 256u) LS >>= 1;
   LS = std::min<uint32_t>(LS, minB);
   const uint32_t nseg_total = nb / LS;
-  Xyzz *segs, *wsum;
+  Ext *segs, *wsum;
   TC_TRY(scratch_t(ctx, "msm.segs", nseg_total, &segs));
   TC_TRY(scratch_t(ctx, "msm.wsum", nw_total, &wsum));
   k_bucket_reduce<<<blocks_for(nseg_total, 128), 128, 0, st>>>(buckets, P, nseg_total, LS, segs);
@@ -919,7 +934,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   return TC_OK;
 }
 
-int msm_device(tc_ctx* ctx, ScalarKind kind, const void* d_scalars, const Aff* d_bases, uint64_t n, Aff* d_out) {
+int msm_device(tc_ctx* ctx, ScalarKind kind, const void* d_scalars, const EdAff* d_bases, uint64_t n, Aff* d_out) {
   if (kind != SCALAR_FP_CANON) return fail(ctx, TC_ERR_ARGUMENT, "msm: scalar kind");
   const void* ptrs[1] = {d_scalars};
   return msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, ptrs, 1, d_bases, n, d_out);

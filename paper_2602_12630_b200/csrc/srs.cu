@@ -103,9 +103,63 @@ __global__ void __launch_bounds__(128) k_fixed(const Aff* table, const Fe* exps,
   }
 }
 
+// Montgomery (u, v) -> Edwards (x, y, t): FB_K points per thread share one inversion
+__global__ void __launch_bounds__(128) k_to_edwards(const Aff* in, uint64_t n, EdAff* out) {
+  uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t i0 = t * FB_K;
+  if (i0 >= n) return;
+  const int cnt = (n - i0 < (uint64_t)FB_K) ? (int)(n - i0) : FB_K;
+  Fe pref[FB_K];
+  Fe run = Fq::one();
+  for (int k = 0; k < cnt; k++) {
+    pref[k] = run;
+    run = Fq::mul(run, aff_ed_den(in[i0 + k]));
+  }
+  Fe inv = Fq::inv(run);
+  for (int k = cnt - 1; k >= 0; k--) {
+    const Aff p = in[i0 + k];
+    const Fe den = aff_ed_den(p);
+    const Fe ik = Fq::mul(inv, pref[k]);
+    inv = Fq::mul(inv, den);
+    EdAff e = aff_to_ed_with_inv(p, ik);
+    out[i0 + k] = EdAff{Fq::red2(e.x), Fq::red2(e.y), Fq::red2(e.t)};
+  }
+}
+
 }  // namespace
 
 namespace tcrt {
+
+int to_edwards_device(tc_ctx* ctx, const Aff* d_in, uint64_t n, EdAff* d_out) {
+  if (n == 0) return TC_OK;
+  k_to_edwards<<<blocks_for((n + FB_K - 1) / FB_K, 128), 128, 0, ctx->stream>>>(d_in, n, d_out);
+  TC_LAUNCHED(ctx);
+  return TC_OK;
+}
+
+int srs_edwards(tc_ctx* ctx, tc_srs* srs, int which, const EdAff** out) {
+  const Aff* src;
+  EdAff** dst;
+  uint64_t n = srs->n;
+  if (which == TC_SRS_LAGRANGE) {
+    src = srs->lagrange, dst = &srs->ed_lagrange;
+  } else if (which == TC_SRS_MONOMIAL) {
+    src = srs->monomial, dst = &srs->ed_monomial;
+  } else {
+    src = srs->sublag, dst = &srs->ed_sublag;
+    n = srs->m > 1 ? srs->sublag_off[srs->m - 1] + srs->shape[srs->m - 1] : 0;
+  }
+  if (!src) return fail(ctx, TC_ERR_VALUE, "srs has no elements of kind %d", which);
+  if (!*dst) {
+    if (cudaMalloc(dst, std::max<uint64_t>(n, 1) * sizeof(EdAff)) != cudaSuccess) {
+      *dst = nullptr;
+      return fail(ctx, TC_ERR_MEMORY, "srs edwards alloc");
+    }
+    TC_TRY(to_edwards_device(ctx, src, n, *dst));
+  }
+  *out = *dst;
+  return TC_OK;
+}
 
 int fixed_base_g(tc_ctx* ctx, const Fe* d_exps, uint64_t n, Aff* d_out) {
   cudaStream_t st = ctx->stream;

@@ -63,6 +63,10 @@ struct tc_srs {
   // sub-grid Lagrange elements g^{prod_{j>=i} L_{j,a_j}(tau_j)} for suffixes i = 1..m-1
   // (commitments of the Lagrange-route opening quotients q_i, which live on axes i..m-1)
   tc::Aff* sublag = nullptr;
+  // twisted Edwards copies (x, y, xy) of the bases the Pippenger MSM reads (lazily built)
+  tc::EdAff* ed_monomial = nullptr;
+  tc::EdAff* ed_lagrange = nullptr;
+  tc::EdAff* ed_sublag = nullptr;
   uint64_t sublag_off[TC_MAX_AXES] = {0};
 };
 
@@ -117,14 +121,20 @@ enum ScalarKind { SCALAR_FP_CANON = 0, SCALAR_I64 = 1 };
 
 // result = sum_k scalars[k] * bases[k]; bases are device affine points.  out_aff on device
 // (one Aff) receives the canonical-Montgomery affine result.
-int msm_device(tc_ctx* ctx, ScalarKind kind, const void* d_scalars, const tc::Aff* d_bases,
+int msm_device(tc_ctx* ctx, ScalarKind kind, const void* d_scalars, const tc::EdAff* d_bases,
                uint64_t n, tc::Aff* d_out);
 
 // L MSMs over the same n bases in one pipeline: d_out[l] = sum_k s_l[k] * bases[k].
 // h_ptrs: L device pointers (host array) to n scalars of `dtype` (TC_DTYPE_FP_LIMBS =
 // canonical limbs; float dtypes are quantised at scale_bits inside the digit kernel).
 int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* h_ptrs, int L,
-                     const tc::Aff* d_bases, uint64_t n, tc::Aff* d_out);
+                     const tc::EdAff* d_bases, uint64_t n, tc::Aff* d_out);
+
+// Montgomery affine points -> twisted Edwards affine (x, y, t = x y), batched inversion
+int to_edwards_device(tc_ctx* ctx, const tc::Aff* d_in, uint64_t n, tc::EdAff* d_out);
+// the Edwards copy of an SRS basis for the Pippenger pipeline (built on first use):
+// which = TC_SRS_MONOMIAL | TC_SRS_LAGRANGE, or 0 for the sub-grid Lagrange elements
+int srs_edwards(tc_ctx* ctx, tc_srs* srs, int which, const tc::EdAff** out);
 
 // L MSMs over a small SRS (n <= SMALL_MSM_MAX) with canonical F_p scalars, via per-point
 // byte-window tables built once per SRS (`which` = TC_SRS_MONOMIAL | TC_SRS_LAGRANGE)
