@@ -969,7 +969,6 @@ int tc_terkle_build(tc_ctx* ctx, const tc_srs* node_srs, const uint8_t* leaves_l
   Aff* d_out;
   TC_TRY(tcrt::scratch_t(ctx, "terkle.vals", cap, &d_vals));
   TC_TRY(tcrt::scratch_t(ctx, "terkle.out", cap / B, &d_out));
-  const Aff* bases = node_srs->lagrange ? node_srs->lagrange : node_srs->monomial;
   bool lag = node_srs->lagrange != nullptr;
   uint64_t written = 0;
   const uint8_t tag[] = {'t', 'e', 'r', 'k', 'l', 'e', '/', 'n', 'o', 'd', 'e'};

@@ -197,6 +197,82 @@ __global__ void __launch_bounds__(256) k_digits(const void* const* ptrs, uint64_
   }
 }
 
+// ---- counting-sort layout (default): digits -> bucket counts -> scan -> scatter -------
+// The radix sort of (key, value) pairs costs 3 onesweep passes over all entries plus a
+// bounds pass.  Instead, the digits are produced twice from the (2 B/elem) inputs:
+//   k_count_digits   — per-bucket entry counts (global RED atomics; windows with few
+//                      buckets, where one bucket takes thousands of hits, are aggregated
+//                      per warp first with __match_any_sync)
+//   exclusive scan   — bucket starts (bucket k = [bstart[k], bstart[k+1]))
+//   k_scatter_digits — each entry claims a slot with an atomic on its bucket cursor and
+//                      writes its value (point index | sign); the order inside a bucket is
+//                      arbitrary, which EC addition does not see
+constexpr uint32_t HOT_BUCKETS = 1024;   // windows with <= this many buckets are warp-aggregated
+
+template <bool SCATTER>
+__device__ __forceinline__ void bucket_hit(uint32_t key, bool hot, bool active, uint32_t val, uint32_t* cnt,
+                                           uint32_t* vals) {
+  // hot is warp-uniform (same window for every lane)
+  if (hot) {
+    const uint32_t act = __ballot_sync(0xffffffffu, active);
+    if (!active) return;
+    const uint32_t peers = __match_any_sync(act, key);
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (lane == leader) {
+      if (SCATTER)
+        base = atomicAdd(cnt + key, (uint32_t)__popc(peers));
+      else
+        atomicAdd(cnt + key, (uint32_t)__popc(peers));
+    }
+    if (SCATTER) {
+      base = __shfl_sync(peers, base, leader);
+      vals[base + __popc(peers & ((1u << lane) - 1u))] = val;
+    }
+  } else if (active) {
+    if (SCATTER)
+      vals[atomicAdd(cnt + key, 1u)] = val;
+    else
+      atomicAdd(cnt + key, 1u);
+  }
+}
+
+template <int DT, bool SCATTER>
+__global__ void __launch_bounds__(256) k_count_digits(const void* const* ptrs, uint64_t n, int scale_bits, WinPlan P,
+                                                      uint32_t* cnt, uint32_t* vals) {
+  const uint32_t l = blockIdx.y;
+  const void* p = ptrs[l];
+  const uint32_t key0 = l * P.nbm;
+  uint32_t f = 0;
+  // whole warps iterate together (the hot-window aggregation needs converged lanes)
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t nr = (n + 31) & ~31ull;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nr; i += stride) {
+    const bool in = i < n;
+    Fe mag;
+    bool neg = false;
+    if (in) load_scalar<DT>(p, i, scale_bits, mag, neg, f);
+    else mag = Fe{{0, 0, 0, 0, 0, 0}};
+    uint32_t carry = 0;
+    for (int w = 0; w < P.nwin; w++) {
+      const int c = P.width[w];
+      const uint32_t half = 1u << (c - 1), full = 1u << c;
+      uint32_t d = window_bits(mag, P.off[w], c) + carry;
+      bool dn = false;
+      if (d > half) {
+        d = full - d;
+        dn = true;
+        carry = 1;
+      } else {
+        carry = 0;
+      }
+      const uint32_t key = key0 + P.base[w] + d - 1u;
+      bucket_hit<SCATTER>(key, half <= HOT_BUCKETS, d != 0, (uint32_t)i | ((neg != dn) ? SIGN_BIT : 0u), cnt, vals);
+    }
+  }
+}
+
 // ---- bucket-major layout without a radix sort (few buckets per MSM) -------------------
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
@@ -325,14 +401,17 @@ __global__ void k_bounds(const uint32_t* keys, const uint32_t* count, uint32_t* 
   if (j + 1 == E || keys[j + 1] != k) bend[k] = (uint32_t)j + 1u;
 }
 
-// level 0 piece counts: np[k] = ceil(size/T) (threads), npm[k] = np[k] if > 1 (items)
+// level 0 piece counts: np[k] = ceil(size/T) (threads), npm[k] = np[k] if > 1 (items);
+// an empty bucket is set to the neutral element here (every other bucket is written by
+// the accumulation levels), so the bucket array needs no separate fill pass
 __global__ void k_count0(const uint32_t* bstart, const uint32_t* bend, uint32_t nb, uint32_t T, uint32_t* np,
-                         uint32_t* npm) {
+                         uint32_t* npm, Ext* buckets) {
   uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k > nb) return;
   uint32_t c = (k == nb) ? 0u : (bend[k] - bstart[k] + T - 1) / T;
   np[k] = c;
   npm[k] = c > 1 ? c : 0u;
+  if (k < nb && c == 0) buckets[k] = ext_zero();
 }
 
 // level >= 1: items of bucket k are [off_in[k], off_in[k+1]) (0 or >= 2 of them)
@@ -384,12 +463,6 @@ __global__ void __launch_bounds__(128) k_accum_aff(const uint32_t* vals, const E
     buckets[k] = acc;
   else
     items[ooff[k] + piece] = acc;
-}
-
-// empty buckets hold the neutral element (0 : 1 : 1 : 0)
-__global__ void k_fill_zero(Ext* b, uint32_t n) {
-  uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < n) b[k] = ext_zero();
 }
 
 // level >= 1: bucket k's items are in[iofs[k] .. iofs[k+1])
@@ -557,7 +630,7 @@ WinPlan plan_windows(const uint32_t* hist, uint32_t nbits, uint64_t L) {
     if (b < NHIST) acc += hist[b];
   }
   above[NHIST + 1] = 0;
-  const int CMAX = 20;
+  static const int CMAX = getenv("TC_MSM_CMAX") ? atoi(getenv("TC_MSM_CMAX")) : 20;
   static const int CMIN_ENV = getenv("TC_MSM_CMIN") ? atoi(getenv("TC_MSM_CMIN")) : 4;
   const int CMIN = std::max(CMIN_ENV, (top + MAXW - 1) / MAXW);   // at most MAXW windows
   std::vector<double> best(top + CMAX + 1, 1e300);
@@ -693,11 +766,8 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   const int end_bit = (int)bitlen_u32(nb - 1);
 
   // 3. non-zero digits, compacted
-  uint32_t *keys, *vals, *keys2, *vals2;
-  TC_TRY(scratch_t(ctx, "msm.keys", cap, &keys));
+  uint32_t *keys = nullptr, *vals, *keys2 = nullptr, *vals2 = nullptr;
   TC_TRY(scratch_t(ctx, "msm.vals", cap, &vals));
-  TC_TRY(scratch_t(ctx, "msm.keys2", cap, &keys2));
-  TC_TRY(scratch_t(ctx, "msm.vals2", cap, &vals2));
   uint32_t* d_count = d_small + NHIST + 2;
   const uint32_t* svals;
   uint32_t *bstart, *bend;
@@ -707,8 +777,45 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   // digits 0.8 + onesweep 2.3 + bounds 0.4 ms): the per-layer slot counters and the
   // __match_any_sync aggregation serialise; kept for small-bucket experiments.
   static const bool want_bucketed = getenv("TC_MSM_BUCKETED") != nullptr;
+  static const bool want_radix = getenv("TC_MSM_SORT") != nullptr;   // radix-sort layout (A/B)
   const bool bucketed = want_bucketed && (size_t)P.nbm * 8 <= 160 * 1024;
-  if (bucketed) {
+  if (!bucketed && !want_radix) {
+    // counting-sort layout: count, scan, scatter (no keys stored, no radix passes)
+    uint32_t *cnt, *cursor;
+    TC_TRY(scratch_t(ctx, "msm.bcount", (uint64_t)nb + 1, &cnt));
+    TC_TRY(scratch_t(ctx, "msm.bstart", (uint64_t)nb + 1, &bstart));
+    TC_TRY(scratch_t(ctx, "msm.cursor", (uint64_t)nb + 1, &cursor));
+    TC_CUDA(ctx, cudaMemsetAsync(cnt, 0, ((uint64_t)nb + 1) * sizeof(uint32_t), st));
+    const unsigned gx = std::min<unsigned>(blocks_for(n, 256), std::max(1u, (unsigned)ctx->num_sms * 16 / (unsigned)L + 1));
+    int s = dispatch_dt(ctx, dtype, [&](auto dt) {
+      k_count_digits<decltype(dt)::value, false><<<dim3(gx, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cnt, nullptr);
+    });
+    if (s) return s;
+    TC_LAUNCHED(ctx);
+    size_t sb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, sb, cnt, bstart, (int)(nb + 1), st);
+    void* d_sb;
+    TC_TRY(scratch(ctx, "msm.scantmp0", sb, &d_sb));
+    TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(d_sb, sb, cnt, bstart, (int)(nb + 1), st));
+    ctx->launches += 2;
+    TC_CUDA(ctx, cudaMemcpyAsync(cursor, bstart, ((uint64_t)nb + 1) * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+    TC_CUDA(ctx, cudaMemcpyAsync(h_small, bstart + nb, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    s = dispatch_dt(ctx, dtype, [&](auto dt) {
+      k_count_digits<decltype(dt)::value, true><<<dim3(gx, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cursor, vals);
+    });
+    if (s) return s;
+    TC_LAUNCHED(ctx);
+    TC_CUDA(ctx, cudaStreamSynchronize(st));
+    E = h_small[0];
+    if (E == 0) {
+      k_fill_inf<<<blocks_for(L, 64), 64, 0, st>>>(d_out, (uint32_t)L);
+      TC_LAUNCHED(ctx);
+      return TC_OK;
+    }
+    svals = vals;
+    bend = bstart + 1;
+  } else if (bucketed) {
+    TC_TRY(scratch_t(ctx, "msm.keys", cap, &keys));
     const uint32_t CH = 8192, CHB = 8192;
     const uint64_t cap_l = n * P.nwin;
     const uint32_t gx = (uint32_t)((n + CH - 1) / CH), gxb = (uint32_t)((cap_l + CHB - 1) / CHB);
@@ -743,6 +850,9 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     bend = bstart + 1;   // bucket k = [bstart[k], bstart[k+1])
     E = cap;             // upper bound (no host readback of the entry count)
   } else {
+    TC_TRY(scratch_t(ctx, "msm.keys", cap, &keys));
+    TC_TRY(scratch_t(ctx, "msm.keys2", cap, &keys2));
+    TC_TRY(scratch_t(ctx, "msm.vals2", cap, &vals2));
     {
       int s = dispatch_dt(ctx, dtype, [&](auto dt) {
         k_digits<decltype(dt)::value><<<dim3(blocks_for(n, 256 * DIG_EPT), L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, keys,
@@ -797,14 +907,12 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   TC_TRY(scratch_t(ctx, "msm.itemsA", max_items, &itemsA));
   TC_TRY(scratch_t(ctx, "msm.itemsB", max_items, &itemsB));
   TC_TRY(scratch_t(ctx, "msm.buckets", nb, &buckets));
-  k_fill_zero<<<blocks_for(nb, 256), 256, 0, st>>>(buckets, nb);   // empty buckets: neutral
-  TC_LAUNCHED(ctx);
   size_t scan_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, np, toff, (int)(nb + 1), st);
   void* d_scan;
   TC_TRY(scratch(ctx, "msm.scantmp", scan_bytes, &d_scan));
 
-  k_count0<<<blocks_for((uint64_t)nb + 1, 256), 256, 0, st>>>(bstart, bend, nb, T, np, npm);
+  k_count0<<<blocks_for((uint64_t)nb + 1, 256), 256, 0, st>>>(bstart, bend, nb, T, np, npm, buckets);
   TC_LAUNCHED(ctx);
   TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(d_scan, scan_bytes, np, toff, (int)(nb + 1), st));
   TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(d_scan, scan_bytes, npm, offA, (int)(nb + 1), st));
