@@ -216,12 +216,40 @@ TC_HD void aff_encode43(const Aff& p, uint8_t out[43]) {
 // and d = -2, a = 2 are additions.  The map is defined on the whole odd-order subgroup
 // the SRS lives in; only the Montgomery 2-torsion point (0, 0) <-> (0, -1) is special.
 // Affine points carry t = x*y (precomputed when the SRS is converted).
-struct EdAff {
+// 16-byte aligned so every load / store is LDG.128 / STG.128 (EdAff padded 72 -> 80 B)
+struct alignas(16) EdAff {
   Fe x, y, t;
 };
-struct Ext {
+struct alignas(16) Ext {
   Fe X, Y, Z, T;
 };
+
+#if defined(__CUDACC__)
+// explicit 128-bit loads (the struct copy alone leaves ptxas with 24 scalar loads)
+TC_D void unpack4(const uint4* q, uint32_t* w, int n4) {
+#pragma unroll
+  for (int i = 0; i < n4; i++) {
+    const uint4 a = q[i];
+    w[4 * i] = a.x, w[4 * i + 1] = a.y, w[4 * i + 2] = a.z, w[4 * i + 3] = a.w;
+  }
+}
+TC_D Ext ld_ext(const Ext* p) {
+  uint32_t w[24];
+  unpack4((const uint4*)p, w, 6);
+  Ext r;
+#pragma unroll
+  for (int i = 0; i < 6; i++) r.X.v[i] = w[i], r.Y.v[i] = w[6 + i], r.Z.v[i] = w[12 + i], r.T.v[i] = w[18 + i];
+  return r;
+}
+TC_D EdAff ld_edaff(const EdAff* p) {
+  uint32_t w[20];
+  unpack4((const uint4*)p, w, 5);
+  EdAff r;
+#pragma unroll
+  for (int i = 0; i < 6; i++) r.x.v[i] = w[i], r.y.v[i] = w[6 + i], r.t.v[i] = w[12 + i];
+  return r;
+}
+#endif
 
 TC_HD Ext ext_zero() { return Ext{Fq::zero(), Fq::one(), Fq::one(), Fq::zero()}; }
 TC_HD Ext ext_from_aff(const EdAff& p) { return Ext{p.x, p.y, Fq::one(), p.t}; }

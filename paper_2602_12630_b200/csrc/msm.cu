@@ -41,6 +41,7 @@ constexpr uint32_t SIGN_BIT = 0x80000000u;
 constexpr int DT_LIMBS = 0;   // template code for canonical F_p scalars
 constexpr int MAXW = 48;      // windows per scalar (>= ceil(163 / 4))
 constexpr int NHIST = 168;    // bit-length histogram bins
+constexpr uint32_t HIST_SAMPLE = 8;   // histogram taken on every 8th element (k_scan_bits)
 constexpr int DIG_EPT = 1;    // elements per thread in k_digits (8 measured 1.7x slower:
                               // per-thread entry ranges break store coalescing)
 
@@ -87,7 +88,7 @@ __global__ void k_scan_bits(const void* const* ptrs, uint64_t n, int scale_bits,
   for (int i = threadIdx.x; i < NHIST; i += blockDim.x) hist[i] = 0;
   __syncthreads();
   const void* p = ptrs[blockIdx.y];
-  uint32_t f = 0;
+  uint32_t f = 0, bmax = 0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t bl;
     if (DT >= 1 && DT <= 3) {
@@ -106,11 +107,19 @@ __global__ void k_scan_bits(const void* const* ptrs, uint64_t n, int scale_bits,
       load_scalar<DT>(p, i, scale_bits, mag, neg, f);
       bl = bitlen6(mag);
     }
-    atomicAdd(&hist[bl], 1u);
+    // the histogram only steers the window plan (any plan is exact), so it is taken on
+    // 1/HIST_SAMPLE of the elements: contended shared atomics were the kernel's cost.  The
+    // maximum bit length (which the plan must cover) and the error flags see every element.
+    if ((i & (HIST_SAMPLE - 1)) == 0) atomicAdd(&hist[bl], 1u);
+    bmax = max(bmax, bl);
   }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) f |= __shfl_xor_sync(0xffffffffu, f, o);
+  for (int o = 16; o; o >>= 1) {
+    f |= __shfl_xor_sync(0xffffffffu, f, o);
+    bmax = max(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
+  }
   if ((threadIdx.x & 31) == 0 && f) atomicOr(out, f);
+  if ((threadIdx.x & 31) == 0 && bmax) atomicMax(out + NHIST + 1, bmax);
   __syncthreads();
   for (int i = threadIdx.x; i < NHIST; i += blockDim.x)
     if (hist[i]) atomicAdd(out + 1 + i, hist[i]);
@@ -271,6 +280,141 @@ __global__ void __launch_bounds__(256) k_count_digits(const void* const* ptrs, u
       bucket_hit<SCATTER>(key, half <= HOT_BUCKETS, d != 0, (uint32_t)i | ((neg != dn) ? SIGN_BIT : 0u), cnt, vals);
     }
   }
+}
+
+// ---- fast path: float inputs whose quantised magnitudes fit 63 bits (fp16 at the
+// reference's scale 2^16 always does).  One block = 2048 consecutive elements of one MSM,
+// 8 per thread from one 16-byte load (two for fp32); magnitudes and digits in uint64.
+// Few-bucket ("hot") windows are counted in shared memory and claimed from the global
+// cursors with ONE atomic per (block, bucket); the blocks are scheduled MSM after MSM,
+// so the scattered 4-byte writes of the MSMs in flight stay in L2 until their sectors
+// are complete.
+constexpr int V_EPT = 8;
+constexpr int HOT_MAXW = 4;        // hot windows per plan handled by the fast path
+constexpr uint32_t HOT_MAXB = 2048;
+
+struct HotPlan {
+  int nhot;
+  uint8_t win[HOT_MAXW];       // hot window ids
+  uint16_t hbase[HOT_MAXW];    // first shared counter of each hot window
+  uint32_t nhotb;              // shared counters in use
+  int8_t slot[MAXW];           // window -> hot slot or -1
+};
+
+template <int DT>
+__device__ __forceinline__ void load_raw8(const void* p, uint64_t i0, uint64_t n, uint32_t raw[V_EPT]) {
+  if (i0 + V_EPT <= n) {
+    if (DT == 1 || DT == 2) {
+      const uint4 a = *(const uint4*)((const uint16_t*)p + i0);
+      const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+      for (int k = 0; k < 4; k++) raw[2 * k] = w[k] & 0xffffu, raw[2 * k + 1] = w[k] >> 16;
+    } else {
+      const uint4 a = *(const uint4*)((const uint32_t*)p + i0), b = *((const uint4*)((const uint32_t*)p + i0) + 1);
+      raw[0] = a.x, raw[1] = a.y, raw[2] = a.z, raw[3] = a.w, raw[4] = b.x, raw[5] = b.y, raw[6] = b.z, raw[7] = b.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < V_EPT; k++) {
+      const uint64_t i = i0 + k;
+      raw[k] = i < n ? ((DT == 1 || DT == 2) ? (uint32_t)((const uint16_t*)p)[i] : ((const uint32_t*)p)[i]) : 0u;
+    }
+  }
+}
+
+// |RNE(v * 2^scale_bits)| < 2^63 and its sign from raw fp16 / bf16 / fp32 bits (non-finite
+// values were rejected by k_scan_bits before this runs; they map to 0 here)
+template <int DT>
+__device__ __forceinline__ uint64_t quant64(uint32_t b, int scale_bits, bool& neg) {
+  uint32_t e, m;
+  int ex;
+  if (DT == 1) {
+    e = (b >> 10) & 0x1f, m = b & 0x3ff, neg = b >> 15;
+    if (e == 0x1f) return 0;
+    m = e ? (m | 0x400u) : m, ex = (e ? (int)e : 1) - 25;
+  } else if (DT == 2) {
+    e = (b >> 7) & 0xff, m = b & 0x7f, neg = b >> 15;
+    if (e == 0xff) return 0;
+    m = e ? (m | 0x80u) : m, ex = (e ? (int)e : 1) - 134;
+  } else {
+    e = (b >> 23) & 0xff, m = b & 0x7fffffu, neg = b >> 31;
+    if (e == 0xff) return 0;
+    m = e ? (m | 0x800000u) : m, ex = (e ? (int)e : 1) - 150;
+  }
+  const int sh = ex + scale_bits;
+  if (sh >= 0) return (uint64_t)m << sh;
+  const int s = -sh;
+  if (s > 31) return 0;   // m < 2^24 -> value < 1/2
+  const uint32_t iq = m >> s, rem = m & ((1u << s) - 1u), half = 1u << (s - 1);
+  return (uint64_t)(iq + ((rem > half || (rem == half && (iq & 1u))) ? 1u : 0u));
+}
+
+template <int DT, bool SCATTER>
+__global__ void __launch_bounds__(256) k_digits_v(const void* const* ptrs, uint64_t n, int scale_bits, WinPlan P,
+                                                  HotPlan H, uint32_t* cnt, uint32_t* vals) {
+  __shared__ uint32_t hcnt[HOT_MAXB];
+  const uint32_t l = blockIdx.y;
+  const void* p = ptrs[l];
+  const uint32_t key0 = l * P.nbm;
+  for (uint32_t h = threadIdx.x; h < H.nhotb; h += blockDim.x) hcnt[h] = 0;
+  __syncthreads();
+  const uint64_t i0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * V_EPT;
+  uint32_t raw[V_EPT];
+  load_raw8<DT>(p, i0, n, raw);
+  uint32_t hd[V_EPT][HOT_MAXW];   // hot digits: counter index | local rank << 12 | sign << 31
+#pragma unroll
+  for (int k = 0; k < V_EPT; k++) {
+#pragma unroll
+    for (int j = 0; j < HOT_MAXW; j++) hd[k][j] = 0xffffffffu;
+    bool neg;
+    const uint64_t mag = (i0 + k < n) ? quant64<DT>(raw[k], scale_bits, neg) : 0ull;
+    uint32_t carry = 0;
+    for (int w = 0; w < P.nwin; w++) {
+      const int c = P.width[w];
+      const uint32_t half = 1u << (c - 1), full = 1u << c;
+      uint32_t d = (uint32_t)((mag >> P.off[w]) & (full - 1u)) + carry;
+      bool dn = false;
+      if (d > half) {
+        d = full - d, dn = true, carry = 1;
+      } else {
+        carry = 0;
+      }
+      if (!d) continue;
+      const int hs = H.slot[w];
+      if (hs >= 0) {
+        const uint32_t h = H.hbase[hs] + d - 1u;
+        const uint32_t r = atomicAdd(&hcnt[h], 1u);
+        hd[k][hs] = h | (r << 12) | ((neg != dn) ? SIGN_BIT : 0u);
+      } else if (SCATTER) {
+        vals[atomicAdd(cnt + key0 + P.base[w] + d - 1u, 1u)] = (uint32_t)(i0 + k) | ((neg != dn) ? SIGN_BIT : 0u);
+      } else {
+        atomicAdd(cnt + key0 + P.base[w] + d - 1u, 1u);
+      }
+    }
+  }
+  if (H.nhot == 0) return;
+  __syncthreads();
+  // one global atomic per used hot bucket of this block; hcnt becomes the claimed base
+  for (int hs = 0; hs < H.nhot; hs++) {
+    const int w = H.win[hs];
+    const uint32_t nbw = 1u << (P.width[w] - 1);
+    for (uint32_t j = threadIdx.x; j < nbw; j += blockDim.x) {
+      const uint32_t h = H.hbase[hs] + j, c = hcnt[h];
+      if (!c) continue;
+      const uint32_t b = atomicAdd(cnt + key0 + P.base[w] + j, c);
+      if (SCATTER) hcnt[h] = b;
+    }
+  }
+  if (!SCATTER) return;
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < V_EPT; k++)
+#pragma unroll
+    for (int j = 0; j < HOT_MAXW; j++) {
+      const uint32_t v = hd[k][j];
+      if (v != 0xffffffffu)
+        vals[hcnt[v & 0xfffu] + ((v >> 12) & 0x7ffffu)] = (uint32_t)(i0 + k) | (v & SIGN_BIT);
+    }
 }
 
 // ---- bucket-major layout without a radix sort (few buckets per MSM) -------------------
@@ -450,12 +594,12 @@ __global__ void __launch_bounds__(128) k_accum_aff(const uint32_t* vals, const E
   uint32_t a = bstart[k] + piece * T;
   uint32_t b = min(a + T, bend[k]);
   uint32_t v = vals[a];
-  EdAff q = bases[v & ~SIGN_BIT];
+  EdAff q = ld_edaff(bases + (v & ~SIGN_BIT));
   if (v & SIGN_BIT) q = edaff_neg(q);
   Ext acc = ext_from_aff(q);
   for (uint32_t j = a + 1; j < b; j++) {
     v = vals[j];
-    q = bases[v & ~SIGN_BIT];
+    q = ld_edaff(bases + (v & ~SIGN_BIT));
     if (v & SIGN_BIT) q = edaff_neg(q);
     ext_madd(acc, q);
   }
@@ -476,8 +620,8 @@ __global__ void __launch_bounds__(128) k_accum_ext(const Ext* in, const uint32_t
   uint32_t piece = p - toff[k];
   uint32_t a = iofs[k] + piece * T;
   uint32_t b = min(a + T, iofs[k + 1]);
-  Ext acc = in[a];
-  for (uint32_t j = a + 1; j < b; j++) ext_add(acc, in[j]);
+  Ext acc = ld_ext(in + a);
+  for (uint32_t j = a + 1; j < b; j++) ext_add(acc, ld_ext(in + j));
   if (toff[k + 1] - toff[k] == 1)
     buckets[k] = acc;
   else
@@ -564,14 +708,14 @@ __global__ void __launch_bounds__(128) k_wsum_level(const Ext* Tin, const Ext* D
   const uint32_t len = min(SEG, G.in_cnt[g] - k * SEG);
   Ext run = ext_zero(), u = ext_zero();
   for (int j = (int)len - 1; j >= 0; j--) {
-    ext_add(run, Tin[a + j]);
+    ext_add(run, ld_ext(Tin + a + j));
     ext_add(u, run);
   }
   Tout[o] = run;
   // D_out = sum of D_in over the segment + SEG^{r-1} * U
   for (uint32_t i = 0; i < dbl_shift; i++) u = ext_dbl(u);
   if (Din)
-    for (uint32_t j = 0; j < len; j++) ext_add(u, Din[a + j]);
+    for (uint32_t j = 0; j < len; j++) ext_add(u, ld_ext(Din + a + j));
   Dout[o] = u;
 }
 
@@ -740,16 +884,13 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     TC_LAUNCHED(ctx);
   }
   uint32_t* h_small = (uint32_t*)((char*)ctx->h_stage + 65536);
-  TC_CUDA(ctx, cudaMemcpyAsync(h_small, d_small, (NHIST + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  TC_CUDA(ctx, cudaMemcpyAsync(h_small, d_small, (NHIST + 2) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   TC_CUDA(ctx, cudaStreamSynchronize(st));
   TC_TRY(quantize_flags_to_status(ctx, h_small[0]));
-  const uint32_t* hist = h_small + 1;
-  uint32_t nbits = 0;
-  for (int b = NHIST - 1; b > 0; b--)
-    if (hist[b]) {
-      nbits = (uint32_t)b;
-      break;
-    }
+  uint32_t hist[NHIST];   // sampled counts scaled back to the population
+  for (int b = 0; b < NHIST; b++) hist[b] = h_small[1 + b] * HIST_SAMPLE;
+  const uint32_t nbits = std::min<uint32_t>(h_small[NHIST + 1], NHIST - 1);   // exact maximum
+  if (nbits) hist[nbits] = std::max<uint32_t>(hist[nbits], 1u);
   if (nbits == 0) {
     k_fill_inf<<<blocks_for(L, 64), 64, 0, st>>>(d_out, (uint32_t)L);
     TC_LAUNCHED(ctx);
@@ -786,9 +927,40 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     TC_TRY(scratch_t(ctx, "msm.bstart", (uint64_t)nb + 1, &bstart));
     TC_TRY(scratch_t(ctx, "msm.cursor", (uint64_t)nb + 1, &cursor));
     TC_CUDA(ctx, cudaMemsetAsync(cnt, 0, ((uint64_t)nb + 1) * sizeof(uint32_t), st));
+    // fast path (k_digits_v) for fp16 / bf16 / fp32 with magnitudes below 2^62 and at most
+    // HOT_MAXW few-bucket windows; the generic kernel otherwise
+    HotPlan H{};
+    H.nhot = 0;
+    H.nhotb = 0;
+    bool fast = (dtype == TC_DTYPE_F16 || dtype == TC_DTYPE_BF16 || dtype == TC_DTYPE_F32) && nbits <= 61 &&
+                !getenv("TC_MSM_GENERIC_DIGITS");
+    for (int l = 0; l < L && fast; l++) fast = ((uintptr_t)h_ptrs[l] & 15u) == 0;   // 16-byte vector loads
+    for (int w = 0; w < P.nwin; w++) {
+      H.slot[w] = -1;
+      const uint32_t nbw = 1u << (P.width[w] - 1);
+      if (nbw <= HOT_BUCKETS) {
+        if (H.nhot == HOT_MAXW || H.nhotb + nbw > HOT_MAXB) {
+          fast = false;
+          continue;
+        }
+        H.slot[w] = (int8_t)H.nhot;
+        H.win[H.nhot] = (uint8_t)w;
+        H.hbase[H.nhot] = (uint16_t)H.nhotb;
+        H.nhotb += nbw;
+        H.nhot++;
+      }
+    }
+    const unsigned gxv = blocks_for(n, 256 * V_EPT);
     const unsigned gx = std::min<unsigned>(blocks_for(n, 256), std::max(1u, (unsigned)ctx->num_sms * 16 / (unsigned)L + 1));
     int s = dispatch_dt(ctx, dtype, [&](auto dt) {
-      k_count_digits<decltype(dt)::value, false><<<dim3(gx, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cnt, nullptr);
+      constexpr int D = decltype(dt)::value;
+      if constexpr (D >= 1 && D <= 3) {
+        if (fast) {
+          k_digits_v<D, false><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, H, cnt, nullptr);
+          return;
+        }
+      }
+      k_count_digits<D, false><<<dim3(gx, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cnt, nullptr);
     });
     if (s) return s;
     TC_LAUNCHED(ctx);
@@ -801,7 +973,14 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     TC_CUDA(ctx, cudaMemcpyAsync(cursor, bstart, ((uint64_t)nb + 1) * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
     TC_CUDA(ctx, cudaMemcpyAsync(h_small, bstart + nb, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     s = dispatch_dt(ctx, dtype, [&](auto dt) {
-      k_count_digits<decltype(dt)::value, true><<<dim3(gx, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cursor, vals);
+      constexpr int D = decltype(dt)::value;
+      if constexpr (D >= 1 && D <= 3) {
+        if (fast) {
+          k_digits_v<D, true><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, H, cursor, vals);
+          return;
+        }
+      }
+      k_count_digits<D, true><<<dim3(gx, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cursor, vals);
     });
     if (s) return s;
     TC_LAUNCHED(ctx);
