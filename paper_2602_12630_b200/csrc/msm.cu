@@ -417,6 +417,56 @@ __global__ void __launch_bounds__(256) k_digits_v(const void* const* ptrs, uint6
     }
 }
 
+// k_scan_bits for fp16 / bf16 / fp32: 8 elements per thread from 16-byte loads
+template <int DT>
+__global__ void __launch_bounds__(256) k_scan_bits_v(const void* const* ptrs, uint64_t n, int scale_bits, uint32_t* out) {
+  __shared__ uint32_t hist[NHIST];
+  for (int i = threadIdx.x; i < NHIST; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  const void* p = ptrs[blockIdx.y];
+  uint32_t f = 0, bmax = 0;
+  for (uint64_t i0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * V_EPT; i0 < n;
+       i0 += (uint64_t)gridDim.x * blockDim.x * V_EPT) {
+    uint32_t raw[V_EPT];
+    load_raw8<DT>(p, i0, n, raw);
+#pragma unroll
+    for (int k = 0; k < V_EPT; k++) {
+      if (i0 + k >= n) break;
+      uint32_t e, m;
+      int ex;
+      bool nf;
+      const uint32_t b = raw[k];
+      if (DT == 1) {
+        e = (b >> 10) & 0x1f, m = b & 0x3ff, nf = e == 0x1f;
+        m = e ? (m | 0x400u) : m, ex = (e ? (int)e : 1) - 25;
+      } else if (DT == 2) {
+        e = (b >> 7) & 0xff, m = b & 0x7f, nf = e == 0xff;
+        m = e ? (m | 0x80u) : m, ex = (e ? (int)e : 1) - 134;
+      } else {
+        e = (b >> 23) & 0xff, m = b & 0x7fffffu, nf = e == 0xff;
+        m = e ? (m | 0x800000u) : m, ex = (e ? (int)e : 1) - 150;
+      }
+      if (nf) f |= QF_NONFINITE;
+      const int sh = ex + scale_bits;
+      const int mb = m ? 32 - __clz(m) : 0;
+      const int bl0 = nf ? 0 : (sh >= 0 ? mb + sh : mb + sh + 1);
+      const uint32_t bl = (uint32_t)(bl0 > 0 ? (bl0 < NHIST - 1 ? bl0 : NHIST - 1) : 0);
+      if (k == 0 && ((i0 / V_EPT) & (HIST_SAMPLE / V_EPT > 1 ? HIST_SAMPLE / V_EPT - 1 : 0)) == 0) atomicAdd(&hist[bl], 1u);
+      bmax = max(bmax, bl);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    f |= __shfl_xor_sync(0xffffffffu, f, o);
+    bmax = max(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
+  }
+  if ((threadIdx.x & 31) == 0 && f) atomicOr(out, f);
+  if ((threadIdx.x & 31) == 0 && bmax) atomicMax(out + NHIST + 1, bmax);
+  __syncthreads();
+  for (int i = threadIdx.x; i < NHIST; i += blockDim.x)
+    if (hist[i]) atomicAdd(out + 1 + i, hist[i]);
+}
+
 // ---- bucket-major layout without a radix sort (few buckets per MSM) -------------------
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
@@ -877,8 +927,17 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   TC_CUDA(ctx, cudaMemsetAsync(d_small, 0, NSMALL * sizeof(uint32_t), st));
   {
     unsigned gx = std::min<unsigned>(blocks_for(n, 256), std::max(1u, (unsigned)ctx->num_sms * 8 / (unsigned)L + 1));
+    bool vec = true;   // 16-byte loads need aligned inputs
+    for (int l = 0; l < L; l++) vec = vec && ((uintptr_t)h_ptrs[l] & 15u) == 0;
     int s = dispatch_dt(ctx, dtype, [&](auto dt) {
-      k_scan_bits<decltype(dt)::value><<<dim3(gx, L), 256, 0, st>>>(d_ptrs, n, scale_bits, d_small);
+      constexpr int D = decltype(dt)::value;
+      if constexpr (D >= 1 && D <= 3) {
+        if (vec) {
+          k_scan_bits_v<D><<<dim3(gx, L), 256, 0, st>>>(d_ptrs, n, scale_bits, d_small);
+          return;
+        }
+      }
+      k_scan_bits<D><<<dim3(gx, L), 256, 0, st>>>(d_ptrs, n, scale_bits, d_small);
     });
     if (s) return s;
     TC_LAUNCHED(ctx);
