@@ -150,6 +150,12 @@ int tc_commit_stream(tc_ctx* ctx, const tc_srs* srs, const void* const* h_cur,
 /* ---- tc_open: y = f_T(omega), pi_i = g^{q_i(tau)} ----------------------- */
 int tc_open(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int scale_bits,
             const uint8_t* omega_le21, int route, uint8_t* out_y21, uint8_t* out_pi43);
+/* count openings (tensor d_ins[i] at point omegas_le21[i*m .. i*m+m)): the quotients of a
+ * group of openings feed ONE batched MSM per axis (config 4's many challenges); outputs
+ * y (count x 21 B) and pi (count x m x 43 B) in input order, bytes identical to tc_open. */
+int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype,
+                  int scale_bits, const uint8_t* omegas_le21, int route, uint8_t* out_y21,
+                  uint8_t* out_pi43);
 
 /* ---- Terkle build ------------------------------------
  * leaves: n x 21 B field elements.  Pads with zeros to B^L (B = node SRS size,

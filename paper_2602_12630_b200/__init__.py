@@ -9,7 +9,7 @@ or a CUDA device the compute entry points raise.
 from .authtree import MembershipProof, TerkleTree, TreeConfig, build, leaf_of, prove, verify
 from .capture import ActivationCapture, infer_and_capture
 from .commit import (Commitment, Srs, TensorOpening, Trapdoors, derive_taus, load_srs, pair, setup_srs, tc_commit,
-                     tc_commit_many, tc_commit_stream, tc_open, tc_verify)
+                     tc_commit_many, tc_commit_stream, tc_open, tc_open_many, tc_verify)
 from .curve import G, P, Q, decode_elem, decode_scalar, encode_elem, encode_scalar, hash_to_scalar
 from .field import PrimeField
 from .mvpoly import Grid, MultiPoly, default_grid, evaluate, interpolate_lagrange, lex_index, open_quotients
@@ -20,5 +20,5 @@ __all__ = [
     "TensorOpening", "TerkleTree", "Trapdoors", "TreeConfig", "build", "decode_elem", "decode_scalar", "default_grid",
     "derive_taus", "encode_elem", "encode_scalar", "evaluate", "hash_to_scalar", "interpolate_lagrange", "leaf_of",
     "lex_index", "load_srs", "open_quotients", "pair", "prove", "prover_commit", "prover_commit_stream", "quantize", "setup_srs", "tc_commit",
-    "tc_commit_many", "tc_commit_stream", "tc_open", "tc_verify", "verify",
+    "tc_commit_many", "tc_commit_stream", "tc_open", "tc_open_many", "tc_verify", "verify",
 ]

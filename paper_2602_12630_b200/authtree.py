@@ -48,6 +48,9 @@ class TerkleTree:
     levels: list               # levels[l][u] = node commitment point (bottom level first)
     values: list               # values[l] = child values of level l (flat, lex per node)
     srs: Srs = field(repr=False, default=None)
+    # node openings already computed: (level, node, slot) -> TensorOpening.  prove() is a
+    # pure function of the (immutable) tree, so repeated challenges reuse them
+    _openings: dict = field(repr=False, default_factory=dict)
 
     @property
     def root(self) -> Commitment:
@@ -162,8 +165,10 @@ def prove(tree: TerkleTree, i: int) -> MembershipProof:
     pos = i
     for l in range(tree.depth):
         u, slot = divmod(pos, B)
-        Z = tree.values[l][u * B:(u + 1) * B]
-        op = tc_open(tree.srs, Z, child_point(slot, tree.config.shape))
+        op = tree._openings.get((l, u, slot))
+        if op is None:
+            Z = tree.values[l][u * B:(u + 1) * B]
+            op = tree._openings[(l, u, slot)] = tc_open(tree.srs, Z, child_point(slot, tree.config.shape))
         nodes.append(tree.levels[l][u])
         openings.append(op)
         pos = u

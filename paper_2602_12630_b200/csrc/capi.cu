@@ -864,6 +864,42 @@ int tc_commit_stream(tc_ctx* ctx, const tc_srs* srs, const void* const* h_cur, c
   return commit_many(ctx, srs, ptrs.data(), count, dtype, scale_bits, route, out43);
 }
 
+// L_k(omega_a) (canonical) and 1 / (k + 1 - omega_a) for every axis, concatenated
+static void lag_weights(const tc_srs* srs, const std::vector<Fe>& om, std::vector<Fe>& lam, std::vector<Fe>& inv) {
+  lam.clear();
+  inv.clear();
+  for (int a = 0; a < srs->m; a++) {
+    const uint32_t d = srs->shape[a];
+    std::vector<Fe> la;
+    axis_tables(om[a], d, true, la);   // L_k(omega_a), canonical
+    const Fe w = Fp::to_mont(om[a]);
+    std::vector<Fe> diff(d), pref(d);
+    Fe run = Fp::one();
+    for (uint32_t k = 0; k < d; k++) {
+      diff[k] = Fp::sub(Fp::to_mont_small(k + 1), w);
+      pref[k] = run;
+      run = Fp::mul(run, diff[k]);
+    }
+    Fe iv = Fp::inv(run);
+    std::vector<Fe> ik(d);
+    for (int k = (int)d - 1; k >= 0; k--) {
+      ik[k] = Fp::canon(Fp::mul(iv, pref[k]));
+      iv = Fp::mul(iv, diff[k]);
+    }
+    for (uint32_t k = 0; k < d; k++) lam.push_back(Fp::canon(Fp::to_mont(la[k])));
+    inv.insert(inv.end(), ik.begin(), ik.end());
+  }
+}
+
+static bool point_on_grid(const tc_srs* srs, const std::vector<Fe>& om) {
+  for (int a = 0; a < srs->m; a++)
+    for (uint32_t k = 1; k <= srs->shape[a]; k++) {
+      Fe z{{k, 0, 0, 0, 0, 0}};
+      if (memcmp(z.v, om[a].v, sizeof z.v) == 0) return true;
+    }
+  return false;
+}
+
 int tc_open(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int scale_bits, const uint8_t* omega_le21,
             int route, uint8_t* out_y21, uint8_t* out_pi43) {
   if (!ctx || !srs || !d_in || !omega_le21 || !out_y21 || !out_pi43) return TC_ERR_ARGUMENT;
@@ -877,38 +913,13 @@ int tc_open(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int sca
   // Lagrange route: quotients evaluated on the grid straight from the samples (no
   // interpolation), committed over the (sub-grid) Lagrange elements.  Needs omega off the
   // grid on every axis (on a node the quotient value is a derivative) — else monomial.
-  bool on_grid = false;
-  for (int a = 0; a < m; a++)
-    for (uint32_t k = 1; k <= srs->shape[a] && !on_grid; k++) {
-      Fe z{{k, 0, 0, 0, 0, 0}};
-      on_grid = (memcmp(z.v, om[a].v, sizeof z.v) == 0);
-    }
+  const bool on_grid = point_on_grid(srs, om);
   const bool lag_ok = srs->lagrange && (m == 1 || srs->sublag) && !on_grid;
   if (route == TC_ROUTE_LAGRANGE && !lag_ok && !on_grid)
     return fail(ctx, TC_ERR_VALUE, "srs has no Lagrange elements");
   if (lag_ok && route != TC_ROUTE_MONOMIAL) {
     std::vector<Fe> lam, inv;
-    for (int a = 0; a < m; a++) {
-      const uint32_t d = srs->shape[a];
-      std::vector<Fe> la;
-      axis_tables(om[a], d, true, la);   // L_k(omega_a), canonical
-      const Fe w = Fp::to_mont(om[a]);
-      std::vector<Fe> diff(d), pref(d);
-      Fe run = Fp::one();
-      for (uint32_t k = 0; k < d; k++) {
-        diff[k] = Fp::sub(Fp::to_mont_small(k + 1), w);
-        pref[k] = run;
-        run = Fp::mul(run, diff[k]);
-      }
-      Fe iv = Fp::inv(run);
-      std::vector<Fe> ik(d);
-      for (int k = (int)d - 1; k >= 0; k--) {
-        ik[k] = Fp::canon(Fp::mul(iv, pref[k]));
-        iv = Fp::mul(iv, diff[k]);
-      }
-      for (uint32_t k = 0; k < d; k++) lam.push_back(Fp::canon(Fp::to_mont(la[k])));
-      inv.insert(inv.end(), ik.begin(), ik.end());
-    }
+    lag_weights(srs, om, lam, inv);
     Fe* qs;
     TC_TRY(tcrt::scratch_t(ctx, "open.q", (uint64_t)m * n, &qs));
     Fe y;
@@ -943,6 +954,71 @@ int tc_open(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int sca
   for (int a = 0; a < m; a++) ptrs[a] = qs + (uint64_t)a * n;
   TC_TRY(msm_srs(ctx, srs, TC_SRS_MONOMIAL, TC_DTYPE_FP_LIMBS, 0, ptrs.data(), m, d_out));
   return fetch_encode_many(ctx, d_out, m, out_pi43);
+}
+
+// Many openings against one SRS (config 4): the Lagrange-route quotients of up to G
+// openings are evaluated, then every axis a runs ONE batched MSM over the (sub-grid)
+// Lagrange bases shared by all of them, so the per-MSM fixed costs (window plan, bucket
+// reduction tails, host round trips) are paid once per group instead of once per proof.
+// Openings whose point lies on the grid (or route = monomial) go through tc_open.
+int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype, int scale_bits,
+                  const uint8_t* omegas_le21, int route, uint8_t* out_y21, uint8_t* out_pi43) {
+  if (!ctx || !srs || (count && (!d_ins || !omegas_le21 || !out_y21 || !out_pi43)) || count < 0)
+    return TC_ERR_ARGUMENT;
+  const uint64_t n = srs->n;
+  const int m = srs->m;
+  std::vector<int> lag;
+  for (int i = 0; i < count; i++) {
+    if (!d_ins[i]) return TC_ERR_ARGUMENT;
+    std::vector<Fe> om(m);
+    for (int j = 0; j < m; j++)
+      if (!le21_to_fe(omegas_le21 + 21 * ((size_t)i * m + j), om[j]))
+        return fail(ctx, TC_ERR_VALUE, "opening %d: point coordinate %d out of range", i, j);
+    const bool lag_ok = srs->lagrange && (m == 1 || srs->sublag) && !point_on_grid(srs, om);
+    if (lag_ok && route != TC_ROUTE_MONOMIAL)
+      lag.push_back(i);
+    else
+      TC_TRY(tc_open(ctx, srs, d_ins[i], dtype, scale_bits, omegas_le21 + 21 * (size_t)i * m, route,
+                     out_y21 + 21 * (size_t)i, out_pi43 + 43 * (size_t)i * m));
+  }
+  if (lag.empty()) return TC_OK;
+  const EdAff *ed_lag, *ed_sub = nullptr;
+  TC_TRY(tcrt::srs_edwards(ctx, const_cast<tc_srs*>(srs), TC_SRS_LAGRANGE, &ed_lag));
+  if (m > 1) TC_TRY(tcrt::srs_edwards(ctx, const_cast<tc_srs*>(srs), 0, &ed_sub));
+  static const uint64_t G_ENV = getenv("TC_OPEN_GROUP") ? (uint64_t)atoi(getenv("TC_OPEN_GROUP")) : 0;
+  const int G = (int)std::max<uint64_t>(1, std::min<uint64_t>(lag.size(), G_ENV ? G_ENV : (1ull << 24) / n));
+  Fe* qall;
+  Aff* d_out;
+  TC_TRY(tcrt::scratch_t(ctx, "openb.q", (uint64_t)G * m * n, &qall));
+  TC_TRY(tcrt::scratch_t(ctx, "openb.out", (uint64_t)G * m, &d_out));
+  std::vector<uint8_t> enc((size_t)G * m * 43);
+  std::vector<Fe> om(m), lam, inv;
+  for (size_t g0 = 0; g0 < lag.size(); g0 += G) {
+    const int gc = (int)std::min<size_t>(G, lag.size() - g0);
+    for (int k = 0; k < gc; k++) {
+      const int i = lag[g0 + k];
+      for (int j = 0; j < m; j++) le21_to_fe(omegas_le21 + 21 * ((size_t)i * m + j), om[j]);
+      lag_weights(srs, om, lam, inv);
+      Fe* vals;
+      TC_TRY(load_field_tensor(ctx, d_ins[i], dtype, n, scale_bits, &vals, "open.vals"));
+      Fe y;
+      TC_TRY(tcrt::open_quotients_lagrange_device(ctx, vals, srs->shape, m, lam, inv, qall + (uint64_t)k * m * n, &y));
+      fe_to_le21(y, out_y21 + 21 * (size_t)i);
+    }
+    uint64_t span = n;
+    std::vector<const void*> ptrs(gc);
+    for (int a = 0; a < m; a++) {
+      const EdAff* bases = a == 0 ? ed_lag : ed_sub + srs->sublag_off[a];
+      for (int k = 0; k < gc; k++) ptrs[k] = qall + ((uint64_t)k * m + a) * n;
+      TC_TRY(tcrt::msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, ptrs.data(), gc, bases, span, d_out + (uint64_t)a * gc));
+      span /= srs->shape[a];
+    }
+    TC_TRY(fetch_encode_many(ctx, d_out, m * gc, enc.data()));
+    for (int a = 0; a < m; a++)
+      for (int k = 0; k < gc; k++)
+        memcpy(out_pi43 + 43 * ((size_t)lag[g0 + k] * m + a), enc.data() + 43 * ((size_t)a * gc + k), 43);
+  }
+  return TC_OK;
 }
 
 // ---- Terkle ----

@@ -305,6 +305,32 @@ def test_commit_stream_prefetch_and_prover_stream():
         assert r == root
 
 
+def test_open_many_matches_tc_open():
+    """tc_open_batch (grouped quotient MSMs, one pipeline per axis) gives the same bytes as
+    tc_open for every opening: repeated tensors, on-grid points (monomial fallback) mixed
+    with random field points, groups smaller than the batch (TC_OPEN_GROUP is read once, so
+    the auto group size is exercised here with more openings than one group holds)."""
+    tcb = T()
+    shape = (4, 8, 16)
+    srs, td = tcb.setup_srs(shape, b"open-many")
+    g = np.random.default_rng(31)
+    xs = [torch.from_numpy((g.standard_t(3, 512) * s).astype(np.float16)).cuda() for s in (0.5, 2.0, 4.0)]
+    rng = random.Random(3)
+    tensors, points = [], []
+    for k in range(11):
+        tensors.append(xs[k % 3])
+        points.append([rng.randrange(O.P) for _ in shape] if k != 4 else [2, 5, 7])
+    got = tcb.tc_open_many(srs, tensors, points)
+    for t, pt, op in zip(tensors, points, got):
+        want = tcb.tc_open(srs, t, pt)
+        assert op == want
+        vals = O.quantize(t.cpu().numpy().astype(np.float64), 16)
+        y, proofs = O.open_trapdoor(vals, shape, list(td.taus), pt)
+        assert op.y == y and list(op.proofs) == proofs
+    C = tcb.tc_commit(srs, xs[0])
+    assert tcb.tc_verify(srs, C, points[0], got[0])
+
+
 # ---------------------------------------------------------------- full-size configs
 def _config3_layer(l):
     scales = np.random.default_rng(12345).uniform(0.5, 4.0, 32)
