@@ -509,7 +509,7 @@ def run_openings(args, dev, rank, world):
                       "unit": "openings/s", "n_gpus": 1, "ms_per_opening": 1e3 * wall / len(chals),
                       "config": {"workload": "config4: 256 challenges on the config-3 tree, layers drawn by a seeded "
                                  "Pareto score vector, random field points",
-                                 "path": "tc_open_many (quotients of 8 openings -> one batched MSM per axis) + "
+                                 "path": "tc_open_many (layers opened >= 6 times: slice commitments H[c',c] once per layer, pi_0 as a d0^2-point MSM; others: quotients of 8 openings -> one batched MSM per axis) + "
                                          "prove() per challenge (node openings memoised per tree)"}}), flush=True)
 
 

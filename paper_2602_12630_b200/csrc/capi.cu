@@ -956,10 +956,16 @@ int tc_open(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int sca
   return fetch_encode_many(ctx, d_out, m, out_pi43);
 }
 
-// Many openings against one SRS (config 4): the Lagrange-route quotients of up to G
-// openings are evaluated, then every axis a runs ONE batched MSM over the (sub-grid)
-// Lagrange bases shared by all of them, so the per-MSM fixed costs (window plan, bucket
-// reduction tails, host round trips) are paid once per group instead of once per proof.
+// Many openings against one SRS (config 4).  Two batched strategies, both exact:
+//  * grouped: the Lagrange-route quotients of up to G openings are evaluated, then every
+//    axis a runs ONE batched MSM over the (sub-grid) Lagrange bases shared by all of them,
+//    so the per-MSM fixed costs are paid once per group;
+//  * slice commitments (a tensor opened >= TC_OPEN_PRECOMP_MIN times, m >= 2): with
+//    R = N / d_0, H[c', c] = sum_rest T[c', rest] G[c, rest] (d_0^2 small-scalar MSMs over
+//    the slices of the Lagrange SRS, computed once per tensor as one multi-base batch), and
+//    pi_0 = sum_{c, c'} (delta_{c c'} - L_c'(omega_0)) / (c + 1 - omega_0) * H[c', c]
+//    (the axis-0 quotient q_0(a) = (T[a] - sum_c' L_c'(omega_0) T[c', a_rest]) / (a_0 + 1
+//    - omega_0), regrouped) — a d_0^2-point MSM per opening instead of an N-point one.
 // Openings whose point lies on the grid (or route = monomial) go through tc_open.
 int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype, int scale_bits,
                   const uint8_t* omegas_le21, int route, uint8_t* out_y21, uint8_t* out_pi43) {
@@ -985,38 +991,98 @@ int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int 
   const EdAff *ed_lag, *ed_sub = nullptr;
   TC_TRY(tcrt::srs_edwards(ctx, const_cast<tc_srs*>(srs), TC_SRS_LAGRANGE, &ed_lag));
   if (m > 1) TC_TRY(tcrt::srs_edwards(ctx, const_cast<tc_srs*>(srs), 0, &ed_sub));
+  size_t esz = 0;
+  if (dtype_size(dtype, &esz)) return fail(ctx, TC_ERR_ARGUMENT, "open: unsupported dtype %d", dtype);
+
+  // split: tensors opened often enough take the slice-commitment route
+  static const int PMIN = getenv("TC_OPEN_PRECOMP_MIN") ? atoi(getenv("TC_OPEN_PRECOMP_MIN")) : 6;
+  const uint32_t d0 = srs->shape[0];
+  const uint64_t R = n / d0;
+  std::map<const void*, std::vector<int>> by_tensor;
+  for (int i : lag) by_tensor[d_ins[i]].push_back(i);
+  std::vector<std::vector<int>> jobs;   // each job: openings sharing one strategy (+ tensor)
+  std::vector<const void*> job_h;       // tensor whose slice commitments the job uses, or null
+  std::vector<int> rest;
+  for (int i : lag) {
+    auto& v = by_tensor[d_ins[i]];
+    if (m >= 2 && PMIN > 0 && (int)v.size() >= PMIN && d0 * d0 <= 4096) {
+      if (v.front() == i) jobs.push_back(v), job_h.push_back(d_ins[i]);
+    } else {
+      rest.push_back(i);
+    }
+  }
   static const uint64_t G_ENV = getenv("TC_OPEN_GROUP") ? (uint64_t)atoi(getenv("TC_OPEN_GROUP")) : 0;
-  const int G = (int)std::max<uint64_t>(1, std::min<uint64_t>(lag.size(), G_ENV ? G_ENV : (1ull << 24) / n));
-  Fe* qall;
-  Aff* d_out;
+  const int G = (int)std::max<uint64_t>(1, G_ENV ? G_ENV : (1ull << 24) / n);
+  for (size_t g0 = 0; g0 < rest.size(); g0 += G) {
+    jobs.push_back(std::vector<int>(rest.begin() + g0, rest.begin() + std::min(rest.size(), g0 + G)));
+    job_h.push_back(nullptr);
+  }
+
+  Fe *qall, *sc = nullptr;
+  Aff *d_out, *hpts = nullptr;
+  EdAff* hed = nullptr;
   TC_TRY(tcrt::scratch_t(ctx, "openb.q", (uint64_t)G * m * n, &qall));
   TC_TRY(tcrt::scratch_t(ctx, "openb.out", (uint64_t)G * m, &d_out));
   std::vector<uint8_t> enc((size_t)G * m * 43);
-  std::vector<Fe> om(m), lam, inv;
-  for (size_t g0 = 0; g0 < lag.size(); g0 += G) {
-    const int gc = (int)std::min<size_t>(G, lag.size() - g0);
-    for (int k = 0; k < gc; k++) {
-      const int i = lag[g0 + k];
-      for (int j = 0; j < m; j++) le21_to_fe(omegas_le21 + 21 * ((size_t)i * m + j), om[j]);
-      lag_weights(srs, om, lam, inv);
-      Fe* vals;
-      TC_TRY(load_field_tensor(ctx, d_ins[i], dtype, n, scale_bits, &vals, "open.vals"));
-      Fe y;
-      TC_TRY(tcrt::open_quotients_lagrange_device(ctx, vals, srs->shape, m, lam, inv, qall + (uint64_t)k * m * n, &y));
-      fe_to_le21(y, out_y21 + 21 * (size_t)i);
+  std::vector<Fe> om(m), lam, inv, stabs;
+  for (size_t jb = 0; jb < jobs.size(); jb++) {
+    const std::vector<int>& ops = jobs[jb];
+    const bool sliced = job_h[jb] != nullptr;
+    if (sliced) {
+      // H[c', c]: d0^2 MSMs of R points, MSM (c', c) = tensor slice c' over SRS slice c
+      const uint32_t nh = d0 * d0;
+      TC_TRY(tcrt::scratch_t(ctx, "openh.pts", (uint64_t)nh, &hpts));
+      TC_TRY(tcrt::scratch_t(ctx, "openh.ed", (uint64_t)nh, &hed));
+      TC_TRY(tcrt::scratch_t(ctx, "openh.s", (uint64_t)G * nh, &sc));
+      std::vector<const void*> hp(nh);
+      std::vector<uint32_t> boff(nh);
+      for (uint32_t cp = 0; cp < d0; cp++)
+        for (uint32_t c = 0; c < d0; c++) {
+          hp[cp * d0 + c] = (const uint8_t*)job_h[jb] + esz * R * cp;
+          boff[cp * d0 + c] = (uint32_t)(R * c);
+        }
+      TC_TRY(tcrt::msm_batch_device(ctx, dtype, scale_bits, hp.data(), (int)nh, ed_lag, R, hpts, boff.data()));
+      TC_TRY(tcrt::to_edwards_device(ctx, hpts, nh, hed));
     }
-    uint64_t span = n;
-    std::vector<const void*> ptrs(gc);
-    for (int a = 0; a < m; a++) {
-      const EdAff* bases = a == 0 ? ed_lag : ed_sub + srs->sublag_off[a];
-      for (int k = 0; k < gc; k++) ptrs[k] = qall + ((uint64_t)k * m + a) * n;
-      TC_TRY(tcrt::msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, ptrs.data(), gc, bases, span, d_out + (uint64_t)a * gc));
-      span /= srs->shape[a];
+    for (size_t g0 = 0; g0 < ops.size(); g0 += G) {
+      const int gc = (int)std::min<size_t>(G, ops.size() - g0);
+      stabs.clear();
+      for (int k = 0; k < gc; k++) {
+        const int i = ops[g0 + k];
+        for (int j = 0; j < m; j++) le21_to_fe(omegas_le21 + 21 * ((size_t)i * m + j), om[j]);
+        lag_weights(srs, om, lam, inv);
+        if (sliced) {
+          stabs.insert(stabs.end(), lam.begin(), lam.begin() + d0);
+          stabs.insert(stabs.end(), inv.begin(), inv.begin() + d0);
+        }
+        Fe* vals;
+        TC_TRY(load_field_tensor(ctx, d_ins[i], dtype, n, scale_bits, &vals, "open.vals"));
+        Fe y;
+        TC_TRY(tcrt::open_quotients_lagrange_device(ctx, vals, srs->shape, m, lam, inv, qall + (uint64_t)k * m * n, &y,
+                                                    sliced));
+        fe_to_le21(y, out_y21 + 21 * (size_t)i);
+      }
+      uint64_t span = n;
+      std::vector<const void*> ptrs(gc);
+      for (int a = 0; a < m; a++) {
+        if (a == 0 && sliced) {
+          const uint32_t nh = d0 * d0;
+          TC_TRY(tcrt::slice_scalars_device(ctx, stabs, d0, (uint32_t)gc, sc));
+          for (int k = 0; k < gc; k++) ptrs[k] = sc + (uint64_t)k * nh;
+          TC_TRY(tcrt::msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, ptrs.data(), gc, hed, nh, d_out));
+        } else {
+          const EdAff* bases = a == 0 ? ed_lag : ed_sub + srs->sublag_off[a];
+          for (int k = 0; k < gc; k++) ptrs[k] = qall + ((uint64_t)k * m + a) * n;
+          TC_TRY(tcrt::msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, ptrs.data(), gc, bases, span,
+                                        d_out + (uint64_t)a * gc));
+        }
+        span /= srs->shape[a];
+      }
+      TC_TRY(fetch_encode_many(ctx, d_out, m * gc, enc.data()));
+      for (int a = 0; a < m; a++)
+        for (int k = 0; k < gc; k++)
+          memcpy(out_pi43 + 43 * ((size_t)ops[g0 + k] * m + a), enc.data() + 43 * ((size_t)a * gc + k), 43);
     }
-    TC_TRY(fetch_encode_many(ctx, d_out, m * gc, enc.data()));
-    for (int a = 0; a < m; a++)
-      for (int k = 0; k < gc; k++)
-        memcpy(out_pi43 + 43 * ((size_t)lag[g0 + k] * m + a), enc.data() + 43 * ((size_t)a * gc + k), 43);
   }
   return TC_OK;
 }

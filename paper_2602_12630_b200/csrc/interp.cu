@@ -110,10 +110,27 @@ __global__ void k_open_axis_lag(const Fe* r, uint32_t d, uint64_t rest, const Fe
   for (uint32_t k = 0; k < d; k++) mac_wide(acc, r[(uint64_t)k * rest + i], lam[k]);
   const Fe next = Fp::canon(Fp::redc(acc));
   rn[i] = next;
+  if (!q) return;   // caller commits this axis another way (slice-commitment openings)
   for (uint32_t k = 0; k < d; k++) {
     const uint64_t pos = (uint64_t)k * rest + i;
     q[pos] = Fp::canon(Fp::mul(Fp::sub(r[pos], next), inv[k]));
   }
+}
+
+// Slice-commitment opening scalars (tc_open_batch): for opening o with axis-0 weights
+// lam = L_c'(omega_0) and inv = 1/(c + 1 - omega_0) (Montgomery form, as k_open_axis_lag
+// takes them; tabs[o] = lam[d] ++ inv[d]), s[o][c' d + c] = (delta_{c c'} - lam[c']) inv[c]
+// (canonical out), so pi_0 = sum s * H[c', c].
+__global__ void k_slice_scalars(const Fe* tabs, uint32_t d, uint32_t count, Fe* out) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t dd = (uint64_t)d * d;
+  if (t >= dd * count) return;
+  const uint64_t o = t / dd;
+  const uint32_t cp = (uint32_t)((t % dd) / d), c = (uint32_t)(t % d);
+  const Fe* lam = tabs + o * 2 * d;
+  const Fe* inv = lam + d;
+  const Fe x = Fp::sub(c == cp ? Fp::one() : Fp::zero(), lam[cp]);   // Montgomery
+  out[t] = Fp::from_mont(Fp::mul(x, inv[c]));                        // canonical
 }
 
 // out[rest] = sum_k c[k, rest] x^k  (Horner along the leading axis of extent d)
@@ -222,7 +239,7 @@ int open_quotients_device(tc_ctx* ctx, const Fe* d_coeffs, const uint32_t* shape
 
 int open_quotients_lagrange_device(tc_ctx* ctx, Fe* d_vals, const uint32_t* shape, int m,
                                    const std::vector<Fe>& lam, const std::vector<Fe>& inv, Fe* d_quotients,
-                                   Fe* h_y) {
+                                   Fe* h_y, bool skip_q0) {
   cudaStream_t st = ctx->stream;
   uint64_t n = 1;
   uint32_t dsum = 0;
@@ -247,7 +264,7 @@ int open_quotients_lagrange_device(tc_ctx* ctx, Fe* d_vals, const uint32_t* shap
     // kernels are stream-ordered, so r_a is never overwritten while it is read
     Fe* rn = (a & 1) ? bufB : bufA;
     k_open_axis_lag<<<blocks_for(rest, 128), 128, 0, st>>>(r, d, rest, tabs + off, tabs + dsum + off, rn,
-                                                           d_quotients + (uint64_t)a * n);
+                                                           (a == 0 && skip_q0) ? nullptr : d_quotients + (uint64_t)a * n);
     TC_LAUNCHED(ctx);
     r = rn;
     span = rest;
@@ -255,6 +272,19 @@ int open_quotients_lagrange_device(tc_ctx* ctx, Fe* d_vals, const uint32_t* shap
   }
   TC_CUDA(ctx, cudaMemcpyAsync(h_y, r, sizeof(Fe), cudaMemcpyDeviceToHost, st));
   TC_CUDA(ctx, cudaStreamSynchronize(st));
+  return TC_OK;
+}
+
+int slice_scalars_device(tc_ctx* ctx, const std::vector<Fe>& tabs_host, uint32_t d, uint32_t count, Fe* d_out) {
+  cudaStream_t st = ctx->stream;
+  Fe* tabs;
+  TC_TRY(scratch_t(ctx, "openh.tabs", tabs_host.size(), &tabs));
+  // pageable source: the synchronous copy completes before tabs_host can change
+  TC_CUDA(ctx, cudaMemcpyAsync(tabs, tabs_host.data(), tabs_host.size() * sizeof(Fe), cudaMemcpyHostToDevice, st));
+  TC_CUDA(ctx, cudaStreamSynchronize(st));
+  const uint64_t tot = (uint64_t)d * d * count;
+  k_slice_scalars<<<blocks_for(tot, 128), 128, 0, st>>>(tabs, d, count, d_out);
+  TC_LAUNCHED(ctx);
   return TC_OK;
 }
 

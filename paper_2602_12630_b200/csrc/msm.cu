@@ -635,11 +635,13 @@ __device__ __forceinline__ uint32_t find_bucket(const uint32_t* off, uint32_t nb
 // add per entry (no exceptional cases, ec.cuh).
 __global__ void __launch_bounds__(128) k_accum_aff(const uint32_t* vals, const EdAff* bases, const uint32_t* bstart,
                                                    const uint32_t* bend, const uint32_t* toff, const uint32_t* ooff,
-                                                   uint32_t nb, uint32_t T, Ext* items, Ext* buckets) {
+                                                   uint32_t nb, uint32_t T, Ext* items, Ext* buckets,
+                                                   const uint32_t* boff, uint32_t nbm) {
   uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t total = toff[nb];
   if (p >= total) return;
   uint32_t k = find_bucket(toff, nb, p);
+  if (boff) bases += boff[k / nbm];   // multi-base batch: MSM l reads bases + boff[l]
   uint32_t piece = p - toff[k];
   uint32_t a = bstart[k] + piece * T;
   uint32_t b = min(a + T, bend[k]);
@@ -890,7 +892,7 @@ namespace tcrt {
 int quantize_flags_to_status(tc_ctx* ctx, uint32_t f);
 
 int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* h_ptrs, int L, const EdAff* d_bases,
-                     uint64_t n, Aff* d_out) {
+                     uint64_t n, Aff* d_out, const uint32_t* h_boff) {
   cudaStream_t st = ctx->stream;
   if (L <= 0) return TC_OK;
   if (n >= (1ull << 31)) return fail(ctx, TC_ERR_VALUE, "msm: too many points (%llu)", (unsigned long long)n);
@@ -909,7 +911,8 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     if ((uint64_t)L > G) {
       for (int l0 = 0; l0 < L; l0 += (int)G) {
         const int cnt = (int)std::min<uint64_t>(G, (uint64_t)(L - l0));
-        TC_TRY(msm_batch_device(ctx, dtype, scale_bits, h_ptrs + l0, cnt, d_bases, n, d_out + l0));
+        TC_TRY(msm_batch_device(ctx, dtype, scale_bits, h_ptrs + l0, cnt, d_bases, n, d_out + l0,
+                                h_boff ? h_boff + l0 : nullptr));
       }
       return TC_OK;
     }
@@ -919,6 +922,14 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   TC_TRY(scratch_t(ctx, "msm.ptrs", (uint64_t)L, (void***)&d_ptrs));
   memcpy(ctx->h_stage, h_ptrs, sizeof(void*) * L);
   TC_CUDA(ctx, cudaMemcpyAsync(d_ptrs, ctx->h_stage, sizeof(void*) * L, cudaMemcpyHostToDevice, st));
+  uint32_t* d_boff = nullptr;
+  if (h_boff) {   // per-MSM base offsets (staged behind the pointers)
+    if (sizeof(void*) * L + sizeof(uint32_t) * L > 65536) return fail(ctx, TC_ERR_VALUE, "msm: batch too large");
+    TC_TRY(scratch_t(ctx, "msm.boff", (uint64_t)L, &d_boff));
+    memcpy((char*)ctx->h_stage + sizeof(void*) * L, h_boff, sizeof(uint32_t) * L);
+    TC_CUDA(ctx, cudaMemcpyAsync(d_boff, (char*)ctx->h_stage + sizeof(void*) * L, sizeof(uint32_t) * L,
+                                 cudaMemcpyHostToDevice, st));
+  }
 
   // 1. bit-length histogram + quantisation status
   uint32_t* d_small;
@@ -1157,7 +1168,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   ctx->launches += 4;
   if (ctx->prof) TC_CUDA(ctx, cudaEventRecord(ctx->ev[0], st));
   k_accum_aff<<<blocks_for((E + T - 1) / T + nb, 128), 128, 0, st>>>(svals, d_bases, bstart, bend, toff, offA, nb, T,
-                                                                       itemsA, buckets);
+                                                                       itemsA, buckets, d_boff, P.nbm);
   TC_LAUNCHED(ctx);
   if (ctx->prof) {
     TC_CUDA(ctx, cudaEventRecord(ctx->ev[1], st));

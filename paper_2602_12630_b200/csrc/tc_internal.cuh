@@ -127,8 +127,10 @@ int msm_device(tc_ctx* ctx, ScalarKind kind, const void* d_scalars, const tc::Ed
 // L MSMs over the same n bases in one pipeline: d_out[l] = sum_k s_l[k] * bases[k].
 // h_ptrs: L device pointers (host array) to n scalars of `dtype` (TC_DTYPE_FP_LIMBS =
 // canonical limbs; float dtypes are quantised at scale_bits inside the digit kernel).
+// h_boff (optional, host, L entries): MSM l reads the bases d_bases + h_boff[l] (batches of
+// MSMs over different slices of one SRS, e.g. the opening slice commitments)
 int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* h_ptrs, int L,
-                     const tc::EdAff* d_bases, uint64_t n, tc::Aff* d_out);
+                     const tc::EdAff* d_bases, uint64_t n, tc::Aff* d_out, const uint32_t* h_boff = nullptr);
 
 // Montgomery affine points -> twisted Edwards affine (x, y, t = x y), batched inversion
 int to_edwards_device(tc_ctx* ctx, const tc::Aff* d_in, uint64_t n, tc::EdAff* d_out);
@@ -164,7 +166,11 @@ int evaluate_device(tc_ctx* ctx, const tc::Fe* d_coeffs, const uint32_t* shape, 
 // q_a is written at d_quotients + a*N (only its first prod_{j>=a} d_j entries); y on host.
 int open_quotients_lagrange_device(tc_ctx* ctx, tc::Fe* d_vals, const uint32_t* shape, int m,
                                    const std::vector<tc::Fe>& lam, const std::vector<tc::Fe>& inv,
-                                   tc::Fe* d_quotients, tc::Fe* h_y);
+                                   tc::Fe* d_quotients, tc::Fe* h_y, bool skip_q0 = false);
+// s[o][c' d + c] = (delta_{c c'} - lam_o[c']) inv_o[c] for `count` openings (tabs: per
+// opening lam[d] ++ inv[d], Montgomery form) — the scalars of pi_0 over slice commitments
+int slice_scalars_device(tc_ctx* ctx, const std::vector<tc::Fe>& tabs_host, uint32_t d, uint32_t count,
+                         tc::Fe* d_out);
 
 // open_quotients on device: coefficient array (canonical) -> m quotient arrays + y
 int open_quotients_device(tc_ctx* ctx, const tc::Fe* d_coeffs, const uint32_t* shape, int m,

@@ -317,8 +317,10 @@ def test_open_many_matches_tc_open():
     xs = [torch.from_numpy((g.standard_t(3, 512) * s).astype(np.float16)).cuda() for s in (0.5, 2.0, 4.0)]
     rng = random.Random(3)
     tensors, points = [], []
-    for k in range(11):
-        tensors.append(xs[k % 3])
+    # xs[0] is opened 9 times (>= TC_OPEN_PRECOMP_MIN: slice-commitment route, one of them
+    # on the grid -> tc_open), xs[1] / xs[2] a few times (grouped route)
+    for k in range(15):
+        tensors.append(xs[0] if k < 9 else xs[1 + k % 2])
         points.append([rng.randrange(O.P) for _ in shape] if k != 4 else [2, 5, 7])
     got = tcb.tc_open_many(srs, tensors, points)
     for t, pt, op in zip(tensors, points, got):
