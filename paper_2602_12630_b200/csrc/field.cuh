@@ -266,7 +266,10 @@ struct Field {
 #endif
 
 #ifndef TC_MULV
-#define TC_MULV 1   // 0: even/odd pair accumulators, 1: operand-scanning rows
+// 0: even/odd pair accumulators (every IMAD.WIDE on an aligned pair, no realigning moves),
+// 1: operand-scanning rows.  Row form was faster with XYZZ; with the Edwards adds the
+// even/odd form wins (k_accum_aff 5.98 -> 5.83 ms, config-3 step 10.14 -> 9.89 ms)
+#define TC_MULV 0
 #endif
 #ifndef TC_SQRV
 #define TC_SQRV 1   // 0: square through the generic product, 1: dedicated 21-product square (3% faster accumulation)

@@ -45,11 +45,24 @@ constexpr uint32_t HIST_SAMPLE = 8;   // histogram taken on every 8th element (k
 constexpr int DIG_EPT = 1;    // elements per thread in k_digits (8 measured 1.7x slower:
                               // per-thread entry ranges break store coalescing)
 
+// mode 0: signed-digit windows (bits [off, off + width) of the magnitude; bucket j of
+//         window w holds digit j + 1).
+// mode 1: float-exponent groups for fp16 / bf16 inputs.  A quantised fp value is
+//         |q| = m 2^k with at most MB = 11 (fp16) / 8 (bf16) significant bits, so group k
+//         holds m = |q| >> k: k = 0 takes |q| < 2^MB (m in [1, 2^MB)), k >= 1 takes
+//         bitlen(|q|) = MB + k (m in [2^(MB-1), 2^MB)).  ONE bucket entry per element (no
+//         carry window) and K * 2^(MB-1) buckets per MSM, none of them empty by construction
+//         of fp16 (a signed-window plan of the same data leaves ~85% of its 2^17 low-window
+//         buckets empty: fp16 has 1024 mantissas per octave).  Bucket j of group w holds
+//         weight mlo[w] + j; the groups are combined with weight 2^off[w] (off[w] = w).
 struct WinPlan {
   int nwin;
-  uint32_t nbm;              // buckets per MSM = sum_w 2^(c_w - 1)
-  uint8_t off[MAXW];         // first bit of window w
-  uint8_t width[MAXW];       // c_w
+  int mode;                  // 0 signed windows, 1 float-exponent groups
+  int mbits;                 // mode 1: significant bits of the input format
+  uint32_t nbm;              // buckets per MSM
+  uint8_t off[MAXW];         // window w: first bit (mode 0) / exponent k (mode 1)
+  uint8_t width[MAXW];       // mode 0: c_w
+  uint32_t mlo[MAXW];        // weight of the window's first bucket (mode 0: 1)
   uint32_t base[MAXW + 1];   // first bucket of window w inside one MSM
 };
 
@@ -368,6 +381,18 @@ __global__ void __launch_bounds__(256) k_digits_v(const void* const* ptrs, uint6
     for (int j = 0; j < HOT_MAXW; j++) hd[k][j] = 0xffffffffu;
     bool neg;
     const uint64_t mag = (i0 + k < n) ? quant64<DT>(raw[k], scale_bits, neg) : 0ull;
+    if (P.mode == 1) {   // float-exponent group: one entry per non-zero element
+      if (!mag) continue;
+      const int bl = 64 - __clzll((long long)mag);
+      const int g = bl > P.mbits ? bl - P.mbits : 0;
+      const uint32_t key = key0 + P.base[g] + (uint32_t)(mag >> g) - P.mlo[g];
+      const uint32_t val = (uint32_t)(i0 + k) | (neg ? SIGN_BIT : 0u);
+      if (SCATTER)
+        vals[atomicAdd(cnt + key, 1u)] = val;
+      else
+        atomicAdd(cnt + key, 1u);
+      continue;
+    }
     uint32_t carry = 0;
     for (int w = 0; w < P.nwin; w++) {
       const int c = P.width[w];
@@ -690,7 +715,7 @@ __global__ void __launch_bounds__(128, 4) k_bucket_reduce(const Ext* buckets, Wi
   uint32_t r = g % P.nbm;
   int w = 0;
   while (w + 1 < P.nwin && P.base[w + 1] <= r) w++;
-  uint32_t lo = r - P.base[w];   // digit of the segment's first bucket minus 1
+  uint32_t lo = r - P.base[w] + P.mlo[w] - 1;   // weight of the segment's first bucket minus 1
   const Ext* bw = buckets + g;
   Ext run = ext_zero(), sum = ext_zero();
   for (int b = (int)LS - 1; b >= 0; b--) {
@@ -771,14 +796,15 @@ __global__ void __launch_bounds__(128) k_wsum_level(const Ext* Tin, const Ext* D
   Dout[o] = u;
 }
 
-// W_g = D_g - c * S_g
-__global__ void k_wsum_final(const Ext* T, const Ext* D, uint32_t ngroups, uint32_t c, Ext* W) {
+// W_g = D_g - c * S_g + (mlo_w - 1) * S_g: sum_j (j+1) x_j re-based to the window's weights
+__global__ void k_wsum_final(const Ext* T, const Ext* D, uint32_t ngroups, uint32_t c, WinPlan P, Ext* W) {
   const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= ngroups) return;
   Ext w = D[g];
-  if (c) {
-    Ext s = ext_mul_small(T[g], c);
-    ext_add(w, ext_neg(s));
+  const int64_t coef = (int64_t)P.mlo[g % P.nwin] - 1 - (int64_t)c;
+  if (coef) {
+    Ext s = ext_mul_small(T[g], (uint32_t)(coef < 0 ? -coef : coef));
+    ext_add(w, coef < 0 ? ext_neg(s) : s);
   }
   W[g] = w;
 }
@@ -790,7 +816,7 @@ __global__ void k_final(const Ext* wsum, uint32_t L, WinPlan P, Aff* out) {
   const Ext* ws = wsum + (uint64_t)l * P.nwin;
   Ext acc = ws[P.nwin - 1];
   for (int w = P.nwin - 2; w >= 0; w--) {
-    for (int i = 0; i < P.width[w]; i++) acc = ext_dbl(acc);
+    for (int i = 0; i < P.off[w + 1] - P.off[w]; i++) acc = ext_dbl(acc);
     ext_add(acc, ws[w]);
   }
   Aff r = ext_to_aff(acc);
@@ -854,12 +880,15 @@ WinPlan plan_windows(const uint32_t* hist, uint32_t nbits, uint64_t L) {
     pos = o;
   }
   WinPlan P;
+  P.mode = 0;
+  P.mbits = 0;
   P.nwin = (int)wins.size();
   uint32_t b = 0;
   for (int w = 0; w < P.nwin; w++) {
     auto oc = wins[P.nwin - 1 - w];
     P.off[w] = (uint8_t)oc.first;
     P.width[w] = (uint8_t)oc.second;
+    P.mlo[w] = 1;
     P.base[w] = b;
     b += 1u << (oc.second - 1);
   }
@@ -870,6 +899,25 @@ WinPlan plan_windows(const uint32_t* hist, uint32_t nbits, uint64_t L) {
     for (int w = 0; w < P.nwin; w++) fprintf(stderr, " [%d,+%d)", P.off[w], P.width[w]);
     fprintf(stderr, " buckets/msm=%u\n", P.nbm);
   }
+  return P;
+}
+
+// mode-1 plan: groups k = 0 .. nbits - MB (see WinPlan)
+WinPlan plan_fp(uint32_t nbits, int mb) {
+  WinPlan P;
+  P.mode = 1;
+  P.mbits = mb;
+  P.nwin = nbits > (uint32_t)mb ? (int)nbits - mb + 1 : 1;
+  uint32_t b = 0;
+  for (int w = 0; w < P.nwin; w++) {
+    P.off[w] = (uint8_t)w;
+    P.width[w] = 0;
+    P.mlo[w] = w ? 1u << (mb - 1) : 1u;
+    P.base[w] = b;
+    b += w ? 1u << (mb - 1) : (1u << mb) - 1u;
+  }
+  P.base[P.nwin] = b;
+  P.nbm = b;
   return P;
 }
 
@@ -967,13 +1015,24 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     return TC_OK;
   }
 
-  // 2. window plan
-  const WinPlan P = plan_windows(hist, nbits, (uint64_t)L);
+  // 2. window plan: float-exponent groups for large fp16 / bf16 batches on the vectorised
+  //    digit path, signed windows from the histogram DP otherwise
+  static const bool want_bucketed = getenv("TC_MSM_BUCKETED") != nullptr;
+  static const bool want_radix = getenv("TC_MSM_SORT") != nullptr;   // radix-sort layout (A/B)
+  static const bool generic_digits = getenv("TC_MSM_GENERIC_DIGITS") != nullptr;
+  static const uint64_t FP_MIN_N = getenv("TC_MSM_FP_MIN_N") ? strtoull(getenv("TC_MSM_FP_MIN_N"), nullptr, 10)
+                                                            : (1ull << 15);
+  bool vec_ok = (dtype == TC_DTYPE_F16 || dtype == TC_DTYPE_BF16 || dtype == TC_DTYPE_F32) && nbits <= 61 &&
+                !generic_digits && !want_radix && !want_bucketed;
+  for (int l = 0; l < L && vec_ok; l++) vec_ok = ((uintptr_t)h_ptrs[l] & 15u) == 0;   // 16-byte vector loads
+  const int fp_mb = dtype == TC_DTYPE_F16 ? 11 : (dtype == TC_DTYPE_BF16 ? 8 : 0);
+  const bool fpmode = vec_ok && fp_mb && n >= FP_MIN_N && (int)nbits - fp_mb + 1 <= MAXW;
+  const WinPlan P = fpmode ? plan_fp(nbits, fp_mb) : plan_windows(hist, nbits, (uint64_t)L);
   if (P.nwin > MAXW) return fail(ctx, TC_ERR_VALUE, "msm: window plan too long");
   const uint64_t nb64 = (uint64_t)L * P.nbm;
   if (nb64 >= (1ull << 31)) return fail(ctx, TC_ERR_VALUE, "msm batch too large (%llu buckets)", (unsigned long long)nb64);
   const uint32_t nb = (uint32_t)nb64;
-  const uint64_t cap = (uint64_t)L * n * P.nwin;
+  const uint64_t cap = (uint64_t)L * n * (P.mode == 1 ? 1 : P.nwin);
   const int end_bit = (int)bitlen_u32(nb - 1);
 
   // 3. non-zero digits, compacted
@@ -987,9 +1046,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   // (TC_MSM_BUCKETED=1).  Measured slower on config 3 (pass A 3.8 ms + scatter 2.8 ms vs
   // digits 0.8 + onesweep 2.3 + bounds 0.4 ms): the per-layer slot counters and the
   // __match_any_sync aggregation serialise; kept for small-bucket experiments.
-  static const bool want_bucketed = getenv("TC_MSM_BUCKETED") != nullptr;
-  static const bool want_radix = getenv("TC_MSM_SORT") != nullptr;   // radix-sort layout (A/B)
-  const bool bucketed = want_bucketed && (size_t)P.nbm * 8 <= 160 * 1024;
+  const bool bucketed = want_bucketed && P.mode == 0 && (size_t)P.nbm * 8 <= 160 * 1024;
   if (!bucketed && !want_radix) {
     // counting-sort layout: count, scan, scatter (no keys stored, no radix passes)
     uint32_t *cnt, *cursor;
@@ -1002,10 +1059,9 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     HotPlan H{};
     H.nhot = 0;
     H.nhotb = 0;
-    bool fast = (dtype == TC_DTYPE_F16 || dtype == TC_DTYPE_BF16 || dtype == TC_DTYPE_F32) && nbits <= 61 &&
-                !getenv("TC_MSM_GENERIC_DIGITS");
-    for (int l = 0; l < L && fast; l++) fast = ((uintptr_t)h_ptrs[l] & 15u) == 0;   // 16-byte vector loads
-    for (int w = 0; w < P.nwin; w++) {
+    bool fast = vec_ok;
+    for (int w = 0; w < MAXW; w++) H.slot[w] = -1;
+    for (int w = 0; w < P.nwin && P.mode == 0; w++) {
       H.slot[w] = -1;
       const uint32_t nbw = 1u << (P.width[w] - 1);
       if (nbw <= HOT_BUCKETS) {
@@ -1020,6 +1076,10 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
         H.nhot++;
       }
     }
+    if (P.mode == 1 && !fast) return fail(ctx, TC_ERR_VALUE, "msm: float-exponent plan needs the vector path");
+    if (getenv("TC_MSM_DEBUG"))
+      fprintf(stderr, "[tc msm] L=%d n=%llu mode=%d groups=%d buckets/msm=%u\n", L, (unsigned long long)n, P.mode,
+              P.nwin, P.nbm);
     const unsigned gxv = blocks_for(n, 256 * V_EPT);
     const unsigned gx = std::min<unsigned>(blocks_for(n, 256), std::max(1u, (unsigned)ctx->num_sms * 16 / (unsigned)L + 1));
     int s = dispatch_dt(ctx, dtype, [&](auto dt) {
@@ -1264,7 +1324,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
       uint64_t p8 = 1;
       for (uint32_t r = 0; r < R; r++) p8 *= SEG;
       const uint32_t c = (uint32_t)((p8 - SEG) / (SEG - 1));
-      k_wsum_final<<<blocks_for(nw_total, 64), 64, 0, st>>>(Tin, Din, nw_total, c, wsum);
+      k_wsum_final<<<blocks_for(nw_total, 64), 64, 0, st>>>(Tin, Din, nw_total, c, P, wsum);
       TC_LAUNCHED(ctx);
       k_final<<<blocks_for(L, 32), 32, 0, st>>>(wsum, (uint32_t)L, P, d_out);
       TC_LAUNCHED(ctx);
@@ -1274,7 +1334,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     }
   }
   uint32_t minB = 1u << 30;
-  for (int w = 0; w < P.nwin; w++) minB = std::min<uint32_t>(minB, 1u << (P.width[w] - 1));
+  for (int w = 0; w < P.nwin; w++) minB = std::min<uint32_t>(minB, P.base[w + 1] - P.base[w]);
   uint32_t LS = 32u;
   while (LS > 2u && (uint64_t)nb / LS < (uint64_t)ctx->num_sms * 256u) LS >>= 1;
   LS = std::min<uint32_t>(LS, minB);

@@ -333,6 +333,42 @@ def test_open_many_matches_tc_open():
     assert tcb.tc_verify(srs, C, points[0], got[0])
 
 
+_FPMODE_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_2602_12630_b200 as tcb
+from oracle import tc_oracle as O
+shape = (8, 8, 16)
+srs, td = tcb.setup_srs(shape, b"fp-mode")
+g = np.random.default_rng(41)
+for dt in (torch.float16, torch.bfloat16):
+    xs = [torch.from_numpy((g.standard_t(3, 1024) * s).astype(np.float32)).to(dt) for s in (0.01, 1.0, 300.0)]
+    xs.append(torch.zeros(1024, dtype=dt))
+    comms = tcb.tc_commit_many(srs, [x.cuda() for x in xs])
+    for x, c in zip(xs, comms):
+        vals = O.quantize(x.float().numpy().astype(np.float64), 16)
+        assert c.elem == O.commit_trapdoor(vals, shape, list(td.taus)), dt
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("fp_min_n", ["1", "1000000000"])
+def test_msm_float_exponent_plan_small(fp_min_n, tmp_path):
+    """The float-exponent window plan (mode 1: one bucket entry per element, groups by
+    binary exponent) forced on small fp16 / bf16 tensors (TC_MSM_FP_MIN_N=1), and the
+    signed-window plan forced on the same (huge threshold): both equal the trapdoor oracle,
+    including tiny / huge / zero values."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "fpmode.py"
+    script.write_text(_FPMODE_SCRIPT.format(root=root))
+    env = dict(os.environ, TC_MSM_FP_MIN_N=fp_min_n)
+    out = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr
+
+
 # ---------------------------------------------------------------- full-size configs
 def _config3_layer(l):
     scales = np.random.default_rng(12345).uniform(0.5, 4.0, 32)
