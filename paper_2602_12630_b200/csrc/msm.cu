@@ -362,9 +362,13 @@ __device__ __forceinline__ uint64_t quant64(uint32_t b, int scale_bits, bool& ne
   return (uint64_t)(iq + ((rem > half || (rem == half && (iq & 1u))) ? 1u : 0u));
 }
 
+// nc: counter copies per bucket (mode 1): block b counts into copy b % nc, so the ~100-300
+// hits a popular fp16 bucket takes per MSM are spread over nc addresses (same-address L2
+// atomics serialise); bucket k's copies are adjacent, so one scan gives every copy its
+// own slice of the bucket and the bucket stays contiguous
 template <int DT, bool SCATTER>
 __global__ void __launch_bounds__(256) k_digits_v(const void* const* ptrs, uint64_t n, int scale_bits, WinPlan P,
-                                                  HotPlan H, uint32_t* cnt, uint32_t* vals) {
+                                                  HotPlan H, uint32_t* cnt, uint32_t* vals, uint32_t nc) {
   __shared__ uint32_t hcnt[HOT_MAXB];
   const uint32_t l = blockIdx.y;
   const void* p = ptrs[l];
@@ -387,10 +391,11 @@ __global__ void __launch_bounds__(256) k_digits_v(const void* const* ptrs, uint6
       const int g = bl > P.mbits ? bl - P.mbits : 0;
       const uint32_t key = key0 + P.base[g] + (uint32_t)(mag >> g) - P.mlo[g];
       const uint32_t val = (uint32_t)(i0 + k) | (neg ? SIGN_BIT : 0u);
+      uint32_t* c = cnt + (uint64_t)key * nc + blockIdx.x % nc;
       if (SCATTER)
-        vals[atomicAdd(cnt + key, 1u)] = val;
+        vals[atomicAdd(c, 1u)] = val;
       else
-        atomicAdd(cnt + key, 1u);
+        atomicAdd(c, 1u);
       continue;
     }
     uint32_t carry = 0;
@@ -490,6 +495,12 @@ __global__ void __launch_bounds__(256) k_scan_bits_v(const void* const* ptrs, ui
   __syncthreads();
   for (int i = threadIdx.x; i < NHIST; i += blockDim.x)
     if (hist[i]) atomicAdd(out + 1 + i, hist[i]);
+}
+
+// bucket starts from the per-copy exclusive scan: bstart[k] = S[k * nc], k = 0..nb
+__global__ void k_copy_starts(const uint32_t* S, uint32_t nb, uint32_t nc, uint32_t* bstart) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k <= nb) bstart[k] = S[(uint64_t)k * nc];
 }
 
 // ---- bucket-major layout without a radix sort (few buckets per MSM) -------------------
@@ -1050,10 +1061,20 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   if (!bucketed && !want_radix) {
     // counting-sort layout: count, scan, scatter (no keys stored, no radix passes)
     uint32_t *cnt, *cursor;
-    TC_TRY(scratch_t(ctx, "msm.bcount", (uint64_t)nb + 1, &cnt));
+    static const uint32_t NC_ENV = getenv("TC_MSM_NC") ? (uint32_t)atoi(getenv("TC_MSM_NC")) : 16u;   // sweep: 1 9.04, 4 7.79, 8 7.53, 16 7.40, 32 7.37 ms
+    const uint32_t NC = P.mode == 1 ? std::max(1u, NC_ENV) : 1u;
+    const uint64_t ncnt = (uint64_t)nb * NC + 1;
+    if (ncnt >= (1ull << 31)) return fail(ctx, TC_ERR_VALUE, "msm: too many bucket counters");
+    uint32_t* S;
+    TC_TRY(scratch_t(ctx, "msm.bcount", ncnt, &cnt));
     TC_TRY(scratch_t(ctx, "msm.bstart", (uint64_t)nb + 1, &bstart));
-    TC_TRY(scratch_t(ctx, "msm.cursor", (uint64_t)nb + 1, &cursor));
-    TC_CUDA(ctx, cudaMemsetAsync(cnt, 0, ((uint64_t)nb + 1) * sizeof(uint32_t), st));
+    TC_TRY(scratch_t(ctx, "msm.cursor", ncnt, &cursor));
+    if (NC > 1) {
+      TC_TRY(scratch_t(ctx, "msm.bscan", ncnt, &S));
+    } else {
+      S = bstart;
+    }
+    TC_CUDA(ctx, cudaMemsetAsync(cnt, 0, ncnt * sizeof(uint32_t), st));
     // fast path (k_digits_v) for fp16 / bf16 / fp32 with magnitudes below 2^62 and at most
     // HOT_MAXW few-bucket windows; the generic kernel otherwise
     HotPlan H{};
@@ -1086,7 +1107,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
       constexpr int D = decltype(dt)::value;
       if constexpr (D >= 1 && D <= 3) {
         if (fast) {
-          k_digits_v<D, false><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, H, cnt, nullptr);
+          k_digits_v<D, false><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, H, cnt, nullptr, NC);
           return;
         }
       }
@@ -1095,18 +1116,22 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     if (s) return s;
     TC_LAUNCHED(ctx);
     size_t sb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, sb, cnt, bstart, (int)(nb + 1), st);
+    cub::DeviceScan::ExclusiveSum(nullptr, sb, cnt, S, (int)ncnt, st);
     void* d_sb;
     TC_TRY(scratch(ctx, "msm.scantmp0", sb, &d_sb));
-    TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(d_sb, sb, cnt, bstart, (int)(nb + 1), st));
+    TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(d_sb, sb, cnt, S, (int)ncnt, st));
     ctx->launches += 2;
-    TC_CUDA(ctx, cudaMemcpyAsync(cursor, bstart, ((uint64_t)nb + 1) * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
-    TC_CUDA(ctx, cudaMemcpyAsync(h_small, bstart + nb, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    if (NC > 1) {
+      k_copy_starts<<<blocks_for((uint64_t)nb + 1, 256), 256, 0, st>>>(S, nb, NC, bstart);
+      TC_LAUNCHED(ctx);
+    }
+    TC_CUDA(ctx, cudaMemcpyAsync(cursor, S, ncnt * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+    TC_CUDA(ctx, cudaMemcpyAsync(h_small, S + (ncnt - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     s = dispatch_dt(ctx, dtype, [&](auto dt) {
       constexpr int D = decltype(dt)::value;
       if constexpr (D >= 1 && D <= 3) {
         if (fast) {
-          k_digits_v<D, true><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, H, cursor, vals);
+          k_digits_v<D, true><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, H, cursor, vals, NC);
           return;
         }
       }
