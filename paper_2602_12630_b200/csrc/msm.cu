@@ -497,6 +497,15 @@ __global__ void __launch_bounds__(256) k_scan_bits_v(const void* const* ptrs, ui
     if (hist[i]) atomicAdd(out + 1 + i, hist[i]);
 }
 
+// largest bucket (sets the number of reduction levels)
+__global__ void k_max_bucket(const uint32_t* bstart, uint32_t nb, uint32_t* out) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t v = k < nb ? bstart[k + 1] - bstart[k] : 0u;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0 && v) atomicMax(out, v);
+}
+
 // bucket starts from the per-copy exclusive scan: bstart[k] = S[k * nc], k = 0..nb
 __global__ void k_copy_starts(const uint32_t* S, uint32_t nb, uint32_t nc, uint32_t* bstart) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1053,6 +1062,8 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   const uint32_t* svals;
   uint32_t *bstart, *bend;
   uint64_t E;
+  bool have_maxb = false;   // exact largest bucket known (counting layout)
+  uint32_t maxb = 0;
   // Optional bucket-major layout by histogram + scatter instead of the radix sort
   // (TC_MSM_BUCKETED=1).  Measured slower on config 3 (pass A 3.8 ms + scatter 2.8 ms vs
   // digits 0.8 + onesweep 2.3 + bounds 0.4 ms): the per-layer slot counters and the
@@ -1127,6 +1138,10 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     }
     TC_CUDA(ctx, cudaMemcpyAsync(cursor, S, ncnt * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
     TC_CUDA(ctx, cudaMemcpyAsync(h_small, S + (ncnt - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    k_max_bucket<<<blocks_for(nb, 256), 256, 0, st>>>(bstart, nb, d_small + NHIST + 3);   // zeroed with d_small
+    TC_LAUNCHED(ctx);
+    TC_CUDA(ctx, cudaMemcpyAsync(h_small + 1, d_small + NHIST + 3, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    have_maxb = true;
     s = dispatch_dt(ctx, dtype, [&](auto dt) {
       constexpr int D = decltype(dt)::value;
       if constexpr (D >= 1 && D <= 3) {
@@ -1141,6 +1156,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     TC_LAUNCHED(ctx);
     TC_CUDA(ctx, cudaStreamSynchronize(st));
     E = h_small[0];
+    maxb = h_small[1];
     if (E == 0) {
       k_fill_inf<<<blocks_for(L, 64), 64, 0, st>>>(d_out, (uint32_t)L);
       TC_LAUNCHED(ctx);
@@ -1227,8 +1243,8 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   static const uint32_t T1_ENV = getenv("TC_MSM_T1") ? (uint32_t)atoi(getenv("TC_MSM_T1")) : 8u;
   const uint32_t T = (E >= (1u << 20)) ? T_ENV : (E >= (1u << 14) ? 16u : 8u);
   const uint32_t T1 = T1_ENV;
-  int levels = 1;
-  for (uint64_t capT = T; capT < n; capT *= T1) levels++;
+  int levels = 1;   // enough for the largest bucket (<= n entries when its size is unknown)
+  for (uint64_t capT = T; capT < (have_maxb ? (uint64_t)maxb : n); capT *= T1) levels++;
   // items = pieces of multi-piece buckets: ceil(sz/T) <= 2 sz / T for sz > T
   const uint64_t max_items = 2 * ((E + T - 1) / T) + 2;
   uint32_t *np, *npm, *toff, *offA, *offB;
