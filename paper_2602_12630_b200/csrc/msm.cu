@@ -512,6 +512,43 @@ __global__ void k_copy_starts(const uint32_t* S, uint32_t nb, uint32_t nc, uint3
   if (k <= nb) bstart[k] = S[(uint64_t)k * nc];
 }
 
+// mode-1 (float-exponent) digit pass: one entry per element; the 8 slot claims of a
+// thread are issued back to back before any of its stores (the atomics' latency overlaps)
+template <int DT, bool SCATTER>
+__global__ void __launch_bounds__(256) k_digits_fp(const void* const* ptrs, uint64_t n, int scale_bits, WinPlan P,
+                                                   uint32_t* __restrict__ cnt, uint32_t* __restrict__ vals,
+                                                   uint32_t nc) {
+  const uint32_t l = blockIdx.y;
+  const uint32_t key0 = l * P.nbm, copy = blockIdx.x % nc;
+  const uint64_t i0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * V_EPT;
+  uint32_t raw[V_EPT], ctr[V_EPT], val[V_EPT];
+  load_raw8<DT>(ptrs[l], i0, n, raw);
+  uint32_t live = 0;
+#pragma unroll
+  for (int k = 0; k < V_EPT; k++) {
+    bool neg;
+    const uint64_t mag = (i0 + k < n) ? quant64<DT>(raw[k], scale_bits, neg) : 0ull;
+    const int bl = mag ? 64 - __clzll((long long)mag) : 0;
+    const int g = bl > P.mbits ? bl - P.mbits : 0;
+    ctr[k] = (key0 + P.base[g] + (uint32_t)(mag >> g) - P.mlo[g]) * nc + copy;
+    val[k] = (uint32_t)(i0 + k) | (neg ? SIGN_BIT : 0u);
+    live |= (mag ? 1u : 0u) << k;
+  }
+  if (SCATTER) {
+    uint32_t slot[V_EPT];
+#pragma unroll
+    for (int k = 0; k < V_EPT; k++)
+      if (live >> k & 1u) slot[k] = atomicAdd(cnt + ctr[k], 1u);
+#pragma unroll
+    for (int k = 0; k < V_EPT; k++)
+      if (live >> k & 1u) vals[slot[k]] = val[k];
+  } else {
+#pragma unroll
+    for (int k = 0; k < V_EPT; k++)
+      if (live >> k & 1u) atomicAdd(cnt + ctr[k], 1u);
+  }
+}
+
 // ---- bucket-major layout without a radix sort (few buckets per MSM) -------------------
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
@@ -678,7 +715,10 @@ __device__ __forceinline__ uint32_t find_bucket(const uint32_t* off, uint32_t nb
 // that fits in one piece is final (written to buckets[k]); otherwise its piece sums go to
 // items.  The accumulator starts as the piece's first point, then one complete 8M mixed
 // add per entry (no exceptional cases, ec.cuh).
-__global__ void __launch_bounds__(128) k_accum_aff(const uint32_t* vals, const EdAff* bases, const uint32_t* bstart,
+#ifndef TC_ACCUM_MINB
+#define TC_ACCUM_MINB 6   // min resident blocks per SM for k_accum_aff: caps registers at 80 (A/B: 1 -> 4.72 ms @104 regs, 6 -> 4.40 ms, 7 -> 4.52, 8 -> 4.51)
+#endif
+__global__ void __launch_bounds__(128, TC_ACCUM_MINB) k_accum_aff(const uint32_t* vals, const EdAff* bases, const uint32_t* bstart,
                                                    const uint32_t* bend, const uint32_t* toff, const uint32_t* ooff,
                                                    uint32_t nb, uint32_t T, Ext* items, Ext* buckets,
                                                    const uint32_t* boff, uint32_t nbm) {
@@ -1118,7 +1158,10 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
       constexpr int D = decltype(dt)::value;
       if constexpr (D >= 1 && D <= 3) {
         if (fast) {
-          k_digits_v<D, false><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, H, cnt, nullptr, NC);
+          if (P.mode == 1)
+            k_digits_fp<D, false><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cnt, nullptr, NC);
+          else
+            k_digits_v<D, false><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, H, cnt, nullptr, NC);
           return;
         }
       }
@@ -1146,7 +1189,10 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
       constexpr int D = decltype(dt)::value;
       if constexpr (D >= 1 && D <= 3) {
         if (fast) {
-          k_digits_v<D, true><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, H, cursor, vals, NC);
+          if (P.mode == 1)
+            k_digits_fp<D, true><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cursor, vals, NC);
+          else
+            k_digits_v<D, true><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, H, cursor, vals, NC);
           return;
         }
       }
