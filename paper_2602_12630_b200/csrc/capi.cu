@@ -4,6 +4,8 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstring>
+#include <map>
+#include <mutex>
 
 #include "sha256.cuh"
 #include "tc_internal.cuh"
@@ -865,18 +867,49 @@ int tc_commit_stream(tc_ctx* ctx, const tc_srs* srs, const void* const* h_cur, c
 }
 
 // L_k(omega_a) (canonical) and 1 / (k + 1 - omega_a) for every axis, concatenated
-static void lag_weights(const tc_srs* srs, const std::vector<Fe>& om, std::vector<Fe>& lam, std::vector<Fe>& inv) {
-  lam.clear();
-  inv.clear();
+// barycentric weights w_i = 1 / prod_{t != i} (x_i - x_t) of the default grid x = 1..d and
+// their inverses, both in Montgomery form, cached per extent
+static const std::pair<std::vector<Fe>, std::vector<Fe>>& bary_weights(uint32_t d) {
+  static std::mutex mu;
+  static std::map<uint32_t, std::pair<std::vector<Fe>, std::vector<Fe>>> cache;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(d);
+  if (it != cache.end()) return it->second;
+  std::vector<Fe> w(d), winv(d);
+  for (uint32_t i = 0; i < d; i++) {
+    Fe prod = Fp::one();
+    for (uint32_t t = 0; t < d; t++) {
+      if (t == i) continue;
+      const Fe diff = Fp::sub(Fp::to_mont_small(i + 1), Fp::to_mont_small(t + 1));
+      prod = Fp::mul(prod, diff);
+    }
+    winv[i] = Fp::canon(prod);
+    w[i] = Fp::canon(Fp::inv(prod));
+  }
+  return cache.emplace(d, std::make_pair(w, winv)).first->second;
+}
+
+// Lagrange-route opening weights for every axis (see tcrt::LagW)
+static void lag_weights(const tc_srs* srs, const std::vector<Fe>& om, tcrt::LagW& W) {
+  W.lam.clear();
+  W.inv.clear();
+  W.der.clear();
+  W.sj.assign(srs->m, -1);
   for (int a = 0; a < srs->m; a++) {
     const uint32_t d = srs->shape[a];
+    int j = -1;   // omega_a = x_j ?
+    for (uint32_t k = 0; k < d && j < 0; k++) {
+      Fe z{{k + 1, 0, 0, 0, 0, 0}};
+      if (memcmp(z.v, om[a].v, sizeof z.v) == 0) j = (int)k;
+    }
+    W.sj[a] = j;
     std::vector<Fe> la;
-    axis_tables(om[a], d, true, la);   // L_k(omega_a), canonical
+    axis_tables(om[a], d, true, la);   // L_k(omega_a), canonical (one-hot on a node)
     const Fe w = Fp::to_mont(om[a]);
     std::vector<Fe> diff(d), pref(d);
     Fe run = Fp::one();
     for (uint32_t k = 0; k < d; k++) {
-      diff[k] = Fp::sub(Fp::to_mont_small(k + 1), w);
+      diff[k] = (int)k == j ? Fp::one() : Fp::sub(Fp::to_mont_small(k + 1), w);   // x_k - omega
       pref[k] = run;
       run = Fp::mul(run, diff[k]);
     }
@@ -886,18 +919,25 @@ static void lag_weights(const tc_srs* srs, const std::vector<Fe>& om, std::vecto
       ik[k] = Fp::canon(Fp::mul(iv, pref[k]));
       iv = Fp::mul(iv, diff[k]);
     }
-    for (uint32_t k = 0; k < d; k++) lam.push_back(Fp::canon(Fp::to_mont(la[k])));
-    inv.insert(inv.end(), ik.begin(), ik.end());
-  }
-}
-
-static bool point_on_grid(const tc_srs* srs, const std::vector<Fe>& om) {
-  for (int a = 0; a < srs->m; a++)
-    for (uint32_t k = 1; k <= srs->shape[a]; k++) {
-      Fe z{{k, 0, 0, 0, 0, 0}};
-      if (memcmp(z.v, om[a].v, sizeof z.v) == 0) return true;
+    std::vector<Fe> dk(d, Fp::zero());
+    if (j >= 0) {
+      // L_i'(x_j) = (w_i / w_j) / (x_j - x_i) = -(w_i / w_j) inv[i]  (i != j),
+      // L_j'(x_j) = sum_{i != j} 1 / (x_j - x_i) = -sum_{i != j} inv[i]
+      ik[j] = Fp::zero();
+      const auto& bw = bary_weights(d);
+      const Fe wj_inv = bw.second[j];
+      Fe sum = Fp::zero();
+      for (uint32_t i = 0; i < d; i++) {
+        if ((int)i == j) continue;
+        dk[i] = Fp::canon(Fp::neg(Fp::mul(Fp::mul(bw.first[i], wj_inv), ik[i])));   // all Montgomery
+        sum = Fp::add(sum, ik[i]);
+      }
+      dk[j] = Fp::canon(Fp::neg(sum));
     }
-  return false;
+    for (uint32_t k = 0; k < d; k++) W.lam.push_back(Fp::canon(Fp::to_mont(la[k])));
+    W.inv.insert(W.inv.end(), ik.begin(), ik.end());
+    W.der.insert(W.der.end(), dk.begin(), dk.end());
+  }
 }
 
 int tc_open(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int scale_bits, const uint8_t* omega_le21,
@@ -911,19 +951,23 @@ int tc_open(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int sca
   Fe* vals;
   TC_TRY(load_field_tensor(ctx, d_in, dtype, n, scale_bits, &vals, "open.vals"));
   // Lagrange route: quotients evaluated on the grid straight from the samples (no
-  // interpolation), committed over the (sub-grid) Lagrange elements.  Needs omega off the
-  // grid on every axis (on a node the quotient value is a derivative) — else monomial.
-  const bool on_grid = point_on_grid(srs, om);
-  const bool lag_ok = srs->lagrange && (m == 1 || srs->sublag) && !on_grid;
-  if (route == TC_ROUTE_LAGRANGE && !lag_ok && !on_grid)
+  // interpolation), committed over the (sub-grid) Lagrange elements.  On an axis where
+  // omega is a grid node x_j (verifier challenges are grid points) the
+  // quotient's value at x_j is the derivative of the fibre interpolant, a contraction with
+  // the weights L_i'(x_j) (lag_weights).
+  const bool lag_ok = srs->lagrange && (m == 1 || srs->sublag);
+  // tiny SRSs (Terkle nodes): the monomial route's quotients go to the fixed-base table
+  // kernel in one call; the Lagrange route would run m Pippenger pipelines
+  if (route == TC_ROUTE_AUTO && n <= SMALL_MSM_MAX && srs->monomial) route = TC_ROUTE_MONOMIAL;
+  if (route == TC_ROUTE_LAGRANGE && !lag_ok)
     return fail(ctx, TC_ERR_VALUE, "srs has no Lagrange elements");
   if (lag_ok && route != TC_ROUTE_MONOMIAL) {
-    std::vector<Fe> lam, inv;
-    lag_weights(srs, om, lam, inv);
+    tcrt::LagW W;
+    lag_weights(srs, om, W);
     Fe* qs;
     TC_TRY(tcrt::scratch_t(ctx, "open.q", (uint64_t)m * n, &qs));
     Fe y;
-    TC_TRY(tcrt::open_quotients_lagrange_device(ctx, vals, srs->shape, m, lam, inv, qs, &y));
+    TC_TRY(tcrt::open_quotients_lagrange_device(ctx, vals, srs->shape, m, W, qs, &y));
     fe_to_le21(y, out_y21);
     Aff* d_out;
     TC_TRY(tcrt::scratch_t(ctx, "open.out", (uint64_t)m, &d_out));
@@ -966,7 +1010,7 @@ int tc_open(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int sca
 //    pi_0 = sum_{c, c'} (delta_{c c'} - L_c'(omega_0)) / (c + 1 - omega_0) * H[c', c]
 //    (the axis-0 quotient q_0(a) = (T[a] - sum_c' L_c'(omega_0) T[c', a_rest]) / (a_0 + 1
 //    - omega_0), regrouped) — a d_0^2-point MSM per opening instead of an N-point one.
-// Openings whose point lies on the grid (or route = monomial) go through tc_open.
+// route = monomial goes through tc_open (interpolation + monomial SRS) per opening.
 int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype, int scale_bits,
                   const uint8_t* omegas_le21, int route, uint8_t* out_y21, uint8_t* out_pi43) {
   if (!ctx || !srs || (count && (!d_ins || !omegas_le21 || !out_y21 || !out_pi43)) || count < 0)
@@ -980,7 +1024,7 @@ int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int 
     for (int j = 0; j < m; j++)
       if (!le21_to_fe(omegas_le21 + 21 * ((size_t)i * m + j), om[j]))
         return fail(ctx, TC_ERR_VALUE, "opening %d: point coordinate %d out of range", i, j);
-    const bool lag_ok = srs->lagrange && (m == 1 || srs->sublag) && !point_on_grid(srs, om);
+    const bool lag_ok = srs->lagrange && (m == 1 || srs->sublag);
     if (lag_ok && route != TC_ROUTE_MONOMIAL)
       lag.push_back(i);
     else
@@ -1024,7 +1068,9 @@ int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int 
   TC_TRY(tcrt::scratch_t(ctx, "openb.q", (uint64_t)G * m * n, &qall));
   TC_TRY(tcrt::scratch_t(ctx, "openb.out", (uint64_t)G * m, &d_out));
   std::vector<uint8_t> enc((size_t)G * m * 43);
-  std::vector<Fe> om(m), lam, inv, stabs;
+  std::vector<Fe> om(m), stabs;
+  std::vector<int> ssj;
+  tcrt::LagW W;
   for (size_t jb = 0; jb < jobs.size(); jb++) {
     const std::vector<int>& ops = jobs[jb];
     const bool sliced = job_h[jb] != nullptr;
@@ -1047,18 +1093,21 @@ int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int 
     for (size_t g0 = 0; g0 < ops.size(); g0 += G) {
       const int gc = (int)std::min<size_t>(G, ops.size() - g0);
       stabs.clear();
+      ssj.clear();
       for (int k = 0; k < gc; k++) {
         const int i = ops[g0 + k];
         for (int j = 0; j < m; j++) le21_to_fe(omegas_le21 + 21 * ((size_t)i * m + j), om[j]);
-        lag_weights(srs, om, lam, inv);
+        lag_weights(srs, om, W);
         if (sliced) {
-          stabs.insert(stabs.end(), lam.begin(), lam.begin() + d0);
-          stabs.insert(stabs.end(), inv.begin(), inv.begin() + d0);
+          stabs.insert(stabs.end(), W.lam.begin(), W.lam.begin() + d0);
+          stabs.insert(stabs.end(), W.inv.begin(), W.inv.begin() + d0);
+          stabs.insert(stabs.end(), W.der.begin(), W.der.begin() + d0);
+          ssj.push_back(W.sj[0]);
         }
         Fe* vals;
         TC_TRY(load_field_tensor(ctx, d_ins[i], dtype, n, scale_bits, &vals, "open.vals"));
         Fe y;
-        TC_TRY(tcrt::open_quotients_lagrange_device(ctx, vals, srs->shape, m, lam, inv, qall + (uint64_t)k * m * n, &y,
+        TC_TRY(tcrt::open_quotients_lagrange_device(ctx, vals, srs->shape, m, W, qall + (uint64_t)k * m * n, &y,
                                                     sliced));
         fe_to_le21(y, out_y21 + 21 * (size_t)i);
       }
@@ -1067,7 +1116,7 @@ int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int 
       for (int a = 0; a < m; a++) {
         if (a == 0 && sliced) {
           const uint32_t nh = d0 * d0;
-          TC_TRY(tcrt::slice_scalars_device(ctx, stabs, d0, (uint32_t)gc, sc));
+          TC_TRY(tcrt::slice_scalars_device(ctx, stabs, ssj, d0, (uint32_t)gc, sc));
           for (int k = 0; k < gc; k++) ptrs[k] = sc + (uint64_t)k * nh;
           TC_TRY(tcrt::msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, ptrs.data(), gc, hed, nh, d_out));
         } else {

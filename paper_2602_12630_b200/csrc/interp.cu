@@ -102,8 +102,8 @@ __global__ void k_divide_axis(Fe* r, Fe* q, uint32_t d, uint64_t s, Fe v_mont) {
 
 // Lagrange-route opening along the leading axis (extent d, `rest` trailing elements):
 // rn[r] = sum_k r[k, r] lam[k];  q[k, r] = (r[k, r] - rn[r]) * inv[k]
-__global__ void k_open_axis_lag(const Fe* r, uint32_t d, uint64_t rest, const Fe* lam, const Fe* inv, Fe* rn,
-                                Fe* q) {
+__global__ void k_open_axis_lag(const Fe* r, uint32_t d, uint64_t rest, const Fe* lam, const Fe* inv, const Fe* der,
+                                int sj, Fe* rn, Fe* q) {
   uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= rest) return;
   uint32_t acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -113,7 +113,13 @@ __global__ void k_open_axis_lag(const Fe* r, uint32_t d, uint64_t rest, const Fe
   if (!q) return;   // caller commits this axis another way (slice-commitment openings)
   for (uint32_t k = 0; k < d; k++) {
     const uint64_t pos = (uint64_t)k * rest + i;
-    q[pos] = Fp::canon(Fp::mul(Fp::sub(r[pos], next), inv[k]));
+    if ((int)k == sj) {   // omega on the node x_k: derivative of the fibre interpolant
+      uint32_t dacc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+      for (uint32_t t = 0; t < d; t++) mac_wide(dacc, r[(uint64_t)t * rest + i], der[t]);
+      q[pos] = Fp::canon(Fp::redc(dacc));
+    } else {
+      q[pos] = Fp::canon(Fp::mul(Fp::sub(r[pos], next), inv[k]));
+    }
   }
 }
 
@@ -121,14 +127,18 @@ __global__ void k_open_axis_lag(const Fe* r, uint32_t d, uint64_t rest, const Fe
 // lam = L_c'(omega_0) and inv = 1/(c + 1 - omega_0) (Montgomery form, as k_open_axis_lag
 // takes them; tabs[o] = lam[d] ++ inv[d]), s[o][c' d + c] = (delta_{c c'} - lam[c']) inv[c]
 // (canonical out), so pi_0 = sum s * H[c', c].
-__global__ void k_slice_scalars(const Fe* tabs, uint32_t d, uint32_t count, Fe* out) {
+__global__ void k_slice_scalars(const Fe* tabs, const int* sj, uint32_t d, uint32_t count, Fe* out) {
   const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   const uint64_t dd = (uint64_t)d * d;
   if (t >= dd * count) return;
   const uint64_t o = t / dd;
   const uint32_t cp = (uint32_t)((t % dd) / d), c = (uint32_t)(t % d);
-  const Fe* lam = tabs + o * 2 * d;
+  const Fe* lam = tabs + o * 3 * d;
   const Fe* inv = lam + d;
+  if ((int)c == sj[o]) {   // omega_0 on the node x_c: q_0 there is sum_c' der[c'] T[c', .]
+    out[t] = Fp::from_mont(lam[2 * d + cp]);
+    return;
+  }
   const Fe x = Fp::sub(c == cp ? Fp::one() : Fp::zero(), lam[cp]);   // Montgomery
   out[t] = Fp::from_mont(Fp::mul(x, inv[c]));                        // canonical
 }
@@ -237,23 +247,23 @@ int open_quotients_device(tc_ctx* ctx, const Fe* d_coeffs, const uint32_t* shape
   return TC_OK;
 }
 
-int open_quotients_lagrange_device(tc_ctx* ctx, Fe* d_vals, const uint32_t* shape, int m,
-                                   const std::vector<Fe>& lam, const std::vector<Fe>& inv, Fe* d_quotients,
-                                   Fe* h_y, bool skip_q0) {
+int open_quotients_lagrange_device(tc_ctx* ctx, Fe* d_vals, const uint32_t* shape, int m, const LagW& W,
+                                   Fe* d_quotients, Fe* h_y, bool skip_q0) {
   cudaStream_t st = ctx->stream;
   uint64_t n = 1;
   uint32_t dsum = 0;
   for (int j = 0; j < m; j++) n *= shape[j], dsum += shape[j];
   Fe *tabs, *bufA, *bufB;
-  TC_TRY(scratch_t(ctx, "openlag.tabs", 2 * (uint64_t)dsum, &tabs));
+  TC_TRY(scratch_t(ctx, "openlag.tabs", 3 * (uint64_t)dsum, &tabs));
   TC_TRY(scratch_t(ctx, "openlag.rA", n / shape[0] + 1, &bufA));
   TC_TRY(scratch_t(ctx, "openlag.rB", (m > 1 ? n / shape[0] / shape[1] : 1) + 1, &bufB));
   // weights + inverses -> device through the pinned staging area, one copy
   Fe* stage = (Fe*)((char*)ctx->h_stage + 512 * 1024);
-  if ((size_t)2 * dsum * sizeof(Fe) > 256 * 1024) return fail(ctx, TC_ERR_VALUE, "open: axes too long");
-  memcpy(stage, lam.data(), dsum * sizeof(Fe));
-  memcpy(stage + dsum, inv.data(), dsum * sizeof(Fe));
-  TC_CUDA(ctx, cudaMemcpyAsync(tabs, stage, 2 * dsum * sizeof(Fe), cudaMemcpyHostToDevice, st));
+  if ((size_t)3 * dsum * sizeof(Fe) > 256 * 1024) return fail(ctx, TC_ERR_VALUE, "open: axes too long");
+  memcpy(stage, W.lam.data(), dsum * sizeof(Fe));
+  memcpy(stage + dsum, W.inv.data(), dsum * sizeof(Fe));
+  memcpy(stage + 2 * dsum, W.der.data(), dsum * sizeof(Fe));
+  TC_CUDA(ctx, cudaMemcpyAsync(tabs, stage, 3 * dsum * sizeof(Fe), cudaMemcpyHostToDevice, st));
   Fe* r = d_vals;
   uint64_t span = n;
   uint32_t off = 0;
@@ -263,7 +273,8 @@ int open_quotients_lagrange_device(tc_ctx* ctx, Fe* d_vals, const uint32_t* shap
     // r_{a+1} alternates between two buffers (A holds r_1, B is large enough for r_2..);
     // kernels are stream-ordered, so r_a is never overwritten while it is read
     Fe* rn = (a & 1) ? bufB : bufA;
-    k_open_axis_lag<<<blocks_for(rest, 128), 128, 0, st>>>(r, d, rest, tabs + off, tabs + dsum + off, rn,
+    k_open_axis_lag<<<blocks_for(rest, 128), 128, 0, st>>>(r, d, rest, tabs + off, tabs + dsum + off,
+                                                           tabs + 2 * dsum + off, W.sj[a], rn,
                                                            (a == 0 && skip_q0) ? nullptr : d_quotients + (uint64_t)a * n);
     TC_LAUNCHED(ctx);
     r = rn;
@@ -275,15 +286,19 @@ int open_quotients_lagrange_device(tc_ctx* ctx, Fe* d_vals, const uint32_t* shap
   return TC_OK;
 }
 
-int slice_scalars_device(tc_ctx* ctx, const std::vector<Fe>& tabs_host, uint32_t d, uint32_t count, Fe* d_out) {
+int slice_scalars_device(tc_ctx* ctx, const std::vector<Fe>& tabs_host, const std::vector<int>& sj, uint32_t d,
+                         uint32_t count, Fe* d_out) {
   cudaStream_t st = ctx->stream;
   Fe* tabs;
+  int* d_sj;
   TC_TRY(scratch_t(ctx, "openh.tabs", tabs_host.size(), &tabs));
-  // pageable source: the synchronous copy completes before tabs_host can change
+  TC_TRY(scratch_t(ctx, "openh.sj", sj.size(), &d_sj));
+  // pageable sources: synchronise before the host vectors can change
   TC_CUDA(ctx, cudaMemcpyAsync(tabs, tabs_host.data(), tabs_host.size() * sizeof(Fe), cudaMemcpyHostToDevice, st));
+  TC_CUDA(ctx, cudaMemcpyAsync(d_sj, sj.data(), sj.size() * sizeof(int), cudaMemcpyHostToDevice, st));
   TC_CUDA(ctx, cudaStreamSynchronize(st));
   const uint64_t tot = (uint64_t)d * d * count;
-  k_slice_scalars<<<blocks_for(tot, 128), 128, 0, st>>>(tabs, d, count, d_out);
+  k_slice_scalars<<<blocks_for(tot, 128), 128, 0, st>>>(tabs, d_sj, d, count, d_out);
   TC_LAUNCHED(ctx);
   return TC_OK;
 }

@@ -164,13 +164,21 @@ int evaluate_device(tc_ctx* ctx, const tc::Fe* d_coeffs, const uint32_t* shape, 
 // per axis a: r_{a+1} = contraction of r_a with lam[a] (Montgomery L_k(omega_a)), and
 // q_a[k, rest] = (r_a[k, rest] - r_{a+1}[rest]) * inv[a][k] (Montgomery 1/(z_k - omega_a)).
 // q_a is written at d_quotients + a*N (only its first prod_{j>=a} d_j entries); y on host.
-int open_quotients_lagrange_device(tc_ctx* ctx, tc::Fe* d_vals, const uint32_t* shape, int m,
-                                   const std::vector<tc::Fe>& lam, const std::vector<tc::Fe>& inv,
+// Per-axis weights of a Lagrange-route opening at omega (Montgomery form, axes concatenated):
+// lam[k] = L_k(omega_a); inv[k] = 1 / (x_k - omega_a) for x_k != omega_a.  When omega_a is the
+// grid node x_j (sj[a] = j, else -1) the quotient's value on that node is the derivative of the
+// fibre interpolant, sum_i r[i] L_i'(x_j): der[i] = L_i'(x_j) (zero when sj[a] < 0).
+struct LagW {
+  std::vector<tc::Fe> lam, inv, der;
+  std::vector<int> sj;
+};
+int open_quotients_lagrange_device(tc_ctx* ctx, tc::Fe* d_vals, const uint32_t* shape, int m, const LagW& W,
                                    tc::Fe* d_quotients, tc::Fe* h_y, bool skip_q0 = false);
-// s[o][c' d + c] = (delta_{c c'} - lam_o[c']) inv_o[c] for `count` openings (tabs: per
-// opening lam[d] ++ inv[d], Montgomery form) — the scalars of pi_0 over slice commitments
-int slice_scalars_device(tc_ctx* ctx, const std::vector<tc::Fe>& tabs_host, uint32_t d, uint32_t count,
-                         tc::Fe* d_out);
+// s[o][c' d + c] = (delta_{c c'} - lam_o[c']) inv_o[c], or der_o[c'] in the column c = sj_o,
+// for `count` openings (tabs: per opening lam[d] ++ inv[d] ++ der[d], Montgomery form; sj per
+// opening, -1 off the grid) — the scalars of pi_0 over slice commitments
+int slice_scalars_device(tc_ctx* ctx, const std::vector<tc::Fe>& tabs_host, const std::vector<int>& sj, uint32_t d,
+                         uint32_t count, tc::Fe* d_out);
 
 // open_quotients on device: coefficient array (canonical) -> m quotient arrays + y
 int open_quotients_device(tc_ctx* ctx, const tc::Fe* d_coeffs, const uint32_t* shape, int m,

@@ -369,6 +369,38 @@ def test_msm_float_exponent_plan_small(fp_min_n, tmp_path):
     assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr
 
 
+def test_openings_at_grid_points_lagrange_route():
+    """Challenges on grid nodes, fully or on some axes only, take the
+    Lagrange route (derivative weights on the node's row): equal to the trapdoor oracle and
+    to the monomial route, through tc_open and through tc_open_many (both its grouped and
+    its slice-commitment paths), and they verify."""
+    tcb = T()
+    shape = (4, 8, 16)
+    srs, td = tcb.setup_srs(shape, b"grid-open")
+    x = torch.from_numpy((np.random.default_rng(43).standard_t(3, 512) * 2).astype(np.float16)).cuda()
+    vals = O.quantize(x.cpu().numpy().astype(np.float64), 16)
+    rng = random.Random(9)
+    pts = [[1, 1, 1], [4, 8, 16], [2, 5, 7], [3, rng.randrange(O.P), 11], [rng.randrange(O.P), 8, rng.randrange(O.P)],
+           [rng.randrange(O.P), rng.randrange(O.P), 1], [1, rng.randrange(O.P), rng.randrange(O.P)]]
+    C = tcb.tc_commit(srs, x)
+    want = [O.open_trapdoor(vals, shape, list(td.taus), pt) for pt in pts]
+    for pt, (y, proofs) in zip(pts, want):
+        op = tcb.tc_open(srs, x, pt)
+        assert op.y == y and list(op.proofs) == proofs
+        assert tcb.tc_open(srs, x, pt, route="monomial") == op
+        assert tcb.tc_verify(srs, C, pt, op)
+    # tc_open_many: 7 openings of one tensor (>= TC_OPEN_PRECOMP_MIN: slice commitments,
+    # grid node on axis 0 included) plus a second tensor's grouped openings
+    x2 = torch.from_numpy((np.random.default_rng(44).standard_t(3, 512)).astype(np.float16)).cuda()
+    got = tcb.tc_open_many(srs, [x] * len(pts) + [x2, x2], pts + pts[:2])
+    for op, (y, proofs) in zip(got, want):
+        assert op.y == y and list(op.proofs) == proofs
+    v2 = O.quantize(x2.cpu().numpy().astype(np.float64), 16)
+    for op, pt in zip(got[len(pts):], pts[:2]):
+        y, proofs = O.open_trapdoor(v2, shape, list(td.taus), pt)
+        assert op.y == y and list(op.proofs) == proofs
+
+
 # ---------------------------------------------------------------- full-size configs
 def _config3_layer(l):
     scales = np.random.default_rng(12345).uniform(0.5, 4.0, 32)
