@@ -856,6 +856,62 @@ __global__ void __launch_bounds__(128) k_wsum_level(const Ext* Tin, const Ext* D
   Dout[o] = u;
 }
 
+// One block per (MSM, window) for windows of <= WB_THREADS * WB_CHUNK buckets (the
+// float-exponent groups): W = sum_j (mlo + j) B_j in ONE launch instead of recursive
+// levels.  Thread t takes the chunk [t C, t C + C) (C = WB_CHUNK, a power of two) and forms
+// T_t = sum of the chunk and U_t = sum (j - tC + 1) B_j by running sums; then
+//     A = sum_j (j+1) B_j = sum_t U_t + C * sum_t t T_t,   sum_t t T_t = sum_{t>=1} R_t,
+// R_t = sum_{s>=t} T_s (a shared-memory suffix scan), S = R_0, and W = A + (mlo - 1) S.
+// Serial depth ~ 2C + 2 log2(threads) + log2(C) + log2(mlo) adds instead of ~27 per level.
+constexpr int WB_THREADS = 128;
+constexpr int WB_CHUNK_LG = 4;   // C = 16: 128 x 16 = 2048 buckets
+
+__global__ void __launch_bounds__(WB_THREADS) k_wsum_block(const Ext* buckets, WinPlan P, Ext* W) {
+  __shared__ Ext sh[WB_THREADS];
+  __shared__ Ext su[WB_THREADS];
+  const uint32_t g = blockIdx.x, l = g / P.nwin, w = g % P.nwin, t = threadIdx.x;
+  const uint32_t nbw = P.base[w + 1] - P.base[w];
+  const Ext* b = buckets + (uint64_t)l * P.nbm + P.base[w];
+  const uint32_t C = 1u << WB_CHUNK_LG, a = t * C, e = min(a + C, nbw);
+  Ext run = ext_zero(), u = ext_zero();
+  for (int j = (int)e - 1; j >= (int)a; j--) {
+    ext_add(run, ld_ext(b + j));
+    ext_add(u, run);
+  }
+  sh[t] = run;
+  su[t] = u;
+  __syncthreads();
+  // inclusive suffix scan R_t = sum_{s >= t} T_s (Hillis-Steele)
+  for (uint32_t o = 1; o < WB_THREADS; o <<= 1) {
+    Ext v = sh[t];
+    if (t + o < WB_THREADS) ext_add(v, sh[t + o]);
+    __syncthreads();
+    sh[t] = v;
+    __syncthreads();
+  }
+  const Ext S = sh[0];
+  // reduce sum_{t>=1} R_t (into sh) and sum_t U_t (into su)
+  if (t == 0) sh[0] = ext_zero();
+  __syncthreads();
+  for (uint32_t o = WB_THREADS / 2; o; o >>= 1) {
+    if (t < o) {
+      Ext x = sh[t], y = su[t];
+      ext_add(x, sh[t + o]);
+      ext_add(y, su[t + o]);
+      sh[t] = x;
+      su[t] = y;
+    }
+    __syncthreads();
+  }
+  if (t != 0) return;
+  Ext A = sh[0];
+  for (int i = 0; i < WB_CHUNK_LG; i++) A = ext_dbl(A);
+  ext_add(A, su[0]);
+  const uint32_t c = P.mlo[w] - 1u;
+  if (c) ext_add(A, ext_mul_small(S, c));
+  W[g] = A;
+}
+
 // W_g = D_g - c * S_g + (mlo_w - 1) * S_g: sum_j (j+1) x_j re-based to the window's weights
 __global__ void k_wsum_final(const Ext* T, const Ext* D, uint32_t ngroups, uint32_t c, WinPlan P, Ext* W) {
   const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1351,6 +1407,21 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   static const bool old_reduce = getenv("TC_MSM_RUNSUM") != nullptr;
   static const uint32_t SEG_LG = getenv("TC_MSM_SEG_LG") ? (uint32_t)atoi(getenv("TC_MSM_SEG_LG")) : 3u;
   const uint32_t SEG = 1u << SEG_LG;
+  uint32_t maxw = 0;
+  for (int w = 0; w < P.nwin; w++) maxw = std::max(maxw, P.base[w + 1] - P.base[w]);
+  static const bool no_block = getenv("TC_MSM_NO_WSUM_BLOCK") != nullptr;
+  // latency-bound small batches (multi-GPU ranks, openings): one block per window; large
+  // batches keep the level recursion, which has more parallelism (measured: 4 layers
+  // 1.58 -> 1.51 ms per step, 32 layers 7.01 -> 7.11 ms with the block kernel)
+  if (!old_reduce && !no_block && maxw <= (uint32_t)WB_THREADS << WB_CHUNK_LG && nw_total <= 256) {
+    Ext* wsum;
+    TC_TRY(scratch_t(ctx, "msm.wsum", nw_total, &wsum));
+    k_wsum_block<<<nw_total, WB_THREADS, 0, st>>>(buckets, P, wsum);
+    TC_LAUNCHED(ctx);
+    k_final<<<blocks_for(L, 32), 32, 0, st>>>(wsum, (uint32_t)L, P, d_out);
+    TC_LAUNCHED(ctx);
+    return TC_OK;
+  }
   if (!old_reduce) {
     // recursive segmentation (k_wsum_level): host builds all level tables, one upload
     std::vector<uint32_t> cnt(nw_total), off(nw_total);

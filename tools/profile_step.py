@@ -35,3 +35,16 @@ root = step()
 torch.cuda.synchronize()
 torch.cuda.nvtx.range_pop()
 print("root", root.to_bytes().hex()[:32])
+
+if os.environ.get("TC_PROFILE_TIME"):
+    import time
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    print("step ms", e0.elapsed_time(e1) / 10, "layers", n_layers)
