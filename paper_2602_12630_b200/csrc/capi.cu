@@ -262,7 +262,7 @@ void axis_tables(const Fe& tau_c, uint32_t d, bool lagrange, std::vector<Fe>& ou
     pref[a] = run;
     run = Fp::mul(run, den[a]);
   }
-  Fe inv = Fp::inv(run);
+  Fe inv = Fp::inv_fast(run);
   std::vector<Fe> res(d);
   for (int a = (int)d - 1; a >= 0; a--) {
     Fe ia = Fp::mul(inv, pref[a]);
@@ -380,7 +380,7 @@ bool host_pairing(const Aff& S, const Aff& T, F2& out) {
   }
   // final exponentiation: (conj(f) / f)^120
   Fe norm = Fq::add(Fq::sqr(f.a), Fq::sqr(f.b));
-  Fe ni = Fq::inv(norm);
+  Fe ni = Fq::inv_fast(norm);
   Fe inva = Fq::mul(f.a, ni), invb = Fq::neg(Fq::mul(f.b, ni));
   F2 g{Fq::add(Fq::mul(f.a, inva), Fq::mul(f.b, invb)), Fq::sub(Fq::mul(f.a, invb), Fq::mul(f.b, inva))};
   F2 o{Fq::one(), Fq::zero()};
@@ -884,7 +884,7 @@ static const std::pair<std::vector<Fe>, std::vector<Fe>>& bary_weights(uint32_t 
       prod = Fp::mul(prod, diff);
     }
     winv[i] = Fp::canon(prod);
-    w[i] = Fp::canon(Fp::inv(prod));
+    w[i] = Fp::canon(Fp::inv_fast(prod));
   }
   return cache.emplace(d, std::make_pair(w, winv)).first->second;
 }
@@ -913,7 +913,7 @@ static void lag_weights(const tc_srs* srs, const std::vector<Fe>& om, tcrt::LagW
       pref[k] = run;
       run = Fp::mul(run, diff[k]);
     }
-    Fe iv = Fp::inv(run);
+    Fe iv = Fp::inv_fast(run);
     std::vector<Fe> ik(d);
     for (int k = (int)d - 1; k >= 0; k--) {
       ik[k] = Fp::canon(Fp::mul(iv, pref[k]));

@@ -165,7 +165,7 @@ TC_HD Xyzz xyzz_mul_small(const Xyzz& p, uint32_t k) {
 // XYZZ -> affine (Montgomery form).  One field inversion of ZZ*ZZZ.
 TC_HD Aff xyzz_to_aff(const Xyzz& p) {
   if (xyzz_is_inf(p)) return aff_inf();
-  Fe t = Fq::inv(Fq::mul(p.ZZ, p.ZZZ));
+  Fe t = Fq::inv_pref(Fq::mul(p.ZZ, p.ZZZ));
   Fe izz = Fq::mul(t, p.ZZZ);   // 1/ZZ
   Fe izzz = Fq::mul(t, p.ZZ);   // 1/ZZZ
   return Aff{Fq::mul(p.X, izz), Fq::mul(p.Y, izzz)};
@@ -326,7 +326,7 @@ TC_HD Aff ext_to_aff(const Ext& p) {
     return Aff{Fq::zero(), Fq::zero()};
   }
   const Fe zpy = Fq::add(p.Z, p.Y);
-  const Fe inv = Fq::inv(Fq::mul(Fq::sub(p.Z, p.Y), p.X));
+  const Fe inv = Fq::inv_pref(Fq::mul(Fq::sub(p.Z, p.Y), p.X));
   return Aff{Fq::mul(Fq::mul(zpy, p.X), inv), Fq::mul(Fq::mul(zpy, p.Z), inv)};
 }
 

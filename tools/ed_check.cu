@@ -58,6 +58,20 @@ int main() {
     // infinity in -> neutral
     bad += !aff_is_inf(ext_to_aff(ext_from_aff(aff_to_ed(aff_inf())))); n++;
   }
+  // binary-Euclid inversion == Fermat inversion (F_q and F_p, random + edge values)
+  std::mt19937_64 r64(9);
+  for (int it = 0; it < 300; it++) {
+    Fe a;
+    for (int i = 0; i < 5; i++) a.v[i] = (uint32_t)r64();
+    a.v[5] = (uint32_t)(r64() % 0x1E0);
+    if (it == 0) a = Fq::one();
+    if (it == 1) a = Fq::zero();
+    if (it == 2) a = Fe{{0x78000076u, 0, 0, 0, 0, 0xF0u}};   // q - 1 (canonical, as Montgomery value)
+    bad += !Fq::eq(Fq::inv_fast(a), Fq::inv(a)); n++;
+    Fe b = a;
+    b.v[5] &= 0x3u;
+    bad += !Fp::eq(Fp::inv_fast(b), Fp::inv(b)); n++;
+  }
   printf("{\"edwards_checks\": %d, \"bad\": %d}\n", n, bad);
   return bad != 0;
 }
