@@ -2,9 +2,10 @@
 // node openings): L independent MSMs over an SRS of only B <= 64 points with full 162-bit
 // scalars.  Pippenger is the wrong tool here (its window-combination Horner is ~160
 // sequential doublings); instead every SRS point gets a byte-window table
-//     tab[k][w][j] = (j+1) * 2^{8w} * G_k        (21 windows x 255 entries, affine)
+//     tab[k][w][j] = (j+1) * 2^{8w} * G_k   (21 windows x 255 entries, twisted Edwards affine)
 // built once per SRS, and one warp per MSM sums the <= 21*B table entries selected by the
-// scalar bytes (mixed adds), reduces across lanes with shuffles and converts to affine.
+// scalar bytes (complete 8M mixed adds), reduces across lanes with shuffles and converts
+// to canonical Montgomery affine.
 #include "tc_internal.cuh"
 
 using namespace tc;
@@ -25,8 +26,9 @@ __global__ void k_tab_bases(const Aff* pts, uint32_t B, Xyzz* q) {
   }
 }
 
-// tab[k][w][j] = (j+1) Q[k][w]
-__global__ void k_tab_fill(const Xyzz* q, uint32_t B, Aff* tab) {
+// tab[k][w][j] = (j+1) Q[k][w], twisted Edwards affine (x, y, xy): the MSM kernel then
+// runs complete, branch-free 8M mixed adds
+__global__ void k_tab_fill(const Xyzz* q, uint32_t B, EdAff* tab) {
   uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= B * SW * SE) return;
   uint32_t j = t % SE + 1, kw = t / SE;
@@ -38,41 +40,42 @@ __global__ void k_tab_fill(const Xyzz* q, uint32_t B, Aff* tab) {
   }
   Aff r = xyzz_to_aff(acc);
   if (!aff_is_inf(r)) r = Aff{Fq::canon(r.x), Fq::canon(r.y)};
-  tab[t] = r;
+  const EdAff e = aff_to_ed(r);
+  tab[t] = EdAff{Fq::red2(e.x), Fq::red2(e.y), Fq::red2(e.t)};
 }
 
-__device__ __forceinline__ Xyzz shfl_xyzz(const Xyzz& p, int src) {
-  Xyzz r;
+__device__ __forceinline__ Ext shfl_ext(const Ext& p, int src) {
+  Ext r;
 #pragma unroll
   for (int i = 0; i < 6; i++) {
     r.X.v[i] = __shfl_down_sync(0xffffffffu, p.X.v[i], src);
     r.Y.v[i] = __shfl_down_sync(0xffffffffu, p.Y.v[i], src);
-    r.ZZ.v[i] = __shfl_down_sync(0xffffffffu, p.ZZ.v[i], src);
-    r.ZZZ.v[i] = __shfl_down_sync(0xffffffffu, p.ZZZ.v[i], src);
+    r.Z.v[i] = __shfl_down_sync(0xffffffffu, p.Z.v[i], src);
+    r.T.v[i] = __shfl_down_sync(0xffffffffu, p.T.v[i], src);
   }
   return r;
 }
 
 // one warp per MSM; scalars are canonical F_p limbs: ptrs[l][k], k < B
-__global__ void __launch_bounds__(128) k_small_msm(const Fe* const* ptrs, uint32_t L, uint32_t B, const Aff* tab,
+__global__ void __launch_bounds__(128) k_small_msm(const Fe* const* ptrs, uint32_t L, uint32_t B, const EdAff* tab,
                                                    Aff* out) {
   const uint32_t l = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
   if (l >= L) return;   // whole warps exit together
   const Fe* s = ptrs[l];
-  Xyzz acc = xyzz_inf();
+  Ext acc = ext_zero();
   for (uint32_t kw = lane; kw < B * SW; kw += 32) {
     const uint32_t k = kw / SW, w = kw % SW;
     const uint32_t byte = (s[k].v[w >> 2] >> (8 * (w & 3))) & 0xffu;
-    if (byte) xyzz_add_aff(acc, tab[(uint64_t)kw * SE + byte - 1]);
+    if (byte) ext_madd(acc, ld_edaff(tab + (uint64_t)kw * SE + byte - 1));
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
-    Xyzz other = shfl_xyzz(acc, o);
-    if (lane < (uint32_t)o) xyzz_add(acc, other);
+    Ext other = shfl_ext(acc, o);
+    if (lane < (uint32_t)o) ext_add(acc, other);
   }
   if (lane == 0) {
-    Aff r = xyzz_to_aff(acc);
+    Aff r = ext_to_aff(acc);
     if (!aff_is_inf(r)) r = Aff{Fq::canon(r.x), Fq::canon(r.y)};
     out[l] = r;
   }
@@ -83,7 +86,7 @@ __global__ void __launch_bounds__(128) k_small_msm(const Fe* const* ptrs, uint32
 namespace tcrt {
 
 // build (once) the byte-window tables of the SRS's `which` elements
-static int small_tables(tc_ctx* ctx, tc_srs* srs, int which, const Aff** out) {
+static int small_tables(tc_ctx* ctx, tc_srs* srs, int which, const EdAff** out) {
   const int idx = (which == TC_SRS_LAGRANGE) ? 1 : 0;
   if (!srs->small_tab[idx]) {
     const Aff* pts = idx ? srs->lagrange : srs->monomial;
@@ -91,8 +94,8 @@ static int small_tables(tc_ctx* ctx, tc_srs* srs, int which, const Aff** out) {
     const uint32_t B = (uint32_t)srs->n;
     Xyzz* q;
     TC_TRY(scratch_t(ctx, "small.q", (uint64_t)B * SW, &q));
-    Aff* tab = nullptr;
-    TC_CUDA(ctx, cudaMalloc(&tab, (size_t)B * SW * SE * sizeof(Aff)));
+    EdAff* tab = nullptr;
+    TC_CUDA(ctx, cudaMalloc(&tab, (size_t)B * SW * SE * sizeof(EdAff)));
     k_tab_bases<<<blocks_for(B, 32), 32, 0, ctx->stream>>>(pts, B, q);
     TC_LAUNCHED(ctx);
     k_tab_fill<<<blocks_for((uint64_t)B * SW * SE, 128), 128, 0, ctx->stream>>>(q, B, tab);
@@ -107,7 +110,7 @@ static int small_tables(tc_ctx* ctx, tc_srs* srs, int which, const Aff** out) {
 int small_msm_device(tc_ctx* ctx, tc_srs* srs, int which, const void* const* h_ptrs, int L, Aff* d_out) {
   if (L <= 0) return TC_OK;
   if (srs->n > ::SMALL_MSM_MAX) return fail(ctx, TC_ERR_VALUE, "small msm: srs too large");
-  const Aff* tab;
+  const EdAff* tab;
   TC_TRY(small_tables(ctx, srs, which, &tab));
   const Fe** d_ptrs;
   TC_TRY(scratch_t(ctx, "small.ptrs", (uint64_t)L, (Fe***)&d_ptrs));

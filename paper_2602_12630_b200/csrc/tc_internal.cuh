@@ -59,7 +59,7 @@ struct tc_srs {
   tc::Aff* monomial = nullptr;   // N affine points, Montgomery form, lex order
   tc::Aff* lagrange = nullptr;   // N affine points g^{L_i(tau)} (optional)
   tc::Aff axis[TC_MAX_AXES];     // g^{tau_j} (host copy)
-  tc::Aff* small_tab[2] = {nullptr, nullptr};   // byte-window tables (monomial, Lagrange), n <= 64
+  tc::EdAff* small_tab[2] = {nullptr, nullptr};   // byte-window tables (monomial, Lagrange), n <= 64
   // sub-grid Lagrange elements g^{prod_{j>=i} L_{j,a_j}(tau_j)} for suffixes i = 1..m-1
   // (commitments of the Lagrange-route opening quotients q_i, which live on axes i..m-1)
   tc::Aff* sublag = nullptr;
