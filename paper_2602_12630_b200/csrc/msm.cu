@@ -1067,10 +1067,15 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     TC_LAUNCHED(ctx);
     return TC_OK;
   }
-  // bound the scratch of one pipeline: at most 2^26 quantised floats (<= 3-4 windows) or
-  // 2^24 full field elements (~14 windows) per batch; larger batches run in groups
+  // bound the scratch of one pipeline: at most 2^28 fp16 / bf16 values (one bucket entry
+  // each under the float-exponent plan: 1 GiB of entries), 2^26 other floats (<= 3-4
+  // windows) or 2^24 full field elements (~14 windows) per batch; larger batches run in
+  // groups (config 5: 6 layers of 41.9 M per pipeline instead of 1, so the reduction tails
+  // are paid 7 times per step instead of 40)
   {
-    const uint64_t per = (dtype == TC_DTYPE_FP_LIMBS) ? (1ull << 24) : (1ull << 26);
+    static const uint64_t PER16 = getenv("TC_MSM_PER16") ? strtoull(getenv("TC_MSM_PER16"), nullptr, 10) : (1ull << 28);
+    const uint64_t per = (dtype == TC_DTYPE_FP_LIMBS) ? (1ull << 24)
+                         : (dtype == TC_DTYPE_F16 || dtype == TC_DTYPE_BF16) ? PER16 : (1ull << 26);
     const uint64_t G = std::max<uint64_t>(1, per / n);
     if ((uint64_t)L > G) {
       for (int l0 = 0; l0 < L; l0 += (int)G) {
