@@ -314,14 +314,24 @@ def main():
     host_pinned2 = [h.clone().pin_memory() for h in host_pinned]
 
     def e2e_stream(steps):
-        """`steps` forwards through protocol.prover_commit_stream: forward k+1's upload runs
-        under forward k's commitments; every forward's 128 MiB is copied inside the region."""
+        """`steps` forwards of pinned host activations through the streaming API: forward
+        k+1's upload runs under forward k's commitments; every forward's bytes are copied
+        inside the region.  One rank: protocol.prover_commit_stream; several: each rank
+        streams its own layers (tc_commit_stream), then the commitment gather and the tree."""
         batches = [host_pinned if k % 2 == 0 else host_pinned2 for k in range(steps)]
         root = None
-        for comms, root, _ in tcb.prover_commit_stream(batches, srs, tree_config=tcfg, node_srs=node_srs,
+        if world == 1:
+            for _, root, _ in tcb.prover_commit_stream(batches, srs, tree_config=tcfg, node_srs=node_srs,
                                                        route=args.route):
-            if world > 1:
-                raise RuntimeError("streaming e2e is single-rank")
+                pass
+            return root
+        for k in range(steps):
+            comms = tcb.tc_commit_stream(srs, batches[k], batches[k + 1] if k + 1 < steps else None,
+                                         route=args.route)
+            encs = allgather_commitments([c.to_bytes() for c in comms], n_layers, rank, world,
+                                         device=dev if backend == "nccl" else None)
+            leaves = [tcb.hash_to_scalar(e, b"terkle/leaf") for e in encs]
+            root = tcb.build(tcfg, leaves, srs=node_srs)[1]
         return root
 
     def timed(fn, steps):
@@ -354,11 +364,10 @@ def main():
     if root_e2e != root:
         raise RuntimeError("e2e root differs from the device-resident root")
     ms_stream = None
-    if world == 1:
-        e2e_stream(2)
-        ms_stream, _, root_s = timed(lambda: e2e_stream(args.steps), 1)
-        if root_s != root:
-            raise RuntimeError("streaming e2e root differs from the device-resident root")
+    e2e_stream(2)
+    ms_stream, _, root_s = timed(lambda: e2e_stream(args.steps), 1)
+    if root_s != root:
+        raise RuntimeError("streaming e2e root differs from the device-resident root")
 
     # dominant kernel: Pippenger bucket accumulation, CUDA events on the ctx stream
     ctx.set_profiling(True)
@@ -411,9 +420,10 @@ def main():
     if ms_stream is not None:
         e2e = dict(e2e_serial, value=per_step_elems / (ms_stream / args.steps / 1e3),
                    ms_per_step=ms_stream / args.steps,
-                   path=f"protocol.prover_commit_stream over {args.steps} forwards of pinned host tensors "
-                        "(tc_commit_stream: forward k+1's upload overlaps forward k's commit; first upload "
-                        "exposed) + Terkle build + commitments/root read back, per step",
+                   path=f"{args.steps} forwards of pinned host tensors through the streaming API "
+                        "(protocol.prover_commit_stream / tc_commit_stream per rank: forward k+1's upload "
+                        "overlaps forward k's commit; first upload exposed) + commitment gather (N > 1) + "
+                        "Terkle build + commitments/root read back, per step",
                    serial=e2e_serial)
     else:
         e2e = e2e_serial
