@@ -257,7 +257,17 @@ TC_HD EdAff edaff_neg(const EdAff& p) { return EdAff{Fq::neg(p.x), p.y, Fq::neg(
 TC_HD Ext ext_neg(const Ext& p) { return Ext{Fq::neg(p.X), p.Y, p.Z, Fq::neg(p.T)}; }
 
 // acc += q (q affine with t = x y): madd-2008-hwcd, a = 2, d = -2
+#ifndef TC_LAZY
+#define TC_LAZY 1   // E and H from unreduced products (Fq::lazy_e_h): 7 reductions per add, not 8
+#endif
 TC_HD void ext_madd(Ext& acc, const EdAff& q) {
+#if TC_LAZY
+  Fe E, H;
+  Fq::lazy_e_h(acc.X, acc.Y, q.x, q.y, E, H);   // E = X1 y2 + Y1 x2, H = Y1 y2 - 2 X1 x2
+  const Fe C2 = Fq::dbl(Fq::mul(acc.T, q.t));   // -d T1 T2
+  const Fe F = Fq::add(acc.Z, C2);               // Z1 - d T1 T2
+  const Fe G = Fq::sub(acc.Z, C2);               // Z1 + d T1 T2
+#else
   const Fe A = Fq::mul(acc.X, q.x);
   const Fe B = Fq::mul(acc.Y, q.y);
   const Fe C2 = Fq::dbl(Fq::mul(acc.T, q.t));   // -d T1 T2
@@ -265,6 +275,7 @@ TC_HD void ext_madd(Ext& acc, const EdAff& q) {
   const Fe F = Fq::add(acc.Z, C2);               // Z1 - d T1 T2
   const Fe G = Fq::sub(acc.Z, C2);               // Z1 + d T1 T2
   const Fe H = Fq::sub(B, Fq::dbl(A));           // B - a A
+#endif
   acc.X = Fq::mul(E, F);
   acc.Y = Fq::mul(G, H);
   acc.T = Fq::mul(E, H);
@@ -273,6 +284,14 @@ TC_HD void ext_madd(Ext& acc, const EdAff& q) {
 
 // acc += q, both extended: add-2008-hwcd (unified, complete here)
 TC_HD void ext_add(Ext& acc, const Ext& q) {
+#if TC_LAZY
+  Fe E, H;
+  Fq::lazy_e_h(acc.X, acc.Y, q.X, q.Y, E, H);
+  const Fe C2 = Fq::dbl(Fq::mul(acc.T, q.T));
+  const Fe D = Fq::mul(acc.Z, q.Z);
+  const Fe F = Fq::add(D, C2);
+  const Fe G = Fq::sub(D, C2);
+#else
   const Fe A = Fq::mul(acc.X, q.X);
   const Fe B = Fq::mul(acc.Y, q.Y);
   const Fe C2 = Fq::dbl(Fq::mul(acc.T, q.T));
@@ -281,6 +300,7 @@ TC_HD void ext_add(Ext& acc, const Ext& q) {
   const Fe F = Fq::add(D, C2);
   const Fe G = Fq::sub(D, C2);
   const Fe H = Fq::sub(B, Fq::dbl(A));
+#endif
   acc.X = Fq::mul(E, F);
   acc.Y = Fq::mul(G, H);
   acc.T = Fq::mul(E, H);

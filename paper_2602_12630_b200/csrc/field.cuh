@@ -53,6 +53,8 @@ struct FpParams {   // scalar field F_p (field.py PrimeField(backend.order))
                             ONE3 = 0xffffffffu, ONE4 = 0xffffffffu, ONE5 = 0x1u;
   static constexpr uint32_t R20 = 0x0u, R21 = 0x40000000u, R22 = 0x800000u, R23 = 0x4000u,
                             R24 = 0x0u, R25 = 0x0u;
+  // 8 p^2 limbs 0..11 (the non-zero ones) for lazy reduction
+  static constexpr uint32_t K0 = 0x10000008u, K1 = 0x80000u, K2 = 0x0u, K5 = 0x20000020u, K6 = 0x0u, K10 = 0x20u;
   // R^3 mod p (binary-inversion result -> Montgomery form)
   static constexpr uint32_t R30 = 0x11000011u, R31 = 0x0u, R32 = 0xe0000000u, R33 = 0xff9fffffu,
                             R34 = 0xffff9fffu, R35 = 0x1u;
@@ -65,6 +67,8 @@ struct FqParams {   // curve base field F_q
                             ONE3 = 0xffffffffu, ONE4 = 0xffffffffu, ONE5 = 0xfu;
   static constexpr uint32_t R20 = 0xc70123b5u, R21 = 0x3ef01234u, R22 = 0x11900000u,
                             R23 = 0x11115111u, R24 = 0x11111111u, R25 = 0xe1u;
+  // 8 q^2 limbs 0..11 (the non-zero ones) for lazy reduction
+  static constexpr uint32_t K0 = 0x8001ba88u, K1 = 0xc200037cu, K2 = 0x1u, K5 = 0x6f900u, K6 = 0x708u, K10 = 0x70800u;
   static constexpr uint32_t R30 = 0x07d3b44au, R31 = 0x148e4c4fu, R32 = 0xd7b0eddfu, R33 = 0xbc809907u,
                             R34 = 0x67894c9au, R35 = 0xc5u;
 };
@@ -424,6 +428,107 @@ struct Field {
     uint32_t T[12];
     mul_wide(T, a, b);
     return redc(T);
+  }
+
+  // ---- 12-limb (unreduced product) arithmetic for lazy reduction --------------------------
+  // r = a - b (a >= b as integers)
+  TC_HD static void w12_sub(uint32_t r[12], const uint32_t a[12], const uint32_t b[12]) {
+#if defined(__CUDA_ARCH__)
+    asm("sub.cc.u32  %0, %12, %24;\n\t"
+        "subc.cc.u32 %1, %13, %25;\n\t"
+        "subc.cc.u32 %2, %14, %26;\n\t"
+        "subc.cc.u32 %3, %15, %27;\n\t"
+        "subc.cc.u32 %4, %16, %28;\n\t"
+        "subc.cc.u32 %5, %17, %29;\n\t"
+        "subc.cc.u32 %6, %18, %30;\n\t"
+        "subc.cc.u32 %7, %19, %31;\n\t"
+        "subc.cc.u32 %8, %20, %32;\n\t"
+        "subc.cc.u32 %9, %21, %33;\n\t"
+        "subc.cc.u32 %10, %22, %34;\n\t"
+        "subc.u32    %11, %23, %35;\n\t"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]), "r"(a[8]),
+          "r"(a[9]), "r"(a[10]), "r"(a[11]), "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3]), "r"(b[4]), "r"(b[5]),
+          "r"(b[6]), "r"(b[7]), "r"(b[8]), "r"(b[9]), "r"(b[10]), "r"(b[11]));
+#else
+    uint64_t br = 0;
+    for (int i = 0; i < 12; i++) {
+      const uint64_t t = (uint64_t)a[i] - b[i] - br;
+      r[i] = (uint32_t)t;
+      br = (t >> 63) & 1u;
+    }
+#endif
+  }
+  // r = a + K where K = 8 m^2 (a multiple of m: adding it leaves redc's result unchanged mod m)
+  TC_HD static void w12_add_8mm(uint32_t r[12], const uint32_t a[12]) {
+    const uint32_t K[12] = {PM::K0, PM::K1, PM::K2, 0, 0, PM::K5, PM::K6, 0, 0, 0, PM::K10, 0};
+#if defined(__CUDA_ARCH__)
+    asm("add.cc.u32  %0, %12, %24;\n\t"
+        "addc.cc.u32 %1, %13, %25;\n\t"
+        "addc.cc.u32 %2, %14, %26;\n\t"
+        "addc.cc.u32 %3, %15, %27;\n\t"
+        "addc.cc.u32 %4, %16, %28;\n\t"
+        "addc.cc.u32 %5, %17, %29;\n\t"
+        "addc.cc.u32 %6, %18, %30;\n\t"
+        "addc.cc.u32 %7, %19, %31;\n\t"
+        "addc.cc.u32 %8, %20, %32;\n\t"
+        "addc.cc.u32 %9, %21, %33;\n\t"
+        "addc.cc.u32 %10, %22, %34;\n\t"
+        "addc.u32    %11, %23, %35;\n\t"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]), "r"(a[8]),
+          "r"(a[9]), "r"(a[10]), "r"(a[11]), "r"(K[0]), "r"(K[1]), "r"(K[2]), "r"(K[3]), "r"(K[4]), "r"(K[5]),
+          "r"(K[6]), "r"(K[7]), "r"(K[8]), "r"(K[9]), "r"(K[10]), "r"(K[11]));
+#else
+    uint64_t c = 0;
+    for (int i = 0; i < 12; i++) {
+      c += (uint64_t)a[i] + K[i];
+      r[i] = (uint32_t)c;
+      c >>= 32;
+    }
+#endif
+  }
+  // Lazy pair for Edwards adds: with A = a1 b1, B = a2 b2 (unreduced) and P = (a1+a2)(b1+b2),
+  //   E = P - A - B = a1 b2 + a2 b1 >= 0 (exact)  and  H = B - 2A + 8m^2 > 0,
+  // both < 12 m^2 < m R, reduced ONCE each: 3 products, 2 reductions (instead of 3 + 3).
+  // The sums must NOT be reduced: (a1 + a2 - 2m)(...) would make P - A - B negative.
+  // a1 + a2 < 4m < 2^170 fits the 6 limbs; P < 16 m^2, P - A - B < 8 m^2.
+  TC_HD static Fe add_raw(const Fe& a, const Fe& b) {
+    Fe r;
+#if defined(__CUDA_ARCH__)
+    asm("add.cc.u32  %0, %6, %12;\n\t"
+        "addc.cc.u32 %1, %7, %13;\n\t"
+        "addc.cc.u32 %2, %8, %14;\n\t"
+        "addc.cc.u32 %3, %9, %15;\n\t"
+        "addc.cc.u32 %4, %10, %16;\n\t"
+        "addc.u32    %5, %11, %17;\n\t"
+        : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5])
+        : "r"(a.v[0]), "r"(a.v[1]), "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]),
+          "r"(b.v[0]), "r"(b.v[1]), "r"(b.v[2]), "r"(b.v[3]), "r"(b.v[4]), "r"(b.v[5]));
+#else
+    uint64_t c = 0;
+    for (int i = 0; i < 6; i++) {
+      c += (uint64_t)a.v[i] + b.v[i];
+      r.v[i] = (uint32_t)c;
+      c >>= 32;
+    }
+#endif
+    return r;
+  }
+  TC_HD static void lazy_e_h(const Fe& a1, const Fe& a2, const Fe& b1, const Fe& b2, Fe& E, Fe& H) {
+    uint32_t A[12], B[12], P[12];
+    mul_wide(A, a1, b1);
+    mul_wide(B, a2, b2);
+    mul_wide(P, add_raw(a1, a2), add_raw(b1, b2));
+    w12_sub(P, P, A);
+    w12_sub(P, P, B);
+    E = redc(P);
+    w12_add_8mm(B, B);
+    w12_sub(B, B, A);
+    w12_sub(B, B, A);
+    H = redc(B);
   }
 
 #if defined(__CUDA_ARCH__)

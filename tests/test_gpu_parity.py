@@ -444,6 +444,24 @@ def test_config3_prover_commit_subset_and_tree():
     assert root.elem == levels[-1][0]
 
 
+def test_commitments_deterministic_across_runs_and_paths():
+    """Bucket order inside the MSM depends on atomic scheduling; the bytes must not.  Eight
+    full config-3 layers committed three times on the device path and once through the host
+    (pinned) path are identical, and two of them equal the trapdoor oracle (this is the test
+    that caught a lazy-reduction bound violated only for rare operand magnitudes)."""
+    tcb = T()
+    shape = (32, 32, 32, 64)
+    srs, td = tcb.setup_srs(shape, b"tc-b200/config3")
+    xs = [_config3_layer(l) for l in range(8)]
+    dev = [torch.from_numpy(x).cuda() for x in xs]
+    runs = [[c.elem for c in tcb.tc_commit_many(srs, dev)] for _ in range(3)]
+    runs.append([c.elem for c in tcb.tc_commit_many(srs, [torch.from_numpy(x).pin_memory() for x in xs])])
+    assert all(r == runs[0] for r in runs[1:])
+    for l in (0, 7):
+        want = O.commit_trapdoor(O.quantize(xs[l].astype(np.float64), 16), shape, list(td.taus))
+        assert runs[0][l] == want
+
+
 @pytest.mark.slow
 def test_config5_layer_trapdoor():
     """One full config-5 layer (41,943,040 fp16 elements, grid (64,128,64,80)) on both routes."""

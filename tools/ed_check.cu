@@ -72,6 +72,24 @@ int main() {
     b.v[5] &= 0x3u;
     bad += !Fp::eq(Fp::inv_fast(b), Fp::inv(b)); n++;
   }
+  // lazy E / H against the reduced formulas on lazy operands close to 2m (the sums exceed 2m)
+  for (int it = 0; it < 2000; it++) {
+    Fe a[4];
+    for (int j = 0; j < 4; j++) {
+      for (int i = 0; i < 5; i++) a[j].v[i] = (uint32_t)r64();
+      a[j].v[5] = (uint32_t)(0x1D0 + r64() % 0x10);   // in [2m - 2^164, 2m): lazy, near the top
+      if (it & 1) a[j].v[5] = (uint32_t)(r64() % 0x1E0);
+      a[j] = Fq::red2(a[j]);
+    }
+    Fe E, H;
+    Fq::lazy_e_h(a[0], a[1], a[2], a[3], E, H);
+    const Fe A = Fq::mul(a[0], a[2]), B = Fq::mul(a[1], a[3]);
+    const Fe E2 = Fq::add(Fq::mul(a[0], a[3]), Fq::mul(a[1], a[2]));
+    const Fe H2 = Fq::sub(B, Fq::dbl(A));
+    bad += !Fq::eq(E, E2) || !Fq::eq(H, H2); n++;
+    // outputs stay lazy (< 2m)
+    bad += (E.v[5] >= 0x1E0u) || (H.v[5] >= 0x1E0u); n++;
+  }
   printf("{\"edwards_checks\": %d, \"bad\": %d}\n", n, bad);
   return bad != 0;
 }
