@@ -539,6 +539,8 @@ __global__ void __launch_bounds__(256) k_digits_fp(const void* const* ptrs, uint
 #pragma unroll
     for (int k = 0; k < V_EPT; k++)
       if (live >> k & 1u) slot[k] = atomicAdd(cnt + ctr[k], 1u);
+    // (measured: the scattered stores of the MSMs in flight combine in L2 — DRAM writes
+    // = the 268 MB of entries; the pass is bound by the 67 M returning atomics)
 #pragma unroll
     for (int k = 0; k < V_EPT; k++)
       if (live >> k & 1u) vals[slot[k]] = val[k];
