@@ -338,6 +338,32 @@ TC_HD Ext ext_mul_small(const Ext& p, uint32_t k) {
   return r;
 }
 
+// k * P through the non-adjacent form (k = 2^10 - 1 costs 10 doublings + 1 add, not
+// 10 + 9): the latency-bound window re-basing multiplies by mlo - 1 = 1023
+TC_HD Ext ext_mul_small_naf(const Ext& p, uint32_t k) {
+  if (k == 0) return ext_zero();
+  int8_t naf[34];
+  int len = 0;
+  uint64_t v = k;
+  while (v) {
+    int d = 0;
+    if (v & 1u) {
+      d = 2 - (int)(v & 3u);   // +1 or -1
+      v -= (uint64_t)(int64_t)d;
+    }
+    naf[len++] = (int8_t)d;
+    v >>= 1;
+  }
+  const Ext np = ext_neg(p);
+  Ext r = naf[len - 1] > 0 ? p : np;
+  for (int i = len - 2; i >= 0; i--) {
+    r = ext_dbl(r);
+    if (naf[i] > 0) ext_add(r, p);
+    if (naf[i] < 0) ext_add(r, np);
+  }
+  return r;
+}
+
 // Edwards (X:Y:Z:T) -> Montgomery affine (u, v) = ((Z+Y)/(Z-Y), (Z+Y) Z / ((Z-Y) X)),
 // one inversion.  Neutral -> infinity; (0 : -1) -> the 2-torsion point (0, 0).
 TC_HD Aff ext_to_aff(const Ext& p) {

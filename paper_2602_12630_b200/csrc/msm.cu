@@ -865,12 +865,16 @@ __global__ void __launch_bounds__(128) k_wsum_level(const Ext* Tin, const Ext* D
 //     A = sum_j (j+1) B_j = sum_t U_t + C * sum_t t T_t,   sum_t t T_t = sum_{t>=1} R_t,
 // R_t = sum_{s>=t} T_s (a shared-memory suffix scan), S = R_0, and W = A + (mlo - 1) S.
 // Serial depth ~ 2C + 2 log2(threads) + log2(C) + log2(mlo) adds instead of ~27 per level.
-constexpr int WB_THREADS = 128;
-constexpr int WB_CHUNK_LG = 4;   // C = 16: 128 x 16 = 2048 buckets
+#ifndef TC_WB_THREADS
+#define TC_WB_THREADS 512
+#endif
+constexpr int WB_THREADS = TC_WB_THREADS;
+constexpr int WB_CHUNK_LG = TC_WB_THREADS == 512 ? 2 : (TC_WB_THREADS == 256 ? 3 : 4);   // 2048 buckets
 
-__global__ void __launch_bounds__(WB_THREADS) k_wsum_block(const Ext* buckets, WinPlan P, Ext* W) {
-  __shared__ Ext sh[WB_THREADS];
-  __shared__ Ext su[WB_THREADS];
+__global__ void __launch_bounds__(WB_THREADS, 1) k_wsum_block(const Ext* buckets, WinPlan P, Ext* W) {
+  extern __shared__ Ext wb_smem[];
+  Ext* sh = wb_smem;
+  Ext* su = wb_smem + WB_THREADS;
   const uint32_t g = blockIdx.x, l = g / P.nwin, w = g % P.nwin, t = threadIdx.x;
   const uint32_t nbw = P.base[w + 1] - P.base[w];
   const Ext* b = buckets + (uint64_t)l * P.nbm + P.base[w];
@@ -910,7 +914,7 @@ __global__ void __launch_bounds__(WB_THREADS) k_wsum_block(const Ext* buckets, W
   for (int i = 0; i < WB_CHUNK_LG; i++) A = ext_dbl(A);
   ext_add(A, su[0]);
   const uint32_t c = P.mlo[w] - 1u;
-  if (c) ext_add(A, ext_mul_small(S, c));
+  if (c) ext_add(A, ext_mul_small_naf(S, c));
   W[g] = A;
 }
 
@@ -921,7 +925,7 @@ __global__ void k_wsum_final(const Ext* T, const Ext* D, uint32_t ngroups, uint3
   Ext w = D[g];
   const int64_t coef = (int64_t)P.mlo[g % P.nwin] - 1 - (int64_t)c;
   if (coef) {
-    Ext s = ext_mul_small(T[g], (uint32_t)(coef < 0 ? -coef : coef));
+    Ext s = ext_mul_small_naf(T[g], (uint32_t)(coef < 0 ? -coef : coef));
     ext_add(w, coef < 0 ? ext_neg(s) : s);
   }
   W[g] = w;
@@ -1420,10 +1424,14 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   // latency-bound small batches (multi-GPU ranks, openings): one block per window; large
   // batches keep the level recursion, which has more parallelism (measured: 4 layers
   // 1.58 -> 1.51 ms per step, 32 layers 7.01 -> 7.11 ms with the block kernel)
-  if (!old_reduce && !no_block && maxw <= (uint32_t)WB_THREADS << WB_CHUNK_LG && nw_total <= 256) {
+  static const uint32_t WB_MAXG = getenv("TC_WB_MAXG") ? (uint32_t)atoi(getenv("TC_WB_MAXG")) : 256u;
+  if (!old_reduce && !no_block && maxw <= (uint32_t)WB_THREADS << WB_CHUNK_LG && nw_total <= WB_MAXG) {
     Ext* wsum;
     TC_TRY(scratch_t(ctx, "msm.wsum", nw_total, &wsum));
-    k_wsum_block<<<nw_total, WB_THREADS, 0, st>>>(buckets, P, wsum);
+    const size_t smem = 2 * WB_THREADS * sizeof(Ext);
+    if (smem > 48 * 1024)
+      TC_CUDA(ctx, cudaFuncSetAttribute(k_wsum_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_wsum_block<<<nw_total, WB_THREADS, smem, st>>>(buckets, P, wsum);
     TC_LAUNCHED(ctx);
     k_final<<<blocks_for(L, 32), 32, 0, st>>>(wsum, (uint32_t)L, P, d_out);
     TC_LAUNCHED(ctx);

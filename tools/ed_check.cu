@@ -53,8 +53,10 @@ int main() {
     Ext zz = ext_zero();
     ext_madd(zz, Qe);
     bad += !aff_eq(ext_to_aff(zz), Q); n++;
-    // small scalar multiple
+    // small scalar multiple (binary and NAF)
     bad += !aff_eq(ext_to_aff(ext_mul_small(ext_from_aff(Pe), 7)), mul_small(g, 7 * a)); n++;
+    for (uint32_t k : {1u, 2u, 3u, 7u, 11u, 1023u, 1024u, 4095u})
+      bad += !aff_eq(ext_to_aff(ext_mul_small_naf(ext_from_aff(Pe), k)), ext_to_aff(ext_mul_small(ext_from_aff(Pe), k))), n++;
     // infinity in -> neutral
     bad += !aff_is_inf(ext_to_aff(ext_from_aff(aff_to_ed(aff_inf())))); n++;
   }

@@ -1,3 +1,4 @@
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?"; tail -2 gpurun_out/pytest_gpu.log
-for nl in 1 4 32; do TC_PROFILE_TIME=1 TC_PROFILE_LAYERS=$nl python tools/profile_step.py | tail -1; done
-TC_PROFILE_LAYERS=4 python tools/profile_step.py > gpurun_out/plain_4.log 2>&1 && ncu --nvtx --nvtx-include "step/" --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_4.csv env TC_PROFILE_LAYERS=4 python tools/profile_step.py > gpurun_out/ncu_4.log 2>&1; python tools/launch_summary.py gpurun_out/launches_4.csv | head -8
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?"; tail -1 gpurun_out/pytest_gpu.log
+for v in "X=1" "TC_WB_MAXG=100000" "TC_MSM_NO_WSUM_BLOCK=1"; do
+for nl in 4 32; do env $v TC_PROFILE_TIME=1 TC_PROFILE_LAYERS=$nl python tools/profile_step.py 2>&1 | tail -1 | sed "s/^/$v /"; done
+done
