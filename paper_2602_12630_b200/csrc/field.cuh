@@ -256,6 +256,29 @@ struct Field {
   }
 #endif
 
+#if defined(__CUDA_ARCH__)
+  // T = ev + od * 2^32 (the even / odd partial-product accumulators of mul_wide)
+  TC_D static void merge_eo(uint32_t T[12], const uint32_t ev[12], const uint32_t od[12]) {
+    T[0] = ev[0];
+    asm("add.cc.u32  %0, %11, %22;\n\t"
+        "addc.cc.u32 %1, %12, %23;\n\t"
+        "addc.cc.u32 %2, %13, %24;\n\t"
+        "addc.cc.u32 %3, %14, %25;\n\t"
+        "addc.cc.u32 %4, %15, %26;\n\t"
+        "addc.cc.u32 %5, %16, %27;\n\t"
+        "addc.cc.u32 %6, %17, %28;\n\t"
+        "addc.cc.u32 %7, %18, %29;\n\t"
+        "addc.cc.u32 %8, %19, %30;\n\t"
+        "addc.cc.u32 %9, %20, %31;\n\t"
+        "addc.u32    %10, %21, %32;\n\t"
+        : "=r"(T[1]), "=r"(T[2]), "=r"(T[3]), "=r"(T[4]), "=r"(T[5]), "=r"(T[6]), "=r"(T[7]), "=r"(T[8]),
+          "=r"(T[9]), "=r"(T[10]), "=r"(T[11])
+        : "r"(ev[1]), "r"(ev[2]), "r"(ev[3]), "r"(ev[4]), "r"(ev[5]), "r"(ev[6]), "r"(ev[7]), "r"(ev[8]),
+          "r"(ev[9]), "r"(ev[10]), "r"(ev[11]), "r"(od[0]), "r"(od[1]), "r"(od[2]), "r"(od[3]), "r"(od[4]),
+          "r"(od[5]), "r"(od[6]), "r"(od[7]), "r"(od[8]), "r"(od[9]), "r"(od[10]));
+  }
+#endif
+
   // T[0..11] = a * b
 #if defined(__CUDA_ARCH__)
   // operand scanning, one row per limb of b: two 7-limb carry chains per row
@@ -313,24 +336,7 @@ struct Field {
     // row 5
     chain3_last(ev[6], ev[7], ev[8], ev[9], ev[10], ev[11], a1, a3, a5, b.v[5]);
     chain3(od[4], od[5], od[6], od[7], od[8], od[9], od[10], a0, a2, a4, b.v[5]);
-    // T = ev + od * 2^32
-    T[0] = ev[0];
-    asm("add.cc.u32  %0, %11, %22;\n\t"
-        "addc.cc.u32 %1, %12, %23;\n\t"
-        "addc.cc.u32 %2, %13, %24;\n\t"
-        "addc.cc.u32 %3, %14, %25;\n\t"
-        "addc.cc.u32 %4, %15, %26;\n\t"
-        "addc.cc.u32 %5, %16, %27;\n\t"
-        "addc.cc.u32 %6, %17, %28;\n\t"
-        "addc.cc.u32 %7, %18, %29;\n\t"
-        "addc.cc.u32 %8, %19, %30;\n\t"
-        "addc.cc.u32 %9, %20, %31;\n\t"
-        "addc.u32    %10, %21, %32;\n\t"
-        : "=r"(T[1]), "=r"(T[2]), "=r"(T[3]), "=r"(T[4]), "=r"(T[5]), "=r"(T[6]), "=r"(T[7]), "=r"(T[8]),
-          "=r"(T[9]), "=r"(T[10]), "=r"(T[11])
-        : "r"(ev[1]), "r"(ev[2]), "r"(ev[3]), "r"(ev[4]), "r"(ev[5]), "r"(ev[6]), "r"(ev[7]), "r"(ev[8]),
-          "r"(ev[9]), "r"(ev[10]), "r"(ev[11]), "r"(od[0]), "r"(od[1]), "r"(od[2]), "r"(od[3]), "r"(od[4]),
-          "r"(od[5]), "r"(od[6]), "r"(od[7]), "r"(od[8]), "r"(od[9]), "r"(od[10]));
+    merge_eo(T, ev, od);
 #else
     for (int i = 0; i < 12; i++) T[i] = 0;
     for (int i = 0; i < 6; i++) {
@@ -690,7 +696,9 @@ struct Field {
     return mul(w_is_one(u) ? x1 : x2, r3);
   }
 
-  // host: binary Euclid, device: Fermat (see inv_fast)
+
+  // host: binary Euclid (inv_fast); device: Fermat (a Stein variant with whole-run shifts
+  // measured 59.9k cycles vs Fermat's 49.5k for one thread, tools/inv_latency.cu)
   TC_HD static Fe inv_pref(const Fe& a) {
 #if defined(__CUDA_ARCH__)
     return inv(a);

@@ -871,7 +871,10 @@ __global__ void __launch_bounds__(128) k_wsum_level(const Ext* Tin, const Ext* D
 constexpr int WB_THREADS = TC_WB_THREADS;
 constexpr int WB_CHUNK_LG = TC_WB_THREADS == 512 ? 2 : (TC_WB_THREADS == 256 ? 3 : 4);   // 2048 buckets
 
-__global__ void __launch_bounds__(WB_THREADS, 1) k_wsum_block(const Ext* buckets, WinPlan P, Ext* W) {
+// prescale: also multiply the window sum by 2^off[w] (its weight in the scalar), so the
+// windows of an MSM only need to be ADDED (k_final_sum): the doublings of all windows run
+// in parallel blocks instead of one Horner chain
+__global__ void __launch_bounds__(WB_THREADS, 1) k_wsum_block(const Ext* buckets, WinPlan P, Ext* W, int prescale) {
   extern __shared__ Ext wb_smem[];
   Ext* sh = wb_smem;
   Ext* su = wb_smem + WB_THREADS;
@@ -915,6 +918,8 @@ __global__ void __launch_bounds__(WB_THREADS, 1) k_wsum_block(const Ext* buckets
   ext_add(A, su[0]);
   const uint32_t c = P.mlo[w] - 1u;
   if (c) ext_add(A, ext_mul_small_naf(S, c));
+  if (prescale)
+    for (int i = 0; i < P.off[w]; i++) A = ext_dbl(A);
   W[g] = A;
 }
 
@@ -947,6 +952,31 @@ __global__ void k_final(const Ext* wsum, uint32_t L, WinPlan P, Aff* out) {
     r.y = Fq::canon(r.y);
   }
   out[l] = r;
+}
+
+// one warp per MSM: sum of its (prescaled) window sums by a shuffle tree, then affine
+__global__ void k_final_sum(const Ext* wsum, uint32_t L, int nwin, Aff* out) {
+  const uint32_t l = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (l >= L) return;   // whole warps
+  Ext acc = ext_zero();
+  for (int w = (int)lane; w < nwin; w += 32) ext_add(acc, ld_ext(wsum + (uint64_t)l * nwin + w));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    Ext other;
+#pragma unroll
+    for (int i = 0; i < 6; i++) {
+      other.X.v[i] = __shfl_down_sync(0xffffffffu, acc.X.v[i], o);
+      other.Y.v[i] = __shfl_down_sync(0xffffffffu, acc.Y.v[i], o);
+      other.Z.v[i] = __shfl_down_sync(0xffffffffu, acc.Z.v[i], o);
+      other.T.v[i] = __shfl_down_sync(0xffffffffu, acc.T.v[i], o);
+    }
+    if (lane < (uint32_t)o) ext_add(acc, other);
+  }
+  if (lane == 0) {
+    Aff r = ext_to_aff(acc);
+    if (!aff_is_inf(r)) r = Aff{Fq::canon(r.x), Fq::canon(r.y)};
+    out[l] = r;
+  }
 }
 
 __global__ void k_fill_inf(Aff* out, uint32_t L) {
@@ -1431,9 +1461,13 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     const size_t smem = 2 * WB_THREADS * sizeof(Ext);
     if (smem > 48 * 1024)
       TC_CUDA(ctx, cudaFuncSetAttribute(k_wsum_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_wsum_block<<<nw_total, WB_THREADS, smem, st>>>(buckets, P, wsum);
+    const bool prescale = P.off[P.nwin - 1] <= 32;
+    k_wsum_block<<<nw_total, WB_THREADS, smem, st>>>(buckets, P, wsum, prescale ? 1 : 0);
     TC_LAUNCHED(ctx);
-    k_final<<<blocks_for(L, 32), 32, 0, st>>>(wsum, (uint32_t)L, P, d_out);
+    if (prescale)
+      k_final_sum<<<blocks_for((uint64_t)L * 32, 128), 128, 0, st>>>(wsum, (uint32_t)L, P.nwin, d_out);
+    else
+      k_final<<<blocks_for(L, 32), 32, 0, st>>>(wsum, (uint32_t)L, P, d_out);
     TC_LAUNCHED(ctx);
     return TC_OK;
   }

@@ -1,4 +1,2 @@
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?"; tail -1 gpurun_out/pytest_gpu.log
-for v in "X=1" "TC_WB_MAXG=100000" "TC_MSM_NO_WSUM_BLOCK=1"; do
-for nl in 4 32; do env $v TC_PROFILE_TIME=1 TC_PROFILE_LAYERS=$nl python tools/profile_step.py 2>&1 | tail -1 | sed "s/^/$v /"; done
-done
+for nl in 1 4 8 32; do TC_PROFILE_TIME=1 TC_PROFILE_LAYERS=$nl python tools/profile_step.py 2>&1 | tail -1; done
