@@ -599,6 +599,7 @@ int tc_srs_destroy(tc_srs* srs) {
   if (srs->sublag) cudaFree(srs->sublag);
   for (auto* e : {srs->ed_monomial, srs->ed_lagrange, srs->ed_sublag})
     if (e) cudaFree(e);
+  for (auto& kv : srs->wintab) cudaFree(kv.second);
   delete srs;
   return TC_OK;
 }
@@ -889,6 +890,21 @@ static const std::pair<std::vector<Fe>, std::vector<Fe>>& bary_weights(uint32_t 
   return cache.emplace(d, std::make_pair(w, winv)).first->second;
 }
 
+// MSM of canonical F_p scalars (opening quotients) over an SRS base range: through the
+// range's fixed-base window table (one shared bucket window, no Horner chain; built on first
+// use) when the table fits the budget, else the windowed Pippenger pipeline.
+static int msm_quotients(tc_ctx* ctx, const tc_srs* srs, const void* const* ptrs, int L, const EdAff* bases,
+                         uint64_t n, Aff* d_out) {
+  static const uint64_t BUDGET = getenv("TC_WINTAB_MB") ? strtoull(getenv("TC_WINTAB_MB"), nullptr, 10) << 20
+                                                        : (4096ull << 20);
+  if (n * tcrt::FB_NDIG * sizeof(EdAff) <= BUDGET) {
+    const EdAff* tab;
+    TC_TRY(tcrt::srs_window_table(ctx, const_cast<tc_srs*>(srs), bases, n, &tab));
+    return tcrt::msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, ptrs, L, tab, n, d_out, nullptr, true);
+  }
+  return tcrt::msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, ptrs, L, bases, n, d_out);
+}
+
 // Lagrange-route opening weights for every axis (see tcrt::LagW)
 static void lag_weights(const tc_srs* srs, const std::vector<Fe>& om, tcrt::LagW& W) {
   W.lam.clear();
@@ -978,7 +994,7 @@ int tc_open(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int sca
     for (int a = 0; a < m; a++) {
       const EdAff* bases = a == 0 ? ed_lag : ed_sub + srs->sublag_off[a];
       const void* ptr = qs + (uint64_t)a * n;
-      TC_TRY(tcrt::msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, &ptr, 1, bases, span, d_out + a));
+      TC_TRY(msm_quotients(ctx, srs, &ptr, 1, bases, span, d_out + a));
       span /= srs->shape[a];
     }
     return fetch_encode_many(ctx, d_out, m, out_pi43);
@@ -1122,7 +1138,7 @@ int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int 
         } else {
           const EdAff* bases = a == 0 ? ed_lag : ed_sub + srs->sublag_off[a];
           for (int k = 0; k < gc; k++) ptrs[k] = qall + ((uint64_t)k * m + a) * n;
-          TC_TRY(tcrt::msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, ptrs.data(), gc, bases, span,
+          TC_TRY(msm_quotients(ctx, srs, ptrs.data(), gc, bases, span,
                                         d_out + (uint64_t)a * gc));
         }
         span /= srs->shape[a];

@@ -55,10 +55,15 @@ constexpr int DIG_EPT = 1;    // elements per thread in k_digits (8 measured 1.7
 //         of fp16 (a signed-window plan of the same data leaves ~85% of its 2^17 low-window
 //         buckets empty: fp16 has 1024 mantissas per octave).  Bucket j of group w holds
 //         weight mlo[w] + j; the groups are combined with weight 2^off[w] (off[w] = w).
+// mode 2: fixed-base windows (openings: canonical F_p scalars against an SRS range with a
+//         window table, srs_window_table).  The scalar's ndig signed digits of cdig bits
+//         index the table copies 2^(cdig w) B, so all digits share ONE window of buckets:
+//         nwin = 1, no Horner doublings, and the bucket reduction is ndig x smaller.
 struct WinPlan {
   int nwin;
-  int mode;                  // 0 signed windows, 1 float-exponent groups
+  int mode;                  // 0 signed windows, 1 float-exponent groups, 2 fixed-base windows
   int mbits;                 // mode 1: significant bits of the input format
+  int ndig, cdig;            // mode 2: digit windows and their width
   uint32_t nbm;              // buckets per MSM
   uint8_t off[MAXW];         // window w: first bit (mode 0) / exponent k (mode 1)
   uint8_t width[MAXW];       // mode 0: c_w
@@ -277,6 +282,22 @@ __global__ void __launch_bounds__(256) k_count_digits(const void* const* ptrs, u
     if (in) load_scalar<DT>(p, i, scale_bits, mag, neg, f);
     else mag = Fe{{0, 0, 0, 0, 0, 0}};
     uint32_t carry = 0;
+    if (P.mode == 2) {   // fixed-base digit windows, one shared set of buckets
+      const int c = P.cdig;
+      const uint32_t half = 1u << (c - 1), full = 1u << c;
+      for (int w = 0; w < P.ndig; w++) {
+        uint32_t d = window_bits(mag, w * c, c) + carry;
+        bool dn = false;
+        if (d > half) {
+          d = full - d, dn = true, carry = 1;
+        } else {
+          carry = 0;
+        }
+        bucket_hit<SCATTER>(key0 + d - 1u, false, d != 0,
+                            (uint32_t)((uint64_t)w * n + i) | ((neg != dn) ? SIGN_BIT : 0u), cnt, vals);
+      }
+      continue;
+    }
     for (int w = 0; w < P.nwin; w++) {
       const int c = P.width[w];
       const uint32_t half = 1u << (c - 1), full = 1u << c;
@@ -1034,6 +1055,7 @@ WinPlan plan_windows(const uint32_t* hist, uint32_t nbits, uint64_t L) {
   WinPlan P;
   P.mode = 0;
   P.mbits = 0;
+  P.ndig = P.cdig = 0;
   P.nwin = (int)wins.size();
   uint32_t b = 0;
   for (int w = 0; w < P.nwin; w++) {
@@ -1054,10 +1076,27 @@ WinPlan plan_windows(const uint32_t* hist, uint32_t nbits, uint64_t L) {
   return P;
 }
 
+// mode-2 plan: one window of 2^(c-1) buckets shared by all digit windows
+WinPlan plan_fb() {
+  WinPlan P;
+  P.mode = 2;
+  P.mbits = 0;
+  P.ndig = tcrt::FB_NDIG;
+  P.cdig = tcrt::FB_C;
+  P.nwin = 1;
+  P.off[0] = 0;
+  P.width[0] = (uint8_t)tcrt::FB_C;
+  P.mlo[0] = 1;
+  P.base[0] = 0;
+  P.base[1] = P.nbm = 1u << (tcrt::FB_C - 1);
+  return P;
+}
+
 // mode-1 plan: groups k = 0 .. nbits - MB (see WinPlan)
 WinPlan plan_fp(uint32_t nbits, int mb) {
   WinPlan P;
   P.mode = 1;
+  P.ndig = P.cdig = 0;
   P.mbits = mb;
   P.nwin = nbits > (uint32_t)mb ? (int)nbits - mb + 1 : 1;
   uint32_t b = 0;
@@ -1092,7 +1131,9 @@ namespace tcrt {
 int quantize_flags_to_status(tc_ctx* ctx, uint32_t f);
 
 int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* h_ptrs, int L, const EdAff* d_bases,
-                     uint64_t n, Aff* d_out, const uint32_t* h_boff) {
+                     uint64_t n, Aff* d_out, const uint32_t* h_boff, bool fbw) {
+  if (fbw && (dtype != TC_DTYPE_FP_LIMBS || n * FB_NDIG >= (1ull << 31)))
+    return fail(ctx, TC_ERR_VALUE, "msm: window-table MSMs take field-element scalars, < 2^31 table points");
   cudaStream_t st = ctx->stream;
   if (L <= 0) return TC_OK;
   if (n >= (1ull << 31)) return fail(ctx, TC_ERR_VALUE, "msm: too many points (%llu)", (unsigned long long)n);
@@ -1117,7 +1158,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
       for (int l0 = 0; l0 < L; l0 += (int)G) {
         const int cnt = (int)std::min<uint64_t>(G, (uint64_t)(L - l0));
         TC_TRY(msm_batch_device(ctx, dtype, scale_bits, h_ptrs + l0, cnt, d_bases, n, d_out + l0,
-                                h_boff ? h_boff + l0 : nullptr));
+                                h_boff ? h_boff + l0 : nullptr, fbw));
       }
       return TC_OK;
     }
@@ -1184,12 +1225,12 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   for (int l = 0; l < L && vec_ok; l++) vec_ok = ((uintptr_t)h_ptrs[l] & 15u) == 0;   // 16-byte vector loads
   const int fp_mb = dtype == TC_DTYPE_F16 ? 11 : (dtype == TC_DTYPE_BF16 ? 8 : 0);
   const bool fpmode = vec_ok && fp_mb && n >= FP_MIN_N && (int)nbits - fp_mb + 1 <= MAXW;
-  const WinPlan P = fpmode ? plan_fp(nbits, fp_mb) : plan_windows(hist, nbits, (uint64_t)L);
+  const WinPlan P = fbw ? plan_fb() : fpmode ? plan_fp(nbits, fp_mb) : plan_windows(hist, nbits, (uint64_t)L);
   if (P.nwin > MAXW) return fail(ctx, TC_ERR_VALUE, "msm: window plan too long");
   const uint64_t nb64 = (uint64_t)L * P.nbm;
   if (nb64 >= (1ull << 31)) return fail(ctx, TC_ERR_VALUE, "msm batch too large (%llu buckets)", (unsigned long long)nb64);
   const uint32_t nb = (uint32_t)nb64;
-  const uint64_t cap = (uint64_t)L * n * (P.mode == 1 ? 1 : P.nwin);
+  const uint64_t cap = (uint64_t)L * n * (P.mode == 1 ? 1 : P.mode == 2 ? P.ndig : P.nwin);
   const int end_bit = (int)bitlen_u32(nb - 1);
 
   // 3. non-zero digits, compacted
@@ -1206,7 +1247,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   // digits 0.8 + onesweep 2.3 + bounds 0.4 ms): the per-layer slot counters and the
   // __match_any_sync aggregation serialise; kept for small-bucket experiments.
   const bool bucketed = want_bucketed && P.mode == 0 && (size_t)P.nbm * 8 <= 160 * 1024;
-  if (!bucketed && !want_radix) {
+  if (!bucketed && (!want_radix || P.mode == 2)) {
     // counting-sort layout: count, scan, scatter (no keys stored, no radix passes)
     uint32_t *cnt, *cursor;
     static const uint32_t NC_ENV = getenv("TC_MSM_NC") ? (uint32_t)atoi(getenv("TC_MSM_NC")) : 16u;   // sweep: 1 9.04, 4 7.79, 8 7.53, 16 7.40, 32 7.37 ms

@@ -126,9 +126,55 @@ __global__ void __launch_bounds__(128) k_to_edwards(const Aff* in, uint64_t n, E
   }
 }
 
+// out[i] = 2^c in[i] (Edwards affine with t = xy): c doublings in extended coordinates, the
+// Z of FB_K points per thread inverted with one shared inversion
+__global__ void __launch_bounds__(128) k_win_step(const EdAff* in, uint64_t n, int c, EdAff* out) {
+  uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t i0 = t * FB_K;
+  if (i0 >= n) return;
+  const int cnt = (n - i0 < (uint64_t)FB_K) ? (int)(n - i0) : FB_K;
+  Ext pts[FB_K];
+  Fe pref[FB_K];
+  Fe run = Fq::one();
+  for (int k = 0; k < cnt; k++) {
+    Ext e = ext_from_aff(ld_edaff(in + i0 + k));
+    for (int j = 0; j < c; j++) e = ext_dbl(e);
+    pts[k] = e;
+    pref[k] = run;
+    run = Fq::mul(run, e.Z);   // Z != 0 on the (complete) Edwards curve
+  }
+  Fe inv = Fq::inv(run);
+  for (int k = cnt - 1; k >= 0; k--) {
+    const Fe iz = Fq::mul(inv, pref[k]);
+    inv = Fq::mul(inv, pts[k].Z);
+    const Fe x = Fq::mul(pts[k].X, iz), y = Fq::mul(pts[k].Y, iz);
+    out[i0 + k] = EdAff{Fq::red2(x), Fq::red2(y), Fq::red2(Fq::mul(x, y))};
+  }
+}
+
 }  // namespace
 
 namespace tcrt {
+
+int srs_window_table(tc_ctx* ctx, tc_srs* srs, const EdAff* bases, uint64_t n, const EdAff** out) {
+  auto it = srs->wintab.find(bases);
+  if (it != srs->wintab.end()) {
+    *out = it->second;
+    return TC_OK;
+  }
+  EdAff* tab = nullptr;
+  if (cudaMalloc(&tab, std::max<uint64_t>(n, 1) * FB_NDIG * sizeof(EdAff)) != cudaSuccess)
+    return fail(ctx, TC_ERR_MEMORY, "window table alloc (%llu points)", (unsigned long long)(n * FB_NDIG));
+  TC_CUDA(ctx, cudaMemcpyAsync(tab, bases, n * sizeof(EdAff), cudaMemcpyDeviceToDevice, ctx->stream));
+  for (int w = 1; w < FB_NDIG; w++) {
+    k_win_step<<<blocks_for((n + FB_K - 1) / FB_K, 128), 128, 0, ctx->stream>>>(tab + (w - 1) * n, n, FB_C,
+                                                                                tab + w * n);
+    TC_LAUNCHED(ctx);
+  }
+  srs->wintab[bases] = tab;
+  *out = tab;
+  return TC_OK;
+}
 
 int to_edwards_device(tc_ctx* ctx, const Aff* d_in, uint64_t n, EdAff* d_out) {
   if (n == 0) return TC_OK;

@@ -67,6 +67,9 @@ struct tc_srs {
   tc::EdAff* ed_monomial = nullptr;
   tc::EdAff* ed_lagrange = nullptr;
   tc::EdAff* ed_sublag = nullptr;
+  // fixed-base window tables for full-scalar MSMs (openings): for a base range B (key:
+  // its first point), FB_NDIG copies 2^(FB_C w) B, w = 0..FB_NDIG-1 (built on first use)
+  std::map<const tc::EdAff*, tc::EdAff*> wintab;
   uint64_t sublag_off[TC_MAX_AXES] = {0};
 };
 
@@ -129,8 +132,18 @@ int msm_device(tc_ctx* ctx, ScalarKind kind, const void* d_scalars, const tc::Ed
 // canonical limbs; float dtypes are quantised at scale_bits inside the digit kernel).
 // h_boff (optional, host, L entries): MSM l reads the bases d_bases + h_boff[l] (batches of
 // MSMs over different slices of one SRS, e.g. the opening slice commitments)
+// fbw: d_bases is a fixed-base window table (srs_window_table, FB_NDIG * n points) and the
+// scalars are canonical F_p: every digit window shares ONE set of buckets (no Horner).
 int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* h_ptrs, int L,
-                     const tc::EdAff* d_bases, uint64_t n, tc::Aff* d_out, const uint32_t* h_boff = nullptr);
+                     const tc::EdAff* d_bases, uint64_t n, tc::Aff* d_out, const uint32_t* h_boff = nullptr,
+                     bool fbw = false);
+
+// fixed-base windowed MSMs over canonical F_p scalars: digit windows of FB_C bits, FB_NDIG
+// of them (covers 162 bits + the final carry); see WinPlan mode 2 in msm.cu
+constexpr int FB_C = 15;
+constexpr int FB_NDIG = 11;
+// the window table of the n bases starting at `bases` (FB_NDIG * n points), built once
+int srs_window_table(tc_ctx* ctx, tc_srs* srs, const tc::EdAff* bases, uint64_t n, const tc::EdAff** out);
 
 // Montgomery affine points -> twisted Edwards affine (x, y, t = x y), batched inversion
 int to_edwards_device(tc_ctx* ctx, const tc::Aff* d_in, uint64_t n, tc::EdAff* d_out);
