@@ -1086,7 +1086,6 @@ int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int 
   std::vector<uint8_t> enc((size_t)G * m * 43);
   std::vector<Fe> om(m), stabs;
   std::vector<int> ssj;
-  tcrt::LagW W;
   for (size_t jb = 0; jb < jobs.size(); jb++) {
     const std::vector<int>& ops = jobs[jb];
     const bool sliced = job_h[jb] != nullptr;
@@ -1110,23 +1109,37 @@ int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int 
       const int gc = (int)std::min<size_t>(G, ops.size() - g0);
       stabs.clear();
       ssj.clear();
+      // field values of the group's tensors (one copy per distinct tensor), then the
+      // quotients of all gc openings with one launch per axis
+      std::vector<tcrt::LagW> Ws(gc);
+      std::vector<const Fe*> vptr(gc);
+      std::map<const void*, const Fe*> loaded;
+      Fe* vbuf;
+      TC_TRY(tcrt::scratch_t(ctx, "openb.vals", (uint64_t)(sliced ? 1 : gc) * n, &vbuf));
       for (int k = 0; k < gc; k++) {
         const int i = ops[g0 + k];
         for (int j = 0; j < m; j++) le21_to_fe(omegas_le21 + 21 * ((size_t)i * m + j), om[j]);
-        lag_weights(srs, om, W);
+        lag_weights(srs, om, Ws[k]);
         if (sliced) {
-          stabs.insert(stabs.end(), W.lam.begin(), W.lam.begin() + d0);
-          stabs.insert(stabs.end(), W.inv.begin(), W.inv.begin() + d0);
-          stabs.insert(stabs.end(), W.der.begin(), W.der.begin() + d0);
-          ssj.push_back(W.sj[0]);
+          stabs.insert(stabs.end(), Ws[k].lam.begin(), Ws[k].lam.begin() + d0);
+          stabs.insert(stabs.end(), Ws[k].inv.begin(), Ws[k].inv.begin() + d0);
+          stabs.insert(stabs.end(), Ws[k].der.begin(), Ws[k].der.begin() + d0);
+          ssj.push_back(Ws[k].sj[0]);
         }
-        Fe* vals;
-        TC_TRY(load_field_tensor(ctx, d_ins[i], dtype, n, scale_bits, &vals, "open.vals"));
-        Fe y;
-        TC_TRY(tcrt::open_quotients_lagrange_device(ctx, vals, srs->shape, m, W, qall + (uint64_t)k * m * n, &y,
-                                                    sliced));
-        fe_to_le21(y, out_y21 + 21 * (size_t)i);
+        auto it = loaded.find(d_ins[i]);
+        if (it == loaded.end()) {
+          Fe* dst = vbuf + (uint64_t)loaded.size() * n;
+          if (dtype == TC_DTYPE_FP_LIMBS)
+            TC_CUDA(ctx, cudaMemcpyAsync(dst, d_ins[i], n * sizeof(Fe), cudaMemcpyDeviceToDevice, ctx->stream));
+          else
+            TC_TRY(tcrt::quantize_device(ctx, d_ins[i], dtype, n, scale_bits, dst));
+          it = loaded.emplace(d_ins[i], dst).first;
+        }
+        vptr[k] = it->second;
       }
+      std::vector<Fe> ys(gc);
+      TC_TRY(tcrt::open_quotients_lagrange_batch(ctx, vptr.data(), gc, srs->shape, m, Ws, qall, ys.data(), sliced));
+      for (int k = 0; k < gc; k++) fe_to_le21(Fp::canon(ys[k]), out_y21 + 21 * (size_t)ops[g0 + k]);
       uint64_t span = n;
       std::vector<const void*> ptrs(gc);
       for (int a = 0; a < m; a++) {

@@ -143,6 +143,39 @@ __global__ void k_slice_scalars(const Fe* tabs, const int* sj, uint32_t d, uint3
   out[t] = Fp::from_mont(Fp::mul(x, inv[c]));                        // canonical
 }
 
+// k_open_axis_lag for `cnt` openings in one launch: thread (o, i); opening o reads r_in[o]
+// (device pointer table), its weights at tabs + o * tstride + {0, dsum, 2 dsum}, writes
+// rn + o * rest and (unless q is null) q + o * qstride.  The per-opening kernels are
+// latency-bound (d sequential MACs per thread); a group's openings now share the launch.
+__global__ void k_open_axis_lag_b(const Fe* const* r_in, uint32_t d, uint64_t rest, const Fe* tabs, uint64_t tstride,
+                                  uint32_t dsum, const int* sj, Fe* rn, Fe* q, uint64_t qstride, uint32_t cnt) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (t >= rest * cnt) return;
+  const uint32_t o = (uint32_t)(t / rest);
+  const uint64_t i = t % rest;
+  const Fe* r = r_in[o];
+  const Fe* lam = tabs + o * tstride;
+  const Fe* inv = lam + dsum;
+  const Fe* der = lam + 2 * dsum;
+  uint32_t acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (uint32_t k = 0; k < d; k++) mac_wide(acc, r[(uint64_t)k * rest + i], lam[k]);
+  const Fe next = Fp::canon(Fp::redc(acc));
+  rn[(uint64_t)o * rest + i] = next;
+  if (!q) return;
+  Fe* qo = q + o * qstride;
+  const int s = sj[o];
+  for (uint32_t k = 0; k < d; k++) {
+    const uint64_t pos = (uint64_t)k * rest + i;
+    if ((int)k == s) {
+      uint32_t dacc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+      for (uint32_t u = 0; u < d; u++) mac_wide(dacc, r[(uint64_t)u * rest + i], der[u]);
+      qo[pos] = Fp::canon(Fp::redc(dacc));
+    } else {
+      qo[pos] = Fp::canon(Fp::mul(Fp::sub(r[pos], next), inv[k]));
+    }
+  }
+}
+
 // out[rest] = sum_k c[k, rest] x^k  (Horner along the leading axis of extent d)
 __global__ void k_horner_lead(const Fe* c, Fe* out, uint32_t d, uint64_t rest, Fe x_mont) {
   uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -282,6 +315,65 @@ int open_quotients_lagrange_device(tc_ctx* ctx, Fe* d_vals, const uint32_t* shap
     off += d;
   }
   TC_CUDA(ctx, cudaMemcpyAsync(h_y, r, sizeof(Fe), cudaMemcpyDeviceToHost, st));
+  TC_CUDA(ctx, cudaStreamSynchronize(st));
+  return TC_OK;
+}
+
+// open_quotients_lagrange_device for `cnt` openings at once: vals[o] (device), weights Ws[o];
+// opening o's quotient a goes to qouts + (o m + a) n; y[o] returned on the host
+int open_quotients_lagrange_batch(tc_ctx* ctx, const Fe* const* vals, int cnt, const uint32_t* shape, int m,
+                                  const std::vector<LagW>& Ws, Fe* qouts, Fe* h_y, bool skip_q0) {
+  cudaStream_t st = ctx->stream;
+  uint64_t n = 1;
+  uint32_t dsum = 0;
+  for (int j = 0; j < m; j++) n *= shape[j], dsum += shape[j];
+  const uint64_t tstride = 3 * (uint64_t)dsum;
+  Fe *tabs, *bufA, *bufB;
+  int* d_sj;
+  const Fe** d_rin;
+  TC_TRY(scratch_t(ctx, "openb.tabs", tstride * cnt, &tabs));
+  TC_TRY(scratch_t(ctx, "openb.sj", (uint64_t)m * cnt, &d_sj));
+  TC_TRY(scratch_t(ctx, "openb.rin", (uint64_t)m * cnt, (Fe***)&d_rin));
+  TC_TRY(scratch_t(ctx, "openb.rA", (n / shape[0]) * cnt + 1, &bufA));
+  TC_TRY(scratch_t(ctx, "openb.rB", (m > 1 ? n / shape[0] / shape[1] : 1) * cnt + 1, &bufB));
+  // host tables: weights per opening, the sj of every (axis, opening), input pointers per axis
+  std::vector<Fe> th(tstride * cnt);
+  std::vector<int> sh((size_t)m * cnt);
+  std::vector<const Fe*> rin((size_t)m * cnt);
+  for (int o = 0; o < cnt; o++) {
+    memcpy(&th[o * tstride], Ws[o].lam.data(), dsum * sizeof(Fe));
+    memcpy(&th[o * tstride + dsum], Ws[o].inv.data(), dsum * sizeof(Fe));
+    memcpy(&th[o * tstride + 2 * dsum], Ws[o].der.data(), dsum * sizeof(Fe));
+    for (int a = 0; a < m; a++) sh[(size_t)a * cnt + o] = Ws[o].sj[a];
+  }
+  uint64_t span = n;
+  for (int a = 0; a < m; a++) {
+    const uint64_t rest_in = span;
+    for (int o = 0; o < cnt; o++)
+      rin[(size_t)a * cnt + o] = a == 0 ? vals[o] : ((a & 1) ? bufA : bufB) + (uint64_t)o * rest_in;
+    span /= shape[a];
+  }
+  // pageable sources: synchronous copies complete before the host vectors go away
+  TC_CUDA(ctx, cudaMemcpyAsync(tabs, th.data(), th.size() * sizeof(Fe), cudaMemcpyHostToDevice, st));
+  TC_CUDA(ctx, cudaMemcpyAsync(d_sj, sh.data(), sh.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  TC_CUDA(ctx, cudaMemcpyAsync(d_rin, rin.data(), rin.size() * sizeof(Fe*), cudaMemcpyHostToDevice, st));
+  span = n;
+  uint32_t off = 0;
+  for (int a = 0; a < m; a++) {
+    const uint32_t d = shape[a];
+    const uint64_t rest = span / d;
+    Fe* rn = (a & 1) ? bufB : bufA;   // r_{a+1}: A for odd a+1 ... (stream order keeps r_a intact)
+    Fe* q = (a == 0 && skip_q0) ? nullptr : qouts + (uint64_t)a * n;
+    k_open_axis_lag_b<<<blocks_for(rest * cnt, 128), 128, 0, st>>>(d_rin + (size_t)a * cnt, d, rest, tabs + off,
+                                                                   tstride, dsum, d_sj + (size_t)a * cnt, rn, q,
+                                                                   (uint64_t)m * n, (uint32_t)cnt);
+    TC_LAUNCHED(ctx);
+    span = rest;
+    off += d;
+  }
+  // y_o = r_m of opening o (one element each)
+  Fe* last = (m & 1) ? bufA : bufB;
+  TC_CUDA(ctx, cudaMemcpyAsync(h_y, last, cnt * sizeof(Fe), cudaMemcpyDeviceToHost, st));
   TC_CUDA(ctx, cudaStreamSynchronize(st));
   return TC_OK;
 }

@@ -1219,7 +1219,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   static const bool want_radix = getenv("TC_MSM_SORT") != nullptr;   // radix-sort layout (A/B)
   static const bool generic_digits = getenv("TC_MSM_GENERIC_DIGITS") != nullptr;
   static const uint64_t FP_MIN_N = getenv("TC_MSM_FP_MIN_N") ? strtoull(getenv("TC_MSM_FP_MIN_N"), nullptr, 10)
-                                                            : (1ull << 15);
+                                                            : (1ull << 18);
   bool vec_ok = (dtype == TC_DTYPE_F16 || dtype == TC_DTYPE_BF16 || dtype == TC_DTYPE_F32) && nbits <= 61 &&
                 !generic_digits && !want_radix && !want_bucketed;
   for (int l = 0; l < L && vec_ok; l++) vec_ok = ((uintptr_t)h_ptrs[l] & 15u) == 0;   // 16-byte vector loads
