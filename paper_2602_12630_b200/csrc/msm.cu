@@ -1423,7 +1423,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   }
 
   // 6. levels (a bucket holds <= n entries)
-  static const uint32_t T_ENV = getenv("TC_MSM_T") ? (uint32_t)atoi(getenv("TC_MSM_T")) : 32u;
+  static const uint32_t T_ENV = getenv("TC_MSM_T") ? (uint32_t)atoi(getenv("TC_MSM_T")) : 16u;   // sweep (config 3): 8 6.75, 12 6.66, 16 6.54, 24 6.60, 32 6.64 ms
   static const uint32_t T1_ENV = getenv("TC_MSM_T1") ? (uint32_t)atoi(getenv("TC_MSM_T1")) : 8u;
   const uint32_t T = (E >= (1u << 20)) ? T_ENV : (E >= (1u << 14) ? 16u : 8u);
   const uint32_t T1 = T1_ENV;
