@@ -292,7 +292,7 @@ int srs_build_points(tc_ctx* ctx, tc_srs* srs, const std::vector<Fe>& taus, bool
 // Edwards copies of every basis the Pippenger pipeline may read (built at setup, so the
 // shared read-only SRS is never mutated by a commit)
 int srs_build_edwards(tc_ctx* ctx, tc_srs* srs) {
-  const EdAff* e;
+  const EdPk* e;
   if (srs->n <= SMALL_MSM_MAX && !srs->sublag) return TC_OK;   // node SRSs use the table kernel
   if (srs->monomial) TC_TRY(tcrt::srs_edwards(ctx, srs, TC_SRS_MONOMIAL, &e));
   if (srs->lagrange) TC_TRY(tcrt::srs_edwards(ctx, srs, TC_SRS_LAGRANGE, &e));
@@ -645,7 +645,7 @@ int tc_open_quotients(tc_ctx* ctx, const uint32_t* d_coeffs, const uint32_t* sha
 
 int tc_msm(tc_ctx* ctx, const tc_srs* srs, int which, const uint32_t* d_scalars, uint64_t n, uint8_t* out43) {
   if (!ctx || !srs || !out43 || (n && !d_scalars)) return TC_ERR_ARGUMENT;
-  const EdAff* bases;
+  const EdPk* bases;
   TC_TRY(tcrt::srs_edwards(ctx, const_cast<tc_srs*>(srs), which, &bases));
   if (n > srs->n) return fail(ctx, TC_ERR_VALUE, "msm: %llu scalars for an srs of %llu elements",
                               (unsigned long long)n, (unsigned long long)srs->n);
@@ -675,7 +675,7 @@ static int msm_srs(tc_ctx* ctx, const tc_srs* srs, int which, int dtype, int sca
   if (!((which == TC_SRS_LAGRANGE) ? srs->lagrange : srs->monomial))
     return fail(ctx, TC_ERR_VALUE, "srs has no elements of kind %d", which);
   if (srs->n > SMALL_MSM_MAX) {
-    const EdAff* bases;
+    const EdPk* bases;
     TC_TRY(tcrt::srs_edwards(ctx, const_cast<tc_srs*>(srs), which, &bases));
     return tcrt::msm_batch_device(ctx, dtype, scale_bits, ptrs, L, bases, srs->n, d_out);
   }
@@ -893,12 +893,12 @@ static const std::pair<std::vector<Fe>, std::vector<Fe>>& bary_weights(uint32_t 
 // MSM of canonical F_p scalars (opening quotients) over an SRS base range: through the
 // range's fixed-base window table (one shared bucket window, no Horner chain; built on first
 // use) when the table fits the budget, else the windowed Pippenger pipeline.
-static int msm_quotients(tc_ctx* ctx, const tc_srs* srs, const void* const* ptrs, int L, const EdAff* bases,
+static int msm_quotients(tc_ctx* ctx, const tc_srs* srs, const void* const* ptrs, int L, const EdPk* bases,
                          uint64_t n, Aff* d_out) {
   static const uint64_t BUDGET = getenv("TC_WINTAB_MB") ? strtoull(getenv("TC_WINTAB_MB"), nullptr, 10) << 20
                                                         : (4096ull << 20);
-  if (n * tcrt::FB_NDIG * sizeof(EdAff) <= BUDGET) {
-    const EdAff* tab;
+  if (n * tcrt::FB_NDIG * sizeof(EdPk) <= BUDGET) {
+    const EdPk* tab;
     TC_TRY(tcrt::srs_window_table(ctx, const_cast<tc_srs*>(srs), bases, n, &tab));
     return tcrt::msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, ptrs, L, tab, n, d_out, nullptr, true);
   }
@@ -988,11 +988,11 @@ int tc_open(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int sca
     Aff* d_out;
     TC_TRY(tcrt::scratch_t(ctx, "open.out", (uint64_t)m, &d_out));
     uint64_t span = n;
-    const EdAff *ed_lag, *ed_sub = nullptr;
+    const EdPk *ed_lag, *ed_sub = nullptr;
     TC_TRY(tcrt::srs_edwards(ctx, const_cast<tc_srs*>(srs), TC_SRS_LAGRANGE, &ed_lag));
     if (m > 1) TC_TRY(tcrt::srs_edwards(ctx, const_cast<tc_srs*>(srs), 0, &ed_sub));
     for (int a = 0; a < m; a++) {
-      const EdAff* bases = a == 0 ? ed_lag : ed_sub + srs->sublag_off[a];
+      const EdPk* bases = a == 0 ? ed_lag : ed_sub + srs->sublag_off[a];
       const void* ptr = qs + (uint64_t)a * n;
       TC_TRY(msm_quotients(ctx, srs, &ptr, 1, bases, span, d_out + a));
       span /= srs->shape[a];
@@ -1048,7 +1048,7 @@ int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int 
                      out_y21 + 21 * (size_t)i, out_pi43 + 43 * (size_t)i * m));
   }
   if (lag.empty()) return TC_OK;
-  const EdAff *ed_lag, *ed_sub = nullptr;
+  const EdPk *ed_lag, *ed_sub = nullptr;
   TC_TRY(tcrt::srs_edwards(ctx, const_cast<tc_srs*>(srs), TC_SRS_LAGRANGE, &ed_lag));
   if (m > 1) TC_TRY(tcrt::srs_edwards(ctx, const_cast<tc_srs*>(srs), 0, &ed_sub));
   size_t esz = 0;
@@ -1080,7 +1080,7 @@ int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int 
 
   Fe *qall, *sc = nullptr;
   Aff *d_out, *hpts = nullptr;
-  EdAff* hed = nullptr;
+  EdPk* hed = nullptr;
   TC_TRY(tcrt::scratch_t(ctx, "openb.q", (uint64_t)G * m * n, &qall));
   TC_TRY(tcrt::scratch_t(ctx, "openb.out", (uint64_t)G * m, &d_out));
   std::vector<uint8_t> enc((size_t)G * m * 43);
@@ -1149,7 +1149,7 @@ int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int 
           for (int k = 0; k < gc; k++) ptrs[k] = sc + (uint64_t)k * nh;
           TC_TRY(tcrt::msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, ptrs.data(), gc, hed, nh, d_out));
         } else {
-          const EdAff* bases = a == 0 ? ed_lag : ed_sub + srs->sublag_off[a];
+          const EdPk* bases = a == 0 ? ed_lag : ed_sub + srs->sublag_off[a];
           for (int k = 0; k < gc; k++) ptrs[k] = qall + ((uint64_t)k * m + a) * n;
           TC_TRY(msm_quotients(ctx, srs, ptrs.data(), gc, bases, span,
                                         d_out + (uint64_t)a * gc));

@@ -741,7 +741,7 @@ __device__ __forceinline__ uint32_t find_bucket(const uint32_t* off, uint32_t nb
 #ifndef TC_ACCUM_MINB
 #define TC_ACCUM_MINB 6   // min resident blocks per SM for k_accum_aff: caps registers at 80 (A/B: 1 -> 4.72 ms @104 regs, 6 -> 4.40 ms, 7 -> 4.52, 8 -> 4.51)
 #endif
-__global__ void __launch_bounds__(128, TC_ACCUM_MINB) k_accum_aff(const uint32_t* vals, const EdAff* bases, const uint32_t* bstart,
+__global__ void __launch_bounds__(128, TC_ACCUM_MINB) k_accum_aff(const uint32_t* vals, const EdPk* bases, const uint32_t* bstart,
                                                    const uint32_t* bend, const uint32_t* toff, const uint32_t* ooff,
                                                    uint32_t nb, uint32_t T, Ext* items, Ext* buckets,
                                                    const uint32_t* boff, uint32_t nbm) {
@@ -754,12 +754,12 @@ __global__ void __launch_bounds__(128, TC_ACCUM_MINB) k_accum_aff(const uint32_t
   uint32_t a = bstart[k] + piece * T;
   uint32_t b = min(a + T, bend[k]);
   uint32_t v = vals[a];
-  EdAff q = ld_edaff(bases + (v & ~SIGN_BIT));
+  EdAff q = ld_edpk(bases + (v & ~SIGN_BIT));
   if (v & SIGN_BIT) q = edaff_neg(q);
   Ext acc = ext_from_aff(q);
   for (uint32_t j = a + 1; j < b; j++) {
     v = vals[j];
-    q = ld_edaff(bases + (v & ~SIGN_BIT));
+    q = ld_edpk(bases + (v & ~SIGN_BIT));
     if (v & SIGN_BIT) q = edaff_neg(q);
     ext_madd(acc, q);
   }
@@ -1130,7 +1130,7 @@ namespace tcrt {
 
 int quantize_flags_to_status(tc_ctx* ctx, uint32_t f);
 
-int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* h_ptrs, int L, const EdAff* d_bases,
+int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* h_ptrs, int L, const EdPk* d_bases,
                      uint64_t n, Aff* d_out, const uint32_t* h_boff, bool fbw) {
   if (fbw && (dtype != TC_DTYPE_FP_LIMBS || n * FB_NDIG >= (1ull << 31)))
     return fail(ctx, TC_ERR_VALUE, "msm: window-table MSMs take field-element scalars, < 2^31 table points");
@@ -1606,7 +1606,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   return TC_OK;
 }
 
-int msm_device(tc_ctx* ctx, ScalarKind kind, const void* d_scalars, const EdAff* d_bases, uint64_t n, Aff* d_out) {
+int msm_device(tc_ctx* ctx, ScalarKind kind, const void* d_scalars, const EdPk* d_bases, uint64_t n, Aff* d_out) {
   if (kind != SCALAR_FP_CANON) return fail(ctx, TC_ERR_ARGUMENT, "msm: scalar kind");
   const void* ptrs[1] = {d_scalars};
   return msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, ptrs, 1, d_bases, n, d_out);

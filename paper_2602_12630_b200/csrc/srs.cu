@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(128) k_fixed(const Aff* table, const Fe* exps,
 }
 
 // Montgomery (u, v) -> Edwards (x, y, t): FB_K points per thread share one inversion
-__global__ void __launch_bounds__(128) k_to_edwards(const Aff* in, uint64_t n, EdAff* out) {
+__global__ void __launch_bounds__(128) k_to_edwards(const Aff* in, uint64_t n, EdPk* out) {
   uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   uint64_t i0 = t * FB_K;
   if (i0 >= n) return;
@@ -122,13 +122,13 @@ __global__ void __launch_bounds__(128) k_to_edwards(const Aff* in, uint64_t n, E
     const Fe ik = Fq::mul(inv, pref[k]);
     inv = Fq::mul(inv, den);
     EdAff e = aff_to_ed_with_inv(p, ik);
-    out[i0 + k] = EdAff{Fq::red2(e.x), Fq::red2(e.y), Fq::red2(e.t)};
+    out[i0 + k] = pack_ed(e);
   }
 }
 
 // out[i] = 2^c in[i] (Edwards affine with t = xy): c doublings in extended coordinates, the
 // Z of FB_K points per thread inverted with one shared inversion
-__global__ void __launch_bounds__(128) k_win_step(const EdAff* in, uint64_t n, int c, EdAff* out) {
+__global__ void __launch_bounds__(128) k_win_step(const EdPk* in, uint64_t n, int c, EdPk* out) {
   uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   uint64_t i0 = t * FB_K;
   if (i0 >= n) return;
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(128) k_win_step(const EdAff* in, uint64_t n, i
   Fe pref[FB_K];
   Fe run = Fq::one();
   for (int k = 0; k < cnt; k++) {
-    Ext e = ext_from_aff(ld_edaff(in + i0 + k));
+    Ext e = ext_from_aff(ld_edpk(in + i0 + k));
     for (int j = 0; j < c; j++) e = ext_dbl(e);
     pts[k] = e;
     pref[k] = run;
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(128) k_win_step(const EdAff* in, uint64_t n, i
     const Fe iz = Fq::mul(inv, pref[k]);
     inv = Fq::mul(inv, pts[k].Z);
     const Fe x = Fq::mul(pts[k].X, iz), y = Fq::mul(pts[k].Y, iz);
-    out[i0 + k] = EdAff{Fq::red2(x), Fq::red2(y), Fq::red2(Fq::mul(x, y))};
+    out[i0 + k] = pack_ed(EdAff{x, y, Fq::mul(x, y)});
   }
 }
 
@@ -156,16 +156,16 @@ __global__ void __launch_bounds__(128) k_win_step(const EdAff* in, uint64_t n, i
 
 namespace tcrt {
 
-int srs_window_table(tc_ctx* ctx, tc_srs* srs, const EdAff* bases, uint64_t n, const EdAff** out) {
+int srs_window_table(tc_ctx* ctx, tc_srs* srs, const EdPk* bases, uint64_t n, const EdPk** out) {
   auto it = srs->wintab.find(bases);
   if (it != srs->wintab.end()) {
     *out = it->second;
     return TC_OK;
   }
-  EdAff* tab = nullptr;
-  if (cudaMalloc(&tab, std::max<uint64_t>(n, 1) * FB_NDIG * sizeof(EdAff)) != cudaSuccess)
+  EdPk* tab = nullptr;
+  if (cudaMalloc(&tab, std::max<uint64_t>(n, 1) * FB_NDIG * sizeof(EdPk)) != cudaSuccess)
     return fail(ctx, TC_ERR_MEMORY, "window table alloc (%llu points)", (unsigned long long)(n * FB_NDIG));
-  TC_CUDA(ctx, cudaMemcpyAsync(tab, bases, n * sizeof(EdAff), cudaMemcpyDeviceToDevice, ctx->stream));
+  TC_CUDA(ctx, cudaMemcpyAsync(tab, bases, n * sizeof(EdPk), cudaMemcpyDeviceToDevice, ctx->stream));
   for (int w = 1; w < FB_NDIG; w++) {
     k_win_step<<<blocks_for((n + FB_K - 1) / FB_K, 128), 128, 0, ctx->stream>>>(tab + (w - 1) * n, n, FB_C,
                                                                                 tab + w * n);
@@ -176,16 +176,16 @@ int srs_window_table(tc_ctx* ctx, tc_srs* srs, const EdAff* bases, uint64_t n, c
   return TC_OK;
 }
 
-int to_edwards_device(tc_ctx* ctx, const Aff* d_in, uint64_t n, EdAff* d_out) {
+int to_edwards_device(tc_ctx* ctx, const Aff* d_in, uint64_t n, EdPk* d_out) {
   if (n == 0) return TC_OK;
   k_to_edwards<<<blocks_for((n + FB_K - 1) / FB_K, 128), 128, 0, ctx->stream>>>(d_in, n, d_out);
   TC_LAUNCHED(ctx);
   return TC_OK;
 }
 
-int srs_edwards(tc_ctx* ctx, tc_srs* srs, int which, const EdAff** out) {
+int srs_edwards(tc_ctx* ctx, tc_srs* srs, int which, const EdPk** out) {
   const Aff* src;
-  EdAff** dst;
+  EdPk** dst;
   uint64_t n = srs->n;
   if (which == TC_SRS_LAGRANGE) {
     src = srs->lagrange, dst = &srs->ed_lagrange;
@@ -197,7 +197,7 @@ int srs_edwards(tc_ctx* ctx, tc_srs* srs, int which, const EdAff** out) {
   }
   if (!src) return fail(ctx, TC_ERR_VALUE, "srs has no elements of kind %d", which);
   if (!*dst) {
-    if (cudaMalloc(dst, std::max<uint64_t>(n, 1) * sizeof(EdAff)) != cudaSuccess) {
+    if (cudaMalloc(dst, std::max<uint64_t>(n, 1) * sizeof(EdPk)) != cudaSuccess) {
       *dst = nullptr;
       return fail(ctx, TC_ERR_MEMORY, "srs edwards alloc");
     }

@@ -64,12 +64,12 @@ struct tc_srs {
   // (commitments of the Lagrange-route opening quotients q_i, which live on axes i..m-1)
   tc::Aff* sublag = nullptr;
   // twisted Edwards copies (x, y, xy) of the bases the Pippenger MSM reads (lazily built)
-  tc::EdAff* ed_monomial = nullptr;
-  tc::EdAff* ed_lagrange = nullptr;
-  tc::EdAff* ed_sublag = nullptr;
+  tc::EdPk* ed_monomial = nullptr;
+  tc::EdPk* ed_lagrange = nullptr;
+  tc::EdPk* ed_sublag = nullptr;
   // fixed-base window tables for full-scalar MSMs (openings): for a base range B (key:
   // its first point), FB_NDIG copies 2^(FB_C w) B, w = 0..FB_NDIG-1 (built on first use)
-  std::map<const tc::EdAff*, tc::EdAff*> wintab;
+  std::map<const tc::EdPk*, tc::EdPk*> wintab;
   uint64_t sublag_off[TC_MAX_AXES] = {0};
 };
 
@@ -124,7 +124,7 @@ enum ScalarKind { SCALAR_FP_CANON = 0, SCALAR_I64 = 1 };
 
 // result = sum_k scalars[k] * bases[k]; bases are device affine points.  out_aff on device
 // (one Aff) receives the canonical-Montgomery affine result.
-int msm_device(tc_ctx* ctx, ScalarKind kind, const void* d_scalars, const tc::EdAff* d_bases,
+int msm_device(tc_ctx* ctx, ScalarKind kind, const void* d_scalars, const tc::EdPk* d_bases,
                uint64_t n, tc::Aff* d_out);
 
 // L MSMs over the same n bases in one pipeline: d_out[l] = sum_k s_l[k] * bases[k].
@@ -135,7 +135,7 @@ int msm_device(tc_ctx* ctx, ScalarKind kind, const void* d_scalars, const tc::Ed
 // fbw: d_bases is a fixed-base window table (srs_window_table, FB_NDIG * n points) and the
 // scalars are canonical F_p: every digit window shares ONE set of buckets (no Horner).
 int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* h_ptrs, int L,
-                     const tc::EdAff* d_bases, uint64_t n, tc::Aff* d_out, const uint32_t* h_boff = nullptr,
+                     const tc::EdPk* d_bases, uint64_t n, tc::Aff* d_out, const uint32_t* h_boff = nullptr,
                      bool fbw = false);
 
 // fixed-base windowed MSMs over canonical F_p scalars: digit windows of FB_C bits, FB_NDIG
@@ -143,13 +143,13 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
 constexpr int FB_C = 15;
 constexpr int FB_NDIG = 11;
 // the window table of the n bases starting at `bases` (FB_NDIG * n points), built once
-int srs_window_table(tc_ctx* ctx, tc_srs* srs, const tc::EdAff* bases, uint64_t n, const tc::EdAff** out);
+int srs_window_table(tc_ctx* ctx, tc_srs* srs, const tc::EdPk* bases, uint64_t n, const tc::EdPk** out);
 
 // Montgomery affine points -> twisted Edwards affine (x, y, t = x y), batched inversion
-int to_edwards_device(tc_ctx* ctx, const tc::Aff* d_in, uint64_t n, tc::EdAff* d_out);
+int to_edwards_device(tc_ctx* ctx, const tc::Aff* d_in, uint64_t n, tc::EdPk* d_out);
 // the Edwards copy of an SRS basis for the Pippenger pipeline (built on first use):
 // which = TC_SRS_MONOMIAL | TC_SRS_LAGRANGE, or 0 for the sub-grid Lagrange elements
-int srs_edwards(tc_ctx* ctx, tc_srs* srs, int which, const tc::EdAff** out);
+int srs_edwards(tc_ctx* ctx, tc_srs* srs, int which, const tc::EdPk** out);
 
 // L MSMs over a small SRS (n <= SMALL_MSM_MAX) with canonical F_p scalars, via per-point
 // byte-window tables built once per SRS (`which` = TC_SRS_MONOMIAL | TC_SRS_LAGRANGE)
