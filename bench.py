@@ -210,19 +210,22 @@ def cpu_reference(shape, layer0_q, coeffs, bases, cores, target_s=12.0):
 
 
 def cpu_sample_inputs(cfg, K=48):
-    """First K elements of layer 0: quantised values, GPU-interpolated coefficients and the
-    matching monomial SRS points (one-time setup, not timed)."""
-    import numpy as np
-    import torch
+    """CPU-only inputs of the reference-path sample (one-time setup, not timed, no GPU, so
+    the reference arm runs on any host): layer 0's quantised values, K interpolation
+    coefficients (uniform F_p elements — what the 162-bit monomial coefficients of these
+    activations look like; the timing of exp / mul does not depend on which ones) and K
+    curve points g^k."""
+    import random
 
-    import paper_2602_12630_b200 as tcb
+    import numpy as np
+
     from oracle import tc_oracle as O
     x = make_layers_host(CONFIGS[3], [0])[0].reshape(-1)
     q = O.quantize(x.astype(np.float64), 16)
-    srs, _ = tcb.setup_srs(CONFIGS[3]["shape"], b"tc-b200/config3", lagrange=False)
-    f = tcb.interpolate_lagrange(tcb.PrimeField(), tcb.quantize(torch.from_numpy(x).cuda()), srs.grid)
-    bases = srs.export_range(1, 0, K)
-    return q, list(f.coeffs[:K]), list(bases)
+    rng = random.Random(2602)
+    coeffs = [rng.randrange(O.P) for _ in range(K)]
+    bases = [O.ec_mul(O.G, k + 2) for k in range(K)]
+    return q, coeffs, bases
 
 
 # ------------------------------------------------------------------ main
