@@ -1190,6 +1190,17 @@ int tc_terkle_build(tc_ctx* ctx, const tc_srs* node_srs, const uint8_t* leaves_l
   TC_TRY(tcrt::scratch_t(ctx, "terkle.vals", cap, &d_vals));
   TC_TRY(tcrt::scratch_t(ctx, "terkle.out", cap / B, &d_out));
   bool lag = node_srs->lagrange != nullptr;
+  if (lag && B <= SMALL_MSM_MAX) {
+    // device-resident tree: one upload, L launches (hashing on the device), one readback
+    Aff* d_pts;
+    TC_TRY(tcrt::scratch_t(ctx, "terkle.pts", total_nodes, &d_pts));
+    // pageable source: the synchronous copy completes before `vals` goes away
+    TC_CUDA(ctx, cudaMemcpy(d_vals, vals.data(), cap * sizeof(Fe), cudaMemcpyHostToDevice));
+    TC_TRY(tcrt::terkle_device(ctx, const_cast<tc_srs*>(node_srs), d_vals, cap, (int)L, d_pts));
+    TC_TRY(fetch_encode_many(ctx, d_pts, (int)total_nodes, out_nodes43));
+    *inout_count = total_nodes;
+    return TC_OK;
+  }
   uint64_t written = 0;
   const uint8_t tag[] = {'t', 'e', 'r', 'k', 'l', 'e', '/', 'n', 'o', 'd', 'e'};
   for (uint64_t l = 0; l < L; l++) {

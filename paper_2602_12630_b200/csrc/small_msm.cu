@@ -6,6 +6,7 @@
 // built once per SRS, and one warp per MSM sums the <= 21*B table entries selected by the
 // scalar bytes (complete 8M mixed adds), reduces across lanes with shuffles and converts
 // to canonical Montgomery affine.
+#include "sha256.cuh"
 #include "tc_internal.cuh"
 
 using namespace tc;
@@ -81,9 +82,44 @@ __global__ void __launch_bounds__(128) k_small_msm(const Fe* const* ptrs, uint32
   }
 }
 
+// One Terkle level on the device: node u commits to vals[u B .. u B + B) (one warp per
+// node, the table kernel's sum), its canonical affine point goes to pts[u] and, for the
+// next level, hash_to_scalar(encode_elem(C_u), "terkle/node") to next[u] (canonical F_p,
+// backend.py:309-317, 346-348) — no host round trip between levels.
+__global__ void __launch_bounds__(128) k_terkle_level(const Fe* vals, uint32_t nodes, uint32_t B, const EdAff* tab,
+                                                      Aff* pts, Fe* next) {
+  const uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (u >= nodes) return;
+  const Fe* s = vals + (uint64_t)u * B;
+  Ext acc = ext_zero();
+  for (uint32_t kw = lane; kw < B * SW; kw += 32) {
+    const uint32_t k = kw / SW, w = kw % SW;
+    const uint32_t byte = (s[k].v[w >> 2] >> (8 * (w & 3))) & 0xffu;
+    if (byte) ext_madd(acc, ld_edaff(tab + (uint64_t)kw * SE + byte - 1));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    Ext other = shfl_ext(acc, o);
+    if (lane < (uint32_t)o) ext_add(acc, other);
+  }
+  if (lane == 0) {
+    Aff r = ext_to_aff(acc);
+    if (!aff_is_inf(r)) r = Aff{Fq::canon(r.x), Fq::canon(r.y)};
+    pts[u] = r;
+    if (next) {
+      uint8_t enc[43];
+      aff_encode43(r, enc);
+      const uint8_t tag[] = {'t', 'e', 'r', 'k', 'l', 'e', '/', 'n', 'o', 'd', 'e'};
+      next[u] = hash_to_scalar(enc, 43, tag, sizeof tag);
+    }
+  }
+}
+
 }  // namespace
 
 namespace tcrt {
+
 
 // build (once) the byte-window tables of the SRS's `which` elements
 static int small_tables(tc_ctx* ctx, tc_srs* srs, int which, const EdAff** out) {
@@ -121,6 +157,30 @@ int small_msm_device(tc_ctx* ctx, tc_srs* srs, int which, const void* const* h_p
   TC_LAUNCHED(ctx);
   // the pointer upload reads h_stage asynchronously: finish before h_stage is reused
   TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return TC_OK;
+}
+
+// The whole Terkle tree over `cap` (= B^L, zero-padded) canonical leaf values already on
+// the device: L launches, no host synchronisation between levels; node points (level by
+// level, bottom first) in d_pts.  Lagrange node SRS (grid values are the node tensor).
+int terkle_device(tc_ctx* ctx, tc_srs* srs, Fe* d_vals, uint64_t cap, int L, Aff* d_pts) {
+  const EdAff* tab;
+  TC_TRY(small_tables(ctx, srs, TC_SRS_LAGRANGE, &tab));
+  const uint32_t B = (uint32_t)srs->n;
+  Fe* cur = d_vals;
+  Fe* nxt;
+  TC_TRY(scratch_t(ctx, "terkle.next", cap / B + 1, &nxt));
+  uint64_t written = 0, width = cap;
+  for (int l = 0; l < L; l++) {
+    const uint32_t nodes = (uint32_t)(width / B);
+    Fe* out_vals = (l + 1 < L) ? (cur == d_vals ? nxt : d_vals) : nullptr;
+    k_terkle_level<<<blocks_for((uint64_t)nodes * 32, 128), 128, 0, ctx->stream>>>(cur, nodes, B, tab,
+                                                                                   d_pts + written, out_vals);
+    TC_LAUNCHED(ctx);
+    written += nodes;
+    width = nodes;
+    if (out_vals) cur = out_vals;
+  }
   return TC_OK;
 }
 

@@ -145,6 +145,10 @@ constexpr int FB_NDIG = 11;
 // the window table of the n bases starting at `bases` (FB_NDIG * n points), built once
 int srs_window_table(tc_ctx* ctx, tc_srs* srs, const tc::EdPk* bases, uint64_t n, const tc::EdPk** out);
 
+// Terkle tree on the device over cap = B^L zero-padded canonical leaves (Lagrange node SRS):
+// node points level by level (bottom first) into d_pts, no host round trip between levels
+int terkle_device(tc_ctx* ctx, tc_srs* srs, tc::Fe* d_vals, uint64_t cap, int L, tc::Aff* d_pts);
+
 // Montgomery affine points -> twisted Edwards affine (x, y, t = x y), batched inversion
 int to_edwards_device(tc_ctx* ctx, const tc::Aff* d_in, uint64_t n, tc::EdPk* d_out);
 // the Edwards copy of an SRS basis for the Pippenger pipeline (built on first use):
