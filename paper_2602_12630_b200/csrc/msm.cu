@@ -6,24 +6,25 @@
 // designates it the single performance hot-spot.  The prover runs many MSMs against one
 // SRS (32 layers per forward, m quotients per opening, 8 nodes per Terkle level), so the
 // whole batch goes through ONE pipeline:
-//   1. k_scan_bits    — histogram of the bit lengths of the centred scalar magnitudes +
-//                       quantisation errors (scalars are canonical F_p limbs, or raw floats
-//                       quantised on the fly: K1 is fused into the MSM)
-//   2. window plan    — (host) variable-width signed windows chosen from that histogram:
-//                       a DP minimising  #non-zero digits + kappa * #buckets.  Heavy-tailed
-//                       activations get a wide low window and a narrow high window, so most
-//                       elements contribute ONE bucket entry, not two.
-//   3. k_digits       — signed digits; only NON-ZERO digits are emitted, compacted per
-//                       block: key = l*nbm + base_w + |d|-1, value = point index | sign<<31
-//   4. radix sort     — (key, value) by bucket, CUB onesweep over the used key bits
-//   5. k_bounds       — [start, end) of every bucket
-//   6. levels         — load-balanced segmented reduction: buckets are cut into pieces of
+//   1. k_scan_bits(_v) — exact maximum bit length + quantisation errors of the scalars
+//                       (canonical F_p limbs, or raw floats quantised on the fly: K1 is
+//                       fused into the MSM), bit-length histogram on a sample
+//   2. window plan    — (host) mode 1 float-exponent groups for large fp16 / bf16 batches
+//                       (one bucket entry per element), mode 2 fixed-base digit windows over
+//                       a window table (opening quotients), else signed windows from a DP
+//                       over the histogram (#non-zero digits + kappa * #buckets)
+//   3. counting sort  — count entries per bucket (k_digits_fp / k_digits_v / k_count_digits,
+//                       RED atomics into 16 counter copies for mode 1), exclusive scan, and
+//                       scatter (point index | sign << 31) into bucket slices
+//   4. levels         — load-balanced segmented reduction: buckets are cut into pieces of
 //                       <= T entries (one thread per piece, extended twisted Edwards
-//                       accumulator, complete 8M mixed adds, ec.cuh); single-piece buckets
-//                       are final at once, multi-piece buckets (the heavy tail) feed
-//                       further levels of T1-way reduction
-//   7. k_bucket_reduce— per segment of buckets: sum_b b * B_b by running sums
-//   8. k_window_sum, k_final — segments -> window sums -> Horner over the windows -> affine
+//                       accumulator, complete 8M mixed adds with lazy reduction, ec.cuh);
+//                       single-piece buckets are final at once, multi-piece buckets (the
+//                       heavy tail) feed further levels of T1-way reduction
+//   5. weighting      — sum_j (mlo + j) B_j per window: recursive segmentation
+//                       (k_wsum_level / k_wsum_final), or one block per window for small
+//                       batches (k_wsum_block); k_final / k_final_sum combine the windows
+//                       and convert to canonical Montgomery affine
 // Affine outputs are canonical and the group is abelian, so any window layout, bucket
 // order or coordinate system reproduces the reference's bytes exactly.  The bases are the
 // SRS points mapped to the twisted Edwards model of the curve (tc_srs::ed_*, built once per
@@ -42,8 +43,6 @@ constexpr int DT_LIMBS = 0;   // template code for canonical F_p scalars
 constexpr int MAXW = 48;      // windows per scalar (>= ceil(163 / 4))
 constexpr int NHIST = 168;    // bit-length histogram bins
 constexpr uint32_t HIST_SAMPLE = 8;   // histogram taken on every 8th element (k_scan_bits)
-constexpr int DIG_EPT = 1;    // elements per thread in k_digits (8 measured 1.7x slower:
-                              // per-thread entry ranges break store coalescing)
 
 // mode 0: signed-digit windows (bits [off, off + width) of the magnitude; bucket j of
 //         window w holds digit j + 1).
@@ -141,87 +140,6 @@ __global__ void k_scan_bits(const void* const* ptrs, uint64_t n, int scale_bits,
   __syncthreads();
   for (int i = threadIdx.x; i < NHIST; i += blockDim.x)
     if (hist[i]) atomicAdd(out + 1 + i, hist[i]);
-}
-
-// signed digits of `mag` under plan P: emit(w, |d|, digit_negative) for non-zero digits
-template <class F>
-__device__ __forceinline__ void for_digits(const Fe& mag, const WinPlan& P, F&& emit) {
-  uint32_t carry = 0;
-  for (int w = 0; w < P.nwin; w++) {
-    const int c = P.width[w];
-    const uint32_t half = 1u << (c - 1), full = 1u << c;
-    uint32_t d = window_bits(mag, P.off[w], c) + carry;
-    bool dn = false;
-    if (d > half) {   // d - 2^c, carry into the next window
-      d = full - d;
-      dn = true;
-      carry = 1;
-    } else {
-      carry = 0;
-    }
-    if (d) emit(w, d, dn);
-  }
-}
-
-template <int DT>
-__global__ void __launch_bounds__(256) k_digits(const void* const* ptrs, uint64_t n, int scale_bits, WinPlan P,
-                                                uint32_t* keys, uint32_t* vals, uint32_t* count) {
-  __shared__ uint32_t warp_tot[8];
-  __shared__ uint32_t base;
-  const uint32_t l = blockIdx.y;
-  // DIG_EPT elements per thread (strided by the block size for coalescing): one global
-  // atomic per DIG_EPT*256 elements instead of per 256
-  const uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x * DIG_EPT + threadIdx.x;
-  const void* p = ptrs[l];
-  uint32_t f = 0, cnt = 0;
-#pragma unroll 1
-  for (int e = 0; e < DIG_EPT; e++) {
-    const uint64_t i = i0 + (uint64_t)e * blockDim.x;
-    if (i < n) {
-      Fe mag;
-      bool neg;
-      load_scalar<DT>(p, i, scale_bits, mag, neg, f);
-      for_digits(mag, P, [&](int, uint32_t, bool) { cnt++; });
-    }
-  }
-  // block-wide exclusive scan of cnt -> one atomic per block
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint32_t incl = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += t;
-  }
-  if (lane == 31) warp_tot[wid] = incl;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t s = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
-      uint32_t t = warp_tot[w];
-      warp_tot[w] = s;
-      s += t;
-    }
-    base = s ? atomicAdd(count, s) : 0u;
-  }
-  __syncthreads();
-  uint32_t pos = base + warp_tot[wid] + incl - cnt;
-  if (cnt) {
-    const uint32_t key0 = l * P.nbm;
-#pragma unroll 1
-    for (int e = 0; e < DIG_EPT; e++) {
-      const uint64_t i = i0 + (uint64_t)e * blockDim.x;
-      if (i < n) {
-        Fe mag;
-        bool neg;
-        load_scalar<DT>(p, i, scale_bits, mag, neg, f);
-        for_digits(mag, P, [&](int w, uint32_t d, bool dn) {
-          keys[pos] = key0 + P.base[w] + d - 1u;
-          vals[pos] = (uint32_t)i | ((neg != dn) ? SIGN_BIT : 0u);
-          pos++;
-        });
-      }
-    }
-  }
 }
 
 // ---- counting-sort layout (default): digits -> bucket counts -> scan -> scatter -------
@@ -572,134 +490,6 @@ __global__ void __launch_bounds__(256) k_digits_fp(const void* const* ptrs, uint
   }
 }
 
-// ---- bucket-major layout without a radix sort (few buckets per MSM) -------------------
-__device__ __forceinline__ uint32_t lanemask_lt() {
-  uint32_t m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
-
-// Pass A: one digit pass.  Per window, a warp reserves slots for its non-zero digits in
-// MSM l's private region (one atomic per warp) and lanes with equal bucket keys combine
-// their shared-memory histogram increments (__match_any_sync); the block's histogram is
-// flushed into the global per-bucket counts at the end.
-template <int DT>
-__global__ void __launch_bounds__(256) k_digits_hist(const void* const* ptrs, uint64_t n, int scale_bits, WinPlan P,
-                                                     uint32_t CH, uint64_t cap_l, uint32_t* keys, uint32_t* vals,
-                                                     uint32_t* lcount, uint32_t* gcount) {
-  extern __shared__ uint32_t hist[];   // P.nbm counters
-  const uint32_t l = blockIdx.y;
-  const uint64_t c0 = (uint64_t)blockIdx.x * CH;
-  const uint64_t c1 = (c0 + CH < n) ? c0 + CH : n;
-  const void* p = ptrs[l];
-  uint32_t* keys_l = keys + l * cap_l;
-  uint32_t* vals_l = vals + l * cap_l;
-  const uint32_t lane = threadIdx.x & 31, ltmask = lanemask_lt();
-  for (uint32_t b = threadIdx.x; b < P.nbm; b += blockDim.x) hist[b] = 0;
-  __syncthreads();
-  uint32_t f = 0;
-  for (uint64_t i0 = c0 + (threadIdx.x & ~31u); i0 < c1; i0 += blockDim.x) {   // warp-uniform trip count
-    const uint64_t i = i0 + lane;
-    const bool valid = i < c1;
-    Fe mag = Fp::zero();
-    bool neg = false;
-    if (valid) load_scalar<DT>(p, i, scale_bits, mag, neg, f);
-    uint32_t carry = 0;
-    for (int w = 0; w < P.nwin; w++) {
-      const int c = P.width[w];
-      const uint32_t half = 1u << (c - 1), full = 1u << c;
-      uint32_t d = window_bits(mag, P.off[w], c) + carry;
-      bool dn = false;
-      if (d > half) {
-        d = full - d;
-        dn = true;
-        carry = 1;
-      } else {
-        carry = 0;
-      }
-      const bool nz = valid && d != 0;
-      const uint32_t act = __ballot_sync(0xffffffffu, nz);
-      if (!act) continue;
-      uint32_t wbase = 0;
-      if (lane == (uint32_t)(__ffs(act) - 1)) wbase = atomicAdd(&lcount[l], (uint32_t)__popc(act));
-      wbase = __shfl_sync(0xffffffffu, wbase, __ffs(act) - 1);
-      if (nz) {
-        const uint32_t key = P.base[w] + d - 1u;
-        const uint32_t at = wbase + __popc(act & ltmask);
-        keys_l[at] = key;
-        vals_l[at] = (uint32_t)i | ((neg != dn) ? SIGN_BIT : 0u);
-        const uint32_t same = __match_any_sync(act, key);
-        if (lane == (uint32_t)(__ffs(same) - 1)) atomicAdd(&hist[key], (uint32_t)__popc(same));
-      }
-    }
-  }
-  if (f) atomicOr(lcount + gridDim.y, f);   // quantisation flags after the L counters
-  __syncthreads();
-  const uint32_t key0 = l * P.nbm;
-  for (uint32_t b = threadIdx.x; b < P.nbm; b += blockDim.x)
-    if (hist[b]) atomicAdd(&gcount[key0 + b], hist[b]);
-}
-
-// Pass B: a block takes a chunk of MSM l's entries, reserves a contiguous slice of every
-// bucket it touches (one global atomic per bucket) and scatters the values there (ranks
-// from warp-aggregated shared-memory atomics).  Order inside a bucket is arbitrary — EC
-// addition is commutative and the result canonical.
-__global__ void __launch_bounds__(256) k_scatter(const uint32_t* keys, const uint32_t* vals, uint64_t cap_l,
-                                                 const uint32_t* lcount, uint32_t CHB, uint32_t nbm,
-                                                 const uint32_t* bstart, uint32_t* gcursor, uint32_t* out) {
-  extern __shared__ uint32_t sh[];   // cnt[nbm], gpos[nbm]
-  uint32_t* cnt = sh;
-  uint32_t* gpos = sh + nbm;
-  const uint32_t l = blockIdx.y;
-  const uint32_t e0 = blockIdx.x * CHB, ecount = lcount[l];
-  if (e0 >= ecount) return;
-  const uint32_t e1 = min(e0 + CHB, ecount);
-  const uint32_t* keys_l = keys + l * cap_l;
-  const uint32_t* vals_l = vals + l * cap_l;
-  const uint32_t key0 = l * nbm, lane = threadIdx.x & 31, ltmask = lanemask_lt();
-  for (uint32_t b = threadIdx.x; b < nbm; b += blockDim.x) cnt[b] = 0;
-  __syncthreads();
-  for (uint32_t j0 = e0 + (threadIdx.x & ~31u); j0 < e1; j0 += blockDim.x) {
-    const uint32_t j = j0 + lane;
-    const bool valid = j < e1;
-    const uint32_t act = __ballot_sync(0xffffffffu, valid);
-    if (valid) {
-      const uint32_t key = keys_l[j];
-      const uint32_t same = __match_any_sync(act, key);
-      if (lane == (uint32_t)(__ffs(same) - 1)) atomicAdd(&cnt[key], (uint32_t)__popc(same));
-    }
-  }
-  __syncthreads();
-  for (uint32_t b = threadIdx.x; b < nbm; b += blockDim.x) {
-    const uint32_t c = cnt[b];
-    gpos[b] = c ? bstart[key0 + b] + atomicAdd(&gcursor[key0 + b], c) : 0u;
-  }
-  __syncthreads();
-  for (uint32_t j0 = e0 + (threadIdx.x & ~31u); j0 < e1; j0 += blockDim.x) {
-    const uint32_t j = j0 + lane;
-    const bool valid = j < e1;
-    const uint32_t act = __ballot_sync(0xffffffffu, valid);
-    if (valid) {
-      const uint32_t key = keys_l[j];
-      const uint32_t same = __match_any_sync(act, key);
-      const uint32_t leader = __ffs(same) - 1;
-      uint32_t b0 = 0;
-      if (lane == leader) b0 = atomicAdd(&gpos[key], (uint32_t)__popc(same));
-      b0 = __shfl_sync(same, b0, leader);
-      out[b0 + __popc(same & ltmask)] = vals_l[j];
-    }
-  }
-}
-
-__global__ void k_bounds(const uint32_t* keys, const uint32_t* count, uint32_t* bstart, uint32_t* bend) {
-  uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  uint32_t E = *count;
-  if (j >= E) return;
-  uint32_t k = keys[j];
-  if (j == 0 || keys[j - 1] != k) bstart[k] = (uint32_t)j;
-  if (j + 1 == E || keys[j + 1] != k) bend[k] = (uint32_t)j + 1u;
-}
-
 // level 0 piece counts: np[k] = ceil(size/T) (threads), npm[k] = np[k] if > 1 (items);
 // an empty bucket is set to the neutral element here (every other bucket is written by
 // the accumulation levels), so the bucket array needs no separate fill pass
@@ -786,50 +576,6 @@ __global__ void __launch_bounds__(128) k_accum_ext(const Ext* in, const uint32_t
     buckets[k] = acc;
   else
     out[ooff[k] + piece] = acc;
-}
-
-// segment s covers buckets [s*LS, (s+1)*LS) of the global bucket array (LS divides every
-// window's bucket count): sum_b (digit_b) * B_b with digit_b = b - base_w + 1
-__global__ void __launch_bounds__(128, 4) k_bucket_reduce(const Ext* buckets, WinPlan P, uint32_t nseg_total,
-                                                       uint32_t LS, Ext* segs) {
-  uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= nseg_total) return;
-  uint32_t g = s * LS;
-  uint32_t r = g % P.nbm;
-  int w = 0;
-  while (w + 1 < P.nwin && P.base[w + 1] <= r) w++;
-  uint32_t lo = r - P.base[w] + P.mlo[w] - 1;   // weight of the segment's first bucket minus 1
-  const Ext* bw = buckets + g;
-  Ext run = ext_zero(), sum = ext_zero();
-  for (int b = (int)LS - 1; b >= 0; b--) {
-    ext_add(run, bw[b]);
-    ext_add(sum, run);
-  }
-  if (lo) {   // sum_b (b + 1) B_b + lo * sum_b B_b
-    Ext extra = ext_mul_small(run, lo);
-    ext_add(sum, extra);
-  }
-  segs[s] = sum;
-}
-
-// one block per (msm, window): tree-sum the window's segments
-__global__ void __launch_bounds__(128) k_window_sum(const Ext* segs, WinPlan P, uint32_t LS, Ext* wsum) {
-  __shared__ Ext sh[128];
-  const uint32_t l = blockIdx.x / P.nwin, w = blockIdx.x % P.nwin;
-  const uint32_t s0 = (l * P.nbm + P.base[w]) / LS, s1 = (l * P.nbm + P.base[w + 1]) / LS;
-  Ext acc = ext_zero();
-  for (uint32_t s = s0 + threadIdx.x; s < s1; s += blockDim.x) ext_add(acc, segs[s]);
-  sh[threadIdx.x] = acc;
-  __syncthreads();
-  for (uint32_t st = blockDim.x / 2; st; st >>= 1) {
-    if (threadIdx.x < st) {
-      Ext a = sh[threadIdx.x];
-      ext_add(a, sh[threadIdx.x + st]);
-      sh[threadIdx.x] = a;
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) wsum[blockIdx.x] = sh[0];
 }
 
 // ---- weighted bucket sums A_g = sum_j (j+1) x_j by recursive segmentation ----------------
@@ -1004,8 +750,6 @@ __global__ void k_fill_inf(Aff* out, uint32_t L) {
   uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l < L) out[l] = aff_inf();
 }
-
-uint32_t bitlen_u32(uint32_t v) { return v ? 32u - __builtin_clz(v) : 0u; }
 
 // Window plan from the bit-length histogram.  Window w (bits [o, o+c)) holds a non-zero
 // digit roughly iff the magnitude has bit length > o (carries included), so it costs
@@ -1215,13 +959,11 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
 
   // 2. window plan: float-exponent groups for large fp16 / bf16 batches on the vectorised
   //    digit path, signed windows from the histogram DP otherwise
-  static const bool want_bucketed = getenv("TC_MSM_BUCKETED") != nullptr;
-  static const bool want_radix = getenv("TC_MSM_SORT") != nullptr;   // radix-sort layout (A/B)
   static const bool generic_digits = getenv("TC_MSM_GENERIC_DIGITS") != nullptr;
   static const uint64_t FP_MIN_N = getenv("TC_MSM_FP_MIN_N") ? strtoull(getenv("TC_MSM_FP_MIN_N"), nullptr, 10)
                                                             : (1ull << 18);
   bool vec_ok = (dtype == TC_DTYPE_F16 || dtype == TC_DTYPE_BF16 || dtype == TC_DTYPE_F32) && nbits <= 61 &&
-                !generic_digits && !want_radix && !want_bucketed;
+                !generic_digits;
   for (int l = 0; l < L && vec_ok; l++) vec_ok = ((uintptr_t)h_ptrs[l] & 15u) == 0;   // 16-byte vector loads
   const int fp_mb = dtype == TC_DTYPE_F16 ? 11 : (dtype == TC_DTYPE_BF16 ? 8 : 0);
   const bool fpmode = vec_ok && fp_mb && n >= FP_MIN_N && (int)nbits - fp_mb + 1 <= MAXW;
@@ -1231,196 +973,115 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   if (nb64 >= (1ull << 31)) return fail(ctx, TC_ERR_VALUE, "msm batch too large (%llu buckets)", (unsigned long long)nb64);
   const uint32_t nb = (uint32_t)nb64;
   const uint64_t cap = (uint64_t)L * n * (P.mode == 1 ? 1 : P.mode == 2 ? P.ndig : P.nwin);
-  const int end_bit = (int)bitlen_u32(nb - 1);
 
   // 3. non-zero digits, compacted
-  uint32_t *keys = nullptr, *vals, *keys2 = nullptr, *vals2 = nullptr;
+  uint32_t* vals;
   TC_TRY(scratch_t(ctx, "msm.vals", cap, &vals));
-  uint32_t* d_count = d_small + NHIST + 2;
   const uint32_t* svals;
   uint32_t *bstart, *bend;
   uint64_t E;
   bool have_maxb = false;   // exact largest bucket known (counting layout)
   uint32_t maxb = 0;
-  // Optional bucket-major layout by histogram + scatter instead of the radix sort
-  // (TC_MSM_BUCKETED=1).  Measured slower on config 3 (pass A 3.8 ms + scatter 2.8 ms vs
-  // digits 0.8 + onesweep 2.3 + bounds 0.4 ms): the per-layer slot counters and the
-  // __match_any_sync aggregation serialise; kept for small-bucket experiments.
-  const bool bucketed = want_bucketed && P.mode == 0 && (size_t)P.nbm * 8 <= 160 * 1024;
-  if (!bucketed && (!want_radix || P.mode == 2)) {
-    // counting-sort layout: count, scan, scatter (no keys stored, no radix passes)
-    uint32_t *cnt, *cursor;
-    static const uint32_t NC_ENV = getenv("TC_MSM_NC") ? (uint32_t)atoi(getenv("TC_MSM_NC")) : 16u;   // sweep: 1 9.04, 4 7.79, 8 7.53, 16 7.40, 32 7.37 ms
-    const uint32_t NC = P.mode == 1 ? std::max(1u, NC_ENV) : 1u;
-    const uint64_t ncnt = (uint64_t)nb * NC + 1;
-    if (ncnt >= (1ull << 31)) return fail(ctx, TC_ERR_VALUE, "msm: too many bucket counters");
-    uint32_t* S;
-    TC_TRY(scratch_t(ctx, "msm.bcount", ncnt, &cnt));
-    TC_TRY(scratch_t(ctx, "msm.bstart", (uint64_t)nb + 1, &bstart));
-    TC_TRY(scratch_t(ctx, "msm.cursor", ncnt, &cursor));
-    if (NC > 1) {
-      TC_TRY(scratch_t(ctx, "msm.bscan", ncnt, &S));
-    } else {
-      S = bstart;
-    }
-    TC_CUDA(ctx, cudaMemsetAsync(cnt, 0, ncnt * sizeof(uint32_t), st));
-    // fast path (k_digits_v) for fp16 / bf16 / fp32 with magnitudes below 2^62 and at most
-    // HOT_MAXW few-bucket windows; the generic kernel otherwise
-    HotPlan H{};
-    H.nhot = 0;
-    H.nhotb = 0;
-    bool fast = vec_ok;
-    for (int w = 0; w < MAXW; w++) H.slot[w] = -1;
-    for (int w = 0; w < P.nwin && P.mode == 0; w++) {
-      H.slot[w] = -1;
-      const uint32_t nbw = 1u << (P.width[w] - 1);
-      if (nbw <= HOT_BUCKETS) {
-        if (H.nhot == HOT_MAXW || H.nhotb + nbw > HOT_MAXB) {
-          fast = false;
-          continue;
-        }
-        H.slot[w] = (int8_t)H.nhot;
-        H.win[H.nhot] = (uint8_t)w;
-        H.hbase[H.nhot] = (uint16_t)H.nhotb;
-        H.nhotb += nbw;
-        H.nhot++;
-      }
-    }
-    if (P.mode == 1 && !fast) return fail(ctx, TC_ERR_VALUE, "msm: float-exponent plan needs the vector path");
-    if (getenv("TC_MSM_DEBUG"))
-      fprintf(stderr, "[tc msm] L=%d n=%llu mode=%d groups=%d buckets/msm=%u\n", L, (unsigned long long)n, P.mode,
-              P.nwin, P.nbm);
-    const unsigned gxv = blocks_for(n, 256 * V_EPT);
-    const unsigned gx = std::min<unsigned>(blocks_for(n, 256), std::max(1u, (unsigned)ctx->num_sms * 16 / (unsigned)L + 1));
-    int s = dispatch_dt(ctx, dtype, [&](auto dt) {
-      constexpr int D = decltype(dt)::value;
-      if constexpr (D >= 1 && D <= 3) {
-        if (fast) {
-          if (P.mode == 1)
-            k_digits_fp<D, false><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cnt, nullptr, NC);
-          else
-            k_digits_v<D, false><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, H, cnt, nullptr, NC);
-          return;
-        }
-      }
-      k_count_digits<D, false><<<dim3(gx, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cnt, nullptr);
-    });
-    if (s) return s;
-    TC_LAUNCHED(ctx);
-    size_t sb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, sb, cnt, S, (int)ncnt, st);
-    void* d_sb;
-    TC_TRY(scratch(ctx, "msm.scantmp0", sb, &d_sb));
-    TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(d_sb, sb, cnt, S, (int)ncnt, st));
-    ctx->launches += 2;
-    if (NC > 1) {
-      k_copy_starts<<<blocks_for((uint64_t)nb + 1, 256), 256, 0, st>>>(S, nb, NC, bstart);
-      TC_LAUNCHED(ctx);
-    }
-    TC_CUDA(ctx, cudaMemcpyAsync(cursor, S, ncnt * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
-    TC_CUDA(ctx, cudaMemcpyAsync(h_small, S + (ncnt - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-    k_max_bucket<<<blocks_for(nb, 256), 256, 0, st>>>(bstart, nb, d_small + NHIST + 3);   // zeroed with d_small
-    TC_LAUNCHED(ctx);
-    TC_CUDA(ctx, cudaMemcpyAsync(h_small + 1, d_small + NHIST + 3, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-    have_maxb = true;
-    s = dispatch_dt(ctx, dtype, [&](auto dt) {
-      constexpr int D = decltype(dt)::value;
-      if constexpr (D >= 1 && D <= 3) {
-        if (fast) {
-          if (P.mode == 1)
-            k_digits_fp<D, true><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cursor, vals, NC);
-          else
-            k_digits_v<D, true><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, H, cursor, vals, NC);
-          return;
-        }
-      }
-      k_count_digits<D, true><<<dim3(gx, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cursor, vals);
-    });
-    if (s) return s;
-    TC_LAUNCHED(ctx);
-    TC_CUDA(ctx, cudaStreamSynchronize(st));
-    E = h_small[0];
-    maxb = h_small[1];
-    if (E == 0) {
-      k_fill_inf<<<blocks_for(L, 64), 64, 0, st>>>(d_out, (uint32_t)L);
-      TC_LAUNCHED(ctx);
-      return TC_OK;
-    }
-    svals = vals;
-    bend = bstart + 1;
-  } else if (bucketed) {
-    TC_TRY(scratch_t(ctx, "msm.keys", cap, &keys));
-    const uint32_t CH = 8192, CHB = 8192;
-    const uint64_t cap_l = n * P.nwin;
-    const uint32_t gx = (uint32_t)((n + CH - 1) / CH), gxb = (uint32_t)((cap_l + CHB - 1) / CHB);
-    uint32_t *lcount, *gcount, *gcursor, *sorted;
-    TC_TRY(scratch_t(ctx, "msm.lcount", (uint64_t)L + 1, &lcount));
-    TC_TRY(scratch_t(ctx, "msm.gcount", (uint64_t)nb + 1, &gcount));
-    TC_TRY(scratch_t(ctx, "msm.gcursor", (uint64_t)nb + 1, &gcursor));
-    TC_TRY(scratch_t(ctx, "msm.bstart", (uint64_t)nb + 1, &bstart));
-    TC_TRY(scratch_t(ctx, "msm.sorted", cap, &sorted));
-    TC_CUDA(ctx, cudaMemsetAsync(lcount, 0, ((uint64_t)L + 1) * sizeof(uint32_t), st));
-    TC_CUDA(ctx, cudaMemsetAsync(gcount, 0, ((uint64_t)nb + 1) * sizeof(uint32_t), st));
-    TC_CUDA(ctx, cudaMemsetAsync(gcursor, 0, ((uint64_t)nb + 1) * sizeof(uint32_t), st));
-    const size_t smemA = (size_t)P.nbm * 4, smemB = (size_t)P.nbm * 8;
-    int s = dispatch_dt(ctx, dtype, [&](auto dt) {
-      auto kern = k_digits_hist<decltype(dt)::value>;
-      if (smemA > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemA);
-      kern<<<dim3(gx, L), 256, smemA, st>>>(d_ptrs, n, scale_bits, P, CH, cap_l, keys, vals, lcount, gcount);
-    });
-    if (s) return s;
-    TC_LAUNCHED(ctx);
-    size_t sb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, sb, gcount, bstart, (int)(nb + 1), st);
-    void* d_sb;
-    TC_TRY(scratch(ctx, "msm.scantmp0", sb, &d_sb));
-    TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(d_sb, sb, gcount, bstart, (int)(nb + 1), st));
-    ctx->launches += 2;
-    if (smemB > 48 * 1024)
-      TC_CUDA(ctx, cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemB));
-    k_scatter<<<dim3(gxb, L), 256, smemB, st>>>(keys, vals, cap_l, lcount, CHB, P.nbm, bstart, gcursor, sorted);
-    TC_LAUNCHED(ctx);
-    svals = sorted;
-    bend = bstart + 1;   // bucket k = [bstart[k], bstart[k+1])
-    E = cap;             // upper bound (no host readback of the entry count)
+  // counting-sort layout: count, scan, scatter (no keys stored, no radix passes)
+  uint32_t *cnt, *cursor;
+  static const uint32_t NC_ENV = getenv("TC_MSM_NC") ? (uint32_t)atoi(getenv("TC_MSM_NC")) : 16u;   // sweep: 1 9.04, 4 7.79, 8 7.53, 16 7.40, 32 7.37 ms
+  const uint32_t NC = P.mode == 1 ? std::max(1u, NC_ENV) : 1u;
+  const uint64_t ncnt = (uint64_t)nb * NC + 1;
+  if (ncnt >= (1ull << 31)) return fail(ctx, TC_ERR_VALUE, "msm: too many bucket counters");
+  uint32_t* S;
+  TC_TRY(scratch_t(ctx, "msm.bcount", ncnt, &cnt));
+  TC_TRY(scratch_t(ctx, "msm.bstart", (uint64_t)nb + 1, &bstart));
+  TC_TRY(scratch_t(ctx, "msm.cursor", ncnt, &cursor));
+  if (NC > 1) {
+    TC_TRY(scratch_t(ctx, "msm.bscan", ncnt, &S));
   } else {
-    TC_TRY(scratch_t(ctx, "msm.keys", cap, &keys));
-    TC_TRY(scratch_t(ctx, "msm.keys2", cap, &keys2));
-    TC_TRY(scratch_t(ctx, "msm.vals2", cap, &vals2));
-    {
-      int s = dispatch_dt(ctx, dtype, [&](auto dt) {
-        k_digits<decltype(dt)::value><<<dim3(blocks_for(n, 256 * DIG_EPT), L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, keys,
-                                                                                    vals, d_count);
-      });
-      if (s) return s;
-      TC_LAUNCHED(ctx);
+    S = bstart;
+  }
+  TC_CUDA(ctx, cudaMemsetAsync(cnt, 0, ncnt * sizeof(uint32_t), st));
+  // fast path (k_digits_v) for fp16 / bf16 / fp32 with magnitudes below 2^62 and at most
+  // HOT_MAXW few-bucket windows; the generic kernel otherwise
+  HotPlan H{};
+  H.nhot = 0;
+  H.nhotb = 0;
+  bool fast = vec_ok;
+  for (int w = 0; w < MAXW; w++) H.slot[w] = -1;
+  for (int w = 0; w < P.nwin && P.mode == 0; w++) {
+    H.slot[w] = -1;
+    const uint32_t nbw = 1u << (P.width[w] - 1);
+    if (nbw <= HOT_BUCKETS) {
+      if (H.nhot == HOT_MAXW || H.nhotb + nbw > HOT_MAXB) {
+        fast = false;
+        continue;
+      }
+      H.slot[w] = (int8_t)H.nhot;
+      H.win[H.nhot] = (uint8_t)w;
+      H.hbase[H.nhot] = (uint16_t)H.nhotb;
+      H.nhotb += nbw;
+      H.nhot++;
     }
-    TC_CUDA(ctx, cudaMemcpyAsync(h_small, d_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-    TC_CUDA(ctx, cudaStreamSynchronize(st));
-    E = h_small[0];
-    if (E == 0) {
-      k_fill_inf<<<blocks_for(L, 64), 64, 0, st>>>(d_out, (uint32_t)L);
-      TC_LAUNCHED(ctx);
-      return TC_OK;
+  }
+  if (P.mode == 1 && !fast) return fail(ctx, TC_ERR_VALUE, "msm: float-exponent plan needs the vector path");
+  if (getenv("TC_MSM_DEBUG"))
+    fprintf(stderr, "[tc msm] L=%d n=%llu mode=%d groups=%d buckets/msm=%u\n", L, (unsigned long long)n, P.mode,
+            P.nwin, P.nbm);
+  const unsigned gxv = blocks_for(n, 256 * V_EPT);
+  const unsigned gx = std::min<unsigned>(blocks_for(n, 256), std::max(1u, (unsigned)ctx->num_sms * 16 / (unsigned)L + 1));
+  int s = dispatch_dt(ctx, dtype, [&](auto dt) {
+    constexpr int D = decltype(dt)::value;
+    if constexpr (D >= 1 && D <= 3) {
+      if (fast) {
+        if (P.mode == 1)
+          k_digits_fp<D, false><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cnt, nullptr, NC);
+        else
+          k_digits_v<D, false><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, H, cnt, nullptr, NC);
+        return;
+      }
     }
-    // 4. sort by bucket
-    size_t tmp_bytes = 0;
-    cub::DoubleBuffer<uint32_t> dk(keys, keys2), dv(vals, vals2);
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, dk, dv, (int)E, 0, end_bit, st);
-    void* d_tmp;
-    TC_TRY(scratch(ctx, "msm.cubtmp", tmp_bytes, &d_tmp));
-    TC_CUDA(ctx, cub::DeviceRadixSort::SortPairs(d_tmp, tmp_bytes, dk, dv, (int)E, 0, end_bit, st));
-    ctx->launches += 1 + (end_bit + 7) / 8;
-    const uint32_t* skeys = dk.Current();
-    svals = dv.Current();
-    // 5. bucket bounds
-    TC_TRY(scratch_t(ctx, "msm.bstart", (uint64_t)nb + 1, &bstart));
-    TC_TRY(scratch_t(ctx, "msm.bend", (uint64_t)nb + 1, &bend));
-    TC_CUDA(ctx, cudaMemsetAsync(bstart, 0, ((uint64_t)nb + 1) * sizeof(uint32_t), st));
-    TC_CUDA(ctx, cudaMemsetAsync(bend, 0, ((uint64_t)nb + 1) * sizeof(uint32_t), st));
-    k_bounds<<<blocks_for(E, 256), 256, 0, st>>>(skeys, d_count, bstart, bend);
+    k_count_digits<D, false><<<dim3(gx, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cnt, nullptr);
+  });
+  if (s) return s;
+  TC_LAUNCHED(ctx);
+  size_t sb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, sb, cnt, S, (int)ncnt, st);
+  void* d_sb;
+  TC_TRY(scratch(ctx, "msm.scantmp0", sb, &d_sb));
+  TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(d_sb, sb, cnt, S, (int)ncnt, st));
+  ctx->launches += 2;
+  if (NC > 1) {
+    k_copy_starts<<<blocks_for((uint64_t)nb + 1, 256), 256, 0, st>>>(S, nb, NC, bstart);
     TC_LAUNCHED(ctx);
   }
+  TC_CUDA(ctx, cudaMemcpyAsync(cursor, S, ncnt * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+  TC_CUDA(ctx, cudaMemcpyAsync(h_small, S + (ncnt - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  k_max_bucket<<<blocks_for(nb, 256), 256, 0, st>>>(bstart, nb, d_small + NHIST + 3);   // zeroed with d_small
+  TC_LAUNCHED(ctx);
+  TC_CUDA(ctx, cudaMemcpyAsync(h_small + 1, d_small + NHIST + 3, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  have_maxb = true;
+  s = dispatch_dt(ctx, dtype, [&](auto dt) {
+    constexpr int D = decltype(dt)::value;
+    if constexpr (D >= 1 && D <= 3) {
+      if (fast) {
+        if (P.mode == 1)
+          k_digits_fp<D, true><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cursor, vals, NC);
+        else
+          k_digits_v<D, true><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, H, cursor, vals, NC);
+        return;
+      }
+    }
+    k_count_digits<D, true><<<dim3(gx, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cursor, vals);
+  });
+  if (s) return s;
+  TC_LAUNCHED(ctx);
+  TC_CUDA(ctx, cudaStreamSynchronize(st));
+  E = h_small[0];
+  maxb = h_small[1];
+  if (E == 0) {
+    k_fill_inf<<<blocks_for(L, 64), 64, 0, st>>>(d_out, (uint32_t)L);
+    TC_LAUNCHED(ctx);
+    return TC_OK;
+  }
+  svals = vals;
+  bend = bstart + 1;
 
   // 6. levels (a bucket holds <= n entries)
   static const uint32_t T_ENV = getenv("TC_MSM_T") ? (uint32_t)atoi(getenv("TC_MSM_T")) : 16u;   // sweep (config 3): 8 6.75, 12 6.66, 16 6.54, 24 6.60, 32 6.64 ms
@@ -1470,11 +1131,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     auto& s = ctx->stats["msm.accumulate"];
     s.ms += ms;
     s.launches += 1;
-    // entries actually accumulated (the bucketed path only has the capacity bound on the
-    // host; its bucket starts are an exclusive scan, so bstart[nb] is the true count)
-    uint32_t e_true = (uint32_t)E;
-    if (bucketed) TC_CUDA(ctx, cudaMemcpy(&e_true, bstart + nb, sizeof(uint32_t), cudaMemcpyDeviceToHost));
-    s.units += (double)e_true;
+    s.units += (double)E;   // bucket entries accumulated
   }
   uint64_t items_bound = max_items;
   for (int lv = 1; lv < levels; lv++) {
@@ -1493,7 +1150,6 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
 
   // 7-8. bucket reduction, window sums, Horner, affine
   const uint32_t nw_total = (uint32_t)L * P.nwin;
-  static const bool old_reduce = getenv("TC_MSM_RUNSUM") != nullptr;
   static const uint32_t SEG_LG = getenv("TC_MSM_SEG_LG") ? (uint32_t)atoi(getenv("TC_MSM_SEG_LG")) : 3u;
   const uint32_t SEG = 1u << SEG_LG;
   uint32_t maxw = 0;
@@ -1503,7 +1159,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   // batches keep the level recursion, which has more parallelism (measured: 4 layers
   // 1.58 -> 1.51 ms per step, 32 layers 7.01 -> 7.11 ms with the block kernel)
   static const uint32_t WB_MAXG = getenv("TC_WB_MAXG") ? (uint32_t)atoi(getenv("TC_WB_MAXG")) : 256u;
-  if (!old_reduce && !no_block && maxw <= (uint32_t)WB_THREADS << WB_CHUNK_LG && nw_total <= WB_MAXG) {
+  if (!no_block && maxw <= (uint32_t)WB_THREADS << WB_CHUNK_LG && nw_total <= WB_MAXG) {
     Ext* wsum;
     TC_TRY(scratch_t(ctx, "msm.wsum", nw_total, &wsum));
     const size_t smem = 2 * WB_THREADS * sizeof(Ext);
@@ -1519,90 +1175,75 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     TC_LAUNCHED(ctx);
     return TC_OK;
   }
-  if (!old_reduce) {
-    // recursive segmentation (k_wsum_level): host builds all level tables, one upload
-    std::vector<uint32_t> cnt(nw_total), off(nw_total);
+  // recursive segmentation (k_wsum_level): host builds all level tables, one upload
+  std::vector<uint32_t> wcnt(nw_total), off(nw_total);
+  for (uint32_t g = 0; g < nw_total; g++) {
+    const uint32_t l = g / P.nwin, w = g % P.nwin;
+    wcnt[g] = P.base[w + 1] - P.base[w];
+    off[g] = l * P.nbm + P.base[w];
+  }
+  std::vector<uint32_t> tabs;   // per level: in_off[ng], in_cnt[ng], out_off[ng+1]
+  std::vector<uint32_t> totals;
+  bool more = true;
+  while (more) {
+    std::vector<uint32_t> oo(nw_total + 1);
+    uint32_t acc = 0;
+    more = false;
     for (uint32_t g = 0; g < nw_total; g++) {
-      const uint32_t l = g / P.nwin, w = g % P.nwin;
-      cnt[g] = P.base[w + 1] - P.base[w];
-      off[g] = l * P.nbm + P.base[w];
+      oo[g] = acc;
+      const uint32_t k = (wcnt[g] + SEG - 1) / SEG;
+      acc += k;
+      if (k > 1) more = true;
     }
-    std::vector<uint32_t> tabs;   // per level: in_off[ng], in_cnt[ng], out_off[ng+1]
-    std::vector<uint32_t> totals;
-    bool more = true;
-    while (more) {
-      std::vector<uint32_t> oo(nw_total + 1);
-      uint32_t acc = 0;
-      more = false;
-      for (uint32_t g = 0; g < nw_total; g++) {
-        oo[g] = acc;
-        const uint32_t k = (cnt[g] + SEG - 1) / SEG;
-        acc += k;
-        if (k > 1) more = true;
-      }
-      oo[nw_total] = acc;
-      tabs.insert(tabs.end(), off.begin(), off.end());
-      tabs.insert(tabs.end(), cnt.begin(), cnt.end());
-      tabs.insert(tabs.end(), oo.begin(), oo.end());
-      totals.push_back(acc);
-      for (uint32_t g = 0; g < nw_total; g++) {
-        off[g] = oo[g];
-        cnt[g] = oo[g + 1] - oo[g];
-      }
-    }
-    const uint32_t R = (uint32_t)totals.size();
-    const size_t tab_bytes = tabs.size() * sizeof(uint32_t);
-    const size_t stage_off = 256 * 1024;
-    if (tab_bytes + stage_off <= ctx->h_stage_bytes && R <= 9) {
-      uint32_t* d_tabs;
-      TC_TRY(scratch_t(ctx, "msm.wtabs", tabs.size(), &d_tabs));
-      memcpy((char*)ctx->h_stage + stage_off, tabs.data(), tab_bytes);
-      TC_CUDA(ctx, cudaMemcpyAsync(d_tabs, (char*)ctx->h_stage + stage_off, tab_bytes, cudaMemcpyHostToDevice, st));
-      Ext *TA, *TB, *DA, *DB, *wsum;
-      TC_TRY(scratch_t(ctx, "msm.wTA", totals[0] + 1, &TA));
-      TC_TRY(scratch_t(ctx, "msm.wTB", totals[0] + 1, &TB));
-      TC_TRY(scratch_t(ctx, "msm.wDA", totals[0] + 1, &DA));
-      TC_TRY(scratch_t(ctx, "msm.wDB", totals[0] + 1, &DB));
-      TC_TRY(scratch_t(ctx, "msm.wsum", nw_total, &wsum));
-      const uint32_t stride = 3 * nw_total + 1;
-      const Ext* Tin = buckets;
-      const Ext* Din = nullptr;
-      for (uint32_t r = 0; r < R; r++) {
-        GroupTab G{d_tabs + r * stride, d_tabs + r * stride + nw_total, d_tabs + r * stride + 2 * nw_total, nw_total};
-        Ext* To = (r & 1) ? TB : TA;
-        Ext* Do = (r & 1) ? DB : DA;
-        k_wsum_level<<<blocks_for(totals[r], 128), 128, 0, st>>>(Tin, Din, G, totals[r], SEG_LG * r, SEG, To, Do);
-        TC_LAUNCHED(ctx);
-        Tin = To;
-        Din = Do;
-      }
-      uint64_t p8 = 1;
-      for (uint32_t r = 0; r < R; r++) p8 *= SEG;
-      const uint32_t c = (uint32_t)((p8 - SEG) / (SEG - 1));
-      k_wsum_final<<<blocks_for(nw_total, 64), 64, 0, st>>>(Tin, Din, nw_total, c, P, wsum);
-      TC_LAUNCHED(ctx);
-      k_final<<<blocks_for(L, 32), 32, 0, st>>>(wsum, (uint32_t)L, P, d_out);
-      TC_LAUNCHED(ctx);
-      // the table upload reads h_stage asynchronously: finish before it can be reused
-      TC_CUDA(ctx, cudaStreamSynchronize(st));
-      return TC_OK;
+    oo[nw_total] = acc;
+    tabs.insert(tabs.end(), off.begin(), off.end());
+    tabs.insert(tabs.end(), wcnt.begin(), wcnt.end());
+    tabs.insert(tabs.end(), oo.begin(), oo.end());
+    totals.push_back(acc);
+    for (uint32_t g = 0; g < nw_total; g++) {
+      off[g] = oo[g];
+      wcnt[g] = oo[g + 1] - oo[g];
     }
   }
-  uint32_t minB = 1u << 30;
-  for (int w = 0; w < P.nwin; w++) minB = std::min<uint32_t>(minB, P.base[w + 1] - P.base[w]);
-  uint32_t LS = 32u;
-  while (LS > 2u && (uint64_t)nb / LS < (uint64_t)ctx->num_sms * 256u) LS >>= 1;
-  LS = std::min<uint32_t>(LS, minB);
-  const uint32_t nseg_total = nb / LS;
-  Ext *segs, *wsum;
-  TC_TRY(scratch_t(ctx, "msm.segs", nseg_total, &segs));
+  const uint32_t R = (uint32_t)totals.size();
+  if (R > 9) return fail(ctx, TC_ERR_VALUE, "msm: bucket window too large (%u levels)", R);   // SEG^R fits 32 bits
+  const size_t tab_bytes = tabs.size() * sizeof(uint32_t);
+  const size_t stage_off = 256 * 1024;
+  uint32_t* d_tabs;
+  TC_TRY(scratch_t(ctx, "msm.wtabs", tabs.size(), &d_tabs));
+  if (tab_bytes + stage_off <= ctx->h_stage_bytes) {
+    memcpy((char*)ctx->h_stage + stage_off, tabs.data(), tab_bytes);
+    TC_CUDA(ctx, cudaMemcpyAsync(d_tabs, (char*)ctx->h_stage + stage_off, tab_bytes, cudaMemcpyHostToDevice, st));
+  } else {   // very large batches: pageable, synchronous
+    TC_CUDA(ctx, cudaMemcpy(d_tabs, tabs.data(), tab_bytes, cudaMemcpyHostToDevice));
+  }
+  Ext *TA, *TB, *DA, *DB, *wsum;
+  TC_TRY(scratch_t(ctx, "msm.wTA", totals[0] + 1, &TA));
+  TC_TRY(scratch_t(ctx, "msm.wTB", totals[0] + 1, &TB));
+  TC_TRY(scratch_t(ctx, "msm.wDA", totals[0] + 1, &DA));
+  TC_TRY(scratch_t(ctx, "msm.wDB", totals[0] + 1, &DB));
   TC_TRY(scratch_t(ctx, "msm.wsum", nw_total, &wsum));
-  k_bucket_reduce<<<blocks_for(nseg_total, 128), 128, 0, st>>>(buckets, P, nseg_total, LS, segs);
-  TC_LAUNCHED(ctx);
-  k_window_sum<<<nw_total, 128, 0, st>>>(segs, P, LS, wsum);
+  const uint32_t stride = 3 * nw_total + 1;
+  const Ext* Tin = buckets;
+  const Ext* Din = nullptr;
+  for (uint32_t r = 0; r < R; r++) {
+    GroupTab G{d_tabs + r * stride, d_tabs + r * stride + nw_total, d_tabs + r * stride + 2 * nw_total, nw_total};
+    Ext* To = (r & 1) ? TB : TA;
+    Ext* Do = (r & 1) ? DB : DA;
+    k_wsum_level<<<blocks_for(totals[r], 128), 128, 0, st>>>(Tin, Din, G, totals[r], SEG_LG * r, SEG, To, Do);
+    TC_LAUNCHED(ctx);
+    Tin = To;
+    Din = Do;
+  }
+  uint64_t p8 = 1;
+  for (uint32_t r = 0; r < R; r++) p8 *= SEG;
+  const uint32_t c = (uint32_t)((p8 - SEG) / (SEG - 1));
+  k_wsum_final<<<blocks_for(nw_total, 64), 64, 0, st>>>(Tin, Din, nw_total, c, P, wsum);
   TC_LAUNCHED(ctx);
   k_final<<<blocks_for(L, 32), 32, 0, st>>>(wsum, (uint32_t)L, P, d_out);
   TC_LAUNCHED(ctx);
+  // the table upload reads h_stage asynchronously: finish before it can be reused
+  TC_CUDA(ctx, cudaStreamSynchronize(st));
   return TC_OK;
 }
 
