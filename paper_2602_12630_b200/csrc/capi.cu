@@ -897,10 +897,11 @@ static int msm_quotients(tc_ctx* ctx, const tc_srs* srs, const void* const* ptrs
                          uint64_t n, Aff* d_out) {
   static const uint64_t BUDGET = getenv("TC_WINTAB_MB") ? strtoull(getenv("TC_WINTAB_MB"), nullptr, 10) << 20
                                                         : (4096ull << 20);
-  if (n * tcrt::FB_NDIG * sizeof(EdPk) <= BUDGET) {
+  const int c = tcrt::fb_width(n);
+  if (n * tcrt::fb_ndig(c) * sizeof(EdPk) <= BUDGET) {
     const EdPk* tab;
     TC_TRY(tcrt::srs_window_table(ctx, const_cast<tc_srs*>(srs), bases, n, &tab));
-    return tcrt::msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, ptrs, L, tab, n, d_out, nullptr, true);
+    return tcrt::msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, ptrs, L, tab, n, d_out, nullptr, c);
   }
   return tcrt::msm_batch_device(ctx, TC_DTYPE_FP_LIMBS, 0, ptrs, L, bases, n, d_out);
 }

@@ -821,18 +821,18 @@ WinPlan plan_windows(const uint32_t* hist, uint32_t nbits, uint64_t L) {
 }
 
 // mode-2 plan: one window of 2^(c-1) buckets shared by all digit windows
-WinPlan plan_fb() {
+WinPlan plan_fb(int c) {
   WinPlan P;
   P.mode = 2;
   P.mbits = 0;
-  P.ndig = tcrt::FB_NDIG;
-  P.cdig = tcrt::FB_C;
+  P.ndig = tcrt::fb_ndig(c);
+  P.cdig = c;
   P.nwin = 1;
   P.off[0] = 0;
-  P.width[0] = (uint8_t)tcrt::FB_C;
+  P.width[0] = (uint8_t)c;
   P.mlo[0] = 1;
   P.base[0] = 0;
-  P.base[1] = P.nbm = 1u << (tcrt::FB_C - 1);
+  P.base[1] = P.nbm = 1u << (c - 1);
   return P;
 }
 
@@ -875,8 +875,8 @@ namespace tcrt {
 int quantize_flags_to_status(tc_ctx* ctx, uint32_t f);
 
 int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* h_ptrs, int L, const EdPk* d_bases,
-                     uint64_t n, Aff* d_out, const uint32_t* h_boff, bool fbw) {
-  if (fbw && (dtype != TC_DTYPE_FP_LIMBS || n * FB_NDIG >= (1ull << 31)))
+                     uint64_t n, Aff* d_out, const uint32_t* h_boff, int fbw) {
+  if (fbw && (dtype != TC_DTYPE_FP_LIMBS || n * fb_ndig(fbw) >= (1ull << 31)))
     return fail(ctx, TC_ERR_VALUE, "msm: window-table MSMs take field-element scalars, < 2^31 table points");
   cudaStream_t st = ctx->stream;
   if (L <= 0) return TC_OK;
@@ -967,7 +967,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   for (int l = 0; l < L && vec_ok; l++) vec_ok = ((uintptr_t)h_ptrs[l] & 15u) == 0;   // 16-byte vector loads
   const int fp_mb = dtype == TC_DTYPE_F16 ? 11 : (dtype == TC_DTYPE_BF16 ? 8 : 0);
   const bool fpmode = vec_ok && fp_mb && n >= FP_MIN_N && (int)nbits - fp_mb + 1 <= MAXW;
-  const WinPlan P = fbw ? plan_fb() : fpmode ? plan_fp(nbits, fp_mb) : plan_windows(hist, nbits, (uint64_t)L);
+  const WinPlan P = fbw ? plan_fb(fbw) : fpmode ? plan_fp(nbits, fp_mb) : plan_windows(hist, nbits, (uint64_t)L);
   if (P.nwin > MAXW) return fail(ctx, TC_ERR_VALUE, "msm: window plan too long");
   const uint64_t nb64 = (uint64_t)L * P.nbm;
   if (nb64 >= (1ull << 31)) return fail(ctx, TC_ERR_VALUE, "msm batch too large (%llu buckets)", (unsigned long long)nb64);

@@ -162,12 +162,13 @@ int srs_window_table(tc_ctx* ctx, tc_srs* srs, const EdPk* bases, uint64_t n, co
     *out = it->second;
     return TC_OK;
   }
+  const int c = fb_width(n), nd = fb_ndig(c);
   EdPk* tab = nullptr;
-  if (cudaMalloc(&tab, std::max<uint64_t>(n, 1) * FB_NDIG * sizeof(EdPk)) != cudaSuccess)
-    return fail(ctx, TC_ERR_MEMORY, "window table alloc (%llu points)", (unsigned long long)(n * FB_NDIG));
+  if (cudaMalloc(&tab, std::max<uint64_t>(n, 1) * nd * sizeof(EdPk)) != cudaSuccess)
+    return fail(ctx, TC_ERR_MEMORY, "window table alloc (%llu points)", (unsigned long long)(n * nd));
   TC_CUDA(ctx, cudaMemcpyAsync(tab, bases, n * sizeof(EdPk), cudaMemcpyDeviceToDevice, ctx->stream));
-  for (int w = 1; w < FB_NDIG; w++) {
-    k_win_step<<<blocks_for((n + FB_K - 1) / FB_K, 128), 128, 0, ctx->stream>>>(tab + (w - 1) * n, n, FB_C,
+  for (int w = 1; w < nd; w++) {
+    k_win_step<<<blocks_for((n + FB_K - 1) / FB_K, 128), 128, 0, ctx->stream>>>(tab + (w - 1) * n, n, c,
                                                                                 tab + w * n);
     TC_LAUNCHED(ctx);
   }

@@ -132,17 +132,24 @@ int msm_device(tc_ctx* ctx, ScalarKind kind, const void* d_scalars, const tc::Ed
 // canonical limbs; float dtypes are quantised at scale_bits inside the digit kernel).
 // h_boff (optional, host, L entries): MSM l reads the bases d_bases + h_boff[l] (batches of
 // MSMs over different slices of one SRS, e.g. the opening slice commitments)
-// fbw: d_bases is a fixed-base window table (srs_window_table, FB_NDIG * n points) and the
-// scalars are canonical F_p: every digit window shares ONE set of buckets (no Horner).
+// fbw > 0: d_bases is a fixed-base window table of digit width fbw (srs_window_table,
+// fb_ndig(fbw) * n points) and the scalars are canonical F_p: every digit window shares ONE
+// set of buckets (no Horner).
 int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* h_ptrs, int L,
                      const tc::EdPk* d_bases, uint64_t n, tc::Aff* d_out, const uint32_t* h_boff = nullptr,
-                     bool fbw = false);
+                     int fbw = 0);
 
-// fixed-base windowed MSMs over canonical F_p scalars: digit windows of FB_C bits, FB_NDIG
-// of them (covers 162 bits + the final carry); see WinPlan mode 2 in msm.cu
-constexpr int FB_C = 15;
-constexpr int FB_NDIG = 11;
-// the window table of the n bases starting at `bases` (FB_NDIG * n points), built once
+// fixed-base windowed MSMs over canonical F_p scalars: digit windows of c bits, ndig(c) =
+// ceil(163 / c) of them (162 bits + the final carry); see WinPlan mode 2 in msm.cu.
+// c = 15 (2^14 buckets, 11 windows) for large ranges, 11 (2^10 buckets, 15 windows) for
+// small ones, whose MSMs are latency-bound: their one bucket window then fits the
+// single-launch block weighting
+constexpr int FB_C_LARGE = 15, FB_C_SMALL = 11;
+constexpr uint64_t FB_SMALL_N = 1ull << 18;
+inline int fb_width(uint64_t n) { return n >= FB_SMALL_N ? FB_C_LARGE : FB_C_SMALL; }
+inline int fb_ndig(int c) { return (163 + c - 1) / c; }
+// the window table of the n bases starting at `bases` (fb_ndig(c) * n points, c = fb_width(n)),
+// built once per SRS range
 int srs_window_table(tc_ctx* ctx, tc_srs* srs, const tc::EdPk* bases, uint64_t n, const tc::EdPk** out);
 
 // Terkle tree on the device over cap = B^L zero-padded canonical leaves (Lagrange node SRS):
