@@ -322,7 +322,8 @@ int open_quotients_lagrange_device(tc_ctx* ctx, Fe* d_vals, const uint32_t* shap
 // open_quotients_lagrange_device for `cnt` openings at once: vals[o] (device), weights Ws[o];
 // opening o's quotient a goes to qouts + (o m + a) n; y[o] returned on the host
 int open_quotients_lagrange_batch(tc_ctx* ctx, const Fe* const* vals, int cnt, const uint32_t* shape, int m,
-                                  const std::vector<LagW>& Ws, Fe* qouts, Fe* h_y, bool skip_q0) {
+                                  const std::vector<LagW>& Ws, Fe* qouts, Fe* h_y, bool skip_q0,
+                                  const uint64_t* qoff, const uint64_t* qstride) {
   cudaStream_t st = ctx->stream;
   uint64_t n = 1;
   uint32_t dsum = 0;
@@ -363,10 +364,12 @@ int open_quotients_lagrange_batch(tc_ctx* ctx, const Fe* const* vals, int cnt, c
     const uint32_t d = shape[a];
     const uint64_t rest = span / d;
     Fe* rn = (a & 1) ? bufB : bufA;   // r_{a+1}: A for odd a+1 ... (stream order keeps r_a intact)
-    Fe* q = (a == 0 && skip_q0) ? nullptr : qouts + (uint64_t)a * n;
+    // quotient a of opening o at qouts + qoff[a] + o qstride[a] (default: (o m + a) n)
+    Fe* q = (a == 0 && skip_q0) ? nullptr : qouts + (qoff ? qoff[a] : (uint64_t)a * n);
     k_open_axis_lag_b<<<blocks_for(rest * cnt, 128), 128, 0, st>>>(d_rin + (size_t)a * cnt, d, rest, tabs + off,
                                                                    tstride, dsum, d_sj + (size_t)a * cnt, rn, q,
-                                                                   (uint64_t)m * n, (uint32_t)cnt);
+                                                                   qstride ? qstride[a] : (uint64_t)m * n,
+                                                                   (uint32_t)cnt);
     TC_LAUNCHED(ctx);
     span = rest;
     off += d;

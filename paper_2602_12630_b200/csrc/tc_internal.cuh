@@ -201,7 +201,8 @@ int open_quotients_lagrange_device(tc_ctx* ctx, tc::Fe* d_vals, const uint32_t* 
 // the same for `cnt` openings in one launch per axis (opening o: vals[o], Ws[o], quotients at
 // qouts + o m n); h_y receives cnt values
 int open_quotients_lagrange_batch(tc_ctx* ctx, const tc::Fe* const* vals, int cnt, const uint32_t* shape, int m,
-                                  const std::vector<LagW>& Ws, tc::Fe* qouts, tc::Fe* h_y, bool skip_q0);
+                                  const std::vector<LagW>& Ws, tc::Fe* qouts, tc::Fe* h_y, bool skip_q0,
+                                  const uint64_t* qoff = nullptr, const uint64_t* qstride = nullptr);
 // s[o][c' d + c] = (delta_{c c'} - lam_o[c']) inv_o[c], or der_o[c'] in the column c = sj_o,
 // for `count` openings (tabs: per opening lam[d] ++ inv[d] ++ der[d], Montgomery form; sj per
 // opening, -1 off the grid) — the scalars of pi_0 over slice commitments
