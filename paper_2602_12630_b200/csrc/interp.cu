@@ -3,11 +3,15 @@
 // interpolate_device  — mvpoly.interpolate_lagrange (mvpoly.py:233-247): for each axis j the
 //   d_j x d_j matrix B_j (column l = monomial coefficients of the l-th Lagrange basis
 //   polynomial on nodes 1..d_j, mvpoly.py:193-218) is applied to every fibre along axis j
-//   (mvpoly.py:168-186).  A block stages FB whole fibres in shared memory; each output
-//   coefficient is a length-d_j dot product accumulated as full 384-bit products and
-//   Montgomery-reduced ONCE (sum < 4 d p^2 < p R for d < 2^28), so a MAC costs the 6x6
-//   product only.  B_j is kept in Montgomery form and the samples canonical, so the
-//   reduction lands directly on canonical coefficients.
+//   (mvpoly.py:168-186).  Axes with <= 128 nodes and enough fibres take the Newton form
+//   instead (k_interp_newton / k_interp_newton_w: forward differences, d divisions by k!,
+//   basis expansion by small-integer multiply-subtracts with the sparse-p fold) — the same
+//   unique interpolant at ~8x fewer wide multiplies.  Otherwise (k_interp_axis) a block
+//   stages FB whole fibres in shared memory; each output coefficient is a length-d_j dot
+//   product accumulated as full 384-bit products and Montgomery-reduced ONCE
+//   (sum < 4 d p^2 < p R for d < 2^28), so a MAC costs the 6x6 product only.  B_j is kept
+//   in Montgomery form and the samples canonical, so the reduction lands directly on
+//   canonical coefficients.
 // open_quotients_device — mvpoly.open_quotients (mvpoly.py:521-534) built from
 //   divide_by_linear (mvpoly.py:452-484): after dividing along axis a the remainder is
 //   independent of X_0..X_a, i.e. supported on the lex prefix of length prod_{t>a} d_t, so
@@ -81,6 +85,197 @@ __global__ void __launch_bounds__(256) k_interp_axis(Fe* data, const Fe* Bm, uin
     Fe r = Fp::canon(Fp::redc(acc));
     // every sample of this block was staged before any write, fibres are disjoint
     data[fibre_addr(f0 + fl, k, d, stride)] = r;
+  }
+}
+
+// a * s mod p for a < 2p, s < 2^20, canonical result.  p = 2^161 + 2^24 + 1 is sparse:
+// t = hi 2^161 + lo  ==  lo - hi (2^24 + 1)  with lo < 2^161 < p and hi (2^24+1) < 2^45,
+// so one borrow-corrected subtraction lands in [0, p) — 6 IMAD.WIDE and no Montgomery step.
+__device__ __forceinline__ Fe fp_mul_u32(const Fe& a, uint32_t s) {
+  uint32_t t[6];
+  uint64_t c = 0;
+#pragma unroll
+  for (int i = 0; i < 6; i++) {
+    c += (uint64_t)a.v[i] * s;
+    t[i] = (uint32_t)c;
+    c >>= 32;
+  }
+  const uint32_t hi = t[5] >> 1;
+  const uint64_t h = (uint64_t)hi * 0x1000001ull;
+  Fe r;
+  uint32_t br;
+  asm("sub.cc.u32  %0, %7, %13;\n\t"
+      "subc.cc.u32 %1, %8, %14;\n\t"
+      "subc.cc.u32 %2, %9, 0;\n\t"
+      "subc.cc.u32 %3, %10, 0;\n\t"
+      "subc.cc.u32 %4, %11, 0;\n\t"
+      "subc.cc.u32 %5, %12, 0;\n\t"
+      "subc.u32    %6, 0, 0;\n\t"
+      : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]), "=r"(br)
+      : "r"(t[0]), "r"(t[1]), "r"(t[2]), "r"(t[3]), "r"(t[4]), "r"(t[5] & 1u), "r"((uint32_t)h),
+        "r"((uint32_t)(h >> 32)));
+  const uint32_t k0 = br ? FpParams::M0 : 0u, k5 = br ? FpParams::M5 : 0u;
+  asm("add.cc.u32  %0, %0, %6;\n\t"
+      "addc.cc.u32 %1, %1, 0;\n\t"
+      "addc.cc.u32 %2, %2, 0;\n\t"
+      "addc.cc.u32 %3, %3, 0;\n\t"
+      "addc.cc.u32 %4, %4, 0;\n\t"
+      "addc.u32    %5, %5, %7;\n\t"
+      : "+r"(r.v[0]), "+r"(r.v[1]), "+r"(r.v[2]), "+r"(r.v[3]), "+r"(r.v[4]), "+r"(r.v[5])
+      : "r"(k0), "r"(k5));
+  return r;
+}
+
+// Newton-form interpolation on the nodes 1..d, one thread per fibre (d <= 32): forward
+// differences (d^2/2 subtractions), c_k = Delta^k y_0 / k! (d Montgomery products), then
+// the Newton basis prod_{j<k} (X - (j+1)) is expanded to monomials in place
+// (d^2/2 multiply-by-small-integer subtractions, fp_mul_u32).  ~8x fewer IMAD.WIDE than
+// the dense d x d matrix (k_interp_axis) and the same unique interpolant, so the output is
+// bit-identical.  Fibres are staged in shared memory limb-major (SoA, padded pitch FB + 1)
+// so the per-thread sweeps are bank-conflict free.
+template <int FB>
+__global__ void __launch_bounds__(FB) k_interp_newton(Fe* data, const Fe* invfact, uint32_t d, uint64_t stride,
+                                                      uint64_t nfib) {
+  extern __shared__ uint32_t sw[];
+  constexpr uint32_t P = FB + 1;
+  const uint64_t f0 = (uint64_t)blockIdx.x * FB;
+  const uint32_t nloc = (nfib - f0 < FB) ? (uint32_t)(nfib - f0) : FB;
+  const uint32_t tot = nloc * d;
+  const bool contiguous = (stride == 1);
+  for (uint32_t idx = threadIdx.x; idx < tot; idx += FB) {
+    uint32_t fl, l;
+    if (contiguous) {
+      fl = idx / d;
+      l = idx - fl * d;
+    } else {
+      l = idx / nloc;
+      fl = idx - l * nloc;
+    }
+    const Fe x = data[fibre_addr(f0 + fl, l, d, stride)];
+#pragma unroll
+    for (int i = 0; i < 6; i++) sw[(l * 6 + i) * P + fl] = x.v[i];
+  }
+  __syncthreads();
+  const uint32_t fl = threadIdx.x;
+  auto LD = [&](uint32_t l) {
+    Fe r;
+#pragma unroll
+    for (int i = 0; i < 6; i++) r.v[i] = sw[(l * 6 + i) * P + fl];
+    return r;
+  };
+  auto ST = [&](uint32_t l, const Fe& x) {
+#pragma unroll
+    for (int i = 0; i < 6; i++) sw[(l * 6 + i) * P + fl] = x.v[i];
+  };
+  if (fl < nloc) {
+    // v[k] <- Delta^k y_0 (descending sweeps keep v[j-1] un-updated when v[j] is)
+    for (uint32_t k = 1; k < d; k++) {
+      Fe hi = LD(d - 1);
+#pragma unroll 4
+      for (uint32_t j = d - 1; j >= k; j--) {
+        const Fe lo = LD(j - 1);
+        ST(j, Fp::sub(hi, lo));
+        hi = lo;
+      }
+    }
+    for (uint32_t k = 2; k < d; k++) ST(k, Fp::mul(LD(k), invfact[k]));
+    // Horner on the Newton form: a <- a (X - (k+1)) + c_k, coefficients in v[k..d)
+    for (int k = (int)d - 2; k >= 0; k--) {
+      const uint32_t s = (uint32_t)k + 1;
+      Fe cur = LD(k);
+#pragma unroll 4
+      for (uint32_t j = k; j + 1 < d; j++) {
+        const Fe nx = LD(j + 1);
+        ST(j, Fp::sub(cur, fp_mul_u32(nx, s)));
+        cur = nx;
+      }
+    }
+  }
+  __syncthreads();
+  for (uint32_t idx = threadIdx.x; idx < tot; idx += FB) {
+    uint32_t f, l;
+    if (contiguous) {
+      f = idx / d;
+      l = idx - f * d;
+    } else {
+      l = idx / nloc;
+      f = idx - l * nloc;
+    }
+    Fe x;
+#pragma unroll
+    for (int i = 0; i < 6; i++) x.v[i] = sw[(l * 6 + i) * P + f];
+    data[fibre_addr(f0 + f, l, d, stride)] = Fp::canon(x);
+  }
+}
+
+// Warp-per-fibre variant of k_interp_newton (fibres longer than 32 nodes): element j = e*32 + lane
+// of the fibre lives in lane `lane`, register slot e (E = ceil(d/32)); the difference and
+// expansion sweeps shift the fibre by one node with warp shuffles, no shared memory.
+__device__ __forceinline__ Fe shfl_fe(const Fe& a, int src) {
+  Fe r;
+#pragma unroll
+  for (int i = 0; i < 6; i++) r.v[i] = __shfl_sync(0xffffffffu, a.v[i], src);
+  return r;
+}
+
+template <int E>
+__global__ void __launch_bounds__(256) k_interp_newton_w(Fe* data, const Fe* invfact, uint32_t d, uint64_t stride,
+                                                         uint64_t nfib) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t f = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); f < nfib; f += nw) {
+    Fe v[E];
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+      const uint32_t j = e * 32 + lane;
+      v[e] = (j < d) ? data[fibre_addr(f, j, d, stride)] : Fp::zero();
+    }
+    for (uint32_t k = 1; k < d; k++) {
+      Fe prev[E];
+#pragma unroll
+      for (int e = 0; e < E; e++) {
+        const Fe up = shfl_fe(v[e], (lane + 31) & 31);
+        if (e == 0) {
+          prev[e] = up;
+        } else {
+          const Fe top = shfl_fe(v[e > 0 ? e - 1 : 0], 31);
+          prev[e] = lane ? up : top;
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < E; e++) {
+        const uint32_t j = e * 32 + lane;
+        if (j >= k && j < d) v[e] = Fp::sub(v[e], prev[e]);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+      const uint32_t j = e * 32 + lane;
+      if (j >= 2 && j < d) v[e] = Fp::mul(v[e], invfact[j]);
+    }
+    for (int k = (int)d - 2; k >= 0; k--) {
+      Fe nx[E];
+#pragma unroll
+      for (int e = 0; e < E; e++) {
+        const Fe dn = shfl_fe(v[e], (lane + 1) & 31);
+        if (e + 1 == E) {
+          nx[e] = dn;
+        } else {
+          const Fe bot = shfl_fe(v[e + 1 < E ? e + 1 : e], 0);
+          nx[e] = (lane == 31) ? bot : dn;
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < E; e++) {
+        const uint32_t j = e * 32 + lane;
+        if ((int)j >= k && j + 1 < d) v[e] = Fp::sub(v[e], fp_mul_u32(nx[e], (uint32_t)k + 1));
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+      const uint32_t j = e * 32 + lane;
+      if (j < d) data[fibre_addr(f, j, d, stride)] = Fp::canon(v[e]);
+    }
   }
 }
 
@@ -233,6 +428,53 @@ int interpolate_device(tc_ctx* ctx, Fe* d_vals, const uint32_t* shape, int m) {
     uint32_t d = shape[j];
     stride /= d;
     if (d == 1) continue;   // degree-0 axis: identity transform
+    const uint64_t nfib = n / d;
+    // Newton form when there are enough fibres to fill the GPU one thread per fibre;
+    // TC_INTERP_NEWTON_MIN_FIB overrides the threshold (tests force it to 1), TC_INTERP_DENSE
+    // keeps the matrix kernel everywhere
+    static const bool newton_off = getenv("TC_INTERP_DENSE") != nullptr;
+    static const uint64_t newton_min =
+        getenv("TC_INTERP_NEWTON_MIN_FIB") ? strtoull(getenv("TC_INTERP_NEWTON_MIN_FIB"), nullptr, 10) : 2048;
+    if (!newton_off && d <= 128 && nfib >= newton_min) {
+      std::string key = "interp.invfact." + std::to_string(d);
+      Fe* dIf;
+      bool have = ctx->scratch.count(key + ".ready") != 0;
+      TC_TRY(scratch_t(ctx, key.c_str(), (uint64_t)d, &dIf));
+      if (!have) {
+        std::vector<Fe> h(d);
+        Fe f = Fp::one();
+        for (uint32_t k = 0; k < d; k++) {
+          if (k > 1) f = Fp::mul(f, Fp::to_mont_small(k));
+          h[k] = Fp::inv_fast(f);
+        }
+        TC_CUDA(ctx, cudaMemcpyAsync(dIf, h.data(), d * sizeof(Fe), cudaMemcpyHostToDevice, st));
+        TC_CUDA(ctx, cudaStreamSynchronize(st));
+        ctx->scratch[key + ".ready"] = tc_ctx::Buf{};
+      }
+      // d <= 32: one thread per fibre (measured 267 us vs 354 us per 2^21-element axis);
+      // longer fibres: one warp per fibre (500 us vs 644 us at d = 64), the SMEM footprint of
+      // the thread-per-fibre kernel caps it at 4 warps per SM there
+      static const bool warp_all = getenv("TC_INTERP_WARP") != nullptr;
+      if (warp_all || d > 32) {
+        const unsigned grid = (unsigned)std::min<uint64_t>((nfib + 7) / 8, 148ull * 8);
+        if (d <= 32) k_interp_newton_w<1><<<grid, 256, 0, st>>>(d_vals, dIf, d, stride, nfib);
+        else if (d <= 64) k_interp_newton_w<2><<<grid, 256, 0, st>>>(d_vals, dIf, d, stride, nfib);
+        else k_interp_newton_w<4><<<grid, 256, 0, st>>>(d_vals, dIf, d, stride, nfib);
+        TC_LAUNCHED(ctx);
+        continue;
+      }
+      constexpr int FB = 64;
+      const size_t smem = (size_t)(FB + 1) * d * 6 * sizeof(uint32_t);
+      static bool attr = false;
+      if (!attr) {
+        TC_CUDA(ctx, cudaFuncSetAttribute(k_interp_newton<FB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)((FB + 1) * 128 * 6 * sizeof(uint32_t))));
+        attr = true;
+      }
+      k_interp_newton<FB><<<(unsigned)((nfib + FB - 1) / FB), FB, smem, st>>>(d_vals, dIf, d, stride, nfib);
+      TC_LAUNCHED(ctx);
+      continue;
+    }
     std::string key = "interp.B." + std::to_string(d);
     Fe* dB;
     bool have = ctx->scratch.count(key + ".ready") != 0;
@@ -244,7 +486,6 @@ int interpolate_device(tc_ctx* ctx, Fe* d_vals, const uint32_t* shape, int m) {
       ctx->scratch[key + ".ready"] = tc_ctx::Buf{};
     }
     uint32_t FB = std::max<uint32_t>(1u, 2048u / d);
-    uint64_t nfib = n / d;
     size_t smem = (size_t)FB * d * sizeof(Fe);
     if (smem > 48 * 1024)
       TC_CUDA(ctx, cudaFuncSetAttribute(k_interp_axis, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -352,6 +352,51 @@ print("ok")
 """
 
 
+_INTERP_SCRIPT = r"""
+import sys, hashlib, json, os, random, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2602_12630_b200 as tcb
+from oracle import tc_oracle as O
+dom = tcb.PrimeField()
+rng = random.Random(12)
+for shape in [(128,), (2, 128), (3, 5, 7, 16), (64, 64), (8, 8, 8, 8), (4, 4, 4, 4, 4, 4), (2, 3, 2, 5)]:
+    n = int(np.prod(shape))
+    # full-range F_p values (p - 1, 0 and random) and small signed ones
+    for vals in ([rng.randrange(O.P) for _ in range(n - 2)] + [O.P - 1, 0],
+                 [rng.randrange(-3, 4) % O.P for _ in range(n)]):
+        f = tcb.interpolate_lagrange(dom, vals, tcb.default_grid(dom, shape))
+        assert list(f.coeffs) == O.interpolate_lagrange(vals, shape), shape
+gold = json.load(open(os.path.join({root!r}, "tests", "golden", "config2.json")))
+x = np.random.default_rng(0).standard_normal(4096, dtype=np.float32)
+vals = O.quantize(x, 16)
+for g in gold:
+    f = tcb.interpolate_lagrange(dom, vals, tcb.default_grid(dom, tuple(g["shape"])))
+    dig = hashlib.sha256(b"".join(O.encode_scalar(c) for c in f.coeffs)).hexdigest()
+    assert dig == g["coeff_digest"], g["shape"]
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{"TC_INTERP_NEWTON_MIN_FIB": "1"}, {"TC_INTERP_NEWTON_MIN_FIB": "1", "TC_INTERP_WARP": "1"},
+                                 {"TC_INTERP_DENSE": "1"}])
+def test_interpolation_newton_and_dense_kernels(env, tmp_path):
+    """All interpolation kernels — the Newton-form ones (forward differences + small-integer
+    basis expansion; thread-per-fibre for <= 32 nodes, warp-per-fibre above, or warp-per-fibre
+    everywhere) forced onto every axis with <= 128 nodes, and the dense Lagrange-matrix one
+    forced everywhere — equal the oracle on full-range F_p values
+    (p - 1 and 0 included), on small signed values and on ragged shapes, and reproduce the
+    reference's config-2 coefficient digests."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "interp.py"
+    script.write_text(_INTERP_SCRIPT.format(root=root))
+    out = subprocess.run([sys.executable, str(script)], env=dict(os.environ, **env), capture_output=True, text=True,
+                         timeout=900)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr
+
+
 @pytest.mark.parametrize("fp_min_n", ["1", "1000000000"])
 def test_msm_float_exponent_plan_small(fp_min_n, tmp_path):
     """The float-exponent window plan (mode 1: one bucket entry per element, groups by
