@@ -456,10 +456,11 @@ __global__ void k_copy_starts(const uint32_t* S, uint32_t nb, uint32_t nc, uint3
 template <int DT, bool SCATTER>
 __global__ void __launch_bounds__(256) k_digits_fp(const void* const* ptrs, uint64_t n, int scale_bits, WinPlan P,
                                                    uint32_t* __restrict__ cnt, uint32_t* __restrict__ vals,
-                                                   uint32_t nc) {
+                                                   uint32_t nc, uint64_t chunk) {
   const uint32_t l = blockIdx.y;
-  const uint32_t key0 = l * P.nbm, copy = blockIdx.x % nc;
   const uint64_t i0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * V_EPT;
+  // counter copy: by block (interleaved copies) or by chunk (counts from k_count_fpb)
+  const uint32_t key0 = l * P.nbm, copy = chunk ? (uint32_t)(i0 / chunk) : blockIdx.x % nc;
   uint32_t raw[V_EPT], ctr[V_EPT], val[V_EPT];
   load_raw8<DT>(ptrs[l], i0, n, raw);
   uint32_t live = 0;
@@ -487,6 +488,90 @@ __global__ void __launch_bounds__(256) k_digits_fp(const void* const* ptrs, uint
 #pragma unroll
     for (int k = 0; k < V_EPT; k++)
       if (live >> k & 1u) atomicAdd(cnt + ctr[k], 1u);
+  }
+}
+
+// mode-1 counting sort with block-private bucket counters (no global atomics at all).
+// Block (x, l) owns chunk x of MSM l and keeps that MSM's nbm bucket counters in shared
+// memory.  k_count_fpb: shared-memory atomics, then the block's counts stored chunk-major
+// (cnt[(l S + x) nbm + b], coalesced).  k_fpb_totals / cub scan / k_fpb_starts turn them
+// into bucket starts and, in place, the start of every (chunk, bucket) run.  k_scatter_fpb:
+// the block loads its run starts into shared memory and hands out slots with shared-memory
+// atomics.  The scatter is launched a few MSMs at a time so the vals region being written
+// stays resident in L2 while the runs' partial sectors fill (one launch over all MSMs let
+// them leave L2 half-written: 1.30 ms vs 0.81 ms for the global-atomic scatter).
+__device__ __forceinline__ uint32_t fp_key(const WinPlan& P, uint64_t mag) {
+  const int bl = 64 - __clzll((long long)mag);
+  const int g = bl > P.mbits ? bl - P.mbits : 0;
+  return P.base[g] + (uint32_t)(mag >> g) - P.mlo[g];
+}
+
+template <int DT, bool SCATTER>
+__global__ void __launch_bounds__(1024) k_fpb_pass(const void* const* ptrs, uint64_t n, int scale_bits, WinPlan P,
+                                                   uint32_t* __restrict__ cnt, uint32_t* __restrict__ vals,
+                                                   uint64_t chunk, uint32_t l0) {
+  extern __shared__ uint32_t h[];
+  const uint32_t l = l0 + blockIdx.y, S = gridDim.x;
+  const uint64_t c0 = (uint64_t)blockIdx.x * chunk;
+  const uint64_t c1 = min(n, c0 + chunk);
+  const void* p = ptrs[l];
+  uint32_t* row = cnt + ((uint64_t)l * S + blockIdx.x) * P.nbm;
+  for (uint32_t b = threadIdx.x; b < P.nbm; b += blockDim.x) h[b] = SCATTER ? row[b] : 0u;
+  __syncthreads();
+  for (uint64_t i0 = c0 + (uint64_t)threadIdx.x * V_EPT; i0 < c1; i0 += (uint64_t)blockDim.x * V_EPT) {
+    uint32_t raw[V_EPT];
+    load_raw8<DT>(p, i0, c1, raw);
+#pragma unroll
+    for (int k = 0; k < V_EPT; k++) {
+      bool neg;
+      const uint64_t mag = (i0 + k < c1) ? quant64<DT>(raw[k], scale_bits, neg) : 0ull;
+      if (mag) {
+        const uint32_t slot = atomicAdd(h + fp_key(P, mag), 1u);
+        if (SCATTER) vals[slot] = (uint32_t)(i0 + k) | (neg ? SIGN_BIT : 0u);
+      }
+    }
+  }
+  if (SCATTER) return;
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < P.nbm; b += blockDim.x) row[b] = h[b];
+}
+
+// tot[l nbm + b] = sum over chunks of cnt[(l S + x) nbm + b]  (loads batched 8 deep: the
+// chunk rows are independent, a one-at-a-time loop is latency bound)
+__global__ void k_fpb_totals(const uint32_t* cnt, uint32_t nbm, uint32_t L, uint32_t S, uint32_t* tot) {
+  const uint64_t key = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (key >= (uint64_t)L * nbm) return;
+  const uint64_t l = key / nbm, b = key - l * nbm;
+  const uint32_t* c = cnt + l * S * nbm + b;
+  uint32_t t = 0;
+  for (uint32_t x0 = 0; x0 < S; x0 += 8) {
+    uint32_t v[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) v[k] = (x0 + k < S) ? __ldg(c + (uint64_t)(x0 + k) * nbm) : 0u;
+#pragma unroll
+    for (int k = 0; k < 8; k++) t += v[k];
+  }
+  tot[key] = t;
+}
+
+// counts -> run starts, in place: run (x, b) of MSM l starts at bstart[l nbm + b] plus the
+// counts of the earlier chunks
+__global__ void k_fpb_starts(uint32_t* __restrict__ cnt, uint32_t nbm, uint32_t L, uint32_t S,
+                             const uint32_t* __restrict__ bstart) {
+  const uint64_t key = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (key >= (uint64_t)L * nbm) return;
+  const uint64_t l = key / nbm, b = key - l * nbm;
+  uint32_t* c = cnt + l * S * nbm + b;
+  uint32_t run = bstart[key];
+  for (uint32_t x0 = 0; x0 < S; x0 += 8) {
+    uint32_t v[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) v[k] = (x0 + k < S) ? c[(uint64_t)(x0 + k) * nbm] : 0u;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      if (x0 + k < S) c[(uint64_t)(x0 + k) * nbm] = run;
+      run += v[k];
+    }
   }
 }
 
@@ -985,6 +1070,75 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   // counting-sort layout: count, scan, scatter (no keys stored, no radix passes)
   uint32_t *cnt, *cursor;
   static const uint32_t NC_ENV = getenv("TC_MSM_NC") ? (uint32_t)atoi(getenv("TC_MSM_NC")) : 16u;   // sweep: 1 9.04, 4 7.79, 8 7.53, 16 7.40, 32 7.37 ms
+  // mode 1 with block-private counters (k_fpb_pass) when one MSM's counters fit twice per
+  // SM in shared memory; otherwise NC interleaved counter copies spread the global atomics
+  static const bool no_blk = getenv("TC_MSM_NO_BLKCNT") != nullptr;
+  static const uint32_t FPB_LG_ENV = getenv("TC_MSM_FPB_LG") ? (uint32_t)atoi(getenv("TC_MSM_FPB_LG")) : 8u;
+  const size_t blk_smem = (size_t)P.nbm * sizeof(uint32_t);
+  const bool blkcnt = P.mode == 1 && vec_ok && !no_blk && blk_smem <= 100 * 1024 && n >= (1u << 16) &&
+                      dtype != TC_DTYPE_F32;
+  if (blkcnt) {
+    // S chunks per MSM so that one scatter launch (LG MSMs) is about one wave of 2 blocks/SM
+    const uint32_t LG = std::max(1u, std::min<uint32_t>(FPB_LG_ENV, (uint32_t)L));
+    const uint64_t conc = (uint64_t)ctx->num_sms * 2;
+    const uint64_t step = 1024ull * V_EPT;
+    const uint64_t S0 = std::max<uint64_t>(1, std::min<uint64_t>(conc / LG, n / step));
+    const uint64_t chunk = ((n + S0 - 1) / S0 + step - 1) / step * step;
+    const uint32_t Sx = (uint32_t)((n + chunk - 1) / chunk);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_fpb_pass<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+      cudaFuncSetAttribute(k_fpb_pass<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+      cudaFuncSetAttribute(k_fpb_pass<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+      cudaFuncSetAttribute(k_fpb_pass<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+      attr = true;
+    }
+    uint32_t *runs, *tot;
+    TC_TRY(scratch_t(ctx, "msm.fpbruns", (uint64_t)nb * Sx, &runs));
+    TC_TRY(scratch_t(ctx, "msm.bcount", (uint64_t)nb + 1, &tot));
+    TC_TRY(scratch_t(ctx, "msm.bstart", (uint64_t)nb + 1, &bstart));
+    TC_CUDA(ctx, cudaMemsetAsync(tot + nb, 0, sizeof(uint32_t), st));
+    if (getenv("TC_MSM_DEBUG"))
+      fprintf(stderr, "[tc msm] L=%d n=%llu mode=1 (block counters: %u chunks x %llu) groups=%d buckets/msm=%u\n", L,
+              (unsigned long long)n, Sx, (unsigned long long)chunk, P.nwin, P.nbm);
+    auto pass = [&](bool scatter, uint32_t l0, uint32_t nl) {
+      if (dtype == TC_DTYPE_F16) {
+        if (scatter)
+          k_fpb_pass<1, true><<<dim3(Sx, nl), 1024, blk_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals, chunk, l0);
+        else
+          k_fpb_pass<1, false><<<dim3(Sx, nl), 1024, blk_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals, chunk, l0);
+      } else {
+        if (scatter)
+          k_fpb_pass<2, true><<<dim3(Sx, nl), 1024, blk_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals, chunk, l0);
+        else
+          k_fpb_pass<2, false><<<dim3(Sx, nl), 1024, blk_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals, chunk, l0);
+      }
+    };
+    pass(false, 0, (uint32_t)L);
+    TC_LAUNCHED(ctx);
+    k_fpb_totals<<<blocks_for(nb, 256), 256, 0, st>>>(runs, P.nbm, (uint32_t)L, Sx, tot);
+    TC_LAUNCHED(ctx);
+    size_t sb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, sb, tot, bstart, (int)(nb + 1), st);
+    void* d_sb;
+    TC_TRY(scratch(ctx, "msm.scantmp0", sb, &d_sb));
+    TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(d_sb, sb, tot, bstart, (int)(nb + 1), st));
+    ctx->launches += 2;
+    k_fpb_starts<<<blocks_for(nb, 256), 256, 0, st>>>(runs, P.nbm, (uint32_t)L, Sx, bstart);
+    TC_LAUNCHED(ctx);
+    TC_CUDA(ctx, cudaMemcpyAsync(h_small, bstart + nb, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    k_max_bucket<<<blocks_for(nb, 256), 256, 0, st>>>(bstart, nb, d_small + NHIST + 3);   // zeroed with d_small
+    TC_LAUNCHED(ctx);
+    TC_CUDA(ctx, cudaMemcpyAsync(h_small + 1, d_small + NHIST + 3, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    have_maxb = true;
+    for (uint32_t l0 = 0; l0 < (uint32_t)L; l0 += LG) {
+      pass(true, l0, std::min<uint32_t>(LG, (uint32_t)L - l0));
+      TC_LAUNCHED(ctx);
+    }
+    TC_CUDA(ctx, cudaStreamSynchronize(st));
+    E = h_small[0];
+    maxb = h_small[1];
+  } else {
   const uint32_t NC = P.mode == 1 ? std::max(1u, NC_ENV) : 1u;
   const uint64_t ncnt = (uint64_t)nb * NC + 1;
   if (ncnt >= (1ull << 31)) return fail(ctx, TC_ERR_VALUE, "msm: too many bucket counters");
@@ -1030,10 +1184,11 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     constexpr int D = decltype(dt)::value;
     if constexpr (D >= 1 && D <= 3) {
       if (fast) {
-        if (P.mode == 1)
-          k_digits_fp<D, false><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cnt, nullptr, NC);
-        else
+        if (P.mode == 1) {
+          k_digits_fp<D, false><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cnt, nullptr, NC, 0);
+        } else {
           k_digits_v<D, false><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, H, cnt, nullptr, NC);
+        }
         return;
       }
     }
@@ -1062,7 +1217,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     if constexpr (D >= 1 && D <= 3) {
       if (fast) {
         if (P.mode == 1)
-          k_digits_fp<D, true><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cursor, vals, NC);
+          k_digits_fp<D, true><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cursor, vals, NC, 0);
         else
           k_digits_v<D, true><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, H, cursor, vals, NC);
         return;
@@ -1075,6 +1230,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   TC_CUDA(ctx, cudaStreamSynchronize(st));
   E = h_small[0];
   maxb = h_small[1];
+  }   // counting layout with global counters
   if (E == 0) {
     k_fill_inf<<<blocks_for(L, 64), 64, 0, st>>>(d_out, (uint32_t)L);
     TC_LAUNCHED(ctx);
