@@ -648,19 +648,21 @@ __global__ void __launch_bounds__(128, TC_ACCUM_MINB) k_accum_aff(const uint32_t
 __global__ void __launch_bounds__(128) k_accum_ext(const Ext* in, const uint32_t* iofs, const uint32_t* toff,
                                                     const uint32_t* ooff, uint32_t nb, uint32_t T, Ext* out,
                                                     Ext* buckets) {
-  uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t total = toff[nb];
-  if (p >= total) return;
-  uint32_t k = find_bucket(toff, nb, p);
-  uint32_t piece = p - toff[k];
-  uint32_t a = iofs[k] + piece * T;
-  uint32_t b = min(a + T, iofs[k + 1]);
-  Ext acc = ld_ext(in + a);
-  for (uint32_t j = a + 1; j < b; j++) ext_add(acc, ld_ext(in + j));
-  if (toff[k + 1] - toff[k] == 1)
-    buckets[k] = acc;
-  else
-    out[ooff[k] + piece] = acc;
+  // grid-stride: the launch is sized from a host-side bound (no read-back of the level's
+  // piece count), so a bounded grid avoids launching mostly-empty blocks on deep levels
+  const uint32_t total = toff[nb];
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < total; p += gridDim.x * blockDim.x) {
+    const uint32_t k = find_bucket(toff, nb, p);
+    const uint32_t piece = p - toff[k];
+    const uint32_t a = iofs[k] + piece * T;
+    const uint32_t b = min(a + T, iofs[k + 1]);
+    Ext acc = ld_ext(in + a);
+    for (uint32_t j = a + 1; j < b; j++) ext_add(acc, ld_ext(in + j));
+    if (toff[k + 1] - toff[k] == 1)
+      buckets[k] = acc;
+    else
+      out[ooff[k] + piece] = acc;
+  }
 }
 
 // ---- weighted bucket sums A_g = sum_j (j+1) x_j by recursive segmentation ----------------
@@ -1298,7 +1300,8 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     ctx->launches += 4;
     // every piece holds >= 1 item, and a multi-piece bucket of c >= 2 items yields
     // ceil(c/T1) <= c items: both threads and the next level's items are <= items_bound
-    k_accum_ext<<<blocks_for(items_bound, 128), 128, 0, st>>>(itemsA, offA, toff, offB, nb, T1, itemsB, buckets);
+    const unsigned gext = (unsigned)std::min<uint64_t>(blocks_for(items_bound, 128), (uint64_t)ctx->num_sms * 16);
+    k_accum_ext<<<gext, 128, 0, st>>>(itemsA, offA, toff, offB, nb, T1, itemsB, buckets);
     TC_LAUNCHED(ctx);
     std::swap(offA, offB);
     std::swap(itemsA, itemsB);
