@@ -397,6 +397,42 @@ def test_interpolation_newton_and_dense_kernels(env, tmp_path):
     assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr
 
 
+_SORT_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_2602_12630_b200 as tcb
+from oracle import tc_oracle as O
+shape = (16, 16, 16, 16)
+srs, td = tcb.setup_srs(shape, b"sort-paths")
+g = np.random.default_rng(52)
+xs = [np.clip(g.standard_t(3, 65536) * s, -65504, 65504).astype(np.float16) for s in (0.003, 1.0, 2.5, 700.0)]
+xs.append(np.zeros(65536, np.float16))
+x = xs[1].copy(); x[::7] = 0; x[5] = np.float16(65504.0); x[6] = np.float16(-6e-8); xs.append(x)
+comms = tcb.tc_commit_many(srs, [torch.from_numpy(v).cuda() for v in xs])
+for v, c in zip(xs, comms):
+    assert c.elem == O.commit_trapdoor(O.quantize(v.astype(np.float64), 16), shape, list(td.taus))
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{}, {"TC_MSM_NO_BLKCNT": "1"}, {"TC_MSM_FPB_LG": "1"}, {"TC_MSM_FPB_LG": "3"}])
+def test_msm_counting_sort_paths(env, tmp_path):
+    """The float-exponent plan's two counting sorts — block-private bucket counters with the
+    scatter launched LG MSMs at a time (several chunks per MSM, ragged last launch), and the
+    global-atomic counters — give commitments equal to the trapdoor oracle on a batch of six
+    65536-element fp16 tensors (tiny, large, all-zero, sparse, max / min-subnormal values)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "sort.py"
+    script.write_text(_SORT_SCRIPT.format(root=root))
+    # the float-exponent plan starts at 2^18 elements by default: force it for 2^16
+    env = dict(os.environ, TC_MSM_FP_MIN_N="65536", **env)
+    out = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr
+
+
 @pytest.mark.parametrize("fp_min_n", ["1", "1000000000"])
 def test_msm_float_exponent_plan_small(fp_min_n, tmp_path):
     """The float-exponent window plan (mode 1: one bucket entry per element, groups by
