@@ -600,6 +600,7 @@ int tc_srs_destroy(tc_srs* srs) {
   for (auto* e : {srs->ed_monomial, srs->ed_lagrange, srs->ed_sublag})
     if (e) cudaFree(e);
   for (auto& kv : srs->wintab) cudaFree(kv.second);
+  if (srs->exptab) cudaFree(srs->exptab);
   delete srs;
   return TC_OK;
 }
@@ -677,7 +678,8 @@ static int msm_srs(tc_ctx* ctx, const tc_srs* srs, int which, int dtype, int sca
   if (srs->n > SMALL_MSM_MAX) {
     const EdPk* bases;
     TC_TRY(tcrt::srs_edwards(ctx, const_cast<tc_srs*>(srs), which, &bases));
-    return tcrt::msm_batch_device(ctx, dtype, scale_bits, ptrs, L, bases, srs->n, d_out);
+    return tcrt::msm_batch_device(ctx, dtype, scale_bits, ptrs, L, bases, srs->n, d_out, nullptr, 0,
+                                  which == TC_SRS_LAGRANGE ? const_cast<tc_srs*>(srs) : nullptr);
   }
   std::vector<const void*> fp(ptrs, ptrs + L);
   if (dtype != TC_DTYPE_FP_LIMBS) {   // quantise first: the table kernel takes field elements

@@ -500,10 +500,11 @@ __global__ void __launch_bounds__(256) k_digits_fp(const void* const* ptrs, uint
 // atomics.  The scatter is launched a few MSMs at a time so the vals region being written
 // stays resident in L2 while the runs' partial sectors fill (one launch over all MSMs let
 // them leave L2 half-written: 1.30 ms vs 0.81 ms for the global-atomic scatter).
-__device__ __forceinline__ uint32_t fp_key(const WinPlan& P, uint64_t mag) {
+__device__ __forceinline__ uint32_t fp_key(const WinPlan& P, uint64_t mag, uint32_t& g) {
   const int bl = 64 - __clzll((long long)mag);
-  const int g = bl > P.mbits ? bl - P.mbits : 0;
-  return P.base[g] + (uint32_t)(mag >> g) - P.mlo[g];
+  g = bl > P.mbits ? (uint32_t)(bl - P.mbits) : 0u;
+  // mode 3: one window of m = |q| >> g in [1, 2^mbits), the exponent goes to the base
+  return P.mode == 3 ? (uint32_t)(mag >> g) - 1u : P.base[g] + (uint32_t)(mag >> g) - P.mlo[g];
 }
 
 template <int DT, bool SCATTER>
@@ -526,14 +527,106 @@ __global__ void __launch_bounds__(1024) k_fpb_pass(const void* const* ptrs, uint
       bool neg;
       const uint64_t mag = (i0 + k < c1) ? quant64<DT>(raw[k], scale_bits, neg) : 0ull;
       if (mag) {
-        const uint32_t slot = atomicAdd(h + fp_key(P, mag), 1u);
-        if (SCATTER) vals[slot] = (uint32_t)(i0 + k) | (neg ? SIGN_BIT : 0u);
+        uint32_t g;
+        const uint32_t slot = atomicAdd(h + fp_key(P, mag, g), 1u);
+        // mode 3 entries index the exponent table: 2^g G_i at g n + i
+        if (SCATTER) vals[slot] = ((P.mode == 3 ? g * (uint32_t)n : 0u) + (uint32_t)(i0 + k)) | (neg ? SIGN_BIT : 0u);
       }
     }
   }
   if (SCATTER) return;
   __syncthreads();
   for (uint32_t b = threadIdx.x; b < P.nbm; b += blockDim.x) row[b] = h[b];
+}
+
+// mode-3 scatter with a block-local counting sort of every 8192-element slice: the slice's
+// entries are ranked per bucket in shared memory, staged in bucket order together with their
+// global slot, and written out by consecutive threads — entries of one bucket (about 4 per
+// slice over 2^11 - 1 buckets) land in consecutive addresses from consecutive lanes, so
+// they share store transactions instead of costing one scattered 4-byte store each.
+constexpr int FPS_THREADS = 512, FPS_EPT = 16, FPS_SLICE = FPS_THREADS * FPS_EPT;   // 8192
+template <int DT>
+__global__ void __launch_bounds__(FPS_THREADS, 2) k_fpb_scatter_sorted(const void* const* ptrs, uint64_t n,
+                                                                        int scale_bits, WinPlan P,
+                                                                        const uint32_t* __restrict__ cnt,
+                                                                        uint32_t* __restrict__ vals, uint64_t chunk,
+                                                                        uint32_t l0) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t NB = P.nbm;                  // <= 2047 (mode 3)
+  uint32_t* h = sm;                           // run cursors (global slots)
+  uint32_t* lo = sm + 2048;                   // per-slice counts -> exclusive offsets, lo[2048] = total
+  uint2* stg = (uint2*)(sm + 2 * 2048 + 32);  // staged (slot, entry), bucket order
+  __shared__ uint32_t wsum[FPS_THREADS / 32];
+  const uint32_t t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const uint32_t l = l0 + blockIdx.y, S = gridDim.x;
+  const uint32_t* row = cnt + ((uint64_t)l * S + blockIdx.x) * NB;
+  for (uint32_t b = t; b < NB; b += FPS_THREADS) h[b] = row[b];
+  const uint64_t c0 = (uint64_t)blockIdx.x * chunk;
+  const uint64_t c1 = min(n, c0 + chunk);
+  const void* p = ptrs[l];
+  for (uint64_t base = c0; base < c1; base += FPS_SLICE) {
+    for (uint32_t b = t; b < 2048; b += FPS_THREADS) lo[b] = 0u;
+    __syncthreads();
+    uint32_t key[FPS_EPT], rk[FPS_EPT], val[FPS_EPT];
+#pragma unroll
+    for (int half = 0; half < 2; half++) {
+      const uint64_t i0 = base + (uint64_t)half * (FPS_SLICE / 2) + (uint64_t)t * V_EPT;
+      uint32_t raw[V_EPT];
+      load_raw8<DT>(p, i0, c1, raw);
+#pragma unroll
+      for (int k = 0; k < V_EPT; k++) {
+        const int e = half * V_EPT + k;
+        bool neg;
+        const uint64_t mag = (i0 + k < c1) ? quant64<DT>(raw[k], scale_bits, neg) : 0ull;
+        key[e] = 0xffffffffu;
+        if (mag) {
+          uint32_t g;
+          key[e] = fp_key(P, mag, g);
+          val[e] = (g * (uint32_t)n + (uint32_t)(i0 + k)) | (neg ? SIGN_BIT : 0u);
+          rk[e] = atomicAdd(lo + key[e], 1u);
+        }
+      }
+    }
+    __syncthreads();
+    // exclusive scan of lo[0..2048): 4 counters per thread, warp shuffles, warp totals
+    uint32_t c[4], sum = 0;
+#pragma unroll
+    for (int j = 0; j < 4; j++) c[j] = lo[4 * t + j], sum += c[j];
+    uint32_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= (uint32_t)o) inc += y;
+    }
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t w = lane < FPS_THREADS / 32 ? wsum[lane] : 0u, wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= (uint32_t)o) wi += y;
+      }
+      if (lane < FPS_THREADS / 32) wsum[lane] = wi - w;
+    }
+    __syncthreads();
+    uint32_t run = wsum[wid] + inc - sum;
+#pragma unroll
+    for (int j = 0; j < 4; j++) lo[4 * t + j] = run, run += c[j];
+    if (t == FPS_THREADS - 1) lo[2048] = run;
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < FPS_EPT; e++)
+      if (key[e] != 0xffffffffu) stg[lo[key[e]] + rk[e]] = make_uint2(h[key[e]] + rk[e], val[e]);
+    __syncthreads();
+    for (uint32_t b = t; b < NB; b += FPS_THREADS) h[b] += lo[b + 1] - lo[b];
+    const uint32_t tot = lo[2048];
+    for (uint32_t s2 = t; s2 < tot; s2 += FPS_THREADS) {
+      const uint2 q = stg[s2];
+      vals[q.x] = q.y;
+    }
+    __syncthreads();
+  }
 }
 
 // tot[l nbm + b] = sum over chunks of cnt[(l S + x) nbm + b]  (loads batched 8 deep: the
@@ -943,6 +1036,23 @@ WinPlan plan_fp(uint32_t nbits, int mb) {
   return P;
 }
 
+// mode 3: the float-exponent plan over an exponent table (srs_exp_table): entry (i, g)
+// reads the base 2^g G_i, so all groups share ONE window of 2^mb - 1 buckets of weight m
+WinPlan plan_fpx(int mb) {
+  WinPlan P;
+  P.mode = 3;
+  P.ndig = P.cdig = 0;
+  P.mbits = mb;
+  P.nwin = 1;
+  P.off[0] = 0;
+  P.width[0] = 0;
+  P.mlo[0] = 1;
+  P.base[0] = 0;
+  P.base[1] = (1u << mb) - 1u;
+  P.nbm = P.base[1];
+  return P;
+}
+
 template <class F>
 int dispatch_dt(tc_ctx* ctx, int dtype, F&& f) {
   switch (dtype) {
@@ -962,7 +1072,7 @@ namespace tcrt {
 int quantize_flags_to_status(tc_ctx* ctx, uint32_t f);
 
 int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* h_ptrs, int L, const EdPk* d_bases,
-                     uint64_t n, Aff* d_out, const uint32_t* h_boff, int fbw) {
+                     uint64_t n, Aff* d_out, const uint32_t* h_boff, int fbw, tc_srs* exp_srs) {
   if (fbw && (dtype != TC_DTYPE_FP_LIMBS || n * fb_ndig(fbw) >= (1ull << 31)))
     return fail(ctx, TC_ERR_VALUE, "msm: window-table MSMs take field-element scalars, < 2^31 table points");
   cudaStream_t st = ctx->stream;
@@ -989,7 +1099,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
       for (int l0 = 0; l0 < L; l0 += (int)G) {
         const int cnt = (int)std::min<uint64_t>(G, (uint64_t)(L - l0));
         TC_TRY(msm_batch_device(ctx, dtype, scale_bits, h_ptrs + l0, cnt, d_bases, n, d_out + l0,
-                                h_boff ? h_boff + l0 : nullptr, fbw));
+                                h_boff ? h_boff + l0 : nullptr, fbw, exp_srs));
       }
       return TC_OK;
     }
@@ -1054,12 +1164,24 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   for (int l = 0; l < L && vec_ok; l++) vec_ok = ((uintptr_t)h_ptrs[l] & 15u) == 0;   // 16-byte vector loads
   const int fp_mb = dtype == TC_DTYPE_F16 ? 11 : (dtype == TC_DTYPE_BF16 ? 8 : 0);
   const bool fpmode = vec_ok && fp_mb && n >= FP_MIN_N && (int)nbits - fp_mb + 1 <= MAXW;
-  const WinPlan P = fbw ? plan_fb(fbw) : fpmode ? plan_fp(nbits, fp_mb) : plan_windows(hist, nbits, (uint64_t)L);
+  WinPlan P = fbw ? plan_fb(fbw) : fpmode ? plan_fp(nbits, fp_mb) : plan_windows(hist, nbits, (uint64_t)L);
+  // exponent-table plan (mode 3) when the caller's bases are a whole Lagrange basis and its
+  // table (depth = the batch's groups) fits in memory
+  static const bool no_exp = getenv("TC_MSM_NO_EXPTAB") != nullptr;
+  const EdPk* bases = d_bases;
+  if (fpmode && !fbw && exp_srs && !h_boff && !no_exp && !getenv("TC_MSM_NO_BLKCNT")) {
+    const int depth = P.nwin;
+    const EdPk* tab = nullptr;
+    if ((uint64_t)depth * n < (1ull << 31) && srs_exp_table(ctx, exp_srs, d_bases, n, depth, &tab) == TC_OK) {
+      P = plan_fpx(fp_mb);
+      bases = tab;
+    }
+  }
   if (P.nwin > MAXW) return fail(ctx, TC_ERR_VALUE, "msm: window plan too long");
   const uint64_t nb64 = (uint64_t)L * P.nbm;
   if (nb64 >= (1ull << 31)) return fail(ctx, TC_ERR_VALUE, "msm batch too large (%llu buckets)", (unsigned long long)nb64);
   const uint32_t nb = (uint32_t)nb64;
-  const uint64_t cap = (uint64_t)L * n * (P.mode == 1 ? 1 : P.mode == 2 ? P.ndig : P.nwin);
+  const uint64_t cap = (uint64_t)L * n * ((P.mode == 1 || P.mode == 3) ? 1 : P.mode == 2 ? P.ndig : P.nwin);
 
   // 3. non-zero digits, compacted
   uint32_t* vals;
@@ -1080,13 +1202,18 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   // ... and when one MSM's entries (4 B each) fit in L2 with room to spare: the scatter's
   // short per-(chunk, bucket) runs must stay in L2 until their sectors fill (config 5,
   // 168 MB of entries per MSM: 157.7 ms with block counters vs 138.4 ms without)
-  const bool blkcnt = P.mode == 1 && vec_ok && !no_blk && blk_smem <= 100 * 1024 && n >= (1u << 16) &&
-                      n * sizeof(uint32_t) <= (16ull << 20) && dtype != TC_DTYPE_F32;
+  // (mode 3: 2^mb - 1 buckets per MSM, so every (chunk, bucket) run is long and fills its
+  // sectors quickly whatever the MSM size)
+  const bool blkcnt = P.mode == 3 || (P.mode == 1 && vec_ok && !no_blk && blk_smem <= 100 * 1024 &&
+                                      n >= (1u << 16) && n * sizeof(uint32_t) <= (16ull << 20) &&
+                                      dtype != TC_DTYPE_F32);
   if (blkcnt) {
     // S chunks per MSM so that one scatter launch (LG MSMs) is about one wave of 2 blocks/SM
     // LG MSMs per scatter launch: their entries (LG n 4 B) stay within 64 MB of L2
-    const uint32_t LG = std::max<uint32_t>(
-        1u, std::min(std::min(FPB_LG_ENV, (uint32_t)L), (uint32_t)((64ull << 20) / (n * sizeof(uint32_t)))));
+    const uint32_t LG = P.mode == 3 ? std::max(1u, std::min(getenv("TC_MSM_FPB_LG") ? FPB_LG_ENV : (uint32_t)L,
+                                                            (uint32_t)L))
+                                    : std::max<uint32_t>(1u, std::min(std::min(FPB_LG_ENV, (uint32_t)L),
+                                                                      (uint32_t)((64ull << 20) / (n * sizeof(uint32_t)))));
     const uint64_t conc = (uint64_t)ctx->num_sms * 2;
     const uint64_t step = 1024ull * V_EPT;
     const uint64_t S0 = std::max<uint64_t>(1, std::min<uint64_t>(conc / LG, n / step));
@@ -1106,9 +1233,27 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     TC_TRY(scratch_t(ctx, "msm.bstart", (uint64_t)nb + 1, &bstart));
     TC_CUDA(ctx, cudaMemsetAsync(tot + nb, 0, sizeof(uint32_t), st));
     if (getenv("TC_MSM_DEBUG"))
-      fprintf(stderr, "[tc msm] L=%d n=%llu mode=1 (block counters: %u chunks x %llu) groups=%d buckets/msm=%u\n", L,
-              (unsigned long long)n, Sx, (unsigned long long)chunk, P.nwin, P.nbm);
+      fprintf(stderr, "[tc msm] L=%d n=%llu mode=%d (block counters: %u chunks x %llu) groups=%d buckets/msm=%u\n", L,
+              (unsigned long long)n, P.mode, Sx, (unsigned long long)chunk, P.nwin, P.nbm);
+    static const bool no_sorted = getenv("TC_MSM_NO_SORTED_SCATTER") != nullptr;
+    const bool sorted = P.mode == 3 && !no_sorted;
+    const size_t fps_smem = (2 * 2048 + 32) * sizeof(uint32_t) + FPS_SLICE * sizeof(uint2);
+    static bool fps_attr = false;
+    if (sorted && !fps_attr) {
+      cudaFuncSetAttribute(k_fpb_scatter_sorted<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fps_smem);
+      cudaFuncSetAttribute(k_fpb_scatter_sorted<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fps_smem);
+      fps_attr = true;
+    }
     auto pass = [&](bool scatter, uint32_t l0, uint32_t nl) {
+      if (scatter && sorted) {
+        if (dtype == TC_DTYPE_F16)
+          k_fpb_scatter_sorted<1><<<dim3(Sx, nl), FPS_THREADS, fps_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals,
+                                                                               chunk, l0);
+        else
+          k_fpb_scatter_sorted<2><<<dim3(Sx, nl), FPS_THREADS, fps_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals,
+                                                                               chunk, l0);
+        return;
+      }
       if (dtype == TC_DTYPE_F16) {
         if (scatter)
           k_fpb_pass<1, true><<<dim3(Sx, nl), 1024, blk_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals, chunk, l0);
@@ -1283,7 +1428,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(d_scan, scan_bytes, npm, offA, (int)(nb + 1), st));
   ctx->launches += 4;
   if (ctx->prof) TC_CUDA(ctx, cudaEventRecord(ctx->ev[0], st));
-  k_accum_aff<<<blocks_for((E + T - 1) / T + nb, 128), 128, 0, st>>>(svals, d_bases, bstart, bend, toff, offA, nb, T,
+  k_accum_aff<<<blocks_for((E + T - 1) / T + nb, 128), 128, 0, st>>>(svals, bases, bstart, bend, toff, offA, nb, T,
                                                                        itemsA, buckets, d_boff, P.nbm);
   TC_LAUNCHED(ctx);
   if (ctx->prof) {

@@ -177,6 +177,41 @@ int srs_window_table(tc_ctx* ctx, tc_srs* srs, const EdPk* bases, uint64_t n, co
   return TC_OK;
 }
 
+int srs_exp_table(tc_ctx* ctx, tc_srs* srs, const EdPk* bases, uint64_t n, int depth, const EdPk** out) {
+  if (srs->exptab && srs->exptab_depth >= depth) {
+    *out = srs->exptab;
+    return TC_OK;
+  }
+  // budget: TC_EXPTAB_GB (default 96) and 8 GB of device memory left free
+  static const uint64_t cap = (getenv("TC_EXPTAB_GB") ? strtoull(getenv("TC_EXPTAB_GB"), nullptr, 10) : 96ull) << 30;
+  const uint64_t bytes = (uint64_t)depth * n * sizeof(EdPk);
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  const uint64_t have = srs->exptab ? (uint64_t)srs->exptab_depth * n * sizeof(EdPk) : 0;
+  if (bytes > cap || bytes > fr + have || fr + have - bytes < (8ull << 30)) return TC_ERR_MEMORY;
+  if (srs->exptab) {
+    TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    cudaFree(srs->exptab);
+    srs->exptab = nullptr;
+    srs->exptab_depth = 0;
+  }
+  EdPk* tab = nullptr;
+  if (cudaMalloc(&tab, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return TC_ERR_MEMORY;
+  }
+  TC_CUDA(ctx, cudaMemcpyAsync(tab, bases, n * sizeof(EdPk), cudaMemcpyDeviceToDevice, ctx->stream));
+  for (int k = 1; k < depth; k++) {
+    k_win_step<<<blocks_for((n + FB_K - 1) / FB_K, 128), 128, 0, ctx->stream>>>(tab + (uint64_t)(k - 1) * n, n, 1,
+                                                                                tab + (uint64_t)k * n);
+    TC_LAUNCHED(ctx);
+  }
+  srs->exptab = tab;
+  srs->exptab_depth = depth;
+  *out = tab;
+  return TC_OK;
+}
+
 int to_edwards_device(tc_ctx* ctx, const Aff* d_in, uint64_t n, EdPk* d_out) {
   if (n == 0) return TC_OK;
   k_to_edwards<<<blocks_for((n + FB_K - 1) / FB_K, 128), 128, 0, ctx->stream>>>(d_in, n, d_out);

@@ -70,6 +70,10 @@ struct tc_srs {
   // fixed-base window tables for full-scalar MSMs (openings): for a base range B (key:
   // its first point), FB_NDIG copies 2^(FB_C w) B, w = 0..FB_NDIG-1 (built on first use)
   std::map<const tc::EdPk*, tc::EdPk*> wintab;
+  // exponent table of the Lagrange basis for fp16 / bf16 commits (WinPlan mode 3):
+  // exptab[k n + i] = 2^k G_i, k < exptab_depth (built on first use, grown on demand)
+  tc::EdPk* exptab = nullptr;
+  int exptab_depth = 0;
   uint64_t sublag_off[TC_MAX_AXES] = {0};
 };
 
@@ -135,9 +139,15 @@ int msm_device(tc_ctx* ctx, ScalarKind kind, const void* d_scalars, const tc::Ed
 // fbw > 0: d_bases is a fixed-base window table of digit width fbw (srs_window_table,
 // fb_ndig(fbw) * n points) and the scalars are canonical F_p: every digit window shares ONE
 // set of buckets (no Horner).
+// exp_srs (optional): d_bases is exp_srs's full Edwards Lagrange basis; fp16 / bf16 batches
+// may then take the exponent-table plan (mode 3, srs_exp_table)
 int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* h_ptrs, int L,
                      const tc::EdPk* d_bases, uint64_t n, tc::Aff* d_out, const uint32_t* h_boff = nullptr,
-                     int fbw = 0);
+                     int fbw = 0, tc_srs* exp_srs = nullptr);
+
+// the exponent table of srs's Edwards Lagrange basis `bases` (n points) with >= depth levels
+// 2^k G_i (k < depth), or TC_ERR_MEMORY when it does not fit the device-memory budget
+int srs_exp_table(tc_ctx* ctx, tc_srs* srs, const tc::EdPk* bases, uint64_t n, int depth, const tc::EdPk** out);
 
 // fixed-base windowed MSMs over canonical F_p scalars: digit windows of c bits, ndig(c) =
 // ceil(163 / c) of them (162 bits + the final carry); see WinPlan mode 2 in msm.cu.

@@ -1,7 +1,5 @@
 #!/bin/bash
-# A/B environment settings on the config-3 bench: each argument is "VAR=val[,VAR=val]"
-for spec in "$@"; do
-  envs=$(echo "$spec" | tr ',' ' ')
-  env $envs python bench.py --steps 5 --warmup 2 --no-cpu --no-forward --no-monomial 2>/dev/null | tail -1 | \
-    python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$spec', round(d['ms_per_step'],3), d['roofline']['work'].split('launches, ')[1], d['root'][:16])"
+# config-3 bench under a list of environment settings (knob sweeps): ab_env.sh "A=1" "B=2 C=3" ...
+for e in "$@"; do
+  echo "== $e $(env $e python bench.py --steps 10 --warmup 3 --no-cpu --no-monomial 2>/dev/null | python -c 'import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d["ms_per_step"], d["e2e"]["value"])')"
 done
