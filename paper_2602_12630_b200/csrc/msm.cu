@@ -564,6 +564,22 @@ __global__ void __launch_bounds__(FPS_THREADS, 2) k_fpb_scatter_sorted(const voi
   const uint64_t c0 = (uint64_t)blockIdx.x * chunk;
   const uint64_t c1 = min(n, c0 + chunk);
   const void* p = ptrs[l];
+  // the next slice's fp16 / bf16 words are loaded (packed, 2 x 16 B per thread) while the
+  // current slice is ranked, scanned, staged and written (the pass was load-latency bound)
+  auto ld16 = [&](uint64_t i0, uint4& w) {
+    if (i0 + V_EPT <= c1) {
+      w = *(const uint4*)((const uint16_t*)p + i0);
+    } else {
+      uint32_t r[V_EPT];
+      load_raw8<DT>(p, i0, c1, r);
+      w = make_uint4(r[0] | r[1] << 16, r[2] | r[3] << 16, r[4] | r[5] << 16, r[6] | r[7] << 16);
+    }
+  };
+  uint4 cur[2];
+  if (c0 < c1) {
+    ld16(c0 + (uint64_t)t * V_EPT, cur[0]);
+    ld16(c0 + FPS_SLICE / 2 + (uint64_t)t * V_EPT, cur[1]);
+  }
   for (uint64_t base = c0; base < c1; base += FPS_SLICE) {
     for (uint32_t b = t; b < 2048; b += FPS_THREADS) lo[b] = 0u;
     __syncthreads();
@@ -571,13 +587,13 @@ __global__ void __launch_bounds__(FPS_THREADS, 2) k_fpb_scatter_sorted(const voi
 #pragma unroll
     for (int half = 0; half < 2; half++) {
       const uint64_t i0 = base + (uint64_t)half * (FPS_SLICE / 2) + (uint64_t)t * V_EPT;
-      uint32_t raw[V_EPT];
-      load_raw8<DT>(p, i0, c1, raw);
+      const uint32_t wv[4] = {cur[half].x, cur[half].y, cur[half].z, cur[half].w};
 #pragma unroll
       for (int k = 0; k < V_EPT; k++) {
         const int e = half * V_EPT + k;
+        const uint32_t rawk = (wv[k >> 1] >> (16 * (k & 1))) & 0xffffu;
         bool neg;
-        const uint64_t mag = (i0 + k < c1) ? quant64<DT>(raw[k], scale_bits, neg) : 0ull;
+        const uint64_t mag = (i0 + k < c1) ? quant64<DT>(rawk, scale_bits, neg) : 0ull;
         key[e] = 0xffffffffu;
         if (mag) {
           uint32_t g;
@@ -586,6 +602,10 @@ __global__ void __launch_bounds__(FPS_THREADS, 2) k_fpb_scatter_sorted(const voi
           rk[e] = atomicAdd(lo + key[e], 1u);
         }
       }
+    }
+    if (base + FPS_SLICE < c1) {
+      ld16(base + FPS_SLICE + (uint64_t)t * V_EPT, cur[0]);
+      ld16(base + FPS_SLICE + FPS_SLICE / 2 + (uint64_t)t * V_EPT, cur[1]);
     }
     __syncthreads();
     // exclusive scan of lo[0..2048): 4 counters per thread, warp shuffles, warp totals
