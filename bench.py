@@ -300,6 +300,10 @@ def main():
     per_step_elems = n_layers * elems_per_layer
 
     def prove_step(layers, route=args.route):
+        if world == 1:
+            # protocol.prover_commit: device tensors take tc_commit_tree (commitments, leaf
+            # hashes and the tree in one device pass, one readback)
+            return tcb.prover_commit(layers, srs, tree_config=tcfg, node_srs=node_srs, route=route)[1]
         comms = tcb.tc_commit_many(srs, layers, route=route)
         encs = [c.to_bytes() for c in comms]
         if world > 1:

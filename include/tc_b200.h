@@ -157,6 +157,19 @@ int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int 
                   int scale_bits, const uint8_t* omegas_le21, int route, uint8_t* out_y21,
                   uint8_t* out_pi43);
 
+/* Commitments of `count` device tensors AND their Terkle tree in one call, all on the device
+ * (protocol.prover_commit): the batched commit, the leaves
+ * hash_to_scalar(encode_elem(C_l), b"terkle/leaf") hashed on the device, the tree levels
+ * (as tc_terkle_build, Lagrange node SRS of <= 64 points), one readback.  Outputs: count x 43
+ * B commitments; node commitments level by level (bottom first, capacity *inout_node_count);
+ * every level's child values as canonical 24-byte LE limbs (leaves zero-padded to B^L first,
+ * then each upper level's; capacity *inout_value_count).  Replaces the reference-side
+ * sequence tc_commit per layer + leaf hashing + build. */
+int tc_commit_tree(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count,
+                   int dtype, int scale_bits, int route, const tc_srs* node_srs,
+                   uint8_t* out_comms43, uint8_t* out_nodes43, uint64_t* inout_node_count,
+                   uint8_t* out_values24, uint64_t* inout_value_count);
+
 /* ---- Terkle build ------------------------------------
  * leaves: n x 21 B field elements.  Pads with zeros to B^L (B = node SRS size,
  * L = max(1, ceil(log_B n))) and commits every node bottom-up; a child node enters its

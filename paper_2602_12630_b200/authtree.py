@@ -156,6 +156,23 @@ def build(config: TreeConfig, leaves, *, srs: Srs = None):
     return tree, tree.root
 
 
+def tree_from_device(config: TreeConfig, n: int, depth: int, nodes_raw: bytes, values_raw: bytes,
+                     srs: Srs) -> TerkleTree:
+    """The TerkleTree of tc_commit_tree's outputs (node encodings level by level, every
+    level's child values as 24-byte LE limbs) — the same object `build` returns."""
+    B = config.arity
+    levels, values, pos, vpos = [], [], 0, 0
+    for l in range(depth):
+        k = B ** (depth - 1 - l)
+        levels.append([decode_elem(nodes_raw[(pos + u) * ELEM_BYTES:(pos + u + 1) * ELEM_BYTES], validate=False)
+                       for u in range(k)])
+        pos += k
+        w = B ** (depth - l)
+        values.append([int.from_bytes(values_raw[24 * (vpos + j):24 * (vpos + j + 1)], "little") for j in range(w)])
+        vpos += w
+    return TerkleTree(config, n, depth, levels, values, srs)
+
+
 def prove(tree: TerkleTree, i: int) -> MembershipProof:
     """L openings, one per level."""
     if not 0 <= i < tree.n:

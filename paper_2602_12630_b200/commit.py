@@ -290,6 +290,45 @@ def tc_commit_many(srs: Srs, tensors, *, scale_bits: int = SCALE_BITS, route: st
             for i in range(len(ptrs))]
 
 
+def tc_commit_tree(srs: Srs, tensors, node_srs: Srs, *, scale_bits: int = SCALE_BITS, route: str = "auto"):
+    """Commit device tensors of the SRS's shape AND build their Terkle tree over `node_srs`
+    in one C call (tc_commit_tree: leaf hashing and every tree level on the device, one
+    readback).  Returns (commitments, node encodings, level values, depth): node encodings
+    are 43-byte commitments level by level (bottom first), level values the canonical
+    24-byte child values of every level (leaves zero-padded to B^L first)."""
+    ctx = _lib.Context.get(srs.device)
+    keeps, ptrs, dts = [], [], set()
+    for T in tensors:
+        ptr, dt, keep = _conv.device_input(T, srs.size, f"cuda:{ctx.device}")
+        ptrs.append(ptr)
+        dts.add(dt)
+        keeps.append(keep)
+    if len(dts) != 1:
+        raise ValueError("tc_commit_tree: all tensors must share one dtype")
+    B = node_srs.size
+    L, cap = 1, B
+    while cap < len(ptrs):
+        cap *= B
+        L += 1
+    n_nodes = sum(B ** (L - 1 - l) for l in range(L))
+    n_vals = sum(B ** (L - l) for l in range(L))
+    arr = (C.c_void_p * len(ptrs))(*ptrs)
+    comms = C.create_string_buffer(ELEM_BYTES * len(ptrs))
+    nodes = C.create_string_buffer(ELEM_BYTES * n_nodes)
+    vals = C.create_string_buffer(24 * n_vals)
+    cn, cv = C.c_uint64(n_nodes), C.c_uint64(n_vals)
+    with ctx.lock:
+        ctx.bind_stream()
+        ctx.check(_lib.lib().tc_commit_tree(ctx.handle, srs.handle, arr, len(ptrs), dts.pop(), scale_bits,
+                                            _route(route), node_srs.handle, comms, nodes, C.byref(cn), vals,
+                                            C.byref(cv)), "tc_commit_tree")
+    del keeps
+    raw = comms.raw
+    commitments = [Commitment(decode_elem(raw[i * ELEM_BYTES:(i + 1) * ELEM_BYTES], validate=False))
+                   for i in range(len(ptrs))]
+    return commitments, nodes.raw, vals.raw, L
+
+
 def tc_commit_stream(srs: Srs, cur, nxt=None, *, scale_bits: int = SCALE_BITS, route: str = "auto"):
     """Streaming commits of host (CPU) float tensors, one call per forward: commits `cur`
     while the upload of `nxt` (the next forward's tensors, or None) runs on the copy stream.

@@ -693,16 +693,14 @@ static int msm_srs(tc_ctx* ctx, const tc_srs* srs, int which, int dtype, int sca
   return tcrt::small_msm_device(ctx, const_cast<tc_srs*>(srs), which, fp.data(), L, d_out);
 }
 
-// count tensors of the SRS shape in one batched MSM pipeline
-static int commit_many(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype, int scale_bits,
-                       int route, uint8_t* out43) {
+// count tensors of the SRS shape in one batched MSM pipeline; points stay on the device
+static int commit_many_dev(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype,
+                           int scale_bits, int route, Aff* d_out) {
   const uint64_t n = srs->n;
   bool lag = (route == TC_ROUTE_LAGRANGE) || (route == TC_ROUTE_AUTO && srs->lagrange);
   if (lag && !srs->lagrange) return fail(ctx, TC_ERR_VALUE, "srs has no Lagrange elements");
   if (!lag && !srs->monomial) return fail(ctx, TC_ERR_VALUE, "srs has no monomial elements");
   if (count == 0) return TC_OK;
-  Aff* d_out;
-  TC_TRY(tcrt::scratch_t(ctx, "commit.out", (uint64_t)count, &d_out));
   if (lag) {
     // C_T = sum_grid T[w] * g^{L_w(tau)}: no interpolation; the raw grid values (quantised
     // inside the digit kernel for float inputs) are the scalars
@@ -729,7 +727,69 @@ static int commit_many(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins,
       TC_TRY(msm_srs(ctx, srs, TC_SRS_MONOMIAL, TC_DTYPE_FP_LIMBS, 0, ptrs.data(), gc, d_out + g0));
     }
   }
+  return TC_OK;
+}
+
+static int commit_many(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype, int scale_bits,
+                       int route, uint8_t* out43) {
+  if (count == 0) return commit_many_dev(ctx, srs, d_ins, 0, dtype, scale_bits, route, nullptr);
+  Aff* d_out;
+  TC_TRY(tcrt::scratch_t(ctx, "commit.out", (uint64_t)count, &d_out));
+  TC_TRY(commit_many_dev(ctx, srs, d_ins, count, dtype, scale_bits, route, d_out));
   return fetch_encode_many(ctx, d_out, count, out43);
+}
+
+// Terkle geometry for n leaves over a node SRS of B points: L levels, cap = B^L slots,
+// node count and child-value count over all levels
+static void terkle_geometry(uint64_t n, uint64_t B, uint64_t& L, uint64_t& cap, uint64_t& nodes, uint64_t& values) {
+  L = 1, cap = B;
+  while (cap < n) cap *= B, L++;
+  nodes = 0, values = 0;
+  uint64_t w = cap;
+  for (uint64_t l = 0; l < L; l++) values += w, w /= B, nodes += w;
+}
+
+int tc_commit_tree(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype, int scale_bits,
+                   int route, const tc_srs* node_srs, uint8_t* out_comms43, uint8_t* out_nodes43,
+                   uint64_t* inout_node_count, uint8_t* out_values24, uint64_t* inout_value_count) {
+  if (!ctx || !srs || !d_ins || !node_srs || !out_comms43 || !out_nodes43 || !inout_node_count || !out_values24 ||
+      !inout_value_count)
+    return TC_ERR_ARGUMENT;
+  if (count <= 0) return fail(ctx, TC_ERR_VALUE, "empty leaf list");
+  const uint64_t B = node_srs->n;
+  if (B < 2) return fail(ctx, TC_ERR_VALUE, "tree arity must be >= 2");
+  if (!node_srs->lagrange || B > SMALL_MSM_MAX)
+    return fail(ctx, TC_ERR_VALUE, "device tree needs a Lagrange node SRS of <= %llu points",
+                (unsigned long long)SMALL_MSM_MAX);
+  uint64_t L, cap, total_nodes, total_values;
+  terkle_geometry((uint64_t)count, B, L, cap, total_nodes, total_values);
+  if (*inout_node_count < total_nodes || *inout_value_count < total_values)
+    return fail(ctx, TC_ERR_VALUE, "need room for %llu nodes and %llu values", (unsigned long long)total_nodes,
+                (unsigned long long)total_values);
+  // commitments and node points in one buffer (one readback), leaves and level values
+  Aff* d_all;
+  Fe *d_vals, *d_levels;
+  TC_TRY(tcrt::scratch_t(ctx, "tree.pts", (uint64_t)count + total_nodes, &d_all));
+  TC_TRY(tcrt::scratch_t(ctx, "tree.vals", cap, &d_vals));
+  TC_TRY(tcrt::scratch_t(ctx, "tree.levels", total_values, &d_levels));
+  TC_TRY(commit_many_dev(ctx, srs, d_ins, count, dtype, scale_bits, route, d_all));
+  TC_TRY(tcrt::leaf_hash_device(ctx, d_all, count, cap, d_vals));
+  TC_TRY(tcrt::terkle_device(ctx, const_cast<tc_srs*>(node_srs), d_vals, cap, (int)L, d_all + count, d_levels));
+  // level values (canonical 24-byte limbs) through the staging buffer, then the points
+  for (uint64_t base = 0; base < total_values;) {
+    const uint64_t k = std::min<uint64_t>(total_values - base, ctx->h_stage_bytes / sizeof(Fe));
+    TC_CUDA(ctx, cudaMemcpyAsync(ctx->h_stage, d_levels + base, k * sizeof(Fe), cudaMemcpyDeviceToHost, ctx->stream));
+    TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    memcpy(out_values24 + 24 * base, ctx->h_stage, k * sizeof(Fe));
+    base += k;
+  }
+  std::vector<uint8_t> enc((size_t)(count + total_nodes) * 43);
+  TC_TRY(fetch_encode_many(ctx, d_all, (int)(count + total_nodes), enc.data()));
+  memcpy(out_comms43, enc.data(), (size_t)count * 43);
+  memcpy(out_nodes43, enc.data() + (size_t)count * 43, (size_t)total_nodes * 43);
+  *inout_node_count = total_nodes;
+  *inout_value_count = total_values;
+  return TC_OK;
 }
 
 int tc_commit(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int scale_bits, int route, uint8_t* out43) {

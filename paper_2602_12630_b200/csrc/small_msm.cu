@@ -116,9 +116,30 @@ __global__ void __launch_bounds__(128) k_terkle_level(const Fe* vals, uint32_t n
   }
 }
 
+// Terkle leaves on the device: vals[i] = hash_to_scalar(encode_elem(C_i), "terkle/leaf")
+// (backend.py:309-317, 346-348) for i < count, zero padding up to cap
+__global__ void k_leaf_hash(const Aff* comms, uint32_t count, uint64_t cap, Fe* vals) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= cap) return;
+  if (i >= count) {
+    vals[i] = Fe{{0, 0, 0, 0, 0, 0}};
+    return;
+  }
+  uint8_t enc[43];
+  aff_encode43(comms[i], enc);
+  const uint8_t tag[] = {'t', 'e', 'r', 'k', 'l', 'e', '/', 'l', 'e', 'a', 'f'};
+  vals[i] = hash_to_scalar(enc, 43, tag, sizeof tag);
+}
+
 }  // namespace
 
 namespace tcrt {
+
+int leaf_hash_device(tc_ctx* ctx, const Aff* d_comms, int count, uint64_t cap, Fe* d_vals) {
+  k_leaf_hash<<<blocks_for(cap, 64), 64, 0, ctx->stream>>>(d_comms, (uint32_t)count, cap, d_vals);
+  TC_LAUNCHED(ctx);
+  return TC_OK;
+}
 
 
 // build (once) the byte-window tables of the SRS's `which` elements
@@ -163,7 +184,7 @@ int small_msm_device(tc_ctx* ctx, tc_srs* srs, int which, const void* const* h_p
 // The whole Terkle tree over `cap` (= B^L, zero-padded) canonical leaf values already on
 // the device: L launches, no host synchronisation between levels; node points (level by
 // level, bottom first) in d_pts.  Lagrange node SRS (grid values are the node tensor).
-int terkle_device(tc_ctx* ctx, tc_srs* srs, Fe* d_vals, uint64_t cap, int L, Aff* d_pts) {
+int terkle_device(tc_ctx* ctx, tc_srs* srs, Fe* d_vals, uint64_t cap, int L, Aff* d_pts, Fe* d_levels) {
   const EdAff* tab;
   TC_TRY(small_tables(ctx, srs, TC_SRS_LAGRANGE, &tab));
   const uint32_t B = (uint32_t)srs->n;
@@ -171,9 +192,14 @@ int terkle_device(tc_ctx* ctx, tc_srs* srs, Fe* d_vals, uint64_t cap, int L, Aff
   Fe* nxt;
   TC_TRY(scratch_t(ctx, "terkle.next", cap / B + 1, &nxt));
   uint64_t written = 0, width = cap;
+  if (d_levels) {   // keep every level's child values: level l's inputs at d_levels + sum of wider levels
+    TC_CUDA(ctx, cudaMemcpyAsync(d_levels, d_vals, cap * sizeof(Fe), cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  uint64_t lvl_off = cap;
   for (int l = 0; l < L; l++) {
     const uint32_t nodes = (uint32_t)(width / B);
-    Fe* out_vals = (l + 1 < L) ? (cur == d_vals ? nxt : d_vals) : nullptr;
+    Fe* out_vals = (l + 1 < L) ? (d_levels ? d_levels + lvl_off : (cur == d_vals ? nxt : d_vals)) : nullptr;
+    if (l + 1 < L) lvl_off += nodes;
     k_terkle_level<<<blocks_for((uint64_t)nodes * 32, 128), 128, 0, ctx->stream>>>(cur, nodes, B, tab,
                                                                                    d_pts + written, out_vals);
     TC_LAUNCHED(ctx);

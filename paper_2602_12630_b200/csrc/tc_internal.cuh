@@ -164,7 +164,13 @@ int srs_window_table(tc_ctx* ctx, tc_srs* srs, const tc::EdPk* bases, uint64_t n
 
 // Terkle tree on the device over cap = B^L zero-padded canonical leaves (Lagrange node SRS):
 // node points level by level (bottom first) into d_pts, no host round trip between levels
-int terkle_device(tc_ctx* ctx, tc_srs* srs, tc::Fe* d_vals, uint64_t cap, int L, tc::Aff* d_pts);
+// d_levels (optional): receives every level's child values (cap + cap/B + ... + B entries,
+// bottom level first) — the tree's `values` without a host recomputation
+int terkle_device(tc_ctx* ctx, tc_srs* srs, tc::Fe* d_vals, uint64_t cap, int L, tc::Aff* d_pts,
+                  tc::Fe* d_levels = nullptr);
+// Terkle leaves hash_to_scalar(encode_elem(C_i), "terkle/leaf") of count device points,
+// zero-padded to cap
+int leaf_hash_device(tc_ctx* ctx, const tc::Aff* d_comms, int count, uint64_t cap, tc::Fe* d_vals);
 
 // Montgomery affine points -> twisted Edwards affine (x, y, t = x y), batched inversion
 int to_edwards_device(tc_ctx* ctx, const tc::Aff* d_in, uint64_t n, tc::EdPk* d_out);

@@ -9,8 +9,9 @@ import ctypes as C
 from dataclasses import dataclass
 
 from . import _conv, _lib
+from . import authtree
 from .authtree import TreeConfig, build, leaf_of
-from .commit import SCALE_BITS, tc_commit_many, tc_commit_stream
+from .commit import SCALE_BITS, tc_commit_many, tc_commit_stream, tc_commit_tree
 
 
 @dataclass
@@ -48,8 +49,20 @@ def quantize(tensor, scale_bits: int = SCALE_BITS) -> FieldTensor:
     return FieldTensor(out, tuple(tensor.shape))
 
 
+def _device_tree_ok(tensors, srs, node) -> bool:
+    """tc_commit_tree applies: CUDA tensors on the SRS's device, a Lagrange node SRS of <= 64
+    points (the device tree path of tc_terkle_build)."""
+    try:
+        import torch
+    except ImportError:
+        return False
+    if node is None or node.size > 64 or not node.has(_lib.SRS_LAGRANGE):
+        return False
+    return all(isinstance(T, torch.Tensor) and T.is_cuda and T.device.index == srs.device for T in tensors)
+
+
 def prover_commit(tensors, srs_pool, *, tree_config: TreeConfig = None, scale_bits: int = SCALE_BITS,
-                  route: str = "auto"):
+                  route: str = "auto", node_srs=None):
     """Per-layer commitments C_l = tc_commit(srs[shape_l], quantize(T_l)) and a Terkle tree
     over leaves hash_to_scalar(encode_elem(C_l), b"terkle/leaf").
 
@@ -67,13 +80,21 @@ def prover_commit(tensors, srs_pool, *, tree_config: TreeConfig = None, scale_bi
             if srs is None:
                 raise ValueError(f"no srs for tensor shape {key}")
         groups.setdefault(id(srs), (srs, []))[1].append(idx)
+    cfg = tree_config or TreeConfig()
+    if len(groups) == 1:
+        srs = next(iter(groups.values()))[0]
+        node = node_srs or authtree.node_srs(cfg, device=srs.device)
+        if _device_tree_ok(tensors, srs, node):
+            # commitments, leaf hashes and the whole tree on the device, one readback
+            commitments, nodes, vals, depth = tc_commit_tree(srs, tensors, node, scale_bits=scale_bits, route=route)
+            tree = authtree.tree_from_device(cfg, len(tensors), depth, nodes, vals, node)
+            return commitments, tree.root, tree
     commitments = [None] * len(tensors)
     for srs, idxs in groups.values():
         cs = tc_commit_many(srs, [tensors[i] for i in idxs], scale_bits=scale_bits, route=route)
         for i, c in zip(idxs, cs):
             commitments[i] = c
-    cfg = tree_config or TreeConfig()
-    tree, root = build(cfg, [leaf_of(c) for c in commitments])
+    tree, root = build(cfg, [leaf_of(c) for c in commitments], srs=node_srs)
     return commitments, root, tree
 
 

@@ -258,6 +258,32 @@ def test_prover_commit_small_layers():
     assert root_c != root
 
 
+@pytest.mark.parametrize("n_layers,node_shape", [(40, (2, 2, 2)), (3, (2, 2)), (9, (3, 3))])
+def test_prover_commit_device_tree_matches_host_build(n_layers, node_shape):
+    """tc_commit_tree (commitments, device leaf hashing and every tree level in one call, the
+    path prover_commit takes for CUDA tensors) gives the same commitments, node points, level
+    values and root as tc_commit_many + host leaf hashing + build, on ragged leaf counts
+    (zero padding), and its membership proofs verify."""
+    tcb = T()
+    shape = (4, 8, 16)
+    srs, td = tcb.setup_srs(shape, b"device-tree")
+    cfg = tcb.TreeConfig(shape=node_shape)
+    node = tcb.authtree.node_srs(cfg, device=0)
+    g = np.random.default_rng(61)
+    xs = [torch.from_numpy((g.standard_t(3, 512) * (0.5 + l % 4)).astype(np.float16)).cuda() for l in range(n_layers)]
+    comms, root, tree = tcb.prover_commit(xs, srs, tree_config=cfg, node_srs=node)
+    comms_h = tcb.tc_commit_many(srs, xs)
+    assert comms == comms_h
+    leaves = [tcb.leaf_of(c) for c in comms_h]
+    assert leaves == [O.leaf_of_commitment(c.elem) for c in comms_h]
+    tree_h, root_h = tcb.build(cfg, leaves, srs=node)
+    assert root == root_h
+    assert tree.levels == tree_h.levels and tree.values == tree_h.values and tree.depth == tree_h.depth
+    for i in sorted({0, n_layers // 2, n_layers - 1}):
+        pf = tcb.prove(tree, i)
+        assert tcb.verify(root, i, leaves[i], pf, cfg, srs=node)
+
+
 @pytest.mark.parametrize("group", [0, 1, 2, 5])
 @pytest.mark.parametrize("pinned", [True, False])
 def test_commit_many_host_inputs_pipelined(group, pinned):
