@@ -170,6 +170,14 @@ int tc_commit_tree(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int
                    uint8_t* out_comms43, uint8_t* out_nodes43, uint64_t* inout_node_count,
                    uint8_t* out_values24, uint64_t* inout_value_count);
 
+/* tc_commit_stream + the device tree of tc_commit_tree, one call per forward
+ * (protocol.prover_commit_stream). */
+int tc_commit_stream_tree(tc_ctx* ctx, const tc_srs* srs, const void* const* h_cur,
+                          const void* const* h_next, int count, int dtype, int scale_bits, int route,
+                          const tc_srs* node_srs, uint8_t* out_comms43, uint8_t* out_nodes43,
+                          uint64_t* inout_node_count, uint8_t* out_values24,
+                          uint64_t* inout_value_count);
+
 /* ---- Terkle build ------------------------------------
  * leaves: n x 21 B field elements.  Pads with zeros to B^L (B = node SRS size,
  * L = max(1, ceil(log_B n))) and commits every node bottom-up; a child node enters its

@@ -74,6 +74,8 @@ _SIGS = [
     ("tc_terkle_build", C.c_int, [_P, _P, C.c_char_p, C.c_uint64, _P, C.POINTER(C.c_uint64)]),
     ("tc_commit_tree", C.c_int, [_P, _P, C.POINTER(_P), C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, _P,
                                  C.POINTER(C.c_uint64), _P, C.POINTER(C.c_uint64)]),
+    ("tc_commit_stream_tree", C.c_int, [_P, _P, C.POINTER(_P), C.POINTER(_P), C.c_int, C.c_int, C.c_int, C.c_int,
+                                        _P, _P, _P, C.POINTER(C.c_uint64), _P, C.POINTER(C.c_uint64)]),
     ("tc_pairing", C.c_int, [C.c_char_p, C.c_char_p, _P]),
     ("tc_verify_host", C.c_int, [C.c_int, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(C.c_int)]),
     ("tc_host_hash_to_scalar", C.c_int, [C.c_char_p, C.c_uint32, C.c_char_p, C.c_uint32, _P]),

@@ -290,6 +290,25 @@ def tc_commit_many(srs: Srs, tensors, *, scale_bits: int = SCALE_BITS, route: st
             for i in range(len(ptrs))]
 
 
+def _tree_buffers(count: int, B: int):
+    """Output buffers of the device tree calls for `count` leaves over arity B."""
+    L, cap = 1, B
+    while cap < count:
+        cap *= B
+        L += 1
+    n_nodes = sum(B ** (L - 1 - l) for l in range(L))
+    n_vals = sum(B ** (L - l) for l in range(L))
+    return (L, C.create_string_buffer(ELEM_BYTES * count), C.create_string_buffer(ELEM_BYTES * n_nodes),
+            C.create_string_buffer(24 * n_vals), C.c_uint64(n_nodes), C.c_uint64(n_vals))
+
+
+def _tree_result(count, L, comms, nodes, vals):
+    raw = comms.raw
+    commitments = [Commitment(decode_elem(raw[i * ELEM_BYTES:(i + 1) * ELEM_BYTES], validate=False))
+                   for i in range(count)]
+    return commitments, nodes.raw, vals.raw, L
+
+
 def tc_commit_tree(srs: Srs, tensors, node_srs: Srs, *, scale_bits: int = SCALE_BITS, route: str = "auto"):
     """Commit device tensors of the SRS's shape AND build their Terkle tree over `node_srs`
     in one C call (tc_commit_tree: leaf hashing and every tree level on the device, one
@@ -305,36 +324,18 @@ def tc_commit_tree(srs: Srs, tensors, node_srs: Srs, *, scale_bits: int = SCALE_
         keeps.append(keep)
     if len(dts) != 1:
         raise ValueError("tc_commit_tree: all tensors must share one dtype")
-    B = node_srs.size
-    L, cap = 1, B
-    while cap < len(ptrs):
-        cap *= B
-        L += 1
-    n_nodes = sum(B ** (L - 1 - l) for l in range(L))
-    n_vals = sum(B ** (L - l) for l in range(L))
+    L, comms, nodes, vals, cn, cv = _tree_buffers(len(ptrs), node_srs.size)
     arr = (C.c_void_p * len(ptrs))(*ptrs)
-    comms = C.create_string_buffer(ELEM_BYTES * len(ptrs))
-    nodes = C.create_string_buffer(ELEM_BYTES * n_nodes)
-    vals = C.create_string_buffer(24 * n_vals)
-    cn, cv = C.c_uint64(n_nodes), C.c_uint64(n_vals)
     with ctx.lock:
         ctx.bind_stream()
         ctx.check(_lib.lib().tc_commit_tree(ctx.handle, srs.handle, arr, len(ptrs), dts.pop(), scale_bits,
                                             _route(route), node_srs.handle, comms, nodes, C.byref(cn), vals,
                                             C.byref(cv)), "tc_commit_tree")
     del keeps
-    raw = comms.raw
-    commitments = [Commitment(decode_elem(raw[i * ELEM_BYTES:(i + 1) * ELEM_BYTES], validate=False))
-                   for i in range(len(ptrs))]
-    return commitments, nodes.raw, vals.raw, L
+    return _tree_result(len(ptrs), L, comms, nodes, vals)
 
 
-def tc_commit_stream(srs: Srs, cur, nxt=None, *, scale_bits: int = SCALE_BITS, route: str = "auto"):
-    """Streaming commits of host (CPU) float tensors, one call per forward: commits `cur`
-    while the upload of `nxt` (the next forward's tensors, or None) runs on the copy stream.
-    `cur` is consumed from the prefetched device slot when it is the previous call's `nxt`.
-    Tensors passed as `nxt` must not change until the call that commits them returns."""
-    ctx = _lib.Context.get(srs.device)
+def _stream_args(srs: Srs, cur, nxt):
     hc = _host_floats(list(cur))
     if hc is None:
         raise ValueError("tc_commit_stream: cur must be CPU float tensors of one dtype")
@@ -351,6 +352,31 @@ def tc_commit_stream(srs: Srs, cur, nxt=None, *, scale_bits: int = SCALE_BITS, r
         if any(t.numel() != srs.size for t in hn[0]):
             raise ValueError("tensor size does not match grid shape")
         narr = (C.c_void_p * len(ts))(*[t.data_ptr() for t in hn[0]])
+    return ts, code, arr, narr
+
+
+def tc_commit_stream_tree(srs: Srs, cur, nxt, node_srs: Srs, *, scale_bits: int = SCALE_BITS,
+                          route: str = "auto"):
+    """tc_commit_stream and the Terkle tree of its commitments on the device in one call
+    (tc_commit_stream_tree); returns what tc_commit_tree returns."""
+    ctx = _lib.Context.get(srs.device)
+    ts, code, arr, narr = _stream_args(srs, cur, nxt)
+    L, comms, nodes, vals, cn, cv = _tree_buffers(len(ts), node_srs.size)
+    with ctx.lock:
+        ctx.bind_stream()
+        ctx.check(_lib.lib().tc_commit_stream_tree(ctx.handle, srs.handle, arr, narr, len(ts), code, scale_bits,
+                                                   _route(route), node_srs.handle, comms, nodes, C.byref(cn),
+                                                   vals, C.byref(cv)), "tc_commit_stream_tree")
+    return _tree_result(len(ts), L, comms, nodes, vals)
+
+
+def tc_commit_stream(srs: Srs, cur, nxt=None, *, scale_bits: int = SCALE_BITS, route: str = "auto"):
+    """Streaming commits of host (CPU) float tensors, one call per forward: commits `cur`
+    while the upload of `nxt` (the next forward's tensors, or None) runs on the copy stream.
+    `cur` is consumed from the prefetched device slot when it is the previous call's `nxt`.
+    Tensors passed as `nxt` must not change until the call that commits them returns."""
+    ctx = _lib.Context.get(srs.device)
+    ts, code, arr, narr = _stream_args(srs, cur, nxt)
     out = C.create_string_buffer(ELEM_BYTES * len(ts))
     with ctx.lock:
         ctx.bind_stream()

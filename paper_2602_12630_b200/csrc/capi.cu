@@ -749,9 +749,10 @@ static void terkle_geometry(uint64_t n, uint64_t B, uint64_t& L, uint64_t& cap, 
   for (uint64_t l = 0; l < L; l++) values += w, w /= B, nodes += w;
 }
 
-int tc_commit_tree(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype, int scale_bits,
-                   int route, const tc_srs* node_srs, uint8_t* out_comms43, uint8_t* out_nodes43,
-                   uint64_t* inout_node_count, uint8_t* out_values24, uint64_t* inout_value_count) {
+static int commit_tree_impl(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype,
+                            int scale_bits, int route, const tc_srs* node_srs, uint8_t* out_comms43,
+                            uint8_t* out_nodes43, uint64_t* inout_node_count, uint8_t* out_values24,
+                            uint64_t* inout_value_count) {
   if (!ctx || !srs || !d_ins || !node_srs || !out_comms43 || !out_nodes43 || !inout_node_count || !out_values24 ||
       !inout_value_count)
     return TC_ERR_ARGUMENT;
@@ -790,6 +791,13 @@ int tc_commit_tree(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int
   *inout_node_count = total_nodes;
   *inout_value_count = total_values;
   return TC_OK;
+}
+
+int tc_commit_tree(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype, int scale_bits,
+                   int route, const tc_srs* node_srs, uint8_t* out_comms43, uint8_t* out_nodes43,
+                   uint64_t* inout_node_count, uint8_t* out_values24, uint64_t* inout_value_count) {
+  return commit_tree_impl(ctx, srs, d_ins, count, dtype, scale_bits, route, node_srs, out_comms43, out_nodes43,
+                          inout_node_count, out_values24, inout_value_count);
 }
 
 int tc_commit(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int scale_bits, int route, uint8_t* out43) {
@@ -886,10 +894,10 @@ static int slot_upload(tc_ctx* ctx, int s, const void* const* h, int count, int 
 // consumed from the slot a previous call prefetched it into (same pointers, count, dtype),
 // else uploaded now.  Host buffers passed as h_next must not change until the call that
 // commits them returns.
-int tc_commit_stream(tc_ctx* ctx, const tc_srs* srs, const void* const* h_cur, const void* const* h_next, int count,
-                     int dtype, int scale_bits, int route, uint8_t* out43) {
-  if (!ctx || !srs || !h_cur || !out43 || count < 0) return TC_ERR_ARGUMENT;
-  if (count == 0) return TC_OK;
+// device pointers of this forward's tensors (from the prefetched slot, or uploaded now) and
+// the next forward's upload started on the copy stream
+static int stream_prepare(tc_ctx* ctx, const tc_srs* srs, const void* const* h_cur, const void* const* h_next,
+                          int count, int dtype, std::vector<const void*>& ptrs) {
   size_t esz;
   if (dtype_size(dtype, &esz)) return fail(ctx, TC_ERR_ARGUMENT, "commit_stream: unsupported dtype %d", dtype);
   for (int i = 0; i < count; i++)
@@ -924,9 +932,29 @@ int tc_commit_stream(tc_ctx* ctx, const tc_srs* srs, const void* const* h_cur, c
     TC_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, o.ready, 0));
     TC_TRY(slot_upload(ctx, 1 - s, h_next, count, dtype, n, esz));
   }
-  std::vector<const void*> ptrs(count);
+  ptrs.resize(count);
   for (int i = 0; i < count; i++) ptrs[i] = cur + (size_t)n * esz * i;
+  return TC_OK;
+}
+
+int tc_commit_stream(tc_ctx* ctx, const tc_srs* srs, const void* const* h_cur, const void* const* h_next, int count,
+                     int dtype, int scale_bits, int route, uint8_t* out43) {
+  if (!ctx || !srs || !h_cur || !out43 || count < 0) return TC_ERR_ARGUMENT;
+  if (count == 0) return TC_OK;
+  std::vector<const void*> ptrs;
+  TC_TRY(stream_prepare(ctx, srs, h_cur, h_next, count, dtype, ptrs));
   return commit_many(ctx, srs, ptrs.data(), count, dtype, scale_bits, route, out43);
+}
+
+int tc_commit_stream_tree(tc_ctx* ctx, const tc_srs* srs, const void* const* h_cur, const void* const* h_next,
+                          int count, int dtype, int scale_bits, int route, const tc_srs* node_srs,
+                          uint8_t* out_comms43, uint8_t* out_nodes43, uint64_t* inout_node_count,
+                          uint8_t* out_values24, uint64_t* inout_value_count) {
+  if (!ctx || !srs || !h_cur || count <= 0) return TC_ERR_ARGUMENT;
+  std::vector<const void*> ptrs;
+  TC_TRY(stream_prepare(ctx, srs, h_cur, h_next, count, dtype, ptrs));
+  return commit_tree_impl(ctx, srs, ptrs.data(), count, dtype, scale_bits, route, node_srs, out_comms43,
+                          out_nodes43, inout_node_count, out_values24, inout_value_count);
 }
 
 // L_k(omega_a) (canonical) and 1 / (k + 1 - omega_a) for every axis, concatenated

@@ -11,7 +11,7 @@ from dataclasses import dataclass
 from . import _conv, _lib
 from . import authtree
 from .authtree import TreeConfig, build, leaf_of
-from .commit import SCALE_BITS, tc_commit_many, tc_commit_stream, tc_commit_tree
+from .commit import SCALE_BITS, tc_commit_many, tc_commit_stream, tc_commit_stream_tree, tc_commit_tree
 
 
 @dataclass
@@ -114,7 +114,15 @@ def prover_commit_stream(batches, srs, *, tree_config: TreeConfig = None, node_s
             nxt = list(next(it))
         except StopIteration:
             nxt = None
-        commitments = tc_commit_stream(srs, cur, nxt, scale_bits=scale_bits, route=route)
-        tree, root = build(cfg, [leaf_of(c) for c in commitments], srs=node_srs)
-        yield commitments, root, tree
+        node = node_srs or authtree.node_srs(cfg, device=srs.device)
+        if node.size <= 64 and node.has(_lib.SRS_LAGRANGE):
+            # commitments, leaf hashes and the tree on the device, one readback per forward
+            commitments, nodes, vals, depth = tc_commit_stream_tree(srs, cur, nxt, node, scale_bits=scale_bits,
+                                                                    route=route)
+            tree = authtree.tree_from_device(cfg, len(commitments), depth, nodes, vals, node)
+            yield commitments, tree.root, tree
+        else:
+            commitments = tc_commit_stream(srs, cur, nxt, scale_bits=scale_bits, route=route)
+            tree, root = build(cfg, [leaf_of(c) for c in commitments], srs=node)
+            yield commitments, root, tree
         cur = nxt
