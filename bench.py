@@ -450,8 +450,8 @@ def main():
                          "achieved": achieved, "peak": peak_tops, "unit": "T word-mul/s",
                          "frac": (achieved / peak_tops) if achieved and peak_tops else None, "traffic": traffic,
                          "traffic_note": "dram read+write bytes per launch of the same kernel on the same workload, "
-                                         "profiles/r01_ncu_accum_summary.txt (random gathers of 80-B Edwards "
-                                         "(x, y, xy) points, 3 sectors each, L2 hit ~30 %: the kernel is "
+                                         "profiles/r01_ncu_accum_summary.txt (random gathers of 64-B packed Edwards "
+                                         "(x, y, xy) points 2^g G_i from the exponent table, L2 hit ~30 %: the kernel is "
                                          "fma-heavy-pipe bound, not DRAM bound)",
                          "hw_pipe": "fma-heavy pipe ~84 % busy (ncu sm__pipe_fmaheavy_cycles_active)",
                          "work": f"{st['units']:.0f} bucket entries x {WORD_MULS_PER_ADD} word-muls "
