@@ -1203,7 +1203,8 @@ int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int 
           hp[cp * d0 + c] = (const uint8_t*)job_h[jb] + esz * R * cp;
           boff[cp * d0 + c] = (uint32_t)(R * c);
         }
-      TC_TRY(tcrt::msm_batch_device(ctx, dtype, scale_bits, hp.data(), (int)nh, ed_lag, R, hpts, boff.data()));
+      TC_TRY(tcrt::msm_batch_device(ctx, dtype, scale_bits, hp.data(), (int)nh, ed_lag, R, hpts, boff.data(), 0,
+                                    const_cast<tc_srs*>(srs)));
       TC_TRY(tcrt::to_edwards_device(ctx, hpts, nh, hed));
     }
     // sliced jobs keep only the quotients of axes >= 1 (n / d0 + ... per opening), packed

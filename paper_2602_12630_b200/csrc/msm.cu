@@ -68,6 +68,7 @@ struct WinPlan {
   uint8_t width[MAXW];       // mode 0: c_w
   uint32_t mlo[MAXW];        // weight of the window's first bucket (mode 0: 1)
   uint32_t base[MAXW + 1];   // first bucket of window w inside one MSM
+  uint32_t tpitch;           // mode 3: points per exponent-table level (entry = g tpitch + i)
 };
 
 __device__ __forceinline__ uint32_t bitlen6(const Fe& a) {
@@ -530,7 +531,7 @@ __global__ void __launch_bounds__(1024) k_fpb_pass(const void* const* ptrs, uint
         uint32_t g;
         const uint32_t slot = atomicAdd(h + fp_key(P, mag, g), 1u);
         // mode 3 entries index the exponent table: 2^g G_i at g n + i
-        if (SCATTER) vals[slot] = ((P.mode == 3 ? g * (uint32_t)n : 0u) + (uint32_t)(i0 + k)) | (neg ? SIGN_BIT : 0u);
+        if (SCATTER) vals[slot] = ((P.mode == 3 ? g * P.tpitch : 0u) + (uint32_t)(i0 + k)) | (neg ? SIGN_BIT : 0u);
       }
     }
   }
@@ -598,7 +599,7 @@ __global__ void __launch_bounds__(FPS_THREADS, 2) k_fpb_scatter_sorted(const voi
         if (mag) {
           uint32_t g;
           key[e] = fp_key(P, mag, g);
-          val[e] = (g * (uint32_t)n + (uint32_t)(i0 + k)) | (neg ? SIGN_BIT : 0u);
+          val[e] = (g * P.tpitch + (uint32_t)(i0 + k)) | (neg ? SIGN_BIT : 0u);
           rk[e] = atomicAdd(lo + key[e], 1u);
         }
       }
@@ -1058,8 +1059,9 @@ WinPlan plan_fp(uint32_t nbits, int mb) {
 
 // mode 3: the float-exponent plan over an exponent table (srs_exp_table): entry (i, g)
 // reads the base 2^g G_i, so all groups share ONE window of 2^mb - 1 buckets of weight m
-WinPlan plan_fpx(int mb) {
+WinPlan plan_fpx(int mb, uint32_t pitch) {
   WinPlan P;
+  P.tpitch = pitch;
   P.mode = 3;
   P.ndig = P.cdig = 0;
   P.mbits = mb;
@@ -1185,16 +1187,22 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   const int fp_mb = dtype == TC_DTYPE_F16 ? 11 : (dtype == TC_DTYPE_BF16 ? 8 : 0);
   const bool fpmode = vec_ok && fp_mb && n >= FP_MIN_N && (int)nbits - fp_mb + 1 <= MAXW;
   WinPlan P = fbw ? plan_fb(fbw) : fpmode ? plan_fp(nbits, fp_mb) : plan_windows(hist, nbits, (uint64_t)L);
-  // exponent-table plan (mode 3) when the caller's bases are a whole Lagrange basis and its
-  // table (depth = the batch's groups) fits in memory
+  P.tpitch = 0;
+  // exponent-table plan (mode 3) when the caller's bases lie in a Lagrange basis whose table
+  // (depth = the batch's exponent groups) fits in memory; its 2^mb - 1 buckets per MSM pay
+  // off from a few times that many points (slice commitments: 1024 MSMs of 65536)
   static const bool no_exp = getenv("TC_MSM_NO_EXPTAB") != nullptr;
+  static const uint64_t EXP_MIN_N =
+      getenv("TC_MSM_EXP_MIN_N") ? strtoull(getenv("TC_MSM_EXP_MIN_N"), nullptr, 10) : (1ull << 14);
   const EdPk* bases = d_bases;
-  if (fpmode && !fbw && exp_srs && !h_boff && !no_exp && !getenv("TC_MSM_NO_BLKCNT")) {
-    const int depth = P.nwin;
+  const int groups = fp_mb ? std::max(1, (int)nbits - fp_mb + 1) : 0;
+  if (!fbw && exp_srs && d_bases == exp_srs->ed_lagrange && !no_exp && !getenv("TC_MSM_NO_BLKCNT") && vec_ok &&
+      fp_mb && n >= EXP_MIN_N &&
+      groups <= MAXW && (uint64_t)groups * exp_srs->n < (1ull << 31)) {
     const EdPk* tab = nullptr;
-    if ((uint64_t)depth * n < (1ull << 31) && srs_exp_table(ctx, exp_srs, d_bases, n, depth, &tab) == TC_OK) {
-      P = plan_fpx(fp_mb);
-      bases = tab;
+    if (srs_exp_table(ctx, exp_srs, d_bases, exp_srs->n, groups, &tab) == TC_OK) {
+      P = plan_fpx(fp_mb, (uint32_t)exp_srs->n);
+      bases = tab;   // multi-base batches (h_boff) index inside the table's level 0 as before
     }
   }
   if (P.nwin > MAXW) return fail(ctx, TC_ERR_VALUE, "msm: window plan too long");
