@@ -441,12 +441,16 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("env", [{}, {"TC_MSM_NO_BLKCNT": "1"}, {"TC_MSM_FPB_LG": "1"}, {"TC_MSM_FPB_LG": "3"}])
+@pytest.mark.parametrize("env", [{}, {"TC_MSM_NO_SORTED_SCATTER": "1"}, {"TC_MSM_FPB_LG": "1"}, {"TC_MSM_FPB_LG": "3"},
+                                 {"TC_MSM_NO_EXPTAB": "1"}, {"TC_EXPTAB_GB": "0"},
+                                 {"TC_MSM_NO_EXPTAB": "1", "TC_MSM_FPB_LG": "3"}, {"TC_MSM_NO_BLKCNT": "1"}])
 def test_msm_counting_sort_paths(env, tmp_path):
-    """The float-exponent plan's two counting sorts — block-private bucket counters with the
-    scatter launched LG MSMs at a time (several chunks per MSM, ragged last launch), and the
-    global-atomic counters — give commitments equal to the trapdoor oracle on a batch of six
-    65536-element fp16 tensors (tiny, large, all-zero, sparse, max / min-subnormal values)."""
+    """Every fp16 commit plan and counting sort gives commitments equal to the trapdoor oracle
+    on a batch of six 65536-element fp16 tensors (tiny, large, all-zero, sparse, max /
+    min-subnormal values): the exponent-table plan (mode 3) with the slice-sorted scatter or
+    the plain block-private one and several scatter groupings (ragged last launch); the
+    float-exponent groups (mode 1) when the table is disabled or over its memory budget, with
+    block-private counters; the global-atomic counters."""
     import os
     import subprocess
     import sys
