@@ -9,13 +9,16 @@
 //   1. k_scan_bits(_v) — exact maximum bit length + quantisation errors of the scalars
 //                       (canonical F_p limbs, or raw floats quantised on the fly: K1 is
 //                       fused into the MSM), bit-length histogram on a sample
-//   2. window plan    — (host) mode 1 float-exponent groups for large fp16 / bf16 batches
-//                       (one bucket entry per element), mode 2 fixed-base digit windows over
-//                       a window table (opening quotients), else signed windows from a DP
-//                       over the histogram (#non-zero digits + kappa * #buckets)
-//   3. counting sort  — count entries per bucket (k_digits_fp / k_digits_v / k_count_digits,
-//                       RED atomics into 16 counter copies for mode 1), exclusive scan, and
-//                       scatter (point index | sign << 31) into bucket slices
+//   2. window plan    — (host) mode 3: fp16 / bf16 over the SRS's exponent table (one
+//                       entry per element, one window of 2^MB - 1 buckets), mode 1
+//                       float-exponent groups when the table does not fit, mode 2 fixed-base
+//                       digit windows over a window table (opening quotients), else signed
+//                       windows from a DP over the histogram (#digits + kappa * #buckets)
+//   3. counting sort  — count entries per bucket, exclusive scan, scatter (table index |
+//                       sign << 31) into bucket slices: block-private shared-memory counters
+//                       (k_fpb_pass, k_fpb_scatter_sorted) for modes 3 / 1, RED atomics
+//                       into counter copies otherwise (k_digits_fp / k_digits_v /
+//                       k_count_digits)
 //   4. levels         — load-balanced segmented reduction: buckets are cut into pieces of
 //                       <= T entries (one thread per piece, extended twisted Edwards
 //                       accumulator, complete 8M mixed adds with lazy reduction, ec.cuh);
@@ -54,6 +57,9 @@ constexpr uint32_t HIST_SAMPLE = 8;   // histogram taken on every 8th element (k
 //         of fp16 (a signed-window plan of the same data leaves ~85% of its 2^17 low-window
 //         buckets empty: fp16 has 1024 mantissas per octave).  Bucket j of group w holds
 //         weight mlo[w] + j; the groups are combined with weight 2^off[w] (off[w] = w).
+// mode 3: mode 1 with the exponent in the base: entry (i, g) reads 2^g G_i from the SRS's
+//         exponent table (srs_exp_table, level pitch tpitch), so every group shares ONE
+//         window of 2^MB - 1 buckets of weight m.
 // mode 2: fixed-base windows (openings: canonical F_p scalars against an SRS range with a
 //         window table, srs_window_table).  The scalar's ndig signed digits of cdig bits
 //         index the table copies 2^(cdig w) B, so all digits share ONE window of buckets:
@@ -457,11 +463,10 @@ __global__ void k_copy_starts(const uint32_t* S, uint32_t nb, uint32_t nc, uint3
 template <int DT, bool SCATTER>
 __global__ void __launch_bounds__(256) k_digits_fp(const void* const* ptrs, uint64_t n, int scale_bits, WinPlan P,
                                                    uint32_t* __restrict__ cnt, uint32_t* __restrict__ vals,
-                                                   uint32_t nc, uint64_t chunk) {
+                                                   uint32_t nc) {
   const uint32_t l = blockIdx.y;
   const uint64_t i0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * V_EPT;
-  // counter copy: by block (interleaved copies) or by chunk (counts from k_count_fpb)
-  const uint32_t key0 = l * P.nbm, copy = chunk ? (uint32_t)(i0 / chunk) : blockIdx.x % nc;
+  const uint32_t key0 = l * P.nbm, copy = blockIdx.x % nc;
   uint32_t raw[V_EPT], ctr[V_EPT], val[V_EPT];
   load_raw8<DT>(ptrs[l], i0, n, raw);
   uint32_t live = 0;
@@ -1365,7 +1370,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     if constexpr (D >= 1 && D <= 3) {
       if (fast) {
         if (P.mode == 1) {
-          k_digits_fp<D, false><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cnt, nullptr, NC, 0);
+          k_digits_fp<D, false><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cnt, nullptr, NC);
         } else {
           k_digits_v<D, false><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, H, cnt, nullptr, NC);
         }
@@ -1397,7 +1402,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     if constexpr (D >= 1 && D <= 3) {
       if (fast) {
         if (P.mode == 1)
-          k_digits_fp<D, true><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cursor, vals, NC, 0);
+          k_digits_fp<D, true><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cursor, vals, NC);
         else
           k_digits_v<D, true><<<dim3(gxv, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, H, cursor, vals, NC);
         return;
