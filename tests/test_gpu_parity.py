@@ -86,6 +86,28 @@ def test_quantize_spec_examples_and_errors():
     assert tcb.quantize(torch.tensor([big, -big], dtype=torch.float32)).tolist() == O.quantize(np.array([big, -big]), 16)
 
 
+@pytest.mark.parametrize("n", [512, 65536])
+def test_commit_rejects_non_finite_and_recovers(n):
+    """A NaN / inf activation makes tc_commit / prover_commit raise ValueError (SPEC.md:536-544
+    quantisation errors) on every MSM plan — small batches plan after reading the scan back,
+    65536-element fp16 batches run the exponent-table plan speculatively and check the scan's
+    flags with the entry count — and the context keeps working afterwards."""
+    tcb = T()
+    shape = (8, 8, 8) if n == 512 else (16, 16, 16, 16)
+    srs, td = tcb.setup_srs(shape, b"non-finite")
+    g = np.random.default_rng(71)
+    good = torch.from_numpy(g.standard_t(3, n).astype(np.float16)).cuda()
+    for bad_val in (float("nan"), float("inf"), -float("inf")):
+        bad = good.clone()
+        bad[n // 3] = bad_val
+        with pytest.raises(ValueError):
+            tcb.tc_commit(srs, bad)
+        with pytest.raises(ValueError):
+            tcb.prover_commit([good, bad], srs)
+    vals = O.quantize(good.cpu().numpy().astype(np.float64), 16)
+    assert tcb.tc_commit(srs, good).elem == O.commit_trapdoor(vals, shape, list(td.taus))
+
+
 # ---------------------------------------------------------------- K2 / K4 polynomial engine
 @pytest.mark.parametrize("case", load("mvpoly.json"), ids=lambda c: "x".join(map(str, c["shape"])))
 def test_mvpoly_device_golden(case):
