@@ -12,6 +12,9 @@ LIMBS = 6
 _FLOAT_DTYPES = None
 
 
+_DEVICES = {}   # device argument -> torch.device (parsing a device string per call is not free)
+
+
 def _float_codes():
     global _FLOAT_DTYPES
     if _FLOAT_DTYPES is None:
@@ -69,6 +72,15 @@ def device_input(T, n: int, device):
     """
     import torch
 
+    if isinstance(T, torch.Tensor):
+        codes = _float_codes()
+        if T.dtype in codes and T.numel() == n and T.is_contiguous():
+            dev = _DEVICES.get(device)
+            if dev is None:
+                dev = _DEVICES[device] = torch.device(device) if isinstance(device, str) else device
+            if T.device == dev:
+                # already resident and dense (the per-forward hot path): no .to() dispatch
+                return T.data_ptr(), codes[T.dtype], T
     if hasattr(T, "limbs") and isinstance(getattr(T, "limbs"), torch.Tensor):
         lt = T.limbs
         if lt.shape[0] != n:
