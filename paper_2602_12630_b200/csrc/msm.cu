@@ -733,7 +733,7 @@ __device__ __forceinline__ uint32_t find_bucket(const uint32_t* off, uint32_t nb
 // items.  The accumulator starts as the piece's first point, then one complete 8M mixed
 // add per entry (no exceptional cases, ec.cuh).
 #ifndef TC_ACCUM_MINB
-#define TC_ACCUM_MINB 6   // min resident blocks per SM for k_accum_aff: caps registers at 80 (A/B: 1 -> 4.72 ms @104 regs, 6 -> 4.40 ms, 7 -> 4.52, 8 -> 4.51)
+#define TC_ACCUM_MINB 5   // min resident blocks per SM for k_accum_aff: 92 registers, no spills (exponent-table plan A/B: 3-4 -> 4.03 ms @94 regs, 5 -> 4.02, 6 -> 4.07 @80 regs + 40 B spills, 7 -> 4.15, 8 -> 4.35)
 #endif
 __global__ void __launch_bounds__(128, TC_ACCUM_MINB) k_accum_aff(const uint32_t* vals, const EdPk* bases, const uint32_t* bstart,
                                                    const uint32_t* bend, const uint32_t* toff, const uint32_t* ooff,
