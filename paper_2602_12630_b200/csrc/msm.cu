@@ -516,7 +516,7 @@ __device__ __forceinline__ uint32_t fp_key(const WinPlan& P, uint64_t mag, uint3
 template <int DT, bool SCATTER>
 __global__ void __launch_bounds__(1024) k_fpb_pass(const void* const* ptrs, uint64_t n, int scale_bits, WinPlan P,
                                                    uint32_t* __restrict__ cnt, uint32_t* __restrict__ vals,
-                                                   uint64_t chunk, uint32_t l0) {
+                                                   uint64_t chunk, uint32_t l0, uint32_t* flags) {
   extern __shared__ uint32_t h[];
   const uint32_t l = l0 + blockIdx.y, S = gridDim.x;
   const uint64_t c0 = (uint64_t)blockIdx.x * chunk;
@@ -525,11 +525,13 @@ __global__ void __launch_bounds__(1024) k_fpb_pass(const void* const* ptrs, uint
   uint32_t* row = cnt + ((uint64_t)l * S + blockIdx.x) * P.nbm;
   for (uint32_t b = threadIdx.x; b < P.nbm; b += blockDim.x) h[b] = SCATTER ? row[b] : 0u;
   __syncthreads();
+  uint32_t nf = 0;   // fused scan (speculative fp16 plan): non-finite inputs
   for (uint64_t i0 = c0 + (uint64_t)threadIdx.x * V_EPT; i0 < c1; i0 += (uint64_t)blockDim.x * V_EPT) {
     uint32_t raw[V_EPT];
     load_raw8<DT>(p, i0, c1, raw);
 #pragma unroll
     for (int k = 0; k < V_EPT; k++) {
+      if (!SCATTER && DT == 1 && (raw[k] & 0x7c00u) == 0x7c00u) nf = 1u;
       bool neg;
       const uint64_t mag = (i0 + k < c1) ? quant64<DT>(raw[k], scale_bits, neg) : 0ull;
       if (mag) {
@@ -541,6 +543,7 @@ __global__ void __launch_bounds__(1024) k_fpb_pass(const void* const* ptrs, uint
     }
   }
   if (SCATTER) return;
+  if (flags && __any_sync(0xffffffffu, nf) && (threadIdx.x & 31) == 0) atomicOr(flags, QF_NONFINITE);
   __syncthreads();
   for (uint32_t b = threadIdx.x; b < P.nbm; b += blockDim.x) row[b] = h[b];
 }
@@ -1150,7 +1153,24 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   const int NSMALL = NHIST + 8;
   TC_TRY(scratch_t(ctx, "msm.small", NSMALL, &d_small));
   TC_CUDA(ctx, cudaMemsetAsync(d_small, 0, NSMALL * sizeof(uint32_t), st));
-  {
+  // fp16 over an exponent table deep enough for ANY finite input (|q| < 2^(16 + scale_bits):
+  // scale_bits + 6 groups) needs nothing from the scan: the plan is fixed, so the scan is
+  // fused into the count pass (its non-finite flag read back with the entry count) and the
+  // pipeline has no host round trip before the sort (speculative mode 3)
+  static const bool no_spec = getenv("TC_MSM_NO_SPEC") != nullptr;
+  static const uint64_t EXP_MIN_N0 =
+      getenv("TC_MSM_EXP_MIN_N") ? strtoull(getenv("TC_MSM_EXP_MIN_N"), nullptr, 10) : (1ull << 14);
+  const EdPk* spec_tab = nullptr;
+  if (!no_spec && !fbw && dtype == TC_DTYPE_F16 && scale_bits + 16 <= 61 && exp_srs &&
+      d_bases == exp_srs->ed_lagrange && n >= EXP_MIN_N0 && n >= (1u << 16) && !getenv("TC_MSM_NO_EXPTAB") &&
+      !getenv("TC_MSM_NO_BLKCNT") && !getenv("TC_MSM_GENERIC_DIGITS") &&
+      (uint64_t)(scale_bits + 6) * exp_srs->n < (1ull << 31)) {
+    bool al = true;
+    for (int l = 0; l < L && al; l++) al = ((uintptr_t)h_ptrs[l] & 15u) == 0;
+    if (!al || srs_exp_table(ctx, exp_srs, d_bases, exp_srs->n, scale_bits + 6, &spec_tab) != TC_OK)
+      spec_tab = nullptr;
+  }
+  if (!spec_tab) {
     unsigned gx = std::min<unsigned>(blocks_for(n, 256), std::max(1u, (unsigned)ctx->num_sms * 8 / (unsigned)L + 1));
     bool vec = true;   // 16-byte loads need aligned inputs
     for (int l = 0; l < L; l++) vec = vec && ((uintptr_t)h_ptrs[l] & 15u) == 0;
@@ -1168,13 +1188,19 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     TC_LAUNCHED(ctx);
   }
   uint32_t* h_small = (uint32_t*)((char*)ctx->h_stage + 65536);
-  TC_CUDA(ctx, cudaMemcpyAsync(h_small, d_small, (NHIST + 2) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-  TC_CUDA(ctx, cudaStreamSynchronize(st));
-  TC_TRY(quantize_flags_to_status(ctx, h_small[0]));
   uint32_t hist[NHIST];   // sampled counts scaled back to the population
-  for (int b = 0; b < NHIST; b++) hist[b] = h_small[1 + b] * HIST_SAMPLE;
-  const uint32_t nbits = std::min<uint32_t>(h_small[NHIST + 1], NHIST - 1);   // exact maximum
-  if (nbits) hist[nbits] = std::max<uint32_t>(hist[nbits], 1u);
+  uint32_t nbits;
+  if (spec_tab) {
+    nbits = (uint32_t)(16 + scale_bits);   // upper bound: the plan does not need the maximum
+    for (int b = 0; b < NHIST; b++) hist[b] = 0;
+  } else {
+    TC_CUDA(ctx, cudaMemcpyAsync(h_small, d_small, (NHIST + 2) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    TC_CUDA(ctx, cudaStreamSynchronize(st));
+    TC_TRY(quantize_flags_to_status(ctx, h_small[0]));
+    for (int b = 0; b < NHIST; b++) hist[b] = h_small[1 + b] * HIST_SAMPLE;
+    nbits = std::min<uint32_t>(h_small[NHIST + 1], NHIST - 1);   // exact maximum
+    if (nbits) hist[nbits] = std::max<uint32_t>(hist[nbits], 1u);
+  }
   if (nbits == 0) {
     k_fill_inf<<<blocks_for(L, 64), 64, 0, st>>>(d_out, (uint32_t)L);
     TC_LAUNCHED(ctx);
@@ -1201,7 +1227,10 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
       getenv("TC_MSM_EXP_MIN_N") ? strtoull(getenv("TC_MSM_EXP_MIN_N"), nullptr, 10) : (1ull << 14);
   const EdPk* bases = d_bases;
   const int groups = fp_mb ? std::max(1, (int)nbits - fp_mb + 1) : 0;
-  if (!fbw && exp_srs && d_bases == exp_srs->ed_lagrange && !no_exp && !getenv("TC_MSM_NO_BLKCNT") && vec_ok &&
+  if (spec_tab) {
+    P = plan_fpx(fp_mb, (uint32_t)exp_srs->n);
+    bases = spec_tab;
+  } else if (!fbw && exp_srs && d_bases == exp_srs->ed_lagrange && !no_exp && !getenv("TC_MSM_NO_BLKCNT") && vec_ok &&
       fp_mb && n >= EXP_MIN_N &&
       groups <= MAXW && (uint64_t)groups * exp_srs->n < (1ull << 31)) {
     const EdPk* tab = nullptr;
@@ -1289,14 +1318,18 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
       }
       if (dtype == TC_DTYPE_F16) {
         if (scatter)
-          k_fpb_pass<1, true><<<dim3(Sx, nl), 1024, blk_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals, chunk, l0);
+          k_fpb_pass<1, true><<<dim3(Sx, nl), 1024, blk_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals, chunk, l0,
+                                                                     nullptr);
         else
-          k_fpb_pass<1, false><<<dim3(Sx, nl), 1024, blk_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals, chunk, l0);
+          k_fpb_pass<1, false><<<dim3(Sx, nl), 1024, blk_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals, chunk, l0,
+                                                                      spec_tab ? d_small : nullptr);
       } else {
         if (scatter)
-          k_fpb_pass<2, true><<<dim3(Sx, nl), 1024, blk_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals, chunk, l0);
+          k_fpb_pass<2, true><<<dim3(Sx, nl), 1024, blk_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals, chunk, l0,
+                                                                     nullptr);
         else
-          k_fpb_pass<2, false><<<dim3(Sx, nl), 1024, blk_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals, chunk, l0);
+          k_fpb_pass<2, false><<<dim3(Sx, nl), 1024, blk_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals, chunk, l0,
+                                                                      nullptr);
       }
     };
     pass(false, 0, (uint32_t)L);
@@ -1315,6 +1348,8 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     k_max_bucket<<<blocks_for(nb, 256), 256, 0, st>>>(bstart, nb, d_small + NHIST + 3);   // zeroed with d_small
     TC_LAUNCHED(ctx);
     TC_CUDA(ctx, cudaMemcpyAsync(h_small + 1, d_small + NHIST + 3, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    if (spec_tab)   // the fused scan's flags, checked after the synchronisation below
+      TC_CUDA(ctx, cudaMemcpyAsync(h_small + 2, d_small, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     have_maxb = true;
     for (uint32_t l0 = 0; l0 < (uint32_t)L; l0 += LG) {
       pass(true, l0, std::min<uint32_t>(LG, (uint32_t)L - l0));
@@ -1323,6 +1358,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     TC_CUDA(ctx, cudaStreamSynchronize(st));
     E = h_small[0];
     maxb = h_small[1];
+    if (spec_tab) TC_TRY(quantize_flags_to_status(ctx, h_small[2]));
   } else {
   const uint32_t NC = P.mode == 1 ? std::max(1u, NC_ENV) : 1u;
   const uint64_t ncnt = (uint64_t)nb * NC + 1;
