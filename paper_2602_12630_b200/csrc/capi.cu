@@ -671,6 +671,9 @@ static int fetch_encode_many(tc_ctx* ctx, const Aff* d_pts, int L, uint8_t* out4
 
 // L MSMs over the SRS's `which` elements: the fixed-base table kernel for small SRSs
 // (Terkle nodes), the batched Pippenger pipeline otherwise
+static int msm_quotients(tc_ctx* ctx, const tc_srs* srs, const void* const* ptrs, int L, const EdPk* bases,
+                         uint64_t n, Aff* d_out);
+
 static int msm_srs(tc_ctx* ctx, const tc_srs* srs, int which, int dtype, int scale_bits, const void* const* ptrs,
                    int L, Aff* d_out) {
   if (!((which == TC_SRS_LAGRANGE) ? srs->lagrange : srs->monomial))
@@ -678,6 +681,12 @@ static int msm_srs(tc_ctx* ctx, const tc_srs* srs, int which, int dtype, int sca
   if (srs->n > SMALL_MSM_MAX) {
     const EdPk* bases;
     TC_TRY(tcrt::srs_edwards(ctx, const_cast<tc_srs*>(srs), which, &bases));
+    // full-width field-element scalars (the monomial route's coefficients) over a large
+    // basis: the fixed-base window table, as for the opening quotients (one shared window
+    // of buckets, no Horner chain)
+    static const bool no_fb = getenv("TC_COMMIT_NO_WINTAB") != nullptr;
+    if (dtype == TC_DTYPE_FP_LIMBS && srs->n >= tcrt::FB_SMALL_N && !no_fb)
+      return msm_quotients(ctx, srs, ptrs, L, bases, srs->n, d_out);
     return tcrt::msm_batch_device(ctx, dtype, scale_bits, ptrs, L, bases, srs->n, d_out, nullptr, 0,
                                   which == TC_SRS_LAGRANGE ? const_cast<tc_srs*>(srs) : nullptr);
   }
