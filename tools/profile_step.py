@@ -23,9 +23,9 @@ node = tcb.authtree.node_srs(tcfg, device=0)
 
 
 def step():
-    comms = tcb.tc_commit_many(srs, layers)
-    leaves = [tcb.hash_to_scalar(c.to_bytes(), b"terkle/leaf") for c in comms]
-    return tcb.build(tcfg, leaves, srs=node)[1]
+    # the bench's step: protocol.prover_commit (tc_commit_tree: commitments, device leaf
+    # hashing and the tree in one call)
+    return tcb.prover_commit(layers, srs, tree_config=tcfg, node_srs=node)[1]
 
 
 step()
