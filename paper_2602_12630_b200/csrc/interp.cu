@@ -208,6 +208,105 @@ __global__ void __launch_bounds__(FB) k_interp_newton(Fe* data, const Fe* invfac
   }
 }
 
+// Two threads per fibre (adjacent lanes, same SMEM fibre layout as k_interp_newton): every
+// sweep is split at its midpoint, the upper thread taking the upper half.  A sweep reads
+// the OLD value across the split point, so that value is read before a __syncwarp and the
+// halves then run concurrently — twice the resident threads for the same shared memory
+// (the one-thread kernel is occupancy-limited by its fibres: 8 warps per SM).
+template <int FB>
+__global__ void __launch_bounds__(2 * FB) k_interp_newton2(Fe* data, const Fe* invfact, uint32_t d, uint64_t stride,
+                                                           uint64_t nfib) {
+  extern __shared__ uint32_t sw[];
+  constexpr uint32_t P = FB + 1;
+  const uint64_t f0 = (uint64_t)blockIdx.x * FB;
+  const uint32_t nloc = (nfib - f0 < FB) ? (uint32_t)(nfib - f0) : FB;
+  const uint32_t tot = nloc * d;
+  const bool contiguous = (stride == 1);
+  for (uint32_t idx = threadIdx.x; idx < tot; idx += 2 * FB) {
+    uint32_t fl, l;
+    if (contiguous) {
+      fl = idx / d;
+      l = idx - fl * d;
+    } else {
+      l = idx / nloc;
+      fl = idx - l * nloc;
+    }
+    const Fe x = data[fibre_addr(f0 + fl, l, d, stride)];
+#pragma unroll
+    for (int i = 0; i < 6; i++) sw[(l * 6 + i) * P + fl] = x.v[i];
+  }
+  __syncthreads();
+  // lanes past nloc sweep a stale column: harmless, never written back
+  const uint32_t fl = threadIdx.x >> 1;
+  const bool upper = (threadIdx.x & 1u) == 0;
+  auto LD = [&](int l) {
+    Fe r;
+#pragma unroll
+    for (int i = 0; i < 6; i++) r.v[i] = sw[(l * 6 + i) * P + fl];
+    return r;
+  };
+  auto ST = [&](int l, const Fe& x) {
+#pragma unroll
+    for (int i = 0; i < 6; i++) sw[(l * 6 + i) * P + fl] = x.v[i];
+  };
+  const int D = (int)d;
+  // both halves run the same code on their own range (no divergent branches inside a warp);
+  // the value just outside a range is read before the __syncwarp that lets the other half
+  // overwrite it.
+  // forward differences: sweep k updates j = D-1 .. k (descending), v[j] -= v[j-1]
+  for (int k = 1; k < D; k++) {
+    const int mid = k + (D - k) / 2;
+    const int lo = upper ? mid : k, hi = upper ? D - 1 : mid - 1;   // this half: j in [lo, hi]
+    const Fe below = LD(lo - 1);
+    __syncwarp();
+    if (hi >= lo) {
+      Fe top = LD(hi);
+      for (int j = hi; j > lo; j--) {
+        const Fe nx = LD(j - 1);
+        ST(j, Fp::sub(top, nx));
+        top = nx;
+      }
+      ST(lo, Fp::sub(top, below));
+    }
+    __syncwarp();
+  }
+  for (int k = 2 + (upper ? 0 : 1); k < D; k += 2) ST(k, Fp::mul(LD(k), invfact[k]));
+  __syncwarp();
+  // basis expansion: step k updates j = k .. D-2 (ascending), v[j] -= (k+1) v[j+1]
+  for (int k = D - 2; k >= 0; k--) {
+    const uint32_t sc = (uint32_t)k + 1;
+    const int mid = k + (D - 1 - k) / 2;
+    const int lo = upper ? mid : k, hi = upper ? D - 2 : mid - 1;   // j in [lo, hi]
+    const Fe above = LD(hi + 1);
+    __syncwarp();
+    if (hi >= lo) {
+      Fe cur = LD(lo);
+      for (int j = lo; j < hi; j++) {
+        const Fe nx = LD(j + 1);
+        ST(j, Fp::sub(cur, fp_mul_u32(nx, sc)));
+        cur = nx;
+      }
+      ST(hi, Fp::sub(cur, fp_mul_u32(above, sc)));
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  for (uint32_t idx = threadIdx.x; idx < tot; idx += 2 * FB) {
+    uint32_t f, l;
+    if (contiguous) {
+      f = idx / d;
+      l = idx - f * d;
+    } else {
+      l = idx / nloc;
+      f = idx - l * nloc;
+    }
+    Fe x;
+#pragma unroll
+    for (int i = 0; i < 6; i++) x.v[i] = sw[(l * 6 + i) * P + f];
+    data[fibre_addr(f0 + f, l, d, stride)] = Fp::canon(x);
+  }
+}
+
 // Warp-per-fibre variant of k_interp_newton (fibres longer than 32 nodes): element j = e*32 + lane
 // of the fibre lives in lane `lane`, register slot e (E = ceil(d/32)); the difference and
 // expansion sweeps shift the fibre by one node with warp shuffles, no shared memory.
@@ -465,6 +564,18 @@ int interpolate_device(tc_ctx* ctx, Fe* d_vals, const uint32_t* shape, int m) {
       }
       constexpr int FB = 64;
       const size_t smem = (size_t)(FB + 1) * d * 6 * sizeof(uint32_t);
+      static const bool one_thread = getenv("TC_INTERP_NEWTON1") != nullptr;
+      if (!one_thread) {
+        static bool attr2 = false;
+        if (!attr2) {
+          TC_CUDA(ctx, cudaFuncSetAttribute(k_interp_newton2<FB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)((FB + 1) * 128 * 6 * sizeof(uint32_t))));
+          attr2 = true;
+        }
+        k_interp_newton2<FB><<<(unsigned)((nfib + FB - 1) / FB), 2 * FB, smem, st>>>(d_vals, dIf, d, stride, nfib);
+        TC_LAUNCHED(ctx);
+        continue;
+      }
       static bool attr = false;
       if (!attr) {
         TC_CUDA(ctx, cudaFuncSetAttribute(k_interp_newton<FB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
