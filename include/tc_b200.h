@@ -170,6 +170,21 @@ int tc_commit_tree(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int
                    uint8_t* out_comms43, uint8_t* out_nodes43, uint64_t* inout_node_count,
                    uint8_t* out_values24, uint64_t* inout_value_count);
 
+/* tc_commit_tree in two halves, for pipelining forwards over several contexts: _launch
+ * enqueues the commitments, the leaf hashing, the tree and the result readback on ctx's
+ * stream and returns (it waits only for the MSM's bucket sizes midway); _finish waits for
+ * that readback and writes the outputs of tc_commit_tree.  One launch in flight per ctx.
+ * tc_commit_stream_tree_launch is the same for HOST inputs (uploaded on ctx's copy
+ * stream).  The ctx stream must be ordered after the producers of d_ins. */
+int tc_commit_tree_launch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count,
+                          int dtype, int scale_bits, int route, const tc_srs* node_srs);
+int tc_commit_stream_tree_launch(tc_ctx* ctx, const tc_srs* srs, const void* const* h_ins,
+                                 int count, int dtype, int scale_bits, int route,
+                                 const tc_srs* node_srs);
+int tc_commit_tree_finish(tc_ctx* ctx, uint8_t* out_comms43, uint8_t* out_nodes43,
+                          uint64_t* inout_node_count, uint8_t* out_values24,
+                          uint64_t* inout_value_count);
+
 /* tc_commit_stream + the device tree of tc_commit_tree, one call per forward
  * (protocol.prover_commit_stream). */
 int tc_commit_stream_tree(tc_ctx* ctx, const tc_srs* srs, const void* const* h_cur,

@@ -13,12 +13,12 @@ from .commit import (Commitment, Srs, TensorOpening, Trapdoors, derive_taus, loa
 from .curve import G, P, Q, decode_elem, decode_scalar, encode_elem, encode_scalar, hash_to_scalar
 from .field import PrimeField
 from .mvpoly import Grid, MultiPoly, default_grid, evaluate, interpolate_lagrange, lex_index, open_quotients
-from .protocol import FieldTensor, prover_commit, prover_commit_stream, quantize
+from .protocol import FieldTensor, prover_commit, prover_commit_pipeline, prover_commit_stream, quantize
 
 __all__ = [
     "ActivationCapture", "infer_and_capture", "Commitment", "FieldTensor", "G", "Grid", "MembershipProof", "MultiPoly", "P", "PrimeField", "Q", "Srs",
     "TensorOpening", "TerkleTree", "Trapdoors", "TreeConfig", "build", "decode_elem", "decode_scalar", "default_grid",
     "derive_taus", "encode_elem", "encode_scalar", "evaluate", "hash_to_scalar", "interpolate_lagrange", "leaf_of",
-    "lex_index", "load_srs", "open_quotients", "pair", "prove", "prover_commit", "prover_commit_stream", "quantize", "setup_srs", "tc_commit",
+    "lex_index", "load_srs", "open_quotients", "pair", "prove", "prover_commit", "prover_commit_pipeline", "prover_commit_stream", "quantize", "setup_srs", "tc_commit",
     "tc_commit_many", "tc_commit_stream", "tc_open", "tc_open_many", "tc_verify", "verify",
 ]

@@ -74,6 +74,9 @@ _SIGS = [
     ("tc_terkle_build", C.c_int, [_P, _P, C.c_char_p, C.c_uint64, _P, C.POINTER(C.c_uint64)]),
     ("tc_commit_tree", C.c_int, [_P, _P, C.POINTER(_P), C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, _P,
                                  C.POINTER(C.c_uint64), _P, C.POINTER(C.c_uint64)]),
+    ("tc_commit_tree_launch", C.c_int, [_P, _P, C.POINTER(_P), C.c_int, C.c_int, C.c_int, C.c_int, _P]),
+    ("tc_commit_stream_tree_launch", C.c_int, [_P, _P, C.POINTER(_P), C.c_int, C.c_int, C.c_int, C.c_int, _P]),
+    ("tc_commit_tree_finish", C.c_int, [_P, _P, _P, C.POINTER(C.c_uint64), _P, C.POINTER(C.c_uint64)]),
     ("tc_commit_stream_tree", C.c_int, [_P, _P, C.POINTER(_P), C.POINTER(_P), C.c_int, C.c_int, C.c_int, C.c_int,
                                         _P, _P, _P, C.POINTER(C.c_uint64), _P, C.POINTER(C.c_uint64)]),
     ("tc_pairing", C.c_int, [C.c_char_p, C.c_char_p, _P]),
@@ -140,6 +143,23 @@ class Context:
             check(lib().tc_ctx_create(device, stream, C.byref(h)), None, "tc_ctx_create")
         self.handle = h
 
+    _pipeline: dict = {}
+
+    @classmethod
+    def pipeline(cls, device: int, k: int) -> "Context":
+        """Context k (0, 1, ...) of the forward pipeline on `device`: its own CUDA stream
+        (kept bound), its own scratch, the device's SRSs shared."""
+        import torch
+
+        with cls._guard:
+            ctx = cls._pipeline.get((device, k))
+            if ctx is None:
+                ctx = cls(device)
+                ctx.fixed_stream = torch.cuda.Stream(device)
+                lib().tc_ctx_set_stream(ctx.handle, ctx.fixed_stream.cuda_stream)
+                cls._pipeline[(device, k)] = ctx
+        return ctx
+
     @classmethod
     def get(cls, device=None) -> "Context":
         import torch
@@ -155,8 +175,14 @@ class Context:
                 cls._by_device[device] = ctx
         return ctx
 
+    fixed_stream = None
+
     def bind_stream(self):
         import torch
+
+        if self.fixed_stream is not None:
+            lib().tc_ctx_set_stream(self.handle, self.fixed_stream.cuda_stream)
+            return
 
         s = torch.cuda.current_stream(self.device).cuda_stream
         lib().tc_ctx_set_stream(self.handle, s)

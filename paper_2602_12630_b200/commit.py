@@ -335,6 +335,57 @@ def tc_commit_tree(srs: Srs, tensors, node_srs: Srs, *, scale_bits: int = SCALE_
     return _tree_result(len(ptrs), L, comms, nodes, vals)
 
 
+def tc_commit_tree_launch(ctx, srs: Srs, tensors, node_srs: Srs, *, scale_bits: int = SCALE_BITS,
+                          route: str = "auto"):
+    """First half of tc_commit_tree on pipeline context `ctx` (_lib.Context.pipeline): enqueue
+    the commitments, leaf hashing, tree and readback, return without waiting for them.  CUDA
+    tensors are ordered after torch's current stream; CPU float tensors are uploaded on the
+    context's copy stream.  Returns the state tc_commit_tree_finish takes (it keeps the
+    inputs alive until then)."""
+    import torch
+
+    tensors = list(tensors)
+    host = _host_floats(tensors)
+    with ctx.lock:
+        # the context's stream runs after everything already queued on torch's stream (the
+        # inputs' producers, SRS setup)
+        ctx.fixed_stream.wait_stream(torch.cuda.current_stream(ctx.device))
+        if host is not None:
+            ts, code = host
+            for t in ts:
+                if t.numel() != srs.size:
+                    raise ValueError("tensor size does not match grid shape")
+            arr = (C.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
+            keep = ts
+            ctx.check(_lib.lib().tc_commit_stream_tree_launch(ctx.handle, srs.handle, arr, len(ts), code, scale_bits,
+                                                              _route(route), node_srs.handle),
+                      "tc_commit_tree_launch")
+        else:
+            keeps, ptrs, dts = [], [], set()
+            for T in tensors:
+                ptr, dt, k = _conv.device_input(T, srs.size, f"cuda:{ctx.device}")
+                ptrs.append(ptr)
+                dts.add(dt)
+                keeps.append(k)
+            if len(dts) != 1:
+                raise ValueError("tc_commit_tree: all tensors must share one dtype")
+            arr = (C.c_void_p * len(ptrs))(*ptrs)
+            keep = keeps
+            ctx.check(_lib.lib().tc_commit_tree_launch(ctx.handle, srs.handle, arr, len(ptrs), dts.pop(), scale_bits,
+                                                       _route(route), node_srs.handle), "tc_commit_tree_launch")
+    return ctx, len(tensors), node_srs.size, keep
+
+
+def tc_commit_tree_finish(state):
+    """Second half: wait for the launched work, return what tc_commit_tree returns."""
+    ctx, count, B, _keep = state
+    L, comms, nodes, vals, cn, cv = _tree_buffers(count, B)
+    with ctx.lock:
+        ctx.check(_lib.lib().tc_commit_tree_finish(ctx.handle, comms, nodes, C.byref(cn), vals, C.byref(cv)),
+                  "tc_commit_tree_finish")
+    return _tree_result(count, L, comms, nodes, vals)
+
+
 def _stream_args(srs: Srs, cur, nxt):
     hc = _host_floats(list(cur))
     if hc is None:

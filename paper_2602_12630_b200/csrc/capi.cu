@@ -443,6 +443,8 @@ int tc_ctx_destroy(tc_ctx* ctx) {
   for (auto& sl : ctx->slot)
     if (sl.ready) cudaEventDestroy(sl.ready);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  if (ctx->h_res) cudaFreeHost(ctx->h_res);
+  if (ctx->res_ev) cudaEventDestroy(ctx->res_ev);
   delete ctx;
   return TC_OK;
 }
@@ -758,14 +760,13 @@ static void terkle_geometry(uint64_t n, uint64_t B, uint64_t& L, uint64_t& cap, 
   for (uint64_t l = 0; l < L; l++) values += w, w /= B, nodes += w;
 }
 
-static int commit_tree_impl(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype,
-                            int scale_bits, int route, const tc_srs* node_srs, uint8_t* out_comms43,
-                            uint8_t* out_nodes43, uint64_t* inout_node_count, uint8_t* out_values24,
-                            uint64_t* inout_value_count) {
-  if (!ctx || !srs || !d_ins || !node_srs || !out_comms43 || !out_nodes43 || !inout_node_count || !out_values24 ||
-      !inout_value_count)
-    return TC_ERR_ARGUMENT;
+// commit + leaves + tree on the ctx stream; the results are copied (asynchronously) into the
+// ctx's pinned result buffer and `res_ev` recorded — tc_commit_tree_finish collects them
+static int commit_tree_launch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype,
+                              int scale_bits, int route, const tc_srs* node_srs) {
+  if (!ctx || !srs || !d_ins || !node_srs) return TC_ERR_ARGUMENT;
   if (count <= 0) return fail(ctx, TC_ERR_VALUE, "empty leaf list");
+  if (ctx->res_pending) return fail(ctx, TC_ERR_VALUE, "commit_tree: previous launch not finished on this context");
   const uint64_t B = node_srs->n;
   if (B < 2) return fail(ctx, TC_ERR_VALUE, "tree arity must be >= 2");
   if (!node_srs->lagrange || B > SMALL_MSM_MAX)
@@ -773,9 +774,6 @@ static int commit_tree_impl(tc_ctx* ctx, const tc_srs* srs, const void* const* d
                 (unsigned long long)SMALL_MSM_MAX);
   uint64_t L, cap, total_nodes, total_values;
   terkle_geometry((uint64_t)count, B, L, cap, total_nodes, total_values);
-  if (*inout_node_count < total_nodes || *inout_value_count < total_values)
-    return fail(ctx, TC_ERR_VALUE, "need room for %llu nodes and %llu values", (unsigned long long)total_nodes,
-                (unsigned long long)total_values);
   // commitments and node points in one buffer (one readback), leaves and level values
   Aff* d_all;
   Fe *d_vals, *d_levels;
@@ -785,21 +783,56 @@ static int commit_tree_impl(tc_ctx* ctx, const tc_srs* srs, const void* const* d
   TC_TRY(commit_many_dev(ctx, srs, d_ins, count, dtype, scale_bits, route, d_all));
   TC_TRY(tcrt::leaf_hash_device(ctx, d_all, count, cap, d_vals));
   TC_TRY(tcrt::terkle_device(ctx, const_cast<tc_srs*>(node_srs), d_vals, cap, (int)L, d_all + count, d_levels));
-  // level values (canonical 24-byte limbs) through the staging buffer, then the points
-  for (uint64_t base = 0; base < total_values;) {
-    const uint64_t k = std::min<uint64_t>(total_values - base, ctx->h_stage_bytes / sizeof(Fe));
-    TC_CUDA(ctx, cudaMemcpyAsync(ctx->h_stage, d_levels + base, k * sizeof(Fe), cudaMemcpyDeviceToHost, ctx->stream));
-    TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    memcpy(out_values24 + 24 * base, ctx->h_stage, k * sizeof(Fe));
-    base += k;
+  const size_t pts_b = (size_t)(count + total_nodes) * sizeof(Aff), vals_b = (size_t)total_values * sizeof(Fe);
+  if (ctx->h_res_bytes < pts_b + vals_b) {
+    if (ctx->h_res) cudaFreeHost(ctx->h_res);
+    ctx->h_res = nullptr;
+    ctx->h_res_bytes = 0;
+    TC_CUDA(ctx, cudaHostAlloc(&ctx->h_res, pts_b + vals_b, cudaHostAllocDefault));
+    ctx->h_res_bytes = pts_b + vals_b;
   }
-  std::vector<uint8_t> enc((size_t)(count + total_nodes) * 43);
-  TC_TRY(fetch_encode_many(ctx, d_all, (int)(count + total_nodes), enc.data()));
-  memcpy(out_comms43, enc.data(), (size_t)count * 43);
-  memcpy(out_nodes43, enc.data() + (size_t)count * 43, (size_t)total_nodes * 43);
-  *inout_node_count = total_nodes;
-  *inout_value_count = total_values;
+  if (!ctx->res_ev) TC_CUDA(ctx, cudaEventCreateWithFlags(&ctx->res_ev, cudaEventDisableTiming));
+  TC_CUDA(ctx, cudaMemcpyAsync(ctx->h_res, d_all, pts_b, cudaMemcpyDeviceToHost, ctx->stream));
+  TC_CUDA(ctx, cudaMemcpyAsync((char*)ctx->h_res + pts_b, d_levels, vals_b, cudaMemcpyDeviceToHost, ctx->stream));
+  TC_CUDA(ctx, cudaEventRecord(ctx->res_ev, ctx->stream));
+  ctx->res_pending = true;
+  ctx->res_count = (uint64_t)count, ctx->res_nodes = total_nodes, ctx->res_values = total_values;
   return TC_OK;
+}
+
+int tc_commit_tree_finish(tc_ctx* ctx, uint8_t* out_comms43, uint8_t* out_nodes43, uint64_t* inout_node_count,
+                          uint8_t* out_values24, uint64_t* inout_value_count) {
+  if (!ctx || !out_comms43 || !out_nodes43 || !inout_node_count || !out_values24 || !inout_value_count)
+    return TC_ERR_ARGUMENT;
+  if (!ctx->res_pending) return fail(ctx, TC_ERR_VALUE, "commit_tree: nothing launched on this context");
+  if (*inout_node_count < ctx->res_nodes || *inout_value_count < ctx->res_values)
+    return fail(ctx, TC_ERR_VALUE, "need room for %llu nodes and %llu values", (unsigned long long)ctx->res_nodes,
+                (unsigned long long)ctx->res_values);
+  TC_CUDA(ctx, cudaEventSynchronize(ctx->res_ev));
+  ctx->res_pending = false;
+  const Aff* pts = (const Aff*)ctx->h_res;
+  for (uint64_t i = 0; i < ctx->res_count; i++) aff_encode43(pts[i], out_comms43 + 43 * i);
+  for (uint64_t i = 0; i < ctx->res_nodes; i++) aff_encode43(pts[ctx->res_count + i], out_nodes43 + 43 * i);
+  memcpy(out_values24, (const char*)ctx->h_res + (ctx->res_count + ctx->res_nodes) * sizeof(Aff),
+         ctx->res_values * sizeof(Fe));
+  *inout_node_count = ctx->res_nodes;
+  *inout_value_count = ctx->res_values;
+  return TC_OK;
+}
+
+int tc_commit_tree_launch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype,
+                          int scale_bits, int route, const tc_srs* node_srs) {
+  return commit_tree_launch(ctx, srs, d_ins, count, dtype, scale_bits, route, node_srs);
+}
+
+static int commit_tree_impl(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype,
+                            int scale_bits, int route, const tc_srs* node_srs, uint8_t* out_comms43,
+                            uint8_t* out_nodes43, uint64_t* inout_node_count, uint8_t* out_values24,
+                            uint64_t* inout_value_count) {
+  if (!out_comms43 || !out_nodes43 || !inout_node_count || !out_values24 || !inout_value_count)
+    return TC_ERR_ARGUMENT;
+  TC_TRY(commit_tree_launch(ctx, srs, d_ins, count, dtype, scale_bits, route, node_srs));
+  return tc_commit_tree_finish(ctx, out_comms43, out_nodes43, inout_node_count, out_values24, inout_value_count);
 }
 
 int tc_commit_tree(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype, int scale_bits,
@@ -953,6 +986,15 @@ int tc_commit_stream(tc_ctx* ctx, const tc_srs* srs, const void* const* h_cur, c
   std::vector<const void*> ptrs;
   TC_TRY(stream_prepare(ctx, srs, h_cur, h_next, count, dtype, ptrs));
   return commit_many(ctx, srs, ptrs.data(), count, dtype, scale_bits, route, out43);
+}
+
+int tc_commit_stream_tree_launch(tc_ctx* ctx, const tc_srs* srs, const void* const* h_cur, int count, int dtype,
+                                 int scale_bits, int route, const tc_srs* node_srs) {
+  if (!ctx || !srs || !h_cur || count <= 0) return TC_ERR_ARGUMENT;
+  if (ctx->res_pending) return fail(ctx, TC_ERR_VALUE, "commit_tree: previous launch not finished on this context");
+  std::vector<const void*> ptrs;
+  TC_TRY(stream_prepare(ctx, srs, h_cur, nullptr, count, dtype, ptrs));
+  return commit_tree_launch(ctx, srs, ptrs.data(), count, dtype, scale_bits, route, node_srs);
 }
 
 int tc_commit_stream_tree(tc_ctx* ctx, const tc_srs* srs, const void* const* h_cur, const void* const* h_next,

@@ -172,6 +172,7 @@ int srs_window_table(tc_ctx* ctx, tc_srs* srs, const EdPk* bases, uint64_t n, co
                                                                                 tab + w * n);
     TC_LAUNCHED(ctx);
   }
+  TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));   // shared with other contexts' streams
   srs->wintab[bases] = tab;
   *out = tab;
   return TC_OK;
@@ -206,6 +207,8 @@ int srs_exp_table(tc_ctx* ctx, tc_srs* srs, const EdPk* bases, uint64_t n, int d
                                                                                 tab + (uint64_t)k * n);
     TC_LAUNCHED(ctx);
   }
+  // other contexts (other streams) read the table from now on: finish building it first
+  TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   srs->exptab = tab;
   srs->exptab_depth = depth;
   *out = tab;

@@ -49,6 +49,13 @@ struct tc_ctx {
     cudaEvent_t ready = nullptr;
   };
   Slot slot[2];
+  // asynchronous commit + tree (tc_commit_tree_launch / _finish): the points and level
+  // values are copied into this pinned buffer on the ctx stream, `res_ev` marks completion
+  void* h_res = nullptr;
+  size_t h_res_bytes = 0;
+  cudaEvent_t res_ev = nullptr;
+  bool res_pending = false;
+  uint64_t res_count = 0, res_nodes = 0, res_values = 0;
 };
 
 struct tc_srs {

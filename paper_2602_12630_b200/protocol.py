@@ -11,7 +11,8 @@ from dataclasses import dataclass
 from . import _conv, _lib
 from . import authtree
 from .authtree import TreeConfig, build, leaf_of
-from .commit import SCALE_BITS, tc_commit_many, tc_commit_stream, tc_commit_stream_tree, tc_commit_tree
+from .commit import (SCALE_BITS, tc_commit_many, tc_commit_stream, tc_commit_stream_tree, tc_commit_tree,
+                     tc_commit_tree_finish, tc_commit_tree_launch)
 
 
 @dataclass
@@ -96,6 +97,47 @@ def prover_commit(tensors, srs_pool, *, tree_config: TreeConfig = None, scale_bi
             commitments[i] = c
     tree, root = build(cfg, [leaf_of(c) for c in commitments], srs=node_srs)
     return commitments, root, tree
+
+
+def prover_commit_pipeline(forwards, srs, *, tree_config: TreeConfig = None, node_srs=None,
+                           scale_bits: int = SCALE_BITS, route: str = "auto", depth: int = 2):
+    """prover_commit over a stream of forwards (each a list of same-shape tensors: CUDA, or
+    CPU floats uploaded on the fly), yielding (commitments, root, tree) per forward in order.
+    `depth` device contexts (own streams and scratch, shared SRS) take the forwards in turn,
+    so forward k+1's sort and accumulation overlap forward k's latency-bound tail (bucket
+    weighting, affine conversion, tree) and its host-side decoding."""
+    cfg = tree_config or TreeConfig()
+    node = node_srs or authtree.node_srs(cfg, device=srs.device)
+    if node.size > 64 or not node.has(_lib.SRS_LAGRANGE):
+        for fwd in forwards:   # no device tree: the plain per-forward path
+            yield prover_commit(list(fwd), srs, tree_config=cfg, scale_bits=scale_bits, route=route,
+                                node_srs=node_srs)
+        return
+    ctxs = [_lib.Context.pipeline(srs.device, k) for k in range(max(1, depth))]
+    pending = []
+    try:
+        for k, fwd in enumerate(forwards):
+            state = tc_commit_tree_launch(ctxs[k % len(ctxs)], srs, list(fwd), node, scale_bits=scale_bits,
+                                          route=route)
+            pending.append(state)
+            if len(pending) == len(ctxs):
+                yield _finish_tree(pending.pop(0), cfg, node)
+        while pending:
+            yield _finish_tree(pending.pop(0), cfg, node)
+    finally:
+        # an error or an early exit leaves launches in flight: collect them so their
+        # contexts can be launched on again
+        for state in pending:
+            try:
+                tc_commit_tree_finish(state)
+            except Exception:
+                pass
+
+
+def _finish_tree(state, cfg, node):
+    commitments, nodes, vals, depth = tc_commit_tree_finish(state)
+    tree = authtree.tree_from_device(cfg, len(commitments), depth, nodes, vals, node)
+    return commitments, tree.root, tree
 
 
 def prover_commit_stream(batches, srs, *, tree_config: TreeConfig = None, node_srs=None,

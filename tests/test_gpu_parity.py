@@ -306,6 +306,39 @@ def test_prover_commit_device_tree_matches_host_build(n_layers, node_shape):
         assert tcb.verify(root, i, leaves[i], pf, cfg, srs=node)
 
 
+@pytest.mark.parametrize("depth", [1, 2, 3])
+def test_prover_commit_pipeline_matches_prover_commit(depth):
+    """prover_commit_pipeline (forwards taken in turn by `depth` contexts with their own
+    streams: tc_commit_tree_launch / _finish) yields, in order, exactly prover_commit's
+    commitments, root and tree for every forward — device and host (CPU) inputs, a failing
+    forward in between raises and the pipeline contexts stay usable."""
+    tcb = T()
+    shape = (16, 16, 16, 16)
+    srs, td = tcb.setup_srs(shape, b"pipeline")
+    cfg = tcb.TreeConfig(shape=(2, 2, 2))
+    node = tcb.authtree.node_srs(cfg, device=0)
+    g = np.random.default_rng(81)
+    fwds = [[torch.from_numpy((g.standard_t(3, 65536) * (0.5 + (f + l) % 3)).astype(np.float16)).cuda()
+             for l in range(5)] for f in range(5)]
+    want = [tcb.prover_commit(f, srs, tree_config=cfg, node_srs=node) for f in fwds]
+    got = list(tcb.prover_commit_pipeline(fwds, srs, tree_config=cfg, node_srs=node, depth=depth))
+    assert len(got) == len(want)
+    for (c1, r1, t1), (c2, r2, t2) in zip(got, want):
+        assert c1 == c2 and r1 == r2 and t1.levels == t2.levels and t1.values == t2.values
+    # host (CPU) inputs through the same pipeline
+    host = [[t.cpu() for t in f] for f in fwds[:3]]
+    got_h = list(tcb.prover_commit_pipeline(host, srs, tree_config=cfg, node_srs=node, depth=depth))
+    assert [r for _, r, _ in got_h] == [r for _, r, _ in want[:3]]
+    vals = O.quantize(fwds[2][1].cpu().numpy().astype(np.float64), 16)
+    assert got[2][0][1].elem == O.commit_trapdoor(vals, shape, list(td.taus))
+    bad = [t.clone() for t in fwds[1]]
+    bad[2][5] = float("nan")
+    with pytest.raises(ValueError):
+        list(tcb.prover_commit_pipeline([fwds[0], bad], srs, tree_config=cfg, node_srs=node, depth=depth))
+    again = list(tcb.prover_commit_pipeline(fwds[:2], srs, tree_config=cfg, node_srs=node, depth=depth))
+    assert [r for _, r, _ in again] == [r for _, r, _ in want[:2]]
+
+
 @pytest.mark.parametrize("group", [0, 1, 2, 5])
 @pytest.mark.parametrize("pinned", [True, False])
 def test_commit_many_host_inputs_pipelined(group, pinned):
