@@ -327,6 +327,13 @@ def main():
         streams its own layers (tc_commit_stream), then the commitment gather and the tree."""
         batches = [host_pinned if k % 2 == 0 else host_pinned2 for k in range(steps)]
         root = None
+        if use_pipe:
+            # host tensors through the forward pipeline: each context uploads its forward on
+            # its own copy stream while the other contexts' forwards compute
+            for _, root, _ in tcb.prover_commit_pipeline(batches, srs, tree_config=tcfg, node_srs=node_srs,
+                                                         route=args.route, depth=PIPE_DEPTH):
+                pass
+            return root
         if world == 1:
             for _, root, _ in tcb.prover_commit_stream(batches, srs, tree_config=tcfg, node_srs=node_srs,
                                                        route=args.route):
@@ -341,12 +348,31 @@ def main():
             root = tcb.build(tcfg, leaves, srs=node_srs)[1]
         return root
 
+    # one rank: forwards go through protocol.prover_commit_pipeline (PIPE_DEPTH device
+    # contexts take them in turn; TC_BENCH_NO_PIPELINE=1: one prover_commit per forward)
+    use_pipe = world == 1 and not os.environ.get("TC_BENCH_NO_PIPELINE")
+    PIPE_DEPTH = int(os.environ.get("TC_PIPE_DEPTH", "3"))
+
+    def all_launches():
+        return ctx.launches + sum(c.launches for c in _lib.Context._pipeline.values())
+
+    def value_run(steps, route=args.route):
+        root = None
+        if use_pipe:
+            for _, root, _ in tcb.prover_commit_pipeline([dev_layers] * steps, srs, tree_config=tcfg,
+                                                         node_srs=node_srs, route=route, depth=PIPE_DEPTH):
+                pass
+            return root
+        for _ in range(steps):
+            root = prove_step(dev_layers, route=route)
+        return root
+
     def timed(fn, steps):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        l0 = ctx.launches
+        l0 = all_launches()
         e0.record()
         for _ in range(steps):
             root = fn()
@@ -359,12 +385,11 @@ def main():
             t = torch.tensor([ms], device=dev if backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
-        return ms, ctx.launches - l0, root
+        return ms, all_launches() - l0, root
 
-    for _ in range(args.warmup):
-        prove_step(dev_layers)
+    value_run(args.warmup)
     with Clocks(local) as clk:
-        ms, launches, root = timed(lambda: prove_step(dev_layers), args.steps)
+        ms, launches, root = timed(lambda: value_run(args.steps), 1)
     for _ in range(args.warmup):
         e2e_step()
     ms_e2e, _, root_e2e = timed(e2e_step, args.steps)
@@ -427,10 +452,14 @@ def main():
     if ms_stream is not None:
         e2e = dict(e2e_serial, value=per_step_elems / (ms_stream / args.steps / 1e3),
                    ms_per_step=ms_stream / args.steps,
-                   path=f"{args.steps} forwards of pinned host tensors through the streaming API "
-                        "(protocol.prover_commit_stream / tc_commit_stream per rank: forward k+1's upload "
-                        "overlaps forward k's commit; first upload exposed) + commitment gather (N > 1) + "
-                        "Terkle build + commitments/root read back, per step",
+                   path=(f"{args.steps} forwards of pinned host tensors through protocol.prover_commit_pipeline "
+                         f"({PIPE_DEPTH} device contexts in turn: each uploads its forward on its own copy stream "
+                         "and commits it while the others' forwards compute; first upload exposed) + device leaf "
+                         "hashing and Terkle tree + commitments / tree read back, per forward" if use_pipe else
+                         f"{args.steps} forwards of pinned host tensors through the streaming API "
+                         "(protocol.prover_commit_stream / tc_commit_stream per rank: forward k+1's upload "
+                         "overlaps forward k's commit; first upload exposed) + commitment gather (N > 1) + "
+                         "Terkle build + commitments/root read back, per step"),
                    serial=e2e_serial)
     else:
         e2e = e2e_serial
@@ -441,7 +470,10 @@ def main():
             "vs_baseline": None, "dtype": "u32 (6-limb F_p/F_q Montgomery); input fp16", "data": "synthetic",
             "config": {"workload": cfg["name"], "route": args.route, "elems_per_step": per_step_elems,
                        "parallelism": f"layers/{world}", "l2": "no flush: fp16 inputs (>=128 MiB) + SRS (96 MiB) "
-                       "exceed the 126 MB L2", "srs": "generated once before timing (trusted setup)"},
+                       "exceed the 126 MB L2", "srs": "generated once before timing (trusted setup)",
+                       "step_api": (f"protocol.prover_commit_pipeline over the {args.steps} timed forwards "
+                                    f"({PIPE_DEPTH} contexts; every forward's commitments, root and tree read back)"
+                                    if use_pipe else "protocol.prover_commit per forward")},
             "overhead_pct": (100.0 * ms_step / fwd) if fwd else None,
             "forward_ms": fwd,
             "e2e": e2e,
