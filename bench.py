@@ -327,7 +327,7 @@ def main():
         streams its own layers (tc_commit_stream), then the commitment gather and the tree."""
         batches = [host_pinned if k % 2 == 0 else host_pinned2 for k in range(steps)]
         root = None
-        if use_pipe:
+        if use_pipe and args.config != 5:
             # host tensors through the forward pipeline: each context uploads its forward on
             # its own copy stream while the other contexts' forwards compute
             for _, root, _ in tcb.prover_commit_pipeline(batches, srs, tree_config=tcfg, node_srs=node_srs,
@@ -455,7 +455,8 @@ def main():
                    path=(f"{args.steps} forwards of pinned host tensors through protocol.prover_commit_pipeline "
                          f"({PIPE_DEPTH} device contexts in turn: each uploads its forward on its own copy stream "
                          "and commits it while the others' forwards compute; first upload exposed) + device leaf "
-                         "hashing and Terkle tree + commitments / tree read back, per forward" if use_pipe else
+                         "hashing and Terkle tree + commitments / tree read back, per forward"
+                         if use_pipe and args.config != 5 else
                          f"{args.steps} forwards of pinned host tensors through the streaming API "
                          "(protocol.prover_commit_stream / tc_commit_stream per rank: forward k+1's upload "
                          "overlaps forward k's commit; first upload exposed) + commitment gather (N > 1) + "
