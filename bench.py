@@ -387,7 +387,7 @@ def main():
             ms = float(t.item())
         return ms, all_launches() - l0, root
 
-    value_run(args.warmup)
+    value_run(max(args.warmup, PIPE_DEPTH if use_pipe else 0))   # every pipeline context warmed
     with Clocks(local) as clk:
         ms, launches, root = timed(lambda: value_run(args.steps), 1)
     for _ in range(args.warmup):
@@ -396,7 +396,7 @@ def main():
     if root_e2e != root:
         raise RuntimeError("e2e root differs from the device-resident root")
     ms_stream = None
-    e2e_stream(2)
+    e2e_stream(max(2, PIPE_DEPTH if use_pipe else 0))
     ms_stream, _, root_s = timed(lambda: e2e_stream(args.steps), 1)
     if root_s != root:
         raise RuntimeError("streaming e2e root differs from the device-resident root")
