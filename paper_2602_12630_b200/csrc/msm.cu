@@ -553,9 +553,13 @@ __global__ void __launch_bounds__(1024) k_fpb_pass(const void* const* ptrs, uint
 // global slot, and written out by consecutive threads — entries of one bucket (about 4 per
 // slice over 2^11 - 1 buckets) land in consecutive addresses from consecutive lanes, so
 // they share store transactions instead of costing one scattered 4-byte store each.
-constexpr int FPS_THREADS = 512, FPS_EPT = 16, FPS_SLICE = FPS_THREADS * FPS_EPT;   // 8192
+#ifndef TC_FPS_THREADS
+#define TC_FPS_THREADS 1024   // 16384-element slices: ~8 entries per bucket per slice (A/B: 512 -> 4.75 ms step, 1024 -> 4.70)
+#endif
+constexpr int FPS_THREADS = TC_FPS_THREADS, FPS_EPT = 16, FPS_SLICE = FPS_THREADS * FPS_EPT;   // 8192
+constexpr int FPS_CPT = 2048 / FPS_THREADS;   // bucket counters per thread in the slice scan
 template <int DT>
-__global__ void __launch_bounds__(FPS_THREADS, 2) k_fpb_scatter_sorted(const void* const* ptrs, uint64_t n,
+__global__ void __launch_bounds__(FPS_THREADS, 1024 / FPS_THREADS) k_fpb_scatter_sorted(const void* const* ptrs, uint64_t n,
                                                                         int scale_bits, WinPlan P,
                                                                         const uint32_t* __restrict__ cnt,
                                                                         uint32_t* __restrict__ vals, uint64_t chunk,
@@ -617,10 +621,10 @@ __global__ void __launch_bounds__(FPS_THREADS, 2) k_fpb_scatter_sorted(const voi
       ld16(base + FPS_SLICE + FPS_SLICE / 2 + (uint64_t)t * V_EPT, cur[1]);
     }
     __syncthreads();
-    // exclusive scan of lo[0..2048): 4 counters per thread, warp shuffles, warp totals
-    uint32_t c[4], sum = 0;
+    // exclusive scan of lo[0..2048): FPS_CPT counters per thread, warp shuffles, warp totals
+    uint32_t c[FPS_CPT], sum = 0;
 #pragma unroll
-    for (int j = 0; j < 4; j++) c[j] = lo[4 * t + j], sum += c[j];
+    for (int j = 0; j < FPS_CPT; j++) c[j] = lo[FPS_CPT * t + j], sum += c[j];
     uint32_t inc = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -641,7 +645,7 @@ __global__ void __launch_bounds__(FPS_THREADS, 2) k_fpb_scatter_sorted(const voi
     __syncthreads();
     uint32_t run = wsum[wid] + inc - sum;
 #pragma unroll
-    for (int j = 0; j < 4; j++) lo[4 * t + j] = run, run += c[j];
+    for (int j = 0; j < FPS_CPT; j++) lo[FPS_CPT * t + j] = run, run += c[j];
     if (t == FPS_THREADS - 1) lo[2048] = run;
     __syncthreads();
 #pragma unroll
@@ -1277,7 +1281,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
                                     : std::max<uint32_t>(1u, std::min(std::min(FPB_LG_ENV, (uint32_t)L),
                                                                       (uint32_t)((64ull << 20) / (n * sizeof(uint32_t)))));
     const uint64_t conc = (uint64_t)ctx->num_sms * 2;
-    const uint64_t step = 1024ull * V_EPT;
+    const uint64_t step = std::max<uint64_t>(1024ull * V_EPT, (uint64_t)FPS_SLICE);   // chunks hold whole slices
     const uint64_t S0 = std::max<uint64_t>(1, std::min<uint64_t>(conc / LG, n / step));
     const uint64_t chunk = ((n + S0 - 1) / S0 + step - 1) / step * step;
     const uint32_t Sx = (uint32_t)((n + chunk - 1) / chunk);
