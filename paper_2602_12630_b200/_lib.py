@@ -147,17 +147,18 @@ class Context:
 
     @classmethod
     def pipeline(cls, device: int, k: int) -> "Context":
-        """Context k (0, 1, ...) of the forward pipeline on `device`: its own CUDA stream
-        (kept bound), its own scratch, the device's SRSs shared."""
+        """Context k (0, 1, ...) of the forward pipeline on `device` for the calling thread:
+        its own CUDA stream (kept bound), its own scratch, the device's SRSs shared."""
         import torch
 
+        key = (device, k, threading.get_ident())
         with cls._guard:
-            ctx = cls._pipeline.get((device, k))
+            ctx = cls._pipeline.get(key)
             if ctx is None:
                 ctx = cls(device)
                 ctx.fixed_stream = torch.cuda.Stream(device)
                 lib().tc_ctx_set_stream(ctx.handle, ctx.fixed_stream.cuda_stream)
-                cls._pipeline[(device, k)] = ctx
+                cls._pipeline[key] = ctx
         return ctx
 
     @classmethod
