@@ -351,6 +351,7 @@ def main():
     # one rank: forwards go through protocol.prover_commit_pipeline (PIPE_DEPTH device
     # contexts take them in turn; TC_BENCH_NO_PIPELINE=1: one prover_commit per forward)
     use_pipe = world == 1 and not os.environ.get("TC_BENCH_NO_PIPELINE")
+    use_pipe_dist = world > 1 and not os.environ.get("TC_BENCH_NO_PIPELINE")
     PIPE_DEPTH = int(os.environ.get("TC_PIPE_DEPTH", "3"))
 
     def all_launches():
@@ -362,6 +363,17 @@ def main():
             for _, root, _ in tcb.prover_commit_pipeline([dev_layers] * steps, srs, tree_config=tcfg,
                                                          node_srs=node_srs, route=route, depth=PIPE_DEPTH):
                 pass
+            return root
+        if use_pipe_dist:
+            # several ranks: each pipelines its own layers' commitments (the local tree of its
+            # layers is not used); per forward, the commitment gather and the global tree run
+            # on the host while the next forwards compute
+            for comms, _, _ in tcb.prover_commit_pipeline([dev_layers] * steps, srs, tree_config=tcfg,
+                                                          node_srs=node_srs, route=route, depth=PIPE_DEPTH):
+                encs = allgather_commitments([c.to_bytes() for c in comms], n_layers, rank, world,
+                                             device=dev if backend == "nccl" else None)
+                leaves = [tcb.hash_to_scalar(e, b"terkle/leaf") for e in encs]
+                root = tcb.build(tcfg, leaves, srs=node_srs)[1]
             return root
         for _ in range(steps):
             root = prove_step(dev_layers, route=route)
@@ -387,7 +399,7 @@ def main():
             ms = float(t.item())
         return ms, all_launches() - l0, root
 
-    value_run(max(args.warmup, PIPE_DEPTH if use_pipe else 0))   # every pipeline context warmed
+    value_run(max(args.warmup, PIPE_DEPTH if (use_pipe or use_pipe_dist) else 0))   # every pipeline context warmed
     with Clocks(local) as clk:
         ms, launches, root = timed(lambda: value_run(args.steps), 1)
     for _ in range(args.warmup):
@@ -474,7 +486,10 @@ def main():
                        "exceed the 126 MB L2", "srs": "generated once before timing (trusted setup)",
                        "step_api": (f"protocol.prover_commit_pipeline over the {args.steps} timed forwards "
                                     f"({PIPE_DEPTH} contexts; every forward's commitments, root and tree read back)"
-                                    if use_pipe else "protocol.prover_commit per forward")},
+                                    if use_pipe else
+                                    f"per rank: protocol.prover_commit_pipeline over its layers ({PIPE_DEPTH} contexts), "
+                                    "then per forward the commitment all-gather and the Terkle build" if use_pipe_dist
+                                    else "protocol.prover_commit per forward")},
             "overhead_pct": (100.0 * ms_step / fwd) if fwd else None,
             "forward_ms": fwd,
             "e2e": e2e,
