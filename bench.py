@@ -321,10 +321,11 @@ def main():
     host_pinned2 = [h.clone().pin_memory() for h in host_pinned]
 
     def e2e_stream(steps):
-        """`steps` forwards of pinned host activations through the streaming API: forward
-        k+1's upload runs under forward k's commitments; every forward's bytes are copied
-        inside the region.  One rank: protocol.prover_commit_stream; several: each rank
-        streams its own layers (tc_commit_stream), then the commitment gather and the tree."""
+        """`steps` forwards of pinned host activations through the public API; every
+        forward's bytes are copied inside the region.  protocol.prover_commit_pipeline (per
+        rank over its layers, then the commitment gather and the tree when N > 1); config 5
+        and TC_BENCH_NO_PIPELINE: protocol.prover_commit_stream / tc_commit_stream (forward
+        k+1's upload under forward k's commitments)."""
         batches = [host_pinned if k % 2 == 0 else host_pinned2 for k in range(steps)]
         root = None
         if use_pipe and args.config != 5:
@@ -333,6 +334,14 @@ def main():
             for _, root, _ in tcb.prover_commit_pipeline(batches, srs, tree_config=tcfg, node_srs=node_srs,
                                                          route=args.route, depth=PIPE_DEPTH):
                 pass
+            return root
+        if use_pipe_dist and args.config != 5:
+            for comms, _, _ in tcb.prover_commit_pipeline(batches, srs, tree_config=tcfg, node_srs=node_srs,
+                                                          route=args.route, depth=PIPE_DEPTH):
+                encs = allgather_commitments([c.to_bytes() for c in comms], n_layers, rank, world,
+                                             device=dev if backend == "nccl" else None)
+                leaves = [tcb.hash_to_scalar(e, b"terkle/leaf") for e in encs]
+                root = tcb.build(tcfg, leaves, srs=node_srs)[1]
             return root
         if world == 1:
             for _, root, _ in tcb.prover_commit_stream(batches, srs, tree_config=tcfg, node_srs=node_srs,
@@ -408,7 +417,7 @@ def main():
     if root_e2e != root:
         raise RuntimeError("e2e root differs from the device-resident root")
     ms_stream = None
-    e2e_stream(max(2, PIPE_DEPTH if use_pipe else 0))
+    e2e_stream(max(2, PIPE_DEPTH if (use_pipe or use_pipe_dist) else 0))
     ms_stream, _, root_s = timed(lambda: e2e_stream(args.steps), 1)
     if root_s != root:
         raise RuntimeError("streaming e2e root differs from the device-resident root")
@@ -467,8 +476,9 @@ def main():
                    path=(f"{args.steps} forwards of pinned host tensors through protocol.prover_commit_pipeline "
                          f"({PIPE_DEPTH} device contexts in turn: each uploads its forward on its own copy stream "
                          "and commits it while the others' forwards compute; first upload exposed) + device leaf "
-                         "hashing and Terkle tree + commitments / tree read back, per forward"
-                         if use_pipe and args.config != 5 else
+                         "hashing and Terkle tree + commitments / tree read back, per forward (N > 1: per "
+                         "rank over its layers, then the commitment gather and the Terkle build)"
+                         if (use_pipe or use_pipe_dist) and args.config != 5 else
                          f"{args.steps} forwards of pinned host tensors through the streaming API "
                          "(protocol.prover_commit_stream / tc_commit_stream per rank: forward k+1's upload "
                          "overlaps forward k's commit; first upload exposed) + commitment gather (N > 1) + "
