@@ -662,6 +662,42 @@ __global__ void __launch_bounds__(FPS_THREADS, 1024 / FPS_THREADS) k_fpb_scatter
   }
 }
 
+// mode-2 (fixed-base window) count with block-private counters: block (x, l) counts the
+// signed digits of chunk x of MSM l in shared memory (2^(c-1) counters) and flushes each
+// non-zero counter with one RED — the scatter (k_count_digits) keeps its global cursors
+__global__ void __launch_bounds__(1024) k_count_fb(const void* const* ptrs, uint64_t n, WinPlan P,
+                                                   uint32_t* __restrict__ cnt, uint64_t chunk) {
+  extern __shared__ uint32_t h[];
+  const uint32_t l = blockIdx.y;
+  const uint64_t c0 = (uint64_t)blockIdx.x * chunk;
+  const uint64_t c1 = min(n, c0 + chunk);
+  const void* p = ptrs[l];
+  for (uint32_t b = threadIdx.x; b < P.nbm; b += blockDim.x) h[b] = 0u;
+  __syncthreads();
+  const int c = P.cdig;
+  const uint32_t half = 1u << (c - 1), full = 1u << c;
+  for (uint64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+    Fe mag;
+    bool neg;
+    uint32_t f = 0;
+    load_scalar<DT_LIMBS>(p, i, 0, mag, neg, f);
+    uint32_t carry = 0;
+    for (int w = 0; w < P.ndig; w++) {
+      uint32_t d = window_bits(mag, w * c, c) + carry;
+      if (d > half) {
+        d = full - d, carry = 1;
+      } else {
+        carry = 0;
+      }
+      if (d) atomicAdd(h + d - 1u, 1u);
+    }
+  }
+  __syncthreads();
+  uint32_t* out = cnt + (uint64_t)l * P.nbm;
+  for (uint32_t b = threadIdx.x; b < P.nbm; b += blockDim.x)
+    if (h[b]) atomicAdd(out + b, h[b]);
+}
+
 // tot[l nbm + b] = sum over chunks of cnt[(l S + x) nbm + b]  (loads batched 8 deep: the
 // chunk rows are independent, a one-at-a-time loop is latency bound)
 __global__ void k_fpb_totals(const uint32_t* cnt, uint32_t nbm, uint32_t L, uint32_t S, uint32_t* tot) {
@@ -1416,6 +1452,21 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
         }
         return;
       }
+    }
+    static const bool no_fbc = getenv("TC_MSM_NO_FB_BLKCNT") != nullptr;
+    if (D == DT_LIMBS && P.mode == 2 && NC == 1 && !no_fbc && P.nbm * sizeof(uint32_t) <= 64 * 1024) {
+      // block-private counters: chunks of >= 16 K scalars, about two waves of 1024 threads
+      const uint64_t conc = (uint64_t)ctx->num_sms * 3;
+      const uint64_t S = std::max<uint64_t>(1, std::min<uint64_t>((conc + L - 1) / (uint64_t)L, n >> 14));
+      const uint64_t chunk = (n + S - 1) / S;
+      static bool fbc_attr = false;
+      if (!fbc_attr) {
+        cudaFuncSetAttribute(k_count_fb, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        fbc_attr = true;
+      }
+      k_count_fb<<<dim3((unsigned)((n + chunk - 1) / chunk), L), 1024, P.nbm * sizeof(uint32_t), st>>>(
+          d_ptrs, n, P, cnt, chunk);
+      return;
     }
     k_count_digits<D, false><<<dim3(gx, L), 256, 0, st>>>(d_ptrs, n, scale_bits, P, cnt, nullptr);
   });
