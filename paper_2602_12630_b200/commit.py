@@ -454,10 +454,42 @@ def tc_open(srs: Srs, T, point, *, scale_bits: int = SCALE_BITS, route: str = "a
     return TensorOpening(int.from_bytes(y.raw, "little"), decode_elems(pis.raw, m))
 
 
-def tc_open_many(srs: Srs, tensors, points, *, scale_bits: int = SCALE_BITS, route: str = "auto"):
-    """tc_open for many (tensor, point) pairs in one C call (tc_open_batch): the quotient
-    MSMs of a group of openings run as one batched pipeline per axis.  Same bytes as
-    calling tc_open on each pair."""
+_OPEN_POOL = None
+
+
+def _open_pool():
+    global _OPEN_POOL
+    if _OPEN_POOL is None:
+        import concurrent.futures as cf
+
+        _OPEN_POOL = cf.ThreadPoolExecutor(max_workers=2, thread_name_prefix="tc-open")
+    return _OPEN_POOL
+
+
+def _open_bins(tensors, nbins: int):
+    """Split opening indices into nbins sets, all openings of one tensor in one set (its
+    slice commitments are built once), balancing a rough cost: a tensor opened k >= 6 times
+    costs its slice commitments plus a little per opening, otherwise k full quotient MSMs."""
+    groups = {}
+    for i, T in enumerate(tensors):
+        groups.setdefault(id(T), []).append(i)
+    cost = lambda ids: 3.0 + 0.05 * len(ids) if len(ids) >= 6 else 1.4 * len(ids)
+    bins = [[] for _ in range(nbins)]
+    load = [0.0] * nbins
+    for ids in sorted(groups.values(), key=cost, reverse=True):
+        j = min(range(nbins), key=lambda b: load[b])
+        bins[j] += ids
+        load[j] += cost(ids)
+    return [sorted(b) for b in bins if b]
+
+
+def tc_open_many(srs: Srs, tensors, points, *, scale_bits: int = SCALE_BITS, route: str = "auto",
+                 parallel: int = 2):
+    """tc_open for many (tensor, point) pairs (tc_open_batch): the quotient MSMs of a group
+    of openings run as one batched pipeline per axis.  With `parallel` > 1 and enough
+    openings, the pairs are split by tensor over that many device contexts driven from
+    worker threads, so one set's latency-bound MSM tails overlap the other's compute.  Same
+    bytes as calling tc_open on each pair."""
     tensors, points = list(tensors), list(points)
     if len(tensors) != len(points):
         raise ValueError("tensors and points differ in length")
@@ -467,26 +499,49 @@ def tc_open_many(srs: Srs, tensors, points, *, scale_bits: int = SCALE_BITS, rou
     for pt in points:
         if len(pt) != m:
             raise ValueError("point arity does not match polynomial")
-    ctx = _lib.Context.get(srs.device)
-    keeps, ptrs, dts, cache = [], [], set(), {}
+    # device inputs on the calling thread's stream (the same layer opened many times is
+    # converted once)
+    cache, conv = {}, []
     for T in tensors:
-        if id(T) not in cache:   # the same layer opened many times is converted once
-            cache[id(T)] = _conv.device_input(T, srs.size, f"cuda:{ctx.device}")
-        ptr, dt, keep = cache[id(T)]
-        ptrs.append(ptr)
-        dts.add(dt)
-        keeps.append(keep)
-    if len(dts) > 1:
+        if id(T) not in cache:
+            cache[id(T)] = _conv.device_input(T, srs.size, f"cuda:{srs.device}")
+        conv.append(cache[id(T)])
+    if len({c[1] for c in conv}) > 1:
         raise ValueError("tc_open_many: all tensors must share one dtype")
+    if parallel > 1 and len(tensors) >= 32:
+        import torch
+
+        bins = _open_bins(tensors, parallel)
+        if len(bins) > 1:
+            cur = torch.cuda.current_stream(srs.device)
+
+            def work(ids):
+                ctx = _lib.Context.pipeline(srs.device, 0)   # one per worker thread
+                ctx.fixed_stream.wait_stream(cur)
+                return ids, _open_batch(ctx, srs, [conv[i] for i in ids], [points[i] for i in ids], scale_bits,
+                                        route)
+
+            out = [None] * len(tensors)
+            for ids, ops in _open_pool().map(work, bins):
+                for i, op in zip(ids, ops):
+                    out[i] = op
+            return out
+    return _open_batch(_lib.Context.get(srs.device), srs, conv, points, scale_bits, route, bind=True)
+
+
+def _open_batch(ctx, srs: Srs, conv, points, scale_bits, route, bind=False):
+    """One tc_open_batch call on `ctx` over device inputs (ptr, dtype, keep-alive)."""
+    m = len(srs.shape)
+    ptrs = [c[0] for c in conv]
     arr = (C.c_void_p * len(ptrs))(*ptrs)
     om = b"".join(encode_scalar(int(w)) for pt in points for w in pt)
     ys = C.create_string_buffer(21 * len(ptrs))
     pis = C.create_string_buffer(ELEM_BYTES * m * len(ptrs))
     with ctx.lock:
-        ctx.bind_stream()
-        ctx.check(_lib.lib().tc_open_batch(ctx.handle, srs.handle, arr, len(ptrs), dts.pop(), scale_bits, om,
+        if bind:
+            ctx.bind_stream()
+        ctx.check(_lib.lib().tc_open_batch(ctx.handle, srs.handle, arr, len(ptrs), conv[0][1], scale_bits, om,
                                            _route(route), ys, pis), "tc_open_many")
-    del keeps
     raw_y, raw_p = ys.raw, pis.raw
     return [TensorOpening(int.from_bytes(raw_y[21 * i:21 * (i + 1)], "little"),
                           decode_elems(raw_p[ELEM_BYTES * m * i:ELEM_BYTES * m * (i + 1)], m))

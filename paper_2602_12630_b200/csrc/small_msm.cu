@@ -144,6 +144,7 @@ int leaf_hash_device(tc_ctx* ctx, const Aff* d_comms, int count, uint64_t cap, F
 
 // build (once) the byte-window tables of the SRS's `which` elements
 static int small_tables(tc_ctx* ctx, tc_srs* srs, int which, const EdAff** out) {
+  std::lock_guard<std::mutex> guard(srs->mu);
   const int idx = (which == TC_SRS_LAGRANGE) ? 1 : 0;
   if (!srs->small_tab[idx]) {
     const Aff* pts = idx ? srs->lagrange : srs->monomial;

@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(128) k_win_step(const EdPk* in, uint64_t n, in
 namespace tcrt {
 
 int srs_window_table(tc_ctx* ctx, tc_srs* srs, const EdPk* bases, uint64_t n, const EdPk** out) {
+  std::lock_guard<std::mutex> guard(srs->mu);
   auto it = srs->wintab.find(bases);
   if (it != srs->wintab.end()) {
     *out = it->second;
@@ -179,6 +180,7 @@ int srs_window_table(tc_ctx* ctx, tc_srs* srs, const EdPk* bases, uint64_t n, co
 }
 
 int srs_exp_table(tc_ctx* ctx, tc_srs* srs, const EdPk* bases, uint64_t n, int depth, const EdPk** out) {
+  std::lock_guard<std::mutex> guard(srs->mu);
   if (srs->exptab && srs->exptab_depth >= depth) {
     *out = srs->exptab;
     return TC_OK;
@@ -235,12 +237,14 @@ int srs_edwards(tc_ctx* ctx, tc_srs* srs, int which, const EdPk** out) {
     n = srs->m > 1 ? srs->sublag_off[srs->m - 1] + srs->shape[srs->m - 1] : 0;
   }
   if (!src) return fail(ctx, TC_ERR_VALUE, "srs has no elements of kind %d", which);
+  std::lock_guard<std::mutex> guard(srs->mu);
   if (!*dst) {
-    if (cudaMalloc(dst, std::max<uint64_t>(n, 1) * sizeof(EdPk)) != cudaSuccess) {
-      *dst = nullptr;
+    EdPk* p = nullptr;
+    if (cudaMalloc(&p, std::max<uint64_t>(n, 1) * sizeof(EdPk)) != cudaSuccess)
       return fail(ctx, TC_ERR_MEMORY, "srs edwards alloc");
-    }
-    TC_TRY(to_edwards_device(ctx, src, n, *dst));
+    TC_TRY(to_edwards_device(ctx, src, n, p));
+    TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));   // shared with other contexts' streams
+    *dst = p;
   }
   *out = *dst;
   return TC_OK;

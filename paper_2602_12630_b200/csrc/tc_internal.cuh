@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -81,6 +82,8 @@ struct tc_srs {
   // exptab[k n + i] = 2^k G_i, k < exptab_depth (built on first use, grown on demand)
   tc::EdPk* exptab = nullptr;
   int exptab_depth = 0;
+  // guards the lazily built tables above when several contexts (threads) share the SRS
+  std::mutex mu;
   uint64_t sublag_off[TC_MAX_AXES] = {0};
 };
 

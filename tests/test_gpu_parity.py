@@ -306,6 +306,30 @@ def test_prover_commit_device_tree_matches_host_build(n_layers, node_shape):
         assert tcb.verify(root, i, leaves[i], pf, cfg, srs=node)
 
 
+def test_open_many_parallel_contexts_match_serial():
+    """tc_open_many with >= 32 openings splits them by tensor over two worker contexts
+    (threads, own streams): the same bytes as the single-context call and as tc_open, for
+    sliced tensors (>= 6 openings), rarely opened ones and on-grid points, and they verify."""
+    tcb = T()
+    shape = (8, 8, 16)
+    srs, td = tcb.setup_srs(shape, b"open-parallel")
+    g = np.random.default_rng(91)
+    xs = [torch.from_numpy((g.standard_t(3, 1024) * (1 + i)).astype(np.float16)).cuda() for i in range(5)]
+    rng = random.Random(17)
+    picks = [0] * 14 + [1] * 9 + [2] * 3 + [3] * 5 + [4] * 2
+    pts = [[rng.randrange(O.P) for _ in shape] for _ in picks]
+    pts[3] = [2, 5, 7]          # on the grid
+    pts[20] = [1, rng.randrange(O.P), 16]
+    ts = [xs[i] for i in picks]
+    par = tcb.tc_open_many(srs, ts, pts)
+    ser = tcb.tc_open_many(srs, ts, pts, parallel=1)
+    assert par == ser
+    C = [tcb.tc_commit(srs, x) for x in xs]
+    for k in (0, 3, 14, 20, 25, 31, 32):
+        assert par[k] == tcb.tc_open(srs, ts[k], pts[k])
+        assert tcb.tc_verify(srs, C[picks[k]], pts[k], par[k])
+
+
 @pytest.mark.parametrize("depth", [1, 2, 3])
 def test_prover_commit_pipeline_matches_prover_commit(depth):
     """prover_commit_pipeline (forwards taken in turn by `depth` contexts with their own
