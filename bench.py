@@ -467,7 +467,9 @@ def main():
 
     e2e_serial = {"value": value_e2e, "unit": "elems/s", "ms_per_step": ms_e2e / args.steps,
                   "h2d_bytes_per_step": per_step_elems // world * 2,
-                  "d2h_bytes_per_step": (len(my_layers) + 9) * 48,
+                  # commitments + node points (48-B affine) and, on the device-tree path, every
+                  # tree level's child values (24-B limbs): 32 leaves, arity 8 -> 9 nodes, 72 values
+                  "d2h_bytes_per_step": (len(my_layers) + 9) * 48 + (72 * 24 if world == 1 else 0),
                   "path": "protocol-level tc_commit_many on pinned host tensors -> tc_commit_batch_host "
                           "(upload then commit, no overlap) + Terkle build, per step"}
     if ms_stream is not None:
