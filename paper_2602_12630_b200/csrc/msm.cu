@@ -553,6 +553,9 @@ __global__ void __launch_bounds__(1024) k_fpb_pass(const void* const* ptrs, uint
 // global slot, and written out by consecutive threads — entries of one bucket (about 4 per
 // slice over 2^11 - 1 buckets) land in consecutive addresses from consecutive lanes, so
 // they share store transactions instead of costing one scattered 4-byte store each.
+#ifndef TC_FPB_THREADS
+#define TC_FPB_THREADS 1024   // block size of the block-private count / scatter passes
+#endif
 #ifndef TC_FPS_THREADS
 #define TC_FPS_THREADS 1024   // 16384-element slices: ~8 entries per bucket per slice (A/B: 512 -> 4.75 ms step, 1024 -> 4.70)
 #endif
@@ -1358,17 +1361,17 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
       }
       if (dtype == TC_DTYPE_F16) {
         if (scatter)
-          k_fpb_pass<1, true><<<dim3(Sx, nl), 1024, blk_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals, chunk, l0,
+          k_fpb_pass<1, true><<<dim3(Sx, nl), TC_FPB_THREADS, blk_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals, chunk, l0,
                                                                      nullptr);
         else
-          k_fpb_pass<1, false><<<dim3(Sx, nl), 1024, blk_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals, chunk, l0,
+          k_fpb_pass<1, false><<<dim3(Sx, nl), TC_FPB_THREADS, blk_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals, chunk, l0,
                                                                       spec_tab ? d_small : nullptr);
       } else {
         if (scatter)
-          k_fpb_pass<2, true><<<dim3(Sx, nl), 1024, blk_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals, chunk, l0,
+          k_fpb_pass<2, true><<<dim3(Sx, nl), TC_FPB_THREADS, blk_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals, chunk, l0,
                                                                      nullptr);
         else
-          k_fpb_pass<2, false><<<dim3(Sx, nl), 1024, blk_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals, chunk, l0,
+          k_fpb_pass<2, false><<<dim3(Sx, nl), TC_FPB_THREADS, blk_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals, chunk, l0,
                                                                       nullptr);
       }
     };
