@@ -513,6 +513,29 @@ __device__ __forceinline__ uint32_t fp_key(const WinPlan& P, uint64_t mag, uint3
   return P.mode == 3 ? (uint32_t)(mag >> g) - 1u : P.base[g] + (uint32_t)(mag >> g) - P.mlo[g];
 }
 
+// mode-3 bucket key straight from the fp16 bits: a normal value with exponent field e >=
+// 25 - scale_bits quantises exactly to (1024 + mantissa) 2^(e - 25 + scale_bits), so its key
+// is 1023 + mantissa and its table level e - 25 + scale_bits (the general path — RNE
+// rounding of small values, zeros, non-finite — through quant64 / fp_key otherwise).
+// Returns false for a zero (no entry).
+template <int DT>
+__device__ __forceinline__ bool key3(uint32_t raw, bool in, int scale_bits, const WinPlan& P, uint32_t& key,
+                                     uint32_t& g, bool& neg) {
+  if (DT == 1 && in) {
+    const int e = (int)((raw >> 10) & 0x1fu);
+    if (e >= 25 - scale_bits && e != 0x1f) {
+      key = 1023u + (raw & 0x3ffu);
+      g = (uint32_t)(e - 25 + scale_bits);
+      neg = (raw >> 15) != 0;
+      return true;
+    }
+  }
+  const uint64_t mag = in ? quant64<DT>(raw, scale_bits, neg) : 0ull;
+  if (!mag) return false;
+  key = fp_key(P, mag, g);
+  return true;
+}
+
 template <int DT, bool SCATTER>
 __global__ void __launch_bounds__(1024) k_fpb_pass(const void* const* ptrs, uint64_t n, int scale_bits, WinPlan P,
                                                    uint32_t* __restrict__ cnt, uint32_t* __restrict__ vals,
@@ -533,10 +556,17 @@ __global__ void __launch_bounds__(1024) k_fpb_pass(const void* const* ptrs, uint
     for (int k = 0; k < V_EPT; k++) {
       if (!SCATTER && DT == 1 && (raw[k] & 0x7c00u) == 0x7c00u) nf = 1u;
       bool neg;
-      const uint64_t mag = (i0 + k < c1) ? quant64<DT>(raw[k], scale_bits, neg) : 0ull;
-      if (mag) {
-        uint32_t g;
-        const uint32_t slot = atomicAdd(h + fp_key(P, mag, g), 1u);
+      uint32_t g, key;
+      bool hit;
+      if (P.mode == 3) {
+        hit = key3<DT>(raw[k], i0 + k < c1, scale_bits, P, key, g, neg);
+      } else {
+        const uint64_t mag = (i0 + k < c1) ? quant64<DT>(raw[k], scale_bits, neg) : 0ull;
+        hit = mag != 0;
+        if (hit) key = fp_key(P, mag, g);
+      }
+      if (hit) {
+        const uint32_t slot = atomicAdd(h + key, 1u);
         // mode 3 entries index the exponent table: 2^g G_i at g n + i
         if (SCATTER) vals[slot] = ((P.mode == 3 ? g * P.tpitch : 0u) + (uint32_t)(i0 + k)) | (neg ? SIGN_BIT : 0u);
       }
@@ -609,11 +639,10 @@ __global__ void __launch_bounds__(FPS_THREADS, 1024 / FPS_THREADS) k_fpb_scatter
         const int e = half * V_EPT + k;
         const uint32_t rawk = (wv[k >> 1] >> (16 * (k & 1))) & 0xffffu;
         bool neg;
-        const uint64_t mag = (i0 + k < c1) ? quant64<DT>(rawk, scale_bits, neg) : 0ull;
+        uint32_t g, kk;
         key[e] = 0xffffffffu;
-        if (mag) {
-          uint32_t g;
-          key[e] = fp_key(P, mag, g);
+        if (key3<DT>(rawk, i0 + k < c1, scale_bits, P, kk, g, neg)) {
+          key[e] = kk;
           val[e] = (g * P.tpitch + (uint32_t)(i0 + k)) | (neg ? SIGN_BIT : 0u);
           rk[e] = atomicAdd(lo + key[e], 1u);
         }
