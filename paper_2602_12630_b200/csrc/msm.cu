@@ -497,15 +497,16 @@ __global__ void __launch_bounds__(256) k_digits_fp(const void* const* ptrs, uint
   }
 }
 
-// mode-1 counting sort with block-private bucket counters (no global atomics at all).
+// Counting sort with block-private bucket counters (modes 1 and 3, no global atomics).
 // Block (x, l) owns chunk x of MSM l and keeps that MSM's nbm bucket counters in shared
-// memory.  k_count_fpb: shared-memory atomics, then the block's counts stored chunk-major
-// (cnt[(l S + x) nbm + b], coalesced).  k_fpb_totals / cub scan / k_fpb_starts turn them
-// into bucket starts and, in place, the start of every (chunk, bucket) run.  k_scatter_fpb:
-// the block loads its run starts into shared memory and hands out slots with shared-memory
-// atomics.  The scatter is launched a few MSMs at a time so the vals region being written
-// stays resident in L2 while the runs' partial sectors fill (one launch over all MSMs let
-// them leave L2 half-written: 1.30 ms vs 0.81 ms for the global-atomic scatter).
+// memory.  k_fpb_pass<.., false>: shared-memory atomics, then the block's counts stored
+// chunk-major (cnt[(l S + x) nbm + b], coalesced).  k_fpb_totals / cub scan / k_fpb_starts
+// turn them into bucket starts and, in place, the start of every (chunk, bucket) run.
+// Scatter: mode 3 k_fpb_scatter_sorted (slice-local counting sort, below); mode 1
+// k_fpb_pass<.., true>: the block loads its run starts into shared memory and hands out
+// slots with shared-memory atomics, launched a few MSMs at a time so the vals region being
+// written stays resident in L2 while the runs' partial sectors fill (one launch over all
+// MSMs let them leave L2 half-written: 1.30 ms vs 0.81 ms for the global-atomic scatter).
 __device__ __forceinline__ uint32_t fp_key(const WinPlan& P, uint64_t mag, uint32_t& g) {
   const int bl = 64 - __clzll((long long)mag);
   g = bl > P.mbits ? (uint32_t)(bl - P.mbits) : 0u;
