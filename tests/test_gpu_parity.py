@@ -516,6 +516,11 @@ x = xs[1].copy(); x[::7] = 0; x[5] = np.float16(65504.0); x[6] = np.float16(-6e-
 comms = tcb.tc_commit_many(srs, [torch.from_numpy(v).cuda() for v in xs])
 for v, c in zip(xs, comms):
     assert c.elem == O.commit_trapdoor(O.quantize(v.astype(np.float64), 16), shape, list(td.taus))
+# the same batch as bf16 (8 significant bits: 255 buckets per MSM, deeper exponent table)
+bs = [torch.from_numpy(v.astype(np.float32)).to(torch.bfloat16) for v in xs[:4]]
+comms = tcb.tc_commit_many(srs, [b.cuda() for b in bs])
+for b, c in zip(bs, comms):
+    assert c.elem == O.commit_trapdoor(O.quantize(b.float().numpy().astype(np.float64), 16), shape, list(td.taus))
 print("ok")
 """
 
