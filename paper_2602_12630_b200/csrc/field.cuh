@@ -412,11 +412,15 @@ struct Field {
 #endif
   }
 
-  // u * M5 for the small top limb of the modulus (q: 0xF0 = 2^8 - 2^4, p: 2).  With
-  // -DTC_REDC_SHIFT the device uses shifts (ALU pipe) instead of the half-rate IMAD.WIDE;
-  // measured 5% SLOWER in k_accum_aff (ptxas then emits twice the IMAD.MOVs), so off.
+  // u * M5 for the small top limb of the modulus (q: 0xF0 = 2^8 - 2^4, p: 2).  The device
+  // uses shifts (ALU pipe) instead of the half-rate IMAD.WIDE on the fma-heavy pipe that
+  // bounds the accumulation (TC_REDC_SHIFT=0 restores the product): k_accum_aff 4.03 ->
+  // 3.97 ms with the exponent-table plan (it measured 5 % slower in an earlier XYZZ build).
+#ifndef TC_REDC_SHIFT
+#define TC_REDC_SHIFT 1
+#endif
   TC_HD static uint64_t mul_m5(uint32_t u) {
-#if defined(__CUDA_ARCH__) && defined(TC_REDC_SHIFT)
+#if defined(__CUDA_ARCH__) && TC_REDC_SHIFT
     uint64_t r;
     if (PM::M5 == 0xF0u) {
       asm("{.reg .u64 a, b;\n\t"
