@@ -577,14 +577,13 @@ def run_openings(args, dev, rank, world):
     for _ in range(max(1, args.warmup)):
         tcb.tc_open_many(srs, [layers[l] for l, _ in chals], [pt for _, pt in chals])
         warm_tree, _ = tcb.build(tree.config, tree.values[0][:tree.n], srs=tree.srs)
-        for l, _ in chals:
-            tcb.prove(warm_tree, l)
+        tcb.prove_many(warm_tree, [l for l, _ in chals])
     tree, _ = tcb.build(tree.config, tree.values[0][:tree.n], srs=tree.srs)
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     ops = tcb.tc_open_many(srs, [layers[l] for l, _ in chals], [pt for _, pt in chals])
     t_open = time.perf_counter() - t0
-    proofs = [tcb.prove(tree, l) for l, _ in chals]
+    proofs = tcb.prove_many(tree, [l for l, _ in chals])   # node openings batched (tc_open_many)
     torch.cuda.synchronize(dev)
     wall = time.perf_counter() - t0
     # spot-check: the batched openings verify on the CPU verifier, membership proofs too

@@ -6,7 +6,7 @@ opening proofs, with hand-written sm_100a CUDA kernels behind a C ABI
 (include/tc_b200.h, libtcb200.so).  There is no CPU fallback: without the built library
 or a CUDA device the compute entry points raise.
 """
-from .authtree import MembershipProof, TerkleTree, TreeConfig, build, leaf_of, prove, verify
+from .authtree import MembershipProof, TerkleTree, TreeConfig, build, leaf_of, prove, prove_many, verify
 from .capture import ActivationCapture, infer_and_capture
 from .commit import (Commitment, Srs, TensorOpening, Trapdoors, derive_taus, load_srs, pair, setup_srs, tc_commit,
                      tc_commit_many, tc_commit_stream, tc_open, tc_open_many, tc_verify)
@@ -19,6 +19,6 @@ __all__ = [
     "ActivationCapture", "infer_and_capture", "Commitment", "FieldTensor", "G", "Grid", "MembershipProof", "MultiPoly", "P", "PrimeField", "Q", "Srs",
     "TensorOpening", "TerkleTree", "Trapdoors", "TreeConfig", "build", "decode_elem", "decode_scalar", "default_grid",
     "derive_taus", "encode_elem", "encode_scalar", "evaluate", "hash_to_scalar", "interpolate_lagrange", "leaf_of",
-    "lex_index", "load_srs", "open_quotients", "pair", "prove", "prover_commit", "prover_commit_pipeline", "prover_commit_stream", "quantize", "setup_srs", "tc_commit",
+    "lex_index", "load_srs", "open_quotients", "pair", "prove", "prove_many", "prover_commit", "prover_commit_pipeline", "prover_commit_stream", "quantize", "setup_srs", "tc_commit",
     "tc_commit_many", "tc_commit_stream", "tc_open", "tc_open_many", "tc_verify", "verify",
 ]

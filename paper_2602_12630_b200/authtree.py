@@ -192,6 +192,32 @@ def prove(tree: TerkleTree, i: int) -> MembershipProof:
     return MembershipProof(i, tuple(nodes), tuple(openings))
 
 
+def prove_many(tree: TerkleTree, indices) -> list:
+    """prove() for many leaves: the node openings none of them has memoised yet are computed
+    together (one tc_open_many call: for the tiny node SRS, every quotient MSM in one
+    table-kernel launch), then each proof is assembled as prove() does."""
+    from .commit import tc_open_many
+
+    B = tree.config.arity
+    need = {}
+    for i in indices:
+        if not 0 <= i < tree.n:
+            raise IndexError(f"leaf index {i} out of range")
+        pos = i
+        for l in range(tree.depth):
+            u, slot = divmod(pos, B)
+            if (l, u, slot) not in tree._openings:
+                need[(l, u, slot)] = None
+            pos = u
+    if need:
+        keys = list(need)
+        zs = [tree.values[l][u * B:(u + 1) * B] for l, u, _ in keys]
+        pts = [child_point(slot, tree.config.shape) for _, _, slot in keys]
+        for key, op in zip(keys, tc_open_many(tree.srs, zs, pts)):
+            tree._openings[key] = op
+    return [prove(tree, i) for i in indices]
+
+
 def verify(root, i: int, leaf: int, proof: MembershipProof, config: TreeConfig, *, srs: Srs = None) -> bool:
     """Every level's opening verifies, opens the expected child value, and the top node
     is the root."""

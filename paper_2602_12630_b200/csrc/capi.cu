@@ -1175,7 +1175,7 @@ int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int 
     return TC_ERR_ARGUMENT;
   const uint64_t n = srs->n;
   const int m = srs->m;
-  std::vector<int> lag;
+  std::vector<int> lag, tiny_ops;
   for (int i = 0; i < count; i++) {
     if (!d_ins[i]) return TC_ERR_ARGUMENT;
     std::vector<Fe> om(m);
@@ -1188,9 +1188,47 @@ int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int 
     const bool tiny = n <= SMALL_MSM_MAX && srs->monomial && route == TC_ROUTE_AUTO;
     if (lag_ok && route != TC_ROUTE_MONOMIAL && !tiny)
       lag.push_back(i);
+    else if (tiny)
+      tiny_ops.push_back(i);
     else
       TC_TRY(tc_open(ctx, srs, d_ins[i], dtype, scale_bits, omegas_le21 + 21 * (size_t)i * m, route,
                      out_y21 + 21 * (size_t)i, out_pi43 + 43 * (size_t)i * m));
+  }
+  if (!tiny_ops.empty()) {
+    // tiny SRSs (Terkle node openings): tc_open's monomial route for all of them with no
+    // host round trip per opening — interpolation and synthetic division per tensor, every
+    // quotient MSM in ONE table-kernel launch, one readback of the points and the values
+    const uint64_t K = tiny_ops.size();
+    Fe *tv, *tq, *ty;
+    Aff* tout;
+    TC_TRY(tcrt::scratch_t(ctx, "opent.vals", K * n, &tv));
+    TC_TRY(tcrt::scratch_t(ctx, "opent.q", K * m * n, &tq));
+    TC_TRY(tcrt::scratch_t(ctx, "opent.y", K, &ty));
+    TC_TRY(tcrt::scratch_t(ctx, "opent.out", K * m, &tout));
+    std::vector<const void*> ptrs(K * m);
+    std::vector<Fe> om(m);
+    for (uint64_t k = 0; k < K; k++) {
+      const int i = tiny_ops[k];
+      Fe* v = tv + k * n;
+      if (dtype == TC_DTYPE_FP_LIMBS)
+        TC_CUDA(ctx, cudaMemcpyAsync(v, d_ins[i], n * sizeof(Fe), cudaMemcpyDeviceToDevice, ctx->stream));
+      else
+        TC_TRY(tcrt::quantize_device(ctx, d_ins[i], dtype, n, scale_bits, v));
+      TC_TRY(tcrt::interpolate_device(ctx, v, srs->shape, m));
+      for (int j = 0; j < m; j++) le21_to_fe(omegas_le21 + 21 * ((size_t)i * m + j), om[j]);
+      TC_TRY(tcrt::open_quotients_device(ctx, v, srs->shape, m, om.data(), tq + k * m * n, nullptr, ty + k));
+      for (int a = 0; a < m; a++) ptrs[k * m + a] = tq + (k * m + a) * n;
+    }
+    TC_TRY(msm_srs(ctx, srs, TC_SRS_MONOMIAL, TC_DTYPE_FP_LIMBS, 0, ptrs.data(), (int)(K * m), tout));
+    std::vector<uint8_t> enc(K * m * 43);
+    TC_TRY(fetch_encode_many(ctx, tout, (int)(K * m), enc.data()));
+    std::vector<Fe> ys(K);
+    TC_CUDA(ctx, cudaMemcpy(ys.data(), ty, K * sizeof(Fe), cudaMemcpyDeviceToHost));
+    for (uint64_t k = 0; k < K; k++) {
+      const int i = tiny_ops[k];
+      fe_to_le21(Fp::canon(ys[k]), out_y21 + 21 * (size_t)i);
+      memcpy(out_pi43 + 43 * (size_t)i * m, enc.data() + 43 * k * m, 43 * (size_t)m);
+    }
   }
   if (lag.empty()) return TC_OK;
   const EdPk *ed_lag, *ed_sub = nullptr;

@@ -610,7 +610,7 @@ int interpolate_device(tc_ctx* ctx, Fe* d_vals, const uint32_t* shape, int m) {
 // r (scratch copy of the coefficients) is consumed; quotients are m x n, zero outside
 // their support.  omega canonical; returns y canonical on the host.
 int open_quotients_device(tc_ctx* ctx, const Fe* d_coeffs, const uint32_t* shape, int m,
-                          const Fe* omega_canon, Fe* d_quotients, Fe* h_y) {
+                          const Fe* omega_canon, Fe* d_quotients, Fe* h_y, Fe* d_y) {
   cudaStream_t st = ctx->stream;
   uint64_t n = 1;
   for (int j = 0; j < m; j++) n *= shape[j];
@@ -626,6 +626,10 @@ int open_quotients_device(tc_ctx* ctx, const Fe* d_coeffs, const uint32_t* shape
     k_divide_axis<<<blocks_for(s, 128), 128, 0, st>>>(r, d_quotients + (uint64_t)a * n, d, s, vm);
     TC_LAUNCHED(ctx);
     span = s;
+  }
+  if (d_y) {   // batched openings: y stays on the device, no host round trip here
+    TC_CUDA(ctx, cudaMemcpyAsync(d_y, r, sizeof(Fe), cudaMemcpyDeviceToDevice, st));
+    return TC_OK;
   }
   TC_CUDA(ctx, cudaMemcpyAsync(h_y, r, sizeof(Fe), cudaMemcpyDeviceToHost, st));
   TC_CUDA(ctx, cudaStreamSynchronize(st));

@@ -237,6 +237,6 @@ int slice_scalars_device(tc_ctx* ctx, const std::vector<tc::Fe>& tabs_host, cons
 
 // open_quotients on device: coefficient array (canonical) -> m quotient arrays + y
 int open_quotients_device(tc_ctx* ctx, const tc::Fe* d_coeffs, const uint32_t* shape, int m,
-                          const tc::Fe* omega_canon, tc::Fe* d_quotients, tc::Fe* h_y);
+                          const tc::Fe* omega_canon, tc::Fe* d_quotients, tc::Fe* h_y, tc::Fe* d_y = nullptr);
 
 }  // namespace tcrt

@@ -306,6 +306,24 @@ def test_prover_commit_device_tree_matches_host_build(n_layers, node_shape):
         assert tcb.verify(root, i, leaves[i], pf, cfg, srs=node)
 
 
+def test_prove_many_matches_prove():
+    """prove_many (all missing node openings through one tc_open_many: the batched tiny-SRS
+    path, one table-kernel launch for every quotient MSM) gives prove()'s proofs, and they
+    verify, on a 40-leaf tree with padding."""
+    tcb = T()
+    cfg = tcb.TreeConfig(shape=(2, 2, 2))
+    rng = random.Random(23)
+    leaves = [rng.randrange(O.P) for _ in range(40)]
+    tree, root = tcb.build(cfg, leaves)
+    idx = [rng.randrange(40) for _ in range(50)] + [0, 39]
+    many = tcb.prove_many(tree, idx)
+    tree2, root2 = tcb.build(cfg, leaves)
+    assert root2 == root
+    for i, pf in zip(idx, many):
+        assert pf == tcb.prove(tree2, i)
+        assert tcb.verify(root, i, leaves[i], pf, cfg)
+
+
 def test_open_many_parallel_contexts_match_serial():
     """tc_open_many with >= 32 openings splits them by tensor over two worker contexts
     (threads, own streams): the same bytes as the single-context call and as tc_open, for
