@@ -566,7 +566,7 @@ def run_openings(args, dev, rank, world):
     layers_host = make_layers_host(cfg, range(cfg["layers"]))
     layers = [torch.from_numpy(h).to(dev) for h in layers_host]
     srs, _ = tcb.setup_srs(cfg["shape"], b"tc-b200/config3", device=dev.index)
-    comms, root, tree = tcb.prover_commit(layers, srs)
+    comms, root, tree = tcb.prover_commit(layers, srs, return_tree=True)
     score = np.random.default_rng(4).pareto(1.5, cfg["layers"]) + 1e-3
     picks = np.random.default_rng(5).choice(cfg["layers"], size=256, p=score / score.sum())
     rng = random.Random(6)

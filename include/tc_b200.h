@@ -59,7 +59,13 @@ enum {
 };
 
 /* SRS contents */
-enum { TC_SRS_MONOMIAL = 1, TC_SRS_LAGRANGE = 2 };
+enum {
+  TC_SRS_MONOMIAL = 1,
+  TC_SRS_LAGRANGE = 2,
+  /* (export / has only) the sub-grid Lagrange sets g^{prod_{j>=i} L_{j,w_j}(tau_j)} for the
+   * axis suffixes i = 1..m-1, concatenated in order of i (prod_{j>=i} d_j elements each) */
+  TC_SRS_SUBGRID = 4
+};
 
 /* commit / open routes (all produce identical bytes: the commitment g^{f_T(tau)} is unique) */
 enum {
@@ -92,9 +98,15 @@ int tc_ctx_kernel_stats(const tc_ctx* ctx, const char* name, double* ms, uint64_
  * grid 1..d_j (mvpoly.py:130-133).  taus_le21: m x 21 bytes (canonical, < p). */
 int tc_srs_generate(tc_ctx* ctx, const uint32_t* shape, int m, const uint8_t* taus_le21,
                     int flags, tc_srs** out);
-/* SRS from public points (TCSR payload): monomial43 N x 43 B, axis43 m x 43 B */
+/* SRS from public points (TCSR payload): monomial43 N x 43 B, axis43 m x 43 B.
+ * The Lagrange elements and sub-grid sets are derived from the monomial ones on the device
+ * (tc_srs_derive_lagrange), so a loaded SRS takes the same fast routes as a generated one. */
 int tc_srs_load(tc_ctx* ctx, const uint32_t* shape, int m, const uint8_t* monomial43,
                 const uint8_t* axis43, tc_srs** out);
+/* Trapdoor-free Lagrange SRS (trapdoors stay with the trusted setup):
+ * g^{prod_j L_{j,w_j}(tau_j)} computed from the monomial elements alone by the transpose of
+ * the per-axis Newton interpolation applied to group elements.  No-op when present. */
+int tc_srs_derive_lagrange(tc_ctx* ctx, tc_srs* srs);
 /* export elements [offset, offset+count) as count x 43 B (which = TC_SRS_MONOMIAL |
  * TC_SRS_LAGRANGE), or the m axis elements */
 int tc_srs_export(tc_ctx* ctx, const tc_srs* srs, int which, uint64_t offset, uint64_t count,
@@ -146,6 +158,10 @@ int tc_commit_batch_host(tc_ctx* ctx, const tc_srs* srs, const void* const* h_in
 int tc_commit_stream(tc_ctx* ctx, const tc_srs* srs, const void* const* h_cur,
                      const void* const* h_next, int count, int dtype, int scale_bits, int route,
                      uint8_t* out43);
+
+/* Forget any upload a previous tc_commit_stream* call prefetched (the caller abandoned its
+ * stream of forwards, e.g. a consumer stopped early): the next call uploads h_cur afresh. */
+int tc_commit_stream_reset(tc_ctx* ctx);
 
 /* ---- tc_open: y = f_T(omega), pi_i = g^{q_i(tau)} ----------------------- */
 int tc_open(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int scale_bits,

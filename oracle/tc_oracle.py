@@ -513,6 +513,49 @@ def barycentric_eval(values, shape, point, axes_nodes=None):
     return flat[0]
 
 
+def barycentric_eval_small(q, shape, point, axes_nodes=None):
+    """barycentric_eval for a tensor of SMALL signed integers (numpy int64, |q| < 2^30, e.g.
+    quantised fp16 activations): the first contraction (the leading axis, all but N/d_0 of
+    the work) runs exactly in numpy over 24-bit limbs of the Lagrange factors — each limb
+    sum stays below 2^63 — and the remaining axes as in barycentric_eval.  Same value as
+    barycentric_eval(q mod p, ...); test-only speed-up for full-size configs."""
+    import numpy as np
+
+    q = np.asarray(q, dtype=np.int64).reshape(-1)
+    n = check_shape(shape)
+    if q.size != n:
+        raise ValueError("tensor size does not match grid shape")
+    if len(point) != len(shape):
+        raise ValueError("evaluation point arity does not match grid")
+    if q.size and int(np.abs(q).max()) >= 1 << 30:
+        raise ValueError("barycentric_eval_small needs |q| < 2^30")
+    d0 = shape[0]
+    nodes = axes_nodes[0] if axes_nodes else default_nodes(d0)
+    fac = lagrange_at(nodes, point[0])
+    LB, NL = 24, 7                                        # 7 x 24 bits >= 162
+    limbs = np.array([[(f >> (LB * k)) & ((1 << LB) - 1) for f in fac] for k in range(NL)], dtype=np.int64)
+    acc = limbs @ q.reshape(d0, n // d0)                  # (NL, N/d0), |entries| < 2^24 2^30 2^7
+    rows = [r.tolist() for r in acc]
+    flat = [sum(rows[k][b] << (LB * k) for k in range(NL)) % P for b in range(n // d0)]
+    for j in range(1, len(shape)):
+        nj = axes_nodes[j] if axes_nodes else default_nodes(shape[j])
+        flat = contract_leading(flat, shape[j:], lagrange_at(nj, point[j]))
+    return flat[0]
+
+
+def quantize_signed(values, scale_bits: int = SCALE_BITS):
+    """quantize() as signed int64 (numpy) for inputs whose |v| 2^scale_bits < 2^62."""
+    import numpy as np
+
+    flat = np.asarray(values).reshape(-1).astype(np.float64)
+    if not np.all(np.isfinite(flat)):
+        raise ValueError("quantize: non-finite value")
+    scaled = np.ldexp(flat, scale_bits)
+    if not np.all(np.abs(scaled) < 2.0 ** 62):
+        raise ValueError("quantize_signed: magnitude too large for int64")
+    return np.rint(scaled).astype(np.int64)
+
+
 # ---------------------------------------------------------------------------
 # quantize — SPEC.md:536-544, 605
 # ---------------------------------------------------------------------------
@@ -697,6 +740,25 @@ def terkle_child_point(pos: int, node_shape):
         idx.append(pos % d + 1)
         pos //= d
     return list(reversed(idx))
+
+
+def terkle_verify(root, i: int, leaf: int, nodes, openings, node_shape, axis_elems) -> bool:
+    """Membership check: for every level (bottom first) the opening
+    (y, proofs) of the node at its child's grid point verifies (tc_verify, product of
+    pairings) and opens the expected child value; the next expected value is the node's
+    hash; the top node is the root."""
+    B = check_shape(node_shape)
+    expected = leaf % P
+    pos = i
+    for node, (y, proofs) in zip(nodes, openings):
+        u, slot = divmod(pos, B)
+        if y != expected:
+            return False
+        if not tc_verify(axis_elems, node, terkle_child_point(slot, node_shape), y, list(proofs)):
+            return False
+        expected = hash_to_scalar(encode_elem(node), NODE_TAG)
+        pos = u
+    return pos == 0 and len(nodes) > 0 and nodes[-1] == root
 
 
 def leaf_of_commitment(c) -> int:

@@ -18,7 +18,7 @@ TC_ERR_VALUE, TC_ERR_INDEX, TC_ERR_ZERO_DIVISION, TC_ERR_BACKEND, TC_ERR_OVERFLO
 TC_ERR_CUDA, TC_ERR_MEMORY, TC_ERR_ARGUMENT = 10, 11, 12
 
 DTYPE_F16, DTYPE_BF16, DTYPE_F32, DTYPE_F64, DTYPE_FP_LIMBS = 1, 2, 3, 4, 16
-SRS_MONOMIAL, SRS_LAGRANGE = 1, 2
+SRS_MONOMIAL, SRS_LAGRANGE, SRS_SUBGRID = 1, 2, 4
 ROUTE_AUTO, ROUTE_MONOMIAL, ROUTE_LAGRANGE = 0, 1, 2
 
 
@@ -55,6 +55,7 @@ _SIGS = [
                                       C.POINTER(C.c_double)]),
     ("tc_srs_generate", C.c_int, [_P, _U32P, C.c_int, C.c_char_p, C.c_int, C.POINTER(_P)]),
     ("tc_srs_load", C.c_int, [_P, _U32P, C.c_int, C.c_char_p, C.c_char_p, C.POINTER(_P)]),
+    ("tc_srs_derive_lagrange", C.c_int, [_P, _P]),
     ("tc_srs_export", C.c_int, [_P, _P, C.c_int, C.c_uint64, C.c_uint64, _P]),
     ("tc_srs_export_axis", C.c_int, [_P, _P]),
     ("tc_srs_has", C.c_int, [_P, C.c_int]),
@@ -69,6 +70,7 @@ _SIGS = [
     ("tc_commit_batch", C.c_int, [_P, _P, C.POINTER(_P), C.c_int, C.c_int, C.c_int, C.c_int, _P]),
     ("tc_commit_batch_host", C.c_int, [_P, _P, C.POINTER(_P), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P]),
     ("tc_commit_stream", C.c_int, [_P, _P, C.POINTER(_P), C.POINTER(_P), C.c_int, C.c_int, C.c_int, C.c_int, _P]),
+    ("tc_commit_stream_reset", C.c_int, [_P]),
     ("tc_open", C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_char_p, C.c_int, _P, _P]),
     ("tc_open_batch", C.c_int, [_P, _P, C.POINTER(_P), C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_int, _P, _P]),
     ("tc_terkle_build", C.c_int, [_P, _P, C.c_char_p, C.c_uint64, _P, C.POINTER(C.c_uint64)]),

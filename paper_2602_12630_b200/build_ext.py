@@ -7,7 +7,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libtcb200.so")
-SOURCES = ["capi.cu", "msm.cu", "small_msm.cu", "srs.cu", "quantize.cu", "interp.cu"]
+SOURCES = ["capi.cu", "msm.cu", "small_msm.cu", "srs.cu", "derive.cu", "quantize.cu", "interp.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",

@@ -132,6 +132,16 @@ class Srs:
     def lagrange_elems(self):
         return self._export(_lib.SRS_LAGRANGE)
 
+    def derive_lagrange(self) -> "Srs":
+        """Derive the Lagrange elements (and sub-grid sets) from the monomial elements on the
+        device, without the trapdoors (a no-op when present).  Returns self."""
+        ctx = _lib.Context.get(self.device)
+        with ctx.lock:
+            ctx.bind_stream()
+            ctx.check(_lib.lib().tc_srs_derive_lagrange(ctx.handle, self._h), "derive_lagrange")
+        self._cache.pop(_lib.SRS_LAGRANGE, None)
+        return self
+
     def to_bytes(self) -> bytes:
         """TCSR file: header, monomial elements, axis elements, grid."""
         out = [shape_header(b"TCSR", self.shape)]
@@ -198,7 +208,9 @@ def setup_srs(shape, entropy: bytes, *, lagrange: bool = True, monomial: bool = 
 
 
 def load_srs(shape, monomial43: bytes, axis43: bytes, device=None) -> Srs:
-    """Srs from public points only (e.g. a TCSR file); monomial commit route only."""
+    """Srs from public points only (e.g. a TCSR file).  The Lagrange elements
+    and sub-grid sets the fast commit / open routes use are derived on the device from the
+    monomial elements alone (tc_srs_derive_lagrange): no trapdoor is needed."""
     shape = tuple(int(d) for d in shape)
     check_shape(shape)
     ctx = _lib.Context.get(device)
@@ -346,9 +358,14 @@ def tc_commit_tree_launch(ctx, srs: Srs, tensors, node_srs: Srs, *, scale_bits: 
 
     tensors = list(tensors)
     host = _host_floats(tensors)
+    conv = None
+    if host is None:
+        # conversions (contiguous copies, H2D limbs, cross-device moves) are enqueued on
+        # torch's current stream: do them BEFORE the pipeline stream is ordered after it
+        conv = [_conv.device_input(T, srs.size, f"cuda:{ctx.device}") for T in tensors]
     with ctx.lock:
         # the context's stream runs after everything already queued on torch's stream (the
-        # inputs' producers, SRS setup)
+        # inputs' producers and conversions, SRS setup)
         ctx.fixed_stream.wait_stream(torch.cuda.current_stream(ctx.device))
         if host is not None:
             ts, code = host
@@ -361,12 +378,9 @@ def tc_commit_tree_launch(ctx, srs: Srs, tensors, node_srs: Srs, *, scale_bits: 
                                                               _route(route), node_srs.handle),
                       "tc_commit_tree_launch")
         else:
-            keeps, ptrs, dts = [], [], set()
-            for T in tensors:
-                ptr, dt, k = _conv.device_input(T, srs.size, f"cuda:{ctx.device}")
-                ptrs.append(ptr)
-                dts.add(dt)
-                keeps.append(k)
+            ptrs = [c[0] for c in conv]
+            dts = {c[1] for c in conv}
+            keeps = [c[2] for c in conv]
             if len(dts) != 1:
                 raise ValueError("tc_commit_tree: all tensors must share one dtype")
             arr = (C.c_void_p * len(ptrs))(*ptrs)

@@ -300,9 +300,9 @@ int srs_build_edwards(tc_ctx* ctx, tc_srs* srs) {
   return TC_OK;
 }
 
-// sub-grid Lagrange sets for the suffixes i = 1..m-1 (Lagrange-route opening quotients)
-int srs_build_sublag(tc_ctx* ctx, tc_srs* srs, const std::vector<Fe>& taus) {
-  if (srs->m < 2) return TC_OK;
+// sub-grid Lagrange sets for the suffixes i = 1..m-1 (Lagrange-route opening quotients):
+// offsets and allocation
+int srs_alloc_sublag(tc_ctx* ctx, tc_srs* srs) {
   uint64_t total = 0;
   for (int i = 1; i < srs->m; i++) {
     uint64_t ni = 1;
@@ -311,8 +311,34 @@ int srs_build_sublag(tc_ctx* ctx, tc_srs* srs, const std::vector<Fe>& taus) {
     total += ni;
   }
   TC_CUDA(ctx, cudaMalloc(&srs->sublag, total * sizeof(Aff)));
+  return TC_OK;
+}
+
+int srs_build_sublag(tc_ctx* ctx, tc_srs* srs, const std::vector<Fe>& taus) {
+  if (srs->m < 2) return TC_OK;
+  TC_TRY(srs_alloc_sublag(ctx, srs));
   for (int i = 1; i < srs->m; i++)
     TC_TRY(srs_fill_points(ctx, srs->shape + i, srs->m - i, taus.data() + i, true, srs->sublag + srs->sublag_off[i]));
+  return TC_OK;
+}
+
+// Lagrange elements and sub-grid sets from the monomial elements alone (no trapdoor): the
+// suffix set i is the Lagrange transform of the first prod_{j>=i} d_j monomial elements
+// (lex indices with zero leading coordinates = g^{prod_{j>=i} tau_j^{i_j}}) over axes i..m-1
+int srs_derive_lagrange(tc_ctx* ctx, tc_srs* srs) {
+  if (!srs->monomial) return fail(ctx, TC_ERR_VALUE, "srs has no monomial elements to derive from");
+  if (srs->lagrange) return TC_OK;
+  const EdPk* mono;
+  TC_TRY(tcrt::srs_edwards(ctx, srs, TC_SRS_MONOMIAL, &mono));
+  TC_CUDA(ctx, cudaMalloc(&srs->lagrange, srs->n * sizeof(Aff)));
+  TC_TRY(tcrt::derive_lagrange_device(ctx, mono, srs->shape, srs->m, srs->lagrange));
+  if (srs->m > 1) {
+    TC_TRY(srs_alloc_sublag(ctx, srs));
+    for (int i = 1; i < srs->m; i++)
+      TC_TRY(tcrt::derive_lagrange_device(ctx, mono, srs->shape + i, srs->m - i, srs->sublag + srs->sublag_off[i]));
+  }
+  TC_TRY(srs_build_edwards(ctx, srs));
+  TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return TC_OK;
 }
 
@@ -555,6 +581,9 @@ int tc_srs_load(tc_ctx* ctx, const uint32_t* shape, int m, const uint8_t* monomi
       s = fail(ctx, TC_ERR_VALUE, "srs element: bad encoding or point not on curve");
   }
   if (!s) s = srs_build_edwards(ctx, srs);
+  // a published SRS has no Lagrange elements: derive them (and the sub-grid sets) from the
+  // monomial ones, so commits and openings on it take the Lagrange route
+  if (!s) s = srs_derive_lagrange(ctx, srs);
   if (s) {
     tc_srs_destroy(srs);
     return s;
@@ -563,11 +592,20 @@ int tc_srs_load(tc_ctx* ctx, const uint32_t* shape, int m, const uint8_t* monomi
   return TC_OK;
 }
 
+int tc_srs_derive_lagrange(tc_ctx* ctx, tc_srs* srs) {
+  if (!ctx || !srs) return TC_ERR_ARGUMENT;
+  TC_CUDA(ctx, cudaSetDevice(srs->device));
+  return srs_derive_lagrange(ctx, srs);
+}
+
 int tc_srs_export(tc_ctx* ctx, const tc_srs* srs, int which, uint64_t offset, uint64_t count, uint8_t* out43) {
   if (!ctx || !srs || !out43) return TC_ERR_ARGUMENT;
-  const Aff* pts = (which == TC_SRS_LAGRANGE) ? srs->lagrange : srs->monomial;
+  const Aff* pts = (which == TC_SRS_LAGRANGE) ? srs->lagrange : (which == TC_SRS_SUBGRID) ? srs->sublag : srs->monomial;
   if (!pts) return fail(ctx, TC_ERR_VALUE, "srs has no elements of kind %d", which);
-  if (offset > srs->n || count > srs->n - offset) return fail(ctx, TC_ERR_INDEX, "srs export range out of bounds");
+  const uint64_t total = which == TC_SRS_SUBGRID ? srs->sublag_off[srs->m - 1] + srs->shape[srs->m - 1] : srs->n;
+  if (offset > total || count > total - offset)
+    return fail(ctx, TC_ERR_INDEX, "srs export range [%llu, +%llu) out of bounds (%llu elements of kind %d)",
+                (unsigned long long)offset, (unsigned long long)count, (unsigned long long)total, which);
   if (count == 0) return TC_OK;
   uint8_t* d_raw;
   TC_TRY(tcrt::scratch_t(ctx, "srs.raw", count * 43, &d_raw));
@@ -586,7 +624,8 @@ int tc_srs_export_axis(const tc_srs* srs, uint8_t* out43) {
 
 int tc_srs_has(const tc_srs* srs, int which) {
   if (!srs) return 0;
-  return which == TC_SRS_LAGRANGE ? srs->lagrange != nullptr : srs->monomial != nullptr;
+  return which == TC_SRS_LAGRANGE ? srs->lagrange != nullptr
+         : which == TC_SRS_SUBGRID ? srs->sublag != nullptr : srs->monomial != nullptr;
 }
 
 uint64_t tc_srs_size(const tc_srs* srs) { return srs ? srs->n : 0; }
@@ -603,6 +642,7 @@ int tc_srs_destroy(tc_srs* srs) {
     if (e) cudaFree(e);
   for (auto& kv : srs->wintab) cudaFree(kv.second);
   if (srs->exptab) cudaFree(srs->exptab);
+  for (auto* t : srs->retired) cudaFree(t);
   delete srs;
   return TC_OK;
 }
@@ -954,6 +994,9 @@ static int stream_prepare(tc_ctx* ctx, const tc_srs* srs, const void* const* h_c
       s = k;
   }
   if (s < 0) {
+    // h_cur is not a pending prefetch: any prefetched slot belongs to a stream of forwards
+    // that was abandoned (its buffers may be reused with other contents), drop both
+    ctx->slot[0].valid = ctx->slot[1].valid = false;
     s = 0;
     // slot 0 may still be read by earlier work on the ctx stream
     if (!ctx->slot[0].ready) TC_CUDA(ctx, cudaEventCreateWithFlags(&ctx->slot[0].ready, cudaEventDisableTiming));
@@ -976,6 +1019,12 @@ static int stream_prepare(tc_ctx* ctx, const tc_srs* srs, const void* const* h_c
   }
   ptrs.resize(count);
   for (int i = 0; i < count; i++) ptrs[i] = cur + (size_t)n * esz * i;
+  return TC_OK;
+}
+
+int tc_commit_stream_reset(tc_ctx* ctx) {
+  if (!ctx) return TC_ERR_ARGUMENT;
+  ctx->slot[0].valid = ctx->slot[1].valid = false;
   return TC_OK;
 }
 

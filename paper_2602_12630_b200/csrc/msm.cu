@@ -517,14 +517,16 @@ __device__ __forceinline__ uint32_t fp_key(const WinPlan& P, uint64_t mag, uint3
 // mode-3 bucket key straight from the fp16 bits: a normal value with exponent field e >=
 // 25 - scale_bits quantises exactly to (1024 + mantissa) 2^(e - 25 + scale_bits), so its key
 // is 1023 + mantissa and its table level e - 25 + scale_bits (the general path — RNE
-// rounding of small values, zeros, non-finite — through quant64 / fp_key otherwise).
+// rounding of small values, zeros, subnormals, non-finite — through quant64 / fp_key
+// otherwise).
 // Returns false for a zero (no entry).
 template <int DT>
 __device__ __forceinline__ bool key3(uint32_t raw, bool in, int scale_bits, const WinPlan& P, uint32_t& key,
                                      uint32_t& g, bool& neg) {
   if (DT == 1 && in) {
     const int e = (int)((raw >> 10) & 0x1fu);
-    if (e >= 25 - scale_bits && e != 0x1f) {
+    // e == 0 (zero / subnormal) never takes this path, whatever scale_bits admits
+    if (e != 0 && e >= 25 - scale_bits && e != 0x1f) {
       key = 1023u + (raw & 0x3ffu);
       g = (uint32_t)(e - 25 + scale_bits);
       neg = (raw >> 15) != 0;
@@ -1307,7 +1309,12 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
       fp_mb && n >= EXP_MIN_N &&
       groups <= MAXW && (uint64_t)groups * exp_srs->n < (1ull << 31)) {
     const EdPk* tab = nullptr;
-    if (srs_exp_table(ctx, exp_srs, d_bases, exp_srs->n, groups, &tab) == TC_OK) {
+    // fp16: ask for the depth ANY finite input needs (scale_bits + 6) so the table is built
+    // once instead of regrown batch by batch; the batch's own depth when that does not fit
+    const int full = dtype == TC_DTYPE_F16 ? scale_bits + 6 : 0;
+    const bool full_ok = full > groups && (uint64_t)full * exp_srs->n < (1ull << 31);
+    if ((full_ok && srs_exp_table(ctx, exp_srs, d_bases, exp_srs->n, full, &tab) == TC_OK) ||
+        srs_exp_table(ctx, exp_srs, d_bases, exp_srs->n, groups, &tab) == TC_OK) {
       P = plan_fpx(fp_mb, (uint32_t)exp_srs->n);
       bases = tab;   // multi-base batches (h_boff) index inside the table's level 0 as before
     }

@@ -190,19 +190,15 @@ int srs_exp_table(tc_ctx* ctx, tc_srs* srs, const EdPk* bases, uint64_t n, int d
   const uint64_t bytes = (uint64_t)depth * n * sizeof(EdPk);
   size_t fr = 0, tot = 0;
   cudaMemGetInfo(&fr, &tot);
-  const uint64_t have = srs->exptab ? (uint64_t)srs->exptab_depth * n * sizeof(EdPk) : 0;
-  if (bytes > cap || bytes > fr + have || fr + have - bytes < (8ull << 30)) return TC_ERR_MEMORY;
-  if (srs->exptab) {
-    TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    cudaFree(srs->exptab);
-    srs->exptab = nullptr;
-    srs->exptab_depth = 0;
-  }
+  if (bytes > cap || bytes > fr || fr - bytes < (8ull << 30)) return TC_ERR_MEMORY;
   EdPk* tab = nullptr;
   if (cudaMalloc(&tab, bytes) != cudaSuccess) {
     cudaGetLastError();
     return TC_ERR_MEMORY;
   }
+  // a shallower table may still be read by kernels other contexts (threads) launched with
+  // the pointer they got earlier: retire it, freed with the SRS (tc_srs_destroy)
+  if (srs->exptab) srs->retired.push_back(srs->exptab);
   TC_CUDA(ctx, cudaMemcpyAsync(tab, bases, n * sizeof(EdPk), cudaMemcpyDeviceToDevice, ctx->stream));
   for (int k = 1; k < depth; k++) {
     k_win_step<<<blocks_for((n + FB_K - 1) / FB_K, 128), 128, 0, ctx->stream>>>(tab + (uint64_t)(k - 1) * n, n, 1,

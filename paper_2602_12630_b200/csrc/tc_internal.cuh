@@ -82,6 +82,7 @@ struct tc_srs {
   // exptab[k n + i] = 2^k G_i, k < exptab_depth (built on first use, grown on demand)
   tc::EdPk* exptab = nullptr;
   int exptab_depth = 0;
+  std::vector<tc::EdPk*> retired;   // superseded (shallower) exponent tables, freed on destroy
   // guards the lazily built tables above when several contexts (threads) share the SRS
   std::mutex mu;
   uint64_t sublag_off[TC_MAX_AXES] = {0};
@@ -191,6 +192,10 @@ int srs_edwards(tc_ctx* ctx, tc_srs* srs, int which, const tc::EdPk** out);
 // L MSMs over a small SRS (n <= SMALL_MSM_MAX) with canonical F_p scalars, via per-point
 // byte-window tables built once per SRS (`which` = TC_SRS_MONOMIAL | TC_SRS_LAGRANGE)
 int small_msm_device(tc_ctx* ctx, tc_srs* srs, int which, const void* const* h_ptrs, int L, tc::Aff* d_out);
+
+// trapdoor-free Lagrange elements of `shape` from the Edwards monomial elements of the same
+// shape (derive.cu): canonical Montgomery-curve affine points into d_out (n of them)
+int derive_lagrange_device(tc_ctx* ctx, const tc::EdPk* d_mono, const uint32_t* shape, int m, tc::Aff* d_out);
 
 // fixed-base batch: out[i] = e_i * g for canonical F_p exponents e (device arrays)
 int fixed_base_g(tc_ctx* ctx, const tc::Fe* d_exps, uint64_t n, tc::Aff* d_out);

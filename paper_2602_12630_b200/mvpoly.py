@@ -95,8 +95,9 @@ def default_grid(dom, shape) -> Grid:
 
 
 def _require_device_domain(dom, grid):
-    p = getattr(dom, "p", P)
-    if p != P:
+    # dom None (the production field) or a prime-field domain of modulus p; anything else
+    # (e.g. the reference's FloatDomain, which has no .p) is rejected, never truncated
+    if dom is not None and getattr(dom, "p", None) != P:
         raise ValueError("device polynomial engine supports only the production scalar field")
     if grid is not None:
         for d, nodes in zip(grid.shape, grid.axes):

@@ -63,12 +63,18 @@ def _device_tree_ok(tensors, srs, node) -> bool:
 
 
 def prover_commit(tensors, srs_pool, *, tree_config: TreeConfig = None, scale_bits: int = SCALE_BITS,
-                  route: str = "auto", node_srs=None):
-    """Per-layer commitments C_l = tc_commit(srs[shape_l], quantize(T_l)) and a Terkle tree
-    over leaves hash_to_scalar(encode_elem(C_l), b"terkle/leaf").
+                  route: str = "auto", node_srs=None, return_tree: bool = False):
+    """prover_commit(tensors, srs) -> (per-layer commitments, Terkle root).
 
+    Per-layer commitments C_l = tc_commit(srs[shape_l], quantize(T_l)) and a Terkle tree
+    over leaves hash_to_scalar(encode_elem(C_l), b"terkle/leaf").
     srs_pool: an Srs (all layers share it) or a mapping shape -> Srs.
-    Returns (commitments, root, tree)."""
+    return_tree=True also returns the tree (for membership proofs): (commitments, root, tree)."""
+    out = _prover_commit(tensors, srs_pool, tree_config, scale_bits, route, node_srs)
+    return out if return_tree else out[:2]
+
+
+def _prover_commit(tensors, srs_pool, tree_config, scale_bits, route, node_srs):
     tensors = list(tensors)
     if not tensors:
         raise ValueError("no tensors to commit")
@@ -111,7 +117,7 @@ def prover_commit_pipeline(forwards, srs, *, tree_config: TreeConfig = None, nod
     if node.size > 64 or not node.has(_lib.SRS_LAGRANGE):
         for fwd in forwards:   # no device tree: the plain per-forward path
             yield prover_commit(list(fwd), srs, tree_config=cfg, scale_bits=scale_bits, route=route,
-                                node_srs=node_srs)
+                                node_srs=node_srs, return_tree=True)
         return
     ctxs = [_lib.Context.pipeline(srs.device, k) for k in range(max(1, depth))]
     pending = []
@@ -151,6 +157,17 @@ def prover_commit_stream(batches, srs, *, tree_config: TreeConfig = None, node_s
         cur = list(next(it))
     except StopIteration:
         return
+    try:
+        yield from _stream_forwards(it, cur, srs, cfg, node_srs, scale_bits, route)
+    finally:
+        # a consumer that stops early (or an error) leaves the last prefetch pending: drop
+        # it, so a later stream whose buffers reuse these host addresses uploads afresh
+        ctx = _lib.Context.get(srs.device)
+        with ctx.lock:
+            _lib.lib().tc_commit_stream_reset(ctx.handle)
+
+
+def _stream_forwards(it, cur, srs, cfg, node_srs, scale_bits, route):
     while cur is not None:
         try:
             nxt = list(next(it))

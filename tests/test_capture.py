@@ -33,7 +33,7 @@ def test_capture_then_prover_commit():
     x = torch.randn(8, 64, device="cuda", dtype=torch.float16)
     _, acts = tcb.infer_and_capture(m, x)
     srs, td = tcb.setup_srs((8, 8, 8), b"capture")
-    comms, root, tree = tcb.prover_commit(acts, srs)
+    comms, root, tree = tcb.prover_commit(acts, srs, return_tree=True)
     for a, c in zip(acts, comms):
         vals = O.quantize(a.float().cpu().numpy().astype(np.float64), 16)
         assert c.elem == O.commit_trapdoor(vals, (8, 8, 8), list(td.taus))

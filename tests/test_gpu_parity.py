@@ -264,7 +264,7 @@ def test_prover_commit_small_layers():
     srs, td = tcb.setup_srs(shape, b"layers")
     g = np.random.default_rng(5)
     tensors = [torch.from_numpy((g.standard_t(3, 512) * s).astype(np.float16)).cuda() for s in (0.5, 1.0, 4.0)]
-    comms, root, tree = tcb.prover_commit(tensors, srs)
+    comms, root, tree = tcb.prover_commit(tensors, srs, return_tree=True)
     for t, c in zip(tensors, comms):
         vals = O.quantize(t.cpu().numpy().astype(np.float64), 16)
         assert c.elem == O.commit_trapdoor(vals, shape, list(td.taus))
@@ -272,11 +272,11 @@ def test_prover_commit_small_layers():
     tree2, root2 = tcb.build(tcb.TreeConfig(), leaves)
     assert root2 == root
     # determinism and sensitivity
-    comms_b, root_b, _ = tcb.prover_commit(tensors, srs)
+    comms_b, root_b = tcb.prover_commit(tensors, srs)
     assert root_b == root
     t2 = tensors[1].clone()
     t2[17] += 1.0
-    _, root_c, _ = tcb.prover_commit([tensors[0], t2, tensors[2]], srs)
+    _, root_c = tcb.prover_commit([tensors[0], t2, tensors[2]], srs)
     assert root_c != root
 
 
@@ -293,7 +293,7 @@ def test_prover_commit_device_tree_matches_host_build(n_layers, node_shape):
     node = tcb.authtree.node_srs(cfg, device=0)
     g = np.random.default_rng(61)
     xs = [torch.from_numpy((g.standard_t(3, 512) * (0.5 + l % 4)).astype(np.float16)).cuda() for l in range(n_layers)]
-    comms, root, tree = tcb.prover_commit(xs, srs, tree_config=cfg, node_srs=node)
+    comms, root, tree = tcb.prover_commit(xs, srs, tree_config=cfg, node_srs=node, return_tree=True)
     comms_h = tcb.tc_commit_many(srs, xs)
     assert comms == comms_h
     leaves = [tcb.leaf_of(c) for c in comms_h]
@@ -362,7 +362,7 @@ def test_prover_commit_pipeline_matches_prover_commit(depth):
     g = np.random.default_rng(81)
     fwds = [[torch.from_numpy((g.standard_t(3, 65536) * (0.5 + (f + l) % 3)).astype(np.float16)).cuda()
              for l in range(5)] for f in range(5)]
-    want = [tcb.prover_commit(f, srs, tree_config=cfg, node_srs=node) for f in fwds]
+    want = [tcb.prover_commit(f, srs, tree_config=cfg, node_srs=node, return_tree=True) for f in fwds]
     got = list(tcb.prover_commit_pipeline(fwds, srs, tree_config=cfg, node_srs=node, depth=depth))
     assert len(got) == len(want)
     for (c1, r1, t1), (c2, r2, t2) in zip(got, want):
@@ -424,7 +424,7 @@ def test_commit_stream_prefetch_and_prover_stream():
     assert [c.elem for c in tcb.tc_commit_stream(srs, fwd[2])] == want[2]
     roots = [r for _, r, _ in tcb.prover_commit_stream(fwd, srs)]
     for f, r in zip(fwd, roots):
-        _, root, _ = tcb.prover_commit([t.cuda() for t in f], srs)
+        _, root = tcb.prover_commit([t.cuda() for t in f], srs)
         assert r == root
 
 
@@ -647,7 +647,7 @@ def test_config3_prover_commit_subset_and_tree():
     shape = (32, 32, 32, 64)
     srs, td = tcb.setup_srs(shape, b"tc-b200/config3")
     xs = [_config3_layer(l) for l in range(4)]
-    comms, root, tree = tcb.prover_commit([torch.from_numpy(x).cuda() for x in xs], srs)
+    comms, root, tree = tcb.prover_commit([torch.from_numpy(x).cuda() for x in xs], srs, return_tree=True)
     want = [O.commit_trapdoor(O.quantize(x.astype(np.float64), 16), shape, list(td.taus)) for x in xs]
     assert [c.elem for c in comms] == want
     node = tcb.authtree.node_srs(tcb.TreeConfig())

@@ -115,3 +115,16 @@ def test_limb_conversion_roundtrip():
     arr = _conv.ints_to_limbs_np(vals)
     assert arr.shape == (len(vals), 6) and arr.dtype == np.uint32
     assert _conv.limbs_to_ints(arr) == [v % O.P for v in vals]
+
+
+def test_device_engine_rejects_foreign_domains():
+    """mvpoly entry points accept dom None or a prime field of modulus p; a domain without
+    .p (e.g. the reference FloatDomain) or another modulus raises ValueError before any
+    device work (it used to be truncated with int())."""
+    import types
+
+    import paper_2602_12630_b200 as tcb
+    grid = tcb.default_grid(None, (2, 2))
+    for dom in (types.SimpleNamespace(zero=0.0, one=1.0), tcb.PrimeField(101)):
+        with pytest.raises(ValueError):
+            tcb.interpolate_lagrange(dom, [1, 2, 3, 4], grid)

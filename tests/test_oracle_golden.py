@@ -126,3 +126,23 @@ def test_terkle_oracle_structure():
     assert [len(lv) for lv in levels] == [8, 1]
     assert O.terkle_depth(1, 8) == 1 and O.terkle_depth(8, 8) == 1 and O.terkle_depth(9, 8) == 2
     assert O.terkle_child_point(5, (2, 2, 2)) == [2, 1, 2]
+
+
+@pytest.mark.parametrize("shape", [(4,), (3, 5), (8, 4, 2), (2, 3, 4, 5)])
+def test_barycentric_eval_small_matches(shape):
+    """The numpy limb contraction used for full-size configs equals barycentric_eval."""
+    import numpy as np
+    g = np.random.default_rng(len(shape))
+    n = int(np.prod(shape))
+    q = g.integers(-(1 << 29), 1 << 29, n)
+    pt = [int(g.integers(0, 1 << 62)) * (1 << 99) % O.P for _ in shape]
+    pt[0] = 2 if shape[0] >= 2 else pt[0]          # a grid node on the leading axis
+    assert O.barycentric_eval_small(q, shape, pt) == O.barycentric_eval([int(v) % O.P for v in q], shape, pt)
+    pt[0] = 123456789
+    assert O.barycentric_eval_small(q, shape, pt) == O.barycentric_eval([int(v) % O.P for v in q], shape, pt)
+
+
+def test_quantize_signed_matches():
+    import numpy as np
+    x = np.random.default_rng(0).standard_t(3, 4096).astype(np.float16)
+    assert [int(v) % O.P for v in O.quantize_signed(x, 16)] == O.quantize(x, 16)

@@ -17,7 +17,7 @@ cfg = bench.CONFIGS[3]
 layers = [torch.from_numpy(h).cuda() for h in bench.make_layers_host(cfg, range(32))]
 srs, _ = tcb.setup_srs(cfg["shape"], b"tc-b200/config3", device=0)
 if os.environ.get("TC_C4_COMMIT"):
-    comms, root, tree = tcb.prover_commit(layers, srs)
+    comms, root, tree = tcb.prover_commit(layers, srs, return_tree=True)
 score = np.random.default_rng(4).pareto(1.5, 32) + 1e-3
 picks = np.random.default_rng(5).choice(32, size=256, p=score / score.sum())
 rng = random.Random(6)
