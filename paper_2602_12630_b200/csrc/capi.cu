@@ -865,6 +865,105 @@ int tc_commit_tree_launch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_i
   return commit_tree_launch(ctx, srs, d_ins, count, dtype, scale_bits, route, node_srs);
 }
 
+// ---- multi-GPU building blocks (dist.py) ----------------------------------------------
+// Each rank commits its share of the (layer, element) space — whole layers, or a layer's
+// contiguous chunk given as a zero-masked copy (a Lagrange-route commitment is linear in
+// the samples, so a chunk's MSM is a partial sum of the layer's commitment) — into device
+// encodings; ONE all-gather exchanges them; every rank then sums the partials per layer
+// and hashes the tree on the device.
+int tc_commit_points_launch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype,
+                            int scale_bits, int route, uint8_t* d_out43) {
+  if (!ctx || !srs || (count > 0 && (!d_ins || !d_out43)) || count < 0) return TC_ERR_ARGUMENT;
+  if (count == 0) return TC_OK;
+  Aff* d_pts;
+  TC_TRY(tcrt::scratch_t(ctx, "dist.pts", (uint64_t)count, &d_pts));
+  TC_TRY(commit_many_dev(ctx, srs, d_ins, count, dtype, scale_bits, route, d_pts));
+  k_encode43<<<tcrt::blocks_for(count, 64), 64, 0, ctx->stream>>>(d_pts, count, d_out43);
+  TC_LAUNCHED(ctx);
+  return TC_OK;
+}
+
+// sum the partial points of each layer (CSR offsets `off`, n_layers + 1 entries)
+__global__ void k_combine_parts(const Aff* parts, const uint32_t* off, int n_layers, Aff* out) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= n_layers) return;
+  const uint32_t a = off[l], b = off[l + 1];
+  if (b - a == 1) {
+    out[l] = parts[a];
+    return;
+  }
+  Xyzz acc = xyzz_inf();
+  for (uint32_t k = a; k < b; k++) xyzz_add_aff(acc, parts[k]);
+  Aff r = xyzz_to_aff(acc);
+  if (!aff_is_inf(r)) r = Aff{Fq::canon(r.x), Fq::canon(r.y)};
+  out[l] = r;
+}
+
+int tc_tree_from_points_launch(tc_ctx* ctx, const tc_srs* node_srs, const uint8_t* d_parts43,
+                               const uint32_t* layer_of, uint64_t nparts, int n_layers) {
+  if (!ctx || !node_srs || !d_parts43 || nparts == 0 || n_layers <= 0) return TC_ERR_ARGUMENT;
+  if (ctx->res_pending) return fail(ctx, TC_ERR_VALUE, "commit_tree: previous launch not finished on this context");
+  const uint64_t B = node_srs->n;
+  if (B < 2 || !node_srs->lagrange || B > SMALL_MSM_MAX)
+    return fail(ctx, TC_ERR_VALUE, "device tree needs a Lagrange node SRS of 2..%llu points",
+                (unsigned long long)SMALL_MSM_MAX);
+  // CSR offsets of the parts per layer (parts of one layer must be adjacent, layers ascending)
+  std::vector<uint32_t> off(n_layers + 1, 0);
+  if (layer_of) {
+    if (nparts > (1ull << 20)) return fail(ctx, TC_ERR_VALUE, "too many parts");
+    for (uint64_t k = 0; k < nparts; k++) {
+      const uint32_t l = layer_of[k];
+      if (l >= (uint32_t)n_layers || (k && l < layer_of[k - 1]))
+        return fail(ctx, TC_ERR_VALUE, "parts must be grouped by ascending layer (< %d)", n_layers);
+      off[l + 1]++;
+    }
+    for (int l = 0; l < n_layers; l++) {
+      if (!off[l + 1]) return fail(ctx, TC_ERR_VALUE, "layer %d has no part", l);
+      off[l + 1] += off[l];
+    }
+  } else {
+    if (nparts != (uint64_t)n_layers) return fail(ctx, TC_ERR_VALUE, "one part per layer expected");
+    for (int l = 0; l <= n_layers; l++) off[l] = (uint32_t)l;
+  }
+  uint64_t L, cap, total_nodes, total_values;
+  terkle_geometry((uint64_t)n_layers, B, L, cap, total_nodes, total_values);
+  Aff *d_parts, *d_all;
+  Fe *d_vals, *d_levels;
+  uint32_t* d_off;
+  TC_TRY(tcrt::scratch_t(ctx, "dist.parts", nparts, &d_parts));
+  TC_TRY(tcrt::scratch_t(ctx, "dist.off", (uint64_t)n_layers + 1, &d_off));
+  TC_TRY(tcrt::scratch_t(ctx, "tree.pts", (uint64_t)n_layers + total_nodes, &d_all));
+  TC_TRY(tcrt::scratch_t(ctx, "tree.vals", cap, &d_vals));
+  TC_TRY(tcrt::scratch_t(ctx, "tree.levels", total_values, &d_levels));
+  if (sizeof(uint32_t) * off.size() > ctx->h_stage_bytes) return fail(ctx, TC_ERR_VALUE, "too many layers");
+  // the offsets ride in the pinned staging buffer: wait for the previous use of it first
+  TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  memcpy(ctx->h_stage, off.data(), sizeof(uint32_t) * off.size());
+  TC_CUDA(ctx, cudaMemcpyAsync(d_off, ctx->h_stage, sizeof(uint32_t) * off.size(), cudaMemcpyHostToDevice, ctx->stream));
+  TC_CUDA(ctx, cudaMemsetAsync(ctx->d_flags, 0, 4, ctx->stream));
+  k_decode43<<<tcrt::blocks_for(nparts, 64), 64, 0, ctx->stream>>>(d_parts43, nparts, d_parts, ctx->d_flags);
+  TC_LAUNCHED(ctx);
+  k_combine_parts<<<tcrt::blocks_for(n_layers, 32), 32, 0, ctx->stream>>>(d_parts, d_off, n_layers, d_all);
+  TC_LAUNCHED(ctx);
+  TC_TRY(tcrt::leaf_hash_device(ctx, d_all, n_layers, cap, d_vals));
+  TC_TRY(tcrt::terkle_device(ctx, const_cast<tc_srs*>(node_srs), d_vals, cap, (int)L, d_all + n_layers, d_levels));
+  const size_t pts_b = (size_t)(n_layers + total_nodes) * sizeof(Aff), vals_b = (size_t)total_values * sizeof(Fe);
+  if (ctx->h_res_bytes < pts_b + vals_b) {
+    if (ctx->h_res) cudaFreeHost(ctx->h_res);
+    ctx->h_res = nullptr;
+    ctx->h_res_bytes = 0;
+    TC_CUDA(ctx, cudaHostAlloc(&ctx->h_res, pts_b + vals_b, cudaHostAllocDefault));
+    ctx->h_res_bytes = pts_b + vals_b;
+  }
+  if (!ctx->res_ev) TC_CUDA(ctx, cudaEventCreateWithFlags(&ctx->res_ev, cudaEventDisableTiming));
+  TC_CUDA(ctx, cudaMemcpyAsync(ctx->h_res, d_all, pts_b, cudaMemcpyDeviceToHost, ctx->stream));
+  TC_CUDA(ctx, cudaMemcpyAsync((char*)ctx->h_res + pts_b, d_levels, vals_b, cudaMemcpyDeviceToHost, ctx->stream));
+  TC_CUDA(ctx, cudaEventRecord(ctx->res_ev, ctx->stream));
+  ctx->res_pending = true;
+  ctx->res_count = (uint64_t)n_layers, ctx->res_nodes = total_nodes, ctx->res_values = total_values;
+  return TC_OK;
+}
+
 static int commit_tree_impl(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype,
                             int scale_bits, int route, const tc_srs* node_srs, uint8_t* out_comms43,
                             uint8_t* out_nodes43, uint64_t* inout_node_count, uint8_t* out_values24,

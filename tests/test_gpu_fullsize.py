@@ -24,7 +24,9 @@ import pytest
 
 from oracle import tc_oracle as O
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu,
+              # the oracle pool forks a process whose CUDA / torch threads the children never use
+              pytest.mark.filterwarnings("ignore:This process .* is multi-threaded:DeprecationWarning")]
 
 torch = pytest.importorskip("torch")
 
