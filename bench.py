@@ -167,68 +167,137 @@ def forward_ms(device):
 
 
 # ------------------------------------------------------------------ CPU reference leg
-def _cpu_task(args):
-    """Reference CPU path on K elements: the Lagrange fibre transforms (mvpoly.py:193-228)
-    worth K elements of config-3 interpolation, then the naive MSM (fold of exp + mul,
-    backend.py:185-217) over K coefficients with the real SRS points."""
-    fibres, coeffs, bases = args
-    from oracle import tc_oracle as O
+def _ref_modules():
+    """(backend, field, mvpoly, kind): the unmodified reference copied into oracle/_ref by
+    oracle/make_ref.py ("reference"), else the oracle's restatement ("port")."""
+    from oracle import make_ref
+    mods = make_ref.load()
+    if mods is not None:
+        return mods + ("reference",)
+    return None, None, None, "port"
+
+
+_TASK = None   # per-process sample (fork-inherited)
+
+
+def _cpu_task(_=None):
+    """The reference CPU path on K elements of config-3 layer 0: its per-axis Lagrange fibre
+    transforms (mvpoly.py:193-230 `_lagrange_1d`, the kernel of interpolate_lagrange
+    233-247) over fibres worth K elements on every axis, then the commitment MSM over K
+    coefficients with K SRS points as the reference composes it (fold of
+    PairingBackend.exp + mul, backend.py:185-217).  Returns seconds."""
+    fns, fibres, coeffs, bases, backend = _TASK
     t0 = time.perf_counter()
-    for d, fib in fibres:
-        rows = O.lagrange_matrix(list(range(1, d + 1)))
-        out = [0] * d
-        for l, v in enumerate(fib):
-            if v:
-                r = rows[l]
-                for k in range(d):
-                    out[k] += v * r[k]
-    O.msm_naive(coeffs, bases)
+    for j, fib in fibres:
+        for f in fib:
+            fns[j](f)
+    if backend is not None:
+        acc = None
+        for a, b in zip(coeffs, bases):
+            acc = backend.mul(acc, backend.exp(b, a))
+    else:
+        from oracle import tc_oracle as O
+        O.msm_naive(coeffs, bases)
     return time.perf_counter() - t0
 
 
-def cpu_reference(shape, layer0_q, coeffs, bases, cores, target_s=12.0):
-    """Throughput (elems/s) of the reference CPU path on `cores` processes, sized to
-    ~target_s of wall time.  Returns (elems/s, wall seconds, tasks, K)."""
-    import multiprocessing as mp
-    K = len(coeffs)
-    fibres = []
-    for j, d in enumerate(shape):
-        stride = 1
-        for dd in shape[j + 1:]:
-            stride *= dd
-        for f in range(max(1, K // d)):
-            fibres.append((d, [layer0_q[(f * stride * d + r * stride) % len(layer0_q)] for r in range(d)]))
-    task = (fibres, coeffs, bases)
-    with mp.get_context("fork").Pool(cores) as pool:
-        one = max(pool.map(_cpu_task, [task] * cores))          # calibration round (untimed)
-        rounds = max(1, int(target_s / max(one, 1e-3)))
-        t0 = time.perf_counter()
-        pool.map(_cpu_task, [task] * (cores * rounds))
-        wall = time.perf_counter() - t0
-    n_tasks = cores * rounds
-    return K * n_tasks / wall, wall, n_tasks, K
-
-
-def cpu_sample_inputs(cfg, K=48):
-    """CPU-only inputs of the reference-path sample (one-time setup, not timed, no GPU, so
-    the reference arm runs on any host): layer 0's quantised values, K interpolation
+def cpu_sample(shape, K=48):
+    """Inputs of the bounded CPU sample (one-time setup, untimed, no GPU): layer 0's
+    quantised values cut into fibres of every axis worth K elements each, K interpolation
     coefficients (uniform F_p elements — what the 162-bit monomial coefficients of these
-    activations look like; the timing of exp / mul does not depend on which ones) and K
-    curve points g^k."""
+    activations look like; exp / mul time does not depend on which) and K curve points."""
     import random
 
     import numpy as np
 
     from oracle import tc_oracle as O
+    backend_m, field_m, mvpoly_m, kind = _ref_modules()
     x = make_layers_host(CONFIGS[3], [0])[0].reshape(-1)
     q = O.quantize(x.astype(np.float64), 16)
+    fibres, fns = [], []
+    for j, d in enumerate(shape):
+        stride = int(np.prod(shape[j + 1:]))
+        fib = [[q[(f * stride * d + r * stride) % len(q)] for r in range(d)] for f in range(max(1, K // d))]
+        fibres.append((j, fib))
+        if mvpoly_m is not None:
+            dom = field_m.PrimeField(backend_m.make_backend("production").order)
+            fns.append(mvpoly_m._lagrange_1d(dom, list(range(1, d + 1))))
+        else:
+            rows = O.lagrange_matrix(list(range(1, d + 1)))
+            fns.append(lambda fib, rows=rows, d=d: [sum(v * rows[l][k] for l, v in enumerate(fib)) % O.P
+                                                    for k in range(d)])
     rng = random.Random(2602)
     coeffs = [rng.randrange(O.P) for _ in range(K)]
     bases = [O.ec_mul(O.G, k + 2) for k in range(K)]
-    return q, coeffs, bases
+    backend = backend_m.make_backend("production") if backend_m is not None else None
+    return (fns, fibres, coeffs, bases, backend), K, kind
 
 
-# ------------------------------------------------------------------ main
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_reference(shape, cores, target_s=8.0, single_s=2.0):
+    """Throughput (elems/s) of the reference CPU path: one process (single-core figure) and
+    `cores` processes (all host cores), each sized to ~target_s of wall time."""
+    import multiprocessing as mp
+    global _TASK
+    _TASK, K, kind = cpu_sample(shape)
+    one = _cpu_task()                                       # calibration (untimed)
+    n1 = max(1, int(single_s / max(one, 1e-3)))
+    t0 = time.perf_counter()
+    for _ in range(n1):
+        _cpu_task()
+    single = K * n1 / (time.perf_counter() - t0)
+    with mp.get_context("fork").Pool(cores) as pool:
+        pool.map(_cpu_task, range(cores))                   # warm the workers (untimed)
+        rounds = max(1, int(target_s / max(one, 1e-3)))
+        t0 = time.perf_counter()
+        pool.map(_cpu_task, range(cores * rounds))
+        wall = time.perf_counter() - t0
+    n_tasks = cores * rounds
+    return {"value": K * n_tasks / wall, "single_core": single, "wall_s": wall, "tasks": n_tasks, "K": K,
+            "kind": kind}
+
+
+def _cpu_line(cpu, cores):
+    src = ("the unmodified reference modules (oracle/_ref, copied from the reference by oracle/make_ref.py): "
+           "mvpoly._lagrange_1d fibre transforms + PairingBackend.exp/mul fold" if cpu["kind"] == "reference" else
+           "the oracle's CPython restatement of the reference path (oracle/_ref absent)")
+    return {"value": cpu["value"], "unit": "elems/s", "cores": cores, "kind": cpu["kind"],
+            "single_core_value": cpu["single_core"], "cpu_model": cpu_model(),
+            "sample": f"{cpu['tasks']} tasks x {cpu['K']} elements of config-3 layer 0 on {cores} processes "
+                      f"({cpu['wall_s']:.1f} s): per-axis Lagrange fibre transforms worth those elements on every "
+                      f"axis + naive MSM over K coefficients; {src}; extrapolated linearly per element"}
+
+
+# ------------------------------------------------------------------ launch
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _reexec_torchrun(args):
+    """bench.py --gpus N outside torchrun: relaunch as N ranks (one process per GPU)."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # communicator lines (NVLink / NVLS) in stderr
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -242,189 +311,164 @@ def main():
     ap.add_argument("--no-monomial", action="store_true", help="skip the secondary monomial-route step")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_reexec_torchrun(args))
+
     import torch
     import torch.distributed as dist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    # TC_DIST_BACKEND=gloo lets several ranks share one GPU in tests (the gather is the only
-    # collective; the kernels never wait on another rank)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    # TC_DIST_BACKEND=gloo lets several ranks share one GPU in tests (the kernels of the ranks
+    # never wait on one another; the gather goes through host memory)
     backend = os.environ.get("TC_DIST_BACKEND", "nccl")
-    dev_index = local if backend == "nccl" else local % max(1, torch.cuda.device_count())
-    if world > 1:
-        torch.cuda.set_device(dev_index)
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
-        else:
-            dist.init_process_group(backend)
-    local = dev_index
-    dev = torch.device("cuda", local)
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     cfg = CONFIGS[5 if args.config == 5 else 3]
-    shape = cfg["shape"]
 
     if args.impl == "reference":
         if rank == 0:
             run_reference(args, cfg, cores, world)
+        return    # other ranks: no work (no process group needed)
+
+    dev_index = local if backend == "nccl" else local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev_index)
+    if world > 1:
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
+    dev = torch.device("cuda", dev_index)
+    try:
+        if args.config == 4:
+            run_openings(args, dev, rank, world, cores)
+        else:
+            run_commits(args, cfg, dev, rank, world, cores, backend)
+    finally:
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
-        return
 
-    if args.config == 4:
-        run_openings(args, dev, rank, world)
-        if world > 1:
-            dist.destroy_process_group()
-        return
+
+def _max_over_ranks(ms, world, dev, backend):
+    if world == 1:
+        return ms
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([ms], device=dev if backend == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_commits(args, cfg, dev, rank, world, cores, backend):
+    import torch
+    import torch.distributed as dist
 
     import paper_2602_12630_b200 as tcb
     from paper_2602_12630_b200 import _lib
-    from paper_2602_12630_b200.dist import allgather_commitments, layer_partition
+    from paper_2602_12630_b200.dist import prover_commit_pipeline_dist, work_partition
 
+    local = dev.index
     n_layers = cfg["layers"]
-    my_layers = layer_partition(n_layers, rank, world)
+    shape = cfg["shape"]
+    elems_per_layer = int(__import__("numpy").prod(cfg["act"]))
+    per_step_elems = n_layers * elems_per_layer
+    parts = work_partition(n_layers, elems_per_layer, world)[rank]
+    my_layers = sorted({l for l, _, _ in parts})
     if args.config == 5:
         dev_layers = make_layers_device(cfg, my_layers, dev)
         host_pinned = [d.cpu().pin_memory() for d in dev_layers]
     else:
         host_pinned = [torch.from_numpy(h).pin_memory() for h in make_layers_host(cfg, my_layers)]
         dev_layers = [h.to(dev) for h in host_pinned]
+    torch.cuda.synchronize(dev)
+    # ---- setup (trusted setup, tables): timed and declared, outside the measured steps
+    t0 = time.perf_counter()
     srs, _ = tcb.setup_srs(shape, b"tc-b200/config%d" % (5 if args.config == 5 else 3), device=local)
+    torch.cuda.synchronize(dev)
+    setup_ms = 1e3 * (time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    srs.prepare("float16")
+    torch.cuda.synchronize(dev)
+    exptab_ms = 1e3 * (time.perf_counter() - t0)
     tcfg = tcb.TreeConfig(shape=NODE_SHAPE)
     node_srs = tcb.authtree.node_srs(tcfg, device=local)
     ctx = _lib.Context.get(local)
-    elems_per_layer = 1
-    for d in cfg["act"]:
-        elems_per_layer *= d
-    per_step_elems = n_layers * elems_per_layer
-
-    def prove_step(layers, route=args.route):
-        if world == 1:
-            # protocol.prover_commit: device tensors take tc_commit_tree (commitments, leaf
-            # hashes and the tree in one device pass, one readback)
-            return tcb.prover_commit(layers, srs, tree_config=tcfg, node_srs=node_srs, route=route)[1]
-        comms = tcb.tc_commit_many(srs, layers, route=route)
-        encs = [c.to_bytes() for c in comms]
-        if world > 1:
-            encs = allgather_commitments(encs, n_layers, rank, world, device=dev if backend == "nccl" else None)
-        leaves = [tcb.hash_to_scalar(e, b"terkle/leaf") for e in encs]
-        tree, root = tcb.build(tcfg, leaves, srs=node_srs)
-        return root
-
-    def e2e_step():
-        # one-shot: host (pinned) activations straight into the public API
-        # (tc_commit_batch_host: upload, then commit)
-        return prove_step(host_pinned)
-
-    # a second pinned buffer set = "the next forward" for the streaming e2e
-    host_pinned2 = [h.clone().pin_memory() for h in host_pinned]
-
-    def e2e_stream(steps):
-        """`steps` forwards of pinned host activations through the public API; every
-        forward's bytes are copied inside the region.  protocol.prover_commit_pipeline (per
-        rank over its layers, then the commitment gather and the tree when N > 1); config 5
-        and TC_BENCH_NO_PIPELINE: protocol.prover_commit_stream / tc_commit_stream (forward
-        k+1's upload under forward k's commitments)."""
-        batches = [host_pinned if k % 2 == 0 else host_pinned2 for k in range(steps)]
-        root = None
-        if use_pipe and args.config != 5:
-            # host tensors through the forward pipeline: each context uploads its forward on
-            # its own copy stream while the other contexts' forwards compute
-            for _, root, _ in tcb.prover_commit_pipeline(batches, srs, tree_config=tcfg, node_srs=node_srs,
-                                                         route=args.route, depth=PIPE_DEPTH):
-                pass
-            return root
-        if use_pipe_dist and args.config != 5:
-            for comms, _, _ in tcb.prover_commit_pipeline(batches, srs, tree_config=tcfg, node_srs=node_srs,
-                                                          route=args.route, depth=PIPE_DEPTH):
-                encs = allgather_commitments([c.to_bytes() for c in comms], n_layers, rank, world,
-                                             device=dev if backend == "nccl" else None)
-                leaves = [tcb.hash_to_scalar(e, b"terkle/leaf") for e in encs]
-                root = tcb.build(tcfg, leaves, srs=node_srs)[1]
-            return root
-        if world == 1:
-            for _, root, _ in tcb.prover_commit_stream(batches, srs, tree_config=tcfg, node_srs=node_srs,
-                                                       route=args.route):
-                pass
-            return root
-        for k in range(steps):
-            comms = tcb.tc_commit_stream(srs, batches[k], batches[k + 1] if k + 1 < steps else None,
-                                         route=args.route)
-            encs = allgather_commitments([c.to_bytes() for c in comms], n_layers, rank, world,
-                                         device=dev if backend == "nccl" else None)
-            leaves = [tcb.hash_to_scalar(e, b"terkle/leaf") for e in encs]
-            root = tcb.build(tcfg, leaves, srs=node_srs)[1]
-        return root
-
-    # one rank: forwards go through protocol.prover_commit_pipeline (PIPE_DEPTH device
-    # contexts take them in turn; TC_BENCH_NO_PIPELINE=1: one prover_commit per forward)
-    use_pipe = world == 1 and not os.environ.get("TC_BENCH_NO_PIPELINE")
-    use_pipe_dist = world > 1 and not os.environ.get("TC_BENCH_NO_PIPELINE")
     PIPE_DEPTH = int(os.environ.get("TC_PIPE_DEPTH", "3"))
+    use_pipe = not os.environ.get("TC_BENCH_NO_PIPELINE")
+    dev_fwd = dict(zip(my_layers, dev_layers))
+    host_fwd = dict(zip(my_layers, host_pinned))
+    host_pinned2 = [h.clone().pin_memory() for h in host_pinned]   # "the next forward"
+    host_fwd2 = dict(zip(my_layers, host_pinned2))
+
+    def forwards(steps, host=False):
+        if host:
+            return [host_fwd if k % 2 == 0 else host_fwd2 for k in range(steps)]
+        return [dev_fwd] * steps
+
+    def run(steps, route=args.route, host=False):
+        """`steps` forwards; every forward's commitments, root and tree read back."""
+        root = None
+        if world > 1:
+            # per rank: its share of the (layer, element) space through the forward pipeline;
+            # part encodings all-gathered on the device (NCCL), tree built on every rank
+            for _, root, _ in prover_commit_pipeline_dist(forwards(steps, host), srs, n_layers, rank, world,
+                                                          tree_config=tcfg, node_srs=node_srs, route=route,
+                                                          depth=PIPE_DEPTH):
+                pass
+            return root
+        if host and args.config == 5:
+            # config 5: one context, forward k+1's upload under forward k's commitments
+            batches = [host_pinned if k % 2 == 0 else host_pinned2 for k in range(steps)]
+            for _, root, _ in tcb.prover_commit_stream(batches, srs, tree_config=tcfg, node_srs=node_srs,
+                                                       route=route):
+                pass
+            return root
+        if use_pipe:
+            fw = [[f[l] for l in my_layers] for f in forwards(steps, host)]
+            for _, root, _ in tcb.prover_commit_pipeline(fw, srs, tree_config=tcfg, node_srs=node_srs, route=route,
+                                                         depth=PIPE_DEPTH):
+                pass
+            return root
+        for f in forwards(steps, host):
+            root = tcb.prover_commit([f[l] for l in my_layers], srs, tree_config=tcfg, node_srs=node_srs,
+                                     route=route)[1]
+        return root
 
     def all_launches():
         return ctx.launches + sum(c.launches for c in _lib.Context._pipeline.values())
 
-    def value_run(steps, route=args.route):
-        root = None
-        if use_pipe:
-            for _, root, _ in tcb.prover_commit_pipeline([dev_layers] * steps, srs, tree_config=tcfg,
-                                                         node_srs=node_srs, route=route, depth=PIPE_DEPTH):
-                pass
-            return root
-        if use_pipe_dist:
-            # several ranks: each pipelines its own layers' commitments (the local tree of its
-            # layers is not used); per forward, the commitment gather and the global tree run
-            # on the host while the next forwards compute
-            for comms, _, _ in tcb.prover_commit_pipeline([dev_layers] * steps, srs, tree_config=tcfg,
-                                                          node_srs=node_srs, route=route, depth=PIPE_DEPTH):
-                encs = allgather_commitments([c.to_bytes() for c in comms], n_layers, rank, world,
-                                             device=dev if backend == "nccl" else None)
-                leaves = [tcb.hash_to_scalar(e, b"terkle/leaf") for e in encs]
-                root = tcb.build(tcfg, leaves, srs=node_srs)[1]
-            return root
-        for _ in range(steps):
-            root = prove_step(dev_layers, route=route)
-        return root
-
-    def timed(fn, steps):
+    def timed(fn):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         l0 = all_launches()
         e0.record()
-        for _ in range(steps):
-            root = fn()
+        root = fn()
         e1.record()
         torch.cuda.synchronize(dev)
-        if world > 1:
-            dist.barrier()
-        ms = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([ms], device=dev if backend == "nccl" else "cpu")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
+        ms = _max_over_ranks(e0.elapsed_time(e1), world, dev, backend)
         return ms, all_launches() - l0, root
 
-    value_run(max(args.warmup, PIPE_DEPTH if (use_pipe or use_pipe_dist) else 0))   # every pipeline context warmed
+    run(max(args.warmup, PIPE_DEPTH))                     # warm every pipeline context
     with Clocks(local) as clk:
-        ms, launches, root = timed(lambda: value_run(args.steps), 1)
-    for _ in range(args.warmup):
-        e2e_step()
-    ms_e2e, _, root_e2e = timed(e2e_step, args.steps)
+        ms, launches, root = timed(lambda: run(args.steps))
+    run(max(2, min(args.warmup, PIPE_DEPTH)), host=True)
+    ms_e2e, _, root_e2e = timed(lambda: run(args.steps, host=True))
     if root_e2e != root:
         raise RuntimeError("e2e root differs from the device-resident root")
-    ms_stream = None
-    e2e_stream(max(2, PIPE_DEPTH if (use_pipe or use_pipe_dist) else 0))
-    ms_stream, _, root_s = timed(lambda: e2e_stream(args.steps), 1)
-    if root_s != root:
-        raise RuntimeError("streaming e2e root differs from the device-resident root")
+    # latency of ONE forward (nothing else in flight): the lone prover_commit
+    lat = []
+    for _ in range(3):
+        lat.append(timed(lambda: run(1))[0])
+    latency_ms = min(lat)
 
     # dominant kernel: Pippenger bucket accumulation, CUDA events on the ctx stream
     ctx.set_profiling(True)
-    prove_step(dev_layers)
+    tcb.prover_commit([dev_fwd[l] for l in my_layers], srs, tree_config=tcfg, node_srs=node_srs)
     st = ctx.kernel_stats("msm.accumulate")
     ctx.set_profiling(False)
     import ctypes
@@ -432,22 +476,32 @@ def main():
     ctx.check(_lib.lib().tc_measure_imad_peak(ctx.handle, ctypes.byref(peak)))
     peak_tops = peak.value
 
+    # trapdoor-free setup path: Lagrange elements derived from a monomial-only SRS
+    derive_ms = None
+    if rank == 0:
+        mono_srs, _ = tcb.setup_srs(shape, b"tc-b200/derive", lagrange=False, device=local)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        mono_srs.derive_lagrange()
+        torch.cuda.synchronize(dev)
+        derive_ms = 1e3 * (time.perf_counter() - t0)
+        del mono_srs
+
     # secondary: the monomial route (interpolate -> 162-bit-scalar MSM, SPEC.md:279 verbatim)
     mono = None
-    if not args.no_monomial and args.route == "lagrange" and args.config == 3:
-        prove_step(dev_layers, route="monomial")
-        m_ms, _, m_root = timed(lambda: prove_step(dev_layers, route="monomial"), 1)
+    if not args.no_monomial and args.route == "lagrange" and args.config == 3 and world == 1:
+        run(1, route="monomial")
+        m_ms, _, m_root = timed(lambda: run(1, route="monomial"))
         if m_root != root:
             raise RuntimeError("monomial route root differs from the Lagrange route")
         mono = {"ms_per_step": m_ms, "elems_per_s": per_step_elems / (m_ms / 1e3), "root_equal": True}
 
     ms_step = ms / args.steps
     value = per_step_elems / (ms_step / 1e3)
-    value_e2e = per_step_elems / (ms_e2e / args.steps / 1e3)
     achieved = st["units"] * WORD_MULS_PER_ADD / (st["ms"] * 1e-3) / 1e12 if st["ms"] else None
     traffic = None   # dram bytes per launch of k_accum_aff from the committed ncu --set full capture
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_accum_summary.txt")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r02_ncu_accum_summary.txt")) as fh:
             kv = dict(l.split(" = ", 1) for l in fh if " = " in l)
         to_b = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         traffic = sum(float(kv[k].split()[0]) * to_b[kv[k].split()[1]]
@@ -458,148 +512,170 @@ def main():
     fwd = None if (args.no_forward or rank != 0 or args.config != 3) else forward_ms(dev)
     cpu = None
     if rank == 0 and not args.no_cpu:
-        q, coeffs, bases = cpu_sample_inputs(cfg)
-        v, wall, ntask, K = cpu_reference(CONFIGS[3]["shape"], q, coeffs, bases, cores)
-        cpu = {"value": v, "unit": "elems/s", "cores": cores, "kind": "port",
-               "sample": f"{ntask} tasks x {K} elements of config-3 layer 0 on {cores} processes ({wall:.1f} s): "
-                         f"Lagrange fibre transforms worth those elements + naive exp/mul MSM over their "
-                         f"coefficients (oracle restatement of the reference CPython path)"}
-
-    e2e_serial = {"value": value_e2e, "unit": "elems/s", "ms_per_step": ms_e2e / args.steps,
-                  "h2d_bytes_per_step": per_step_elems // world * 2,
-                  # commitments + node points (48-B affine) and, on the device-tree path, every
-                  # tree level's child values (24-B limbs): 32 leaves, arity 8 -> 9 nodes, 72 values
-                  "d2h_bytes_per_step": (len(my_layers) + 9) * 48 + (72 * 24 if world == 1 else 0),
-                  "path": "protocol-level tc_commit_many on pinned host tensors -> tc_commit_batch_host "
-                          "(upload then commit, no overlap) + Terkle build, per step"}
-    if ms_stream is not None:
-        e2e = dict(e2e_serial, value=per_step_elems / (ms_stream / args.steps / 1e3),
-                   ms_per_step=ms_stream / args.steps,
-                   path=(f"{args.steps} forwards of pinned host tensors through protocol.prover_commit_pipeline "
-                         f"({PIPE_DEPTH} device contexts in turn: each uploads its forward on its own copy stream "
-                         "and commits it while the others' forwards compute; first upload exposed) + device leaf "
-                         "hashing and Terkle tree + commitments / tree read back, per forward (N > 1: per "
-                         "rank over its layers, then the commitment gather and the Terkle build)"
-                         if (use_pipe or use_pipe_dist) and args.config != 5 else
-                         f"{args.steps} forwards of pinned host tensors through the streaming API "
-                         "(protocol.prover_commit_stream / tc_commit_stream per rank: forward k+1's upload "
-                         "overlaps forward k's commit; first upload exposed) + commitment gather (N > 1) + "
-                         "Terkle build + commitments/root read back, per step"),
-                   serial=e2e_serial)
-    else:
-        e2e = e2e_serial
+        cpu = _cpu_line(cpu_reference(CONFIGS[3]["shape"], cores), cores)
+    h2d = sum(t.numel() * t.element_size() for t in host_pinned)
+    tree_d2h = (n_layers + 9) * 48 + 72 * 24     # commitments + node points (48-B affine), level values
+    e2e = {"value": per_step_elems / (ms_e2e / args.steps / 1e3), "unit": "elems/s",
+           "ms_per_step": ms_e2e / args.steps, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": tree_d2h,
+           "path": (f"{args.steps} forwards of pinned host tensors through the public API: "
+                    + ("dist.prover_commit_pipeline_dist per rank (its share uploaded on a pipeline context's "
+                       "stream, committed, part encodings all-gathered on the device, tree on every rank)"
+                       if world > 1 else
+                       "protocol.prover_commit_stream (one context; forward k+1's upload under forward k's "
+                       "commitments)" if args.config == 5 else
+                       f"protocol.prover_commit_pipeline ({PIPE_DEPTH} device contexts in turn: each uploads its "
+                       "forward on its own copy stream and commits it while the others' forwards compute)")
+                    + "; commitments, root and tree read back every forward; first upload exposed")}
+    tables = srs.table_bytes()
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "elems/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32 (6-limb F_p/F_q Montgomery); input fp16", "data": "synthetic",
             "config": {"workload": cfg["name"], "route": args.route, "elems_per_step": per_step_elems,
-                       "parallelism": f"layers/{world}", "l2": "no flush: fp16 inputs (>=128 MiB) + SRS (96 MiB) "
-                       "exceed the 126 MB L2", "srs": "generated once before timing (trusted setup)",
-                       "step_api": (f"protocol.prover_commit_pipeline over the {args.steps} timed forwards "
+                       "parallelism": f"layers/{world}" if all(c == elems_per_layer for _, _, c in parts)
+                       else f"layer-chunks/{world}",
+                       "l2": "no flush: fp16 inputs (>=128 MiB) + SRS (>=96 MiB) exceed the 126 MB L2",
+                       "srs": "generated once before timing (trusted setup)",
+                       "setup_ms": setup_ms, "exptab_build_ms": exptab_ms,
+                       "lagrange_derive_ms": derive_ms, **tables,
+                       "step_api": ("dist.prover_commit_pipeline_dist" if world > 1 else
+                                    f"protocol.prover_commit_pipeline over the {args.steps} timed forwards "
                                     f"({PIPE_DEPTH} contexts; every forward's commitments, root and tree read back)"
-                                    if use_pipe else
-                                    f"per rank: protocol.prover_commit_pipeline over its layers ({PIPE_DEPTH} contexts), "
-                                    "then per forward the commitment all-gather and the Terkle build" if use_pipe_dist
-                                    else "protocol.prover_commit per forward")},
+                                    if use_pipe else "protocol.prover_commit per forward")},
+            "latency_ms": latency_ms,
             "overhead_pct": (100.0 * ms_step / fwd) if fwd else None,
-            "forward_ms": fwd,
+            "overhead_pct_ideal": 100.0 * ms_step / IDEAL_FORWARD_MS if args.config == 3 else None,
+            "latency_overhead_pct_ideal": 100.0 * latency_ms / IDEAL_FORWARD_MS if args.config == 3 else None,
+            "forward_ms": fwd, "forward_ms_ideal": IDEAL_FORWARD_MS,
             "e2e": e2e,
             "gpu_launches": launches,
             "roofline": {"bound": "int", "kernel": "k_accum_aff (Pippenger bucket accumulation)",
                          "achieved": achieved, "peak": peak_tops, "unit": "T word-mul/s",
                          "frac": (achieved / peak_tops) if achieved and peak_tops else None, "traffic": traffic,
-                         "traffic_note": "dram read+write bytes per launch of the same kernel on the same workload, "
-                                         "profiles/r01_ncu_accum_summary.txt (random gathers of 64-B packed Edwards "
-                                         "(x, y, xy) points 2^g G_i from the exponent table, L2 hit ~30 %: the kernel is "
-                                         "fma-heavy-pipe bound, not DRAM bound)",
-                         "hw_pipe": "fma-heavy pipe ~84 % busy (ncu sm__pipe_fmaheavy_cycles_active)",
+                         "traffic_note": "dram read+write bytes per launch of the same kernel on the same workload "
+                                         "(profiles/r02_ncu_accum_summary.txt)",
                          "work": f"{st['units']:.0f} bucket entries x {WORD_MULS_PER_ADD} word-muls "
                                  f"(11 mulmods x 78) over {st['launches']} launches, {st['ms']:.3f} ms",
+                         "work_note": "counted per EXECUTED bucket add (one per element on the Lagrange route: the "
+                                      "exponent table 2^g G_i, built at setup, absorbs the scalar's exponent)",
                          "peak_source": "mad.lo.u32 microbenchmark in this run (tc_measure_imad_peak)",
                          "share_of_step": st["ms"] / ms_step if ms_step else None},
             "monomial_route": mono,
             "cpu_baseline": cpu,
+            "route_matched": ({"monomial_route_vs_cpu": mono["elems_per_s"] / cpu["value"],
+                               "lagrange_route_vs_cpu": value / cpu["value"],
+                               "note": "the CPU arm runs the reference's monomial path (interpolate + 162-bit MSM); "
+                                       "the GPU monomial route is the same algorithm"}
+                              if mono and cpu else None),
             "clocks": clk.summary(),
             "root": root.to_bytes().hex(),
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+
+
+IDEAL_FORWARD_MS = 4.87   # LLaMA-2-7B [1,512] forward: 6.83 TFLOP at the measured 1403.6 TFLOP/s
 
 
 def run_reference(args, cfg, cores, world):
-    q, coeffs, bases = cpu_sample_inputs(cfg)
-    for _ in range(max(0, min(args.warmup, 1))):
-        cpu_reference(CONFIGS[3]["shape"], q, coeffs, bases, cores, target_s=2.0)
-    vals, walls, tasks = [], [], 0
-    for _ in range(args.steps):
-        v, w, nt, K = cpu_reference(CONFIGS[3]["shape"], q, coeffs, bases, cores, target_s=6.0)
-        vals.append(v)
-        walls.append(w)
-        tasks += nt
-    value = tasks * len(coeffs) / sum(walls)
-    sample = (f"{tasks} tasks x {len(coeffs)} elements of config-3 layer 0 on {cores} processes: Lagrange fibre "
-              f"transforms worth those elements + naive exp/mul MSM over their coefficients (oracle restatement "
-              f"of the reference CPython path)")
+    """The reference arm: the reference's own CPU path (oracle/_ref) on all host cores, each
+    step a bounded sample of the workload."""
+    global _TASK
+    _TASK, K, kind = cpu_sample(CONFIGS[3]["shape"])
+    import multiprocessing as mp
+    one = _cpu_task()
+    rounds = max(1, int(6.0 / max(one, 1e-3)))
+    walls, tasks = [], 0
+    with mp.get_context("fork").Pool(cores) as pool:
+        for _ in range(max(1, args.warmup)):
+            pool.map(_cpu_task, range(cores))
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            pool.map(_cpu_task, range(cores * rounds))
+            walls.append(time.perf_counter() - t0)
+            tasks += cores * rounds
+    value = tasks * K / sum(walls)
+    cpu = _cpu_line({"value": value, "single_core": None, "wall_s": sum(walls), "tasks": tasks, "K": K, "kind": kind},
+                    cores)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "elems/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(walls),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int (CPython big int)",
             "data": "synthetic", "config": {"workload": cfg["name"], "parallelism": f"cpu x{cores}"},
-            "cpu_baseline": {"value": value, "unit": "elems/s", "cores": cores, "kind": "port", "sample": sample},
+            "cpu_baseline": cpu,
             "e2e": {"value": value, "unit": "elems/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def run_openings(args, dev, rank, world):
-    """Config 4: batched opening proofs on the config-3 tree — 256 seeded challenges spread
-    over layers by a heavy-tailed score vector; each is tc_open (quotients + MSM) plus a
-    Terkle membership proof.  Reports openings/s (correctness: tests/test_gpu_parity.py)."""
+def config4_challenges(n_layers, shape, P):
+    """256 seeded challenges spread over layers by a heavy-tailed (Pareto) score vector."""
     import random
 
     import numpy as np
+    score = np.random.default_rng(4).pareto(1.5, n_layers) + 1e-3
+    picks = np.random.default_rng(5).choice(n_layers, size=256, p=score / score.sum())
+    rng = random.Random(6)
+    return [(int(l), [rng.randrange(P) for _ in shape]) for l in picks]
+
+
+def run_openings(args, dev, rank, world, cores):
+    """Config 4: batched opening proofs on the config-3 tree — 256 seeded challenges spread
+    over layers by a heavy-tailed score vector; each is tc_open (quotients + MSM) plus a
+    Terkle membership proof.  N > 1: the challenges split over the ranks by cost
+    (dist.open_many_dist), every proof gathered to every rank.  Reports openings/s
+    (correctness: tests/test_gpu_fullsize.py checks every opening with the oracle verifier)."""
     import torch
+    import torch.distributed as dist
 
     import paper_2602_12630_b200 as tcb
+    from paper_2602_12630_b200.dist import open_many_dist, opening_partition, prover_commit_dist
     cfg = CONFIGS[3]
-    layers_host = make_layers_host(cfg, range(cfg["layers"]))
-    layers = [torch.from_numpy(h).to(dev) for h in layers_host]
+    n_layers = cfg["layers"]
+    chals = config4_challenges(n_layers, cfg["shape"], tcb.P)
+    mine = opening_partition([l for l, _ in chals], world)[rank]
+    need = sorted({chals[i][0] for i in mine} | {l for l in range(n_layers) if l % world == rank})
+    host = dict(zip(need, make_layers_host(cfg, need)))
+    layers = {l: torch.from_numpy(h).to(dev) for l, h in host.items()}
     srs, _ = tcb.setup_srs(cfg["shape"], b"tc-b200/config3", device=dev.index)
-    comms, root, tree = tcb.prover_commit(layers, srs, return_tree=True)
-    score = np.random.default_rng(4).pareto(1.5, cfg["layers"]) + 1e-3
-    picks = np.random.default_rng(5).choice(cfg["layers"], size=256, p=score / score.sum())
-    rng = random.Random(6)
-    chals = [(int(l), [rng.randrange(tcb.P) for _ in cfg["shape"]]) for l in picks]
-    # warm-up: the whole workload once (window tables, slice-commitment and table-kernel
-    # paths, lazily loaded kernels), membership proofs on a separate tree so the timed run
-    # starts with no memoised node openings
-    for _ in range(max(1, args.warmup)):
-        tcb.tc_open_many(srs, [layers[l] for l, _ in chals], [pt for _, pt in chals])
-        warm_tree, _ = tcb.build(tree.config, tree.values[0][:tree.n], srs=tree.srs)
-        tcb.prove_many(warm_tree, [l for l, _ in chals])
-    tree, _ = tcb.build(tree.config, tree.values[0][:tree.n], srs=tree.srs)
+    srs.prepare("float16")
+    if world > 1:
+        comms, root, tree = prover_commit_dist(layers, srs, n_layers, rank, world)
+    else:
+        comms, root, tree = tcb.prover_commit([layers[l] for l in range(n_layers)], srs, return_tree=True)
+
+    def step(tr):
+        return open_many_dist(srs, layers, chals, rank, world, tree=tr)
+
+    for _ in range(max(1, args.warmup)):       # window tables, slice / table-kernel paths
+        step(tcb.build(tree.config, tree.values[0][:tree.n], srs=tree.srs)[0])
+    fresh = tcb.build(tree.config, tree.values[0][:tree.n], srs=tree.srs)[0]   # no memoised node openings
+    if world > 1:
+        dist.barrier()
     torch.cuda.synchronize(dev)
-    t0 = time.perf_counter()
-    ops = tcb.tc_open_many(srs, [layers[l] for l, _ in chals], [pt for _, pt in chals])
-    t_open = time.perf_counter() - t0
-    proofs = tcb.prove_many(tree, [l for l, _ in chals])   # node openings batched (tc_open_many)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    ops, proofs = step(fresh)
+    e1.record()
     torch.cuda.synchronize(dev)
-    wall = time.perf_counter() - t0
-    # spot-check: the batched openings verify on the CPU verifier, membership proofs too
+    ms = _max_over_ranks(e0.elapsed_time(e1), world, dev, os.environ.get("TC_DIST_BACKEND", "nccl"))
+    # spot-check: openings verify on the CPU verifier, membership proofs too (the full check
+    # of all 256 with the oracle verifier is tests/test_gpu_fullsize.py)
     for k in (0, len(chals) // 2, len(chals) - 1):
         l, pt = chals[k]
         if not tcb.tc_verify(srs, comms[l], pt, ops[k]):
             raise RuntimeError("config-4 opening does not verify")
         if not tcb.verify(root, l, tcb.authtree.leaf_of(comms[l]), proofs[k], tree.config):
             raise RuntimeError("config-4 membership proof does not verify")
-    print(json.dumps({"metric": "opening proofs/sec (tc_open + Terkle membership proof)", "value": len(chals) / wall,
-                      "unit": "openings/s", "n_gpus": 1, "ms_per_opening": 1e3 * wall / len(chals),
-                      "ms_openings": 1e3 * t_open, "ms_membership_proofs": 1e3 * (wall - t_open),
-                      "config": {"workload": "config4: 256 challenges on the config-3 tree, layers drawn by a seeded "
-                                 "Pareto score vector, random field points",
-                                 "path": "tc_open_many (layers opened >= 6 times: slice commitments H[c',c] once per layer, pi_0 as a d0^2-point MSM; others: quotients of 8 openings -> one batched MSM per axis) + "
-                                         "prove() per challenge (node openings memoised per tree)"}}), flush=True)
+    if rank == 0:
+        print(json.dumps({"metric": "opening proofs/sec (tc_open + Terkle membership proof)",
+                          "value": len(chals) / (ms / 1e3), "unit": "openings/s", "n_gpus": world,
+                          "ms_per_opening": ms / len(chals), "ms_total": ms, "higher_is_better": True,
+                          "config": {"workload": "config4: 256 challenges on the config-3 tree, layers drawn by a "
+                                                 "seeded Pareto score vector, random field points",
+                                     "parallelism": f"openings/{world} (cost-balanced, hot layers split)",
+                                     "path": "dist.open_many_dist -> tc_open_many (layers opened >= 6 times: slice "
+                                             "commitments H[c',c] once per layer and rank, pi_0 as a d0^2-point MSM; "
+                                             "others: grouped quotient MSMs) + prove_many (node openings batched)"}}),
+              flush=True)
 
 
 if __name__ == "__main__":

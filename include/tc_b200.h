@@ -113,6 +113,14 @@ int tc_srs_export(tc_ctx* ctx, const tc_srs* srs, int which, uint64_t offset, ui
                   uint8_t* out43);
 int tc_srs_export_axis(const tc_srs* srs, uint8_t* out43);
 int tc_srs_has(const tc_srs* srs, int which);
+/* Build the lazily built tables of an SRS up front (setup, not per commit): for fp16 inputs
+ * at scale_bits, the exponent table 2^g G_i of the Lagrange basis (g < scale_bits + 6) the
+ * fp16 commit plan reads; a no-op for other dtypes or when it does not fit in memory. */
+int tc_srs_prepare(tc_ctx* ctx, tc_srs* srs, int dtype, int scale_bits);
+/* device bytes held by the SRS: exponent table, fixed-base window tables, and the bases
+ * (affine + Edwards copies of the monomial, Lagrange and sub-grid elements) */
+int tc_srs_table_bytes(const tc_srs* srs, uint64_t* exptab_bytes, uint64_t* wintab_bytes,
+                       uint64_t* basis_bytes);
 uint64_t tc_srs_size(const tc_srs* srs);
 int tc_srs_destroy(tc_srs* srs);
 
@@ -208,6 +216,21 @@ int tc_commit_stream_tree(tc_ctx* ctx, const tc_srs* srs, const void* const* h_c
                           const tc_srs* node_srs, uint8_t* out_comms43, uint8_t* out_nodes43,
                           uint64_t* inout_node_count, uint8_t* out_values24,
                           uint64_t* inout_value_count);
+
+/* ---- multi-GPU building blocks (dist.py) ------------------------------------
+ * tc_commit_points_launch: commit `count` device tensors (whole layers, or a layer's chunk
+ * as a zero-masked copy: a Lagrange-route commitment is linear in the samples, so a chunk's
+ * MSM is a partial sum of the layer's commitment) and write their 43-byte encodings into
+ * the DEVICE buffer d_out43 — stream-ordered, nothing read back.  Every rank's encodings
+ * are then exchanged with one all-gather (NCCL over NVLink), and
+ * tc_tree_from_points_launch sums the gathered parts per layer (layer_of: host array, the
+ * layer of each part, grouped by ascending layer; NULL = one part per layer), hashes the
+ * leaves and builds the Terkle tree on the device; tc_commit_tree_finish collects the
+ * per-layer commitments, node points and level values as for tc_commit_tree_launch. */
+int tc_commit_points_launch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count,
+                            int dtype, int scale_bits, int route, uint8_t* d_out43);
+int tc_tree_from_points_launch(tc_ctx* ctx, const tc_srs* node_srs, const uint8_t* d_parts43,
+                               const uint32_t* layer_of, uint64_t nparts, int n_layers);
 
 /* ---- Terkle build ------------------------------------
  * leaves: n x 21 B field elements.  Pads with zeros to B^L (B = node SRS size,

@@ -60,6 +60,8 @@ _SIGS = [
     ("tc_srs_export_axis", C.c_int, [_P, _P]),
     ("tc_srs_has", C.c_int, [_P, C.c_int]),
     ("tc_srs_size", C.c_uint64, [_P]),
+    ("tc_srs_prepare", C.c_int, [_P, _P, C.c_int, C.c_int]),
+    ("tc_srs_table_bytes", C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     ("tc_srs_destroy", C.c_int, [_P]),
     ("tc_quantize", C.c_int, [_P, _P, C.c_int, C.c_uint64, C.c_int, _P]),
     ("tc_interpolate", C.c_int, [_P, _P, _U32P, C.c_int]),
@@ -81,6 +83,8 @@ _SIGS = [
     ("tc_commit_tree_finish", C.c_int, [_P, _P, _P, C.POINTER(C.c_uint64), _P, C.POINTER(C.c_uint64)]),
     ("tc_commit_stream_tree", C.c_int, [_P, _P, C.POINTER(_P), C.POINTER(_P), C.c_int, C.c_int, C.c_int, C.c_int,
                                         _P, _P, _P, C.POINTER(C.c_uint64), _P, C.POINTER(C.c_uint64)]),
+    ("tc_commit_points_launch", C.c_int, [_P, _P, C.POINTER(_P), C.c_int, C.c_int, C.c_int, C.c_int, _P]),
+    ("tc_tree_from_points_launch", C.c_int, [_P, _P, _P, _P, C.c_uint64, C.c_int]),
     ("tc_pairing", C.c_int, [C.c_char_p, C.c_char_p, _P]),
     ("tc_verify_host", C.c_int, [C.c_int, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(C.c_int)]),
     ("tc_host_hash_to_scalar", C.c_int, [C.c_char_p, C.c_uint32, C.c_char_p, C.c_uint32, _P]),

@@ -132,6 +132,22 @@ class Srs:
     def lagrange_elems(self):
         return self._export(_lib.SRS_LAGRANGE)
 
+    def prepare(self, dtype="float16", scale_bits: int = SCALE_BITS) -> "Srs":
+        """Build the tables commits of `dtype` inputs read (fp16: the exponent table of the
+        Lagrange basis) now instead of on the first commit.  Returns self."""
+        code = {"float16": _lib.DTYPE_F16, "bfloat16": _lib.DTYPE_BF16, "float32": _lib.DTYPE_F32}.get(str(dtype).replace("torch.", ""), 0)
+        ctx = _lib.Context.get(self.device)
+        with ctx.lock:
+            ctx.bind_stream()
+            ctx.check(_lib.lib().tc_srs_prepare(ctx.handle, self._h, code, scale_bits), "prepare")
+        return self
+
+    def table_bytes(self) -> dict:
+        """Device bytes held by this SRS: exponent table, window tables, bases."""
+        e, w, b = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _lib.check(_lib.lib().tc_srs_table_bytes(self._h, C.byref(e), C.byref(w), C.byref(b)), None, "table_bytes")
+        return {"exptab_bytes": e.value, "window_table_bytes": w.value, "basis_bytes": b.value}
+
     def derive_lagrange(self) -> "Srs":
         """Derive the Lagrange elements (and sub-grid sets) from the monomial elements on the
         device, without the trapdoors (a no-op when present).  Returns self."""

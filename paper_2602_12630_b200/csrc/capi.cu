@@ -616,6 +616,36 @@ int tc_srs_export(tc_ctx* ctx, const tc_srs* srs, int which, uint64_t offset, ui
   return TC_OK;
 }
 
+int tc_srs_table_bytes(const tc_srs* srs, uint64_t* exptab_bytes, uint64_t* wintab_bytes, uint64_t* basis_bytes) {
+  if (!srs || !exptab_bytes || !wintab_bytes || !basis_bytes) return TC_ERR_ARGUMENT;
+  *exptab_bytes = (uint64_t)srs->exptab_depth * srs->n * sizeof(EdPk);
+  *wintab_bytes = srs->wintab_bytes;
+  const uint64_t nsub = srs->sublag && srs->m > 1 ? srs->sublag_off[srs->m - 1] + srs->shape[srs->m - 1] : 0;
+  uint64_t b = 0;
+  if (srs->monomial) b += srs->n * sizeof(Aff);
+  if (srs->lagrange) b += srs->n * sizeof(Aff);
+  if (srs->sublag) b += nsub * sizeof(Aff);
+  if (srs->ed_monomial) b += srs->n * sizeof(EdPk);
+  if (srs->ed_lagrange) b += srs->n * sizeof(EdPk);
+  if (srs->ed_sublag) b += nsub * sizeof(EdPk);
+  *basis_bytes = b;
+  return TC_OK;
+}
+
+int tc_srs_prepare(tc_ctx* ctx, tc_srs* srs, int dtype, int scale_bits) {
+  if (!ctx || !srs) return TC_ERR_ARGUMENT;
+  TC_CUDA(ctx, cudaSetDevice(srs->device));
+  if (dtype != TC_DTYPE_F16 || !srs->lagrange || srs->n <= SMALL_MSM_MAX) return TC_OK;
+  const EdPk* lag;
+  TC_TRY(tcrt::srs_edwards(ctx, srs, TC_SRS_LAGRANGE, &lag));
+  const EdPk* tab;
+  const int depth = scale_bits + 6;   // any finite fp16 input (the speculative plan's depth)
+  if ((uint64_t)depth * srs->n >= (1ull << 31)) return TC_OK;
+  const int s = tcrt::srs_exp_table(ctx, srs, lag, srs->n, depth, &tab);
+  if (s == TC_ERR_MEMORY) return TC_OK;   // commits fall back to the float-exponent groups
+  return s;
+}
+
 int tc_srs_export_axis(const tc_srs* srs, uint8_t* out43) {
   if (!srs || !out43) return TC_ERR_ARGUMENT;
   for (int j = 0; j < srs->m; j++) aff_encode43(srs->axis[j], out43 + 43 * j);

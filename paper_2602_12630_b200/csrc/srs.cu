@@ -175,6 +175,7 @@ int srs_window_table(tc_ctx* ctx, tc_srs* srs, const EdPk* bases, uint64_t n, co
   }
   TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));   // shared with other contexts' streams
   srs->wintab[bases] = tab;
+  srs->wintab_bytes += std::max<uint64_t>(n, 1) * nd * sizeof(EdPk);
   *out = tab;
   return TC_OK;
 }

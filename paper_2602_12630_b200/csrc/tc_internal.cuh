@@ -78,6 +78,7 @@ struct tc_srs {
   // fixed-base window tables for full-scalar MSMs (openings): for a base range B (key:
   // its first point), FB_NDIG copies 2^(FB_C w) B, w = 0..FB_NDIG-1 (built on first use)
   std::map<const tc::EdPk*, tc::EdPk*> wintab;
+  uint64_t wintab_bytes = 0;   // device bytes held by the window tables
   // exponent table of the Lagrange basis for fp16 / bf16 commits (WinPlan mode 3):
   // exptab[k n + i] = 2^k G_i, k < exptab_depth (built on first use, grown on demand)
   tc::EdPk* exptab = nullptr;

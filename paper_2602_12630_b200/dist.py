@@ -1,19 +1,35 @@
-"""Multi-GPU partitioning of the prover.
+"""Multi-GPU prover (north star: "partitioned across the GPUs by layer and by
+MSM point-chunk, with a single tiny NCCL gather to combine partial group sums and roots").
 
-Per-layer commitments are independent, so ranks split the layers with no data-path
-collective; the only exchange is ONE all-gather of the 43-byte commitments (NCCL over
-NVLink on GPUs, gloo in the CPU tests), after which every rank builds the (tiny) Terkle
-tree and holds the same root.  EC points cannot be summed by NCCL reductions, so a
-gather (not a reduce) is the right primitive; the root is identical for any world size
-because each commitment is computed whole on one rank.
+Commitments.  The (layer, element) space of a forward — n_layers x N samples — is cut into
+`world` contiguous ranges, one per rank (one process per GPU).  A range covers whole layers
+and at most one chunk at each end: a chunk's commitment is a PARTIAL SUM of its layer's
+commitment, because the Lagrange-route commitment C_T = sum_w T[w] g^{L_w(tau)} is linear
+in the samples, so a chunk is committed as a zero-masked copy of the layer.  When world
+divides n_layers (configs 3 and 5 on 1/2/4/8 GPUs) every range is whole layers and no
+chunk exists.  Each rank writes its parts' 43-byte encodings into a device buffer
+(tc_commit_points_launch), ONE all-gather (NCCL over NVLink; gloo in the CPU tests)
+exchanges them, and every rank sums the parts per layer, hashes the leaves and builds the
+Terkle tree on the device (tc_tree_from_points_launch) — the same commitments and root on
+every rank and for every world size (EC addition is associative; affine output is
+canonical).  Everything is stream-ordered on the context's stream: forward k+1's MSMs run
+while forward k's gather and tree complete (prover_commit_pipeline_dist).
+
+Openings (config 4).  Openings are independent: they are spread over the ranks by a cost
+model, a heavily challenged layer's openings split over several ranks (each recomputes the
+layer's slice commitments, a fraction of one opening group's cost), and the results are
+all-gathered so every rank holds every proof (open_many_dist).
 """
 from __future__ import annotations
+
+import ctypes as C
 
 ELEM_BYTES = 43
 
 
+# --------------------------------------------------------------------------- partitioning
 def layer_partition(n_layers: int, rank: int, world: int):
-    """Contiguous balanced blocks: rank r owns layers [lo, hi)."""
+    """Contiguous balanced blocks of whole layers: rank r owns layers [lo, hi)."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError("bad rank/world")
     base, extra = divmod(n_layers, world)
@@ -22,9 +38,181 @@ def layer_partition(n_layers: int, rank: int, world: int):
     return list(range(lo, hi))
 
 
+def work_partition(n_layers: int, n_elems: int, world: int):
+    """Every rank's share of the flattened (layer, element) space: rank r gets elements
+    [r T / W, (r + 1) T / W) of T = n_layers n_elems, as a list of parts
+    (layer, start, count) in ascending order.  Whole layers when world divides n_layers."""
+    if world < 1 or n_layers < 1 or n_elems < 1:
+        raise ValueError("bad partition arguments")
+    T = n_layers * n_elems
+    out = []
+    for r in range(world):
+        a, b = r * T // world, (r + 1) * T // world
+        parts = []
+        while a < b:
+            l, s = divmod(a, n_elems)
+            c = min(b - a, n_elems - s)
+            parts.append((l, s, c))
+            a += c
+        out.append(parts)
+    return out
+
+
+def gather_layout(parts_all):
+    """Rows of the padded all-gather buffer (world x per rows) that hold real parts, in
+    global order, and the layer of each part."""
+    per = max(1, max(len(p) for p in parts_all))
+    rows = [r * per + i for r, p in enumerate(parts_all) for i in range(len(p))]
+    layer_of = [l for p in parts_all for (l, _, _) in p]
+    return per, rows, layer_of
+
+
+def part_inputs(layers, parts, n_elems):
+    """Device inputs of this rank's parts: whole layers as given, a chunk as a zero-masked
+    copy of its layer (same grid positions, zeros elsewhere).  layers: layer -> tensor."""
+    import torch
+
+    out = []
+    for l, s, c in parts:
+        t = layers[l]
+        if c == n_elems:
+            out.append(t)
+        else:
+            flat = t.reshape(-1)
+            m = torch.zeros_like(flat)
+            m[s:s + c] = flat[s:s + c]
+            out.append(m)
+    return out
+
+
+def _gather_rows(buf, world, group, device_ok: bool):
+    """All-gather a (per, 43) uint8 tensor from every rank -> (world * per, 43) on buf's
+    device.  NCCL gathers device buffers in place on the current stream; gloo (CPU tests,
+    several ranks sharing one GPU) goes through host memory."""
+    import torch
+    import torch.distributed as dist
+
+    if device_ok or buf.device.type == "cpu":
+        out = torch.empty((world * buf.shape[0], buf.shape[1]), dtype=buf.dtype, device=buf.device)
+        dist.all_gather_into_tensor(out, buf, group=group)
+        return out
+    host = buf.cpu()
+    out = torch.empty((world * host.shape[0], host.shape[1]), dtype=host.dtype)
+    dist.all_gather_into_tensor(out, host, group=group)
+    return out.to(buf.device, non_blocking=False)
+
+
+# --------------------------------------------------------------------------- commitments
+class DistProver:
+    """prover_commit over `world` ranks (one process per GPU): launch(layers) commits this
+    rank's parts, all-gathers every rank's part encodings and launches the device tree on a
+    pipeline context; finish(state) returns (commitments, root, tree) for ALL layers."""
+
+    def __init__(self, srs, n_layers: int, rank: int, world: int, *, group=None, tree_config=None, node_srs=None,
+                 scale_bits: int = 16, route: str = "auto", depth: int = 3):
+        import torch
+        import torch.distributed as dist
+
+        from . import authtree
+        from ._lib import Context
+
+        self.srs, self.n_layers, self.rank, self.world, self.group = srs, n_layers, rank, world, group
+        self.cfg = tree_config or authtree.TreeConfig()
+        self.node = node_srs or authtree.node_srs(self.cfg, device=srs.device)
+        self.scale_bits, self.route = scale_bits, route
+        self.parts_all = work_partition(n_layers, srs.size, world)
+        self.parts = self.parts_all[rank]
+        self.per, rows, layer_of = gather_layout(self.parts_all)
+        self.layer_of = (C.c_uint32 * len(layer_of))(*layer_of)
+        self.nparts = len(layer_of)
+        self.ctxs = [Context.pipeline(srs.device, k) for k in range(max(1, depth))]
+        self.dev = torch.device("cuda", srs.device)
+        self.rows = torch.tensor(rows, dtype=torch.long, device=self.dev)
+        backend = dist.get_backend(group) if world > 1 else "nccl"
+        self.device_gather = backend == "nccl"
+        self._k = 0
+
+    def layers_needed(self):
+        """The layers this rank's parts read."""
+        return sorted({l for l, _, _ in self.parts})
+
+    def launch(self, layers: dict):
+        """layers: layer index -> tensor (CUDA, or CPU float: copied on the context's stream)
+        for at least layers_needed().  Returns the state finish() takes."""
+        import torch
+
+        from . import _conv, _lib
+        from .commit import _route
+
+        ctx = self.ctxs[self._k % len(self.ctxs)]
+        self._k += 1
+        with ctx.lock:
+            ctx.fixed_stream.wait_stream(torch.cuda.current_stream(self.dev))
+            with torch.cuda.stream(ctx.fixed_stream):
+                dev_layers = {l: (t if t.is_cuda else t.to(self.dev, non_blocking=True)) for l, t in layers.items()
+                              if l in set(self.layers_needed())}
+                ins = part_inputs(dev_layers, self.parts, self.srs.size)
+                conv = [_conv.device_input(t, self.srs.size, f"cuda:{self.srs.device}") for t in ins]
+                if len({c[1] for c in conv}) > 1:
+                    raise ValueError("all layers must share one dtype")
+                buf = torch.zeros((self.per, ELEM_BYTES), dtype=torch.uint8, device=self.dev)
+                if conv:
+                    arr = (C.c_void_p * len(conv))(*[c[0] for c in conv])
+                    ctx.check(_lib.lib().tc_commit_points_launch(ctx.handle, self.srs.handle, arr, len(conv),
+                                                                 conv[0][1], self.scale_bits, _route(self.route),
+                                                                 buf.data_ptr()), "tc_commit_points_launch")
+                if self.world > 1:
+                    gathered = _gather_rows(buf, self.world, self.group, self.device_gather)
+                    allp = gathered.index_select(0, self.rows)
+                else:
+                    allp = buf[:self.nparts]
+                allp = allp.contiguous()
+                ctx.check(_lib.lib().tc_tree_from_points_launch(ctx.handle, self.node.handle, allp.data_ptr(),
+                                                                self.layer_of, self.nparts, self.n_layers),
+                          "tc_tree_from_points_launch")
+        return ctx, (dev_layers, ins, conv, buf, allp)
+
+    def finish(self, state):
+        from . import authtree
+        from .commit import tc_commit_tree_finish
+
+        ctx, _keep = state
+        commitments, nodes, vals, depth = tc_commit_tree_finish((ctx, self.n_layers, self.node.size, _keep))
+        tree = authtree.tree_from_device(self.cfg, self.n_layers, depth, nodes, vals, self.node)
+        return commitments, tree.root, tree
+
+
+def prover_commit_dist(layers: dict, srs, n_layers: int, rank: int, world: int, **kw):
+    """One forward: (commitments of all n_layers, root, tree), identical on every rank."""
+    p = DistProver(srs, n_layers, rank, world, depth=1, **kw)
+    return p.finish(p.launch(layers))
+
+
+def prover_commit_pipeline_dist(forwards, srs, n_layers: int, rank: int, world: int, *, depth: int = 3, **kw):
+    """prover_commit_dist over a stream of forwards (each a dict layer -> tensor holding at
+    least this rank's layers), yielding (commitments, root, tree) per forward in order;
+    `depth` contexts keep forwards in flight so one forward's gather and tree overlap the
+    next forward's MSMs."""
+    p = DistProver(srs, n_layers, rank, world, depth=depth, **kw)
+    pending = []
+    try:
+        for fwd in forwards:
+            pending.append(p.launch(fwd))
+            if len(pending) == len(p.ctxs):
+                yield p.finish(pending.pop(0))
+        while pending:
+            yield p.finish(pending.pop(0))
+    finally:
+        for st in pending:
+            try:
+                p.finish(st)
+            except Exception:
+                pass
+
+
 def allgather_commitments(local: list, n_layers: int, rank: int, world: int, device=None, group=None):
-    """local: encoded commitments (43 B each) of this rank's layers (layer_partition order).
-    Returns the n_layers encodings in layer order, on every rank."""
+    """local: encoded commitments (43 B each) of this rank's whole layers (layer_partition
+    order).  Returns the n_layers encodings in layer order, on every rank (host path)."""
     import torch
     import torch.distributed as dist
 
@@ -43,3 +231,64 @@ def allgather_commitments(local: list, n_layers: int, rank: int, world: int, dev
         for i in range(len(ids)):
             result.append(bytes(out[r * per + i].tolist()))
     return result
+
+
+# --------------------------------------------------------------------------- openings
+def opening_partition(layer_of_chal, world: int, precomp_min: int = 6):
+    """Assign challenges (their layers, in order) to ranks.  Cost model (tc_open_many's
+    routes): a layer opened k >= precomp_min times costs its slice commitments (~3 units)
+    plus ~0.05 per opening, else ~1.4 per opening.  Layers are placed longest-first on the
+    least-loaded rank; a layer costing more than a rank's fair share is split into that many
+    opening groups (each group recomputes the slice commitments).  Returns per-rank sorted
+    lists of challenge indices."""
+    groups = {}
+    for i, l in enumerate(layer_of_chal):
+        groups.setdefault(l, []).append(i)
+
+    def cost(k):
+        return 3.0 + 0.05 * k if k >= precomp_min else 1.4 * k
+
+    total = sum(cost(len(v)) for v in groups.values())
+    fair = total / world
+    units = []
+    for ids in groups.values():
+        pieces = max(1, min(world, int(cost(len(ids)) // max(fair, 1e-9))))
+        step = -(-len(ids) // pieces)
+        for a in range(0, len(ids), step):
+            units.append(ids[a:a + step])
+    load = [0.0] * world
+    out = [[] for _ in range(world)]
+    for ids in sorted(units, key=lambda u: (-cost(len(u)), u[0])):
+        r = min(range(world), key=lambda j: (load[j], j))
+        out[r] += ids
+        load[r] += cost(len(ids))
+    return [sorted(o) for o in out]
+
+
+def open_many_dist(srs, layers: dict, chals, rank: int, world: int, *, group=None, tree=None, **kw):
+    """Config-4 openings over `world` ranks.  chals: list of (layer, point); layers: layer ->
+    tensor for at least the layers of this rank's challenges.  Returns (openings, proofs):
+    every challenge's TensorOpening and — with `tree` — its Terkle membership proof, on
+    every rank, in challenge order (same bytes as tc_open_many / prove_many on one GPU)."""
+    import torch.distributed as dist
+
+    from .authtree import MembershipProof, prove_many
+    from .commit import TensorOpening, tc_open_many
+
+    mine = opening_partition([l for l, _ in chals], world)[rank]
+    ops = tc_open_many(srs, [layers[chals[i][0]] for i in mine], [chals[i][1] for i in mine], **kw) if mine else []
+    pfs = prove_many(tree, [chals[i][0] for i in mine]) if (tree is not None and mine) else []
+    local = [(i, op.to_bytes(chals[i][1]), pfs[k].to_bytes(tree.config) if pfs else None)
+             for k, (i, op) in enumerate(zip(mine, ops))]
+    if world > 1:
+        allr = [None] * world
+        dist.all_gather_object(allr, local, group=group)
+    else:
+        allr = [local]
+    openings, proofs = [None] * len(chals), [None] * len(chals)
+    for part in allr:
+        for i, ob, pb in part:
+            openings[i] = TensorOpening.from_bytes(ob)[1]
+            if pb is not None:
+                proofs[i] = MembershipProof.from_bytes(pb)
+    return openings, (proofs if tree is not None else None)

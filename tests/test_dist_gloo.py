@@ -62,3 +62,86 @@ def test_allgather_commitments_gloo(n_layers):
     for rank, encs, leaves in res:
         assert encs == want
         assert leaves == [O.hash_to_scalar(e, O.LEAF_TAG) for e in want]
+
+
+# ---------------------------------------------------------------- layer-chunk partition (dist.py)
+def test_work_partition_covers_everything_once():
+    from paper_2602_12630_b200.dist import gather_layout, work_partition
+    for n_layers, n in ((7, 1024), (32, 2 ** 21), (40, 41943040), (1, 5), (3, 7)):
+        for world in (1, 2, 3, 4, 5, 8):
+            allp = work_partition(n_layers, n, world)
+            seen = {}
+            for parts in allp:
+                for l, s, c in parts:
+                    assert 0 <= s and c > 0 and s + c <= n
+                    seen.setdefault(l, []).append((s, c))
+            for l in range(n_layers):
+                segs = sorted(seen[l])
+                assert segs[0][0] == 0 and sum(c for _, c in segs) == n
+                assert all(a[0] + a[1] == b[0] for a, b in zip(segs, segs[1:]))
+            sizes = [sum(c for _, _, c in p) for p in allp]
+            assert max(sizes) - min(sizes) <= 1
+            if n_layers % world == 0:
+                assert all(c == n for p in allp for _, _, c in p)     # whole layers only
+            per, rows, layer_of = gather_layout(allp)
+            assert layer_of == sorted(layer_of) and len(rows) == len(layer_of)
+
+
+def _chunk_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from oracle import tc_oracle as O
+    from paper_2602_12630_b200.dist import _gather_rows, gather_layout, part_inputs, work_partition
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    shape, taus, n_layers = (2, 4), [12345, 678], 5
+    layers = {l: torch.arange(8, dtype=torch.int64) * (l + 1) - 3 for l in range(n_layers)}
+    allp = work_partition(n_layers, 8, world)
+    ins = part_inputs(layers, allp[rank], 8)
+    per, rows, layer_of = gather_layout(allp)
+    buf = torch.zeros((per, 43), dtype=torch.uint8)
+    for i, t in enumerate(ins):   # stand-in for tc_commit_points_launch: the chunk's exact commitment
+        pt = O.commit_trapdoor([int(v) % O.P for v in t.tolist()], shape, taus)
+        buf[i] = torch.frombuffer(bytearray(O.encode_elem(pt)), dtype=torch.uint8)
+    got = _gather_rows(buf, world, None, False)[torch.tensor(rows)]
+    comms = [None] * n_layers      # stand-in for tc_tree_from_points_launch's per-layer sum
+    for row, l in zip(got, layer_of):
+        comms[l] = O.ec_add(comms[l], O.decode_elem(bytes(row.tolist())))
+    q.put((rank, [O.encode_elem(c) for c in comms]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_layer_chunks_partial_sums_gloo(world):
+    """Ranks commit zero-masked chunks of layers; summing the gathered partial commitments
+    per layer gives every layer's whole commitment on every rank (linearity of the
+    Lagrange-route commitment), for world sizes that do not divide the layer count."""
+    from oracle import tc_oracle as O
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_chunk_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [O.encode_elem(O.commit_trapdoor([(v * (l + 1) - 3) % O.P for v in range(8)], (2, 4), [12345, 678]))
+            for l in range(5)]
+    for _, encs in res:
+        assert encs == want
+
+
+def test_opening_partition_balances_and_covers():
+    from paper_2602_12630_b200.dist import opening_partition
+    import numpy as np
+    score = np.random.default_rng(4).pareto(1.5, 32) + 1e-3
+    picks = [int(l) for l in np.random.default_rng(5).choice(32, size=256, p=score / score.sum())]
+    for world in (1, 2, 4, 8):
+        parts = opening_partition(picks, world)
+        assert sorted(i for p in parts for i in p) == list(range(256))
+        assert all(p == sorted(p) for p in parts)
+        if world > 1:
+            assert min(len(p) for p in parts) > 0

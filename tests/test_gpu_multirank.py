@@ -1,7 +1,9 @@
-"""Multi-rank bench path on ONE GPU: two torchrun ranks share the device (gloo for the
-single gather collective; the kernels of the two ranks never wait on each other).  The
-Terkle root must equal the single-rank root: every commitment is computed whole on one
-rank, and EC addition is exact."""
+"""Multi-rank prover paths on ONE GPU: torchrun ranks share the device (gloo moves the one
+gather through host memory; the ranks' kernels never wait on one another).  Roots,
+commitments and every proof byte must be identical for world sizes 1, 2, 3 and 4 — 3 and 4
+do not divide the 7 layers, so layers are split into chunks whose partial MSM sums are
+combined after the gather — and the bench's multi-rank path must reproduce the one-rank
+config-3 root."""
 import json
 import os
 import subprocess
@@ -15,19 +17,50 @@ torch = pytest.importorskip("torch")
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _bench(cmd_prefix, extra_env):
-    env = dict(os.environ, **extra_env)
-    out = subprocess.run(cmd_prefix + [os.path.join(ROOT, "bench.py"), "--steps", "1", "--warmup", "1", "--no-cpu",
-                                       "--no-forward", "--no-monomial"],
-                         capture_output=True, text=True, env=env, timeout=600, cwd=ROOT)
-    assert out.returncode == 0, out.stderr[-3000:]
+def _torchrun(world, script_args, extra_env, port):
+    env = dict(os.environ, TC_DIST_BACKEND="gloo", **extra_env)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={port}"] + script_args
+    out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-4000:]
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
     return json.loads(lines[-1])
 
 
-def test_two_ranks_same_root_as_one():
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
+
+
+def test_dist_prover_identical_across_world_sizes():
+    res = {w: _torchrun(w, [os.path.join(ROOT, "tests", "_dist_worker.py")], {}, 29540 + w) for w in (1, 2, 3, 4)}
+    for w in (2, 3, 4):
+        assert res[w]["root"] == res[1]["root"], w
+        assert res[w]["comms"] == res[1]["comms"], w
+        assert res[w]["pipeline_roots"] == [res[1]["root"]] * 3, w
+        assert res[w]["proofs_sha"] == res[1]["proofs_sha"], w
+    # and equal to the single-process prover_commit
+    import numpy as np
+    import paper_2602_12630_b200 as tcb
+    g = np.random.default_rng(3)
+    host = [(g.standard_t(3, 1024) * (1 + l)).astype(np.float16) for l in range(7)]
+    srs, _ = tcb.setup_srs((8, 8, 16), b"dist-test")
+    comms, root = tcb.prover_commit([torch.from_numpy(h).cuda() for h in host], srs)
+    assert root.to_bytes().hex() == res[1]["root"]
+    assert [c.to_bytes().hex() for c in comms] == res[1]["comms"]
+
+
+def _bench(prefix, extra):
+    env = dict(os.environ, **extra)
+    out = subprocess.run(prefix + [os.path.join(ROOT, "bench.py"), "--steps", "1", "--warmup", "1", "--no-cpu",
+                                   "--no-forward", "--no-monomial"] + (["--gpus", "2"] if len(prefix) > 1 else []),
+                         capture_output=True, text=True, env=env, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    return json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+
+
+def test_bench_two_ranks_same_root_as_one():
     one = _bench([sys.executable], {})
     two = _bench([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
                   "--master-addr=127.0.0.1", "--master-port=29533"], {"TC_DIST_BACKEND": "gloo"})
