@@ -29,6 +29,18 @@ int fail(tc_ctx* ctx, int code, const char* fmt, ...) {
   return code;
 }
 
+int func_smem(tc_ctx* ctx, const void* func, int bytes) {
+  static std::mutex mu;
+  static std::set<std::tuple<int, const void*, int>> done;
+  int dev = 0;
+  TC_CUDA(ctx, cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count({dev, func, bytes})) return TC_OK;
+  TC_CUDA(ctx, cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.insert({dev, func, bytes});
+  return TC_OK;
+}
+
 int scratch(tc_ctx* ctx, const char* name, size_t bytes, void** out) {
   auto& b = ctx->scratch[name];
   if (b.n < bytes) {

@@ -566,22 +566,12 @@ int interpolate_device(tc_ctx* ctx, Fe* d_vals, const uint32_t* shape, int m) {
       const size_t smem = (size_t)(FB + 1) * d * 6 * sizeof(uint32_t);
       static const bool one_thread = getenv("TC_INTERP_NEWTON1") != nullptr;
       if (!one_thread) {
-        static bool attr2 = false;
-        if (!attr2) {
-          TC_CUDA(ctx, cudaFuncSetAttribute(k_interp_newton2<FB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)((FB + 1) * 128 * 6 * sizeof(uint32_t))));
-          attr2 = true;
-        }
+        TC_TRY(func_smem(ctx, (const void*)k_interp_newton2<FB>, (int)((FB + 1) * 128 * 6 * sizeof(uint32_t))));
         k_interp_newton2<FB><<<(unsigned)((nfib + FB - 1) / FB), 2 * FB, smem, st>>>(d_vals, dIf, d, stride, nfib);
         TC_LAUNCHED(ctx);
         continue;
       }
-      static bool attr = false;
-      if (!attr) {
-        TC_CUDA(ctx, cudaFuncSetAttribute(k_interp_newton<FB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)((FB + 1) * 128 * 6 * sizeof(uint32_t))));
-        attr = true;
-      }
+      TC_TRY(func_smem(ctx, (const void*)k_interp_newton<FB>, (int)((FB + 1) * 128 * 6 * sizeof(uint32_t))));
       k_interp_newton<FB><<<(unsigned)((nfib + FB - 1) / FB), FB, smem, st>>>(d_vals, dIf, d, stride, nfib);
       TC_LAUNCHED(ctx);
       continue;
@@ -599,7 +589,7 @@ int interpolate_device(tc_ctx* ctx, Fe* d_vals, const uint32_t* shape, int m) {
     uint32_t FB = std::max<uint32_t>(1u, 2048u / d);
     size_t smem = (size_t)FB * d * sizeof(Fe);
     if (smem > 48 * 1024)
-      TC_CUDA(ctx, cudaFuncSetAttribute(k_interp_axis, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      TC_TRY(func_smem(ctx, (const void*)k_interp_axis, (int)smem));
     unsigned grid = (unsigned)((nfib + FB - 1) / FB);
     k_interp_axis<<<grid, 256, smem, st>>>(d_vals, dB, d, stride, nfib, FB);
     TC_LAUNCHED(ctx);

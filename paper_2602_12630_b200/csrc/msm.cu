@@ -810,8 +810,11 @@ __device__ __forceinline__ uint32_t find_bucket(const uint32_t* off, uint32_t nb
 // that fits in one piece is final (written to buckets[k]); otherwise its piece sums go to
 // items.  The accumulator starts as the piece's first point, then one complete 8M mixed
 // add per entry (no exceptional cases, ec.cuh).
+#ifndef TC_ACCUM_PF
+#define TC_ACCUM_PF 1   // A/B (config 3): 0 -> 3.982 ms, 1 -> 3.909 (MINB 4), 2 (+L2 prefetch) -> 4.15, 3 (point in registers) -> 4.14
+#endif
 #ifndef TC_ACCUM_MINB
-#define TC_ACCUM_MINB 5   // min resident blocks per SM for k_accum_aff: 92 registers, no spills (exponent-table plan A/B: 3-4 -> 4.03 ms @94 regs, 5 -> 4.02, 6 -> 4.07 @80 regs + 40 B spills, 7 -> 4.15, 8 -> 4.35)
+#define TC_ACCUM_MINB 4   // min resident blocks per SM for k_accum_aff (PF 1: 94-96 registers; A/B MINB 3 -> 3.908 ms, 4 -> 3.909, 5 -> 3.94; earlier PF 0 sweep: 5 -> 4.02, 6 -> 4.07 with spills, 8 -> 4.35)
 #endif
 __global__ void __launch_bounds__(128, TC_ACCUM_MINB) k_accum_aff(const uint32_t* vals, const EdPk* bases, const uint32_t* bstart,
                                                    const uint32_t* bend, const uint32_t* toff, const uint32_t* ooff,
@@ -829,12 +832,46 @@ __global__ void __launch_bounds__(128, TC_ACCUM_MINB) k_accum_aff(const uint32_t
   EdAff q = ld_edpk(bases + (v & ~SIGN_BIT));
   if (v & SIGN_BIT) q = edaff_neg(q);
   Ext acc = ext_from_aff(q);
+#if TC_ACCUM_PF == 3
+  // the next point in registers (gathered during the current add), its index two ahead
+  uint32_t vn = a + 1 < b ? vals[a + 1] : 0u;
+  uint32_t vnn = a + 2 < b ? vals[a + 2] : 0u;
+  EdAff qn = ld_edpk(bases + (vn & ~SIGN_BIT));
+  for (uint32_t j = a + 1; j < b; j++) {
+    q = qn;
+    v = vn;
+    vn = vnn;
+    if (j + 1 < b) qn = ld_edpk(bases + (vn & ~SIGN_BIT));
+    vnn = j + 2 < b ? vals[j + 2] : 0u;
+    if (v & SIGN_BIT) q = edaff_neg(q);
+    ext_madd(acc, q);
+  }
+#elif TC_ACCUM_PF
+  // software-pipelined entry index: the next point's address is known one add ahead, so
+  // its gather (and, PF 2, an L2 prefetch of its line) overlaps the current add
+  uint32_t vn = a + 1 < b ? vals[a + 1] : 0u;
+  for (uint32_t j = a + 1; j < b; j++) {
+    v = vn;
+#if TC_ACCUM_PF >= 2
+    if (j + 1 < b) {
+      vn = vals[j + 1];
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(bases + (vn & ~SIGN_BIT)));
+    }
+#else
+    vn = j + 1 < b ? vals[j + 1] : 0u;
+#endif
+    q = ld_edpk(bases + (v & ~SIGN_BIT));
+    if (v & SIGN_BIT) q = edaff_neg(q);
+    ext_madd(acc, q);
+  }
+#else
   for (uint32_t j = a + 1; j < b; j++) {
     v = vals[j];
     q = ld_edpk(bases + (v & ~SIGN_BIT));
     if (v & SIGN_BIT) q = edaff_neg(q);
     ext_madd(acc, q);
   }
+#endif
   if (toff[k + 1] - toff[k] == 1)
     buckets[k] = acc;
   else
@@ -1361,14 +1398,10 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     const uint64_t S0 = std::max<uint64_t>(1, std::min<uint64_t>(conc / LG, n / step));
     const uint64_t chunk = ((n + S0 - 1) / S0 + step - 1) / step * step;
     const uint32_t Sx = (uint32_t)((n + chunk - 1) / chunk);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_fpb_pass<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-      cudaFuncSetAttribute(k_fpb_pass<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-      cudaFuncSetAttribute(k_fpb_pass<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-      cudaFuncSetAttribute(k_fpb_pass<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-      attr = true;
-    }
+    TC_TRY(func_smem(ctx, (const void*)k_fpb_pass<1, false>, 100 * 1024));
+    TC_TRY(func_smem(ctx, (const void*)k_fpb_pass<1, true>, 100 * 1024));
+    TC_TRY(func_smem(ctx, (const void*)k_fpb_pass<2, false>, 100 * 1024));
+    TC_TRY(func_smem(ctx, (const void*)k_fpb_pass<2, true>, 100 * 1024));
     uint32_t *runs, *tot;
     TC_TRY(scratch_t(ctx, "msm.fpbruns", (uint64_t)nb * Sx, &runs));
     TC_TRY(scratch_t(ctx, "msm.bcount", (uint64_t)nb + 1, &tot));
@@ -1380,11 +1413,9 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     static const bool no_sorted = getenv("TC_MSM_NO_SORTED_SCATTER") != nullptr;
     const bool sorted = P.mode == 3 && !no_sorted;
     const size_t fps_smem = (2 * 2048 + 32) * sizeof(uint32_t) + FPS_SLICE * sizeof(uint2);
-    static bool fps_attr = false;
-    if (sorted && !fps_attr) {
-      cudaFuncSetAttribute(k_fpb_scatter_sorted<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fps_smem);
-      cudaFuncSetAttribute(k_fpb_scatter_sorted<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fps_smem);
-      fps_attr = true;
+    if (sorted) {
+      TC_TRY(func_smem(ctx, (const void*)k_fpb_scatter_sorted<1>, (int)fps_smem));
+      TC_TRY(func_smem(ctx, (const void*)k_fpb_scatter_sorted<2>, (int)fps_smem));
     }
     auto pass = [&](bool scatter, uint32_t l0, uint32_t nl) {
       if (scatter && sorted) {
@@ -1481,6 +1512,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
             P.nwin, P.nbm);
   const unsigned gxv = blocks_for(n, 256 * V_EPT);
   const unsigned gx = std::min<unsigned>(blocks_for(n, 256), std::max(1u, (unsigned)ctx->num_sms * 16 / (unsigned)L + 1));
+  TC_TRY(func_smem(ctx, (const void*)k_count_fb, 64 * 1024));
   int s = dispatch_dt(ctx, dtype, [&](auto dt) {
     constexpr int D = decltype(dt)::value;
     if constexpr (D >= 1 && D <= 3) {
@@ -1499,11 +1531,6 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
       const uint64_t conc = (uint64_t)ctx->num_sms * 3;
       const uint64_t S = std::max<uint64_t>(1, std::min<uint64_t>((conc + L - 1) / (uint64_t)L, n >> 14));
       const uint64_t chunk = (n + S - 1) / S;
-      static bool fbc_attr = false;
-      if (!fbc_attr) {
-        cudaFuncSetAttribute(k_count_fb, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-        fbc_attr = true;
-      }
       k_count_fb<<<dim3((unsigned)((n + chunk - 1) / chunk), L), 1024, P.nbm * sizeof(uint32_t), st>>>(
           d_ptrs, n, P, cnt, chunk);
       return;
@@ -1637,7 +1664,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     TC_TRY(scratch_t(ctx, "msm.wsum", nw_total, &wsum));
     const size_t smem = 2 * WB_THREADS * sizeof(Ext);
     if (smem > 48 * 1024)
-      TC_CUDA(ctx, cudaFuncSetAttribute(k_wsum_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      TC_TRY(func_smem(ctx, (const void*)k_wsum_block, (int)smem));
     const bool prescale = P.off[P.nwin - 1] <= 32;
     k_wsum_block<<<nw_total, WB_THREADS, smem, st>>>(buckets, P, wsum, prescale ? 1 : 0);
     TC_LAUNCHED(ctx);

@@ -7,6 +7,8 @@
 #include <cstdio>
 #include <map>
 #include <mutex>
+#include <set>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -118,6 +120,11 @@ int fail(tc_ctx* ctx, int code, const char* fmt, ...);
     int s_ = (call);          \
     if (s_ != TC_OK) return s_; \
   } while (0)
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for `func` on the calling thread's
+// current device, once per (device, kernel, size): the attribute is per device, so a
+// process driving several GPUs sets it on each
+int func_smem(tc_ctx* ctx, const void* func, int bytes);
 
 // grow-only scratch buffer named `name` of at least `bytes` (stream ordered)
 int scratch(tc_ctx* ctx, const char* name, size_t bytes, void** out);
