@@ -91,6 +91,11 @@ uint64_t tc_ctx_launch_count(const tc_ctx* ctx);
 int tc_ctx_set_profiling(tc_ctx* ctx, int on);
 int tc_ctx_kernel_stats(const tc_ctx* ctx, const char* name, double* ms, uint64_t* launches,
                         double* units);
+/* Debug: with TC_SCRATCH_GUARD=1 in the environment when the context is created, every
+ * scratch buffer gets a 256-byte canary right after its requested size; this checks them
+ * all (after synchronising the stream) and returns how many were overwritten (their names
+ * in tc_ctx_last_error).  An out-of-bounds-write detector for the kernels' work buffers. */
+int tc_ctx_check_guards(tc_ctx* ctx, uint64_t* bad_buffers);
 
 /* ---- setup_srs (Srs SPEC.md:44-50) ----------------------------------
  * Monomial elements g^{prod_j tau_j^{i_j}} in lex order (mvpoly.py:3-5) and, with

@@ -53,6 +53,7 @@ _SIGS = [
     ("tc_ctx_set_profiling", C.c_int, [_P, C.c_int]),
     ("tc_ctx_kernel_stats", C.c_int, [_P, C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64),
                                       C.POINTER(C.c_double)]),
+    ("tc_ctx_check_guards", C.c_int, [_P, C.POINTER(C.c_uint64)]),
     ("tc_srs_generate", C.c_int, [_P, _U32P, C.c_int, C.c_char_p, C.c_int, C.POINTER(_P)]),
     ("tc_srs_load", C.c_int, [_P, _U32P, C.c_int, C.c_char_p, C.c_char_p, C.POINTER(_P)]),
     ("tc_srs_derive_lagrange", C.c_int, [_P, _P]),

@@ -59,10 +59,45 @@ int scratch(tc_ctx* ctx, const char* name, size_t bytes, void** out) {
     b.n = want;
   }
   *out = b.p;
+  if (ctx->guard) {
+    // out-of-bounds-write canary right after the requested size (want >= bytes + 256)
+    TC_CUDA(ctx, cudaMemsetAsync((char*)b.p + bytes, 0xA5, GUARD_BYTES, ctx->stream));
+    ctx->guards[name] = std::make_pair((char*)b.p + bytes, bytes);
+  }
   return TC_OK;
 }
 
 }  // namespace tcrt
+
+namespace {
+__global__ void k_check_guard(const uint8_t* g, uint32_t n, uint32_t* bad) {
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
+    if (g[i] != 0xA5) {
+      atomicAdd(bad, 1u);
+      return;
+    }
+}
+}  // namespace
+
+int tc_ctx_check_guards(tc_ctx* ctx, uint64_t* bad_buffers) {
+  if (!ctx || !bad_buffers) return TC_ERR_ARGUMENT;
+  *bad_buffers = 0;
+  if (!ctx->guard) return tcrt::fail(ctx, TC_ERR_VALUE, "scratch guards are off (set TC_SCRATCH_GUARD=1 before creating the context)");
+  TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  std::string bad;
+  for (auto& kv : ctx->guards) {
+    TC_CUDA(ctx, cudaMemsetAsync(ctx->d_flags, 0, 4, ctx->stream));
+    k_check_guard<<<1, 256, 0, ctx->stream>>>((const uint8_t*)kv.second.first, tcrt::GUARD_BYTES, ctx->d_flags);
+    TC_CUDA(ctx, cudaMemcpyAsync(ctx->h_flags, ctx->d_flags, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ctx->h_flags[0]) {
+      ++*bad_buffers;
+      bad += kv.first + "(" + std::to_string(kv.second.second) + " B) ";
+    }
+  }
+  if (*bad_buffers) tcrt::fail(ctx, TC_ERR_VALUE, "write past the end of scratch: %s", bad.c_str());
+  return TC_OK;
+}
 
 using tcrt::fail;
 
@@ -457,6 +492,7 @@ int tc_ctx_create(int device, void* cuda_stream, tc_ctx** out) {
   cudaDeviceProp prop;
   if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) ctx->num_sms = prop.multiProcessorCount;
   ctx->h_stage_bytes = 1 << 20;
+  ctx->guard = getenv("TC_SCRATCH_GUARD") && atoi(getenv("TC_SCRATCH_GUARD")) != 0;
   if (cudaMalloc(&ctx->d_flags, 64) != cudaSuccess || cudaMallocHost(&ctx->h_flags, 64) != cudaSuccess ||
       cudaMallocHost(&ctx->h_stage, ctx->h_stage_bytes) != cudaSuccess) {
     delete ctx;

@@ -59,6 +59,10 @@ struct tc_ctx {
   cudaEvent_t res_ev = nullptr;
   bool res_pending = false;
   uint64_t res_count = 0, res_nodes = 0, res_values = 0;
+  // TC_SCRATCH_GUARD=1: a canary after the requested size of every scratch buffer, checked
+  // by tc_ctx_check_guards (out-of-bounds writes; compute-sanitizer is closed on this pool)
+  bool guard = false;
+  std::map<std::string, std::pair<void*, size_t>> guards;
 };
 
 struct tc_srs {
@@ -128,6 +132,7 @@ int func_smem(tc_ctx* ctx, const void* func, int bytes);
 
 // grow-only scratch buffer named `name` of at least `bytes` (stream ordered)
 int scratch(tc_ctx* ctx, const char* name, size_t bytes, void** out);
+constexpr uint32_t GUARD_BYTES = 256;   // canary size (scratch always allocates >= 256 B of slack)
 
 template <class T>
 int scratch_t(tc_ctx* ctx, const char* name, size_t count, T** out) {

@@ -24,3 +24,25 @@ def reference():
         sys.path.insert(0, REFERENCE_SRC)
     from tensorcommit import backend, field, mvpoly
     return backend, field, mvpoly
+
+
+@pytest.fixture(autouse=True)
+def _scratch_guards():
+    """With TC_SCRATCH_GUARD=1 every library context puts a canary after each scratch buffer;
+    after every test, all contexts' canaries must be intact (no out-of-bounds writes)."""
+    yield
+    if os.environ.get("TC_SCRATCH_GUARD", "0") in ("", "0"):
+        return
+    import ctypes as C
+    try:
+        from paper_2602_12630_b200 import _lib
+    except ImportError:
+        return
+    if _lib._lib is None:
+        return
+    ctxs = list(_lib.Context._by_device.values()) + list(_lib.Context._pipeline.values())
+    for ctx in ctxs:
+        bad = C.c_uint64()
+        with ctx.lock:
+            ctx.check(_lib.lib().tc_ctx_check_guards(ctx.handle, C.byref(bad)), "check_guards")
+        assert bad.value == 0
