@@ -43,7 +43,7 @@ int func_smem(tc_ctx* ctx, const void* func, int bytes) {
 
 int scratch(tc_ctx* ctx, const char* name, size_t bytes, void** out) {
   auto& b = ctx->scratch[name];
-  if (b.n < bytes) {
+  if (b.n < bytes + (ctx->guard ? GUARD_BYTES : 0)) {
     if (b.p) {
       cudaError_t e = cudaFreeAsync(b.p, ctx->stream);
       if (e != cudaSuccess) return fail(ctx, TC_ERR_CUDA, "cudaFreeAsync(%s): %s", name, cudaGetErrorString(e));
