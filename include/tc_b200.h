@@ -258,6 +258,12 @@ int tc_host_hash_to_scalar(const uint8_t* data, uint32_t n, const uint8_t* tag, 
                            uint8_t* out21);
 
 /* ---- self-test hooks (host arithmetic of the shared __host__ __device__ core) ----------- */
+/* the Terkle child value hash_to_scalar(encode_elem(P), b"terkle/node" | b"terkle/leaf") as
+ * the device kernels compute it (register-assembled SHA-256 message), on the host */
+int tc_host_hash_point(const uint8_t* p43, int node, uint8_t* out21);
+/* canonical a^-1 in F_q (field 0) or F_p (field 1) by method 0 = safegcd (Bernstein-Yang),
+ * 1 = Fermat, 2 = binary Euclid — the shared __host__ __device__ code, run on the host */
+int tc_host_field_inv(int field, int method, const uint32_t* a, uint32_t* out);
 int tc_host_fq_mul(const uint32_t* a, const uint32_t* b, uint32_t* out);   /* canonical */
 int tc_host_fp_mul(const uint32_t* a, const uint32_t* b, uint32_t* out);   /* canonical */
 int tc_host_g_mul(const uint8_t* k_le21, uint8_t* out43);                  /* k * g */

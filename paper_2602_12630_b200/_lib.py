@@ -88,6 +88,8 @@ _SIGS = [
     ("tc_tree_from_points_launch", C.c_int, [_P, _P, _P, _P, C.c_uint64, C.c_int]),
     ("tc_pairing", C.c_int, [C.c_char_p, C.c_char_p, _P]),
     ("tc_verify_host", C.c_int, [C.c_int, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(C.c_int)]),
+    ("tc_host_hash_point", C.c_int, [C.c_char_p, C.c_int, _P]),
+    ("tc_host_field_inv", C.c_int, [C.c_int, C.c_int, _U32P, _U32P]),
     ("tc_host_hash_to_scalar", C.c_int, [C.c_char_p, C.c_uint32, C.c_char_p, C.c_uint32, _P]),
     ("tc_host_fq_mul", C.c_int, [_U32P, _U32P, _U32P]),
     ("tc_host_fp_mul", C.c_int, [_U32P, _U32P, _U32P]),

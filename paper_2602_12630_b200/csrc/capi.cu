@@ -898,9 +898,24 @@ static int commit_tree_launch(tc_ctx* ctx, const tc_srs* srs, const void* const*
   TC_TRY(tcrt::scratch_t(ctx, "tree.pts", (uint64_t)count + total_nodes, &d_all));
   TC_TRY(tcrt::scratch_t(ctx, "tree.vals", cap, &d_vals));
   TC_TRY(tcrt::scratch_t(ctx, "tree.levels", total_values, &d_levels));
-  TC_TRY(commit_many_dev(ctx, srs, d_ins, count, dtype, scale_bits, route, d_all));
-  TC_TRY(tcrt::leaf_hash_device(ctx, d_all, count, cap, d_vals));
-  TC_TRY(tcrt::terkle_device(ctx, const_cast<tc_srs*>(node_srs), d_vals, cap, (int)L, d_all + count, d_levels));
+  // the MSM batch hands over its window sums (deferred finish) so the commitments, leaves
+  // and every tree level run as ONE single-block tail kernel; any other MSM plan writes the
+  // points and the tree runs level by level
+  static const bool no_tail = getenv("TC_NO_TREE_TAIL") != nullptr;
+  ctx->defer_req = !no_tail && cap <= 1024;
+  ctx->defer_wsum = nullptr;
+  const int cs = commit_many_dev(ctx, srs, d_ins, count, dtype, scale_bits, route, d_all);
+  ctx->defer_req = false;
+  TC_TRY(cs);
+  if (ctx->defer_wsum) {
+    if (ctx->defer_L != count) return fail(ctx, TC_ERR_VALUE, "deferred finish: %d of %d MSMs", ctx->defer_L, count);
+    TC_TRY(tcrt::tree_tail_device(ctx, const_cast<tc_srs*>(node_srs), ctx->defer_wsum, count, ctx->defer_nwin, cap,
+                                  (int)L, d_all, d_levels));
+    ctx->defer_wsum = nullptr;
+  } else {
+    TC_TRY(tcrt::leaf_hash_device(ctx, d_all, count, cap, d_vals));
+    TC_TRY(tcrt::terkle_device(ctx, const_cast<tc_srs*>(node_srs), d_vals, cap, (int)L, d_all + count, d_levels));
+  }
   const size_t pts_b = (size_t)(count + total_nodes) * sizeof(Aff), vals_b = (size_t)total_values * sizeof(Fe);
   if (ctx->h_res_bytes < pts_b + vals_b) {
     if (ctx->h_res) cudaFreeHost(ctx->h_res);
@@ -1725,6 +1740,29 @@ int tc_host_g_mul(const uint8_t* k_le21, uint8_t* out43) {
   aff_encode43(host_aff(host_mul(g_host(), k)), out43);
   return TC_OK;
 }
+int tc_host_field_inv(int field, int method, const uint32_t* a, uint32_t* out) {
+  if (!a || !out || field < 0 || field > 1 || method < 0 || method > 2) return TC_ERR_ARGUMENT;
+  Fe x, r;
+  for (int i = 0; i < 6; i++) x.v[i] = a[i];
+  if (field == 0) {
+    const Fe m = Fq::to_mont(x);
+    r = Fq::from_mont(method == 0 ? Fq::inv_bygcd(m) : method == 1 ? Fq::inv(m) : Fq::inv_fast(m));
+  } else {
+    const Fe m = Fp::to_mont(x);
+    r = Fp::from_mont(method == 0 ? Fp::inv_bygcd(m) : method == 1 ? Fp::inv(m) : Fp::inv_fast(m));
+  }
+  for (int i = 0; i < 6; i++) out[i] = r.v[i];
+  return TC_OK;
+}
+
+int tc_host_hash_point(const uint8_t* p43, int node, uint8_t* out21) {
+  if (!p43 || !out21) return TC_ERR_ARGUMENT;
+  Aff a;
+  if (!decode43(p43, a)) return TC_ERR_VALUE;
+  fe_to_le21(hash_point_to_scalar(a, node != 0), out21);
+  return TC_OK;
+}
+
 int tc_host_hash_to_scalar(const uint8_t* data, uint32_t n, const uint8_t* tag, uint32_t tn, uint8_t* out21) {
   fe_to_le21(hash_to_scalar(data, n, tag, tn), out21);
   return TC_OK;

@@ -751,13 +751,161 @@ struct Field {
   }
 
 
-  // host: binary Euclid (inv_fast); device: Fermat (a Stein variant with whole-run shifts
-  // measured 59.9k cycles vs Fermat's 49.5k for one thread, tools/inv_latency.cu)
+  // ---- Bernstein-Yang "safegcd" inversion (variable-time divsteps, batches of 30 on
+  // signed 30-bit limbs, after libsecp256k1's modinv32_var): ~13 batches of cheap 32-bit
+  // steps + 6-limb matrix updates instead of Fermat's 167 dependent squarings — the
+  // single-thread latency that sits on the commit / tree tail (ext_to_aff per MSM, per
+  // Terkle node).  tools/tail_latency.cu measures both.
+  TC_HD static void to30(const Fe& a, int32_t r[6]) {
+    const uint32_t M = 0x3FFFFFFFu;
+    r[0] = (int32_t)(a.v[0] & M);
+    r[1] = (int32_t)(((a.v[0] >> 30) | (a.v[1] << 2)) & M);
+    r[2] = (int32_t)(((a.v[1] >> 28) | (a.v[2] << 4)) & M);
+    r[3] = (int32_t)(((a.v[2] >> 26) | (a.v[3] << 6)) & M);
+    r[4] = (int32_t)(((a.v[3] >> 24) | (a.v[4] << 8)) & M);
+    r[5] = (int32_t)((a.v[4] >> 22) | (a.v[5] << 10));   // < 2^28 for the moduli here
+  }
+  TC_HD static Fe from30(const int32_t r[6]) {   // limbs in [0, 2^30), value < 2^192
+    const uint32_t a0 = (uint32_t)r[0], a1 = (uint32_t)r[1], a2 = (uint32_t)r[2], a3 = (uint32_t)r[3],
+                   a4 = (uint32_t)r[4], a5 = (uint32_t)r[5];
+    return Fe{{a0 | (a1 << 30), (a1 >> 2) | (a2 << 28), (a2 >> 4) | (a3 << 26), (a3 >> 6) | (a4 << 24),
+               (a4 >> 8) | (a5 << 22), a5 >> 10}};
+  }
+  TC_HD static int ctz32(uint32_t x) {
+#if defined(__CUDA_ARCH__)
+    return __ffs((int)x) - 1;
+#else
+    return __builtin_ctz(x);
+#endif
+  }
+  // 30 divsteps on the low words: transition matrix [u v; q r] (scaled by 2^30), new eta
+  TC_HD static int32_t divsteps30(int32_t eta, uint32_t f0, uint32_t g0, int32_t& tu, int32_t& tv, int32_t& tq,
+                                  int32_t& tr) {
+    uint32_t u = 1, v = 0, q = 0, r = 1;
+    uint32_t f = f0, g = g0;
+    int i = 30;
+    for (;;) {
+      const int zeros = ctz32(g | (0xFFFFFFFFu << i));   // sentinel: count only up to i
+      g >>= zeros;
+      u <<= zeros;
+      v <<= zeros;
+      eta -= zeros;
+      i -= zeros;
+      if (i == 0) break;
+      if (eta < 0) {   // swap (f, g), (u, q), (v, r); negate the old f, u, v
+        uint32_t t;
+        eta = -eta;
+        t = f, f = g, g = 0u - t;
+        t = u, u = q, q = 0u - t;
+        t = v, v = r, r = 0u - t;
+      }
+      const int limit = (eta + 1) > i ? i : (eta + 1);
+      const uint32_t m = (0xFFFFFFFFu >> (32 - limit)) & 255u;
+      // -(f^-1) mod 256 by Newton's iteration (f odd: f * f = 1 mod 8)
+      uint32_t y = f;
+      y *= 2u - f * y;
+      y *= 2u - f * y;
+      const uint32_t w = (g * (0u - y)) & m;
+      g += f * w;
+      q += u * w;
+      r += v * w;
+    }
+    tu = (int32_t)u, tv = (int32_t)v, tq = (int32_t)q, tr = (int32_t)r;
+    return eta;
+  }
+  TC_HD static Fe inv_bygcd(const Fe& a_mont) {
+    const Fe x = canon(a_mont);
+    if ((x.v[0] | x.v[1] | x.v[2] | x.v[3] | x.v[4] | x.v[5]) == 0) return zero();
+    const int32_t M30 = 0x3FFFFFFF;
+    int32_t md[6], f[6], g[6], d[6] = {0, 0, 0, 0, 0, 0}, e[6] = {1, 0, 0, 0, 0, 0};
+    to30(modulus(), md);
+    to30(x, g);
+    for (int i = 0; i < 6; i++) f[i] = md[i];
+    const uint32_t minv30 = (0u - PM::NP) & 0x3FFFFFFFu;   // modulus^-1 mod 2^30
+    int len = 6;
+    int32_t eta = -1;
+    for (;;) {
+      int32_t u, v, q, r;
+      eta = divsteps30(eta, (uint32_t)f[0], (uint32_t)g[0], u, v, q, r);
+      {   // [d, e] <- t [d, e] / 2^30 mod m (d, e stay in (-2m, m))
+        const int32_t sd = d[5] >> 31, se = e[5] >> 31;
+        int32_t mdd = (u & sd) + (v & se), mee = (q & sd) + (r & se);
+        int64_t cd = (int64_t)u * d[0] + (int64_t)v * e[0];
+        int64_t ce = (int64_t)q * d[0] + (int64_t)r * e[0];
+        mdd -= (int32_t)((minv30 * (uint32_t)cd + (uint32_t)mdd) & (uint32_t)M30);
+        mee -= (int32_t)((minv30 * (uint32_t)ce + (uint32_t)mee) & (uint32_t)M30);
+        cd += (int64_t)md[0] * mdd;
+        ce += (int64_t)md[0] * mee;
+        cd >>= 30;
+        ce >>= 30;
+        for (int i = 1; i < 6; i++) {
+          cd += (int64_t)u * d[i] + (int64_t)v * e[i] + (int64_t)md[i] * mdd;
+          ce += (int64_t)q * d[i] + (int64_t)r * e[i] + (int64_t)md[i] * mee;
+          d[i - 1] = (int32_t)cd & M30;
+          cd >>= 30;
+          e[i - 1] = (int32_t)ce & M30;
+          ce >>= 30;
+        }
+        d[5] = (int32_t)cd;
+        e[5] = (int32_t)ce;
+      }
+      {   // [f, g] <- t [f, g] / 2^30 (exact)
+        int64_t cf = (int64_t)u * f[0] + (int64_t)v * g[0];
+        int64_t cg = (int64_t)q * f[0] + (int64_t)r * g[0];
+        cf >>= 30;
+        cg >>= 30;
+        for (int i = 1; i < len; i++) {
+          cf += (int64_t)u * f[i] + (int64_t)v * g[i];
+          cg += (int64_t)q * f[i] + (int64_t)r * g[i];
+          f[i - 1] = (int32_t)cf & M30;
+          cf >>= 30;
+          g[i - 1] = (int32_t)cg & M30;
+          cg >>= 30;
+        }
+        f[len - 1] = (int32_t)cf;
+        g[len - 1] = (int32_t)cg;
+      }
+      if (g[0] == 0) {
+        int32_t c = 0;
+        for (int j = 1; j < len; j++) c |= g[j];
+        if (c == 0) break;
+      }
+      const int32_t fn = f[len - 1], gn = g[len - 1];
+      int32_t c = (len - 2) >> 31;
+      c |= fn ^ (fn >> 31);
+      c |= gn ^ (gn >> 31);
+      if (c == 0) {   // both top limbs 0 / -1: fold them into the limb below
+        f[len - 2] = (int32_t)((uint32_t)f[len - 2] | ((uint32_t)fn << 30));
+        g[len - 2] = (int32_t)((uint32_t)g[len - 2] | ((uint32_t)gn << 30));
+        --len;
+      }
+    }
+    // d = +-x^-1 in (-2m, m): fold in the sign of f (= +-1), bring to [0, m)
+    {
+      const int32_t add1 = d[5] >> 31, neg = f[len - 1] >> 31;
+      for (int i = 0; i < 6; i++) d[i] += md[i] & add1;
+      for (int i = 0; i < 6; i++) d[i] = (d[i] ^ neg) - neg;
+      for (int i = 0; i < 5; i++) d[i + 1] += d[i] >> 30, d[i] &= M30;
+      const int32_t add2 = d[5] >> 31;
+      for (int i = 0; i < 6; i++) d[i] += md[i] & add2;
+      for (int i = 0; i < 5; i++) d[i + 1] += d[i] >> 30, d[i] &= M30;
+    }
+    // (aR)^-1 = a^-1 R^-1; times R^3 through one Montgomery product -> a^-1 R
+    const Fe r3{{PM::R30, PM::R31, PM::R32, PM::R33, PM::R34, PM::R35}};
+    return mul(from30(d), r3);
+  }
+
+  // single-thread (latency-bound) inversions: safegcd on host and device (Fermat `inv`
+  // stays for the batch kernels, where its branch-free schedule keeps warps converged)
   TC_HD static Fe inv_pref(const Fe& a) {
 #if defined(__CUDA_ARCH__)
-    return inv(a);
+#ifndef TC_INV_FERMAT
+    return inv_bygcd(a);
 #else
-    return inv_fast(a);
+    return inv(a);
+#endif
+#else
+    return inv_bygcd(a);
 #endif
   }
 

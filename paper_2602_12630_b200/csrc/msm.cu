@@ -1238,11 +1238,18 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
                          : (dtype == TC_DTYPE_F16 || dtype == TC_DTYPE_BF16) ? PER16 : (1ull << 26);
     const uint64_t G = std::max<uint64_t>(1, per / n);
     if ((uint64_t)L > G) {
+      const bool defer = ctx->defer_req;   // several pipelines: each finishes its own points
+      ctx->defer_req = false;
       for (int l0 = 0; l0 < L; l0 += (int)G) {
         const int cnt = (int)std::min<uint64_t>(G, (uint64_t)(L - l0));
-        TC_TRY(msm_batch_device(ctx, dtype, scale_bits, h_ptrs + l0, cnt, d_bases, n, d_out + l0,
-                                h_boff ? h_boff + l0 : nullptr, fbw, exp_srs));
+        const int st2 = msm_batch_device(ctx, dtype, scale_bits, h_ptrs + l0, cnt, d_bases, n, d_out + l0,
+                                         h_boff ? h_boff + l0 : nullptr, fbw, exp_srs);
+        if (st2) {
+          ctx->defer_req = defer;
+          return st2;
+        }
       }
+      ctx->defer_req = defer;
       return TC_OK;
     }
   }
@@ -1668,6 +1675,14 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     const bool prescale = P.off[P.nwin - 1] <= 32;
     k_wsum_block<<<nw_total, WB_THREADS, smem, st>>>(buckets, P, wsum, prescale ? 1 : 0);
     TC_LAUNCHED(ctx);
+    if (prescale && ctx->defer_req) {
+      // the caller (commit + tree) sums the windows and converts to affine inside its own
+      // fused tail kernel: hand over the prescaled window sums instead of the points
+      ctx->defer_wsum = wsum;
+      ctx->defer_nwin = P.nwin;
+      ctx->defer_L = L;
+      return TC_OK;
+    }
     if (prescale)
       k_final_sum<<<blocks_for((uint64_t)L * 32, 128), 128, 0, st>>>(wsum, (uint32_t)L, P.nwin, d_out);
     else

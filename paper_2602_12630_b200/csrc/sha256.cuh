@@ -5,9 +5,26 @@
 #include <cstdint>
 #include <cstring>
 
-#include "field.cuh"
+#include "ec.cuh"
 
 namespace tc {
+
+#define TC_SHA256_K                                                                                           \
+  {0x428a2f98u, 0x71374491u, 0xb5c0fbcfu, 0xe9b5dba5u, 0x3956c25bu, 0x59f111f1u, 0x923f82a4u, 0xab1c5ed5u,     \
+   0xd807aa98u, 0x12835b01u, 0x243185beu, 0x550c7dc3u, 0x72be5d74u, 0x80deb1feu, 0x9bdc06a7u, 0xc19bf174u,     \
+   0xe49b69c1u, 0xefbe4786u, 0x0fc19dc6u, 0x240ca1ccu, 0x2de92c6fu, 0x4a7484aau, 0x5cb0a9dcu, 0x76f988dau,     \
+   0x983e5152u, 0xa831c66du, 0xb00327c8u, 0xbf597fc7u, 0xc6e00bf3u, 0xd5a79147u, 0x06ca6351u, 0x14292967u,     \
+   0x27b70a85u, 0x2e1b2138u, 0x4d2c6dfcu, 0x53380d13u, 0x650a7354u, 0x766a0abbu, 0x81c2c92eu, 0x92722c85u,     \
+   0xa2bfe8a1u, 0xa81a664bu, 0xc24b8b70u, 0xc76c51a3u, 0xd192e819u, 0xd6990624u, 0xf40e3585u, 0x106aa070u,     \
+   0x19a4c116u, 0x1e376c08u, 0x2748774cu, 0x34b0bcb5u, 0x391c0cb3u, 0x4ed8aa4au, 0x5b9cca4fu, 0x682e6ff3u,     \
+   0x748f82eeu, 0x78a5636fu, 0x84c87814u, 0x8cc70208u, 0x90befffau, 0xa4506cebu, 0xbef9a3f7u, 0xc67178f2u}
+#if defined(__CUDACC__)
+static __constant__ uint32_t sha256_k[64] = TC_SHA256_K;
+#endif
+inline const uint32_t* sha256_k_host() {
+  static const uint32_t k[64] = TC_SHA256_K;
+  return k;
+}
 
 struct Sha256 {
   uint32_t h[8];
@@ -25,32 +42,36 @@ struct Sha256 {
     total = 0;
   }
 
+  // round constants: __constant__ on the device (uniform loads), a static table on the host
+  TC_HD static uint32_t K(int i) {
+#if defined(__CUDA_ARCH__)
+    return sha256_k[i];
+#else
+    return sha256_k_host()[i];
+#endif
+  }
+
+  // one compression; fully unrolled so the 16-word message window stays in registers
   TC_HD void block(const uint8_t* p) {
-    const uint32_t K[64] = {
-        0x428a2f98u, 0x71374491u, 0xb5c0fbcfu, 0xe9b5dba5u, 0x3956c25bu, 0x59f111f1u, 0x923f82a4u, 0xab1c5ed5u,
-        0xd807aa98u, 0x12835b01u, 0x243185beu, 0x550c7dc3u, 0x72be5d74u, 0x80deb1feu, 0x9bdc06a7u, 0xc19bf174u,
-        0xe49b69c1u, 0xefbe4786u, 0x0fc19dc6u, 0x240ca1ccu, 0x2de92c6fu, 0x4a7484aau, 0x5cb0a9dcu, 0x76f988dau,
-        0x983e5152u, 0xa831c66du, 0xb00327c8u, 0xbf597fc7u, 0xc6e00bf3u, 0xd5a79147u, 0x06ca6351u, 0x14292967u,
-        0x27b70a85u, 0x2e1b2138u, 0x4d2c6dfcu, 0x53380d13u, 0x650a7354u, 0x766a0abbu, 0x81c2c92eu, 0x92722c85u,
-        0xa2bfe8a1u, 0xa81a664bu, 0xc24b8b70u, 0xc76c51a3u, 0xd192e819u, 0xd6990624u, 0xf40e3585u, 0x106aa070u,
-        0x19a4c116u, 0x1e376c08u, 0x2748774cu, 0x34b0bcb5u, 0x391c0cb3u, 0x4ed8aa4au, 0x5b9cca4fu, 0x682e6ff3u,
-        0x748f82eeu, 0x78a5636fu, 0x84c87814u, 0x8cc70208u, 0x90befffau, 0xa4506cebu, 0xbef9a3f7u, 0xc67178f2u};
-    uint32_t w[64];
+    uint32_t w[16];
+#pragma unroll
     for (int i = 0; i < 16; i++)
       w[i] = ((uint32_t)p[4 * i] << 24) | ((uint32_t)p[4 * i + 1] << 16) | ((uint32_t)p[4 * i + 2] << 8) | p[4 * i + 3];
-    for (int i = 16; i < 64; i++) {
-      uint32_t s0 = rotr(w[i - 15], 7) ^ rotr(w[i - 15], 18) ^ (w[i - 15] >> 3);
-      uint32_t s1 = rotr(w[i - 2], 17) ^ rotr(w[i - 2], 19) ^ (w[i - 2] >> 10);
-      w[i] = w[i - 16] + s0 + w[i - 7] + s1;
-    }
     uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7];
+#pragma unroll
     for (int i = 0; i < 64; i++) {
-      uint32_t S1 = rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25);
-      uint32_t ch = (e & f) ^ (~e & g);
-      uint32_t t1 = hh + S1 + ch + K[i] + w[i];
-      uint32_t S0 = rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22);
-      uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
-      uint32_t t2 = S0 + mj;
+      if (i >= 16) {
+        const uint32_t x15 = w[(i - 15) & 15], x2 = w[(i - 2) & 15];
+        const uint32_t s0 = rotr(x15, 7) ^ rotr(x15, 18) ^ (x15 >> 3);
+        const uint32_t s1 = rotr(x2, 17) ^ rotr(x2, 19) ^ (x2 >> 10);
+        w[i & 15] += s0 + w[(i - 7) & 15] + s1;
+      }
+      const uint32_t S1 = rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25);
+      const uint32_t ch = (e & f) ^ (~e & g);
+      const uint32_t t1 = hh + S1 + ch + K(i) + w[i & 15];
+      const uint32_t S0 = rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22);
+      const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+      const uint32_t t2 = S0 + mj;
       hh = g;
       g = f;
       f = e;
@@ -61,6 +82,16 @@ struct Sha256 {
       a = t1 + t2;
     }
     h[0] += a, h[1] += b, h[2] += c, h[3] += d, h[4] += e, h[5] += f, h[6] += g, h[7] += hh;
+  }
+
+  // one compression over 16 big-endian message words already in registers
+  TC_HD void block_words(const uint32_t* m) {
+    uint8_t p[64];
+#pragma unroll
+    for (int i = 0; i < 16; i++)
+      p[4 * i] = (uint8_t)(m[i] >> 24), p[4 * i + 1] = (uint8_t)(m[i] >> 16), p[4 * i + 2] = (uint8_t)(m[i] >> 8),
+      p[4 * i + 3] = (uint8_t)m[i];
+    block(p);
   }
 
   TC_HD void update(const uint8_t* p, uint32_t n) {
@@ -121,6 +152,66 @@ TC_HD Fe hash_to_scalar(const uint8_t* data, uint32_t n, const uint8_t* tag, uin
   // lo * R2 < 2^192 * p < p * R.  2^192 mod p in Montgomery form is R2 (= R * R mod p).
   Fe a = Fp::to_mont(lo);
   Fe b = Fp::mul(Fp::to_mont(hi), Fp::r2());
+  return Fp::from_mont(Fp::add(Fp::red2(a), Fp::red2(b)));
+}
+
+// hash_to_scalar(encode_elem(P), tag) for the Terkle tags b"terkle/leaf" / b"terkle/node"
+// (backend.py:309-317, 346-348) with the 62-byte message
+// "tc/h2f/" || tag || "/" || (0x04 || x LE21 || y LE21) and its SHA-256 padding assembled
+// as 32 words at compile-time byte positions (registers, no byte buffer), two compressions.
+TC_HD Fe hash_point_to_scalar(const Aff& P, bool node) {
+  uint32_t xc[6], yc[6];
+  bool inf;
+  aff_to_canonical(P, xc, yc, &inf);
+  const char* pre = "tc/h2f/terkle/";
+  uint32_t m[32];
+#pragma unroll
+  for (int wd = 0; wd < 32; wd++) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int b = 0; b < 4; b++) {
+      const int i = 4 * wd + b;
+      uint32_t byte;
+      if (i < 14) {
+        byte = (uint8_t)pre[i];
+      } else if (i < 18) {
+        byte = (uint8_t)(node ? "node"[i - 14] : "leaf"[i - 14]);
+      } else if (i == 18) {
+        byte = '/';
+      } else if (i == 19) {
+        byte = inf ? 0u : 4u;
+      } else if (i < 41) {
+        const int k = i - 20;
+        byte = inf ? 0u : (xc[k >> 2] >> (8 * (k & 3))) & 0xffu;
+      } else if (i < 62) {
+        const int k = i - 41;
+        byte = inf ? 0u : (yc[k >> 2] >> (8 * (k & 3))) & 0xffu;
+      } else if (i == 62) {
+        byte = 0x80u;
+      } else if (i < 120) {
+        byte = 0u;
+      } else {
+        byte = (uint32_t)((62ull * 8ull >> (8 * (127 - i))) & 0xffu);   // message length in bits, big-endian
+      }
+      v = (v << 8) | byte;
+    }
+    m[wd] = v;
+  }
+  Sha256 s;
+  s.init();
+  s.block_words(m);
+  s.block_words(m + 16);
+  // the digest as a little-endian 256-bit integer: byte-swap the big-endian state words
+  Fe lo, hi;
+  auto bswap = [](uint32_t x) { return (x >> 24) | ((x >> 8) & 0xff00u) | ((x << 8) & 0xff0000u) | (x << 24); };
+#pragma unroll
+  for (int i = 0; i < 6; i++) lo.v[i] = bswap(s.h[i]);
+  hi.v[0] = bswap(s.h[6]);
+  hi.v[1] = bswap(s.h[7]);
+#pragma unroll
+  for (int i = 2; i < 6; i++) hi.v[i] = 0;
+  const Fe a = Fp::to_mont(lo);
+  const Fe b = Fp::mul(Fp::to_mont(hi), Fp::r2());
   return Fp::from_mont(Fp::add(Fp::red2(a), Fp::red2(b)));
 }
 

@@ -107,12 +107,7 @@ __global__ void __launch_bounds__(128) k_terkle_level(const Fe* vals, uint32_t n
     Aff r = ext_to_aff(acc);
     if (!aff_is_inf(r)) r = Aff{Fq::canon(r.x), Fq::canon(r.y)};
     pts[u] = r;
-    if (next) {
-      uint8_t enc[43];
-      aff_encode43(r, enc);
-      const uint8_t tag[] = {'t', 'e', 'r', 'k', 'l', 'e', '/', 'n', 'o', 'd', 'e'};
-      next[u] = hash_to_scalar(enc, 43, tag, sizeof tag);
-    }
+    if (next) next[u] = hash_point_to_scalar(r, true);
   }
 }
 
@@ -125,10 +120,73 @@ __global__ void k_leaf_hash(const Aff* comms, uint32_t count, uint64_t cap, Fe* 
     vals[i] = Fe{{0, 0, 0, 0, 0, 0}};
     return;
   }
-  uint8_t enc[43];
-  aff_encode43(comms[i], enc);
-  const uint8_t tag[] = {'t', 'e', 'r', 'k', 'l', 'e', '/', 'l', 'e', 'a', 'f'};
-  vals[i] = hash_to_scalar(enc, 43, tag, sizeof tag);
+  vals[i] = hash_point_to_scalar(comms[i], false);
+}
+
+// The tail of a forward's commit + tree (the deferred MSM finish): warp l sums MSM l's
+// prescaled window sums, converts the commitment to canonical affine and hashes its leaf
+// (the inversions of all MSMs run in parallel, 4 warps per SM); warps >= count write the
+// zero padding up to cap.  One launch instead of k_final_sum + k_leaf_hash.
+__global__ void __launch_bounds__(128) k_final_leaf(const Ext* wsum, uint32_t count, int nwin, uint32_t cap, Aff* pts,
+                                                    Fe* vals) {
+  const uint32_t l = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (l >= cap) return;   // whole warps
+  if (l >= count) {
+    if (lane == 0) vals[l] = Fe{{0, 0, 0, 0, 0, 0}};
+    return;
+  }
+  Ext acc = ext_zero();
+  for (int k = (int)lane; k < nwin; k += 32) ext_add(acc, ld_ext(wsum + (uint64_t)l * nwin + k));
+  if (nwin > 1) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      Ext other = shfl_ext(acc, o);
+      if (lane < (uint32_t)o) ext_add(acc, other);
+    }
+  }
+  if (lane == 0) {
+    Aff r = ext_to_aff(acc);
+    if (!aff_is_inf(r)) r = Aff{Fq::canon(r.x), Fq::canon(r.y)};
+    pts[l] = r;
+    vals[l] = hash_point_to_scalar(r, false);
+  }
+}
+
+// One Terkle level with one BLOCK per node: the node's B x 21 byte-window entries spread
+// over TL_THREADS lanes (one mixed add each for B = 8), warp shuffles, then the warps'
+// partial sums through shared memory; thread 0 converts, stores and hashes for the parent.
+constexpr int TL_THREADS = 256;
+__global__ void __launch_bounds__(TL_THREADS) k_terkle_level_b(const Fe* vals, uint32_t B, const EdAff* tab, Aff* pts,
+                                                               Fe* next) {
+  __shared__ Ext part[TL_THREADS / 32];
+  const uint32_t u = blockIdx.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const Fe* sv = vals + (uint64_t)u * B;
+  Ext acc = ext_zero();
+  for (uint32_t kw = t; kw < B * SW; kw += TL_THREADS) {
+    const uint32_t k = kw / SW, wi = kw % SW;
+    const uint32_t byte = (sv[k].v[wi >> 2] >> (8 * (wi & 3))) & 0xffu;
+    if (byte) ext_madd(acc, ld_edaff(tab + (uint64_t)kw * SE + byte - 1));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    Ext other = shfl_ext(acc, o);
+    if (lane < (uint32_t)o) ext_add(acc, other);
+  }
+  if (lane == 0) part[w] = acc;
+  __syncthreads();
+  if (t >= 32) return;
+  acc = t < TL_THREADS / 32 ? part[t] : ext_zero();
+#pragma unroll
+  for (int o = TL_THREADS / 64; o; o >>= 1) {
+    Ext other = shfl_ext(acc, o);
+    if (lane < (uint32_t)o) ext_add(acc, other);
+  }
+  if (t == 0) {
+    Aff r = ext_to_aff(acc);
+    if (!aff_is_inf(r)) r = Aff{Fq::canon(r.x), Fq::canon(r.y)};
+    pts[u] = r;
+    if (next) next[u] = hash_point_to_scalar(r, true);
+  }
 }
 
 }  // namespace
@@ -179,6 +237,28 @@ int small_msm_device(tc_ctx* ctx, tc_srs* srs, int which, const void* const* h_p
   TC_LAUNCHED(ctx);
   // the pointer upload reads h_stage asynchronously: finish before h_stage is reused
   TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return TC_OK;
+}
+
+int tree_tail_device(tc_ctx* ctx, tc_srs* node_srs, const Ext* wsum, int count, int nwin, uint64_t cap, int L,
+                     Aff* d_pts, Fe* d_levels) {
+  const EdAff* tab;
+  TC_TRY(small_tables(ctx, node_srs, TC_SRS_LAGRANGE, &tab));
+  const uint32_t B = (uint32_t)node_srs->n;
+  // level 0's child values (the leaves) go straight into d_levels
+  k_final_leaf<<<blocks_for(cap * 32, 128), 128, 0, ctx->stream>>>(wsum, (uint32_t)count, nwin, (uint32_t)cap, d_pts,
+                                                                  d_levels);
+  TC_LAUNCHED(ctx);
+  uint64_t width = cap, in_off = 0, pts_off = count;
+  for (int l = 0; l < L; l++) {
+    const uint32_t nodes = (uint32_t)(width / B);
+    Fe* out = l + 1 < L ? d_levels + in_off + width : nullptr;
+    k_terkle_level_b<<<nodes, TL_THREADS, 0, ctx->stream>>>(d_levels + in_off, B, tab, d_pts + pts_off, out);
+    TC_LAUNCHED(ctx);
+    in_off += width;
+    pts_off += nodes;
+    width = nodes;
+  }
   return TC_OK;
 }
 

@@ -62,6 +62,12 @@ struct tc_ctx {
   // TC_SCRATCH_GUARD=1: a canary after the requested size of every scratch buffer, checked
   // by tc_ctx_check_guards (out-of-bounds writes; compute-sanitizer is closed on this pool)
   bool guard = false;
+  // deferred MSM finish (commit + tree): with defer_req set, a single-pipeline MSM batch on
+  // the block window-sum path leaves its L x nwin prescaled window sums in defer_wsum and
+  // does not write the points; the caller's fused tail kernel sums and converts them
+  bool defer_req = false;
+  tc::Ext* defer_wsum = nullptr;
+  int defer_nwin = 0, defer_L = 0;
   std::map<std::string, std::pair<void*, size_t>> guards;
 };
 
@@ -192,6 +198,12 @@ int srs_window_table(tc_ctx* ctx, tc_srs* srs, const tc::EdPk* bases, uint64_t n
 // bottom level first) — the tree's `values` without a host recomputation
 int terkle_device(tc_ctx* ctx, tc_srs* srs, tc::Fe* d_vals, uint64_t cap, int L, tc::Aff* d_pts,
                   tc::Fe* d_levels = nullptr);
+// commit + tree tail in ONE single-block kernel: the count MSMs' window sums (count x nwin
+// prescaled Ext, msm_batch_device's deferred finish) -> canonical affine commitments
+// (d_pts[0..count)), leaves hash_to_scalar(encode_elem(C), "terkle/leaf") padded to cap,
+// every tree level (node points after the commitments, level values in d_levels)
+int tree_tail_device(tc_ctx* ctx, tc_srs* node_srs, const tc::Ext* wsum, int count, int nwin, uint64_t cap, int L,
+                     tc::Aff* d_pts, tc::Fe* d_levels);
 // Terkle leaves hash_to_scalar(encode_elem(C_i), "terkle/leaf") of count device points,
 // zero-padded to cap
 int leaf_hash_device(tc_ctx* ctx, const tc::Aff* d_comms, int count, uint64_t cap, tc::Fe* d_vals);

@@ -128,3 +128,37 @@ def test_device_engine_rejects_foreign_domains():
     for dom in (types.SimpleNamespace(zero=0.0, one=1.0), tcb.PrimeField(101)):
         with pytest.raises(ValueError):
             tcb.interpolate_lagrange(dom, [1, 2, 3, 4], grid)
+
+
+def test_host_hash_point_matches_oracle():
+    """The device Terkle child hash (register-assembled SHA-256 message) equals
+    hash_to_scalar(encode_elem(P), tag) (backend.py:309-317, 346-348), run on the host."""
+    from paper_2602_12630_b200 import _lib
+    L = _lib.lib()
+    rng = random.Random(3)
+    pts = [None] + [O.ec_mul(O.G, rng.randrange(1, O.P)) for _ in range(20)]
+    for pt in pts:
+        enc = O.encode_elem(pt)
+        for node, tag in ((1, O.NODE_TAG), (0, O.LEAF_TAG)):
+            out = C.create_string_buffer(21)
+            assert L.tc_host_hash_point(enc, node, out) == 0
+            assert int.from_bytes(out.raw, "little") == O.hash_to_scalar(enc, tag)
+
+
+@pytest.mark.parametrize("field", [0, 1])
+def test_host_field_inversions_agree(field):
+    """safegcd (the latency-path inversion), Fermat and binary Euclid give a^-1 mod m for
+    random and edge values (F_q: q = 120p - 1, F_p: p = 2^161 + 2^24 + 1)."""
+    from paper_2602_12630_b200 import _lib
+    L = _lib.lib()
+    m = O.Q if field == 0 else O.P
+    rng = random.Random(field)
+    vals = [1, 2, 3, m - 1, m - 2, (m + 1) // 2, 2 ** 30, 2 ** 60 + 1, 2 ** 150, m >> 1]
+    vals += [rng.randrange(1, m) for _ in range(400)]
+    for a in vals:
+        arr = (C.c_uint32 * 6)(*[(a >> (32 * i)) & 0xffffffff for i in range(6)])
+        for method in (0, 1, 2):
+            out = (C.c_uint32 * 6)()
+            assert L.tc_host_field_inv(field, method, arr, out) == 0
+            got = sum(int(out[i]) << (32 * i) for i in range(6))
+            assert got == pow(a, -1, m), (a, method)
