@@ -46,3 +46,47 @@ def test_tcop_tctp_roundtrip():
     assert MembershipProof.from_bytes(raw) == pf
     with pytest.raises(ValueError):
         MembershipProof.from_bytes(raw[:-1])
+
+
+def test_tcop_tctp_cross_checked_with_oracle_verifier():
+    """Openings and membership proofs produced by the ORACLE (the reference's arithmetic),
+    serialised through the package's TCOP / TCTP encoders, decode to
+    objects the oracle verifiers accept; the TCOP byte layout is checked field by field."""
+    import struct
+
+    from paper_2602_12630_b200.authtree import MembershipProof, TreeConfig
+    from paper_2602_12630_b200.commit import TensorOpening
+    rng = random.Random(4)
+    shape = (2, 3)
+    srs_elems, axis, taus = O.setup_srs(shape, b"wire")
+    vals = [rng.randrange(O.P) for _ in range(6)]
+    C = O.tc_commit(srs_elems, vals, shape)
+    pt = [rng.randrange(O.P) for _ in shape]
+    y, proofs = O.tc_open(srs_elems, vals, shape, pt)
+    raw = TensorOpening(y, tuple(proofs)).to_bytes(pt)
+    assert raw[:4] == b"TCOP" and struct.unpack_from("<H", raw, 4)[0] == 2
+    assert raw[6:6 + 42] == b"".join(O.encode_scalar(w) for w in pt)
+    assert raw[48:69] == O.encode_scalar(y)
+    assert raw[69:] == b"".join(O.encode_elem(e) for e in proofs)
+    pt2, op2 = TensorOpening.from_bytes(raw)
+    assert O.tc_verify(axis, C, list(pt2), op2.y, list(op2.proofs))
+    assert not O.tc_verify(axis, C, list(pt2), (op2.y + 1) % O.P, list(op2.proofs))
+    # a two-level Terkle membership proof (node shape (2,2), 5 leaves -> 16 slots)
+    node_shape = (2, 2)
+    n_srs, n_axis, _ = O.setup_srs(node_shape, b"wire-node")
+    leaves = [rng.randrange(O.P) for _ in range(5)]
+    levels, values = O.terkle_build(leaves, node_shape, lambda z: O.tc_commit(n_srs, z, node_shape))
+    i = 4
+    nodes, ops = [], []
+    pos = i
+    for lv in range(len(levels)):
+        u, slot = divmod(pos, 4)
+        z = values[lv][4 * u:4 * u + 4]
+        yy, pp = O.tc_open(n_srs, z, node_shape, O.terkle_child_point(slot, node_shape))
+        nodes.append(levels[lv][u])
+        ops.append(TensorOpening(yy, tuple(pp)))
+        pos = u
+    raw = MembershipProof(i, tuple(nodes), tuple(ops)).to_bytes(TreeConfig(shape=node_shape))
+    pf = MembershipProof.from_bytes(raw)
+    assert O.terkle_verify(levels[-1][0], i, leaves[i], list(pf.nodes), [(o.y, o.proofs) for o in pf.openings],
+                           node_shape, n_axis)
