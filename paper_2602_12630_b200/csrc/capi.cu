@@ -518,6 +518,7 @@ int tc_ctx_destroy(tc_ctx* ctx) {
     if (sl.ready) cudaEventDestroy(sl.ready);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->h_res) cudaFreeHost(ctx->h_res);
+  if (ctx->h_off) cudaFreeHost(ctx->h_off);
   if (ctx->res_ev) cudaEventDestroy(ctx->res_ev);
   delete ctx;
   return TC_OK;
@@ -1028,11 +1029,19 @@ int tc_tree_from_points_launch(tc_ctx* ctx, const tc_srs* node_srs, const uint8_
   TC_TRY(tcrt::scratch_t(ctx, "tree.pts", (uint64_t)n_layers + total_nodes, &d_all));
   TC_TRY(tcrt::scratch_t(ctx, "tree.vals", cap, &d_vals));
   TC_TRY(tcrt::scratch_t(ctx, "tree.levels", total_values, &d_levels));
-  if (sizeof(uint32_t) * off.size() > ctx->h_stage_bytes) return fail(ctx, TC_ERR_VALUE, "too many layers");
-  // the offsets ride in the pinned staging buffer: wait for the previous use of it first
-  TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  memcpy(ctx->h_stage, off.data(), sizeof(uint32_t) * off.size());
-  TC_CUDA(ctx, cudaMemcpyAsync(d_off, ctx->h_stage, sizeof(uint32_t) * off.size(), cudaMemcpyHostToDevice, ctx->stream));
+  // the offsets go up through a pinned buffer of this ctx used by nothing else: its previous
+  // upload belonged to the previous launch on this ctx, which tc_commit_tree_finish waited
+  // for — no stream synchronisation here, so the launch stays asynchronous
+  const size_t off_b = sizeof(uint32_t) * off.size();
+  if (ctx->h_off_bytes < off_b) {
+    if (ctx->h_off) cudaFreeHost(ctx->h_off);
+    ctx->h_off = nullptr;
+    ctx->h_off_bytes = 0;
+    TC_CUDA(ctx, cudaHostAlloc(&ctx->h_off, off_b, cudaHostAllocDefault));
+    ctx->h_off_bytes = off_b;
+  }
+  memcpy(ctx->h_off, off.data(), off_b);
+  TC_CUDA(ctx, cudaMemcpyAsync(d_off, ctx->h_off, off_b, cudaMemcpyHostToDevice, ctx->stream));
   TC_CUDA(ctx, cudaMemsetAsync(ctx->d_flags, 0, 4, ctx->stream));
   k_decode43<<<tcrt::blocks_for(nparts, 64), 64, 0, ctx->stream>>>(d_parts43, nparts, d_parts, ctx->d_flags);
   TC_LAUNCHED(ctx);

@@ -59,6 +59,8 @@ struct tc_ctx {
   cudaEvent_t res_ev = nullptr;
   bool res_pending = false;
   uint64_t res_count = 0, res_nodes = 0, res_values = 0;
+  void* h_off = nullptr;   // pinned per-layer part offsets of tc_tree_from_points_launch
+  size_t h_off_bytes = 0;
   // TC_SCRATCH_GUARD=1: a canary after the requested size of every scratch buffer, checked
   // by tc_ctx_check_guards (out-of-bounds writes; compute-sanitizer is closed on this pool)
   bool guard = false;
