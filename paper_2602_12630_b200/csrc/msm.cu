@@ -978,7 +978,10 @@ __global__ void __launch_bounds__(WB_THREADS, 1) k_wsum_block(const Ext* buckets
   sh[t] = run;
   su[t] = u;
   __syncthreads();
-  // inclusive suffix scan R_t = sum_{s >= t} T_s (Hillis-Steele)
+  // inclusive suffix scan R_t = sum_{s >= t} T_s (Hillis-Steele).  The scan and reduction
+  // loops stay rolled: one copy of the Edwards add instead of nine straight-line ones keeps
+  // this latency-bound kernel in the instruction cache
+#pragma unroll 1
   for (uint32_t o = 1; o < WB_THREADS; o <<= 1) {
     Ext v = sh[t];
     if (t + o < WB_THREADS) ext_add(v, sh[t + o]);
@@ -990,6 +993,7 @@ __global__ void __launch_bounds__(WB_THREADS, 1) k_wsum_block(const Ext* buckets
   // reduce sum_{t>=1} R_t (into sh) and sum_t U_t (into su)
   if (t == 0) sh[0] = ext_zero();
   __syncthreads();
+#pragma unroll 1
   for (uint32_t o = WB_THREADS / 2; o; o >>= 1) {
     if (t < o) {
       Ext x = sh[t], y = su[t];
@@ -1048,7 +1052,7 @@ __global__ void k_final_sum(const Ext* wsum, uint32_t L, int nwin, Aff* out) {
   if (l >= L) return;   // whole warps
   Ext acc = ext_zero();
   for (int w = (int)lane; w < nwin; w += 32) ext_add(acc, ld_ext(wsum + (uint64_t)l * nwin + w));
-#pragma unroll
+#pragma unroll 1
   for (int o = 16; o; o >>= 1) {
     Ext other;
 #pragma unroll

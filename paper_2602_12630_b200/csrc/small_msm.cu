@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(128) k_small_msm(const Fe* const* ptrs, uint32
     const uint32_t byte = (s[k].v[w >> 2] >> (8 * (w & 3))) & 0xffu;
     if (byte) ext_madd(acc, ld_edaff(tab + (uint64_t)kw * SE + byte - 1));
   }
-#pragma unroll
+#pragma unroll 1   // one copy of the add: these latency-bound kernels would miss the icache
   for (int o = 16; o; o >>= 1) {
     Ext other = shfl_ext(acc, o);
     if (lane < (uint32_t)o) ext_add(acc, other);
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(128) k_terkle_level(const Fe* vals, uint32_t n
     const uint32_t byte = (s[k].v[w >> 2] >> (8 * (w & 3))) & 0xffu;
     if (byte) ext_madd(acc, ld_edaff(tab + (uint64_t)kw * SE + byte - 1));
   }
-#pragma unroll
+#pragma unroll 1   // one copy of the add: these latency-bound kernels would miss the icache
   for (int o = 16; o; o >>= 1) {
     Ext other = shfl_ext(acc, o);
     if (lane < (uint32_t)o) ext_add(acc, other);
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(128) k_final_leaf(const Ext* wsum, uint32_t co
   Ext acc = ext_zero();
   for (int k = (int)lane; k < nwin; k += 32) ext_add(acc, ld_ext(wsum + (uint64_t)l * nwin + k));
   if (nwin > 1) {
-#pragma unroll
+#pragma unroll 1
     for (int o = 16; o; o >>= 1) {
       Ext other = shfl_ext(acc, o);
       if (lane < (uint32_t)o) ext_add(acc, other);
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(TL_THREADS) k_terkle_level_b(const Fe* vals, u
     const uint32_t byte = (sv[k].v[wi >> 2] >> (8 * (wi & 3))) & 0xffu;
     if (byte) ext_madd(acc, ld_edaff(tab + (uint64_t)kw * SE + byte - 1));
   }
-#pragma unroll
+#pragma unroll 1   // one copy of the add: these latency-bound kernels would miss the icache
   for (int o = 16; o; o >>= 1) {
     Ext other = shfl_ext(acc, o);
     if (lane < (uint32_t)o) ext_add(acc, other);
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(TL_THREADS) k_terkle_level_b(const Fe* vals, u
   __syncthreads();
   if (t >= 32) return;
   acc = t < TL_THREADS / 32 ? part[t] : ext_zero();
-#pragma unroll
+#pragma unroll 1
   for (int o = TL_THREADS / 64; o; o >>= 1) {
     Ext other = shfl_ext(acc, o);
     if (lane < (uint32_t)o) ext_add(acc, other);
