@@ -1600,11 +1600,17 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   // (config 5: ~2300 per bucket) take longer pieces (fewer items for the tail levels:
   // 6-layer batch 22.0 -> 21.5 ms at 64)
   uint32_t T = (E >= (1u << 20)) ? T_ENV : (E >= (1u << 14) ? 16u : 8u);
+  // exponent-table plan (mode 3, ~1000 entries per bucket): pieces of 32 with 16 items per
+  // reduction thread (A/B over 40 forwards: T 64 / T1 8 -> 4.479 ms per step, 32 / 16 ->
+  // 4.463, 24 / 8 -> 4.480; shorter pieces shorten the accumulation's last wave, the
+  // wider reduction keeps the item levels at two)
+  const bool m3 = P.mode == 3 && !getenv("TC_MSM_T") && !getenv("TC_MSM_T1");
   if (!getenv("TC_MSM_T") && E >= (1u << 20)) {
     const uint64_t per_bucket = E / std::max<uint64_t>(1, nb);
-    while (T < 64 && (uint64_t)T * 16 <= per_bucket) T *= 2;
+    const uint32_t tmax = m3 ? 32u : 64u;
+    while (T < tmax && (uint64_t)T * 16 <= per_bucket) T *= 2;
   }
-  const uint32_t T1 = T1_ENV;
+  const uint32_t T1 = (m3 && T == 32) ? 16u : T1_ENV;
   int levels = 1;   // enough for the largest bucket (<= n entries when its size is unknown)
   for (uint64_t capT = T; capT < (have_maxb ? (uint64_t)maxb : n); capT *= T1) levels++;
   // items = pieces of multi-piece buckets: ceil(sz/T) <= 2 sz / T for sz > T
