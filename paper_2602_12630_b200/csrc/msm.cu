@@ -75,6 +75,7 @@ struct WinPlan {
   uint32_t mlo[MAXW];        // weight of the window's first bucket (mode 0: 1)
   uint32_t base[MAXW + 1];   // first bucket of window w inside one MSM
   uint32_t tpitch;           // mode 3: points per exponent-table level (entry = g tpitch + i)
+  const uint32_t* ktab = nullptr;   // mode 3, fp16: per |bit pattern| key | g << 16 (0xFFFFFFFF: no entry)
 };
 
 __device__ __forceinline__ uint32_t bitlen6(const Fe& a) {
@@ -523,6 +524,16 @@ __device__ __forceinline__ uint32_t fp_key(const WinPlan& P, uint64_t mag, uint3
 template <int DT>
 __device__ __forceinline__ bool key3(uint32_t raw, bool in, int scale_bits, const WinPlan& P, uint32_t& key,
                                      uint32_t& g, bool& neg) {
+  if (DT == 1 && P.ktab) {
+    // branch-free: one cached table load per element (built by k_build_ktab from the same
+    // quant64 / fp_key as below, so every bit pattern maps exactly as the general path)
+    if (!in) return false;
+    const uint32_t e = __ldg(P.ktab + (raw & 0x7fffu));
+    key = e & 0xffffu;
+    g = e >> 16;
+    neg = (raw >> 15) != 0;
+    return e != 0xffffffffu;
+  }
   if (DT == 1 && in) {
     const int e = (int)((raw >> 10) & 0x1fu);
     // e == 0 (zero / subnormal) never takes this path, whatever scale_bits admits
@@ -537,6 +548,19 @@ __device__ __forceinline__ bool key3(uint32_t raw, bool in, int scale_bits, cons
   if (!mag) return false;
   key = fp_key(P, mag, g);
   return true;
+}
+
+// the fp16 key table of the exponent-table plan: entry r (r = |bit pattern|) = the bucket key
+// | table level g << 16 of the quantised magnitude, 0xFFFFFFFF when it quantises to zero (or
+// is not finite: the count pass flags those from the raw bits)
+__global__ void k_build_ktab(uint32_t* tab, int scale_bits, WinPlan P) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= 32768u) return;
+  bool neg;
+  const uint64_t mag = ((r & 0x7c00u) == 0x7c00u) ? 0ull : quant64<1>(r, scale_bits, neg);
+  uint32_t g = 0, key = 0;
+  if (mag) key = fp_key(P, mag, g);
+  tab[r] = mag ? (key | (g << 16)) : 0xffffffffu;
 }
 
 template <int DT, bool SCATTER>
@@ -1217,6 +1241,25 @@ namespace tcrt {
 
 int quantize_flags_to_status(tc_ctx* ctx, uint32_t f);
 
+// fp16 inputs on the exponent-table plan classify every element with one table load
+// (k_build_ktab, per context and scale_bits) instead of the per-element branches of key3
+static int attach_ktab(tc_ctx* ctx, int dtype, int scale_bits, WinPlan& P) {
+  P.ktab = nullptr;
+  static const bool off = getenv("TC_NO_KTAB") != nullptr;
+  if (off || dtype != TC_DTYPE_F16) return TC_OK;
+  const std::string key = "msm.ktab." + std::to_string(scale_bits);
+  uint32_t* tab;
+  const bool have = ctx->scratch.count(key + ".ready") != 0;
+  TC_TRY(scratch_t(ctx, key.c_str(), 32768, &tab));
+  if (!have) {
+    k_build_ktab<<<128, 256, 0, ctx->stream>>>(tab, scale_bits, P);
+    TC_LAUNCHED(ctx);
+    ctx->scratch[key + ".ready"] = tc_ctx::Buf{};
+  }
+  P.ktab = tab;
+  return TC_OK;
+}
+
 int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* h_ptrs, int L, const EdPk* d_bases,
                      uint64_t n, Aff* d_out, const uint32_t* h_boff, int fbw, tc_srs* exp_srs) {
   if (fbw && (dtype != TC_DTYPE_FP_LIMBS || n * fb_ndig(fbw) >= (1ull << 31)))
@@ -1352,6 +1395,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   const int groups = fp_mb ? std::max(1, (int)nbits - fp_mb + 1) : 0;
   if (spec_tab) {
     P = plan_fpx(fp_mb, (uint32_t)exp_srs->n);
+    TC_TRY(attach_ktab(ctx, dtype, scale_bits, P));
     bases = spec_tab;
   } else if (!fbw && exp_srs && d_bases == exp_srs->ed_lagrange && !no_exp && !getenv("TC_MSM_NO_BLKCNT") && vec_ok &&
       fp_mb && n >= EXP_MIN_N &&
@@ -1364,6 +1408,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     if ((full_ok && srs_exp_table(ctx, exp_srs, d_bases, exp_srs->n, full, &tab) == TC_OK) ||
         srs_exp_table(ctx, exp_srs, d_bases, exp_srs->n, groups, &tab) == TC_OK) {
       P = plan_fpx(fp_mb, (uint32_t)exp_srs->n);
+      TC_TRY(attach_ktab(ctx, dtype, scale_bits, P));
       bases = tab;   // multi-base batches (h_boff) index inside the table's level 0 as before
     }
   }
@@ -1428,13 +1473,18 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
       TC_TRY(func_smem(ctx, (const void*)k_fpb_scatter_sorted<1>, (int)fps_smem));
       TC_TRY(func_smem(ctx, (const void*)k_fpb_scatter_sorted<2>, (int)fps_smem));
     }
+    // the fp16 key table pays in the ALU-bound count pass (131 -> 100 us on config 3) but not
+    // in the barrier-bound slice-sorted scatter (366 -> 458 us: its key phase is latency
+    // bound and the table load adds to it), which keeps the branchy key3 path
+    WinPlan Pns = P;
+    Pns.ktab = nullptr;
     auto pass = [&](bool scatter, uint32_t l0, uint32_t nl) {
       if (scatter && sorted) {
         if (dtype == TC_DTYPE_F16)
-          k_fpb_scatter_sorted<1><<<dim3(Sx, nl), FPS_THREADS, fps_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals,
+          k_fpb_scatter_sorted<1><<<dim3(Sx, nl), FPS_THREADS, fps_smem, st>>>(d_ptrs, n, scale_bits, Pns, runs, vals,
                                                                                chunk, l0);
         else
-          k_fpb_scatter_sorted<2><<<dim3(Sx, nl), FPS_THREADS, fps_smem, st>>>(d_ptrs, n, scale_bits, P, runs, vals,
+          k_fpb_scatter_sorted<2><<<dim3(Sx, nl), FPS_THREADS, fps_smem, st>>>(d_ptrs, n, scale_bits, Pns, runs, vals,
                                                                                chunk, l0);
         return;
       }
