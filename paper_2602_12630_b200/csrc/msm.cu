@@ -834,6 +834,9 @@ __device__ __forceinline__ uint32_t find_bucket(const uint32_t* off, uint32_t nb
 // that fits in one piece is final (written to buckets[k]); otherwise its piece sums go to
 // items.  The accumulator starts as the piece's first point, then one complete 8M mixed
 // add per entry (no exceptional cases, ec.cuh).
+#ifndef TC_M3_SMALL_E
+#define TC_M3_SMALL_E (1ull << 24)   // exponent-table batches below this many entries take 16-entry pieces
+#endif
 #ifndef TC_ACCUM_PF
 #define TC_ACCUM_PF 1   // A/B (config 3): 0 -> 3.982 ms, 1 -> 3.909 (MINB 4), 2 (+L2 prefetch) -> 4.15, 3 (point in registers) -> 4.14
 #endif
@@ -1657,10 +1660,12 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   const bool m3 = P.mode == 3 && !getenv("TC_MSM_T") && !getenv("TC_MSM_T1");
   if (!getenv("TC_MSM_T") && E >= (1u << 20)) {
     const uint64_t per_bucket = E / std::max<uint64_t>(1, nb);
-    const uint32_t tmax = m3 ? 32u : 64u;
+    // smaller batches (a multi-GPU rank's few layers) have fewer waves: shorter pieces still
+    // (4 layers: 0.706 -> 0.686 ms per pipelined forward at 16; 32 layers: 16 is slower)
+    const uint32_t tmax = m3 ? (E < TC_M3_SMALL_E ? 16u : 32u) : 64u;
     while (T < tmax && (uint64_t)T * 16 <= per_bucket) T *= 2;
   }
-  const uint32_t T1 = (m3 && T == 32) ? 16u : T1_ENV;
+  const uint32_t T1 = (m3 && T >= 16) ? 16u : T1_ENV;
   int levels = 1;   // enough for the largest bucket (<= n entries when its size is unknown)
   for (uint64_t capT = T; capT < (have_maxb ? (uint64_t)maxb : n); capT *= T1) levels++;
   // items = pieces of multi-piece buckets: ceil(sz/T) <= 2 sz / T for sz > T

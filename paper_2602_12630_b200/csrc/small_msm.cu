@@ -82,35 +82,6 @@ __global__ void __launch_bounds__(128) k_small_msm(const Fe* const* ptrs, uint32
   }
 }
 
-// One Terkle level on the device: node u commits to vals[u B .. u B + B) (one warp per
-// node, the table kernel's sum), its canonical affine point goes to pts[u] and, for the
-// next level, hash_to_scalar(encode_elem(C_u), "terkle/node") to next[u] (canonical F_p,
-// backend.py:309-317, 346-348) — no host round trip between levels.
-__global__ void __launch_bounds__(128) k_terkle_level(const Fe* vals, uint32_t nodes, uint32_t B, const EdAff* tab,
-                                                      Aff* pts, Fe* next) {
-  const uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t lane = threadIdx.x & 31;
-  if (u >= nodes) return;
-  const Fe* s = vals + (uint64_t)u * B;
-  Ext acc = ext_zero();
-  for (uint32_t kw = lane; kw < B * SW; kw += 32) {
-    const uint32_t k = kw / SW, w = kw % SW;
-    const uint32_t byte = (s[k].v[w >> 2] >> (8 * (w & 3))) & 0xffu;
-    if (byte) ext_madd(acc, ld_edaff(tab + (uint64_t)kw * SE + byte - 1));
-  }
-#pragma unroll 1   // one copy of the add: these latency-bound kernels would miss the icache
-  for (int o = 16; o; o >>= 1) {
-    Ext other = shfl_ext(acc, o);
-    if (lane < (uint32_t)o) ext_add(acc, other);
-  }
-  if (lane == 0) {
-    Aff r = ext_to_aff(acc);
-    if (!aff_is_inf(r)) r = Aff{Fq::canon(r.x), Fq::canon(r.y)};
-    pts[u] = r;
-    if (next) next[u] = hash_point_to_scalar(r, true);
-  }
-}
-
 // Terkle leaves on the device: vals[i] = hash_to_scalar(encode_elem(C_i), "terkle/leaf")
 // (backend.py:309-317, 346-348) for i < count, zero padding up to cap
 __global__ void k_leaf_hash(const Aff* comms, uint32_t count, uint64_t cap, Fe* vals) {
@@ -281,8 +252,7 @@ int terkle_device(tc_ctx* ctx, tc_srs* srs, Fe* d_vals, uint64_t cap, int L, Aff
     const uint32_t nodes = (uint32_t)(width / B);
     Fe* out_vals = (l + 1 < L) ? (d_levels ? d_levels + lvl_off : (cur == d_vals ? nxt : d_vals)) : nullptr;
     if (l + 1 < L) lvl_off += nodes;
-    k_terkle_level<<<blocks_for((uint64_t)nodes * 32, 128), 128, 0, ctx->stream>>>(cur, nodes, B, tab,
-                                                                                   d_pts + written, out_vals);
+    k_terkle_level_b<<<nodes, TL_THREADS, 0, ctx->stream>>>(cur, B, tab, d_pts + written, out_vals);
     TC_LAUNCHED(ctx);
     written += nodes;
     width = nodes;
