@@ -627,12 +627,14 @@ def run_openings(args, dev, rank, world, cores):
     import torch.distributed as dist
 
     import paper_2602_12630_b200 as tcb
-    from paper_2602_12630_b200.dist import open_many_dist, opening_partition, prover_commit_dist
+    from paper_2602_12630_b200.dist import open_many_dist, opening_partition, prover_commit_dist, work_partition
     cfg = CONFIGS[3]
     n_layers = cfg["layers"]
     chals = config4_challenges(n_layers, cfg["shape"], tcb.P)
     mine = opening_partition([l for l, _ in chals], world)[rank]
-    need = sorted({chals[i][0] for i in mine} | {l for l in range(n_layers) if l % world == rank})
+    n_elems = int(__import__("numpy").prod(cfg["act"]))
+    # this rank's challenged layers and the layers of its commitment share (dist.py)
+    need = sorted({chals[i][0] for i in mine} | {l for l, _, _ in work_partition(n_layers, n_elems, world)[rank]})
     host = dict(zip(need, make_layers_host(cfg, need)))
     layers = {l: torch.from_numpy(h).to(dev) for l, h in host.items()}
     srs, _ = tcb.setup_srs(cfg["shape"], b"tc-b200/config3", device=dev.index)

@@ -66,3 +66,17 @@ def test_bench_two_ranks_same_root_as_one():
                   "--master-addr=127.0.0.1", "--master-port=29533"], {"TC_DIST_BACKEND": "gloo"})
     assert two["n_gpus"] == 2 and two["config"]["parallelism"] == "layers/2"
     assert two["root"] == one["root"]
+
+
+def test_bench_config4_two_ranks():
+    """bench.py --config 4 under torchrun with 2 ranks: openings split by cost over the
+    ranks, every proof gathered to every rank; the bench verifies a sample of openings and
+    membership proofs on each rank before reporting."""
+    env = dict(os.environ, TC_DIST_BACKEND="gloo")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                          "--master-addr=127.0.0.1", "--master-port=29537", os.path.join(ROOT, "bench.py"),
+                          "--gpus", "2", "--config", "4", "--steps", "1", "--warmup", "1"],
+                         capture_output=True, text=True, env=env, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0
