@@ -377,13 +377,42 @@ int srs_derive_lagrange(tc_ctx* ctx, tc_srs* srs) {
   if (srs->lagrange) return TC_OK;
   const EdPk* mono;
   TC_TRY(tcrt::srs_edwards(ctx, srs, TC_SRS_MONOMIAL, &mono));
-  TC_CUDA(ctx, cudaMalloc(&srs->lagrange, srs->n * sizeof(Aff)));
-  TC_TRY(tcrt::derive_lagrange_device(ctx, mono, srs->shape, srs->m, srs->lagrange));
-  if (srs->m > 1) {
-    TC_TRY(srs_alloc_sublag(ctx, srs));
-    for (int i = 1; i < srs->m; i++)
-      TC_TRY(tcrt::derive_lagrange_device(ctx, mono, srs->shape + i, srs->m - i, srs->sublag + srs->sublag_off[i]));
+  // derive into buffers the SRS does not own yet: a failure leaves it monomial-only, never
+  // with a half-computed Lagrange set the routes would trust
+  Aff *lag = nullptr, *sub = nullptr;
+  auto cleanup = [&](int s) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(lag);
+    cudaFree(sub);
+    return s;
+  };
+  if (cudaMalloc(&lag, srs->n * sizeof(Aff)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(ctx, TC_ERR_MEMORY, "derive: Lagrange set of %llu points", (unsigned long long)srs->n);
   }
+  int s = tcrt::derive_lagrange_device(ctx, mono, srs->shape, srs->m, lag);
+  if (s) return cleanup(s);
+  uint64_t off[TC_MAX_AXES] = {0}, total = 0;
+  for (int i = 1; i < srs->m; i++) {
+    uint64_t ni = 1;
+    for (int j = i; j < srs->m; j++) ni *= srs->shape[j];
+    off[i] = total;
+    total += ni;
+  }
+  if (srs->m > 1) {
+    if (cudaMalloc(&sub, total * sizeof(Aff)) != cudaSuccess) {
+      cudaGetLastError();
+      return cleanup(fail(ctx, TC_ERR_MEMORY, "derive: sub-grid sets of %llu points", (unsigned long long)total));
+    }
+    for (int i = 1; i < srs->m && !s; i++)
+      s = tcrt::derive_lagrange_device(ctx, mono, srs->shape + i, srs->m - i, sub + off[i]);
+    if (s) return cleanup(s);
+  }
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+    return cleanup(fail(ctx, TC_ERR_CUDA, "derive: %s", cudaGetErrorString(cudaGetLastError())));
+  srs->lagrange = lag;
+  srs->sublag = sub;
+  for (int i = 0; i < TC_MAX_AXES; i++) srs->sublag_off[i] = off[i];
   TC_TRY(srs_build_edwards(ctx, srs));
   TC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return TC_OK;
