@@ -549,6 +549,7 @@ int tc_ctx_destroy(tc_ctx* ctx) {
   if (ctx->h_res) cudaFreeHost(ctx->h_res);
   if (ctx->h_off) cudaFreeHost(ctx->h_off);
   if (ctx->res_ev) cudaEventDestroy(ctx->res_ev);
+  if (ctx->ev_mid) cudaEventDestroy(ctx->ev_mid);
   delete ctx;
   return TC_OK;
 }

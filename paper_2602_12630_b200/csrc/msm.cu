@@ -1429,6 +1429,66 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   uint64_t E;
   bool have_maxb = false;   // exact largest bucket known (counting layout)
   uint32_t maxb = 0;
+  // level 0 of the bucket accumulation: piece tables (k_count0 + scans) and k_accum_aff.
+  // E_plan sizes pieces and scratch (an upper bound is fine: surplus threads exit on the
+  // device-side piece count); the block-counter path queues it BEFORE the host waits for
+  // the entry count, so the GPU goes from the scatter straight into the accumulation
+  struct Level0 {
+    uint32_t T = 0, T1 = 0;
+    uint64_t max_items = 0;
+    uint32_t *np, *npm, *toff, *offA, *offB;
+    Ext *itemsA, *itemsB, *buckets;
+    void* d_scan;
+    size_t scan_bytes = 0;
+  } L0;
+  bool early0 = false;
+  auto level0 = [&](uint64_t E_plan) -> int {
+    static const uint32_t T_ENV = getenv("TC_MSM_T") ? (uint32_t)atoi(getenv("TC_MSM_T")) : 16u;   // sweep (config 3): 8 6.75, 12 6.66, 16 6.54, 24 6.60, 32 6.64 ms
+    static const uint32_t T1_ENV = getenv("TC_MSM_T1") ? (uint32_t)atoi(getenv("TC_MSM_T1")) : 8u;
+    // piece length: 16 entries balances config 3 (~114 entries per bucket); dense buckets
+    // (config 5: ~2300 per bucket) take longer pieces (fewer items for the tail levels:
+    // 6-layer batch 22.0 -> 21.5 ms at 64)
+    uint32_t T = (E_plan >= (1u << 20)) ? T_ENV : (E_plan >= (1u << 14) ? 16u : 8u);
+    // exponent-table plan (mode 3, ~1000 entries per bucket): pieces of 32 with 16 items per
+    // reduction thread (A/B over 40 forwards: T 64 / T1 8 -> 4.479 ms per step, 32 / 16 ->
+    // 4.463, 24 / 8 -> 4.480; shorter pieces shorten the accumulation's last wave, the
+    // wider reduction keeps the item levels at two)
+    const bool m3 = P.mode == 3 && !getenv("TC_MSM_T") && !getenv("TC_MSM_T1");
+    if (!getenv("TC_MSM_T") && E_plan >= (1u << 20)) {
+      const uint64_t per_bucket = E_plan / std::max<uint64_t>(1, nb);
+      // smaller batches (a multi-GPU rank's few layers) have fewer waves: shorter pieces still
+      // (4 layers: 0.706 -> 0.686 ms per pipelined forward at 16; 32 layers: 16 is slower)
+      const uint32_t tmax = m3 ? (E_plan < TC_M3_SMALL_E ? 16u : 32u) : 64u;
+      while (T < tmax && (uint64_t)T * 16 <= per_bucket) T *= 2;
+    }
+    L0.T = T;
+    L0.T1 = (m3 && T >= 16) ? 16u : T1_ENV;
+    // items = pieces of multi-piece buckets: ceil(sz/T) <= 2 sz / T for sz > T
+    L0.max_items = 2 * ((E_plan + T - 1) / T) + 2;
+    TC_TRY(scratch_t(ctx, "msm.np", (uint64_t)nb + 1, &L0.np));
+    TC_TRY(scratch_t(ctx, "msm.npm", (uint64_t)nb + 1, &L0.npm));
+    TC_TRY(scratch_t(ctx, "msm.toff", (uint64_t)nb + 1, &L0.toff));
+    TC_TRY(scratch_t(ctx, "msm.offA", (uint64_t)nb + 1, &L0.offA));
+    TC_TRY(scratch_t(ctx, "msm.offB", (uint64_t)nb + 1, &L0.offB));
+    TC_TRY(scratch_t(ctx, "msm.itemsA", L0.max_items, &L0.itemsA));
+    TC_TRY(scratch_t(ctx, "msm.itemsB", L0.max_items, &L0.itemsB));
+    TC_TRY(scratch_t(ctx, "msm.buckets", nb, &L0.buckets));
+    L0.scan_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, L0.scan_bytes, L0.np, L0.toff, (int)(nb + 1), st);
+    TC_TRY(scratch(ctx, "msm.scantmp", L0.scan_bytes, &L0.d_scan));
+    k_count0<<<blocks_for((uint64_t)nb + 1, 256), 256, 0, st>>>(bstart, bend, nb, T, L0.np, L0.npm, L0.buckets);
+    TC_LAUNCHED(ctx);
+    TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(L0.d_scan, L0.scan_bytes, L0.np, L0.toff, (int)(nb + 1), st));
+    TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(L0.d_scan, L0.scan_bytes, L0.npm, L0.offA, (int)(nb + 1), st));
+    ctx->launches += 4;
+    if (ctx->prof) TC_CUDA(ctx, cudaEventRecord(ctx->ev[0], st));
+    k_accum_aff<<<blocks_for((E_plan + T - 1) / T + nb, 128), 128, 0, st>>>(svals, bases, bstart, bend, L0.toff,
+                                                                            L0.offA, nb, T, L0.itemsA, L0.buckets,
+                                                                            d_boff, P.nbm);
+    TC_LAUNCHED(ctx);
+    if (ctx->prof) TC_CUDA(ctx, cudaEventRecord(ctx->ev[1], st));
+    return TC_OK;
+  };
   // counting-sort layout: count, scan, scatter (no keys stored, no radix passes)
   uint32_t *cnt, *cursor;
   static const uint32_t NC_ENV = getenv("TC_MSM_NC") ? (uint32_t)atoi(getenv("TC_MSM_NC")) : 16u;   // sweep: 1 9.04, 4 7.79, 8 7.53, 16 7.40, 32 7.37 ms
@@ -1530,7 +1590,20 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
       pass(true, l0, std::min<uint32_t>(LG, (uint32_t)L - l0));
       TC_LAUNCHED(ctx);
     }
-    TC_CUDA(ctx, cudaStreamSynchronize(st));
+    svals = vals;
+    bend = bstart + 1;
+    static const bool no_early = getenv("TC_MSM_NO_EARLY0") != nullptr;
+    if (!no_early && n * (uint64_t)L < (1ull << 31)) {   // every element at most one entry (modes 1 / 3)
+      // the host waits for the entry count / largest bucket (an event after the scatter),
+      // NOT for the accumulation queued behind it
+      if (!ctx->ev_mid) TC_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_mid, cudaEventDisableTiming));
+      TC_CUDA(ctx, cudaEventRecord(ctx->ev_mid, st));
+      TC_TRY(level0((uint64_t)L * n));
+      early0 = true;
+      TC_CUDA(ctx, cudaEventSynchronize(ctx->ev_mid));
+    } else {
+      TC_CUDA(ctx, cudaStreamSynchronize(st));
+    }
     E = h_small[0];
     maxb = h_small[1];
     if (spec_tab) TC_TRY(quantize_flags_to_status(ctx, h_small[2]));
@@ -1646,64 +1719,25 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   svals = vals;
   bend = bstart + 1;
 
-  // 6. levels (a bucket holds <= n entries)
-  static const uint32_t T_ENV = getenv("TC_MSM_T") ? (uint32_t)atoi(getenv("TC_MSM_T")) : 16u;   // sweep (config 3): 8 6.75, 12 6.66, 16 6.54, 24 6.60, 32 6.64 ms
-  static const uint32_t T1_ENV = getenv("TC_MSM_T1") ? (uint32_t)atoi(getenv("TC_MSM_T1")) : 8u;
-  // piece length: 16 entries balances config 3 (~114 entries per bucket); dense buckets
-  // (config 5: ~2300 per bucket) take longer pieces (fewer items for the tail levels:
-  // 6-layer batch 22.0 -> 21.5 ms at 64)
-  uint32_t T = (E >= (1u << 20)) ? T_ENV : (E >= (1u << 14) ? 16u : 8u);
-  // exponent-table plan (mode 3, ~1000 entries per bucket): pieces of 32 with 16 items per
-  // reduction thread (A/B over 40 forwards: T 64 / T1 8 -> 4.479 ms per step, 32 / 16 ->
-  // 4.463, 24 / 8 -> 4.480; shorter pieces shorten the accumulation's last wave, the
-  // wider reduction keeps the item levels at two)
-  const bool m3 = P.mode == 3 && !getenv("TC_MSM_T") && !getenv("TC_MSM_T1");
-  if (!getenv("TC_MSM_T") && E >= (1u << 20)) {
-    const uint64_t per_bucket = E / std::max<uint64_t>(1, nb);
-    // smaller batches (a multi-GPU rank's few layers) have fewer waves: shorter pieces still
-    // (4 layers: 0.706 -> 0.686 ms per pipelined forward at 16; 32 layers: 16 is slower)
-    const uint32_t tmax = m3 ? (E < TC_M3_SMALL_E ? 16u : 32u) : 64u;
-    while (T < tmax && (uint64_t)T * 16 <= per_bucket) T *= 2;
-  }
-  const uint32_t T1 = (m3 && T >= 16) ? 16u : T1_ENV;
-  int levels = 1;   // enough for the largest bucket (<= n entries when its size is unknown)
-  for (uint64_t capT = T; capT < (have_maxb ? (uint64_t)maxb : n); capT *= T1) levels++;
-  // items = pieces of multi-piece buckets: ceil(sz/T) <= 2 sz / T for sz > T
-  const uint64_t max_items = 2 * ((E + T - 1) / T) + 2;
-  uint32_t *np, *npm, *toff, *offA, *offB;
-  Ext *itemsA, *itemsB, *buckets;
-  TC_TRY(scratch_t(ctx, "msm.np", (uint64_t)nb + 1, &np));
-  TC_TRY(scratch_t(ctx, "msm.npm", (uint64_t)nb + 1, &npm));
-  TC_TRY(scratch_t(ctx, "msm.toff", (uint64_t)nb + 1, &toff));
-  TC_TRY(scratch_t(ctx, "msm.offA", (uint64_t)nb + 1, &offA));
-  TC_TRY(scratch_t(ctx, "msm.offB", (uint64_t)nb + 1, &offB));
-  TC_TRY(scratch_t(ctx, "msm.itemsA", max_items, &itemsA));
-  TC_TRY(scratch_t(ctx, "msm.itemsB", max_items, &itemsB));
-  TC_TRY(scratch_t(ctx, "msm.buckets", nb, &buckets));
-  size_t scan_bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, np, toff, (int)(nb + 1), st);
-  void* d_scan;
-  TC_TRY(scratch(ctx, "msm.scantmp", scan_bytes, &d_scan));
-
-  k_count0<<<blocks_for((uint64_t)nb + 1, 256), 256, 0, st>>>(bstart, bend, nb, T, np, npm, buckets);
-  TC_LAUNCHED(ctx);
-  TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(d_scan, scan_bytes, np, toff, (int)(nb + 1), st));
-  TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(d_scan, scan_bytes, npm, offA, (int)(nb + 1), st));
-  ctx->launches += 4;
-  if (ctx->prof) TC_CUDA(ctx, cudaEventRecord(ctx->ev[0], st));
-  k_accum_aff<<<blocks_for((E + T - 1) / T + nb, 128), 128, 0, st>>>(svals, bases, bstart, bend, toff, offA, nb, T,
-                                                                       itemsA, buckets, d_boff, P.nbm);
-  TC_LAUNCHED(ctx);
+  // 6. levels (a bucket holds <= n entries); level 0 may already be queued (early0)
+  if (!early0) TC_TRY(level0(E));
   if (ctx->prof) {
-    TC_CUDA(ctx, cudaEventRecord(ctx->ev[1], st));
     TC_CUDA(ctx, cudaEventSynchronize(ctx->ev[1]));
     float ms = 0;
     TC_CUDA(ctx, cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]));
-    auto& s = ctx->stats["msm.accumulate"];
-    s.ms += ms;
-    s.launches += 1;
-    s.units += (double)E;   // bucket entries accumulated
+    auto& st_ = ctx->stats["msm.accumulate"];
+    st_.ms += ms;
+    st_.launches += 1;
+    st_.units += (double)E;   // bucket entries accumulated
   }
+  int levels = 1;   // enough for the largest bucket (<= n entries when its size is unknown)
+  for (uint64_t capT = L0.T; capT < (have_maxb ? (uint64_t)maxb : n); capT *= L0.T1) levels++;
+  const uint32_t T1 = L0.T1;
+  const uint64_t max_items = L0.max_items;
+  uint32_t *np = L0.np, *npm = L0.npm, *toff = L0.toff, *offA = L0.offA, *offB = L0.offB;
+  Ext *itemsA = L0.itemsA, *itemsB = L0.itemsB, *buckets = L0.buckets;
+  void* d_scan = L0.d_scan;
+  size_t scan_bytes = L0.scan_bytes;
   uint64_t items_bound = max_items;
   for (int lv = 1; lv < levels; lv++) {
     k_count<<<blocks_for((uint64_t)nb + 1, 256), 256, 0, st>>>(offA, nb, T1, np, npm);

@@ -39,6 +39,7 @@ struct tc_ctx {
   };
   std::map<std::string, Stat> stats;
   cudaEvent_t ev[2] = {nullptr, nullptr};
+  cudaEvent_t ev_mid = nullptr;   // MSM pipeline: entry counts read back (host waits on it)
   // host-input pipeline (tc_commit_batch_host): a copy stream and one event per group
   cudaStream_t copy_stream = nullptr;
   std::vector<cudaEvent_t> copy_ev;
