@@ -23,6 +23,7 @@ all-gathered so every rank holds every proof (open_many_dist).
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 ELEM_BYTES = 43
 
@@ -128,7 +129,10 @@ class DistProver:
         self.ctxs = [Context.pipeline(srs.device, k) for k in range(max(1, depth))]
         self.dev = torch.device("cuda", srs.device)
         self.rows = torch.tensor(rows, dtype=torch.long, device=self.dev)
-        backend = dist.get_backend(group) if world > 1 else "nccl"
+        # TC_DIST_FORCE_GATHER=1: run the all-gather even for one rank (tests the NCCL call
+        # and its stream ordering on a single GPU)
+        self.force_gather = os.environ.get("TC_DIST_FORCE_GATHER", "0") not in ("", "0") and dist.is_initialized()
+        backend = dist.get_backend(group) if (world > 1 or self.force_gather) else "nccl"
         self.device_gather = backend == "nccl"
         self._k = 0
 
@@ -161,7 +165,7 @@ class DistProver:
                     ctx.check(_lib.lib().tc_commit_points_launch(ctx.handle, self.srs.handle, arr, len(conv),
                                                                  conv[0][1], self.scale_bits, _route(self.route),
                                                                  buf.data_ptr()), "tc_commit_points_launch")
-                if self.world > 1:
+                if self.world > 1 or self.force_gather:
                     gathered = _gather_rows(buf, self.world, self.group, self.device_gather)
                     allp = gathered.index_select(0, self.rows)
                 else:

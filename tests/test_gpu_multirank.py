@@ -80,3 +80,41 @@ def test_bench_config4_two_ranks():
     assert out.returncode == 0, out.stderr[-3000:]
     line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["value"] > 0
+
+
+_NCCL1 = r'''
+import os, sys, json
+sys.path.insert(0, os.environ["TC_ROOT"])
+import numpy as np, torch, torch.distributed as dist
+import paper_2602_12630_b200 as tcb
+from paper_2602_12630_b200.dist import prover_commit_pipeline_dist
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+g = np.random.default_rng(3)
+host = [(g.standard_t(3, 1024) * (1 + l)).astype(np.float16) for l in range(7)]
+layers = {l: torch.from_numpy(h).cuda() for l, h in enumerate(host)}
+srs, _ = tcb.setup_srs((8, 8, 16), b"dist-test")
+roots = [r.to_bytes().hex() for _, r, _ in prover_commit_pipeline_dist([layers] * 4, srs, 7, 0, 1, depth=3)]
+print(json.dumps({"roots": roots}))
+dist.destroy_process_group()
+'''
+
+
+def test_nccl_device_gather_one_rank():
+    """The NCCL all-gather of the part encodings (device buffers, issued on the pipeline
+    context's stream) on a one-rank NCCL group, forced on: four pipelined forwards give the
+    single-process root."""
+    env = dict(os.environ, TC_DIST_FORCE_GATHER="1", TC_ROOT=ROOT)
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+                          "--master-addr=127.0.0.1", "--master-port=29539", "--no-python",
+                          sys.executable, "-c", _NCCL1], capture_output=True, text=True, env=env, timeout=600,
+                         cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    roots = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])["roots"]
+    import numpy as np
+    import paper_2602_12630_b200 as tcb
+    g = np.random.default_rng(3)
+    host = [(g.standard_t(3, 1024) * (1 + l)).astype(np.float16) for l in range(7)]
+    srs, _ = tcb.setup_srs((8, 8, 16), b"dist-test")
+    _, root = tcb.prover_commit([torch.from_numpy(h).cuda() for h in host], srs)
+    assert roots == [root.to_bytes().hex()] * 4
