@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <set>
@@ -188,8 +189,11 @@ int srs_exp_table(tc_ctx* ctx, tc_srs* srs, const tc::EdPk* bases, uint64_t n, i
 // small ones, whose MSMs are latency-bound: their one bucket window then fits the
 // single-launch block weighting
 constexpr int FB_C_LARGE = 15, FB_C_SMALL = 11;
-constexpr uint64_t FB_SMALL_N = 1ull << 18;
-inline int fb_width(uint64_t n) { return n >= FB_SMALL_N ? FB_C_LARGE : FB_C_SMALL; }
+constexpr uint64_t FB_SMALL_N = 1ull << 16;   // config 4 (65536-point quotient ranges): 2^18 -> 119.8 ms, 2^16 -> 118.2 ms
+inline int fb_width(uint64_t n) {
+  static const uint64_t small_n = getenv("TC_FB_SMALL_N") ? strtoull(getenv("TC_FB_SMALL_N"), nullptr, 10) : FB_SMALL_N;
+  return n >= small_n ? FB_C_LARGE : FB_C_SMALL;
+}
 inline int fb_ndig(int c) { return (163 + c - 1) / c; }
 // the window table of the n bases starting at `bases` (fb_ndig(c) * n points, c = fb_width(n)),
 // built once per SRS range
