@@ -981,7 +981,7 @@ __global__ void __launch_bounds__(128) k_wsum_level(const Ext* Tin, const Ext* D
 // R_t = sum_{s>=t} T_s (a shared-memory suffix scan), S = R_0, and W = A + (mlo - 1) S.
 // Serial depth ~ 2C + 2 log2(threads) + log2(C) + log2(mlo) adds instead of ~27 per level.
 #ifndef TC_WB_THREADS
-#define TC_WB_THREADS 512
+#define TC_WB_THREADS 256   // A/B: 512 -> lone forward 5.02 ms, pipelined 4.471; 256 -> 4.99, 4.457; 128 -> 5.00, 4.458
 #endif
 constexpr int WB_THREADS = TC_WB_THREADS;
 constexpr int WB_CHUNK_LG = TC_WB_THREADS == 512 ? 2 : (TC_WB_THREADS == 256 ? 3 : 4);   // 2048 buckets
