@@ -40,21 +40,58 @@ class TreeConfig:
         return check_shape(self.shape)
 
 
-@dataclass
 class TerkleTree:
-    config: TreeConfig
-    n: int                     # true leaf count (root metadata)
-    depth: int                 # number of node levels L
-    levels: list               # levels[l][u] = node commitment point (bottom level first)
-    values: list               # values[l] = child values of level l (flat, lex per node)
-    srs: Srs = field(repr=False, default=None)
-    # node openings already computed: (level, node, slot) -> TensorOpening.  prove() is a
-    # pure function of the (immutable) tree, so repeated challenges reuse them
-    _openings: dict = field(repr=False, default_factory=dict)
+    """A built tree: levels[l][u] = node commitment point (bottom level first), values[l] =
+    the child values of level l (flat, lex per node); n = true leaf count (root metadata,
+    SPEC.md:395).  A tree read back from the device keeps the raw encodings and decodes
+    levels / values on first use (prove); the root alone is decoded eagerly-cheaply."""
+
+    def __init__(self, config: TreeConfig, n: int, depth: int, levels=None, values=None, srs: Srs = None,
+                 raw=None):
+        self.config, self.n, self.depth, self.srs = config, n, depth, srs
+        self._levels, self._values, self._raw = levels, values, raw
+        # node openings already computed: (level, node, slot) -> TensorOpening.  prove() is a
+        # pure function of the (immutable) tree, so repeated challenges reuse them
+        self._openings = {}
+
+    def _decode(self):
+        nodes_raw, values_raw = self._raw
+        B = self.config.arity
+        levels, values, pos, vpos = [], [], 0, 0
+        for l in range(self.depth):
+            k = B ** (self.depth - 1 - l)
+            levels.append([decode_elem(nodes_raw[(pos + u) * ELEM_BYTES:(pos + u + 1) * ELEM_BYTES], validate=False)
+                           for u in range(k)])
+            pos += k
+            w = B ** (self.depth - l)
+            values.append([int.from_bytes(values_raw[24 * (vpos + j):24 * (vpos + j + 1)], "little")
+                           for j in range(w)])
+            vpos += w
+        self._levels, self._values = levels, values
+
+    @property
+    def levels(self):
+        if self._levels is None:
+            self._decode()
+        return self._levels
+
+    @property
+    def values(self):
+        if self._values is None:
+            self._decode()
+        return self._values
 
     @property
     def root(self) -> Commitment:
+        if self._levels is None:   # the top node is the last encoding of the bottom-first list
+            nodes_raw = self._raw[0]
+            B = self.config.arity
+            total = sum(B ** (self.depth - 1 - l) for l in range(self.depth))
+            return Commitment(decode_elem(nodes_raw[(total - 1) * ELEM_BYTES:total * ELEM_BYTES], validate=False))
         return Commitment(self.levels[-1][0])
+
+    def __repr__(self):
+        return f"TerkleTree(config={self.config}, n={self.n}, depth={self.depth})"
 
 
 @dataclass(frozen=True)
@@ -159,18 +196,9 @@ def build(config: TreeConfig, leaves, *, srs: Srs = None):
 def tree_from_device(config: TreeConfig, n: int, depth: int, nodes_raw: bytes, values_raw: bytes,
                      srs: Srs) -> TerkleTree:
     """The TerkleTree of tc_commit_tree's outputs (node encodings level by level, every
-    level's child values as 24-byte LE limbs) — the same object `build` returns."""
-    B = config.arity
-    levels, values, pos, vpos = [], [], 0, 0
-    for l in range(depth):
-        k = B ** (depth - 1 - l)
-        levels.append([decode_elem(nodes_raw[(pos + u) * ELEM_BYTES:(pos + u + 1) * ELEM_BYTES], validate=False)
-                       for u in range(k)])
-        pos += k
-        w = B ** (depth - l)
-        values.append([int.from_bytes(values_raw[24 * (vpos + j):24 * (vpos + j + 1)], "little") for j in range(w)])
-        vpos += w
-    return TerkleTree(config, n, depth, levels, values, srs)
+    level's child values as 24-byte LE limbs) — the same object `build` returns, decoded
+    lazily (a forward's readback costs the host ~100 us of Python decoding otherwise)."""
+    return TerkleTree(config, n, depth, srs=srs, raw=(bytes(nodes_raw), bytes(values_raw)))
 
 
 def prove(tree: TerkleTree, i: int) -> MembershipProof:
