@@ -799,11 +799,18 @@ __global__ void k_fpb_starts(uint32_t* __restrict__ cnt, uint32_t nbm, uint32_t 
 // level 0 piece counts: np[k] = ceil(size/T) (threads), npm[k] = np[k] if > 1 (items);
 // an empty bucket is set to the neutral element here (every other bucket is written by
 // the accumulation levels), so the bucket array needs no separate fill pass
-__global__ void k_count0(const uint32_t* bstart, const uint32_t* bend, uint32_t nb, uint32_t T, uint32_t* np,
-                         uint32_t* npm, Ext* buckets) {
+// buckets from `tail` on take pieces of Ts entries (the accumulation dispatches them last:
+// short pieces there shorten its final wave)
+__device__ __forceinline__ uint32_t piece_len(uint32_t k, uint32_t T, uint32_t tail, uint32_t Ts) {
+  return k >= tail ? Ts : T;
+}
+
+__global__ void k_count0(const uint32_t* bstart, const uint32_t* bend, uint32_t nb, uint32_t T, uint32_t tail,
+                         uint32_t Ts, uint32_t* np, uint32_t* npm, Ext* buckets) {
   uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k > nb) return;
-  uint32_t c = (k == nb) ? 0u : (bend[k] - bstart[k] + T - 1) / T;
+  const uint32_t Tk = piece_len(k, T, tail, Ts);
+  uint32_t c = (k == nb) ? 0u : (bend[k] - bstart[k] + Tk - 1) / Tk;
   np[k] = c;
   npm[k] = c > 1 ? c : 0u;
   if (k < nb && c == 0) buckets[k] = ext_zero();
@@ -845,16 +852,17 @@ __device__ __forceinline__ uint32_t find_bucket(const uint32_t* off, uint32_t nb
 #endif
 __global__ void __launch_bounds__(128, TC_ACCUM_MINB) k_accum_aff(const uint32_t* vals, const EdPk* bases, const uint32_t* bstart,
                                                    const uint32_t* bend, const uint32_t* toff, const uint32_t* ooff,
-                                                   uint32_t nb, uint32_t T, Ext* items, Ext* buckets,
-                                                   const uint32_t* boff, uint32_t nbm) {
+                                                   uint32_t nb, uint32_t T, uint32_t tail, uint32_t Ts,
+                                                   Ext* items, Ext* buckets, const uint32_t* boff, uint32_t nbm) {
   uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t total = toff[nb];
   if (p >= total) return;
   uint32_t k = find_bucket(toff, nb, p);
   if (boff) bases += boff[k / nbm];   // multi-base batch: MSM l reads bases + boff[l]
   uint32_t piece = p - toff[k];
-  uint32_t a = bstart[k] + piece * T;
-  uint32_t b = min(a + T, bend[k]);
+  const uint32_t Tk = piece_len(k, T, tail, Ts);
+  uint32_t a = bstart[k] + piece * Tk;
+  uint32_t b = min(a + Tk, bend[k]);
   uint32_t v = vals[a];
   EdAff q = ld_edpk(bases + (v & ~SIGN_BIT));
   if (v & SIGN_BIT) q = edaff_neg(q);
@@ -1434,7 +1442,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   // device-side piece count); the block-counter path queues it BEFORE the host waits for
   // the entry count, so the GPU goes from the scatter straight into the accumulation
   struct Level0 {
-    uint32_t T = 0, T1 = 0;
+    uint32_t T = 0, T1 = 0, tail = 0, Ts = 0, Tmin = 0;
     uint64_t max_items = 0;
     uint32_t *np, *npm, *toff, *offA, *offB;
     Ext *itemsA, *itemsB, *buckets;
@@ -1464,7 +1472,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     L0.T = T;
     L0.T1 = (m3 && T >= 16) ? 16u : T1_ENV;
     // items = pieces of multi-piece buckets: ceil(sz/T) <= 2 sz / T for sz > T
-    L0.max_items = 2 * ((E_plan + T - 1) / T) + 2;
+    L0.max_items = 2 * ((E_plan + std::max<uint32_t>(4u, T / 4) - 1) / std::max<uint32_t>(4u, T / 4)) + 2;
     TC_TRY(scratch_t(ctx, "msm.np", (uint64_t)nb + 1, &L0.np));
     TC_TRY(scratch_t(ctx, "msm.npm", (uint64_t)nb + 1, &L0.npm));
     TC_TRY(scratch_t(ctx, "msm.toff", (uint64_t)nb + 1, &L0.toff));
@@ -1476,15 +1484,27 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     L0.scan_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, L0.scan_bytes, L0.np, L0.toff, (int)(nb + 1), st);
     TC_TRY(scratch(ctx, "msm.scantmp", L0.scan_bytes, &L0.d_scan));
-    k_count0<<<blocks_for((uint64_t)nb + 1, 256), 256, 0, st>>>(bstart, bend, nb, T, L0.np, L0.npm, L0.buckets);
+    // the last TC_MSM_TAIL_PCT % of the buckets take quarter-length pieces (off by default:
+    // config 3, 3 % -> 4.496 ms per step vs 4.457 — the accumulation's last wave shrinks by
+    // 25 us but the short pieces need one more reduction level)
+    static const uint32_t TAIL_PCT = getenv("TC_MSM_TAIL_PCT") ? (uint32_t)atoi(getenv("TC_MSM_TAIL_PCT")) : 0u;
+    const uint32_t tail = TAIL_PCT ? (uint32_t)((uint64_t)nb * (100 - std::min(TAIL_PCT, 100u)) / 100) : nb;
+    const uint32_t Ts = std::max<uint32_t>(4u, T / 4);
+    L0.tail = tail;
+    L0.Ts = Ts;
+    k_count0<<<blocks_for((uint64_t)nb + 1, 256), 256, 0, st>>>(bstart, bend, nb, T, tail, Ts, L0.np, L0.npm,
+                                                                L0.buckets);
     TC_LAUNCHED(ctx);
     TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(L0.d_scan, L0.scan_bytes, L0.np, L0.toff, (int)(nb + 1), st));
     TC_CUDA(ctx, cub::DeviceScan::ExclusiveSum(L0.d_scan, L0.scan_bytes, L0.npm, L0.offA, (int)(nb + 1), st));
     ctx->launches += 4;
     if (ctx->prof) TC_CUDA(ctx, cudaEventRecord(ctx->ev[0], st));
-    k_accum_aff<<<blocks_for((E_plan + T - 1) / T + nb, 128), 128, 0, st>>>(svals, bases, bstart, bend, L0.toff,
-                                                                            L0.offA, nb, T, L0.itemsA, L0.buckets,
-                                                                            d_boff, P.nbm);
+    // pieces <= sum_k ceil(size_k / T_k) <= E / min(T_k) + nb; surplus threads exit
+    const uint32_t Tmin = tail < nb ? Ts : T;
+    L0.Tmin = Tmin;
+    k_accum_aff<<<blocks_for((E_plan + Tmin - 1) / Tmin + nb, 128), 128, 0, st>>>(svals, bases, bstart, bend, L0.toff,
+                                                                              L0.offA, nb, T, tail, Ts, L0.itemsA,
+                                                                              L0.buckets, d_boff, P.nbm);
     TC_LAUNCHED(ctx);
     if (ctx->prof) TC_CUDA(ctx, cudaEventRecord(ctx->ev[1], st));
     return TC_OK;
@@ -1731,7 +1751,8 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     st_.units += (double)E;   // bucket entries accumulated
   }
   int levels = 1;   // enough for the largest bucket (<= n entries when its size is unknown)
-  for (uint64_t capT = L0.T; capT < (have_maxb ? (uint64_t)maxb : n); capT *= L0.T1) levels++;
+  // the shortest pieces (tail buckets) leave the most items per bucket
+  for (uint64_t capT = L0.Tmin; capT < (have_maxb ? (uint64_t)maxb : n); capT *= L0.T1) levels++;
   const uint32_t T1 = L0.T1;
   const uint64_t max_items = L0.max_items;
   uint32_t *np = L0.np, *npm = L0.npm, *toff = L0.toff, *offA = L0.offA, *offB = L0.offB;

@@ -545,7 +545,9 @@ print("ok")
 
 @pytest.mark.parametrize("env", [{}, {"TC_MSM_NO_SORTED_SCATTER": "1"}, {"TC_MSM_FPB_LG": "1"}, {"TC_MSM_FPB_LG": "3"},
                                  {"TC_MSM_NO_EXPTAB": "1"}, {"TC_EXPTAB_GB": "0"},
-                                 {"TC_MSM_NO_EXPTAB": "1", "TC_MSM_FPB_LG": "3"}, {"TC_MSM_NO_BLKCNT": "1"}])
+                                 {"TC_MSM_NO_EXPTAB": "1", "TC_MSM_FPB_LG": "3"}, {"TC_MSM_NO_BLKCNT": "1"},
+                                 {"TC_MSM_TAIL_PCT": "40"}, {"TC_MSM_NO_EARLY0": "1"}, {"TC_NO_KTAB": "1"},
+                                 {"TC_MSM_T": "8", "TC_MSM_T1": "4"}])
 def test_msm_counting_sort_paths(env, tmp_path):
     """Every fp16 commit plan and counting sort gives commitments equal to the trapdoor oracle
     on a batch of six 65536-element fp16 tensors (tiny, large, all-zero, sparse, max /
