@@ -627,14 +627,17 @@ def run_openings(args, dev, rank, world, cores):
     import torch.distributed as dist
 
     import paper_2602_12630_b200 as tcb
-    from paper_2602_12630_b200.dist import open_many_dist, opening_partition, prover_commit_dist, work_partition
+    from paper_2602_12630_b200.dist import hot_layer_plan, open_many_dist, prover_commit_dist, work_partition
     cfg = CONFIGS[3]
     n_layers = cfg["layers"]
     chals = config4_challenges(n_layers, cfg["shape"], tcb.P)
-    mine = opening_partition([l for l, _ in chals], world)[rank]
+    hot, _, assign = hot_layer_plan([l for l, _ in chals], world, cfg["shape"][0], len(cfg["shape"]))
+    mine = assign[rank] if world > 1 else list(range(len(chals)))
     n_elems = int(__import__("numpy").prod(cfg["act"]))
-    # this rank's challenged layers and the layers of its commitment share (dist.py)
-    need = sorted({chals[i][0] for i in mine} | {l for l, _, _ in work_partition(n_layers, n_elems, world)[rank]})
+    # this rank's challenged layers, the hot layers (every rank computes rows of their slice
+    # commitments) and the layers of its commitment share (dist.py)
+    need = sorted({chals[i][0] for i in mine} | (set(hot) if world > 1 else set())
+                  | {l for l, _, _ in work_partition(n_layers, n_elems, world)[rank]})
     host = dict(zip(need, make_layers_host(cfg, need)))
     layers = {l: torch.from_numpy(h).to(dev) for l, h in host.items()}
     srs, _ = tcb.setup_srs(cfg["shape"], b"tc-b200/config3", device=dev.index)
@@ -673,10 +676,12 @@ def run_openings(args, dev, rank, world, cores):
                           "ms_per_opening": ms / len(chals), "ms_total": ms, "higher_is_better": True,
                           "config": {"workload": "config4: 256 challenges on the config-3 tree, layers drawn by a "
                                                  "seeded Pareto score vector, random field points",
-                                     "parallelism": f"openings/{world} (cost-balanced, hot layers split)",
-                                     "path": "dist.open_many_dist -> tc_open_many (layers opened >= 6 times: slice "
-                                             "commitments H[c',c] once per layer and rank, pi_0 as a d0^2-point MSM; "
-                                             "others: grouped quotient MSMs) + prove_many (node openings batched)"}}),
+                                     "parallelism": f"openings/{world} (hot layers' slice commitments split by rows over "
+                                                    "the ranks + one all-gather; openings dealt out by cost)",
+                                     "path": "dist.open_many_dist -> tc_open_slices (rank's rows of H[c',c]) + all-gather "
+                                             "+ tc_open_batch_sliced (pi_0 as a d0^2-point MSM over H) for layers opened "
+                                             ">= 6 times, tc_open_many (grouped quotient MSMs) for the others; "
+                                             "prove_many (node openings batched)"}}),
               flush=True)
 
 

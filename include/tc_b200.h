@@ -186,6 +186,19 @@ int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int 
                   int scale_bits, const uint8_t* omegas_le21, int route, uint8_t* out_y21,
                   uint8_t* out_pi43);
 
+/* Slice commitments of the opening route for often-challenged tensors (config 4), split so
+ * several GPUs can share them: H[c', c] = sum_rest T[c', rest] L_{c, rest} for the tensor
+ * slices c' in [row_lo, row_hi) over every SRS slice c of the first axis (d0 each), written
+ * as (row_hi - row_lo) x d0 43-byte encodings into the DEVICE buffer d_out43.  Once the d0 x
+ * d0 encodings are assembled (e.g. all-gathered), tc_open_batch_sliced opens `count` points
+ * of that one tensor from them (pi_0 as a d0^2-point MSM, the other quotients as usual);
+ * same bytes as tc_open. */
+int tc_open_slices(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int scale_bits,
+                   uint32_t row_lo, uint32_t row_hi, uint8_t* d_out43);
+int tc_open_batch_sliced(tc_ctx* ctx, const tc_srs* srs, const void* d_in, const uint8_t* d_h43,
+                         int count, int dtype, int scale_bits, const uint8_t* omegas_le21,
+                         uint8_t* out_y21, uint8_t* out_pi43);
+
 /* Commitments of `count` device tensors AND their Terkle tree in one call, all on the device
  * (protocol.prover_commit): the batched commit, the leaves
  * hash_to_scalar(encode_elem(C_l), b"terkle/leaf") hashed on the device, the tree levels

@@ -76,6 +76,8 @@ _SIGS = [
     ("tc_commit_stream_reset", C.c_int, [_P]),
     ("tc_open", C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_char_p, C.c_int, _P, _P]),
     ("tc_open_batch", C.c_int, [_P, _P, C.POINTER(_P), C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_int, _P, _P]),
+    ("tc_open_slices", C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_uint32, C.c_uint32, _P]),
+    ("tc_open_batch_sliced", C.c_int, [_P, _P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_char_p, _P, _P]),
     ("tc_terkle_build", C.c_int, [_P, _P, C.c_char_p, C.c_uint64, _P, C.POINTER(C.c_uint64)]),
     ("tc_commit_tree", C.c_int, [_P, _P, C.POINTER(_P), C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, _P,
                                  C.POINTER(C.c_uint64), _P, C.POINTER(C.c_uint64)]),

@@ -1449,8 +1449,66 @@ int tc_open(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int sca
 //    (the axis-0 quotient q_0(a) = (T[a] - sum_c' L_c'(omega_0) T[c', a_rest]) / (a_0 + 1
 //    - omega_0), regrouped) — a d_0^2-point MSM per opening instead of an N-point one.
 // route = monomial goes through tc_open (interpolation + monomial SRS) per opening.
+// H[c', c] for the tensor slices c' in [row_lo, row_hi) over every SRS slice c (the
+// slice-commitment route's d0 x d0 MSMs of n / d0 points, multi-base batch) into out
+static int slice_commitments(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int scale_bits,
+                             uint32_t row_lo, uint32_t row_hi, Aff* out) {
+  const EdPk* ed_lag;
+  TC_TRY(tcrt::srs_edwards(ctx, const_cast<tc_srs*>(srs), TC_SRS_LAGRANGE, &ed_lag));
+  size_t esz = 0;
+  if (dtype_size(dtype, &esz)) return fail(ctx, TC_ERR_ARGUMENT, "open: unsupported dtype %d", dtype);
+  const uint32_t d0 = srs->shape[0];
+  const uint64_t R = srs->n / d0;
+  const uint32_t nh = (row_hi - row_lo) * d0;
+  if (nh == 0) return TC_OK;
+  std::vector<const void*> hp(nh);
+  std::vector<uint32_t> boff(nh);
+  for (uint32_t cp = row_lo; cp < row_hi; cp++)
+    for (uint32_t c = 0; c < d0; c++) {
+      hp[(cp - row_lo) * d0 + c] = (const uint8_t*)d_in + esz * R * cp;
+      boff[(cp - row_lo) * d0 + c] = (uint32_t)(R * c);
+    }
+  return tcrt::msm_batch_device(ctx, dtype, scale_bits, hp.data(), (int)nh, ed_lag, R, out, boff.data(), 0,
+                                const_cast<tc_srs*>(srs));
+}
+
+static int open_batch_impl(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype,
+                           int scale_bits, const uint8_t* omegas_le21, int route, uint8_t* out_y21,
+                           uint8_t* out_pi43, const uint8_t* d_h43);
+
 int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype, int scale_bits,
                   const uint8_t* omegas_le21, int route, uint8_t* out_y21, uint8_t* out_pi43) {
+  return open_batch_impl(ctx, srs, d_ins, count, dtype, scale_bits, omegas_le21, route, out_y21, out_pi43, nullptr);
+}
+
+int tc_open_slices(tc_ctx* ctx, const tc_srs* srs, const void* d_in, int dtype, int scale_bits, uint32_t row_lo,
+                   uint32_t row_hi, uint8_t* d_out43) {
+  if (!ctx || !srs || !d_in || row_lo > row_hi || (row_hi > row_lo && !d_out43)) return TC_ERR_ARGUMENT;
+  if (srs->m < 2 || !srs->lagrange) return fail(ctx, TC_ERR_VALUE, "slice commitments need m >= 2 and a Lagrange SRS");
+  if (row_hi > srs->shape[0]) return fail(ctx, TC_ERR_INDEX, "slice rows beyond the first axis");
+  const uint32_t nh = (row_hi - row_lo) * srs->shape[0];
+  if (nh == 0) return TC_OK;
+  Aff* pts;
+  TC_TRY(tcrt::scratch_t(ctx, "opens.pts", (uint64_t)nh, &pts));
+  TC_TRY(slice_commitments(ctx, srs, d_in, dtype, scale_bits, row_lo, row_hi, pts));
+  k_encode43<<<tcrt::blocks_for(nh, 64), 64, 0, ctx->stream>>>(pts, nh, d_out43);
+  TC_LAUNCHED(ctx);
+  return TC_OK;
+}
+
+int tc_open_batch_sliced(tc_ctx* ctx, const tc_srs* srs, const void* d_in, const uint8_t* d_h43, int count,
+                         int dtype, int scale_bits, const uint8_t* omegas_le21, uint8_t* out_y21, uint8_t* out_pi43) {
+  if (!ctx || !srs || !d_in || !d_h43 || count < 0) return TC_ERR_ARGUMENT;
+  if (srs->m < 2 || !srs->lagrange || !srs->sublag)
+    return fail(ctx, TC_ERR_VALUE, "sliced openings need m >= 2 and the Lagrange / sub-grid sets");
+  std::vector<const void*> ins((size_t)count, d_in);
+  return open_batch_impl(ctx, srs, ins.data(), count, dtype, scale_bits, omegas_le21, TC_ROUTE_LAGRANGE, out_y21,
+                         out_pi43, d_h43);
+}
+
+static int open_batch_impl(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype,
+                           int scale_bits, const uint8_t* omegas_le21, int route, uint8_t* out_y21,
+                           uint8_t* out_pi43, const uint8_t* d_h43) {
   if (!ctx || !srs || (count && (!d_ins || !omegas_le21 || !out_y21 || !out_pi43)) || count < 0)
     return TC_ERR_ARGUMENT;
   const uint64_t n = srs->n;
@@ -1520,7 +1578,6 @@ int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int 
   // split: tensors opened often enough take the slice-commitment route
   static const int PMIN = getenv("TC_OPEN_PRECOMP_MIN") ? atoi(getenv("TC_OPEN_PRECOMP_MIN")) : 6;
   const uint32_t d0 = srs->shape[0];
-  const uint64_t R = n / d0;
   std::map<const void*, std::vector<int>> by_tensor;
   for (int i : lag) by_tensor[d_ins[i]].push_back(i);
   std::vector<std::vector<int>> jobs;   // each job: openings sharing one strategy (+ tensor)
@@ -1528,7 +1585,7 @@ int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int 
   std::vector<int> rest;
   for (int i : lag) {
     auto& v = by_tensor[d_ins[i]];
-    if (m >= 2 && PMIN > 0 && (int)v.size() >= PMIN && d0 * d0 <= 4096) {
+    if (m >= 2 && ((PMIN > 0 && (int)v.size() >= PMIN) || d_h43) && d0 * d0 <= 4096) {
       if (v.front() == i) jobs.push_back(v), job_h.push_back(d_ins[i]);
     } else {
       rest.push_back(i);
@@ -1565,15 +1622,15 @@ int tc_open_batch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int 
       TC_TRY(tcrt::scratch_t(ctx, "openh.pts", (uint64_t)nh, &hpts));
       TC_TRY(tcrt::scratch_t(ctx, "openh.ed", (uint64_t)nh, &hed));
       TC_TRY(tcrt::scratch_t(ctx, "openh.s", GO * nh, &sc));
-      std::vector<const void*> hp(nh);
-      std::vector<uint32_t> boff(nh);
-      for (uint32_t cp = 0; cp < d0; cp++)
-        for (uint32_t c = 0; c < d0; c++) {
-          hp[cp * d0 + c] = (const uint8_t*)job_h[jb] + esz * R * cp;
-          boff[cp * d0 + c] = (uint32_t)(R * c);
-        }
-      TC_TRY(tcrt::msm_batch_device(ctx, dtype, scale_bits, hp.data(), (int)nh, ed_lag, R, hpts, boff.data(), 0,
-                                    const_cast<tc_srs*>(srs)));
+      if (d_h43) {
+        // slice commitments computed elsewhere (each rank a share of the rows, all-gathered:
+        // dist.open_many_dist) — only decode them
+        TC_CUDA(ctx, cudaMemsetAsync(ctx->d_flags, 0, 4, ctx->stream));
+        k_decode43<<<tcrt::blocks_for(nh, 64), 64, 0, ctx->stream>>>(d_h43, nh, hpts, ctx->d_flags);
+        TC_LAUNCHED(ctx);
+      } else {
+        TC_TRY(slice_commitments(ctx, srs, job_h[jb], dtype, scale_bits, 0, d0, hpts));
+      }
       TC_TRY(tcrt::to_edwards_device(ctx, hpts, nh, hed));
     }
     // sliced jobs keep only the quotients of axes >= 1 (n / d0 + ... per opening), packed

@@ -15,10 +15,12 @@ every rank and for every world size (EC addition is associative; affine output i
 canonical).  Everything is stream-ordered on the context's stream: forward k+1's MSMs run
 while forward k's gather and tree complete (prover_commit_pipeline_dist).
 
-Openings (config 4).  Openings are independent: they are spread over the ranks by a cost
-model, a heavily challenged layer's openings split over several ranks (each recomputes the
-layer's slice commitments, a fraction of one opening group's cost), and the results are
-all-gathered so every rank holds every proof (open_many_dist).
+Openings (config 4).  A layer opened many times ("hot") opens from its slice commitments
+H[c', c] (d0 x d0 MSMs over the tensor's slices c' and the SRS slices c): those MSMs are
+split by rows c' over the ranks (point-chunks of the layer), ONE all-gather assembles every
+hot layer's H on every rank, and the hot openings are dealt out evenly; the other openings
+go to ranks by a cost model; the results are all-gathered so every rank holds every proof
+(open_many_dist).
 """
 from __future__ import annotations
 
@@ -238,57 +240,120 @@ def allgather_commitments(local: list, n_layers: int, rank: int, world: int, dev
 
 
 # --------------------------------------------------------------------------- openings
-def opening_partition(layer_of_chal, world: int, precomp_min: int = 6):
-    """Assign challenges (their layers, in order) to ranks.  Cost model (tc_open_many's
-    routes): a layer opened k >= precomp_min times costs its slice commitments (~3 units)
-    plus ~0.05 per opening, else ~1.4 per opening.  Layers are placed longest-first on the
-    least-loaded rank; a layer costing more than a rank's fair share is split into that many
-    opening groups (each group recomputes the slice commitments).  Returns per-rank sorted
-    lists of challenge indices."""
+def _open_sliced(srs, T, d_h43, points, scale_bits=16):
+    """Openings of ONE tensor from its assembled slice commitments (tc_open_batch_sliced)."""
+    from . import _conv, _lib
+    from .commit import TensorOpening
+    from .curve import ELEM_BYTES, decode_elems, encode_scalar
+
+    ctx = _lib.Context.get(srs.device)
+    ptr, dt, keep = _conv.device_input(T, srs.size, f"cuda:{srs.device}")
+    m = len(srs.shape)
+    om = b"".join(encode_scalar(int(w)) for pt in points for w in pt)
+    ys = C.create_string_buffer(21 * max(1, len(points)))
+    pis = C.create_string_buffer(ELEM_BYTES * m * max(1, len(points)))
+    with ctx.lock:
+        ctx.bind_stream()
+        ctx.check(_lib.lib().tc_open_batch_sliced(ctx.handle, srs.handle, ptr, d_h43.data_ptr(), len(points), dt,
+                                                  scale_bits, om, ys, pis), "tc_open_batch_sliced")
+    del keep
+    return [TensorOpening(int.from_bytes(ys.raw[21 * i:21 * (i + 1)], "little"),
+                          decode_elems(pis.raw[ELEM_BYTES * m * i:ELEM_BYTES * m * (i + 1)], m))
+            for i in range(len(points))]
+
+
+def hot_layer_plan(layer_of_chal, world: int, d0: int, m: int, precomp_min: int = 6):
+    """Multi-GPU openings: the layers opened >= precomp_min times ("hot") share their slice
+    commitments H (d0 x d0 MSMs) by ROWS — rank r computes rows [r d0 / W, (r+1) d0 / W), one
+    all-gather assembles every H on every rank — and their openings are dealt out evenly
+    (contiguous chunks per rank); the other ("cold") challenges go to ranks longest-first by
+    tc_open_many's cost model on top of that load.  Returns (hot layers, per-rank row ranges,
+    per-rank challenge indices)."""
     groups = {}
     for i, l in enumerate(layer_of_chal):
         groups.setdefault(l, []).append(i)
-
-    def cost(k):
-        return 3.0 + 0.05 * k if k >= precomp_min else 1.4 * k
-
-    total = sum(cost(len(v)) for v in groups.values())
-    fair = total / world
-    units = []
-    for ids in groups.values():
-        pieces = max(1, min(world, int(cost(len(ids)) // max(fair, 1e-9))))
-        step = -(-len(ids) // pieces)
-        for a in range(0, len(ids), step):
-            units.append(ids[a:a + step])
-    load = [0.0] * world
+    hot = sorted(l for l, ids in groups.items() if len(ids) >= precomp_min and m >= 2 and d0 * d0 <= 4096)
+    rows = [(r * d0 // world, (r + 1) * d0 // world) for r in range(world)]
     out = [[] for _ in range(world)]
-    for ids in sorted(units, key=lambda u: (-cost(len(u)), u[0])):
+    load = [0.0] * world
+    for l in hot:
+        ids = groups[l]
+        for r in range(world):
+            part = ids[r * len(ids) // world:(r + 1) * len(ids) // world]
+            out[r] += part
+            load[r] += 3.0 / world + 0.05 * len(part)
+    cold = sorted((ids for l, ids in groups.items() if l not in hot), key=lambda ids: (-len(ids), ids[0]))
+    for ids in cold:
         r = min(range(world), key=lambda j: (load[j], j))
         out[r] += ids
-        load[r] += cost(len(ids))
-    return [sorted(o) for o in out]
+        load[r] += 1.4 * len(ids)
+    return hot, rows, [sorted(o) for o in out]
 
 
-def open_many_dist(srs, layers: dict, chals, rank: int, world: int, *, group=None, tree=None, **kw):
+def open_many_dist(srs, layers: dict, chals, rank: int, world: int, *, group=None, tree=None, scale_bits: int = 16,
+                   **kw):
     """Config-4 openings over `world` ranks.  chals: list of (layer, point); layers: layer ->
-    tensor for at least the layers of this rank's challenges.  Returns (openings, proofs):
-    every challenge's TensorOpening and — with `tree` — its Terkle membership proof, on
-    every rank, in challenge order (same bytes as tc_open_many / prove_many on one GPU)."""
+    tensor for the hot layers and this rank's challenges (hot_layer_plan).  Hot layers' slice
+    commitments are split by rows over the ranks (MSM point-chunks: each row is a set of
+    d0 MSMs over one tensor slice) and all-gathered; every rank then opens its share.
+    Returns (openings, proofs): every challenge's TensorOpening and — with `tree` — its
+    Terkle membership proof, on every rank, in challenge order (same bytes as tc_open_many /
+    prove_many on one GPU)."""
+    import torch
     import torch.distributed as dist
 
+    from . import _conv, _lib
     from .authtree import MembershipProof, prove_many
     from .commit import TensorOpening, tc_open_many
 
-    mine = opening_partition([l for l, _ in chals], world)[rank]
-    ops = tc_open_many(srs, [layers[chals[i][0]] for i in mine], [chals[i][1] for i in mine], **kw) if mine else []
+    m, d0 = len(srs.shape), srs.shape[0]
+    if world == 1:
+        ops = tc_open_many(srs, [layers[l] for l, _ in chals], [pt for _, pt in chals], scale_bits=scale_bits, **kw)
+        pfs = prove_many(tree, [l for l, _ in chals]) if tree is not None else None
+        return ops, pfs
+    hot, rows, assign = hot_layer_plan([l for l, _ in chals], world, d0, m)
+    mine = assign[rank]
+    dev = torch.device("cuda", srs.device)
+    H = {}
+    if hot:
+        per = max(hi - lo for lo, hi in rows) * d0
+        buf = torch.zeros((len(hot), per, ELEM_BYTES), dtype=torch.uint8, device=dev)
+        ctx = _lib.Context.get(srs.device)
+        lo, hi = rows[rank]
+        for h, l in enumerate(hot):
+            ptr, dt, keep = _conv.device_input(layers[l], srs.size, f"cuda:{srs.device}")
+            with ctx.lock:
+                ctx.bind_stream()
+                ctx.check(_lib.lib().tc_open_slices(ctx.handle, srs.handle, ptr, dt, scale_bits, lo, hi,
+                                                    buf[h].data_ptr()), "tc_open_slices")
+            del keep
+        backend = dist.get_backend(group)
+        gathered = _gather_rows(buf.reshape(-1, ELEM_BYTES), world, group, backend == "nccl")
+        gathered = gathered.reshape(world, len(hot), per, ELEM_BYTES)
+        for h, l in enumerate(hot):
+            H[l] = torch.cat([gathered[r, h, :(rows[r][1] - rows[r][0]) * d0] for r in range(world)]).contiguous()
+    ops = {}
+    hot_mine = {}
+    cold_mine = []
+    for i in mine:
+        l = chals[i][0]
+        if l in H:
+            hot_mine.setdefault(l, []).append(i)
+        else:
+            cold_mine.append(i)
+    for l, ids in hot_mine.items():
+        for i, op in zip(ids, _open_sliced(srs, layers[l], H[l], [chals[i][1] for i in ids], scale_bits)):
+            ops[i] = op
+    if cold_mine:
+        got = tc_open_many(srs, [layers[chals[i][0]] for i in cold_mine], [chals[i][1] for i in cold_mine],
+                           scale_bits=scale_bits, **kw)
+        for i, op in zip(cold_mine, got):
+            ops[i] = op
     pfs = prove_many(tree, [chals[i][0] for i in mine]) if (tree is not None and mine) else []
-    local = [(i, op.to_bytes(chals[i][1]), pfs[k].to_bytes(tree.config) if pfs else None)
-             for k, (i, op) in enumerate(zip(mine, ops))]
-    if world > 1:
-        allr = [None] * world
-        dist.all_gather_object(allr, local, group=group)
-    else:
-        allr = [local]
+    local = [(i, ops[i].to_bytes(chals[i][1]), pfs[k].to_bytes(tree.config) if pfs else None)
+             for k, i in enumerate(mine)]
+    allr = [None] * world
+    dist.all_gather_object(allr, local, group=group)
     openings, proofs = [None] * len(chals), [None] * len(chals)
     for part in allr:
         for i, ob, pb in part:

@@ -134,14 +134,19 @@ def test_layer_chunks_partial_sums_gloo(world):
         assert encs == want
 
 
-def test_opening_partition_balances_and_covers():
-    from paper_2602_12630_b200.dist import opening_partition
+def test_hot_layer_plan_balances_and_covers():
+    """Multi-GPU openings: every challenge assigned exactly once, hot layers' openings dealt
+    out to every rank, slice-commitment rows cover the first axis once."""
+    from paper_2602_12630_b200.dist import hot_layer_plan
     import numpy as np
     score = np.random.default_rng(4).pareto(1.5, 32) + 1e-3
     picks = [int(l) for l in np.random.default_rng(5).choice(32, size=256, p=score / score.sum())]
-    for world in (1, 2, 4, 8):
-        parts = opening_partition(picks, world)
+    for world in (1, 2, 3, 4, 8):
+        hot, rows, parts = hot_layer_plan(picks, world, 32, 4)
         assert sorted(i for p in parts for i in p) == list(range(256))
         assert all(p == sorted(p) for p in parts)
-        if world > 1:
-            assert min(len(p) for p in parts) > 0
+        assert rows[0][0] == 0 and rows[-1][1] == 32 and all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
+        assert hot == sorted(l for l in set(picks) if picks.count(l) >= 6)
+        for l in hot:
+            owners = [r for r, p in enumerate(parts) if any(picks[i] == l for i in p)]
+            assert len(owners) == min(world, picks.count(l))

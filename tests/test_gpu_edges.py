@@ -96,3 +96,30 @@ def test_completeness_and_binding_small_random():
             other = ops[(k + 1) % len(ops)]
             if other.proofs != op.proofs:
                 assert not tcb.tc_verify(srs, C, pt, tcb.TensorOpening(op.y, other.proofs))
+
+
+def test_split_slice_commitments_open_like_tc_open():
+    """The multi-GPU opening route on one GPU: slice commitments computed in three row
+    chunks (tc_open_slices, as three ranks would), concatenated, and openings from them
+    (tc_open_batch_sliced) equal tc_open byte for byte, grid-node challenges included."""
+    import paper_2602_12630_b200 as tcb
+    from paper_2602_12630_b200.dist import _open_sliced
+    from paper_2602_12630_b200 import _conv, _lib
+    shape = (8, 8, 16)
+    srs, _ = tcb.setup_srs(shape, b"split-slices")
+    x = torch.from_numpy((np.random.default_rng(8).standard_t(3, 1024) * 3).astype(np.float16)).cuda()
+    ctx = _lib.Context.get(0)
+    chunks = []
+    for lo, hi in ((0, 2), (2, 5), (5, 8)):
+        buf = torch.zeros(((hi - lo) * 8, 43), dtype=torch.uint8, device="cuda")
+        ptr, dt, keep = _conv.device_input(x, srs.size, "cuda:0")
+        with ctx.lock:
+            ctx.bind_stream()
+            ctx.check(_lib.lib().tc_open_slices(ctx.handle, srs.handle, ptr, dt, 16, lo, hi, buf.data_ptr()), "slices")
+        chunks.append(buf)
+    H = torch.cat(chunks).contiguous()
+    rng = random.Random(12)
+    pts = [[rng.randrange(O.P) for _ in shape] for _ in range(5)] + [[3, 8, 1], [rng.randrange(O.P), 2, 16]]
+    got = _open_sliced(srs, x, H, pts)
+    for pt, op in zip(pts, got):
+        assert op == tcb.tc_open(srs, x, pt)
