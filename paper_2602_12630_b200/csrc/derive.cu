@@ -19,10 +19,10 @@
 //      — subtractions only.
 //
 // The three stages are separable linear maps, so they commute across axes.  Points live
-// in extended twisted Edwards coordinates (complete addition: no special cases for the
-// neutral element, which appears when a trapdoor hits a grid node); the result is mapped
-// back to canonical Montgomery-curve affine points, so the bytes equal the trapdoor-
-// generated elements (g^{L_w(tau)} is unique).  Cost per element: sum_j (d_j - 1)/2 small
+// in the extended twisted Edwards coordinates of the MSM model (ec.cuh: the neutral element,
+// which appears when a trapdoor hits a grid node, needs no special case); the result is
+// mapped back to canonical affine points of the reference curve, so the bytes equal the
+// trapdoor-generated elements (g^{L_w(tau)} is unique).  Cost per element: sum_j (d_j - 1)/2 small
 // multiplications + one 162-bit multiplication + sum_j (d_j - 1)/2 additions.
 #include "tc_internal.cuh"
 
@@ -120,8 +120,8 @@ __global__ void __launch_bounds__(128) k_dv_taylor(Ext* __restrict__ w, uint64_t
   }
 }
 
-// extended Edwards -> canonical Montgomery affine (u, v) = ((Z+Y)/(Z-Y), (Z+Y) Z/((Z-Y) X)),
-// DV_K points per thread sharing one inversion; the neutral element -> infinity
+// Edwards points of the MSM model -> canonical E affine (ec.cuh ext_to_aff: psi, one
+// inversion), DV_K points per thread sharing one inversion; the neutral element -> infinity
 __global__ void __launch_bounds__(128) k_dv_store(const Ext* __restrict__ w, uint64_t n, Aff* __restrict__ out) {
   const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   const uint64_t i0 = t * DV_K;
@@ -132,21 +132,16 @@ __global__ void __launch_bounds__(128) k_dv_store(const Ext* __restrict__ w, uin
   for (int k = 0; k < cnt; k++) {
     const Ext p = ld_ext_g(w + i0 + k);
     pref[k] = run;
-    if (!Fq::is_zero(p.X)) run = Fq::mul(run, Fq::mul(Fq::sub(p.Z, p.Y), p.X));
+    run = Fq::mul(run, ext_to_aff_den(p));
   }
   Fe inv = Fq::inv(run);
   for (int k = cnt - 1; k >= 0; k--) {
     const Ext p = ld_ext_g(w + i0 + k);
-    Aff r;
-    if (Fq::is_zero(p.X)) {
-      // the neutral element (0 : 1); (0 : -1) is 2-torsion, outside the order-p subgroup
-      r = Fq::eq(p.Y, p.Z) ? aff_inf() : Aff{Fq::zero(), Fq::zero()};
-    } else {
-      const Fe ik = Fq::mul(inv, pref[k]);
-      inv = Fq::mul(inv, Fq::mul(Fq::sub(p.Z, p.Y), p.X));
-      const Fe zpy = Fq::add(p.Z, p.Y);
-      r = Aff{Fq::canon(Fq::mul(Fq::mul(zpy, p.X), ik)), Fq::canon(Fq::mul(Fq::mul(zpy, p.Z), ik))};
-    }
+    const Fe den = ext_to_aff_den(p);
+    const Fe ik = Fq::mul(inv, pref[k]);
+    inv = Fq::mul(inv, den);
+    Aff r = ext_to_aff_with_inv(p, ik);
+    if (!aff_is_inf(r)) r = Aff{Fq::canon(r.x), Fq::canon(r.y)};
     out[i0 + k] = r;
   }
 }

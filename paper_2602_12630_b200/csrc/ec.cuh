@@ -206,16 +206,24 @@ TC_HD void aff_encode43(const Aff& p, uint8_t out[43]) {
   }
 }
 
-// ---- twisted Edwards model for the MSM ---------------------------------------------------
-// The reference curve y^2 = x^3 + x is the Montgomery curve B v^2 = u^3 + A u^2 + u with
-// A = 0, B = 1, hence birational to the twisted Edwards curve a x^2 + y^2 = 1 + d x^2 y^2
-// with a = (A+2)/B = 2, d = (A-2)/B = -2 via x = u/v, y = (u-1)/(u+1).  Over F_q
-// (q = 7 mod 8) a = 2 is a square and d = -2 is not, so the unified extended-coordinate
-// addition (Hisil-Wong-Carter-Dawson 2008) is COMPLETE: no branch for P + P, P - P or the
-// neutral element.  A mixed add costs 8M (XYZZ: 8M + 2S), a full add 9M (XYZZ: 12M + 2S),
-// and d = -2, a = 2 are additions.  The map is defined on the whole odd-order subgroup
-// the SRS lives in; only the Montgomery 2-torsion point (0, 0) <-> (0, -1) is special.
-// Affine points carry t = x*y (precomputed when the SRS is converted).
+// ---- twisted Edwards model for the MSM: the 2-isogenous curve, a = -1 ------------------
+// E: y^2 = x^3 + x has the rational 2-torsion point (0, 0); the 2-isogeny with that kernel,
+//   phi(x, y) = ((x^2 + 1) / x, y (1 - x^2) / x^2),
+// maps E onto E': Y^2 = X^3 - 4X, and its dual psi(X, Y) = (Y^2 / (4 X^2), Y (-4 - X^2) / (8 X^2))
+// maps back with psi(phi(P)) = 2P.  E' has all three 2-torsion points; through X = u - 2,
+// u = sqrt(8) w it is the Montgomery curve B v^2 = w^3 + A w^2 + w (A = -6 / sqrt 8) whose
+// twisted Edwards model, after scaling, has a = -1 and a non-square d' — the model of the
+// fastest mixed addition (Hisil-Wong-Carter-Dawson madd-2008-hwcd-3: 7M with the table
+// storing 2d' x y, against 8M for E's own a = 2 model).  a = -1 is not a square mod q, so the
+// unified formulas have exceptional inputs, but only of order 2 or 4: every point here lies
+// in the order-p subgroup (p odd), where they never occur.
+//
+// Convention: an Edwards point stands for an E point P as phi([h] P), h = 2^-1 mod p
+// (= 2^160 + 2^23 + 1: 160 doublings and 2 additions).  Every MSM base is converted that way
+// (aff_to_ed), group operations commute with phi o [h], and ext_to_aff returns
+// psi(phi([h] S)) = 2 h S = S — the reference's point, canonical affine, bytes unchanged.
+// Both maps are closed rational functions of one inversion each (derivation and check in
+// DESIGN.md "Edwards model"; tests/test_edwards_host.py runs them on the host).
 // 16-byte aligned so every load / store is LDG.128 / STG.128 (EdAff padded 72 -> 80 B)
 struct alignas(16) EdAff {
   Fe x, y, t;
@@ -291,72 +299,59 @@ TC_D EdAff ld_edpk(const EdPk* p) {
 }
 #endif
 
+// constants of the a = -1 model in Montgomery form (tools: DESIGN.md "Edwards model")
+TC_HD Fe ed1_s8() { return Fe{{0xf0e3fc7fu, 0x7af10ac5u, 0xd178846bu, 0xb9b458afu, 0x365aaf7eu, 0x0000007bu}}; }   // sqrt(8)
+TC_HD Fe ed1_c1() { return Fe{{0x224fdc49u, 0xbe788564u, 0xe8bc4235u, 0x5cda2c57u, 0x9b2d57bfu, 0x00000095u}}; }   // 1 / (sqrt(8) s)
+TC_HD Fe ed1_k() { return Fe{{0xb90be8e9u, 0x4db37eccu, 0x2e59caf6u, 0x4b8bd7c2u, 0x73bfc60fu, 0x00000089u}}; }    // 2 d'
+TC_HD Fe ed1_kinv() { return Fe{{0x899ae3edu, 0x75132055u, 0x74698d42u, 0x2d1d0a0fu, 0xa3100e7cu, 0x00000071u}}; } // 1 / (2 d')
+TC_HD Fe ed1_cx() { return Fe{{0x993cdc1eu, 0x0e3bd4e3u, 0xba1dee52u, 0x192e9d40u, 0x26954205u, 0x000000b3u}}; }   // 1 / (4 s^2)
+TC_HD Fe ed1_cy() { return Fe{{0xd5b076b1u, 0xdefc42b1u, 0xf45e211au, 0xae6d162bu, 0xcd96abdfu, 0x00000052u}}; }   // -1 / (8 s)
+
 TC_HD Ext ext_zero() { return Ext{Fq::zero(), Fq::one(), Fq::one(), Fq::zero()}; }
-TC_HD Ext ext_from_aff(const EdAff& p) { return Ext{p.x, p.y, Fq::one(), p.t}; }
+// table points carry t = 2 d' x y; the accumulator's T = X Y / Z
+TC_HD Ext ext_from_aff(const EdAff& p) { return Ext{p.x, p.y, Fq::one(), Fq::mul(p.t, ed1_kinv())}; }
+TC_HD EdAff edaff_from_xy(const Fe& x, const Fe& y) { return EdAff{x, y, Fq::mul(Fq::mul(x, y), ed1_k())}; }
 TC_HD EdAff edaff_neg(const EdAff& p) { return EdAff{Fq::neg(p.x), p.y, Fq::neg(p.t)}; }
 TC_HD Ext ext_neg(const Ext& p) { return Ext{Fq::neg(p.X), p.Y, p.Z, Fq::neg(p.T)}; }
 
-// acc += q (q affine with t = x y): madd-2008-hwcd, a = 2, d = -2
-#ifndef TC_LAZY
-#define TC_LAZY 1   // E and H from unreduced products (Fq::lazy_e_h): 7 reductions per add, not 8
-#endif
+// acc += q (q affine with t = 2 d' x y): madd-2008-hwcd-3, a = -1 — 7 products, 7 reductions
+// (E and H from unreduced products, Fq::lazy_e_h1)
 TC_HD void ext_madd(Ext& acc, const EdAff& q) {
-#if TC_LAZY
   Fe E, H;
-  Fq::lazy_e_h(acc.X, acc.Y, q.x, q.y, E, H);   // E = X1 y2 + Y1 x2, H = Y1 y2 - 2 X1 x2
-  const Fe C2 = Fq::dbl(Fq::mul(acc.T, q.t));   // -d T1 T2
-  const Fe F = Fq::add(acc.Z, C2);               // Z1 - d T1 T2
-  const Fe G = Fq::sub(acc.Z, C2);               // Z1 + d T1 T2
-#else
-  const Fe A = Fq::mul(acc.X, q.x);
-  const Fe B = Fq::mul(acc.Y, q.y);
-  const Fe C2 = Fq::dbl(Fq::mul(acc.T, q.t));   // -d T1 T2
-  const Fe E = Fq::sub(Fq::sub(Fq::mul(Fq::add(acc.X, acc.Y), Fq::add(q.x, q.y)), A), B);
-  const Fe F = Fq::add(acc.Z, C2);               // Z1 - d T1 T2
-  const Fe G = Fq::sub(acc.Z, C2);               // Z1 + d T1 T2
-  const Fe H = Fq::sub(B, Fq::dbl(A));           // B - a A
-#endif
+  Fq::lazy_e_h1(acc.X, acc.Y, q.x, q.y, E, H);   // E = 2(X1 y2 + Y1 x2), H = 2(Y1 y2 + X1 x2)
+  const Fe C = Fq::mul(acc.T, q.t);               // 2 d' T1 T2
+  const Fe D = Fq::dbl(acc.Z);                    // 2 Z1
+  const Fe F = Fq::sub(D, C);
+  const Fe G = Fq::add(D, C);
   acc.X = Fq::mul(E, F);
   acc.Y = Fq::mul(G, H);
   acc.T = Fq::mul(E, H);
   acc.Z = Fq::mul(F, G);
 }
 
-// acc += q, both extended: add-2008-hwcd (unified, complete here)
+// acc += q, both extended: add-2008-hwcd-3, a = -1 (9M)
 TC_HD void ext_add(Ext& acc, const Ext& q) {
-#if TC_LAZY
   Fe E, H;
-  Fq::lazy_e_h(acc.X, acc.Y, q.X, q.Y, E, H);
-  const Fe C2 = Fq::dbl(Fq::mul(acc.T, q.T));
-  const Fe D = Fq::mul(acc.Z, q.Z);
-  const Fe F = Fq::add(D, C2);
-  const Fe G = Fq::sub(D, C2);
-#else
-  const Fe A = Fq::mul(acc.X, q.X);
-  const Fe B = Fq::mul(acc.Y, q.Y);
-  const Fe C2 = Fq::dbl(Fq::mul(acc.T, q.T));
-  const Fe D = Fq::mul(acc.Z, q.Z);
-  const Fe E = Fq::sub(Fq::sub(Fq::mul(Fq::add(acc.X, acc.Y), Fq::add(q.X, q.Y)), A), B);
-  const Fe F = Fq::add(D, C2);
-  const Fe G = Fq::sub(D, C2);
-  const Fe H = Fq::sub(B, Fq::dbl(A));
-#endif
+  Fq::lazy_e_h1(acc.X, acc.Y, q.X, q.Y, E, H);
+  const Fe C = Fq::mul(Fq::mul(acc.T, q.T), ed1_k());
+  const Fe D = Fq::dbl(Fq::mul(acc.Z, q.Z));
+  const Fe F = Fq::sub(D, C);
+  const Fe G = Fq::add(D, C);
   acc.X = Fq::mul(E, F);
   acc.Y = Fq::mul(G, H);
   acc.T = Fq::mul(E, H);
   acc.Z = Fq::mul(F, G);
 }
 
-// 2P: dbl-2008-hwcd, a = 2 (4M + 4S)
+// 2P: dbl-2008-hwcd, a = -1 (4M + 4S)
 TC_HD Ext ext_dbl(const Ext& p) {
   const Fe A = Fq::sqr(p.X);
   const Fe B = Fq::sqr(p.Y);
   const Fe C = Fq::dbl(Fq::sqr(p.Z));
-  const Fe D = Fq::dbl(A);
   const Fe E = Fq::sub(Fq::sub(Fq::sqr(Fq::add(p.X, p.Y)), A), B);
-  const Fe G = Fq::add(D, B);
+  const Fe G = Fq::sub(B, A);         // a A + B
   const Fe F = Fq::sub(G, C);
-  const Fe H = Fq::sub(D, B);
+  const Fe H = Fq::neg(Fq::add(A, B));   // a A - B
   return Ext{Fq::mul(E, F), Fq::mul(G, H), Fq::mul(F, G), Fq::mul(E, H)};
 }
 
@@ -404,35 +399,66 @@ TC_HD Ext ext_mul_small_naf(const Ext& p, uint32_t k) {
   return r;
 }
 
-// Edwards (X:Y:Z:T) -> Montgomery affine (u, v) = ((Z+Y)/(Z-Y), (Z+Y) Z / ((Z-Y) X)),
-// one inversion.  Neutral -> infinity; (0 : -1) -> the 2-torsion point (0, 0).
+// Edwards (X:Y:Z:T) on E' -> psi -> canonical-ready Montgomery-form affine point of E:
+// with N = sqrt8 (Z + Y) - 2 (Z - Y) and one inversion of D = X^2 N^2 (Z - Y),
+//   x = ((Z + Y) Z)^2 (Z - Y) / (4 s^2 D),  y = -(Z + Y) Z (4 (Z - Y)^2 + N^2) X / (8 s D).
+// The neutral element (X = 0) -> infinity.  ext_to_aff_den / _with_inv: batch-inversion form.
+TC_HD Fe ext_to_aff_den(const Ext& p) {
+  if (Fq::is_zero(p.X)) return Fq::one();
+  const Fe zm = Fq::sub(p.Z, p.Y);
+  const Fe N = Fq::sub(Fq::mul(ed1_s8(), Fq::add(p.Z, p.Y)), Fq::dbl(zm));
+  return Fq::mul(Fq::mul(Fq::sqr(p.X), Fq::sqr(N)), zm);
+}
+TC_HD Aff ext_to_aff_with_inv(const Ext& p, const Fe& inv) {
+  if (Fq::is_zero(p.X)) return aff_inf();
+  const Fe zp = Fq::add(p.Z, p.Y), zm = Fq::sub(p.Z, p.Y);
+  const Fe N = Fq::sub(Fq::mul(ed1_s8(), zp), Fq::dbl(zm));
+  const Fe zpz = Fq::mul(zp, p.Z);
+  const Fe x = Fq::mul(Fq::mul(Fq::mul(Fq::sqr(zpz), zm), inv), ed1_cx());
+  const Fe w = Fq::add(Fq::dbl(Fq::dbl(Fq::sqr(zm))), Fq::sqr(N));   // 4 (Z - Y)^2 + N^2
+  const Fe y = Fq::mul(Fq::mul(Fq::mul(Fq::mul(zpz, w), p.X), inv), ed1_cy());
+  return Aff{x, y};
+}
 TC_HD Aff ext_to_aff(const Ext& p) {
-  if (Fq::is_zero(p.X)) {
-    if (Fq::eq(p.Y, p.Z)) return aff_inf();
-    return Aff{Fq::zero(), Fq::zero()};
-  }
-  const Fe zpy = Fq::add(p.Z, p.Y);
-  const Fe inv = Fq::inv_pref(Fq::mul(Fq::sub(p.Z, p.Y), p.X));
-  return Aff{Fq::mul(Fq::mul(zpy, p.X), inv), Fq::mul(Fq::mul(zpy, p.Z), inv)};
+  if (Fq::is_zero(p.X)) return aff_inf();
+  return ext_to_aff_with_inv(p, Fq::inv_pref(ext_to_aff_den(p)));
 }
 
-// Montgomery affine -> Edwards affine given inv = 1 / (v (u + 1)):
-// x = u / v = u (u + 1) inv, y = (u - 1) / (u + 1) = (u - 1) v inv, t = x y.
-// `den` returns v (u + 1) (1 for the special points so a batch inversion stays valid).
-TC_HD Fe aff_ed_den(const Aff& p) {
-  if (aff_is_inf(p) || Fq::is_zero(p.y)) return Fq::one();
-  return Fq::mul(p.y, Fq::add(p.x, Fq::one()));
+// [h] P on E, h = 2^-1 mod p = 2^160 + 2^23 + 1 (XYZZ: 160 doublings, 2 mixed adds)
+TC_HD Xyzz xyzz_mul_half(const Aff& p) {
+  if (aff_is_inf(p)) return xyzz_inf();
+  Xyzz acc = xyzz_from_aff(p);
+  for (int b = 159; b >= 0; b--) {
+    acc = xyzz_dbl(acc);
+    if (b == 23 || b == 0) xyzz_add_aff(acc, p);
+  }
+  return acc;
 }
-TC_HD EdAff aff_to_ed_with_inv(const Aff& p, const Fe& inv) {
-  if (aff_is_inf(p)) return EdAff{Fq::zero(), Fq::one(), Fq::zero()};
-  if (Fq::is_zero(p.y)) return EdAff{Fq::zero(), Fq::neg(Fq::one()), Fq::zero()};   // (0,0) -> (0,-1)
-  const Fe x = Fq::mul(Fq::mul(p.x, Fq::add(p.x, Fq::one())), inv);
-  const Fe y = Fq::mul(Fq::mul(Fq::sub(p.x, Fq::one()), p.y), inv);
-  return EdAff{x, y, Fq::mul(x, y)};
+
+// E affine point Q (already [h]-scaled) -> E' Edwards (x_e, y_e, 2 d' x_e y_e):
+//   x_e = c1 x (x + 1) / (y (1 - x)),  y_e = ((x + 1)^2 - sqrt8 x) / ((x + 1)^2 + sqrt8 x),
+// one inversion of den = y (1 - x) ((x + 1)^2 + sqrt8 x) (never 0 in the odd-order subgroup:
+// its zeros are points of order 2 or 4).  Infinity -> the neutral (0, 1).
+TC_HD Fe aff_ed_den(const Aff& q) {
+  if (aff_is_inf(q)) return Fq::one();
+  const Fe x1 = Fq::add(q.x, Fq::one());
+  const Fe sq = Fq::add(Fq::sqr(x1), Fq::mul(ed1_s8(), q.x));
+  return Fq::mul(Fq::mul(q.y, Fq::sub(Fq::one(), q.x)), sq);
 }
+TC_HD EdAff aff_to_ed_with_inv(const Aff& q, const Fe& inv) {
+  if (aff_is_inf(q)) return EdAff{Fq::zero(), Fq::one(), Fq::zero()};
+  const Fe x1 = Fq::add(q.x, Fq::one());
+  const Fe a = Fq::sqr(x1), sx = Fq::mul(ed1_s8(), q.x);
+  const Fe xe = Fq::mul(Fq::mul(Fq::mul(Fq::mul(ed1_c1(), q.x), x1), Fq::add(a, sx)), inv);
+  const Fe ye = Fq::mul(Fq::mul(Fq::sub(a, sx), Fq::mul(q.y, Fq::sub(Fq::one(), q.x))), inv);
+  return edaff_from_xy(xe, ye);
+}
+// the model's image of an E point that is ALREADY [h]-scaled
+TC_HD EdAff aff_to_ed_noh(const Aff& q) { return aff_to_ed_with_inv(q, Fq::inv_pref(aff_ed_den(q))); }
+// the model's image of an E point P: phi([h] P)
 TC_HD EdAff aff_to_ed(const Aff& p) {
-  const Fe d = aff_ed_den(p);
-  return aff_to_ed_with_inv(p, Fq::inv(d));
+  const Aff q = xyzz_to_aff(xyzz_mul_half(p));
+  return aff_to_ed_noh(q);
 }
 
 }  // namespace tc

@@ -305,6 +305,9 @@ struct Field {
 // even/odd form wins (k_accum_aff 5.98 -> 5.83 ms, config-3 step 10.14 -> 9.89 ms)
 #define TC_MULV 0
 #endif
+#ifndef TC_E_H1_2ARR
+#define TC_E_H1_2ARR 0
+#endif
 #ifndef TC_SQRV
 #define TC_SQRV 1   // 0: square through the generic product, 1: dedicated 21-product square (3% faster accumulation)
 #endif
@@ -576,6 +579,63 @@ struct Field {
     }
 #endif
     return r;
+  }
+  // r = a + b (12 limbs, no overflow for the bounded products here)
+  TC_HD static void w12_add(uint32_t r[12], const uint32_t a[12], const uint32_t b[12]) {
+#if defined(__CUDA_ARCH__)
+    asm("add.cc.u32  %0, %12, %24;\n\t"
+        "addc.cc.u32 %1, %13, %25;\n\t"
+        "addc.cc.u32 %2, %14, %26;\n\t"
+        "addc.cc.u32 %3, %15, %27;\n\t"
+        "addc.cc.u32 %4, %16, %28;\n\t"
+        "addc.cc.u32 %5, %17, %29;\n\t"
+        "addc.cc.u32 %6, %18, %30;\n\t"
+        "addc.cc.u32 %7, %19, %31;\n\t"
+        "addc.cc.u32 %8, %20, %32;\n\t"
+        "addc.cc.u32 %9, %21, %33;\n\t"
+        "addc.cc.u32 %10, %22, %34;\n\t"
+        "addc.u32    %11, %23, %35;\n\t"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]), "r"(a[8]),
+          "r"(a[9]), "r"(a[10]), "r"(a[11]), "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3]), "r"(b[4]), "r"(b[5]),
+          "r"(b[6]), "r"(b[7]), "r"(b[8]), "r"(b[9]), "r"(b[10]), "r"(b[11]));
+#else
+    uint64_t c = 0;
+    for (int i = 0; i < 12; i++) {
+      c += (uint64_t)a[i] + b[i];
+      r[i] = (uint32_t)c;
+      c >>= 32;
+    }
+#endif
+  }
+  // Lazy pair for the a = -1 Edwards adds (ec.cuh): A = (Y1 - X1)(y2 - x2) with the lazy
+  // [0, 2m) differences, B = (Y1 + X1)(y2 + x2) with unreduced sums, then
+  //   E = B - A + 8m^2 = 2 (X1 y2 + Y1 x2)  and  H = B + A = 2 (X1 x2 + Y1 y2)   (mod m),
+  // 2 products and 2 reductions.  A < 4m^2, B < 16m^2 (sums < 4m): E < 24m^2, H < 20m^2 < m R.
+  TC_HD static void lazy_e_h1(const Fe& X1, const Fe& Y1, const Fe& x2, const Fe& y2, Fe& E, Fe& H) {
+#if TC_E_H1_2ARR
+    // two 12-limb arrays: E_raw = B + 8m^2 - A in place, then H_raw = E_raw + 2A
+    // (= B + A + 8m^2 < 28 m^2)
+    uint32_t A[12], B[12];
+    mul_wide(A, sub(Y1, X1), sub(y2, x2));
+    mul_wide(B, add_raw(Y1, X1), add_raw(y2, x2));
+    w12_add_8mm(B, B);
+    w12_sub(B, B, A);
+    E = redc(B);
+    w12_add(A, A, A);
+    w12_add(A, A, B);
+    H = redc(A);
+#else
+    uint32_t A[12], B[12], T[12];
+    mul_wide(A, sub(Y1, X1), sub(y2, x2));
+    mul_wide(B, add_raw(Y1, X1), add_raw(y2, x2));
+    w12_add(T, B, A);
+    H = redc(T);
+    w12_add_8mm(B, B);
+    w12_sub(B, B, A);
+    E = redc(B);
+#endif
   }
   TC_HD static void lazy_e_h(const Fe& a1, const Fe& a2, const Fe& b1, const Fe& b2, Fe& E, Fe& H) {
     uint32_t A[12], B[12], P[12];

@@ -20,7 +20,7 @@ constexpr int SE = 255;   // non-zero byte values
 __global__ void k_tab_bases(const Aff* pts, uint32_t B, Xyzz* q) {
   uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= B) return;
-  Xyzz acc = xyzz_from_aff(pts[k]);
+  Xyzz acc = xyzz_mul_half(pts[k]);   // the MSM model's bases are phi([h] G_k) (ec.cuh)
   for (int w = 0; w < SW; w++) {
     q[k * SW + w] = acc;
     for (int i = 0; i < 8; i++) acc = xyzz_dbl(acc);
@@ -41,7 +41,7 @@ __global__ void k_tab_fill(const Xyzz* q, uint32_t B, EdAff* tab) {
   }
   Aff r = xyzz_to_aff(acc);
   if (!aff_is_inf(r)) r = Aff{Fq::canon(r.x), Fq::canon(r.y)};
-  const EdAff e = aff_to_ed(r);
+  const EdAff e = aff_to_ed_noh(r);   // r = (j+1) 2^{8w} [h] G_k
   tab[t] = EdAff{Fq::red2(e.x), Fq::red2(e.y), Fq::red2(e.t)};
 }
 

@@ -103,30 +103,47 @@ __global__ void __launch_bounds__(128) k_fixed(const Aff* table, const Fe* exps,
   }
 }
 
-// Montgomery (u, v) -> Edwards (x, y, t): FB_K points per thread share one inversion
+// E affine points -> the MSM's Edwards model phi([h] P) (ec.cuh): [h] P in XYZZ, then two
+// Montgomery batch inversions over FB_K points per thread (XYZZ -> affine, affine -> Edwards)
 __global__ void __launch_bounds__(128) k_to_edwards(const Aff* in, uint64_t n, EdPk* out) {
   uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   uint64_t i0 = t * FB_K;
   if (i0 >= n) return;
   const int cnt = (n - i0 < (uint64_t)FB_K) ? (int)(n - i0) : FB_K;
+  Xyzz h[FB_K];
   Fe pref[FB_K];
   Fe run = Fq::one();
   for (int k = 0; k < cnt; k++) {
+    h[k] = xyzz_mul_half(in[i0 + k]);
     pref[k] = run;
-    run = Fq::mul(run, aff_ed_den(in[i0 + k]));
+    if (!xyzz_is_inf(h[k])) run = Fq::mul(run, Fq::mul(h[k].ZZ, h[k].ZZZ));
   }
   Fe inv = Fq::inv(run);
+  Aff q[FB_K];
   for (int k = cnt - 1; k >= 0; k--) {
-    const Aff p = in[i0 + k];
-    const Fe den = aff_ed_den(p);
+    if (xyzz_is_inf(h[k])) {
+      q[k] = aff_inf();
+    } else {
+      const Fe iz = Fq::mul(inv, pref[k]);
+      inv = Fq::mul(inv, Fq::mul(h[k].ZZ, h[k].ZZZ));
+      q[k] = xyzz_to_aff_with_inv(h[k], iz);
+    }
+  }
+  run = Fq::one();
+  for (int k = 0; k < cnt; k++) {
+    pref[k] = run;
+    run = Fq::mul(run, aff_ed_den(q[k]));
+  }
+  inv = Fq::inv(run);
+  for (int k = cnt - 1; k >= 0; k--) {
+    const Fe den = aff_ed_den(q[k]);
     const Fe ik = Fq::mul(inv, pref[k]);
     inv = Fq::mul(inv, den);
-    EdAff e = aff_to_ed_with_inv(p, ik);
-    out[i0 + k] = pack_ed(e);
+    out[i0 + k] = pack_ed(aff_to_ed_with_inv(q[k], ik));
   }
 }
 
-// out[i] = 2^c in[i] (Edwards affine with t = xy): c doublings in extended coordinates, the
+// out[i] = 2^c in[i] (Edwards affine with t = 2 d' x y): c doublings in extended coordinates, the
 // Z of FB_K points per thread inverted with one shared inversion
 __global__ void __launch_bounds__(128) k_win_step(const EdPk* in, uint64_t n, int c, EdPk* out) {
   uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -148,7 +165,7 @@ __global__ void __launch_bounds__(128) k_win_step(const EdPk* in, uint64_t n, in
     const Fe iz = Fq::mul(inv, pref[k]);
     inv = Fq::mul(inv, pts[k].Z);
     const Fe x = Fq::mul(pts[k].X, iz), y = Fq::mul(pts[k].Y, iz);
-    out[i0 + k] = pack_ed(EdAff{x, y, Fq::mul(x, y)});
+    out[i0 + k] = pack_ed(edaff_from_xy(x, y));
   }
 }
 
