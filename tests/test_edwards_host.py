@@ -1,8 +1,9 @@
-"""Host check of the twisted Edwards MSM arithmetic (csrc/ec.cuh: complete extended-coordinate
-adds on a x^2 + y^2 = 1 + d x^2 y^2, a = 2, d = -2) against the XYZZ / Montgomery affine
-arithmetic the reference's curve y^2 = x^3 + x (backend.py:102-146) is written in:
-round trips, sums, doublings, P + P and P - P through the mixed add, the neutral element.
-The same __host__ __device__ code runs in the kernels; compiled here with nvcc (host only)."""
+"""Host check of the twisted Edwards MSM arithmetic (csrc/ec.cuh: extended-coordinate adds on
+the a = -1 model of the 2-isogenous curve E': Y^2 = X^3 - 4X, bases phi([1/2] P), results
+psi(.)) against the XYZZ / Montgomery affine arithmetic the reference's curve y^2 = x^3 + x
+(backend.py:102-146) is written in: round trips, sums, doublings, P + P and P - P through
+the mixed add, the neutral element, small multiples.  The same __host__ __device__ code runs
+in the kernels; compiled here with nvcc (host only)."""
 import os
 import shutil
 import subprocess

@@ -1,4 +1,5 @@
-// Host check of the twisted Edwards MSM arithmetic (ec.cuh) against the XYZZ/affine
+// Host check of the twisted Edwards MSM arithmetic (ec.cuh: a = -1 model of the 2-isogenous
+// curve, bases phi([1/2] P), results psi(.)) against the XYZZ/affine
 // Montgomery arithmetic: random multiples of g, sums, doublings, P - P, neutral.
 // nvcc -std=c++17 --expt-relaxed-constexpr -o /tmp/ed_check tools/ed_check.cu && /tmp/ed_check
 #include <cstdio>
