@@ -83,6 +83,10 @@ int tc_abi_version(void);
 int tc_ctx_create(int device, void* cuda_stream, tc_ctx** out);
 int tc_ctx_destroy(tc_ctx* ctx);
 int tc_ctx_set_stream(tc_ctx* ctx, void* cuda_stream);
+/* Mark a context as one of a forward pipeline's (its own stream, several launches in
+ * flight): tc_commit_tree_launch then runs each forward's post-accumulation tail on a
+ * low-priority stream so the next forward's MSM blocks are scheduled first. */
+int tc_ctx_set_pipelined(tc_ctx* ctx, int on);
 int tc_ctx_synchronize(tc_ctx* ctx);
 const char* tc_ctx_last_error(const tc_ctx* ctx);
 uint64_t tc_ctx_launch_count(const tc_ctx* ctx);

@@ -47,6 +47,7 @@ _SIGS = [
     ("tc_ctx_create", C.c_int, [C.c_int, _P, C.POINTER(_P)]),
     ("tc_ctx_destroy", C.c_int, [_P]),
     ("tc_ctx_set_stream", C.c_int, [_P, _P]),
+    ("tc_ctx_set_pipelined", C.c_int, [_P, C.c_int]),
     ("tc_ctx_synchronize", C.c_int, [_P]),
     ("tc_ctx_last_error", C.c_char_p, [_P]),
     ("tc_ctx_launch_count", C.c_uint64, [_P]),
@@ -167,8 +168,11 @@ class Context:
             ctx = cls._pipeline.get(key)
             if ctx is None:
                 ctx = cls(device)
-                ctx.fixed_stream = torch.cuda.Stream(device)
+                # high priority: this context's count / scatter / accumulation; each forward's
+                # latency-bound tail goes to a low-priority stream (tc_ctx_set_pipelined)
+                ctx.fixed_stream = torch.cuda.Stream(device, priority=-1)
                 lib().tc_ctx_set_stream(ctx.handle, ctx.fixed_stream.cuda_stream)
+                lib().tc_ctx_set_pipelined(ctx.handle, 1)
                 cls._pipeline[key] = ctx
         return ctx
 

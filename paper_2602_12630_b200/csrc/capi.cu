@@ -550,7 +550,15 @@ int tc_ctx_destroy(tc_ctx* ctx) {
   if (ctx->h_off) cudaFreeHost(ctx->h_off);
   if (ctx->res_ev) cudaEventDestroy(ctx->res_ev);
   if (ctx->ev_mid) cudaEventDestroy(ctx->ev_mid);
+  if (ctx->ev_tail) cudaEventDestroy(ctx->ev_tail);
+  if (ctx->tail_stream) cudaStreamDestroy(ctx->tail_stream);
   delete ctx;
+  return TC_OK;
+}
+
+int tc_ctx_set_pipelined(tc_ctx* ctx, int on) {
+  if (!ctx) return TC_ERR_ARGUMENT;
+  ctx->pipelined = on != 0;
   return TC_OK;
 }
 
@@ -935,9 +943,25 @@ static int commit_tree_launch(tc_ctx* ctx, const tc_srs* srs, const void* const*
   static const bool no_tail = getenv("TC_NO_TREE_TAIL") != nullptr;
   ctx->defer_req = !no_tail && cap <= 1024;
   ctx->defer_wsum = nullptr;
+  // pipeline contexts (a stream of their own): the post-accumulation tail on a low-priority
+  // stream (tc_ctx::tail_split); the context's stream is restored below, ordered after it
+  static const bool split = getenv("TC_TAIL_SPLIT") ? atoi(getenv("TC_TAIL_SPLIT")) != 0 : true;
+  cudaStream_t home = ctx->stream;
+  if (split && ctx->pipelined) {
+    if (!ctx->tail_stream) {
+      int lo = 0, hi = 0;
+      TC_CUDA(ctx, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      TC_CUDA(ctx, cudaStreamCreateWithPriority(&ctx->tail_stream, cudaStreamNonBlocking, lo));
+    }
+    ctx->tail_split = true;
+  }
   const int cs = commit_many_dev(ctx, srs, d_ins, count, dtype, scale_bits, route, d_all);
   ctx->defer_req = false;
-  TC_TRY(cs);
+  ctx->tail_split = false;
+  if (cs) {
+    ctx->stream = home;
+    return cs;
+  }
   if (ctx->defer_wsum) {
     if (ctx->defer_L != count) return fail(ctx, TC_ERR_VALUE, "deferred finish: %d of %d MSMs", ctx->defer_L, count);
     TC_TRY(tcrt::tree_tail_device(ctx, const_cast<tc_srs*>(node_srs), ctx->defer_wsum, count, ctx->defer_nwin, cap,
@@ -959,6 +983,10 @@ static int commit_tree_launch(tc_ctx* ctx, const tc_srs* srs, const void* const*
   TC_CUDA(ctx, cudaMemcpyAsync(ctx->h_res, d_all, pts_b, cudaMemcpyDeviceToHost, ctx->stream));
   TC_CUDA(ctx, cudaMemcpyAsync((char*)ctx->h_res + pts_b, d_levels, vals_b, cudaMemcpyDeviceToHost, ctx->stream));
   TC_CUDA(ctx, cudaEventRecord(ctx->res_ev, ctx->stream));
+  if (ctx->stream != home) {   // back on the context's own stream, ordered after the tail
+    TC_CUDA(ctx, cudaStreamWaitEvent(home, ctx->res_ev, 0));
+    ctx->stream = home;
+  }
   ctx->res_pending = true;
   ctx->res_count = (uint64_t)count, ctx->res_nodes = total_nodes, ctx->res_values = total_values;
   return TC_OK;

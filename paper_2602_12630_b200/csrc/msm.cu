@@ -1741,6 +1741,15 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
 
   // 6. levels (a bucket holds <= n entries); level 0 may already be queued (early0)
   if (!early0) TC_TRY(level0(E));
+  if (ctx->tail_split && ctx->tail_stream && ctx->stream != ctx->tail_stream) {
+    // the rest of this forward on the context's low-priority tail stream (tc_ctx::tail_split)
+    if (!ctx->ev_tail) TC_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_tail, cudaEventDisableTiming));
+    TC_CUDA(ctx, cudaEventRecord(ctx->ev_tail, st));
+    TC_CUDA(ctx, cudaStreamWaitEvent(ctx->tail_stream, ctx->ev_tail, 0));
+    ctx->main_stream = ctx->stream;
+    ctx->stream = ctx->tail_stream;
+    st = ctx->tail_stream;
+  }
   if (ctx->prof) {
     TC_CUDA(ctx, cudaEventSynchronize(ctx->ev[1]));
     float ms = 0;

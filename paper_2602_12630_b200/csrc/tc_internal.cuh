@@ -70,6 +70,14 @@ struct tc_ctx {
   // the block window-sum path leaves its L x nwin prescaled window sums in defer_wsum and
   // does not write the points; the caller's fused tail kernel sums and converts them
   bool defer_req = false;
+  // commit + tree launches of a pipeline context: everything after the level-0 bucket
+  // accumulation (reduction levels, window sums, tree, readback) runs on a LOW-priority
+  // stream, so the next forward's count / scatter / accumulation blocks are dispatched
+  // first and this forward's latency-bound tail fills the gaps
+  bool tail_split = false;
+  bool pipelined = false;   // set by tc_ctx_set_pipelined (the forward pipeline's contexts)
+  cudaStream_t tail_stream = nullptr, main_stream = nullptr;
+  cudaEvent_t ev_tail = nullptr;
   tc::Ext* defer_wsum = nullptr;
   int defer_nwin = 0, defer_L = 0;
   std::map<std::string, std::pair<void*, size_t>> guards;
