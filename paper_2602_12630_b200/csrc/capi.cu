@@ -522,6 +522,7 @@ int tc_ctx_create(int device, void* cuda_stream, tc_ctx** out) {
   if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) ctx->num_sms = prop.multiProcessorCount;
   ctx->h_stage_bytes = 1 << 20;
   ctx->guard = getenv("TC_SCRATCH_GUARD") && atoi(getenv("TC_SCRATCH_GUARD")) != 0;
+  if (getenv("TC_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(getenv("TC_L2_FETCH")));
   if (cudaMalloc(&ctx->d_flags, 64) != cudaSuccess || cudaMallocHost(&ctx->h_flags, 64) != cudaSuccess ||
       cudaMallocHost(&ctx->h_stage, ctx->h_stage_bytes) != cudaSuccess) {
     delete ctx;
