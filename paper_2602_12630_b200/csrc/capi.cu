@@ -918,6 +918,33 @@ static void terkle_geometry(uint64_t n, uint64_t B, uint64_t& L, uint64_t& cap, 
   for (uint64_t l = 0; l < L; l++) values += w, w /= B, nodes += w;
 }
 
+// Pipeline contexts (tc_ctx_set_pipelined): the forward's post-accumulation tail runs on a
+// low-priority stream of the context (msm_batch_device switches to it after the level-0
+// accumulation when tail_split is set), so other forwards' sort and accumulation blocks are
+// dispatched first.  tail_end orders the context's own stream after the tail.
+static int tail_begin(tc_ctx* ctx) {
+  static const bool split = getenv("TC_TAIL_SPLIT") ? atoi(getenv("TC_TAIL_SPLIT")) != 0 : true;
+  if (!split || !ctx->pipelined) return TC_OK;
+  if (!ctx->tail_stream) {
+    int lo = 0, hi = 0;
+    TC_CUDA(ctx, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    TC_CUDA(ctx, cudaStreamCreateWithPriority(&ctx->tail_stream, cudaStreamNonBlocking, lo));
+  }
+  ctx->tail_split = true;
+  return TC_OK;
+}
+
+static int tail_end(tc_ctx* ctx, cudaStream_t home) {
+  ctx->tail_split = false;
+  if (ctx->stream == home) return TC_OK;
+  const cudaStream_t tail = ctx->stream;
+  ctx->stream = home;
+  if (!ctx->ev_tail) TC_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_tail, cudaEventDisableTiming));
+  TC_CUDA(ctx, cudaEventRecord(ctx->ev_tail, tail));
+  TC_CUDA(ctx, cudaStreamWaitEvent(home, ctx->ev_tail, 0));
+  return TC_OK;
+}
+
 // commit + leaves + tree on the ctx stream; the results are copied (asynchronously) into the
 // ctx's pinned result buffer and `res_ev` recorded — tc_commit_tree_finish collects them
 static int commit_tree_launch(tc_ctx* ctx, const tc_srs* srs, const void* const* d_ins, int count, int dtype,
@@ -944,18 +971,10 @@ static int commit_tree_launch(tc_ctx* ctx, const tc_srs* srs, const void* const*
   static const bool no_tail = getenv("TC_NO_TREE_TAIL") != nullptr;
   ctx->defer_req = !no_tail && cap <= 1024;
   ctx->defer_wsum = nullptr;
-  // pipeline contexts (a stream of their own): the post-accumulation tail on a low-priority
-  // stream (tc_ctx::tail_split); the context's stream is restored below, ordered after it
-  static const bool split = getenv("TC_TAIL_SPLIT") ? atoi(getenv("TC_TAIL_SPLIT")) != 0 : true;
+  // pipeline contexts: the post-accumulation tail on the low-priority stream (tail_begin);
+  // the context's stream is restored below, ordered after it
   cudaStream_t home = ctx->stream;
-  if (split && ctx->pipelined) {
-    if (!ctx->tail_stream) {
-      int lo = 0, hi = 0;
-      TC_CUDA(ctx, cudaDeviceGetStreamPriorityRange(&lo, &hi));
-      TC_CUDA(ctx, cudaStreamCreateWithPriority(&ctx->tail_stream, cudaStreamNonBlocking, lo));
-    }
-    ctx->tail_split = true;
-  }
+  TC_TRY(tail_begin(ctx));
   const int cs = commit_many_dev(ctx, srs, d_ins, count, dtype, scale_bits, route, d_all);
   ctx->defer_req = false;
   ctx->tail_split = false;
@@ -1030,10 +1049,16 @@ int tc_commit_points_launch(tc_ctx* ctx, const tc_srs* srs, const void* const* d
   if (count == 0) return TC_OK;
   Aff* d_pts;
   TC_TRY(tcrt::scratch_t(ctx, "dist.pts", (uint64_t)count, &d_pts));
-  TC_TRY(commit_many_dev(ctx, srs, d_ins, count, dtype, scale_bits, route, d_pts));
-  k_encode43<<<tcrt::blocks_for(count, 64), 64, 0, ctx->stream>>>(d_pts, count, d_out43);
-  TC_LAUNCHED(ctx);
-  return TC_OK;
+  cudaStream_t home = ctx->stream;
+  TC_TRY(tail_begin(ctx));
+  const int cs = commit_many_dev(ctx, srs, d_ins, count, dtype, scale_bits, route, d_pts);
+  ctx->tail_split = false;
+  if (!cs) {
+    k_encode43<<<tcrt::blocks_for(count, 64), 64, 0, ctx->stream>>>(d_pts, count, d_out43);
+    TC_LAUNCHED(ctx);
+  }
+  const int te = tail_end(ctx, home);
+  return cs ? cs : te;
 }
 
 // sum the partial points of each layer (CSR offsets `off`, n_layers + 1 entries)
