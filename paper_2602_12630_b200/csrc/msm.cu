@@ -724,6 +724,9 @@ __global__ void __launch_bounds__(FPS_THREADS, 1024 / FPS_THREADS) k_fpb_scatter
 // mode-2 (fixed-base window) count with block-private counters: block (x, l) counts the
 // signed digits of chunk x of MSM l in shared memory (2^(c-1) counters) and flushes each
 // non-zero counter with one RED — the scatter (k_count_digits) keeps its global cursors
+// ROWS: the block's counts are stored chunk-major (cnt[(l S + x) nbm + b], as k_fpb_pass) for
+// the block-private scatter k_scatter_fb instead of being added into global counters
+template <bool ROWS>
 __global__ void __launch_bounds__(1024) k_count_fb(const void* const* ptrs, uint64_t n, WinPlan P,
                                                    uint32_t* __restrict__ cnt, uint64_t chunk) {
   extern __shared__ uint32_t h[];
@@ -752,9 +755,51 @@ __global__ void __launch_bounds__(1024) k_count_fb(const void* const* ptrs, uint
     }
   }
   __syncthreads();
+  if (ROWS) {
+    uint32_t* row = cnt + ((uint64_t)l * gridDim.x + blockIdx.x) * P.nbm;
+    for (uint32_t b = threadIdx.x; b < P.nbm; b += blockDim.x) row[b] = h[b];
+    return;
+  }
   uint32_t* out = cnt + (uint64_t)l * P.nbm;
   for (uint32_t b = threadIdx.x; b < P.nbm; b += blockDim.x)
     if (h[b]) atomicAdd(out + b, h[b]);
+}
+
+// mode-2 scatter with block-private cursors: block (x, l) loads the run starts of chunk x of
+// MSM l (k_fpb_starts over k_count_fb<true>'s rows) into shared memory and hands out slots
+// with shared-memory atomics — no global atomics (the global-cursor scatter is bound by
+// L2 atomic throughput: 738 M digits of a config-3 monomial step in 10.7 ms).  A chunk's
+// run per bucket holds ~n ndig / (S nbm) entries, so its sectors fill within the block.
+__global__ void __launch_bounds__(1024) k_scatter_fb(const void* const* ptrs, uint64_t n, WinPlan P,
+                                                     const uint32_t* __restrict__ runs, uint32_t* __restrict__ vals,
+                                                     uint64_t chunk, uint32_t l0) {
+  extern __shared__ uint32_t h[];
+  const uint32_t l = l0 + blockIdx.y;
+  const uint64_t c0 = (uint64_t)blockIdx.x * chunk;
+  const uint64_t c1 = min(n, c0 + chunk);
+  const void* p = ptrs[l];
+  const uint32_t* row = runs + ((uint64_t)l * gridDim.x + blockIdx.x) * P.nbm;
+  for (uint32_t b = threadIdx.x; b < P.nbm; b += blockDim.x) h[b] = row[b];
+  __syncthreads();
+  const int c = P.cdig;
+  const uint32_t half = 1u << (c - 1), full = 1u << c;
+  for (uint64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+    Fe mag;
+    bool neg;
+    uint32_t f = 0;
+    load_scalar<DT_LIMBS>(p, i, 0, mag, neg, f);
+    uint32_t carry = 0;
+    for (int w = 0; w < P.ndig; w++) {
+      uint32_t d = window_bits(mag, w * c, c) + carry;
+      bool dn = false;
+      if (d > half) {
+        d = full - d, dn = true, carry = 1;
+      } else {
+        carry = 0;
+      }
+      if (d) vals[atomicAdd(h + d - 1u, 1u)] = (uint32_t)((uint64_t)w * n + i) | ((neg != dn) ? SIGN_BIT : 0u);
+    }
+  }
 }
 
 // tot[l nbm + b] = sum over chunks of cnt[(l S + x) nbm + b]  (loads batched 8 deep: the
@@ -1522,21 +1567,31 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
   // 168 MB of entries per MSM: 157.7 ms with block counters vs 138.4 ms without)
   // (mode 3: 2^mb - 1 buckets per MSM, so every (chunk, bucket) run is long and fills its
   // sectors quickly whatever the MSM size)
-  const bool blkcnt = P.mode == 3 || (P.mode == 1 && vec_ok && !no_blk && blk_smem <= 100 * 1024 &&
-                                      n >= (1u << 16) && n * sizeof(uint32_t) <= (16ull << 20) &&
-                                      dtype != TC_DTYPE_F32);
+  // mode 2 (fixed-base digit windows of canonical scalars): block-private counters and
+  // cursors over 2^(c-1) buckets (TC_MSM_NO_FB_SCATTER: the global-cursor scatter)
+  static const bool no_fbs = getenv("TC_MSM_NO_FB_SCATTER") != nullptr;
+  const bool fbs = P.mode == 2 && dtype == TC_DTYPE_FP_LIMBS && !no_fbs && blk_smem <= 64 * 1024 &&
+                   n >= (1u << 14) && (uint64_t)n * P.ndig < (1ull << 31);
+  const bool blkcnt = P.mode == 3 || fbs ||
+                      (P.mode == 1 && vec_ok && !no_blk && blk_smem <= 100 * 1024 && n >= (1u << 16) &&
+                       n * sizeof(uint32_t) <= (16ull << 20) && dtype != TC_DTYPE_F32);
   if (blkcnt) {
     // S chunks per MSM so that one scatter launch (LG MSMs) is about one wave of 2 blocks/SM
     // LG MSMs per scatter launch: their entries (LG n 4 B) stay within 64 MB of L2
+    const uint64_t ent_per_msm = n * (P.mode == 2 ? (uint64_t)P.ndig : 1ull);
     const uint32_t LG = P.mode == 3 ? std::max(1u, std::min(getenv("TC_MSM_FPB_LG") ? FPB_LG_ENV : (uint32_t)L,
                                                             (uint32_t)L))
                                     : std::max<uint32_t>(1u, std::min(std::min(FPB_LG_ENV, (uint32_t)L),
-                                                                      (uint32_t)((64ull << 20) / (n * sizeof(uint32_t)))));
+                                                                      (uint32_t)((64ull << 20) / (ent_per_msm * sizeof(uint32_t)))));
     const uint64_t conc = (uint64_t)ctx->num_sms * 2;
     const uint64_t step = std::max<uint64_t>(1024ull * V_EPT, (uint64_t)FPS_SLICE);   // chunks hold whole slices
     const uint64_t S0 = std::max<uint64_t>(1, std::min<uint64_t>(conc / LG, n / step));
     const uint64_t chunk = ((n + S0 - 1) / S0 + step - 1) / step * step;
     const uint32_t Sx = (uint32_t)((n + chunk - 1) / chunk);
+    if (fbs) {
+      TC_TRY(func_smem(ctx, (const void*)k_count_fb<true>, 64 * 1024));
+      TC_TRY(func_smem(ctx, (const void*)k_scatter_fb, 64 * 1024));
+    }
     TC_TRY(func_smem(ctx, (const void*)k_fpb_pass<1, false>, 100 * 1024));
     TC_TRY(func_smem(ctx, (const void*)k_fpb_pass<1, true>, 100 * 1024));
     TC_TRY(func_smem(ctx, (const void*)k_fpb_pass<2, false>, 100 * 1024));
@@ -1562,6 +1617,13 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     WinPlan Pns = P;
     Pns.ktab = nullptr;
     auto pass = [&](bool scatter, uint32_t l0, uint32_t nl) {
+      if (fbs) {
+        if (scatter)
+          k_scatter_fb<<<dim3(Sx, nl), 1024, blk_smem, st>>>(d_ptrs, n, P, runs, vals, chunk, l0);
+        else
+          k_count_fb<true><<<dim3(Sx, nl), 1024, blk_smem, st>>>(d_ptrs, n, P, runs, chunk);
+        return;
+      }
       if (scatter && sorted) {
         if (dtype == TC_DTYPE_F16)
           k_fpb_scatter_sorted<1><<<dim3(Sx, nl), FPS_THREADS, fps_smem, st>>>(d_ptrs, n, scale_bits, Pns, runs, vals,
@@ -1613,7 +1675,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
     svals = vals;
     bend = bstart + 1;
     static const bool no_early = getenv("TC_MSM_NO_EARLY0") != nullptr;
-    if (!no_early && n * (uint64_t)L < (1ull << 31)) {   // every element at most one entry (modes 1 / 3)
+    if (!no_early && P.mode != 2 && n * (uint64_t)L < (1ull << 31)) {   // every element at most one entry (modes 1 / 3)
       // the host waits for the entry count / largest bucket (an event after the scatter),
       // NOT for the accumulation queued behind it
       if (!ctx->ev_mid) TC_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_mid, cudaEventDisableTiming));
@@ -1669,7 +1731,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
             P.nwin, P.nbm);
   const unsigned gxv = blocks_for(n, 256 * V_EPT);
   const unsigned gx = std::min<unsigned>(blocks_for(n, 256), std::max(1u, (unsigned)ctx->num_sms * 16 / (unsigned)L + 1));
-  TC_TRY(func_smem(ctx, (const void*)k_count_fb, 64 * 1024));
+  TC_TRY(func_smem(ctx, (const void*)k_count_fb<false>, 64 * 1024));
   int s = dispatch_dt(ctx, dtype, [&](auto dt) {
     constexpr int D = decltype(dt)::value;
     if constexpr (D >= 1 && D <= 3) {
@@ -1688,7 +1750,7 @@ int msm_batch_device(tc_ctx* ctx, int dtype, int scale_bits, const void* const* 
       const uint64_t conc = (uint64_t)ctx->num_sms * 3;
       const uint64_t S = std::max<uint64_t>(1, std::min<uint64_t>((conc + L - 1) / (uint64_t)L, n >> 14));
       const uint64_t chunk = (n + S - 1) / S;
-      k_count_fb<<<dim3((unsigned)((n + chunk - 1) / chunk), L), 1024, P.nbm * sizeof(uint32_t), st>>>(
+      k_count_fb<false><<<dim3((unsigned)((n + chunk - 1) / chunk), L), 1024, P.nbm * sizeof(uint32_t), st>>>(
           d_ptrs, n, P, cnt, chunk);
       return;
     }
