@@ -378,6 +378,88 @@ __global__ void __launch_bounds__(256) k_interp_newton_w(Fe* data, const Fe* inv
   }
 }
 
+// Register-blocked Newton interpolation (d a multiple of EPT, G = d / EPT <= 32): a block
+// holds 32 fibres, lane = fibre; warp q keeps elements [q EPT, (q+1) EPT) of its lane's
+// fibre in registers.  Each sweep step needs one neighbour element from the next-lower
+// (differences) or next-higher (expansion) warp, exchanged through a double-buffered
+// shared-memory slot with one barrier per step; a warp whose elements are all below the
+// step's start skips the step (warp-uniform), so the triangular sweeps cost d^2/2 updates
+// per fibre like the scalar form — without the shared-memory traffic of k_interp_newton2
+// (12 words per update) or the lane masking of the warp-per-fibre k_interp_newton_w.
+template <int EPT>
+__global__ void __launch_bounds__(256) k_interp_newton_b(Fe* data, const Fe* __restrict__ invfact, uint32_t d,
+                                                         uint64_t stride, uint64_t nfib) {
+  extern __shared__ uint32_t sx[];   // [2][G][6][32]
+  const uint32_t lane = threadIdx.x & 31, q = threadIdx.x >> 5, G = d / EPT;
+  const uint64_t f = (uint64_t)blockIdx.x * 32 + lane;
+  const bool live = f < nfib;
+  const int j0 = (int)(q * EPT);
+  Fe v[EPT];
+#pragma unroll
+  for (int e = 0; e < EPT; e++) v[e] = live ? data[fibre_addr(f, (uint32_t)(j0 + e), d, stride)] : Fp::zero();
+  auto slot = [&](int b, uint32_t w, int i) -> uint32_t& { return sx[((b * G + w) * 6 + i) * 32 + lane]; };
+  // forward differences: step k sets v[j] -= v[j-1] for j = d-1 .. k (descending)
+  for (int k = 1; k < (int)d; k++) {
+    const int b = k & 1;
+    if (q + 1 < G && j0 + EPT >= k) {   // old top element, read by the next warp
+#pragma unroll
+      for (int i = 0; i < 6; i++) slot(b, q, i) = v[EPT - 1].v[i];
+    }
+    __syncthreads();
+    if (j0 + EPT - 1 >= k) {
+      Fe below;
+      if (q > 0) {
+#pragma unroll
+        for (int i = 0; i < 6; i++) below.v[i] = slot(b, q - 1, i);
+      }
+      if (j0 >= k) {   // the whole range (every step but the EPT - 1 where k falls inside it)
+#pragma unroll
+        for (int e = EPT - 1; e >= 1; e--) v[e] = Fp::sub(v[e], v[e - 1]);
+        v[0] = Fp::sub(v[0], below);
+      } else {
+#pragma unroll
+        for (int e = EPT - 1; e >= 1; e--)
+          if (j0 + e >= k) v[e] = Fp::sub(v[e], v[e - 1]);
+      }
+    }
+  }
+  // c_k = Delta^k y_0 / k!
+#pragma unroll
+  for (int e = 0; e < EPT; e++)
+    if (j0 + e >= 2) v[e] = Fp::mul(v[e], invfact[j0 + e]);
+  // Newton basis -> monomials: step k sets v[j] -= (k+1) v[j+1] for j = k .. d-2 (ascending)
+  for (int k = (int)d - 2; k >= 0; k--) {
+    const int b = k & 1;
+    if (q > 0 && j0 - 1 >= k) {   // old bottom element, read by the previous warp
+#pragma unroll
+      for (int i = 0; i < 6; i++) slot(b, q, i) = v[0].v[i];
+    }
+    __syncthreads();
+    if (j0 + EPT - 1 >= k) {
+      Fe above;
+      if (q + 1 < G) {
+#pragma unroll
+        for (int i = 0; i < 6; i++) above.v[i] = slot(b, q + 1, i);
+      }
+      const uint32_t sc = (uint32_t)k + 1;
+      if (j0 >= k && q + 1 < G) {   // the whole range, not the fibre's top element
+#pragma unroll
+        for (int e = 0; e < EPT; e++) v[e] = Fp::sub(v[e], fp_mul_u32(e + 1 < EPT ? v[e + 1] : above, sc));
+      } else {
+#pragma unroll
+        for (int e = 0; e < EPT; e++) {
+          const int j = j0 + e;
+          if (j >= k && j <= (int)d - 2) v[e] = Fp::sub(v[e], fp_mul_u32(e + 1 < EPT ? v[e + 1] : above, sc));
+        }
+      }
+    }
+  }
+  if (live) {
+#pragma unroll
+    for (int e = 0; e < EPT; e++) data[fibre_addr(f, (uint32_t)(j0 + e), d, stride)] = Fp::canon(v[e]);
+  }
+}
+
 // divide the prefix-supported remainder r by (X_a - v) along axis a (extent d, stride s):
 // fibres i in [0, s); q written at the same offsets; r keeps only its X_a^0 slice
 __global__ void k_divide_axis(Fe* r, Fe* q, uint32_t d, uint64_t s, Fe v_mont) {
@@ -554,6 +636,15 @@ int interpolate_device(tc_ctx* ctx, Fe* d_vals, const uint32_t* shape, int m) {
       // longer fibres: one warp per fibre (500 us vs 644 us at d = 64), the SMEM footprint of
       // the thread-per-fibre kernel caps it at 4 warps per SM there
       static const bool warp_all = getenv("TC_INTERP_WARP") != nullptr;
+      static const bool no_blocked = getenv("TC_INTERP_NO_BLOCKED") != nullptr;
+      if (!warp_all && !no_blocked && d % 8 == 0 && d / 8 <= 8) {
+        // register-blocked kernel: 8 elements per thread, d / 8 warps per 32 fibres
+        const uint32_t G = d / 8;
+        k_interp_newton_b<8><<<(unsigned)((nfib + 31) / 32), 32 * G, 2 * G * 6 * 32 * sizeof(uint32_t), st>>>(
+            d_vals, dIf, d, stride, nfib);
+        TC_LAUNCHED(ctx);
+        continue;
+      }
       if (warp_all || d > 32) {
         const unsigned grid = (unsigned)std::min<uint64_t>((nfib + 7) / 8, 148ull * 8);
         if (d <= 32) k_interp_newton_w<1><<<grid, 256, 0, st>>>(d_vals, dIf, d, stride, nfib);

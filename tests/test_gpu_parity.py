@@ -500,11 +500,14 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("env", [{"TC_INTERP_NEWTON_MIN_FIB": "1"}, {"TC_INTERP_NEWTON_MIN_FIB": "1", "TC_INTERP_WARP": "1"},
+@pytest.mark.parametrize("env", [{"TC_INTERP_NEWTON_MIN_FIB": "1"},
+                                 {"TC_INTERP_NEWTON_MIN_FIB": "1", "TC_INTERP_NO_BLOCKED": "1"},
+                                 {"TC_INTERP_NEWTON_MIN_FIB": "1", "TC_INTERP_WARP": "1"},
                                  {"TC_INTERP_DENSE": "1"}])
 def test_interpolation_newton_and_dense_kernels(env, tmp_path):
     """All interpolation kernels — the Newton-form ones (forward differences + small-integer
-    basis expansion; thread-per-fibre for <= 32 nodes, warp-per-fibre above, or warp-per-fibre
+    basis expansion; register-blocked 8 elements per thread for multiples of 8 nodes up to 64,
+    thread-pair-per-fibre for <= 32 nodes otherwise, warp-per-fibre above, or warp-per-fibre
     everywhere) forced onto every axis with <= 128 nodes, and the dense Lagrange-matrix one
     forced everywhere — equal the oracle on full-range F_p values
     (p - 1 and 0 included), on small signed values and on ragged shapes, and reproduce the
