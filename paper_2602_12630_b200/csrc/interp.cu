@@ -637,8 +637,10 @@ int interpolate_device(tc_ctx* ctx, Fe* d_vals, const uint32_t* shape, int m) {
       // the thread-per-fibre kernel caps it at 4 warps per SM there
       static const bool warp_all = getenv("TC_INTERP_WARP") != nullptr;
       static const bool no_blocked = getenv("TC_INTERP_NO_BLOCKED") != nullptr;
-      if (!warp_all && !no_blocked && d % 8 == 0 && d / 8 <= 8) {
-        // register-blocked kernel: 8 elements per thread, d / 8 warps per 32 fibres
+      if (!warp_all && !no_blocked && d % 8 == 0 && d <= 32) {
+        // register-blocked kernel: 8 elements per thread, d / 8 warps per 32 fibres (config 3's
+        // 32-node axes: 23.4 -> 19.4 ms per forward; 4 elements per thread measured the same;
+        // at 64 nodes the warp-per-fibre kernel stays ahead, 15.9 vs 16.3 ms)
         const uint32_t G = d / 8;
         k_interp_newton_b<8><<<(unsigned)((nfib + 31) / 32), 32 * G, 2 * G * 6 * 32 * sizeof(uint32_t), st>>>(
             d_vals, dIf, d, stride, nfib);

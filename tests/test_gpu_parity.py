@@ -506,7 +506,7 @@ print("ok")
                                  {"TC_INTERP_DENSE": "1"}])
 def test_interpolation_newton_and_dense_kernels(env, tmp_path):
     """All interpolation kernels — the Newton-form ones (forward differences + small-integer
-    basis expansion; register-blocked 8 elements per thread for multiples of 8 nodes up to 64,
+    basis expansion; register-blocked 8 elements per thread for multiples of 8 nodes up to 32,
     thread-pair-per-fibre for <= 32 nodes otherwise, warp-per-fibre above, or warp-per-fibre
     everywhere) forced onto every axis with <= 128 nodes, and the dense Lagrange-matrix one
     forced everywhere — equal the oracle on full-range F_p values
