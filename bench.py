@@ -301,8 +301,8 @@ def _reexec_torchrun(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=3, choices=[3, 4, 5])
     ap.add_argument("--route", default="lagrange", choices=["lagrange", "monomial"])
@@ -584,7 +584,9 @@ def run_reference(args, cfg, cores, world):
     _TASK, K, kind = cpu_sample(CONFIGS[3]["shape"])
     import multiprocessing as mp
     one = _cpu_task()
-    rounds = max(1, int(6.0 / max(one, 1e-3)))
+    # each step a bounded sample: ~6 s, less for long runs (the whole run stays ~2 minutes)
+    per_step_s = min(6.0, max(1.0, 120.0 / max(1, args.steps)))
+    rounds = max(1, int(per_step_s / max(one, 1e-3)))
     walls, tasks = [], 0
     with mp.get_context("fork").Pool(cores) as pool:
         for _ in range(max(1, args.warmup)):
