@@ -396,7 +396,7 @@ def run_commits(args, cfg, dev, rank, world, cores, backend):
     tcfg = tcb.TreeConfig(shape=NODE_SHAPE)
     node_srs = tcb.authtree.node_srs(tcfg, device=local)
     ctx = _lib.Context.get(local)
-    PIPE_DEPTH = int(os.environ.get("TC_PIPE_DEPTH", "3"))
+    PIPE_DEPTH = int(os.environ.get("TC_PIPE_DEPTH", "4"))
     use_pipe = not os.environ.get("TC_BENCH_NO_PIPELINE")
     dev_fwd = dict(zip(my_layers, dev_layers))
     host_fwd = dict(zip(my_layers, host_pinned))

@@ -112,7 +112,7 @@ class DistProver:
     pipeline context; finish(state) returns (commitments, root, tree) for ALL layers."""
 
     def __init__(self, srs, n_layers: int, rank: int, world: int, *, group=None, tree_config=None, node_srs=None,
-                 scale_bits: int = 16, route: str = "auto", depth: int = 3):
+                 scale_bits: int = 16, route: str = "auto", depth: int = 4):
         import torch
         import torch.distributed as dist
 
@@ -194,7 +194,7 @@ def prover_commit_dist(layers: dict, srs, n_layers: int, rank: int, world: int, 
     return p.finish(p.launch(layers))
 
 
-def prover_commit_pipeline_dist(forwards, srs, n_layers: int, rank: int, world: int, *, depth: int = 3, **kw):
+def prover_commit_pipeline_dist(forwards, srs, n_layers: int, rank: int, world: int, *, depth: int = 4, **kw):
     """prover_commit_dist over a stream of forwards (each a dict layer -> tensor holding at
     least this rank's layers), yielding (commitments, root, tree) per forward in order;
     `depth` contexts keep forwards in flight so one forward's gather and tree overlap the

@@ -19,10 +19,11 @@ layers = [torch.from_numpy(h).to(dev) for h in bench.make_layers_host(cfg, range
 srs, _ = tcb.setup_srs(cfg["shape"], b"tc-b200/config3", device=0)
 srs.prepare("float16")
 K = 20
+DEPTH = int(os.environ.get("TC_PROBE_DEPTH", "3"))
 
 
 def timed(fn):
-    fn(3)
+    fn(max(3, DEPTH + 2))
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -35,7 +36,7 @@ def timed(fn):
 def pipe(n):
     def f(k):
         r = None
-        for _, r, _ in tcb.prover_commit_pipeline([layers[:n]] * k, srs, depth=3):
+        for _, r, _ in tcb.prover_commit_pipeline([layers[:n]] * k, srs, depth=DEPTH):
             pass
         return r
     return f
@@ -46,7 +47,7 @@ def dpipe(n):
 
     def f(k):
         r = None
-        for _, r, _ in prover_commit_pipeline_dist([d] * k, srs, n, 0, 1, depth=3):
+        for _, r, _ in prover_commit_pipeline_dist([d] * k, srs, n, 0, 1, depth=DEPTH):
             pass
         return r
     return f
