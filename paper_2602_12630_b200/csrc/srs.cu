@@ -104,22 +104,26 @@ __global__ void __launch_bounds__(128) k_fixed(const Aff* table, const Fe* exps,
 }
 
 // E affine points -> the MSM's Edwards model phi([h] P) (ec.cuh): [h] P in XYZZ, then two
-// Montgomery batch inversions over FB_K points per thread (XYZZ -> affine, affine -> Edwards)
+// Montgomery batch inversions over K points per thread (XYZZ -> affine, affine -> Edwards).
+// K = FB_K for SRS-sized inputs; K = 1 for small ones (an opening's d0^2 slice commitments),
+// whose conversion is latency-bound: 1024 points at 8 per thread ran on 128 threads of one SM
+// (3.2 ms of serial doublings), one per thread spreads them over the GPU
+template <int K>
 __global__ void __launch_bounds__(128) k_to_edwards(const Aff* in, uint64_t n, EdPk* out) {
   uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  uint64_t i0 = t * FB_K;
+  uint64_t i0 = t * K;
   if (i0 >= n) return;
-  const int cnt = (n - i0 < (uint64_t)FB_K) ? (int)(n - i0) : FB_K;
-  Xyzz h[FB_K];
-  Fe pref[FB_K];
+  const int cnt = (n - i0 < (uint64_t)K) ? (int)(n - i0) : K;
+  Xyzz h[K];
+  Fe pref[K];
   Fe run = Fq::one();
   for (int k = 0; k < cnt; k++) {
     h[k] = xyzz_mul_half(in[i0 + k]);
     pref[k] = run;
     if (!xyzz_is_inf(h[k])) run = Fq::mul(run, Fq::mul(h[k].ZZ, h[k].ZZZ));
   }
-  Fe inv = Fq::inv(run);
-  Aff q[FB_K];
+  Fe inv = Fq::inv_pref(run);
+  Aff q[K];
   for (int k = cnt - 1; k >= 0; k--) {
     if (xyzz_is_inf(h[k])) {
       q[k] = aff_inf();
@@ -134,7 +138,7 @@ __global__ void __launch_bounds__(128) k_to_edwards(const Aff* in, uint64_t n, E
     pref[k] = run;
     run = Fq::mul(run, aff_ed_den(q[k]));
   }
-  inv = Fq::inv(run);
+  inv = Fq::inv_pref(run);
   for (int k = cnt - 1; k >= 0; k--) {
     const Fe den = aff_ed_den(q[k]);
     const Fe ik = Fq::mul(inv, pref[k]);
@@ -233,7 +237,10 @@ int srs_exp_table(tc_ctx* ctx, tc_srs* srs, const EdPk* bases, uint64_t n, int d
 
 int to_edwards_device(tc_ctx* ctx, const Aff* d_in, uint64_t n, EdPk* d_out) {
   if (n == 0) return TC_OK;
-  k_to_edwards<<<blocks_for((n + FB_K - 1) / FB_K, 128), 128, 0, ctx->stream>>>(d_in, n, d_out);
+  if (n <= (uint64_t)ctx->num_sms * 128 * 4)
+    k_to_edwards<1><<<blocks_for(n, 64), 64, 0, ctx->stream>>>(d_in, n, d_out);
+  else
+    k_to_edwards<FB_K><<<blocks_for((n + FB_K - 1) / FB_K, 128), 128, 0, ctx->stream>>>(d_in, n, d_out);
   TC_LAUNCHED(ctx);
   return TC_OK;
 }

@@ -28,7 +28,7 @@ torch.cuda.synchronize()
 for rep in range(int(os.environ.get("TC_C4_REPS", "1"))):
     torch.cuda.nvtx.range_push("open")
     t0 = time.perf_counter()
-    tcb.tc_open_many(srs, ts, pts)
+    tcb.tc_open_many(srs, ts, pts, **({"parallel": 1} if os.environ.get("TC_C4_SERIAL") else {}))
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     torch.cuda.nvtx.range_pop()
