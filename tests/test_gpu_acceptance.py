@@ -9,7 +9,9 @@ the CPU pairing verifier as the checkers):
 3. division / opening identity: coefficient-exact f = sum_i q_i (X_i - w_i) + y
    on 10^3 random polynomials up to shape 5 x 5 x 5 (GPU quotients, host identity);
 4. interpolation cross-oracle: the GPU interpolant equals the oracle's
-   Lagrange interpolant on 10^3 random field instances (and evaluates back to the samples).
+   Lagrange interpolant on 10^3 random field instances (and evaluates back to the samples);
+7. proof-size formula, terkle part: ceil(log_B n) levels of m quotient
+   elements for n in {B, B^2, B^3}.
 """
 import itertools
 import random
@@ -181,3 +183,26 @@ def test_interpolation_cross_oracle_1000_instances():
             for d, x in zip(shape, node):
                 idx = idx * d + (x - 1)
             assert tcb.evaluate(dom, f, node) == vals[idx] % O.P
+
+
+@pytest.mark.parametrize("node_shape", [(2,), (2, 2), (2, 2, 2), (4, 4, 4)], ids=lambda s: "x".join(map(str, s)))
+def test_terkle_proof_size_formula(node_shape):
+    """SPEC.md:693 (terkle part): a membership proof carries ceil(log_B n) levels of m
+    quotient elements (B = prod(node shape), m = its order) for n in {B, B^2, B^3}; every
+    proof verifies, and the TCTP encoding has exactly that many levels."""
+    import paper_2602_12630_b200 as tcb
+    cfg = tcb.TreeConfig(shape=node_shape)
+    B, m = cfg.arity, len(node_shape)
+    rng = random.Random(693 + B)
+    for e in (1, 2, 3):
+        n = B ** e
+        leaves = [rng.randrange(O.P) for _ in range(n)]
+        tree, root = tcb.build(cfg, leaves)
+        for i in sorted({0, n - 1, rng.randrange(n)}):
+            pf = tcb.prove(tree, i)
+            assert len(pf.nodes) == e and len(pf.openings) == e
+            assert all(len(op.proofs) == m for op in pf.openings)
+            assert tcb.verify(root, i, leaves[i], pf, cfg)
+            assert not tcb.verify(root, i, (leaves[i] + 1) % O.P, pf, cfg)
+            raw = pf.to_bytes(cfg)
+            assert raw[:4] == b"TCTP" and int.from_bytes(raw[5:7], "little") == e
