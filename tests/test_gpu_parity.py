@@ -348,7 +348,7 @@ def test_open_many_parallel_contexts_match_serial():
         assert tcb.tc_verify(srs, C[picks[k]], pts[k], par[k])
 
 
-@pytest.mark.parametrize("depth", [1, 2, 3])
+@pytest.mark.parametrize("depth", [1, 2, 3, 4])
 def test_prover_commit_pipeline_matches_prover_commit(depth):
     """prover_commit_pipeline (forwards taken in turn by `depth` contexts with their own
     streams: tc_commit_tree_launch / _finish) yields, in order, exactly prover_commit's
@@ -379,6 +379,46 @@ def test_prover_commit_pipeline_matches_prover_commit(depth):
         list(tcb.prover_commit_pipeline([fwds[0], bad], srs, tree_config=cfg, node_srs=node, depth=depth))
     again = list(tcb.prover_commit_pipeline(fwds[:2], srs, tree_config=cfg, node_srs=node, depth=depth))
     assert [r for _, r, _ in again] == [r for _, r, _ in want[:2]]
+
+
+@pytest.mark.parametrize("dtype", ["bfloat16", "float32"])
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_prover_commit_pipeline_other_dtypes(dtype, split, tmp_path):
+    """The forward pipeline on bf16 (exponent-table plan with 8-bit mantissas) and fp32
+    (signed-window plans) inputs, with and without the low-priority tail stream
+    (TC_TAIL_SPLIT): the same roots as prover_commit and the trapdoor commitments."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "pipe.py"
+    script.write_text(_PIPE_DTYPE_SCRIPT.format(root=root, dtype=dtype))
+    out = subprocess.run([sys.executable, str(script)], env=dict(os.environ, TC_TAIL_SPLIT=split),
+                         capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr
+
+
+_PIPE_DTYPE_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_2602_12630_b200 as tcb
+from oracle import tc_oracle as O
+shape = (16, 16, 16, 16)
+srs, td = tcb.setup_srs(shape, b"pipeline-dtypes")
+cfg = tcb.TreeConfig(shape=(2, 2, 2))
+node = tcb.authtree.node_srs(cfg, device=0)
+g = np.random.default_rng(82)
+dt = getattr(torch, {dtype!r})
+fwds = [[torch.from_numpy((g.standard_t(3, 65536) * (0.5 + (f + l) % 3)).astype(np.float32)).to(dt).cuda()
+         for l in range(6)] for f in range(5)]
+want = [tcb.prover_commit(f, srs, tree_config=cfg, node_srs=node, return_tree=True) for f in fwds]
+for depth in (2, 4):
+    got = list(tcb.prover_commit_pipeline(fwds, srs, tree_config=cfg, node_srs=node, depth=depth))
+    assert [(c, r) for c, r, _ in got] == [(c, r) for c, r, _ in want], depth
+vals = O.quantize(fwds[3][4].float().cpu().numpy().astype(np.float64), 16)
+assert want[3][0][4].elem == O.commit_trapdoor(vals, shape, list(td.taus))
+print("ok")
+"""
 
 
 @pytest.mark.parametrize("group", [0, 1, 2, 5])
