@@ -893,7 +893,7 @@ __device__ __forceinline__ uint32_t find_bucket(const uint32_t* off, uint32_t nb
 #define TC_ACCUM_PF 1   // A/B (config 3): 0 -> 3.982 ms, 1 -> 3.909 (MINB 4), 2 (+L2 prefetch) -> 4.15, 3 (point in registers) -> 4.14
 #endif
 #ifndef TC_ACCUM_MINB
-#define TC_ACCUM_MINB 6   // min resident blocks per SM for k_accum_aff (a = -1 model, PF 1): 4 -> 112 registers, 3.768 ms; 5 -> 95, 3.641; 6 -> 80 + 24 B stack, 3.629 (the a = 2 model ran best at 4 / 96)
+#define TC_ACCUM_MINB 6   // min resident blocks per SM for k_accum_aff (a = -1 model, PF 1): 4 -> 112 registers, 3.768 ms; 5 -> 95, 3.641; 6 -> 80 + 24 B stack, 3.629; 7 -> 72 + 68 B spills, 0.844 vs 0.857 of the peak (the a = 2 model ran best at 4 / 96)
 #endif
 __global__ void __launch_bounds__(128, TC_ACCUM_MINB) k_accum_aff(const uint32_t* vals, const EdPk* bases, const uint32_t* bstart,
                                                    const uint32_t* bend, const uint32_t* toff, const uint32_t* ooff,
