@@ -415,17 +415,20 @@ struct Field {
 #endif
   }
 
-  // u * M5 for the small top limb of the modulus (q: 0xF0 = 2^8 - 2^4, p: 2).  The device
-  // uses shifts (ALU pipe) instead of the half-rate IMAD.WIDE on the fma-heavy pipe that
-  // bounds the accumulation (TC_REDC_SHIFT=0 restores the product): k_accum_aff 4.03 ->
-  // 3.97 ms with the exponent-table plan (it measured 5 % slower in an earlier XYZZ build).
+  // u * M5 for the small top limb of the modulus (q: 0xF0 = 2^8 - 2^4, p: 2).  p's is a
+  // shift.  q's: TC_REDC_SHIFT=1 forms 2^8 u - 2^4 u with 64-bit shifts (LEA + IMAD.SHL +
+  // SHF), 0 (default) one IMAD.WIDE — which one schedules better depends on the rest of the
+  // accumulation loop: shifts won with the earlier add orderings (k_accum_aff 4.03 -> 3.97 ms),
+  // the product wins with the tuned mixed-add order (4.182 -> 4.164 ms per forward)
 #ifndef TC_REDC_SHIFT
-#define TC_REDC_SHIFT 1
+#define TC_REDC_SHIFT 0
 #endif
   TC_HD static uint64_t mul_m5(uint32_t u) {
-#if defined(__CUDA_ARCH__) && TC_REDC_SHIFT
-    uint64_t r;
+#if defined(__CUDA_ARCH__)
+    if (PM::M5 == 2u) return (uint64_t)u << 1;
+#if TC_REDC_SHIFT
     if (PM::M5 == 0xF0u) {
+      uint64_t r;
       asm("{.reg .u64 a, b;\n\t"
           "cvt.u64.u32 a, %1;\n\t"
           "shl.b64 b, a, 8;\n\t"
@@ -434,7 +437,7 @@ struct Field {
           : "=l"(r) : "r"(u));
       return r;
     }
-    if (PM::M5 == 2u) return (uint64_t)u << 1;
+#endif
 #endif
     return (uint64_t)u * PM::M5;
   }
